@@ -1,0 +1,288 @@
+// K5: graph preparation (outside the timed region, like the reference's
+// build_csr, which bench.py:1-7 keeps out of its timers).
+//
+//   gee_build_sym_csr  symmetric CSR of a listed edge list: degree count,
+//                      exclusive scan (CUB), atomic-cursor scatter.  The
+//                      reference's counting sort is build_csr + csr_fill
+//                      (graph.py:159-184, _kernels.py:229-238); here every
+//                      list is mirrored because the edge pass applies both
+//                      updates per listed edge (encoder.py:106-120).
+//   gee_csr_rows       per-arc source row of a stored CSR (COO expansion).
+//   gee_graph_stats    weight statistics that size the pull fixed point.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "gee_common.cuh"
+
+namespace {
+
+__global__ void k_degree(const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t s,
+                         int64_t n, int symmetric, unsigned long long *__restrict__ deg,
+                         unsigned long long *__restrict__ bad)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t u = src[i], v = dst[i];
+        if (u < 0 || v < 0 || u >= n || v >= n) {
+            atomicAdd(bad, 1ull);
+            continue;
+        }
+        atomicAdd(&deg[u + 1], 1ull);
+        if (symmetric) atomicAdd(&deg[v + 1], 1ull);
+    }
+}
+
+// Unordered fill: atomic cursor per row (arc order within a row unspecified).
+__global__ void k_scatter(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                          const float *__restrict__ w, int64_t s, int64_t n, int symmetric,
+                          unsigned long long *__restrict__ cursor, int32_t *__restrict__ targets,
+                          float *__restrict__ weights)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t u = src[i], v = dst[i];
+        if (u < 0 || v < 0 || u >= n || v >= n) continue;
+        unsigned long long pu = atomicAdd(&cursor[u], 1ull);
+        targets[pu] = v;
+        if (weights) weights[pu] = w[i];
+        if (symmetric) {
+            unsigned long long pv = atomicAdd(&cursor[v], 1ull);
+            targets[pv] = u;
+            if (weights) weights[pv] = w[i];
+        }
+    }
+}
+
+// Stable fill, step 1: arc a -> (row key, arc id).  Symmetric lists number
+// the original arc 2i and its mirror 2i+1, so a stable sort by row gives
+// build_csr's order: mirror right after the original (graph.py:170-176).
+__global__ void k_arc_keys(const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t s,
+                           int symmetric, uint32_t *__restrict__ keys, uint32_t *__restrict__ ids)
+{
+    const int64_t arcs = symmetric ? 2 * s : s;
+    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < arcs;
+         a += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = symmetric ? a >> 1 : a;
+        const bool mirror = symmetric && (a & 1);
+        keys[a] = (uint32_t)(mirror ? dst[i] : src[i]);
+        ids[a] = (uint32_t)a;
+    }
+}
+
+// Stable fill, step 2: gather targets/weights in sorted arc order.
+__global__ void k_arc_gather(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                             const float *__restrict__ w, int64_t arcs, int symmetric,
+                             const uint32_t *__restrict__ ids, int32_t *__restrict__ targets,
+                             float *__restrict__ weights)
+{
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < arcs;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = ids[p];
+        const int64_t i = symmetric ? a >> 1 : a;
+        const bool mirror = symmetric && (a & 1);
+        targets[p] = mirror ? src[i] : dst[i];
+        if (weights) weights[p] = w[i];
+    }
+}
+
+__global__ void k_csr_rows(const int64_t *__restrict__ offsets, int64_t n, int32_t *__restrict__ rows)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; r < n; r += warps) {
+        const int64_t lo = offsets[r], hi = offsets[r + 1];
+        for (int64_t e = lo + lane; e < hi; e += 32) rows[e] = (int32_t)r;
+    }
+}
+
+// Non-negative doubles / floats order like their bit patterns.
+__device__ __forceinline__ void atomic_max_pos(double *p, double v)
+{
+    atomicMax(reinterpret_cast<unsigned long long *>(p), (unsigned long long)__double_as_longlong(v));
+}
+__device__ __forceinline__ void atomic_min_pos(double *p, double v)
+{
+    atomicMin(reinterpret_cast<unsigned long long *>(p), (unsigned long long)__double_as_longlong(v));
+}
+
+struct Stats {
+    double max_row_abs;
+    double min_abs_nz;
+    double max_abs;
+    int32_t nonfinite;
+};
+
+__global__ void k_graph_stats(const int64_t *__restrict__ offsets, const float *__restrict__ w, int64_t n,
+                              Stats *__restrict__ out)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double best_row = 0.0, best_min = INFINITY, best_max = 0.0;
+    int nonfinite = 0;
+    for (int64_t r = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; r < n; r += warps) {
+        const int64_t lo = offsets[r], hi = offsets[r + 1];
+        double sum = 0.0;
+        if (w) {
+            for (int64_t e = lo + lane; e < hi; e += 32) {
+                float x = fabsf(w[e]);
+                if (!isfinite(x)) nonfinite = 1;
+                sum += x;
+                if (x > 0.f) best_min = fmin(best_min, (double)x);
+                best_max = fmax(best_max, (double)x);
+            }
+            for (int d = 16; d; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+        } else {
+            sum = (double)(hi - lo);
+        }
+        best_row = fmax(best_row, sum);
+    }
+    for (int d = 16; d; d >>= 1) {
+        best_row = fmax(best_row, __shfl_xor_sync(0xffffffffu, best_row, d));
+        best_min = fmin(best_min, __shfl_xor_sync(0xffffffffu, best_min, d));
+        best_max = fmax(best_max, __shfl_xor_sync(0xffffffffu, best_max, d));
+        nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, d);
+    }
+    if (lane == 0) {
+        atomic_max_pos(&out->max_row_abs, best_row);
+        if (best_min < INFINITY) atomic_min_pos(&out->min_abs_nz, best_min);
+        atomic_max_pos(&out->max_abs, best_max);
+        if (nonfinite) atomicOr(&out->nonfinite, 1);
+    }
+}
+
+int grid_for(int64_t items, int per_block, int waves)
+{
+    int64_t want = (items + per_block - 1) / per_block;
+    int64_t cap = (int64_t)gee::sm_count() * waves;
+    return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+}  // namespace
+
+extern "C" {
+
+int gee_build_csr(const int32_t *src, const int32_t *dst, const float *w, int64_t s, int64_t n,
+                  int32_t symmetric, int32_t stable, int64_t *offsets, int32_t *targets, float *weights,
+                  void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(n >= 0 && s >= 0, GEE_ERR_INVALID, "n and s must be nonnegative");
+    GEE_REQUIRE(n <= INT32_MAX, GEE_ERR_INVALID, "node count %lld exceeds CSR limit", (long long)n);
+    GEE_REQUIRE(offsets != nullptr, GEE_ERR_INVALID, "offsets must not be NULL");
+    const int64_t arcs = symmetric ? 2 * s : s;
+    GEE_REQUIRE(!stable || arcs <= (int64_t)UINT32_MAX, GEE_ERR_INVALID,
+                "stable CSR build supports at most 2^32-1 arcs");
+    cudaStream_t st = gee::as_stream(stream);
+    auto *deg = reinterpret_cast<unsigned long long *>(offsets);
+    GEE_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t) * (size_t)(n + 1), st));
+    if (s == 0) return GEE_OK;
+    GEE_REQUIRE(src && dst && targets, GEE_ERR_INVALID, "NULL array argument");
+    GEE_REQUIRE(!w || weights, GEE_ERR_INVALID, "weights output required for weighted input");
+    unsigned long long *bad = nullptr, *cursor = nullptr;
+    uint32_t *kbuf = nullptr, *vbuf = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int rc = GEE_OK;
+    unsigned long long nbad = 0;
+    GEE_CUDA(cudaMallocAsync((void **)&bad, sizeof(unsigned long long), st));
+    GEE_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), st));
+    k_degree<<<grid_for(s, 256, 16), 256, 0, st>>>(src, dst, s, n, symmetric, deg, bad);
+    if ((rc = gee::check_launch("k_degree"))) goto out;
+    cudaMemcpyAsync(&nbad, bad, sizeof(nbad), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) { gee::set_error("sync failed"); rc = GEE_ERR_CUDA; goto out; }
+    if (nbad) {
+        gee::set_error("%llu edge endpoints outside [0, %lld)", nbad, (long long)n);
+        rc = GEE_ERR_RANGE;
+        goto out;
+    }
+    // inclusive scan of deg[1..n] in place gives offsets (offsets[0] = 0)
+    cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, offsets + 1, offsets + 1, n, st);
+    if (cudaMallocAsync(&tmp, tmp_bytes, st) != cudaSuccess) { gee::set_error("scratch alloc failed"); rc = GEE_ERR_CUDA; goto out; }
+    cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, offsets + 1, offsets + 1, n, st);
+    if ((rc = gee::check_launch("DeviceScan::InclusiveSum"))) goto out;
+    cudaFreeAsync(tmp, st);
+    tmp = nullptr;
+    if (!stable) {
+        if (cudaMallocAsync((void **)&cursor, sizeof(unsigned long long) * (size_t)(n ? n : 1), st) != cudaSuccess) {
+            gee::set_error("cursor alloc failed");
+            rc = GEE_ERR_CUDA;
+            goto out;
+        }
+        cudaMemcpyAsync(cursor, offsets, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToDevice, st);
+        k_scatter<<<grid_for(s, 256, 16), 256, 0, st>>>(src, dst, w, s, n, symmetric, cursor, targets,
+                                                        w ? weights : nullptr);
+        rc = gee::check_launch("k_scatter");
+        goto out;
+    }
+    {
+        // 4 buffers of `arcs` u32: keys/ids in, keys/ids out (cub::DoubleBuffer)
+        if (cudaMallocAsync((void **)&kbuf, sizeof(uint32_t) * (size_t)arcs * 2, st) != cudaSuccess ||
+            cudaMallocAsync((void **)&vbuf, sizeof(uint32_t) * (size_t)arcs * 2, st) != cudaSuccess) {
+            gee::set_error("sort buffers alloc failed (%lld arcs)", (long long)arcs);
+            rc = GEE_ERR_CUDA;
+            goto out;
+        }
+        k_arc_keys<<<grid_for(arcs, 256, 16), 256, 0, st>>>(src, dst, s, symmetric, kbuf, vbuf);
+        if ((rc = gee::check_launch("k_arc_keys"))) goto out;
+        cub::DoubleBuffer<uint32_t> kd(kbuf, kbuf + arcs), vd(vbuf, vbuf + arcs);
+        int end_bit = 1;
+        while (end_bit < 32 && ((int64_t)1 << end_bit) < n) end_bit++;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kd, vd, arcs, 0, end_bit, st);
+        if (cudaMallocAsync(&tmp, tmp_bytes, st) != cudaSuccess) { gee::set_error("sort scratch alloc failed"); rc = GEE_ERR_CUDA; goto out; }
+        cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kd, vd, arcs, 0, end_bit, st);
+        if ((rc = gee::check_launch("DeviceRadixSort::SortPairs"))) goto out;
+        k_arc_gather<<<grid_for(arcs, 256, 16), 256, 0, st>>>(src, dst, w, arcs, symmetric, vd.Current(), targets,
+                                                              w ? weights : nullptr);
+        rc = gee::check_launch("k_arc_gather");
+    }
+out:
+    if (tmp) cudaFreeAsync(tmp, st);
+    if (cursor) cudaFreeAsync(cursor, st);
+    if (kbuf) cudaFreeAsync(kbuf, st);
+    if (vbuf) cudaFreeAsync(vbuf, st);
+    if (bad) cudaFreeAsync(bad, st);
+    return rc;
+}
+
+int gee_build_sym_csr(const int32_t *src, const int32_t *dst, const float *w, int64_t s, int64_t n,
+                      int64_t *offsets, int32_t *targets, float *weights, void *stream)
+{
+    return gee_build_csr(src, dst, w, s, n, 1, 0, offsets, targets, weights, stream);
+}
+
+int gee_csr_rows(const int64_t *offsets, int64_t n, int64_t arcs, int32_t *rows, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(n >= 0 && arcs >= 0, GEE_ERR_INVALID, "n and arcs must be nonnegative");
+    if (n == 0 || arcs == 0) return GEE_OK;
+    cudaStream_t st = gee::as_stream(stream);
+    k_csr_rows<<<grid_for(n * 32, 256, 16), 256, 0, st>>>(offsets, n, rows);
+    return gee::check_launch("k_csr_rows");
+}
+
+int gee_graph_stats(const int64_t *offsets, const float *w, int64_t n, int64_t arcs, double *max_row_abs,
+                    double *min_abs_nz, double *max_abs, int32_t *nonfinite, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(n >= 0 && arcs >= 0, GEE_ERR_INVALID, "n and arcs must be nonnegative");
+    Stats h{0.0, INFINITY, 0.0, 0};
+    if (n > 0 && arcs > 0) {
+        cudaStream_t st = gee::as_stream(stream);
+        Stats *d = nullptr;
+        GEE_CUDA(cudaMallocAsync((void **)&d, sizeof(Stats), st));
+        cudaMemcpyAsync(d, &h, sizeof(Stats), cudaMemcpyHostToDevice, st);
+        k_graph_stats<<<grid_for(n * 32, 256, 16), 256, 0, st>>>(offsets, w, n, d);
+        int rc = gee::check_launch("k_graph_stats");
+        cudaMemcpyAsync(&h, d, sizeof(Stats), cudaMemcpyDeviceToHost, st);
+        cudaFreeAsync(d, st);
+        GEE_CUDA(cudaStreamSynchronize(st));
+        if (rc) return rc;
+    }
+    if (max_row_abs) *max_row_abs = h.max_row_abs;
+    if (min_abs_nz) *min_abs_nz = h.min_abs_nz == INFINITY ? 0.0 : h.min_abs_nz;
+    if (max_abs) *max_abs = h.max_abs;
+    if (nonfinite) *nonfinite = h.nonfinite;
+    return GEE_OK;
+}
+
+}  // extern "C"

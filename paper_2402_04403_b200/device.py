@@ -1,0 +1,288 @@
+"""HBM-resident graphs and the edge-pass engine over the C ABI.
+
+torch provides device memory and streams only; every byte of the edge pass
+is computed by libgee_b200.so (include/gee_b200.h).  Nothing here falls back
+to the CPU: without a CUDA device the calls raise.
+"""
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib, ptr
+from .errors import ValidationError
+
+
+def require_cuda(device=None):
+    if not torch.cuda.is_available():
+        raise RuntimeError("the GEE edge pass runs on a CUDA device (sm_100a); none is visible")
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def to_device(a, dtype, device):
+    """numpy / torch array -> contiguous CUDA tensor of `dtype`."""
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=dtype).contiguous()
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.to(device=device, dtype=dtype, non_blocking=False).contiguous()
+
+
+def _stream():
+    return _lib.stream_handle()
+
+
+def label_dtype(k):
+    return {1: torch.uint8, 2: torch.int16, 4: torch.int32}[lib.gee_label_bytes(k)]
+
+
+class DeviceGraph:
+    """A listed edge multiset resident in HBM, laid out for the edge pass.
+
+    pull layout  symmetric CSR: row x holds (v, w) for every listed edge
+                 touching x (both endpoints; self-loops twice) -- the
+                 reference's SOURCE_ONLY storage (encoder.py:37-55) -- plus
+                 the tile plan (tile_row) and the fixed-point exponent.
+    push layout  the COO lists themselves (src, dst, w) with the edge rule
+                 (both updates, or source-only for arc lists).
+    """
+
+    def __init__(self, n, s_listed, device):
+        self.n = int(n)
+        self.s = int(s_listed)  # listed edges: the GEPS numerator
+        self.device = device
+        self.offsets = self.targets = self.weights = None
+        self.tile_row = None
+        self.scale_exp = 0
+        self.rel_err = 0.0
+        self.max_row_abs = 0.0
+        self.src = self.dst = self.w = None
+        self.coo_source_only = False
+
+    # ---------------------------------------------------------------- build
+    @classmethod
+    def from_edges(cls, src, dst, w, n, device=None, pull=True, keep_coo=False, stable=False):
+        """Upload a listed edge list and build the requested layouts."""
+        dev = require_cuda(device)
+        g = cls(n, len(src), dev)
+        src_d = to_device(src, torch.int32, dev)
+        dst_d = to_device(dst, torch.int32, dev)
+        w_d = to_device(w, torch.float32, dev)
+        if pull:
+            g._build_sym(src_d, dst_d, w_d, stable)
+        if keep_coo or not pull:
+            g.src, g.dst, g.w = src_d, dst_d, w_d
+        return g
+
+    @classmethod
+    def from_csr(cls, offsets, targets, weights, n, symmetric, device=None, pull=True, keep_coo=False):
+        """Upload a stored CsrGraph.
+
+        symmetric=True  (SOURCE_ONLY storage: each listed undirected edge is
+                         two arcs) -> already the pull layout; listed edges =
+                         arcs / 2.
+        symmetric=False (BOTH_ENDPOINTS storage: one arc per listed edge)
+                         -> expanded to COO and mirrored for pull.
+        """
+        dev = require_cuda(device)
+        off_d = to_device(offsets, torch.int64, dev)
+        tgt_d = to_device(targets, torch.int32, dev)
+        w_d = to_device(weights, torch.float32, dev)
+        arcs = int(tgt_d.numel())
+        if symmetric:
+            g = cls(n, arcs // 2, dev)
+            g.offsets, g.targets, g.weights = off_d, tgt_d, w_d
+            g._plan()
+            if keep_coo or not pull:
+                rows = torch.empty(arcs, dtype=torch.int32, device=dev)
+                check(lib.gee_csr_rows(ptr(off_d), n, arcs, ptr(rows), _stream()), "gee_csr_rows")
+                g.src, g.dst, g.w, g.coo_source_only = rows, tgt_d, w_d, True
+            return g
+        g = cls(n, arcs, dev)
+        rows = torch.empty(arcs, dtype=torch.int32, device=dev)
+        if arcs:
+            check(lib.gee_csr_rows(ptr(off_d), n, arcs, ptr(rows), _stream()), "gee_csr_rows")
+        if pull:
+            g._build_sym(rows, tgt_d, w_d, stable=False)
+        if keep_coo or not pull:
+            g.src, g.dst, g.w = rows, tgt_d, w_d
+        return g
+
+    def _build_sym(self, src_d, dst_d, w_d, stable):
+        n, s, dev = self.n, int(src_d.numel()), self.device
+        self.offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.targets = torch.empty(2 * s, dtype=torch.int32, device=dev)
+        self.weights = torch.empty(2 * s, dtype=torch.float32, device=dev) if w_d is not None else None
+        check(lib.gee_build_csr(ptr(src_d), ptr(dst_d), ptr(w_d), s, n, 1, 1 if stable else 0,
+                                ptr(self.offsets), ptr(self.targets), ptr(self.weights), _stream()),
+              "gee_build_csr")
+        self._plan()
+
+    def _plan(self):
+        arcs = self.arcs
+        n_tiles = int(lib.gee_pull_tiles(arcs))
+        self.tile_row = torch.empty(n_tiles + 1, dtype=torch.int64, device=self.device)
+        check(lib.gee_pull_plan(ptr(self.offsets), self.n, arcs, ptr(self.tile_row), _stream()), "gee_pull_plan")
+        mx, mn, mxa = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        nf = ctypes.c_int32()
+        check(lib.gee_graph_stats(ptr(self.offsets), ptr(self.weights), self.n, arcs, ctypes.byref(mx),
+                                  ctypes.byref(mn), ctypes.byref(mxa), ctypes.byref(nf), _stream()),
+              "gee_graph_stats")
+        if nf.value:
+            raise ValidationError("arc weights must be finite")
+        self.max_row_abs = mx.value
+        e, rel = ctypes.c_int32(), ctypes.c_double()
+        check(lib.gee_pull_scale_exp(mx.value, mn.value, ctypes.byref(e), ctypes.byref(rel)), "gee_pull_scale_exp")
+        self.scale_exp, self.rel_err = e.value, rel.value
+
+    @property
+    def arcs(self):
+        return 0 if self.targets is None else int(self.targets.numel())
+
+    @property
+    def has_pull(self):
+        return self.offsets is not None
+
+    @property
+    def has_push(self):
+        return self.src is not None
+
+    @property
+    def weighted(self):
+        return (self.weights is not None) if self.has_pull else (self.w is not None)
+
+    def csr_bytes(self):
+        b = 0
+        for t in (self.offsets, self.targets, self.weights):
+            if t is not None:
+                b += t.numel() * t.element_size()
+        return b
+
+
+# Fixed-point pull is accepted when its worst per-term relative rounding is
+# this far inside the 1e-4 parity bound.
+PULL_REL_ERR_MAX = 1e-6
+
+
+class Embedder:
+    """Reusable device state for one (n, k): projection buffers, compact
+    labels and the pull slot buffer.  `project` + `pull`/`push` is one edge
+    pass; nothing is allocated on those calls once warm."""
+
+    def __init__(self, n, k, device=None):
+        self.device = require_cuda(device)
+        self.n, self.k = int(n), int(k)
+        if self.k < 1:
+            raise ValidationError("class count k must be positive")
+        dev = self.device
+        self.counts = torch.zeros(self.k + 1, dtype=torch.int64, device=dev)
+        self.inv32 = torch.zeros(self.k + 1, dtype=torch.float32, device=dev)
+        self.inv64 = torch.zeros(self.k + 1, dtype=torch.float64, device=dev)
+        self.bad = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.label_bytes = int(lib.gee_label_bytes(self.k))
+        self.compact = torch.empty(max(self.n, 1), dtype=label_dtype(self.k), device=dev)
+        self.slots = None
+
+    # ------------------------------------------------------------------ K1
+    def project(self, labels_d, validate=True):
+        """Histogram + inv + compact labels (build_projection)."""
+        if labels_d.numel() != self.n:
+            raise ValidationError(f"graph has {self.n} nodes but labels have {labels_d.numel()}")
+        check(lib.gee_build_projection(ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.inv32),
+                                       ptr(self.inv64), ptr(self.compact), ptr(self.bad), None, _stream()),
+              "gee_build_projection")
+        if validate and int(self.bad.item()):
+            raise ValidationError(f"{int(self.bad.item())} labels outside [0, {self.k}]")
+        return self.counts
+
+    # ------------------------------------------------------------------ K4
+    def _ensure_slots(self, arcs):
+        need = int(lib.gee_pull_slots_bytes(arcs, self.k))
+        if self.slots is None or self.slots.numel() * 8 < need:
+            self.slots = torch.zeros(math.ceil(need / 8), dtype=torch.int64, device=self.device)
+
+    def new_z(self):
+        return torch.empty((self.n, self.k), dtype=torch.float32, device=self.device)
+
+    def pull(self, g: DeviceGraph, z=None):
+        if not g.has_pull:
+            raise ValidationError("graph has no pull (symmetric CSR) layout")
+        if g.n != self.n:
+            raise ValidationError(f"graph has {g.n} nodes but labels have {self.n}")
+        if g.weighted and g.rel_err > PULL_REL_ERR_MAX:
+            raise ValidationError(
+                f"weights span too wide a range for the exact fixed-point pull "
+                f"(rounding bound {g.rel_err:.2e}); use variant='push'")
+        z = self.new_z() if z is None else z
+        self._ensure_slots(g.arcs)
+        check(lib.gee_embed_csr_pull(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
+                                     ptr(g.tile_row), g.scale_exp, ptr(self.compact), self.label_bytes,
+                                     ptr(self.inv64), self.k, ptr(z), ptr(self.slots), _stream()),
+              "gee_embed_csr_pull")
+        return z
+
+    # ------------------------------------------------------------------ K3
+    def push(self, g: DeviceGraph, z=None, precombine=False, zero=True):
+        if not g.has_push:
+            raise ValidationError("graph has no push (COO) layout")
+        if g.n != self.n:
+            raise ValidationError(f"graph has {g.n} nodes but labels have {self.n}")
+        z = self.new_z() if z is None else z
+        flags = (_lib.GEE_ZERO_Z if zero else 0) | (_lib.GEE_SOURCE_ONLY if g.coo_source_only else 0)
+        if precombine:
+            flags |= _lib.GEE_PRECOMBINE
+        check(lib.gee_embed_coo(ptr(g.src), ptr(g.dst), ptr(g.w), int(g.src.numel()), ptr(self.compact),
+                                self.label_bytes, ptr(self.inv32), g.n, self.k, ptr(z), flags, _stream()),
+              "gee_embed_coo")
+        return z
+
+    def embed(self, g: DeviceGraph, labels_d, variant="auto", z=None, validate=True):
+        """One edge pass: projection then the chosen edge map."""
+        self.project(labels_d, validate=validate)
+        v = choose_variant(g, variant)
+        return self.pull(g, z) if v == "pull" else self.push(g, z)
+
+
+def choose_variant(g: DeviceGraph, variant="auto"):
+    """Pull wherever its layout exists and its fixed point is exact enough.
+
+    Measured on B200 (profiles/): pull writes each Z row once and reads
+    labels through L1/L2 with no Z read-modify-write; push pays a 32 B
+    sector RMW per red.global once Z outgrows L2 (~20 G red/s).
+    """
+    if variant not in ("auto", "pull", "push"):
+        raise ValidationError(f"unknown variant {variant!r}")
+    if variant != "auto":
+        return variant
+    if g.has_pull and (not g.weighted or g.rel_err <= PULL_REL_ERR_MAX):
+        return "pull"
+    if g.has_push:
+        return "push"
+    return "pull"
+
+
+def build_csr(el, stable=True):
+    """graph.build_csr on the GPU (mirror arcs for undirected lists)."""
+    from .graph import CsrGraph, _is_torch
+
+    dev = require_cuda(el.src.device if _is_torch(el.src) and el.src.is_cuda else None)
+    on_host = not (_is_torch(el.src) and el.src.is_cuda)
+    src_d = to_device(el.src, torch.int32, dev)
+    dst_d = to_device(el.dst, torch.int32, dev)
+    w_d = to_device(el.w, torch.float32, dev)
+    s, n = el.s, el.n
+    sym = 0 if el.directed else 1
+    arcs = s * (2 if sym else 1)
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    targets = torch.empty(arcs, dtype=torch.int32, device=dev)
+    weights = torch.empty(arcs, dtype=torch.float32, device=dev) if w_d is not None else None
+    check(lib.gee_build_csr(ptr(src_d), ptr(dst_d), ptr(w_d), s, n, sym, 1 if stable else 0, ptr(offsets),
+                            ptr(targets), ptr(weights), _stream()), "gee_build_csr")
+    if on_host:
+        offsets, targets = offsets.cpu().numpy(), targets.cpu().numpy()
+        weights = weights.cpu().numpy() if weights is not None else None
+    return CsrGraph(n=n, offsets=offsets, targets=targets, weights=weights, directed=el.directed)

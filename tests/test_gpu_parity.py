@@ -1,0 +1,258 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle.
+
+Bar (BASELINE.json north_star):
+  * class counts bit-exact;
+  * Z max relative error <= 1e-4 per entry vs the f64 oracle, entries that
+    are zero in the oracle exactly zero;
+  * exact equality where the values are fp32-representable (chain, mirror,
+    two-hub, hammer);
+  * the pull variant bit-stable run to run.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import case, golden_cases, rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2402_04403_b200 as gb  # noqa: E402
+from paper_2402_04403_b200 import synth  # noqa: E402
+from paper_2402_04403_b200.device import DeviceGraph, Embedder  # noqa: E402
+
+TOL = 1e-4  # max relative error vs the f64 oracle (fp32 Z)
+
+EXACT_CASES = ("chain", "mirror", "two_hub", "star_exact", "self_loops", "empty", "unlabeled")
+
+
+def _el(c):
+    w = c["w"]
+    return gb.EdgeList(n=int(c["n"]), src=c["src"], dst=c["dst"], w=w, directed=bool(c["directed"]))
+
+
+def _y(c):
+    return gb.LabelVector(labels=c["labels"], k=int(c["k"]))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("variant", ["pull", "push"])
+def test_golden_embed_serial(golden, variant):
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        z = gb.embed_serial(_el(c), _y(c), variant=variant)
+        assert z.dtype == np.float32 and z.shape == c["z_serial"].shape
+        assert rel_err(z, c["z_serial"]) <= TOL, (name, variant)
+        if name in ("chain", "mirror", "two_hub", "self_loops", "empty", "unlabeled"):
+            assert np.array_equal(z.astype(np.float64), c["z_serial"]), (name, variant)
+
+
+@pytest.mark.parametrize("variant", ["pull", "push"])
+def test_golden_embed_parallel_on_reference_csr(golden, variant):
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        g = gb.CsrGraph(n=int(c["n"]), offsets=c["csr_offsets"], targets=c["csr_targets"],
+                        weights=c["csr_weights"], directed=bool(c["directed"]))
+        z = gb.embed_parallel(g, _y(c), workers=8, variant=variant)
+        assert rel_err(z, c["z_parallel"]) <= TOL, (name, variant)
+        assert rel_err(z, c["z_serial"]) <= TOL, (name, variant)
+
+
+def test_class_counts_bit_exact(golden):
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        assert np.array_equal(gb.class_counts(_y(c)), c["class_counts"]), name
+    for i in range(5):
+        c = case(golden, f"counts{i}")
+        y = gb.LabelVector(labels=c["labels"], k=int(c["k"]))
+        assert np.array_equal(gb.class_counts(y), c["bincount"][1:])
+
+
+def test_projection_kats(golden):
+    for i in range(6):
+        c = case(golden, f"proj{i}")
+        p = gb.build_projection(gb.LabelVector(labels=c["labels"], k=int(c["k"])))
+        assert np.array_equal(p.to_dense(), c["dense"])
+
+
+def test_projection_warnings(caplog):
+    with caplog.at_level("WARNING", logger="paper_2402_04403_b200.encoder"):
+        gb.build_projection(gb.LabelVector(labels=[1, 1], k=3))
+    assert "no members" in caplog.text
+    with caplog.at_level("WARNING", logger="paper_2402_04403_b200.encoder"):
+        gb.build_projection(gb.LabelVector(labels=[0, 0], k=2))
+    assert "identically zero" in caplog.text
+
+
+def test_build_csr_matches_reference_order(golden):
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        g = gb.build_csr(_el(c), stable=True)
+        assert np.array_equal(g.offsets, c["csr_offsets"]), name
+        assert np.array_equal(g.targets, c["csr_targets"]), name
+        w = np.ones(g.s) if g.weights is None else g.weights
+        assert np.array_equal(np.asarray(w, dtype=np.float64), c["csr_weights"]), name
+
+
+def test_pull_bit_stable(golden):
+    for name in ("rand1", "rand2", "rand4", "rand5"):
+        c = case(golden, name)
+        a = gb.embed_serial(_el(c), _y(c), variant="pull")
+        b = gb.embed_serial(_el(c), _y(c), variant="pull")
+        assert np.array_equal(a, b), name
+
+
+def test_star_closed_form():
+    leaves = 1000
+    el = gb.EdgeList(n=leaves + 1, src=np.zeros(leaves), dst=np.arange(1, leaves + 1), directed=False)
+    y = gb.LabelVector(labels=[0] + [1] * leaves, k=1)
+    g = gb.build_csr(el)
+    for variant in ("pull", "push"):
+        z = gb.embed_parallel(g, y, variant=variant)
+        assert abs(z[0, 0] - 1.0) <= 1e-6
+        assert not z[1:].any()
+
+
+def two_hub(leaves):
+    n = leaves + 2
+    ids = np.arange(1, leaves + 1)
+    src = np.concatenate([np.zeros(leaves, np.int64), np.full(leaves, n - 1)])
+    dst = np.concatenate([ids, ids])
+    labels = np.zeros(n, dtype=np.int64)
+    labels[0] = labels[n - 1] = 1
+    return gb.EdgeList(n=n, src=src, dst=dst, directed=True), gb.LabelVector(labels=labels, k=2)
+
+
+@pytest.mark.parametrize("variant", ["pull", "push"])
+def test_race_graph_every_run(variant):
+    el, y = two_hub(100_000)
+    expected = oracle.serial_embed(el.src, el.dst, None, y.labels, el.n, y.k)
+    assert np.allclose(expected[1:-1, 0], 1.0)
+    dev = torch.device("cuda")
+    g = DeviceGraph.from_edges(el.src, el.dst, None, el.n, device=dev, pull=variant == "pull",
+                               keep_coo=variant == "push")
+    emb = Embedder(el.n, y.k, dev)
+    lab = torch.from_numpy(y.labels).to(dev)
+    z = emb.new_z()
+    for _ in range(100):
+        emb.embed(g, lab, variant=variant, z=z)
+        assert np.array_equal(z.cpu().numpy().astype(np.float64), expected)
+
+
+def test_red_hammer_exact():
+    # every edge hits Z[0, 0]; 0.5 increments stay exact in fp32
+    s = 800_000
+    el = gb.EdgeList(n=2, src=np.zeros(s), dst=np.ones(s), w=np.full(s, 0.5), directed=True)
+    y = gb.LabelVector(labels=[0, 1], k=1)
+    for variant in ("push", "pull"):
+        z = gb.embed_serial(el, y, variant=variant)
+        assert z[0, 0] == s * 0.5 and z[1, 0] == 0.0, variant
+
+
+def test_out_buffer_reused_and_validated(golden):
+    c = case(golden, "chain")
+    g = gb.CsrGraph(n=3, offsets=c["csr_offsets"], targets=c["csr_targets"], weights=c["csr_weights"])
+    out = np.full((3, 2), 7.0)
+    z = gb.embed_parallel(g, _y(c), workers=2, out=out)
+    assert z is out and out.tolist() == c["z_serial"].tolist()
+    out_d = torch.full((3, 2), 7.0, device="cuda")
+    z = gb.embed_parallel(g, _y(c), out=out_d)
+    assert z is out_d and z.cpu().numpy().tolist() == c["z_serial"].tolist()
+    with pytest.raises(gb.ValidationError):
+        gb.embed_parallel(g, _y(c), out=np.zeros((2, 2)))
+    with pytest.raises(gb.ValidationError):
+        gb.embed_parallel(g, _y(c), workers=0)
+    with pytest.raises(gb.ValidationError):
+        gb.embed_parallel(g, gb.LabelVector(labels=[1], k=2))
+    with pytest.raises(gb.ValidationError):
+        gb.embed_serial(_el(c), gb.LabelVector(labels=[1, 2], k=2))
+
+
+def test_device_tensors_in_device_tensor_out(golden):
+    c = case(golden, "rand4")
+    dev = torch.device("cuda")
+    z = gb.embed(torch.from_numpy(c["src"]).to(dev), torch.from_numpy(c["dst"]).to(dev),
+                 torch.from_numpy(c["labels"]).to(dev), int(c["n"]), int(c["k"]),
+                 weights=torch.from_numpy(c["w"]).to(dev), directed=bool(c["directed"]))
+    assert isinstance(z, torch.Tensor) and z.is_cuda
+    assert rel_err(z.cpu().numpy(), c["z_serial"]) <= TOL
+
+
+def test_synth_gpu_matches_numpy_restatement():
+    s, scale, seed = 20000, 16, 77
+    src, dst, w = synth.rmat_edges(scale, s, seed, weighted=True, first=12345)
+    es, ed, ew = synth.rmat_edges_numpy(scale, s, seed, weighted=True, first=12345)
+    assert np.array_equal(src.cpu().numpy(), es) and np.array_equal(dst.cpu().numpy(), ed)
+    assert np.array_equal(w.cpu().numpy(), ew)
+    src, dst, w = synth.er_edges(1000003, s, seed, weighted=True)
+    es, ed, ew = synth.er_edges_numpy(1000003, s, seed, weighted=True)
+    assert np.array_equal(src.cpu().numpy(), es) and np.array_equal(dst.cpu().numpy(), ed)
+    assert np.array_equal(w.cpu().numpy(), ew)
+    y = synth.uniform_labels(5000, 50, seed)
+    assert np.array_equal(y.cpu().numpy(), synth.uniform_labels_numpy(5000, 50, seed))
+
+
+def test_empty_and_trailing_rows():
+    # rows after the last arc and isolated rows in between must be zero
+    el = gb.EdgeList(n=10, src=[2, 3], dst=[3, 2], w=[1.0, 2.0])
+    y = gb.LabelVector(labels=[1] * 10, k=1)
+    for variant in ("pull", "push"):
+        z = gb.embed_serial(el, y, variant=variant)
+        exp = oracle.serial_embed(el.src, el.dst, el.w, y.labels, 10, 1)
+        assert rel_err(z, exp) <= TOL
+
+
+def _check_random(rng, n, s, k, weighted, directed, frac, variant):
+    src = rng.integers(0, n, s)
+    dst = rng.integers(0, n, s)
+    w = (2.0 * (1.0 - rng.random(s))).astype(np.float32) if weighted else None
+    y = gb.random_labels(n, k, frac, int(rng.integers(0, 2**31)))
+    el = gb.EdgeList(n=n, src=src, dst=dst, w=w, directed=directed)
+    z = gb.embed_serial(el, y, variant=variant)
+    exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
+    assert rel_err(z, exp) <= TOL
+
+
+@pytest.mark.parametrize("variant", ["pull", "push"])
+def test_random_battery(variant):
+    # test_acceptance.py:77-98 shapes, restated to the fp32 tolerance
+    rng = np.random.default_rng(2024)
+    for i in range(30):
+        n = int(rng.integers(2, 10_001))
+        s = int(rng.integers(0, 100_001))
+        _check_random(rng, n, s, (2, 10, 50, 300, 1000)[i % 5], bool(i % 3), bool(i % 2), (0.1, 1.0)[i % 2], variant)
+
+
+def test_hub_rows_span_many_tiles():
+    # one row with 100k arcs crosses ~25 pull tiles; plus a dense cluster
+    rng = np.random.default_rng(7)
+    n, k = 5000, 20
+    src = np.concatenate([np.zeros(100_000, np.int64), rng.integers(0, n, 50_000)])
+    dst = np.concatenate([rng.integers(0, n, 100_000), rng.integers(0, 50, 50_000)])
+    w = (1.0 - rng.random(src.size)).astype(np.float32)
+    y = gb.random_labels(n, k, 0.7, 5)
+    el = gb.EdgeList(n=n, src=src, dst=dst, w=w, directed=True)
+    exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
+    for variant in ("pull", "push"):
+        assert rel_err(gb.embed_serial(el, y, variant=variant), exp) <= TOL, variant
+
+
+def test_mass_accounting():
+    rng = np.random.default_rng(5)
+    for i in range(10):
+        n = int(rng.integers(2, 3000))
+        s = int(rng.integers(1, 30_000))
+        src, dst = rng.integers(0, n, s), rng.integers(0, n, s)
+        w = (2.0 * (1.0 - rng.random(s))).astype(np.float32)
+        y = gb.random_labels(n, 10, 0.1, seed=i)
+        _, inv, row = oracle.projection(y.labels, 10)
+        lab = y.labels
+        mass = np.where(lab[dst] > 0, row[dst] * w, 0.0).sum() + np.where(lab[src] > 0, row[src] * w, 0.0).sum()
+        z = gb.embed_serial(gb.EdgeList(n=n, src=src, dst=dst, w=w, directed=bool(i % 2)), y)
+        assert abs(z.astype(np.float64).sum() - mass) <= 1e-5 * max(1.0, abs(mass))

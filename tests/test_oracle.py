@@ -1,0 +1,127 @@
+"""Pin the CPU oracle (oracle/) to the reference before trusting it.
+
+Golden vectors come from running the reference itself
+(tests/golden/make_golden.py); the known-answer tests restate the
+reference's own (test_encoder.py, test_parallel.py, test_labeling.py).
+CPU only.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import case, golden_cases
+
+CHAIN_Z = [[0.5, 0.0], [0.5, 1.0], [0.5, 0.0]]
+
+
+def test_golden_has_cases(golden):
+    names = golden_cases(golden)
+    assert {"chain", "mirror", "star", "two_hub", "self_loops", "empty", "unlabeled"} <= set(names)
+    assert sum(n.startswith("rand") for n in names) == 10
+
+
+def test_serial_oracle_bitwise_equals_reference(golden):
+    # same arithmetic in the same order as serial_pass (_kernels.py:210-226)
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        z = oracle.serial_embed(c["src"], c["dst"], c["w"], c["labels"], int(c["n"]), int(c["k"]))
+        assert np.array_equal(z, c["z_serial"]), name
+
+
+def test_numpy_reference_matches_reference(golden):
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        z = oracle.numpy_reference(c["src"], c["dst"], c["w"], c["labels"], int(c["n"]), int(c["k"]))
+        assert np.max(np.abs(z - c["z_serial"]), initial=0.0) <= 1e-9, name
+
+
+def test_projection_matches_reference(golden):
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        counts, inv, row = oracle.projection(c["labels"], int(c["k"]))
+        assert np.array_equal(counts[1:], c["class_counts"]), name
+        assert np.array_equal(row, c["row_value"]), name
+
+
+def test_projection_kats(golden):
+    for i in range(6):
+        c = case(golden, f"proj{i}")
+        k = int(c["k"])
+        counts, inv, row = oracle.projection(c["labels"], k)
+        dense = np.zeros((c["labels"].size, k))
+        idx = np.nonzero(c["labels"])[0]
+        dense[idx, c["labels"][idx] - 1] = row[idx]
+        assert np.array_equal(dense, c["dense"])
+        assert np.array_equal(counts[1:], c["class_counts"])
+    for i in range(5):
+        c = case(golden, f"counts{i}")
+        assert np.array_equal(oracle.bincount(c["labels"], int(c["k"])), c["bincount"])
+
+
+def test_bincount_rejects_out_of_range():
+    with pytest.raises(ValueError):
+        oracle.bincount([0, 3], 2)
+
+
+def test_build_csr_matches_reference(golden):
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        off, tgt, wts = oracle.build_csr(c["src"], c["dst"], c["w"], int(c["n"]), bool(c["directed"]))
+        assert np.array_equal(off, c["csr_offsets"]), name
+        assert np.array_equal(tgt, c["csr_targets"]), name
+        assert np.array_equal(wts, c["csr_weights"]), name
+
+
+@pytest.mark.parametrize("workers", [1, 2, 4, 8])
+def test_parallel_port_matches_reference(golden, workers):
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        k = int(c["k"])
+        w = None if np.all(c["csr_weights"] == 1.0) else c["csr_weights"]
+        z = oracle.parallel_embed(c["csr_offsets"], c["csr_targets"], w, c["labels"], k, bool(c["directed"]), workers)
+        assert np.max(np.abs(z - c["z_parallel"]), initial=0.0) <= 1e-9, (name, workers)
+        assert np.max(np.abs(z - c["z_serial"]), initial=0.0) <= 1e-9, (name, workers)
+
+
+def test_known_answers(golden):
+    assert case(golden, "chain")["z_serial"].tolist() == CHAIN_Z
+    assert case(golden, "mirror")["z_parallel"].tolist() == [[0.0, 1.0], [1.0, 0.0]]
+    assert abs(case(golden, "star")["z_serial"][0, 0] - 1.0) <= 1e-12
+    assert np.allclose(case(golden, "two_hub")["z_serial"][1:-1, 0], 1.0)
+    assert not case(golden, "unlabeled")["z_serial"].any()
+    assert not case(golden, "empty")["z_serial"].any()
+
+
+def test_atomic_hammer_never_loses_updates():
+    z = oracle.atomic_hammer(100000, 0.5, 8)  # test_parallel.py:67-79
+    assert z[1] == 8 * 100000 * 0.5
+    assert z[0] == 0.0
+
+
+def test_sampled_rows_match_serial(golden):
+    for name in golden_cases(golden):
+        c = case(golden, name)
+        n, k = int(c["n"]), int(c["k"])
+        if not np.all(c["w"] == c["w"].astype(np.float32)):
+            continue
+        rows = np.arange(0, n, 3)
+        zs = oracle.sampled_rows(c["src"], c["dst"], c["w"].astype(np.float32), c["labels"], k, rows)
+        assert np.array_equal(zs, c["z_serial"][rows]), name
+
+
+def test_race_graph_port_every_run(golden):
+    c = case(golden, "two_hub")
+    k = int(c["k"])
+    for _ in range(20):
+        z = oracle.parallel_embed(c["csr_offsets"], c["csr_targets"], None, c["labels"], k, True, 8)
+        assert np.max(np.abs(z - c["z_serial"])) <= 1e-9
+
+
+def test_random_labels_mirror_reproduces_reference_stream(golden):
+    from paper_2402_04403_b200.labeling import random_labels
+
+    for i in range(3):
+        c = case(golden, f"rl{i}")
+        n, k, seed = (int(x) for x in c["args"])
+        assert np.array_equal(random_labels(n, k, float(c["fraction"]), seed).labels, c["labels"])
