@@ -1,0 +1,476 @@
+"""GEE edge-pass benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[3], the one the north-star metric is quoted
+on; it fits one B200): C4 = R-MAT(.57,.19,.19,.05) scale 27 (134M nodes),
+1.8e9 directed fp32-weighted edges, K = 50 uniform labels, seeded synthetic
+(Friendster is not available).
+
+A step = one edge pass over the whole graph:
+    K1 class histogram + inv + compact labels   (labels are an input)
+    K4 pull edge map (+ trailing-row zero fill + cross-tile finalize)
+Graph preparation (symmetric CSR build, tile plan, weight statistics) is
+outside the timed region, as the reference's bench keeps build_csr out
+(reference bench.py:1-7).  Inputs (30 GB CSR) are far larger than the
+126 MB L2, so no L2 flush is needed between steps.
+
+    value    listed edges / device time, inputs resident in HBM (GEPS)
+    e2e      same metric through the host-buffer path: pinned host CSR +
+             labels -> H2D, weight stats + tile plan, the step, Z -> pinned
+             host, all inside the timed region
+    roofline the pull kernel: algorithmic bytes / its CUDA-event time
+    cpu_baseline  the reference's parallel CPU edge map (oracle/ pthreads
+             port of embed_parallel, CAS f64 atomics), all host threads, on a
+             1/16 self-similar sample of C4 (R-MAT scale 23, same edge
+             factor, K, weights)
+
+Multi-GPU (torchrun, N ranks): each rank owns a contiguous row range
+balanced by arc counts (no collective on the data path: each rank writes
+its own Z rows); value = listed edges of the whole graph / max-over-ranks
+device time ("scaling": "strong", fixed total work).
+
+`--impl reference` times the CPU reference path alone (rank 0; other ranks
+exit 0).
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GEE edges/sec (GEPS) and % HBM roofline at 1/2/4/8 B200 vs host-CPU oracle"
+UNIT = "GEPS (1e9 listed edges/s)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (smaller runs)")
+    ap.add_argument("--edges", type=int, default=None, help="edge-count override")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-push", action="store_true")
+    ap.add_argument("--cpu-sample-div", type=int, default=16)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- helpers
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(workload):
+    """dram bytes per pull launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        if t.get("workload") == workload:
+            return float(t["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx.append(float(f[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(n_gpus):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        dist.barrier(device_ids=[torch.cuda.current_device()])
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------- CPU baseline
+def cpu_sample_graph(cfg_idx, div, scale_override):
+    """A self-similar 1/div sample of the workload in the reference's dtypes:
+    directed CSR (one arc per listed edge, BOTH_ENDPOINTS), int64 offsets,
+    int32 targets, f64 weights; int32 labels + f64 row_value."""
+    import torch
+
+    import oracle
+    from paper_2402_04403_b200 import synth
+
+    cfg = synth.CONFIGS[cfg_idx]
+    base_scale = scale_override or {3: 24, 4: 27}.get(cfg_idx, None)
+    if base_scale is None:
+        raise SystemExit("CPU sample defined for R-MAT configs")
+    shift = int(round(np.log2(div)))
+    scale = base_scale - shift
+    n = 1 << scale
+    s = int(round(cfg.s / cfg.n * n)) if not scale_override else int(round(cfg.s / cfg.n * n))
+    src, dst, w = synth.rmat_edges(scale, s, seed=cfg_idx, weighted=cfg.weighted, device="cuda")
+    y = synth.uniform_labels(n, cfg.k, seed=cfg_idx, device="cuda") if cfg_idx == 4 else None
+    if y is None:
+        from paper_2402_04403_b200.labeling import random_labels
+
+        y_h = random_labels(n, cfg.k, 0.1, seed=cfg_idx).labels
+    else:
+        y_h = y.cpu().numpy()
+    src_h, dst_h = src.cpu().numpy(), dst.cpu().numpy()
+    w_h = w.cpu().numpy().astype(np.float64) if w is not None else None
+    del src, dst, w
+    torch.cuda.empty_cache()
+    directed = True  # one arc per listed edge + BOTH accounting == the listed-edge pass
+    off, tgt, wts = oracle.build_csr(src_h, dst_h, w_h, n, directed)
+    del src_h, dst_h
+    _, _, row = oracle.projection(y_h, cfg.k)
+    return {"n": n, "s": s, "k": cfg.k, "scale": scale, "offsets": off, "targets": tgt,
+            "weights": None if w_h is None else wts, "labels": y_h.astype(np.int32), "row": row,
+            "sample": f"R-MAT scale {scale} (1/{div} of the workload's nodes and edges), {s} listed edges, "
+                      f"K={cfg.k}, same generator/weights/labels; reference dtypes (f64 Z)"}
+
+
+def time_cpu_reference(sample, steps, warmup, workers):
+    import oracle
+
+    z = np.empty((sample["n"], sample["k"]), dtype=np.float64)
+    args = (sample["offsets"], sample["targets"], sample["weights"], sample["labels"], sample["k"], True, workers)
+    kw = dict(out=z, row_value=sample["row"], label32=sample["labels"])
+    for _ in range(max(1, warmup)):
+        oracle.parallel_embed(*args, **kw)
+    times = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        oracle.parallel_embed(*args, **kw)
+        times.append(time.perf_counter() - t0)
+    return float(np.median(times)), times
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2402_04403_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    workers = os.cpu_count() or 1
+    sample = cpu_sample_graph(args.config, args.cpu_sample_div, args.scale)
+    steps = max(1, min(args.steps, 5))
+    med, times = time_cpu_reference(sample, steps, min(args.warmup, 1), workers)
+    geps = sample["s"] / med / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": geps, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": med * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "sample": sample["sample"], "world_size": world},
+        "cpu_baseline": {"value": geps, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": sample["sample"]},
+        "e2e": {"value": geps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- GPU arm
+def build_shard(args, world, rank):
+    """Generate the workload on this GPU and build this rank's pull layout."""
+    import torch
+
+    from paper_2402_04403_b200 import _lib, synth
+    from paper_2402_04403_b200.device import DeviceGraph, to_device
+    from paper_2402_04403_b200 import shard as shard_mod
+
+    t0 = time.perf_counter()
+    src, dst, w, y, n, k, directed = synth.make_config(args.config, scale_override=args.scale,
+                                                       edges_override=args.edges)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    s = int(src.numel())
+    t0 = time.perf_counter()
+    if world == 1:
+        g = DeviceGraph.from_edges(src, dst, w, n, pull=True, keep_coo=not args.no_push)
+        row_lo, row_hi = 0, n
+    else:
+        g, row_lo, row_hi = shard_mod.build_row_shard(src, dst, w, n, world, rank)
+        del src, dst, w
+    torch.cuda.synchronize()
+    t_prep = time.perf_counter() - t0
+    return g, y, n, k, s, directed, row_lo, row_hi, t_gen, t_prep
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    from paper_2402_04403_b200 import synth
+    from paper_2402_04403_b200.device import Embedder
+
+    world, rank, local = dist_setup(args.gpus)
+    cfg = synth.CONFIGS[args.config]
+    g, y, n, k, s, directed, row_lo, row_hi, t_gen, t_prep = build_shard(args, world, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    emb = Embedder(n, k, dev)
+    rows = row_hi - row_lo
+    z = torch.empty((rows, k), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(z_out):
+        emb.project(y, validate=False)
+        return emb.pull(g, z_out)
+
+    # warm-up (also validates labels once)
+    emb.project(y, validate=True)
+    for _ in range(args.warmup):
+        step(z)
+    torch.cuda.synchronize()
+
+    ev_pull = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for i in range(args.steps):
+            emb.project(y, validate=False)
+            ev_pull[i][0].record(stream)
+            emb.pull(g, z)
+            ev_pull[i][1].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+        # short timed regions get few nvidia-smi samples: keep the same load
+        # running (untimed) for another second so the clock record covers it
+        t_extra = time.perf_counter()
+        while time.perf_counter() - t_extra < 1.0:
+            step(z)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_total = start.elapsed_time(end)
+    ms_total = max_over_ranks(ms_total, world)
+    ms_step = ms_total / args.steps
+    ms_pull = float(np.mean([a.elapsed_time(b) for a, b in ev_pull]))
+    clk = clocks.summary()
+
+    # launches of OUR kernels per step: k_label_hist, k_inv, k_zero_tail, k_pull, k_pull_finalize
+    launches_per_step = 5
+
+    # roofline of the pull kernel (algorithmic bytes: its edges once as COO-
+    # equivalent listed edges, compact labels once, Z once)
+    peak_gbs, peak_kind = load_peaks()
+    weighted = g.weighted
+    s_local = g.arcs // 2 if world > 1 else s
+    pull_bytes = s_local * (8 + 4 * weighted) + n * 1 + rows * k * 4
+    achieved = pull_bytes / (ms_pull * 1e-3) / 1e9
+    step_bmin = s * (8 + 4 * weighted) + 4 * n + 4 * n * k  # SURVEY 8(d) B_min, whole graph
+    workload = cfg.name if not (args.scale or args.edges) else f"{cfg.name}-reduced(scale={args.scale},s={s})"
+
+    result = {
+        "metric": METRIC,
+        "value": s / (ms_step * 1e-3) / 1e9,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 (exact int64 fixed-point accumulation)" if weighted else "f32 (exact u32 counts)",
+        "data": "synthetic (seeded R-MAT; Friendster unavailable)",
+        "config": {"workload": workload, "n": n, "s_listed_edges": s, "k": k, "weighted": bool(weighted),
+                   "directed": bool(directed), "variant": "pull", "sym_arcs": g.arcs,
+                   "parallelism": f"row-range x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs (CSR %.1f GB) >> 126 MB L2; no flush needed" % (g.csr_bytes() / 1e9),
+                   "gen_s": round(t_gen, 3), "prep_s": round(t_prep, 3)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+                     "frac": achieved / peak_gbs, "traffic": load_traffic(workload), "kernel": "k_pull",
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_launch": pull_bytes,
+                     "pull_ms": ms_pull, "step_bmin_bytes": step_bmin,
+                     "step_frac": step_bmin / (ms_step * 1e-3) / 1e9 / (peak_gbs * world)},
+        "clocks": clk,
+        "gpu_launches": launches_per_step * args.steps,
+    }
+
+    # ---- variant measurement: push on the same graph (chosen by measurement)
+    if world == 1 and g.has_push:
+        zp = torch.empty((n, k), dtype=torch.float32, device=dev)
+        emb.push(g, zp)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        a.record(stream)
+        for _ in range(reps):
+            emb.project(y, validate=False)
+            emb.push(g, zp)
+        b.record(stream)
+        torch.cuda.synchronize()
+        result["variants_ms_per_step"] = {"pull": ms_step, "push": a.elapsed_time(b) / reps}
+        del zp
+        g.src = g.dst = g.w = None
+        torch.cuda.empty_cache()
+
+    # ---- e2e through host buffers
+    if not args.no_e2e and world == 1:
+        result["e2e"] = run_e2e(g, y, emb, z, s, args)
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    if not args.no_cpu and world == 1 and rank == 0:
+        try:
+            sample = cpu_sample_graph(args.config, args.cpu_sample_div, args.scale)
+            workers = os.cpu_count() or 1
+            med, _ = time_cpu_reference(sample, 3, 1, workers)
+            result["cpu_baseline"] = {"value": sample["s"] / med / 1e9, "unit": UNIT, "cores": workers,
+                                      "kind": "port", "sample": sample["sample"], "ms_per_step": med * 1e3}
+        except SystemExit as e:
+            result["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                                      "sample": str(e)}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(g, y, emb, z, s, args):
+    """Host buffers in, host Z out: pinned H2D of the CSR + labels, weight
+    statistics + tile plan, histogram, pull, D2H of Z -- all timed."""
+    import torch
+
+    from paper_2402_04403_b200.device import DeviceGraph
+
+    dev = z.device
+    pin = lambda t: None if t is None else t.cpu().pin_memory()  # noqa: E731
+    h_off, h_tgt, h_w, h_y = pin(g.offsets), pin(g.targets), pin(g.weights), pin(y)
+    h_z = torch.empty(z.shape, dtype=torch.float32).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in (h_off, h_tgt, h_w, h_y) if t is not None)
+    d2h = h_z.numel() * 4
+    d_off, d_tgt, d_y = g.offsets, g.targets, y
+    d_w = g.weights
+    stream = torch.cuda.current_stream()
+
+    def e2e_step():
+        d_off.copy_(h_off, non_blocking=True)
+        d_tgt.copy_(h_tgt, non_blocking=True)
+        if h_w is not None:
+            d_w.copy_(h_w, non_blocking=True)
+        d_y.copy_(h_y, non_blocking=True)
+        g2 = DeviceGraph(g.n, g.s, dev)
+        g2.offsets, g2.targets, g2.weights = d_off, d_tgt, d_w
+        g2._plan()  # tile plan + weight statistics (host sync for the exponent)
+        emb.project(d_y, validate=False)
+        emb.pull(g2, z)
+        h_z.copy_(z, non_blocking=True)
+        stream.synchronize()
+
+    e2e_step()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.e2e_steps
+    return {"value": s / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "steps": args.e2e_steps,
+            "path": "host pinned CSR+labels -> gee_graph_stats/gee_pull_plan/gee_build_projection/"
+                    "gee_embed_csr_pull -> host pinned Z"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

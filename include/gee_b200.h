@@ -108,6 +108,17 @@ int gee_build_csr(const int32_t *src, const int32_t *dst, const float *w, int64_
                   int64_t n, int32_t symmetric, int32_t stable, int64_t *offsets,
                   int32_t *targets, float *weights, void *stream);
 
+/* Multi-GPU row-range ownership: offsets[n+1] of the full
+ * symmetric CSR (degree count + scan, no fill) for the partition planner,
+ * then the shard of rows [row_lo, row_hi): offsets[rows+1] rebased to 0,
+ * targets/weights of those rows' arcs (sized full_offsets[hi]-full_offsets[lo]). */
+int gee_sym_offsets(const int32_t *src, const int32_t *dst, int64_t s, int64_t n,
+                    int64_t *offsets, void *stream);
+int gee_build_sym_csr_rows(const int32_t *src, const int32_t *dst, const float *w, int64_t s,
+                           int64_t n, int64_t row_lo, int64_t row_hi,
+                           const int64_t *full_offsets, int64_t *offsets, int32_t *targets,
+                           float *weights, void *stream);
+
 /* CSR (offsets, arcs) -> per-arc source row (COO src) for a stored CsrGraph,
  * so that a directed CsrGraph (EdgeAccounting.BOTH_ENDPOINTS) can be fed to
  * gee_build_sym_csr or gee_embed_coo.  rows[arcs] int32. */

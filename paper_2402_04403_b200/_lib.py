@@ -46,6 +46,8 @@ SIGNATURES = {
     "gee_build_sym_csr": (c_int, [vp, vp, vp, c_i64, c_i64, vp, vp, vp, vp]),
     "gee_build_csr": (c_int, [vp, vp, vp, c_i64, c_i64, c_i32, c_i32, vp, vp, vp, vp]),
     "gee_csr_rows": (c_int, [vp, c_i64, c_i64, vp, vp]),
+    "gee_sym_offsets": (c_int, [vp, vp, c_i64, c_i64, vp, vp]),
+    "gee_build_sym_csr_rows": (c_int, [vp, vp, vp, c_i64, c_i64, c_i64, c_i64, vp, vp, vp, vp, vp]),
     "gee_graph_stats": (c_int, [vp, vp, c_i64, c_i64, P_dbl, P_dbl, P_dbl, P_i32, vp]),
     "gee_pull_tiles": (c_i64, [c_i64]),
     "gee_pull_slots_bytes": (c_size, [c_i64, c_i32]),

@@ -85,6 +85,39 @@ __global__ void k_arc_gather(const int32_t *__restrict__ src, const int32_t *__r
     }
 }
 
+// Row-range shard of the symmetric CSR: keep arcs whose row is in [lo, hi).
+__global__ void k_scatter_rows(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                               const float *__restrict__ w, int64_t s, int64_t lo, int64_t hi,
+                               unsigned long long *__restrict__ cursor, int32_t *__restrict__ targets,
+                               float *__restrict__ weights)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = src[i], v = dst[i];
+        if (u >= lo && u < hi) {
+            unsigned long long p = atomicAdd(&cursor[u - lo], 1ull);
+            targets[p] = v;
+            if (weights) weights[p] = w[i];
+        }
+        if (v >= lo && v < hi) {
+            unsigned long long p = atomicAdd(&cursor[v - lo], 1ull);
+            targets[p] = u;
+            if (weights) weights[p] = w[i];
+        }
+    }
+}
+
+__global__ void k_rebase(const int64_t *__restrict__ full, int64_t lo, int64_t rows, int64_t *__restrict__ local,
+                         unsigned long long *__restrict__ cursor)
+{
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = full[lo + r] - full[lo];
+        local[r] = v;
+        if (r < rows) cursor[r] = (unsigned long long)v;
+    }
+}
+
 __global__ void k_csr_rows(const int64_t *__restrict__ offsets, int64_t n, int32_t *__restrict__ rows)
 {
     const int lane = threadIdx.x & 31;
@@ -248,6 +281,64 @@ int gee_build_sym_csr(const int32_t *src, const int32_t *dst, const float *w, in
                       int64_t *offsets, int32_t *targets, float *weights, void *stream)
 {
     return gee_build_csr(src, dst, w, s, n, 1, 0, offsets, targets, weights, stream);
+}
+
+int gee_sym_offsets(const int32_t *src, const int32_t *dst, int64_t s, int64_t n, int64_t *offsets,
+                    void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(n >= 0 && s >= 0, GEE_ERR_INVALID, "n and s must be nonnegative");
+    GEE_REQUIRE(offsets != nullptr, GEE_ERR_INVALID, "offsets must not be NULL");
+    cudaStream_t st = gee::as_stream(stream);
+    GEE_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t) * (size_t)(n + 1), st));
+    if (s == 0 || n == 0) return GEE_OK;
+    unsigned long long *bad = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    unsigned long long nbad = 0;
+    int rc = GEE_OK;
+    GEE_CUDA(cudaMallocAsync((void **)&bad, sizeof(unsigned long long), st));
+    GEE_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), st));
+    k_degree<<<grid_for(s, 256, 16), 256, 0, st>>>(src, dst, s, n, 1, reinterpret_cast<unsigned long long *>(offsets),
+                                                   bad);
+    if ((rc = gee::check_launch("k_degree"))) goto out;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, offsets + 1, offsets + 1, n, st);
+    if (cudaMallocAsync(&tmp, tmp_bytes, st) != cudaSuccess) { gee::set_error("scratch alloc failed"); rc = GEE_ERR_CUDA; goto out; }
+    cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, offsets + 1, offsets + 1, n, st);
+    if ((rc = gee::check_launch("DeviceScan::InclusiveSum"))) goto out;
+    cudaMemcpyAsync(&nbad, bad, sizeof(nbad), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) { gee::set_error("sync failed"); rc = GEE_ERR_CUDA; goto out; }
+    if (nbad) {
+        gee::set_error("%llu edge endpoints outside [0, %lld)", nbad, (long long)n);
+        rc = GEE_ERR_RANGE;
+    }
+out:
+    if (tmp) cudaFreeAsync(tmp, st);
+    if (bad) cudaFreeAsync(bad, st);
+    return rc;
+}
+
+int gee_build_sym_csr_rows(const int32_t *src, const int32_t *dst, const float *w, int64_t s, int64_t n,
+                           int64_t row_lo, int64_t row_hi, const int64_t *full_offsets, int64_t *offsets,
+                           int32_t *targets, float *weights, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(0 <= row_lo && row_lo <= row_hi && row_hi <= n, GEE_ERR_INVALID, "row range [%lld, %lld) outside [0, %lld]",
+                (long long)row_lo, (long long)row_hi, (long long)n);
+    GEE_REQUIRE(full_offsets && offsets, GEE_ERR_INVALID, "offsets must not be NULL");
+    cudaStream_t st = gee::as_stream(stream);
+    const int64_t rows = row_hi - row_lo;
+    unsigned long long *cursor = nullptr;
+    GEE_CUDA(cudaMallocAsync((void **)&cursor, sizeof(unsigned long long) * (size_t)(rows ? rows : 1), st));
+    k_rebase<<<grid_for(rows + 1, 256, 16), 256, 0, st>>>(full_offsets, row_lo, rows, offsets, cursor);
+    int rc = gee::check_launch("k_rebase");
+    if (!rc && s > 0 && rows > 0) {
+        k_scatter_rows<<<grid_for(s, 256, 16), 256, 0, st>>>(src, dst, w, s, row_lo, row_hi, cursor, targets,
+                                                             w ? weights : nullptr);
+        rc = gee::check_launch("k_scatter_rows");
+    }
+    cudaFreeAsync(cursor, st);
+    return rc;
 }
 
 int gee_csr_rows(const int64_t *offsets, int64_t n, int64_t arcs, int32_t *rows, void *stream)

@@ -52,7 +52,8 @@ class DeviceGraph:
     """
 
     def __init__(self, n, s_listed, device):
-        self.n = int(n)
+        self.n = int(n)  # rows of this layout (a shard's local rows)
+        self.n_nodes = int(n)  # nodes the labels cover (global for a shard)
         self.s = int(s_listed)  # listed edges: the GEPS numerator
         self.device = device
         self.offsets = self.targets = self.weights = None
@@ -211,13 +212,14 @@ class Embedder:
     def pull(self, g: DeviceGraph, z=None):
         if not g.has_pull:
             raise ValidationError("graph has no pull (symmetric CSR) layout")
-        if g.n != self.n:
+        if g.n_nodes != self.n:
             raise ValidationError(f"graph has {g.n} nodes but labels have {self.n}")
         if g.weighted and g.rel_err > PULL_REL_ERR_MAX:
             raise ValidationError(
                 f"weights span too wide a range for the exact fixed-point pull "
                 f"(rounding bound {g.rel_err:.2e}); use variant='push'")
-        z = self.new_z() if z is None else z
+        if z is None:
+            z = torch.empty((g.n, self.k), dtype=torch.float32, device=self.device)
         self._ensure_slots(g.arcs)
         check(lib.gee_embed_csr_pull(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
                                      ptr(g.tile_row), g.scale_exp, ptr(self.compact), self.label_bytes,
@@ -229,7 +231,7 @@ class Embedder:
     def push(self, g: DeviceGraph, z=None, precombine=False, zero=True):
         if not g.has_push:
             raise ValidationError("graph has no push (COO) layout")
-        if g.n != self.n:
+        if g.n_nodes != self.n:
             raise ValidationError(f"graph has {g.n} nodes but labels have {self.n}")
         z = self.new_z() if z is None else z
         flags = (_lib.GEE_ZERO_Z if zero else 0) | (_lib.GEE_SOURCE_ONLY if g.coo_source_only else 0)
