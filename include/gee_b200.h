@@ -48,9 +48,13 @@ int gee_version(void);
 /* Thread-local message of the last failing call ("" if none). */
 const char *gee_last_error(void);
 
-/* Bytes per compact label the library uses for k classes: 1 (k <= 255),
- * 2 (k <= 65535) or 4. */
-int gee_label_bytes(int32_t k);
+/* Packed label format.  gee_build_projection writes the labels as u32
+ * words holding per = 32/bits labels of `bits` bits each, label i in word
+ * i/per at bit (i%per)*bits; bits = gee_label_bits(k), the smallest of
+ * {1,2,3,4,5,6,8,10,16} that holds k (32 = raw int32 labels, one per word).
+ * K=50 -> 6 bits, 5 per word (C4's 134M labels: 107 MB, L2-resident). */
+int gee_label_bits(int32_t k);
+int64_t gee_label_words(int64_t n, int32_t label_bits);
 
 /* ---------------------------------------------------------------- K1 ----
  * Class-count histogram + projection scalars.
@@ -59,7 +63,7 @@ int gee_label_bytes(int32_t k);
  *   counts[k+1]   int64, bit-exact np.bincount(labels, minlength=k+1)
  *   inv_f32[k+1]  float, inv_f32[c] = (float)(1.0/counts[c]) or 0; inv[0] = 0
  *   inv_f64[k+1]  double, same in f64 (may be NULL)
- *   compact       n labels narrowed to gee_label_bytes(k) bytes (may be NULL)
+ *   packed        gee_label_words(n, gee_label_bits(k)) packed label words (may be NULL)
  *   bad           int64 device scalar: number of labels outside [0,k] (may be
  *                 NULL).  Counts of out-of-range labels are dropped.
  *   work          device scratch of gee_projection_work_bytes(k) bytes
@@ -67,7 +71,7 @@ int gee_label_bytes(int32_t k);
 size_t gee_projection_work_bytes(int32_t k);
 int gee_build_projection(const int32_t *labels, int64_t n, int32_t k,
                          int64_t *counts, float *inv_f32, double *inv_f64,
-                         void *compact, int64_t *bad, void *work, void *stream);
+                         uint32_t *packed, int64_t *bad, void *work, void *stream);
 
 /* ---------------------------------------------------------------- K3 ----
  * Push edge map over a listed edge list (COO, structure of arrays).
@@ -77,12 +81,13 @@ int gee_build_projection(const int32_t *labels, int64_t n, int32_t k,
  *   Per edge i (u=src[i], v=dst[i], w = w ? w[i] : 1):
  *     if Y[v]: Z[u, Y[v]-1] += inv[Y[v]] * w
  *     if Y[u] and !(flags & GEE_SOURCE_ONLY): Z[v, Y[u]-1] += inv[Y[u]] * w
- *   labels: compact labels (label_bytes = 1, 2 or 4).  inv: inv_f32[k+1].
+ *   labels: packed words with label_bits = gee_label_bits(k), or raw int32
+ *   labels with label_bits = 32.  inv: inv_f32[k+1].
  *   Accumulation order is unspecified (fp32 atomics): results match the
  *   serial f64 oracle within fp32 accumulation error.
  */
 int gee_embed_coo(const int32_t *src, const int32_t *dst, const float *w, int64_t s,
-                  const void *labels, int32_t label_bytes, const float *inv,
+                  const uint32_t *labels, int32_t label_bits, const float *inv,
                   int64_t n, int32_t k, float *z, uint32_t flags, void *stream);
 
 /* ---------------------------------------------------------------- K5 ----
@@ -148,14 +153,14 @@ int gee_graph_stats(const int64_t *offsets, const float *w, int64_t n, int64_t a
  * zero_worker _kernels.py:124-135, arc_pass_worker _kernels.py:138-207)
  * for SOURCE_ONLY (symmetric) storage.
  */
-#define GEE_TILE_ARCS 4096
+#define GEE_TILE_ARCS 2048
 int64_t gee_pull_tiles(int64_t arcs);
 size_t gee_pull_slots_bytes(int64_t arcs, int32_t k);
 int gee_pull_plan(const int64_t *offsets, int64_t n, int64_t arcs, int64_t *tile_row,
                   void *stream);
 int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const float *w,
                        int64_t n, int64_t arcs, const int64_t *tile_row, int32_t scale_exp,
-                       const void *labels, int32_t label_bytes, const double *inv,
+                       const uint32_t *labels, int32_t label_bits, const double *inv,
                        int32_t k, float *z, void *slots, void *stream);
 
 /* Choose the fixed-point exponent for a weighted pull: the largest e with

@@ -21,7 +21,7 @@ GEE_ZERO_Z = 1
 GEE_SOURCE_ONLY = 2
 GEE_PRECOMBINE = 4
 
-TILE_ARCS = 4096
+TILE_ARCS = 2048
 
 c_int = ctypes.c_int
 c_i32 = ctypes.c_int32
@@ -39,7 +39,8 @@ P_i32 = ctypes.POINTER(ctypes.c_int32)
 SIGNATURES = {
     "gee_version": (c_int, []),
     "gee_last_error": (ctypes.c_char_p, []),
-    "gee_label_bytes": (c_int, [c_i32]),
+    "gee_label_bits": (c_int, [c_i32]),
+    "gee_label_words": (c_i64, [c_i64, c_i32]),
     "gee_projection_work_bytes": (c_size, [c_i32]),
     "gee_build_projection": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp, vp, vp, vp]),
     "gee_embed_coo": (c_int, [vp, vp, vp, c_i64, vp, c_i32, vp, c_i64, c_i32, vp, c_u32, vp]),

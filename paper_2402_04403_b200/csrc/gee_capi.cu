@@ -36,11 +36,4 @@ int gee_version(void) { return 100; }
 
 const char *gee_last_error(void) { return gee::g_err; }
 
-int gee_label_bytes(int32_t k)
-{
-    if (k <= 255) return 1;
-    if (k <= 65535) return 2;
-    return 4;
-}
-
 }  // extern "C"

@@ -1,15 +1,15 @@
-// K1: class-count histogram + projection scalars + compact labels.
+// K1: class-count histogram + projection scalars + packed labels.
 //
 // Restates build_projection (reference encoder.py:80-103): counts =
 // np.bincount(labels, minlength=k+1) (:87), inv[c] = 1/counts[c] for
 // nonempty classes, inv[0] = 0 (:95-97).  W is never materialised: the edge
 // kernels look up inv[Y[x]].
 //
-// One pass over the int32 labels (HBM-bound: 4 B read + label_bytes written
-// per node).  Each CTA keeps up to 32 lane-privatised copies of the K+1 bin
+// One pass over the int32 labels (HBM-bound: 4 B read + bits/8 B written per
+// node).  Each thread builds one packed label word (gee_common.cuh
+// LabelFmt); each CTA keeps up to 32 lane-privatised copies of the K+1 bin
 // histogram in shared memory (u32 ATOMS.ADD, measured 8.5 op/clk/SM on
-// B200), flushes them with 64-bit global atomics, and narrows each label to
-// u8/u16 on the way through so the edge kernels gather 1-2 B per endpoint.
+// B200) and flushes them with 64-bit global atomics.
 #include "gee_common.cuh"
 
 namespace {
@@ -17,14 +17,10 @@ namespace {
 constexpr int HIST_THREADS = 512;
 constexpr int HIST_SMEM_WORDS = 12288;  // 48 KB of bins
 
-template <typename LB>
-__device__ __forceinline__ void put_label(LB *compact, int64_t i, int32_t c) { compact[i] = (LB)c; }
-
-template <typename LB>
 __global__ void __launch_bounds__(HIST_THREADS)
-k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k,
-             unsigned long long *__restrict__ counts, LB *__restrict__ compact,
-             unsigned long long *__restrict__ bad, int copies, bool vec)
+k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, gee::LabelFmt f,
+             unsigned long long *__restrict__ counts, uint32_t *__restrict__ packed,
+             unsigned long long *__restrict__ bad, int copies)
 {
     extern __shared__ uint32_t hist[];  // copies * (k+1) bins
     const int bins = k + 1;
@@ -34,36 +30,27 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k,
     __syncthreads();
     uint32_t *mine = smem ? hist + (threadIdx.x % copies) * bins : nullptr;
     uint32_t nbad = 0;
-
-    auto count = [&](int64_t i, int32_t c) {
-        if ((uint32_t)c > (uint32_t)k) {  // outside [0, k] (LabelVector, labeling.py:24-29)
-            nbad++;
-            c = 0;
-        } else if (smem) {
-            atomicAdd(&mine[c], 1u);
-        } else {
-            atomicAdd(&counts[c], 1ull);
-        }
-        if (compact) put_label(compact, i, c);
-    };
-
+    const int64_t words = (n + f.per - 1) / f.per;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t done = 0;
-    if (vec) {
-        const int64_t n4 = n >> 2;
-        const int4 *l4 = reinterpret_cast<const int4 *>(labels);
-        for (int64_t q = start; q < n4; q += stride) {
-            int4 v = __ldcs(l4 + q);
-            count(4 * q + 0, v.x);
-            count(4 * q + 1, v.y);
-            count(4 * q + 2, v.z);
-            count(4 * q + 3, v.w);
+    for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < words; wi += stride) {
+        uint32_t word = 0;
+        const int64_t i0 = wi * f.per;
+        for (uint32_t j = 0; j < f.per; j++) {
+            const int64_t i = i0 + j;
+            if (i >= n) break;
+            int32_t c = __ldcs(labels + i);
+            if ((uint32_t)c > (uint32_t)k) {  // outside [0, k] (LabelVector, labeling.py:24-29)
+                nbad++;
+                c = 0;
+            } else if (smem) {
+                atomicAdd(&mine[c], 1u);
+            } else {
+                atomicAdd(&counts[c], 1ull);
+            }
+            word |= ((uint32_t)c & f.mask) << (j * f.bits);
         }
-        done = n4 << 2;
+        if (packed) __stcs(packed + wi, word);
     }
-    for (int64_t i = done + start; i < n; i += stride) count(i, __ldcs(labels + i));
-
     __syncthreads();
     if (smem) {
         for (int c = threadIdx.x; c < bins; c += blockDim.x) {
@@ -86,49 +73,54 @@ __global__ void k_inv(const unsigned long long *__restrict__ counts, int32_t k,
     if (inv64) inv64[c] = d;
 }
 
-template <typename LB>
-int launch_hist(const int32_t *labels, int64_t n, int32_t k, unsigned long long *counts,
-                LB *compact, unsigned long long *bad, cudaStream_t st)
-{
-    const int bins = k + 1;
-    int copies = HIST_SMEM_WORDS / bins;
-    if (copies > 32) copies = 32;
-    size_t sh = copies > 0 ? (size_t)copies * bins * sizeof(uint32_t) : 0;
-    int64_t want = (n + HIST_THREADS * 4 - 1) / (HIST_THREADS * 4);
-    int64_t cap = (int64_t)gee::sm_count() * 4;
-    int grid = (int)(want < 1 ? 1 : (want > cap ? cap : want));
-    bool vec = gee::aligned16(labels);
-    k_label_hist<LB><<<grid, HIST_THREADS, sh, st>>>(labels, n, k, counts, compact, bad, copies, vec);
-    return gee::check_launch("k_label_hist");
-}
-
 }  // namespace
 
 extern "C" {
 
+int gee_label_bits(int32_t k)
+{
+    static const int widths[] = {1, 2, 3, 4, 5, 6, 8, 10, 16};
+    for (int b : widths)
+        if (k <= (1 << b) - 1) return b;
+    return 32;
+}
+
+int64_t gee_label_words(int64_t n, int32_t label_bits)
+{
+    if (label_bits != 32 && (label_bits < 1 || label_bits > 16)) return -1;
+    const int64_t per = 32 / label_bits;
+    return (n + per - 1) / per;
+}
+
 size_t gee_projection_work_bytes(int32_t) { return 0; }
 
 int gee_build_projection(const int32_t *labels, int64_t n, int32_t k, int64_t *counts,
-                         float *inv_f32, double *inv_f64, void *compact, int64_t *bad,
+                         float *inv_f32, double *inv_f64, uint32_t *packed, int64_t *bad,
                          void *, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1, GEE_ERR_INVALID, "class count k must be positive (got %d)", k);
     GEE_REQUIRE(n >= 0, GEE_ERR_INVALID, "node count must be nonnegative");
+    GEE_REQUIRE(n <= INT32_MAX, GEE_ERR_INVALID, "node count %lld exceeds int32", (long long)n);
     GEE_REQUIRE(counts != nullptr, GEE_ERR_INVALID, "counts must not be NULL");
     GEE_REQUIRE(n == 0 || labels != nullptr, GEE_ERR_INVALID, "labels must not be NULL");
     cudaStream_t st = gee::as_stream(stream);
     GEE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t)(k + 1), st));
     if (bad) GEE_CUDA(cudaMemsetAsync(bad, 0, sizeof(int64_t), st));
     auto *cnt = reinterpret_cast<unsigned long long *>(counts);
-    auto *nb = reinterpret_cast<unsigned long long *>(bad);
-    int rc = GEE_OK;
     if (n > 0) {
-        switch (gee_label_bytes(k)) {
-        case 1: rc = launch_hist<uint8_t>(labels, n, k, cnt, (uint8_t *)compact, nb, st); break;
-        case 2: rc = launch_hist<uint16_t>(labels, n, k, cnt, (uint16_t *)compact, nb, st); break;
-        default: rc = launch_hist<int32_t>(labels, n, k, cnt, (int32_t *)compact, nb, st); break;
-        }
+        const gee::LabelFmt f = gee::label_fmt(gee_label_bits(k));
+        const int bins = k + 1;
+        int copies = HIST_SMEM_WORDS / bins;
+        if (copies > 32) copies = 32;
+        size_t sh = copies > 0 ? (size_t)copies * bins * sizeof(uint32_t) : 0;
+        const int64_t words = (n + f.per - 1) / f.per;
+        int64_t want = (words + HIST_THREADS - 1) / HIST_THREADS;
+        int64_t cap = (int64_t)gee::sm_count() * 4;
+        int grid = (int)(want < 1 ? 1 : (want > cap ? cap : want));
+        k_label_hist<<<grid, HIST_THREADS, sh, st>>>(labels, n, k, f, cnt, packed,
+                                                     reinterpret_cast<unsigned long long *>(bad), copies);
+        int rc = gee::check_launch("k_label_hist");
         if (rc) return rc;
     }
     if (inv_f32 || inv_f64) {

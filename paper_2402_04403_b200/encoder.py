@@ -196,7 +196,7 @@ def embed_parallel(
     """
     import torch
 
-    from .device import DeviceGraph, Embedder, require_cuda, to_device
+    from .device import PULL_REL_ERR_MAX, DeviceGraph, Embedder, require_cuda, to_device
 
     if g.n != y.n:
         raise ValidationError(f"graph has {g.n} nodes but labels have {y.n}")
@@ -216,7 +216,7 @@ def embed_parallel(
     want_push = variant == "push"
     dg = DeviceGraph.from_csr(g.offsets, g.targets, g.weights, g.n, symmetric, device=dev,
                               pull=not want_push, keep_coo=want_push)
-    if variant == "auto" and dg.weighted and dg.rel_err > 1e-6:
+    if variant == "auto" and dg.weighted and dg.rel_err > PULL_REL_ERR_MAX:
         dg = DeviceGraph.from_csr(g.offsets, g.targets, g.weights, g.n, symmetric, device=dev,
                                   pull=False, keep_coo=True)
         variant = "push"
