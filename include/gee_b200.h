@@ -153,7 +153,7 @@ int gee_graph_stats(const int64_t *offsets, const float *w, int64_t n, int64_t a
  * zero_worker _kernels.py:124-135, arc_pass_worker _kernels.py:138-207)
  * for SOURCE_ONLY (symmetric) storage.
  */
-#define GEE_TILE_ARCS 2048
+#define GEE_TILE_ARCS 4096
 int64_t gee_pull_tiles(int64_t arcs);
 size_t gee_pull_slots_bytes(int64_t arcs, int32_t k);
 int gee_pull_plan(const int64_t *offsets, int64_t n, int64_t arcs, int64_t *tile_row,
@@ -162,6 +162,28 @@ int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const flo
                        int64_t n, int64_t arcs, const int64_t *tile_row, int32_t scale_exp,
                        const uint32_t *labels, int32_t label_bits, const double *inv,
                        int32_t k, float *z, void *slots, void *stream);
+
+/* Hot-label tier (graph preparation; see gee_hot.cu).  gee_hot_plan ranks
+ * vertices by degree offsets[v+1]-offsets[v] (descending, ties by id) and
+ * marks the top max_hot with degree >= min_degree: hot_rank[v] = rank or -1,
+ * hot_vertex[rank] = v (may be NULL), *n_hot (host) = count.
+ * gee_hot_encode rewrites targets t of hot vertices as 0x80000000|rank.
+ * gee_build_projection_hot additionally scatters labels into hot_labels
+ * (u8 if k <= 255 else u16, gee_hot_label_bytes) at their ranks, and
+ * gee_embed_csr_pull_hot reads hot targets from that table (its head staged
+ * in shared memory) and cold targets from the packed labels. */
+int gee_hot_plan(const int64_t *offsets, int64_t n, int64_t max_hot, int64_t min_degree,
+                 int32_t *hot_rank, int32_t *hot_vertex, int64_t *n_hot, void *stream);
+int gee_hot_encode(int32_t *targets, int64_t arcs, const int32_t *hot_rank, void *stream);
+int gee_hot_label_bytes(int32_t k);
+int gee_build_projection_hot(const int32_t *labels, int64_t n, int32_t k, int64_t *counts,
+                             float *inv_f32, double *inv_f64, uint32_t *packed, int64_t *bad,
+                             const int32_t *hot_rank, void *hot_labels, void *stream);
+int gee_embed_csr_pull_hot(const int64_t *offsets, const int32_t *targets, const float *w,
+                           int64_t n, int64_t arcs, const int64_t *tile_row, int32_t scale_exp,
+                           const uint32_t *labels, int32_t label_bits, const void *hot_labels,
+                           int64_t n_hot, const double *inv, int32_t k, float *z, void *slots,
+                           void *stream);
 
 /* Choose the fixed-point exponent for a weighted pull: the largest e with
  * max_row_abs * 2^e < 2^62.  Returns the relative quantisation bound

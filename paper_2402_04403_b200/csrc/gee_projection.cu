@@ -20,7 +20,8 @@ constexpr int HIST_SMEM_WORDS = 12288;  // 48 KB of bins
 __global__ void __launch_bounds__(HIST_THREADS)
 k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, gee::LabelFmt f,
              unsigned long long *__restrict__ counts, uint32_t *__restrict__ packed,
-             unsigned long long *__restrict__ bad, int copies)
+             unsigned long long *__restrict__ bad, int copies, const int32_t *__restrict__ hot_rank,
+             void *__restrict__ hot_labels, int hot_bytes)
 {
     extern __shared__ uint32_t hist[];  // copies * (k+1) bins
     const int bins = k + 1;
@@ -48,6 +49,13 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, gee::Labe
                 atomicAdd(&counts[c], 1ull);
             }
             word |= ((uint32_t)c & f.mask) << (j * f.bits);
+            if (hot_rank) {  // hot tier: dense rank-ordered copy (gee_hot.cu)
+                const int32_t r = __ldcs(hot_rank + i);
+                if (r >= 0) {
+                    if (hot_bytes == 1) static_cast<uint8_t *>(hot_labels)[r] = (uint8_t)c;
+                    else static_cast<uint16_t *>(hot_labels)[r] = (uint16_t)c;
+                }
+            }
         }
         if (packed) __stcs(packed + wi, word);
     }
@@ -94,9 +102,9 @@ int64_t gee_label_words(int64_t n, int32_t label_bits)
 
 size_t gee_projection_work_bytes(int32_t) { return 0; }
 
-int gee_build_projection(const int32_t *labels, int64_t n, int32_t k, int64_t *counts,
-                         float *inv_f32, double *inv_f64, uint32_t *packed, int64_t *bad,
-                         void *, void *stream)
+int gee_build_projection_hot(const int32_t *labels, int64_t n, int32_t k, int64_t *counts, float *inv_f32,
+                             double *inv_f64, uint32_t *packed, int64_t *bad, const int32_t *hot_rank,
+                             void *hot_labels, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1, GEE_ERR_INVALID, "class count k must be positive (got %d)", k);
@@ -104,6 +112,8 @@ int gee_build_projection(const int32_t *labels, int64_t n, int32_t k, int64_t *c
     GEE_REQUIRE(n <= INT32_MAX, GEE_ERR_INVALID, "node count %lld exceeds int32", (long long)n);
     GEE_REQUIRE(counts != nullptr, GEE_ERR_INVALID, "counts must not be NULL");
     GEE_REQUIRE(n == 0 || labels != nullptr, GEE_ERR_INVALID, "labels must not be NULL");
+    GEE_REQUIRE(!hot_rank || (hot_labels && k <= 65535), GEE_ERR_INVALID,
+                "hot tier needs hot_labels and k <= 65535");
     cudaStream_t st = gee::as_stream(stream);
     GEE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t)(k + 1), st));
     if (bad) GEE_CUDA(cudaMemsetAsync(bad, 0, sizeof(int64_t), st));
@@ -119,7 +129,8 @@ int gee_build_projection(const int32_t *labels, int64_t n, int32_t k, int64_t *c
         int64_t cap = (int64_t)gee::sm_count() * 4;
         int grid = (int)(want < 1 ? 1 : (want > cap ? cap : want));
         k_label_hist<<<grid, HIST_THREADS, sh, st>>>(labels, n, k, f, cnt, packed,
-                                                     reinterpret_cast<unsigned long long *>(bad), copies);
+                                                     reinterpret_cast<unsigned long long *>(bad), copies, hot_rank,
+                                                     hot_labels, k <= 255 ? 1 : 2);
         int rc = gee::check_launch("k_label_hist");
         if (rc) return rc;
     }
@@ -128,6 +139,12 @@ int gee_build_projection(const int32_t *labels, int64_t n, int32_t k, int64_t *c
         return gee::check_launch("k_inv");
     }
     return GEE_OK;
+}
+
+int gee_build_projection(const int32_t *labels, int64_t n, int32_t k, int64_t *counts, float *inv_f32,
+                         double *inv_f64, uint32_t *packed, int64_t *bad, void *, void *stream)
+{
+    return gee_build_projection_hot(labels, n, k, counts, inv_f32, inv_f64, packed, bad, nullptr, nullptr, stream);
 }
 
 }  // extern "C"

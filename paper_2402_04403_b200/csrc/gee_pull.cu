@@ -20,27 +20,30 @@
 //                   sm_100a, 64-bit shared atomics are CAS loops).
 //
 // Work decomposition (balanced by arcs, hub rows split for free):
-//   tile j = arcs [j*T, (j+1)*T), T = GEE_TILE_ARCS = 256 threads x 8 arcs;
+//   tile j = arcs [j*T, (j+1)*T), T = GEE_TILE_ARCS = 1024 threads x 4 arcs;
 //   tile j OWNS the rows whose first-arc position offsets[r] lies in it;
 //   tile_row[j] = first owned row (gee_pull_plan, a lower_bound per tile).
-//   Persistent CTAs (4 per SM) walk tiles j = blockIdx.x, += gridDim.x.
-//   Per tile: arcs stream in (128-bit, L2 evict-first), labels are gathered
-//   (packed words, L2 evict-last), the tile's row offsets are staged in
-//   shared memory and each thread finds its arcs' rows by one binary search
-//   plus a forward walk.  Rows that run past their owner tile (hubs) are
+//   One persistent 1024-thread CTA per SM walks tiles j = blockIdx.x,
+//   += gridDim.x through a two-stage software pipeline: while tile j is
+//   accumulated, tile j+G's labels are being gathered and its row offsets
+//   staged (cp.async), and tile j+2G's arcs stream in (128-bit, L2
+//   evict-first).  Labels come from the hot tier (gee_hot.cu: shared-memory
+//   head, then an L2-resident rank-ordered table) or the packed array (L2
+//   evict-last).  Each thread finds its arcs' rows in the staged offsets by
+//   one binary search plus a forward walk.  Rows that run past their owner tile (hubs) are
 //   summed exactly through 64-bit global atomics into the owner tile's slot
 //   and written by k_pull_finalize.
 #include "gee_common.cuh"
 
 namespace {
 
-constexpr int PT = 256;                  // threads per CTA
-constexpr int APT = 8;                   // arcs per thread
-constexpr int TILE = PT * APT;           // 2048
+constexpr int PT = 1024;                 // threads per CTA (one persistent CTA per SM)
+constexpr int APT = 4;                   // arcs per thread
+constexpr int TILE = PT * APT;           // 4096
 static_assert(TILE == GEE_TILE_ARCS, "tile size mismatch with header");
-constexpr int CTAS_PER_SM = 4;
-constexpr int SMEM_BYTES = 54 * 1024;    // 4 CTAs per SM (228 KB)
-constexpr int OFF_MAX = 513;             // staged offsets per window (<= 512 rows)
+constexpr int SMEM_BYTES = 227 * 1024;   // opt-in maximum per CTA on sm_100a
+constexpr int OFF_MAX = 513;             // staged offsets per buffer (<= 512 rows)
+constexpr int WIN_BYTES_MAX = 120 * 1024;
 
 __device__ __forceinline__ int64_t lower_bound_i64(const int64_t *__restrict__ a, int64_t lo,
                                                    int64_t hi, int64_t key)
@@ -66,108 +69,220 @@ __global__ void k_pull_plan(const int64_t *__restrict__ offsets, int64_t n, int6
     tile_row[j] = lower_bound_i64(offsets, 0, n + 1, key);
 }
 
-__device__ __forceinline__ int4 ld_stream4(const int32_t *p) { return __ldcs(reinterpret_cast<const int4 *>(p)); }
-__device__ __forceinline__ float4 ld_stream4(const float *p) { return __ldcs(reinterpret_cast<const float4 *>(p)); }
+template <typename HT>
+__device__ __forceinline__ uint32_t ld_hot(const HT *p, uint64_t pol);
+template <>
+__device__ __forceinline__ uint32_t ld_hot<uint8_t>(const uint8_t *p, uint64_t pol)
+{
+    uint16_t v;
+    asm("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <>
+__device__ __forceinline__ uint32_t ld_hot<uint16_t>(const uint16_t *p, uint64_t pol)
+{
+    uint16_t v;
+    asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem)
+{
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+struct TileArcs {  // stage A: streamed arcs of a tile
+    int32_t t[APT];
+    float w[APT];
+    int32_t r0, r1;  // tile_row[j], tile_row[j+1]
+};
+struct TileLabs {  // stage B: gathered labels of a tile
+    uint32_t l[APT];
+    float w[APT];
+    int32_t r0, r1;
+};
 
 template <bool WEIGHTED>
-__global__ void __launch_bounds__(PT, CTAS_PER_SM)
+__device__ __forceinline__ void load_arcs(TileArcs &A, int64_t j, int tid, const int32_t *__restrict__ targets,
+                                          const float *__restrict__ w, int64_t arcs,
+                                          const int64_t *__restrict__ tile_row)
+{
+    const int64_t a0 = j * (int64_t)TILE, a1 = min(a0 + (int64_t)TILE, arcs);
+    const int64_t e0 = a0 + (int64_t)tid * APT;
+    if (e0 + APT <= a1) {
+        const int4 t4 = __ldcs(reinterpret_cast<const int4 *>(targets + e0));
+        A.t[0] = t4.x; A.t[1] = t4.y; A.t[2] = t4.z; A.t[3] = t4.w;
+        if (WEIGHTED) {
+            const float4 w4 = __ldcs(reinterpret_cast<const float4 *>(w + e0));
+            A.w[0] = w4.x; A.w[1] = w4.y; A.w[2] = w4.z; A.w[3] = w4.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < APT; i++) {
+            const bool ok = e0 + i < a1;
+            A.t[i] = ok ? __ldcs(targets + e0 + i) : 0;
+            if (WEIGHTED) A.w[i] = ok ? __ldcs(w + e0 + i) : 0.f;
+        }
+    }
+    A.r0 = (int32_t)tile_row[j];
+    A.r1 = (int32_t)tile_row[j + 1];
+}
+
+template <bool WEIGHTED, typename HT>
+__device__ __forceinline__ void gather_labs(TileLabs &B, const TileArcs &A, int64_t j, int tid, int64_t arcs,
+                                            const uint32_t *__restrict__ labels, const gee::LabelFmt &lf,
+                                            const HT *__restrict__ hot, const HT *__restrict__ hot_s, uint32_t hot0,
+                                            uint32_t k, uint64_t pol)
+{
+    const int64_t e0 = j * (int64_t)TILE + (int64_t)tid * APT;
+#pragma unroll
+    for (int i = 0; i < APT; i++) {
+        const int32_t t = A.t[i];
+        uint32_t lab;
+        if (e0 + i >= arcs) {
+            lab = 0u;
+        } else if (t < 0) {  // hot vertex: rank-ordered table (smem head, then L2)
+            const uint32_t h = (uint32_t)t & 0x7fffffffu;
+            lab = h < hot0 ? (uint32_t)hot_s[h] : ld_hot(hot + h, pol);
+        } else {
+            lab = gee::gather_label(labels, (uint32_t)t, lf, pol);
+        }
+        B.l[i] = lab > k ? 0u : lab;  // raw int32 labels: drop out-of-range
+        if (WEIGHTED) B.w[i] = A.w[i];
+    }
+    B.r0 = A.r0;
+    B.r1 = A.r1;
+}
+
+// Stage offsets[start .. start+cnt) into smem with cp.async (one 8 B copy per thread).
+__device__ __forceinline__ void stage_offsets(int64_t *buf, const int64_t *__restrict__ offsets, int32_t r0,
+                                              int32_t r1, int tid)
+{
+    const int32_t start = r0 > 0 ? r0 - 1 : 0;
+    const int32_t cnt = min(r1 - start + 1, OFF_MAX);
+    if (tid < cnt) cp_async8(buf + tid, offsets + start + tid);
+}
+
+template <bool WEIGHTED, typename HT>
+__global__ void __launch_bounds__(PT, 1)
 k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
        const float *__restrict__ w, int64_t arcs, const int64_t *__restrict__ tile_row, int64_t n_tiles,
        float qscale, double dscale, const uint32_t *__restrict__ labels, gee::LabelFmt lf,
-       const double *__restrict__ inv, int32_t k, float *__restrict__ z,
-       unsigned long long *__restrict__ slots, int win_rows)
+       const HT *__restrict__ hot, int32_t hot0, const double *__restrict__ inv, int32_t k,
+       float *__restrict__ z, unsigned long long *__restrict__ slots, int win_rows)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    int64_t *off_s = reinterpret_cast<int64_t *>(smem_raw);          // OFF_MAX
-    float *sc = reinterpret_cast<float *>(off_s + OFF_MAX + 1);      // k+1 output scales
+    int64_t *off_buf = reinterpret_cast<int64_t *>(smem_raw);         // 2 x OFF_MAX
+    float *sc = reinterpret_cast<float *>(off_buf + 2 * OFF_MAX + 2);  // k+1 output scales
     uint32_t *acc_lo = reinterpret_cast<uint32_t *>(sc + ((k + 4) & ~3));
-    uint32_t *acc_hi = acc_lo + (size_t)win_rows * k;                // weighted only
+    uint32_t *acc_hi = acc_lo + (size_t)win_rows * k;                 // weighted only
+    HT *hot_s = reinterpret_cast<HT *>(acc_lo + (size_t)win_rows * k * (WEIGHTED ? 2 : 1));
 
     const int tid = threadIdx.x;
     const int kk = k;
     const uint64_t pol = gee::policy_evict_last();
     // Z[x, c] = sum * sc[c+1]: inv folded with the fixed-point scale, fp32.
     for (int c = tid; c <= kk; c += PT) sc[c] = (float)(inv[c] * dscale);
+    {  // stage the head of the hot tier (hot0 * sizeof(HT) is a multiple of 16 B)
+        const int vec = (int)((size_t)hot0 * sizeof(HT) / 16);
+        const uint4 *src = reinterpret_cast<const uint4 *>(hot);
+        uint4 *dst = reinterpret_cast<uint4 *>(hot_s);
+        for (int i = tid; i < vec; i += PT) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
 
-    for (int64_t j = blockIdx.x; j < n_tiles; j += gridDim.x) {
-        const int64_t a0 = j * (int64_t)TILE;
-        const int64_t a1 = min(a0 + (int64_t)TILE, arcs);
-        const int64_t e0 = a0 + (int64_t)tid * APT;
-        // --- issue this thread's arc loads first (independent of the plan)
-        int32_t tgt[APT];
-        float wt[APT];
-        if (e0 + APT <= a1) {
-            const int4 t0 = ld_stream4(targets + e0), t1 = ld_stream4(targets + e0 + 4);
-            tgt[0] = t0.x; tgt[1] = t0.y; tgt[2] = t0.z; tgt[3] = t0.w;
-            tgt[4] = t1.x; tgt[5] = t1.y; tgt[6] = t1.z; tgt[7] = t1.w;
-            if (WEIGHTED) {
-                const float4 w0 = ld_stream4(w + e0), w1 = ld_stream4(w + e0 + 4);
-                wt[0] = w0.x; wt[1] = w0.y; wt[2] = w0.z; wt[3] = w0.w;
-                wt[4] = w1.x; wt[5] = w1.y; wt[6] = w1.z; wt[7] = w1.w;
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < APT; i++) {
-                const bool ok = e0 + i < a1;
-                tgt[i] = ok ? __ldcs(targets + e0 + i) : -1;
-                if (WEIGHTED) wt[i] = ok ? __ldcs(w + e0 + i) : 0.f;
-            }
-        }
-        const int64_t R0 = tile_row[j], R1 = tile_row[j + 1];
-        const int64_t offR0 = offsets[R0], offR1 = offsets[R1];
-        // --- label gathers (latency-bound; all APT in flight)
+    const int64_t G = gridDim.x;
+    int64_t jA = blockIdx.x;
+    if (jA >= n_tiles) return;
+    TileArcs A;
+    TileLabs B;
+    // prologue: tile j0 gathered + staged, tile j0+G arcs in flight
+    load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row);
+    gather_labs<WEIGHTED>(B, A, jA, tid, arcs, labels, lf, hot, hot_s, (uint32_t)hot0, (uint32_t)kk, pol);
+    stage_offsets(off_buf, offsets, B.r0, B.r1, tid);
+    cp_async_commit();
+    jA += G;
+    if (jA < n_tiles) load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row);
+    int buf = 0;
+
+    for (int64_t j = blockIdx.x; j < n_tiles; j += G) {
+        // current tile j: labels/weights from stage B
         uint32_t lab[APT];
+        float wcur[APT];
 #pragma unroll
         for (int i = 0; i < APT; i++) {
-            lab[i] = tgt[i] >= 0 ? gee::gather_label(labels, (uint32_t)tgt[i], lf, pol) : 0u;
-            if (lab[i] > (uint32_t)kk) lab[i] = 0u;  // raw int32 labels: drop out-of-range
+            lab[i] = B.l[i];
+            if (WEIGHTED) wcur[i] = B.w[i];
         }
-        int64_t q[APT];
-        if (WEIGHTED) {
-#pragma unroll
-            for (int i = 0; i < APT; i++) q[i] = __float2ll_rn(wt[i] * qscale);
+        const int32_t R0 = B.r0, R1 = B.r1;
+        // advance the pipeline: gather tile j+G, stage its offsets, load tile j+2G
+        const bool more = jA < n_tiles;
+        if (more) {
+            gather_labs<WEIGHTED>(B, A, jA, tid, arcs, labels, lf, hot, hot_s, (uint32_t)hot0, (uint32_t)kk, pol);
+            stage_offsets(off_buf + (buf ^ 1) * OFF_MAX, offsets, B.r0, B.r1, tid);
         }
-        // Head row: the row holding arc a0 started in an earlier tile.
-        const bool has_head = offR0 > a0;  // also true when R0 == n (offsets[n] = arcs > a0)
-        const int64_t base = has_head ? R0 - 1 : R0;
-        // Tail row: the last owned row continues into later tiles.
-        const bool tail_cut = (R1 > R0) && (offR1 > a1);
-        const int64_t rows_total = R1 - base;
+        cp_async_commit();
+        jA += G;
+        if (jA < n_tiles) load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row);
+        cp_async_wait<1>();  // tile j's staged offsets have landed (tile j+G's may be in flight)
 
-        for (int64_t wo = 0; wo < rows_total; wo += win_rows) {
-            const int nr = (int)min((int64_t)win_rows, rows_total - wo);
-            const int64_t wrow0 = base + wo;
-            // stage offsets[wrow0 .. wrow0+nr] and zero the window
-            for (int i = tid; i <= nr; i += PT) off_s[i] = __ldcs(offsets + wrow0 + i);
+        // ---- process tile j
+        const int64_t a0 = j * (int64_t)TILE, a1 = min(a0 + (int64_t)TILE, arcs);
+        const int64_t e0 = a0 + (int64_t)tid * APT;
+        int64_t *off_s = off_buf + buf * OFF_MAX;
+        int32_t st0 = R0 > 0 ? R0 - 1 : 0;           // first staged row
+        int32_t scnt = min(R1 - st0 + 1, OFF_MAX);   // staged count
+        __syncthreads();                             // staged offsets visible to all threads
+        const int64_t offR0 = off_s[R0 - st0];
+        const bool has_head = offR0 > a0;            // also when R0 == n (offsets[n] = arcs > a0)
+        const int64_t offR1 = (R1 - st0 < scnt) ? off_s[R1 - st0] : __ldcs(offsets + R1);
+        const bool tail_cut = (R1 > R0) && (offR1 > a1);
+        const int32_t base = has_head ? R0 - 1 : R0;
+        const int32_t rows_total = R1 - base;
+
+        for (int32_t wo = 0; wo < rows_total; wo += win_rows) {
+            const int nr = min(win_rows, rows_total - wo);
+            const int32_t wrow0 = base + wo;
             const int words = nr * kk;
+            if (wrow0 - st0 + nr >= scnt) {
+                // window not (fully) staged: restage synchronously (large tiles only)
+                __syncthreads();
+                for (int i = tid; i <= nr; i += PT) off_s[i] = __ldcs(offsets + wrow0 + i);
+                st0 = wrow0;
+                scnt = nr + 1;
+            }
             for (int i = tid; i < words; i += PT) {
                 acc_lo[i] = 0u;
                 if (WEIGHTED) acc_hi[i] = 0u;
             }
             __syncthreads();
-            // my arcs inside this window's arc range
-            const int64_t wa0 = max(off_s[0], a0), wa1 = min(off_s[nr], a1);
+            const int64_t *ow = off_s + (wrow0 - st0);  // ow[r] = offsets[wrow0 + r]
+            const int64_t wa0 = max(ow[0], a0), wa1 = min(ow[nr], a1);
             const int64_t m0 = max(e0, wa0), m1 = min(e0 + APT, wa1);
             if (m0 < m1) {
-                // row of m0: last r in [0, nr) with off_s[r] <= m0
-                int lo = 0, hi = nr;  // off_s[lo] <= m0 < off_s[hi]
+                int lo = 0, hi = nr;  // ow[lo] <= m0 < ow[hi]
                 while (hi - lo > 1) {
                     const int mid = (lo + hi) >> 1;
-                    if (off_s[mid] <= m0) lo = mid;
+                    if (ow[mid] <= m0) lo = mid;
                     else hi = mid;
                 }
                 int r = lo;
-                int64_t next = off_s[r + 1];
+                int64_t next = ow[r + 1];
 #pragma unroll
                 for (int i = 0; i < APT; i++) {
                     const int64_t e = e0 + i;
                     if (e < m0 || e >= m1) continue;
-                    while (e >= next) next = off_s[++r + 1];
+                    while (e >= next) next = ow[++r + 1];
                     if (lab[i] == 0u) continue;
                     const int idx = r * kk + (int)lab[i] - 1;
                     if (WEIGHTED) {
-                        const uint32_t lo32 = (uint32_t)(unsigned long long)q[i];
-                        uint32_t hi32 = (uint32_t)((unsigned long long)q[i] >> 32);
+                        const unsigned long long q = (unsigned long long)__float2ll_rn(wcur[i] * qscale);
+                        const uint32_t lo32 = (uint32_t)q;
+                        uint32_t hi32 = (uint32_t)(q >> 32);
                         const uint32_t old = atomicAdd(&acc_lo[idx], lo32);
                         hi32 += (old + lo32 < old) ? 1u : 0u;  // carry out of the low plane
                         if (hi32) atomicAdd(&acc_hi[idx], hi32);
@@ -179,12 +294,12 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
             __syncthreads();
 
             // complete rows of this window -> Z (flat, coalesced, streaming stores)
-            const int64_t fin_lo = max(wrow0, R0);  // a head row is partial
-            const int64_t fin_hi = min(wrow0 + nr, tail_cut ? R1 - 1 : R1);
+            const int32_t fin_lo = max(wrow0, R0);  // a head row is partial
+            const int32_t fin_hi = min(wrow0 + nr, tail_cut ? R1 - 1 : R1);
             if (fin_hi > fin_lo) {
-                const int off = (int)(fin_lo - wrow0) * kk;
-                const int total = (int)(fin_hi - fin_lo) * kk;
-                float *zo = z + fin_lo * (int64_t)kk;
+                const int off = (fin_lo - wrow0) * kk;
+                const int total = (fin_hi - fin_lo) * kk;
+                float *zo = z + (int64_t)fin_lo * kk;
                 int c = tid % kk, rr = tid / kk;
                 const int dc = PT % kk, dr = PT / kk;
                 for (int e = tid; e < total; e += PT) {
@@ -207,7 +322,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
             }
             // partial rows: the head (owned by an earlier tile) and a cut tail
             for (int part = 0; part < 2; part++) {
-                int64_t row;
+                int32_t row;
                 if (part == 0) {
                     if (!(has_head && wo == 0)) continue;
                     row = base;
@@ -216,8 +331,8 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     row = R1 - 1;
                     if (row < wrow0 || row >= wrow0 + nr) continue;
                 }
-                const int64_t owner = part == 0 ? off_s[0] / TILE : j;
-                const int lr = (int)(row - wrow0);
+                const int64_t owner = part == 0 ? ow[0] / TILE : j;
+                const int lr = row - wrow0;
                 for (int c = tid; c < kk; c += PT) {
                     const int idx = lr * kk + c;
                     const unsigned long long v =
@@ -227,7 +342,9 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
             }
             __syncthreads();
         }
+        buf ^= 1;
     }
+    cp_async_wait<0>();
 }
 
 // Write the rows that spanned tiles from their owner's slot; re-zero slots.
@@ -266,38 +383,51 @@ __global__ void k_zero_tail(const int64_t *__restrict__ first_row, int64_t n, in
 
 size_t pull_fixed_smem(int32_t k)
 {
-    return (OFF_MAX + 1) * sizeof(int64_t) + (size_t)((k + 4) & ~3) * sizeof(float);
+    return (2 * OFF_MAX + 2) * sizeof(int64_t) + (size_t)((k + 4) & ~3) * sizeof(float);
 }
 
-int pull_win_rows(int32_t k, bool weighted)
+struct PullShape {
+    int win_rows;
+    int hot0;
+    size_t smem;
+};
+
+PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int hot_bytes)
 {
+    PullShape p{0, 0, 0};
     const size_t fixed = pull_fixed_smem(k);
-    if (fixed >= SMEM_BYTES) return 0;
     const size_t per_row = (size_t)k * sizeof(uint32_t) * (weighted ? 2 : 1);
-    int rows = (int)((SMEM_BYTES - fixed) / per_row);
-    return rows > OFF_MAX - 1 ? OFF_MAX - 1 : rows;
+    if (fixed + per_row > SMEM_BYTES) return p;
+    size_t win_bytes = per_row * (OFF_MAX - 1);
+    if (win_bytes > WIN_BYTES_MAX) win_bytes = WIN_BYTES_MAX > per_row ? WIN_BYTES_MAX : per_row;
+    if (fixed + win_bytes > SMEM_BYTES) win_bytes = SMEM_BYTES - fixed;
+    p.win_rows = (int)(win_bytes / per_row);
+    if (p.win_rows > OFF_MAX - 1) p.win_rows = OFF_MAX - 1;
+    const size_t used = fixed + (size_t)p.win_rows * per_row;
+    size_t hot_cap = (SMEM_BYTES - used) / (size_t)hot_bytes;
+    hot_cap &= ~(size_t)15;  // whole 16 B vectors (k_pull stages it with uint4 copies)
+    p.hot0 = (int)(n_hot < (int64_t)hot_cap ? n_hot : (int64_t)hot_cap);
+    p.smem = used + (((size_t)p.hot0 * hot_bytes + 15) & ~(size_t)15);
+    return p;
 }
 
-template <bool WEIGHTED>
+template <bool WEIGHTED, typename HT>
 int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t arcs,
                 const int64_t *tile_row, int32_t scale_exp, const uint32_t *labels, gee::LabelFmt lf,
-                const double *inv, int32_t k, float *z, unsigned long long *slots, cudaStream_t st)
+                const HT *hot, int64_t n_hot, const double *inv, int32_t k, float *z, unsigned long long *slots,
+                cudaStream_t st)
 {
     const int64_t n_tiles = gee_pull_tiles(arcs);
-    const int win = pull_win_rows(k, WEIGHTED);
-    GEE_REQUIRE(win >= 1, GEE_ERR_INVALID, "k=%d too large for the pull window", k);
-    const size_t sh = pull_fixed_smem(k) + (size_t)win * k * sizeof(uint32_t) * (WEIGHTED ? 2 : 1);
-    auto kern = k_pull<WEIGHTED>;
-    GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    int per_sm = 0;
-    GEE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PT, sh));
-    if (per_sm < 1) per_sm = 1;
-    const int64_t cap = (int64_t)gee::sm_count() * per_sm;
+    const PullShape ps = pull_shape(k, WEIGHTED, hot ? n_hot : 0, (int)sizeof(HT));
+    GEE_REQUIRE(ps.win_rows >= 1, GEE_ERR_INVALID, "k=%d too large for the pull window", k);
+    auto kern = k_pull<WEIGHTED, HT>;
+    GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps.smem));
+    const int64_t cap = (int64_t)gee::sm_count();
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = WEIGHTED ? ldexp(1.0, -scale_exp) : 1.0;
-    kern<<<grid, PT, sh, st>>>(offsets, targets, w, arcs, tile_row, n_tiles, qscale, dscale, labels, lf, inv, k, z,
-                               slots, win);
+    kern<<<grid, PT, ps.smem, st>>>(offsets, targets, w, arcs, tile_row, n_tiles, qscale, dscale, labels, lf, hot,
+                                    ps.hot0, inv, k, z, slots, ps.win_rows);
     int rc = gee::check_launch("k_pull");
     if (rc) return rc;
     const int64_t want = (n_tiles * 32 + 255) / 256;
@@ -347,10 +477,10 @@ int gee_pull_scale_exp(double max_row_abs, double min_abs_nz, int32_t *scale_exp
     return GEE_OK;
 }
 
-int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n,
-                       int64_t arcs, const int64_t *tile_row, int32_t scale_exp, const uint32_t *labels,
-                       int32_t label_bits, const double *inv, int32_t k, float *z, void *slots,
-                       void *stream)
+int gee_embed_csr_pull_hot(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n,
+                           int64_t arcs, const int64_t *tile_row, int32_t scale_exp, const uint32_t *labels,
+                           int32_t label_bits, const void *hot_labels, int64_t n_hot, const double *inv,
+                           int32_t k, float *z, void *slots, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1, GEE_ERR_INVALID, "class count k must be positive (got %d)", k);
@@ -358,6 +488,8 @@ int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const flo
     GEE_REQUIRE(n <= INT32_MAX, GEE_ERR_INVALID, "node count %lld exceeds int32 targets", (long long)n);
     GEE_REQUIRE(label_bits == 32 || label_bits == gee_label_bits(k), GEE_ERR_INVALID,
                 "label_bits must be 32 (raw int32) or gee_label_bits(k)=%d (got %d)", gee_label_bits(k), label_bits);
+    GEE_REQUIRE(n_hot == 0 || (hot_labels && k <= 65535 && n_hot <= n), GEE_ERR_INVALID,
+                "hot tier needs hot_labels, k <= 65535 and n_hot <= n");
     cudaStream_t st = gee::as_stream(stream);
     if (n == 0) return GEE_OK;
     GEE_REQUIRE(offsets && tile_row && z, GEE_ERR_INVALID, "NULL array argument");
@@ -378,8 +510,27 @@ int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const flo
     }
     const gee::LabelFmt lf = gee::label_fmt(label_bits);
     auto *sl = reinterpret_cast<unsigned long long *>(slots);
-    return w ? launch_pull<true>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, inv, k, z, sl, st)
-             : launch_pull<false>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, inv, k, z, sl, st);
+    if (k <= 255) {
+        const auto *h = static_cast<const uint8_t *>(hot_labels);
+        return w ? launch_pull<true, uint8_t>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, h, n_hot,
+                                              inv, k, z, sl, st)
+                 : launch_pull<false, uint8_t>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, h, n_hot,
+                                               inv, k, z, sl, st);
+    }
+    const auto *h = static_cast<const uint16_t *>(hot_labels);
+    return w ? launch_pull<true, uint16_t>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, h, n_hot, inv,
+                                           k, z, sl, st)
+             : launch_pull<false, uint16_t>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, h, n_hot, inv,
+                                            k, z, sl, st);
+}
+
+int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n,
+                       int64_t arcs, const int64_t *tile_row, int32_t scale_exp, const uint32_t *labels,
+                       int32_t label_bits, const double *inv, int32_t k, float *z, void *slots,
+                       void *stream)
+{
+    return gee_embed_csr_pull_hot(offsets, targets, w, n, arcs, tile_row, scale_exp, labels, label_bits, nullptr, 0,
+                                  inv, k, z, slots, stream);
 }
 
 }  // extern "C"

@@ -59,6 +59,10 @@ class DeviceGraph:
         self.max_row_abs = 0.0
         self.src = self.dst = self.w = None
         self.coo_source_only = False
+        self.hot_rank = None  # int32[n_nodes]: degree rank of hot vertices, -1 cold
+        self.n_hot = 0
+        self.hot_k = None  # k the hot tier was planned for (None = not planned)
+        self._owns_targets = False
 
     # ---------------------------------------------------------------- build
     @classmethod
@@ -93,6 +97,7 @@ class DeviceGraph:
         if symmetric:
             g = cls(n, arcs // 2, dev)
             g.offsets, g.targets, g.weights = off_d, tgt_d, w_d
+            g._owns_targets = not (isinstance(targets, torch.Tensor) and targets.data_ptr() == tgt_d.data_ptr())
             g._plan()
             if keep_coo or not pull:
                 rows = torch.empty(arcs, dtype=torch.int32, device=dev)
@@ -117,6 +122,7 @@ class DeviceGraph:
         check(lib.gee_build_csr(ptr(src_d), ptr(dst_d), ptr(w_d), s, n, 1, 1 if stable else 0,
                                 ptr(self.offsets), ptr(self.targets), ptr(self.weights), _stream()),
               "gee_build_csr")
+        self._owns_targets = True
         self._plan()
 
     def _plan(self):
@@ -135,6 +141,40 @@ class DeviceGraph:
         e, rel = ctypes.c_int32(), ctypes.c_double()
         check(lib.gee_pull_scale_exp(mx.value, mn.value, ctypes.byref(e), ctypes.byref(rel)), "gee_pull_scale_exp")
         self.scale_exp, self.rel_err = e.value, rel.value
+
+    # Hot-label tier (csrc/gee_hot.cu): worth it when the packed label array
+    # outgrows what L2 keeps resident under random access and degrees are
+    # skewed (R-MAT); ER graphs end up with few or no hot vertices.
+    HOT_MIN_PACKED_BYTES = 16 << 20
+    HOT_MAX = 16 << 20
+
+    def prepare_hot(self, k, enable=None):
+        """Plan the hot tier for k classes (once; rewrites the pull targets)."""
+        if self.hot_k == k or not self.has_pull:
+            return
+        if self.hot_k is not None:
+            raise ValidationError("hot tier already planned for a different k")
+        bits = int(lib.gee_label_bits(k))
+        packed_bytes = int(lib.gee_label_words(self.n_nodes, bits)) * 4
+        if enable is None:
+            enable = packed_bytes > self.HOT_MIN_PACKED_BYTES and k <= 65535 and self.n == self.n_nodes
+        self.hot_k = k
+        if not enable or self.arcs == 0:
+            return
+        if not self._owns_targets:
+            self.targets = self.targets.clone()
+            self._owns_targets = True
+        n = self.n_nodes
+        self.hot_rank = torch.empty(n, dtype=torch.int32, device=self.device)
+        nh = ctypes.c_int64()
+        max_hot = min(n, self.HOT_MAX // int(lib.gee_hot_label_bytes(k)))
+        check(lib.gee_hot_plan(ptr(self.offsets), n, max_hot, 2, ptr(self.hot_rank), None, ctypes.byref(nh),
+                               _stream()), "gee_hot_plan")
+        self.n_hot = int(nh.value)
+        if self.n_hot == 0:
+            self.hot_rank = None
+            return
+        check(lib.gee_hot_encode(ptr(self.targets), self.arcs, ptr(self.hot_rank), _stream()), "gee_hot_encode")
 
     @property
     def arcs(self):
@@ -184,15 +224,27 @@ class Embedder:
         words = int(lib.gee_label_words(self.n, self.label_bits))
         self.packed = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
         self.slots = None
+        self.hot_labels = None
+        self._hot_for = None
 
     # ------------------------------------------------------------------ K1
-    def project(self, labels_d, validate=True):
-        """Histogram + inv + compact labels (build_projection)."""
+    def project(self, labels_d, validate=True, g=None):
+        """Histogram + inv + packed labels (build_projection); with a graph
+        that has a hot tier, also its rank-ordered hot label table."""
         if labels_d.numel() != self.n:
             raise ValidationError(f"graph has {self.n} nodes but labels have {labels_d.numel()}")
-        check(lib.gee_build_projection(ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.inv32),
-                                       ptr(self.inv64), ptr(self.packed), ptr(self.bad), None, _stream()),
+        hot_rank = None
+        if g is not None and g.hot_rank is not None:
+            hb = int(lib.gee_hot_label_bytes(self.k))
+            need = (g.n_hot * hb + 15) // 16 * 16
+            if self.hot_labels is None or self.hot_labels.numel() < need:
+                self.hot_labels = torch.zeros(need, dtype=torch.uint8, device=self.device)
+            hot_rank = g.hot_rank
+        check(lib.gee_build_projection_hot(ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.inv32),
+                                           ptr(self.inv64), ptr(self.packed), ptr(self.bad), ptr(hot_rank),
+                                           ptr(self.hot_labels) if hot_rank is not None else None, _stream()),
               "gee_build_projection")
+        self._hot_for = g if hot_rank is not None else None
         if validate and int(self.bad.item()):
             raise ValidationError(f"{int(self.bad.item())} labels outside [0, {self.k}]")
         return self.counts
@@ -215,12 +267,17 @@ class Embedder:
             raise ValidationError(
                 f"weights span too wide a range for the exact fixed-point pull "
                 f"(rounding bound {g.rel_err:.2e}); use variant='push'")
+        if g.hot_k != self.k:
+            raise ValidationError("call Embedder.project(labels, g=graph) (or graph.prepare_hot(k)) first")
+        if g.hot_rank is not None and (self.hot_labels is None or self._hot_for is not g):
+            raise ValidationError("hot label table not built for this graph: call project(labels, g=graph)")
         if z is None:
             z = torch.empty((g.n, self.k), dtype=torch.float32, device=self.device)
         self._ensure_slots(g.arcs)
-        check(lib.gee_embed_csr_pull(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
-                                     ptr(g.tile_row), g.scale_exp, ptr(self.packed), self.label_bits,
-                                     ptr(self.inv64), self.k, ptr(z), ptr(self.slots), _stream()),
+        check(lib.gee_embed_csr_pull_hot(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
+                                         ptr(g.tile_row), g.scale_exp, ptr(self.packed), self.label_bits,
+                                         ptr(self.hot_labels) if g.n_hot else None, g.n_hot, ptr(self.inv64),
+                                         self.k, ptr(z), ptr(self.slots), _stream()),
               "gee_embed_csr_pull")
         return z
 
@@ -241,8 +298,10 @@ class Embedder:
 
     def embed(self, g: DeviceGraph, labels_d, variant="auto", z=None, validate=True):
         """One edge pass: projection then the chosen edge map."""
-        self.project(labels_d, validate=validate)
         v = choose_variant(g, variant)
+        if v == "pull":
+            g.prepare_hot(self.k)
+        self.project(labels_d, validate=validate, g=g if v == "pull" else None)
         return self.pull(g, z) if v == "pull" else self.push(g, z)
 
 

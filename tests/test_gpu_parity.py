@@ -256,3 +256,40 @@ def test_mass_accounting():
         mass = np.where(lab[dst] > 0, row[dst] * w, 0.0).sum() + np.where(lab[src] > 0, row[src] * w, 0.0).sum()
         z = gb.embed_serial(gb.EdgeList(n=n, src=src, dst=dst, w=w, directed=bool(i % 2)), y)
         assert abs(z.astype(np.float64).sum() - mass) <= 1e-5 * max(1.0, abs(mass))
+
+
+@pytest.mark.parametrize("k,weighted", [(50, True), (300, False), (5, False)])
+def test_hot_tier_all_three_label_paths(k, weighted):
+    # forced hot tier on a skewed graph: shared-memory head, L2 table and
+    # cold packed labels are all exercised (n_hot exceeds the smem head)
+    scale, s = 19, 4_000_000
+    src, dst, w = synth.rmat_edges(scale, s, seed=11, weighted=weighted)
+    n = 1 << scale
+    y = synth.uniform_labels(n, k, seed=12)
+    dev = torch.device("cuda")
+    g = DeviceGraph.from_edges(src, dst, w, n, device=dev, pull=True)
+    g.prepare_hot(k, enable=True)
+    assert g.n_hot > 120_000 and g.n_hot < n
+    emb = Embedder(n, k, dev)
+    z = emb.embed(g, y, variant="pull").cpu().numpy()
+    exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), None if w is None else w.cpu().numpy(),
+                              y.cpu().numpy(), n, k)
+    assert rel_err(z, exp) <= TOL
+    z2 = emb.embed(g, y, variant="pull").cpu().numpy()
+    assert np.array_equal(z, z2)  # bit-stable
+
+
+def test_hot_plan_ranks_by_degree():
+    src = np.array([0, 0, 0, 1, 1, 2, 5, 5, 5, 5], dtype=np.int64)
+    dst = np.array([1, 2, 3, 2, 3, 3, 4, 4, 4, 4], dtype=np.int64)
+    dev = torch.device("cuda")
+    g = DeviceGraph.from_edges(src, dst, None, 6, device=dev, pull=True)
+    g.prepare_hot(3, enable=True)
+    deg = np.bincount(np.concatenate([src, dst]), minlength=6)
+    rank = g.hot_rank.cpu().numpy()
+    order = sorted(range(6), key=lambda v: (-deg[v], v))
+    hot = [v for v in order if deg[v] >= 2]
+    assert g.n_hot == len(hot)
+    for r, v in enumerate(hot):
+        assert rank[v] == r
+    assert all(rank[v] == -1 for v in range(6) if deg[v] < 2)
