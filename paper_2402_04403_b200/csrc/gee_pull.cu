@@ -69,23 +69,6 @@ __global__ void k_pull_plan(const int64_t *__restrict__ offsets, int64_t n, int6
     tile_row[j] = lower_bound_i64(offsets, 0, n + 1, key);
 }
 
-template <typename HT>
-__device__ __forceinline__ uint32_t ld_hot(const HT *p, uint64_t pol);
-template <>
-__device__ __forceinline__ uint32_t ld_hot<uint8_t>(const uint8_t *p, uint64_t pol)
-{
-    uint16_t v;
-    asm("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
-    return v;
-}
-template <>
-__device__ __forceinline__ uint32_t ld_hot<uint16_t>(const uint16_t *p, uint64_t pol)
-{
-    uint16_t v;
-    asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
-    return v;
-}
-
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem)
 {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -132,25 +115,34 @@ __device__ __forceinline__ void load_arcs(TileArcs &A, int64_t j, int tid, const
     A.r1 = (int32_t)tile_row[j + 1];
 }
 
+// Label of every arc of a tile.  Hot targets (t < 0) below hot0 read the
+// shared-memory head; other hot targets read the L2 hot table (as u32 words,
+// format hf: 8 or 16 bits); cold targets read the packed array (format lf).
+// Branch-free apart from the predicated global load.
 template <bool WEIGHTED, typename HT>
 __device__ __forceinline__ void gather_labs(TileLabs &B, const TileArcs &A, int64_t j, int tid, int64_t arcs,
                                             const uint32_t *__restrict__ labels, const gee::LabelFmt &lf,
-                                            const HT *__restrict__ hot, const HT *__restrict__ hot_s, uint32_t hot0,
-                                            uint32_t k, uint64_t pol)
+                                            const uint32_t *__restrict__ hot_words, const gee::LabelFmt &hf,
+                                            const HT *__restrict__ hot_s, uint32_t hot0, uint32_t k, uint64_t pol)
 {
     const int64_t e0 = j * (int64_t)TILE + (int64_t)tid * APT;
 #pragma unroll
     for (int i = 0; i < APT; i++) {
         const int32_t t = A.t[i];
-        uint32_t lab;
-        if (e0 + i >= arcs) {
-            lab = 0u;
-        } else if (t < 0) {  // hot vertex: rank-ordered table (smem head, then L2)
-            const uint32_t h = (uint32_t)t & 0x7fffffffu;
-            lab = h < hot0 ? (uint32_t)hot_s[h] : ld_hot(hot + h, pol);
-        } else {
-            lab = gee::gather_label(labels, (uint32_t)t, lf, pol);
-        }
+        const bool hot = t < 0;
+        const uint32_t idx = (uint32_t)t & 0x7fffffffu;
+        const bool in_smem = hot && idx < hot0;
+        const uint32_t ls = (uint32_t)hot_s[in_smem ? idx : 0u];
+        const uint32_t magic = hot ? hf.magic : lf.magic, shift = hot ? hf.shift : lf.shift;
+        const uint32_t per = hot ? hf.per : lf.per, bits = hot ? hf.bits : lf.bits;
+        const uint32_t mask = hot ? hf.mask : lf.mask;
+        const uint32_t wi = (uint32_t)(((uint64_t)idx * magic) >> shift);
+        const uint32_t sh = (idx - wi * per) * bits;
+        const uint32_t *p = (hot ? hot_words : labels) + wi;
+        uint32_t word = 0u;
+        if (!in_smem && e0 + i < arcs) word = gee::ld_label_word(p, pol);
+        uint32_t lab = in_smem ? ls : ((word >> sh) & mask);
+        if (e0 + i >= arcs) lab = 0u;
         B.l[i] = lab > k ? 0u : lab;  // raw int32 labels: drop out-of-range
         if (WEIGHTED) B.w[i] = A.w[i];
     }
@@ -172,19 +164,22 @@ __global__ void __launch_bounds__(PT, 1)
 k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
        const float *__restrict__ w, int64_t arcs, const int64_t *__restrict__ tile_row, int64_t n_tiles,
        float qscale, double dscale, const uint32_t *__restrict__ labels, gee::LabelFmt lf,
-       const HT *__restrict__ hot, int32_t hot0, const double *__restrict__ inv, int32_t k,
+       const HT *__restrict__ hot, gee::LabelFmt hf, int32_t hot0, const double *__restrict__ inv, int32_t k,
        float *__restrict__ z, unsigned long long *__restrict__ slots, int win_rows)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     int64_t *off_buf = reinterpret_cast<int64_t *>(smem_raw);         // 2 x OFF_MAX
     float *sc = reinterpret_cast<float *>(off_buf + 2 * OFF_MAX + 2);  // k+1 output scales
     uint32_t *acc_lo = reinterpret_cast<uint32_t *>(sc + ((k + 4) & ~3));
-    uint32_t *acc_hi = acc_lo + (size_t)win_rows * k;                 // weighted only
-    HT *hot_s = reinterpret_cast<HT *>(acc_lo + (size_t)win_rows * k * (WEIGHTED ? 2 : 1));
+    const size_t plane = ((size_t)win_rows * k + 3) & ~(size_t)3;     // 16 B aligned planes
+    uint32_t *acc_hi = acc_lo + plane;                                 // weighted only
+    HT *hot_s = reinterpret_cast<HT *>(acc_lo + plane * (WEIGHTED ? 2 : 1));
 
     const int tid = threadIdx.x;
+    const int lane = tid & 31;
     const int kk = k;
     const uint64_t pol = gee::policy_evict_last();
+    const uint32_t *hot_words = reinterpret_cast<const uint32_t *>(hot);
     // Z[x, c] = sum * sc[c+1]: inv folded with the fixed-point scale, fp32.
     for (int c = tid; c <= kk; c += PT) sc[c] = (float)(inv[c] * dscale);
     {  // stage the head of the hot tier (hot0 * sizeof(HT) is a multiple of 16 B)
@@ -202,7 +197,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
     TileLabs B;
     // prologue: tile j0 gathered + staged, tile j0+G arcs in flight
     load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row);
-    gather_labs<WEIGHTED>(B, A, jA, tid, arcs, labels, lf, hot, hot_s, (uint32_t)hot0, (uint32_t)kk, pol);
+    gather_labs<WEIGHTED>(B, A, jA, tid, arcs, labels, lf, hot_words, hf, hot_s, (uint32_t)hot0, (uint32_t)kk, pol);
     stage_offsets(off_buf, offsets, B.r0, B.r1, tid);
     cp_async_commit();
     jA += G;
@@ -222,7 +217,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         // advance the pipeline: gather tile j+G, stage its offsets, load tile j+2G
         const bool more = jA < n_tiles;
         if (more) {
-            gather_labs<WEIGHTED>(B, A, jA, tid, arcs, labels, lf, hot, hot_s, (uint32_t)hot0, (uint32_t)kk, pol);
+            gather_labs<WEIGHTED>(B, A, jA, tid, arcs, labels, lf, hot_words, hf, hot_s, (uint32_t)hot0, (uint32_t)kk, pol);
             stage_offsets(off_buf + (buf ^ 1) * OFF_MAX, offsets, B.r0, B.r1, tid);
         }
         cp_async_commit();
@@ -255,16 +250,41 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 st0 = wrow0;
                 scnt = nr + 1;
             }
-            for (int i = tid; i < words; i += PT) {
-                acc_lo[i] = 0u;
-                if (WEIGHTED) acc_hi[i] = 0u;
+            {  // zero the window: acc planes are 16 B aligned, words rounded up to 4
+                uint4 *a4 = reinterpret_cast<uint4 *>(acc_lo);
+                const int w4 = (words + 3) >> 2;
+                const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
+                for (int i = tid; i < w4; i += PT) a4[i] = zero4;
+                if (WEIGHTED) {
+                    uint4 *h4 = reinterpret_cast<uint4 *>(acc_hi);
+                    for (int i = tid; i < w4; i += PT) h4[i] = zero4;
+                }
             }
             __syncthreads();
             const int64_t *ow = off_s + (wrow0 - st0);  // ow[r] = offsets[wrow0 + r]
             const int64_t wa0 = max(ow[0], a0), wa1 = min(ow[nr], a1);
             const int64_t m0 = max(e0, wa0), m1 = min(e0 + APT, wa1);
+            // Row of this thread's first arc: the warp brackets its first arc
+            // with two 32-way ballots, then each lane gallops from there.
+            const int64_t ew = max(a0 + (int64_t)(tid & ~31) * APT, wa0);
+            int rw = 0;
+            if (ew < wa1) {
+                const int step = (nr + 31) >> 5;  // <= 16
+                int cand = min(lane * step, nr);
+                unsigned bal = __ballot_sync(0xffffffffu, ow[cand] <= ew);
+                int b = (31 - __clz(bal)) * step;  // ow[b] <= ew
+                cand = min(b + lane, nr);
+                bal = __ballot_sync(0xffffffffu, lane < step && ow[cand] <= ew);
+                rw = b + (31 - __clz(bal));
+            }
             if (m0 < m1) {
-                int lo = 0, hi = nr;  // ow[lo] <= m0 < ow[hi]
+                // gallop from rw: find last r with ow[r] <= m0
+                int lo = rw, g = 1;
+                while (lo + g < nr && ow[lo + g] <= m0) {
+                    lo += g;
+                    g <<= 1;
+                }
+                int hi = min(lo + g, nr);  // ow[lo] <= m0 < ow[hi] (ow[nr] >= m1 > m0)
                 while (hi - lo > 1) {
                     const int mid = (lo + hi) >> 1;
                     if (ow[mid] <= m0) lo = mid;
@@ -300,24 +320,17 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 const int off = (fin_lo - wrow0) * kk;
                 const int total = (fin_hi - fin_lo) * kk;
                 float *zo = z + (int64_t)fin_lo * kk;
-                int c = tid % kk, rr = tid / kk;
-                const int dc = PT % kk, dr = PT / kk;
+                const uint32_t *plo = acc_lo + off;
+                const uint32_t *phi = acc_hi + off;
+                int c = tid % kk;
+                const int dc = PT % kk;
                 for (int e = tid; e < total; e += PT) {
-                    const int idx = off + rr * kk + c;
                     float v;
-                    if (WEIGHTED) {
-                        const long long s64 = (long long)(((unsigned long long)acc_hi[idx] << 32) | acc_lo[idx]);
-                        v = (float)s64;
-                    } else {
-                        v = (float)acc_lo[idx];
-                    }
+                    if (WEIGHTED) v = (float)(long long)(((unsigned long long)phi[e] << 32) | plo[e]);
+                    else v = (float)plo[e];
                     __stcs(zo + e, v * sc[c + 1]);
                     c += dc;
-                    rr += dr;
-                    if (c >= kk) {
-                        c -= kk;
-                        rr++;
-                    }
+                    if (c >= kk) c -= kk;
                 }
             }
             // partial rows: the head (owned by an earlier tile) and a cut tail
@@ -403,11 +416,13 @@ PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int hot_bytes)
     if (fixed + win_bytes > SMEM_BYTES) win_bytes = SMEM_BYTES - fixed;
     p.win_rows = (int)(win_bytes / per_row);
     if (p.win_rows > OFF_MAX - 1) p.win_rows = OFF_MAX - 1;
-    const size_t used = fixed + (size_t)p.win_rows * per_row;
+    const size_t plane = (((size_t)p.win_rows * k + 3) & ~(size_t)3) * sizeof(uint32_t);
+    const size_t used = fixed + plane * (weighted ? 2 : 1) + 16;  // + 16 B: hot_s is never empty
     size_t hot_cap = (SMEM_BYTES - used) / (size_t)hot_bytes;
     hot_cap &= ~(size_t)15;  // whole 16 B vectors (k_pull stages it with uint4 copies)
     p.hot0 = (int)(n_hot < (int64_t)hot_cap ? n_hot : (int64_t)hot_cap);
-    p.smem = used + (((size_t)p.hot0 * hot_bytes + 15) & ~(size_t)15);
+    p.hot0 &= ~15;  // the rest of the hot tier is read from the L2 table
+    p.smem = used + (size_t)p.hot0 * hot_bytes;
     return p;
 }
 
@@ -426,8 +441,9 @@ int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, 
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = WEIGHTED ? ldexp(1.0, -scale_exp) : 1.0;
+    const gee::LabelFmt hf = gee::label_fmt(sizeof(HT) == 1 ? 8 : 16);
     kern<<<grid, PT, ps.smem, st>>>(offsets, targets, w, arcs, tile_row, n_tiles, qscale, dscale, labels, lf, hot,
-                                    ps.hot0, inv, k, z, slots, ps.win_rows);
+                                    hf, ps.hot0, inv, k, z, slots, ps.win_rows);
     int rc = gee::check_launch("k_pull");
     if (rc) return rc;
     const int64_t want = (n_tiles * 32 + 255) / 256;
