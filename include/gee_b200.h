@@ -18,9 +18,17 @@
  *   - Z is a dense row-major (n, k) float32 array.  Its accumulator is exact
  *     integer arithmetic in the pull path and fp32 red.global in the push path.
  *   - Hot-path calls (gee_build_projection, gee_embed_coo, gee_embed_csr_pull)
- *     never allocate; graph-preparation calls (gee_build_sym_csr,
- *     gee_pull_plan, gee_graph_stats) may allocate stream-ordered scratch
- *     with cudaMallocAsync and free it before returning.
+ *     never allocate; graph-preparation calls (gee_build_csr, gee_hot_plan,
+ *     gee_graph_stats, ...) may allocate stream-ordered scratch with
+ *     cudaMallocAsync and free it before returning.
+ *
+ * Label table.  The edge kernels read labels from a table of
+ * gee_label_bytes(k)-byte entries (u8 for k <= 255, u16 for k <= 65535,
+ * else int32) laid out as
+ *     [ n_hot hot-tier labels in degree-rank order | n labels by vertex id | 0 ]
+ * (gee_label_table_bytes(n, n_hot, k) bytes).  Pull targets hold table
+ * slots: rank r for a hot vertex, n_hot + v for a cold vertex v
+ * (gee_hot_encode); with n_hot = 0 the slot is the vertex id itself.
  */
 #ifndef GEE_B200_H
 #define GEE_B200_H
@@ -48,30 +56,28 @@ int gee_version(void);
 /* Thread-local message of the last failing call ("" if none). */
 const char *gee_last_error(void);
 
-/* Packed label format.  gee_build_projection writes the labels as u32
- * words holding per = 32/bits labels of `bits` bits each, label i in word
- * i/per at bit (i%per)*bits; bits = gee_label_bits(k), the smallest of
- * {1,2,3,4,5,6,8,10,16} that holds k (32 = raw int32 labels, one per word).
- * K=50 -> 6 bits, 5 per word (C4's 134M labels: 107 MB, L2-resident). */
-int gee_label_bits(int32_t k);
-int64_t gee_label_words(int64_t n, int32_t label_bits);
+/* Bytes per label-table entry for k classes (1, 2 or 4) and table size. */
+int gee_label_bytes(int32_t k);
+size_t gee_label_table_bytes(int64_t n, int64_t n_hot, int32_t k);
 
 /* ---------------------------------------------------------------- K1 ----
- * Class-count histogram + projection scalars.
+ * Class-count histogram + projection scalars + label table.
  * Replaces build_projection (encoder.py:80-103: np.bincount at :87, inv at
  * :95-97) and class_counts (labeling.py:107-109).
  *   counts[k+1]   int64, bit-exact np.bincount(labels, minlength=k+1)
  *   inv_f32[k+1]  float, inv_f32[c] = (float)(1.0/counts[c]) or 0; inv[0] = 0
  *   inv_f64[k+1]  double, same in f64 (may be NULL)
- *   packed        gee_label_words(n, gee_label_bits(k)) packed label words (may be NULL)
+ *   table         label table (may be NULL): table[n_hot + v] = Y[v],
+ *                 table[hot_rank[v]] = Y[v] for hot v, table[n_hot + n] = 0
+ *   hot_rank      int32[n] (gee_hot_plan) or NULL when n_hot == 0
  *   bad           int64 device scalar: number of labels outside [0,k] (may be
- *                 NULL).  Counts of out-of-range labels are dropped.
- *   work          device scratch of gee_projection_work_bytes(k) bytes
+ *                 NULL).  Out-of-range labels count as 0 (unknown).
  */
 size_t gee_projection_work_bytes(int32_t k);
 int gee_build_projection(const int32_t *labels, int64_t n, int32_t k,
                          int64_t *counts, float *inv_f32, double *inv_f64,
-                         uint32_t *packed, int64_t *bad, void *work, void *stream);
+                         void *table, const int32_t *hot_rank, int64_t n_hot,
+                         int64_t *bad, void *stream);
 
 /* ---------------------------------------------------------------- K3 ----
  * Push edge map over a listed edge list (COO, structure of arrays).
@@ -81,37 +87,32 @@ int gee_build_projection(const int32_t *labels, int64_t n, int32_t k,
  *   Per edge i (u=src[i], v=dst[i], w = w ? w[i] : 1):
  *     if Y[v]: Z[u, Y[v]-1] += inv[Y[v]] * w
  *     if Y[u] and !(flags & GEE_SOURCE_ONLY): Z[v, Y[u]-1] += inv[Y[u]] * w
- *   labels: packed words with label_bits = gee_label_bits(k), or raw int32
- *   labels with label_bits = 32.  inv: inv_f32[k+1].
- *   Accumulation order is unspecified (fp32 atomics): results match the
- *   serial f64 oracle within fp32 accumulation error.
+ *   Y[x] = table[label_off + x] (label_off = n_hot of the table).
+ *   inv: inv_f32[k+1].  Accumulation order is unspecified (fp32 atomics):
+ *   results match the serial f64 oracle within fp32 accumulation error.
  */
 int gee_embed_coo(const int32_t *src, const int32_t *dst, const float *w, int64_t s,
-                  const uint32_t *labels, int32_t label_bits, const float *inv,
+                  const void *table, int64_t label_off, const float *inv,
                   int64_t n, int32_t k, float *z, uint32_t flags, void *stream);
 
 /* ---------------------------------------------------------------- K5 ----
- * Symmetric CSR of a listed edge list: row u holds (v, w) and row v holds
- * (u, w) for every listed edge (self-loops appear twice in row u).  This is
- * build_csr's undirected layout (graph.py:159-184, csr_fill
- * _kernels.py:229-238) applied to EVERY list, because the edge pass applies
- * both updates per listed edge whatever `directed` says (encoder.py:106-120).
- * Arc order within a row is unspecified (the pull accumulator is exact
- * integer arithmetic, so Z does not depend on it).
- *   offsets[n+1] int64; targets[2s] int32; weights[2s] float (NULL if w NULL)
- */
-int gee_build_sym_csr(const int32_t *src, const int32_t *dst, const float *w, int64_t s,
-                      int64_t n, int64_t *offsets, int32_t *targets, float *weights,
-                      void *stream);
-
-/* build_csr itself (graph.py:159-184): symmetric != 0 stores the mirror arc
- * of every listed edge (undirected EdgeList); 0 stores one arc per edge
- * (directed).  stable != 0 keeps the reference's arc order exactly (input
- * order, mirror right after the original; CUB radix sort by row, at most
- * 2^32-1 arcs); stable == 0 fills rows through atomic cursors. */
+ * build_csr (graph.py:159-184, csr_fill _kernels.py:229-238):
+ * symmetric != 0 stores the mirror arc of every listed edge (row u holds
+ * (v, w) and row v holds (u, w); self-loops twice); 0 stores one arc per
+ * edge.  stable != 0 keeps the reference's arc order exactly (input order,
+ * mirror right after the original; CUB radix sort by row, at most 2^32-1
+ * arcs); stable == 0 fills rows through atomic cursors (order unspecified --
+ * the pull accumulator is exact integer arithmetic, so Z does not depend on
+ * it).  offsets[n+1] int64; targets[arcs] int32; weights[arcs] float (NULL
+ * if w NULL).  The pull layout is the symmetric CSR of EVERY list, because
+ * the edge pass applies both updates per listed edge whatever `directed`
+ * says (encoder.py:106-120). */
 int gee_build_csr(const int32_t *src, const int32_t *dst, const float *w, int64_t s,
                   int64_t n, int32_t symmetric, int32_t stable, int64_t *offsets,
                   int32_t *targets, float *weights, void *stream);
+int gee_build_sym_csr(const int32_t *src, const int32_t *dst, const float *w, int64_t s,
+                      int64_t n, int64_t *offsets, int32_t *targets, float *weights,
+                      void *stream);
 
 /* Multi-GPU row-range ownership: offsets[n+1] of the full
  * symmetric CSR (degree count + scan, no fill) for the partition planner,
@@ -126,7 +127,7 @@ int gee_build_sym_csr_rows(const int32_t *src, const int32_t *dst, const float *
 
 /* CSR (offsets, arcs) -> per-arc source row (COO src) for a stored CsrGraph,
  * so that a directed CsrGraph (EdgeAccounting.BOTH_ENDPOINTS) can be fed to
- * gee_build_sym_csr or gee_embed_coo.  rows[arcs] int32. */
+ * gee_build_csr or gee_embed_coo.  rows[arcs] int32. */
 int gee_csr_rows(const int64_t *offsets, int64_t n, int64_t arcs, int32_t *rows, void *stream);
 
 /* Graph statistics that size the pull accumulator (host outputs):
@@ -136,19 +137,29 @@ int gee_graph_stats(const int64_t *offsets, const float *w, int64_t n, int64_t a
                     double *max_row_abs, double *min_abs_nz, double *max_abs,
                     int32_t *nonfinite, void *stream);
 
+/* Hot-label tier (see gee_hot.cu): gee_hot_plan ranks vertices by degree
+ * offsets[v+1]-offsets[v] (descending, ties by id) and marks the top
+ * max_hot with degree >= min_degree: hot_rank[v] = rank or -1,
+ * hot_vertex[rank] = v (may be NULL), *n_hot (host) = count.
+ * gee_hot_encode rewrites CSR targets into label-table slots: rank for hot
+ * vertices, n_hot + v otherwise. */
+int gee_hot_plan(const int64_t *offsets, int64_t n, int64_t max_hot, int64_t min_degree,
+                 int32_t *hot_rank, int32_t *hot_vertex, int64_t *n_hot, void *stream);
+int gee_hot_encode(int32_t *targets, int64_t arcs, const int32_t *hot_rank, int64_t n_hot,
+                   void *stream);
+
 /* ---------------------------------------------------------------- K4 ----
- * Pull (row-owner) edge map over a symmetric CSR.  Tile j covers arcs
- * [j*GEE_TILE_ARCS, (j+1)*GEE_TILE_ARCS) and owns the rows whose first arc
- * position offsets[r] falls in it; tile_row[j] = first such row
- * (gee_pull_plan).  Per row x:
+ * Pull (row-owner) edge map over a symmetric CSR whose targets are
+ * label-table slots.  Tile j covers arcs [j*GEE_TILE_ARCS, (j+1)*GEE_TILE_ARCS)
+ * and owns the rows whose first arc position offsets[r] falls in it;
+ * tile_row[j] = first such row (gee_pull_plan).  Per row x:
  *     Z[x, c] = inv[c+1] * sum_{arcs x->v, Y[v]=c+1} w
  * accumulated exactly in integers (unit weights: counts; weighted: fixed
  * point w*2^scale_exp rounded to int64), so Z is bit-stable run to run and
  * independent of arc order.  Every row of Z is written exactly once; no
  * zeroing is needed.  Rows that span tiles are combined through `slots`
  * (gee_pull_slots_bytes bytes, zero on first use, left zero on return).
- *   w == NULL means unit weights (scale_exp ignored).
- *   inv: inv_f64[k+1].
+ *   w == NULL means unit weights (scale_exp ignored).  inv: inv_f64[k+1].
  * Replaces embed_parallel's zero wave + arc wave (encoder.py:123-194,
  * zero_worker _kernels.py:124-135, arc_pass_worker _kernels.py:138-207)
  * for SOURCE_ONLY (symmetric) storage.
@@ -160,30 +171,8 @@ int gee_pull_plan(const int64_t *offsets, int64_t n, int64_t arcs, int64_t *tile
                   void *stream);
 int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const float *w,
                        int64_t n, int64_t arcs, const int64_t *tile_row, int32_t scale_exp,
-                       const uint32_t *labels, int32_t label_bits, const double *inv,
-                       int32_t k, float *z, void *slots, void *stream);
-
-/* Hot-label tier (graph preparation; see gee_hot.cu).  gee_hot_plan ranks
- * vertices by degree offsets[v+1]-offsets[v] (descending, ties by id) and
- * marks the top max_hot with degree >= min_degree: hot_rank[v] = rank or -1,
- * hot_vertex[rank] = v (may be NULL), *n_hot (host) = count.
- * gee_hot_encode rewrites targets t of hot vertices as 0x80000000|rank.
- * gee_build_projection_hot additionally scatters labels into hot_labels
- * (u8 if k <= 255 else u16, gee_hot_label_bytes) at their ranks, and
- * gee_embed_csr_pull_hot reads hot targets from that table (its head staged
- * in shared memory) and cold targets from the packed labels. */
-int gee_hot_plan(const int64_t *offsets, int64_t n, int64_t max_hot, int64_t min_degree,
-                 int32_t *hot_rank, int32_t *hot_vertex, int64_t *n_hot, void *stream);
-int gee_hot_encode(int32_t *targets, int64_t arcs, const int32_t *hot_rank, void *stream);
-int gee_hot_label_bytes(int32_t k);
-int gee_build_projection_hot(const int32_t *labels, int64_t n, int32_t k, int64_t *counts,
-                             float *inv_f32, double *inv_f64, uint32_t *packed, int64_t *bad,
-                             const int32_t *hot_rank, void *hot_labels, void *stream);
-int gee_embed_csr_pull_hot(const int64_t *offsets, const int32_t *targets, const float *w,
-                           int64_t n, int64_t arcs, const int64_t *tile_row, int32_t scale_exp,
-                           const uint32_t *labels, int32_t label_bits, const void *hot_labels,
-                           int64_t n_hot, const double *inv, int32_t k, float *z, void *slots,
-                           void *stream);
+                       const void *table, int64_t n_hot, const double *inv, int32_t k,
+                       float *z, void *slots, void *stream);
 
 /* Choose the fixed-point exponent for a weighted pull: the largest e with
  * max_row_abs * 2^e < 2^62.  Returns the relative quantisation bound

@@ -39,28 +39,24 @@ P_i32 = ctypes.POINTER(ctypes.c_int32)
 SIGNATURES = {
     "gee_version": (c_int, []),
     "gee_last_error": (ctypes.c_char_p, []),
-    "gee_label_bits": (c_int, [c_i32]),
-    "gee_label_words": (c_i64, [c_i64, c_i32]),
+    "gee_label_bytes": (c_int, [c_i32]),
+    "gee_label_table_bytes": (c_size, [c_i64, c_i64, c_i32]),
     "gee_projection_work_bytes": (c_size, [c_i32]),
-    "gee_build_projection": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp, vp, vp, vp]),
-    "gee_embed_coo": (c_int, [vp, vp, vp, c_i64, vp, c_i32, vp, c_i64, c_i32, vp, c_u32, vp]),
-    "gee_build_sym_csr": (c_int, [vp, vp, vp, c_i64, c_i64, vp, vp, vp, vp]),
+    "gee_build_projection": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp, vp, c_i64, vp, vp]),
+    "gee_embed_coo": (c_int, [vp, vp, vp, c_i64, vp, c_i64, vp, c_i64, c_i32, vp, c_u32, vp]),
     "gee_build_csr": (c_int, [vp, vp, vp, c_i64, c_i64, c_i32, c_i32, vp, vp, vp, vp]),
-    "gee_csr_rows": (c_int, [vp, c_i64, c_i64, vp, vp]),
+    "gee_build_sym_csr": (c_int, [vp, vp, vp, c_i64, c_i64, vp, vp, vp, vp]),
     "gee_sym_offsets": (c_int, [vp, vp, c_i64, c_i64, vp, vp]),
     "gee_build_sym_csr_rows": (c_int, [vp, vp, vp, c_i64, c_i64, c_i64, c_i64, vp, vp, vp, vp, vp]),
+    "gee_csr_rows": (c_int, [vp, c_i64, c_i64, vp, vp]),
     "gee_graph_stats": (c_int, [vp, vp, c_i64, c_i64, P_dbl, P_dbl, P_dbl, P_i32, vp]),
+    "gee_hot_plan": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, ctypes.POINTER(c_i64), vp]),
+    "gee_hot_encode": (c_int, [vp, c_i64, vp, c_i64, vp]),
     "gee_pull_tiles": (c_i64, [c_i64]),
     "gee_pull_slots_bytes": (c_size, [c_i64, c_i32]),
     "gee_pull_plan": (c_int, [vp, c_i64, c_i64, vp, vp]),
-    "gee_embed_csr_pull": (c_int, [vp, vp, vp, c_i64, c_i64, vp, c_i32, vp, c_i32, vp, c_i32, vp, vp, vp]),
+    "gee_embed_csr_pull": (c_int, [vp, vp, vp, c_i64, c_i64, vp, c_i32, vp, c_i64, vp, c_i32, vp, vp, vp]),
     "gee_pull_scale_exp": (c_int, [c_dbl, c_dbl, P_i32, P_dbl]),
-    "gee_hot_plan": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, ctypes.POINTER(c_i64), vp]),
-    "gee_hot_encode": (c_int, [vp, c_i64, vp, vp]),
-    "gee_hot_label_bytes": (c_int, [c_i32]),
-    "gee_build_projection_hot": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp, vp, vp, vp, vp]),
-    "gee_embed_csr_pull_hot": (c_int, [vp, vp, vp, c_i64, c_i64, vp, c_i32, vp, c_i32, vp, c_i64, vp, c_i32, vp,
-                                       vp, vp]),
     "gee_synth_word": (c_u64, [c_u64, c_u64, c_u64]),
     "gee_synth_rmat": (c_int, [vp, vp, vp, c_i64, c_i64, c_i32, c_dbl, c_dbl, c_dbl, c_u64, c_i32, vp]),
     "gee_synth_er": (c_int, [vp, vp, vp, c_i64, c_i64, c_i64, c_u64, vp]),

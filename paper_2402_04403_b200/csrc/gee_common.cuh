@@ -39,29 +39,34 @@ template <typename T>
 __device__ __forceinline__ T ldg_ro(const T *p) { return __ldg(p); }
 
 // ---------------------------------------------------------------- labels
-// Compact labels are packed into u32 words: `per` labels of `bits` bits per
-// word (bits = smallest width holding k; per = 32 / bits).  K=50 packs five
-// 6-bit labels per word, so C4's 134M labels take 107 MB and stay resident
-// in the 126 MB L2.  bits == 32 (per == 1) reads raw int32 labels.
-struct LabelFmt {
-    uint32_t bits, per, mask;
-    uint32_t magic, shift;  // t / per == (t * magic) >> shift for 0 <= t < 2^31
-};
-
-// magic = ceil(2^(31+l) / per) with 2^l >= per: < 2^32, and the rounding
-// error t*(magic*per - 2^(31+l)) / (per 2^(31+l)) < 2^-l <= 1/per keeps the
-// floor exact for every 31-bit t.
-inline LabelFmt label_fmt(int bits)
+// The edge kernels read labels from a "label table": one u8 (k <= 255), u16
+// (k <= 65535) or int32 entry per slot, laid out as
+//     [ hot tier: n_hot labels in degree-rank order | n labels by vertex id | 0 ]
+// (gee_build_projection writes it; gee_hot.cu plans the hot tier).  A CSR
+// target stores its slot directly: rank for a hot vertex, n_hot + v for a
+// cold one; the trailing zero slot is the sentinel for padding arcs.
+template <typename LT>
+__device__ __forceinline__ uint32_t ld_label(const LT *p, uint64_t pol);
+template <>
+__device__ __forceinline__ uint32_t ld_label<uint8_t>(const uint8_t *p, uint64_t pol)
 {
-    LabelFmt f;
-    f.bits = (uint32_t)bits;
-    f.per = 32u / f.bits;
-    f.mask = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
-    uint32_t l = 0;
-    while ((1u << l) < f.per) l++;
-    f.shift = 31 + l;
-    f.magic = (uint32_t)(((1ull << f.shift) + f.per - 1) / f.per);
-    return f;
+    uint16_t v;
+    asm("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <>
+__device__ __forceinline__ uint32_t ld_label<uint16_t>(const uint16_t *p, uint64_t pol)
+{
+    uint16_t v;
+    asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <>
+__device__ __forceinline__ uint32_t ld_label<int32_t>(const int32_t *p, uint64_t pol)
+{
+    uint32_t v;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
 }
 
 __device__ __forceinline__ uint64_t policy_evict_last()
@@ -69,23 +74,6 @@ __device__ __forceinline__ uint64_t policy_evict_last()
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
-}
-
-// Label gather: read-only path, L2 evict_last so the streamed CSR/Z bytes
-// do not push the label words out of L2.
-__device__ __forceinline__ uint32_t ld_label_word(const uint32_t *p, uint64_t pol)
-{
-    uint32_t v;
-    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-    return v;
-}
-
-__device__ __forceinline__ uint32_t gather_label(const uint32_t *__restrict__ words, uint32_t t,
-                                                 const LabelFmt &f, uint64_t pol)
-{
-    const uint32_t wi = (uint32_t)(((uint64_t)t * f.magic) >> f.shift);
-    const uint32_t sh = (t - wi * f.per) * f.bits;
-    return (ld_label_word(words + wi, pol) >> sh) & f.mask;
 }
 
 }  // namespace gee

@@ -8,11 +8,11 @@
 //
 // gee_hot_plan ranks vertices by symmetric degree (stable radix sort,
 // descending; ties by vertex id) and keeps the top `max_hot` with degree >=
-// min_degree; gee_hot_encode rewrites CSR targets of hot vertices as
-// 0x80000000 | rank.  In the timed region, gee_build_projection_hot
-// scatters the labels of hot vertices into a dense rank-ordered table
-// (u8/u16) that stays in L2, and each pull CTA stages its head in shared
-// memory.  Cold targets keep their vertex id and use the packed array.
+// min_degree; gee_hot_encode rewrites CSR targets into label-table slots
+// (rank for hot vertices, n_hot + v otherwise).  In the timed region
+// gee_build_projection also writes the hot vertices' labels at their ranks:
+// a dense prefix of the label table that stays in L2, and whose head each
+// pull CTA stages in shared memory.
 #include <cub/device/device_radix_sort.cuh>
 
 #include "gee_common.cuh"
@@ -54,14 +54,13 @@ __global__ void k_assign_ranks(const int32_t *__restrict__ sorted_ids, const uns
     }
 }
 
-__global__ void k_hot_encode(int32_t *__restrict__ targets, int64_t arcs, const int32_t *__restrict__ hot_rank)
+__global__ void k_hot_encode(int32_t *__restrict__ targets, int64_t arcs, const int32_t *__restrict__ hot_rank,
+                             int32_t n_hot)
 {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < arcs; e += (int64_t)gridDim.x * blockDim.x) {
         const int32_t t = targets[e];
-        if (t >= 0) {
-            const int32_t r = hot_rank[t];
-            if (r >= 0) targets[e] = (int32_t)(0x80000000u | (uint32_t)r);
-        }
+        const int32_t r = hot_rank[t];
+        targets[e] = r >= 0 ? r : n_hot + t;
     }
 }
 
@@ -139,16 +138,14 @@ out:
     return rc;
 }
 
-int gee_hot_encode(int32_t *targets, int64_t arcs, const int32_t *hot_rank, void *stream)
+int gee_hot_encode(int32_t *targets, int64_t arcs, const int32_t *hot_rank, int64_t n_hot, void *stream)
 {
     gee::clear_error();
-    GEE_REQUIRE(arcs >= 0, GEE_ERR_INVALID, "arcs must be nonnegative");
+    GEE_REQUIRE(arcs >= 0 && n_hot >= 0 && n_hot < INT32_MAX, GEE_ERR_INVALID, "bad arcs / n_hot");
     if (arcs == 0) return GEE_OK;
     GEE_REQUIRE(targets && hot_rank, GEE_ERR_INVALID, "NULL array argument");
-    k_hot_encode<<<grid_for(arcs), 256, 0, gee::as_stream(stream)>>>(targets, arcs, hot_rank);
+    k_hot_encode<<<grid_for(arcs), 256, 0, gee::as_stream(stream)>>>(targets, arcs, hot_rank, (int32_t)n_hot);
     return gee::check_launch("k_hot_encode");
 }
-
-int gee_hot_label_bytes(int32_t k) { return k <= 255 ? 1 : 2; }
 
 }  // extern "C"

@@ -20,25 +20,26 @@
 //                   sm_100a, 64-bit shared atomics are CAS loops).
 //
 // Work decomposition (balanced by arcs, hub rows split for free):
-//   tile j = arcs [j*T, (j+1)*T), T = GEE_TILE_ARCS = 1024 threads x 4 arcs;
+//   tile j = arcs [j*T, (j+1)*T), T = GEE_TILE_ARCS = 512 threads x 8 arcs;
 //   tile j OWNS the rows whose first-arc position offsets[r] lies in it;
 //   tile_row[j] = first owned row (gee_pull_plan, a lower_bound per tile).
-//   One persistent 1024-thread CTA per SM walks tiles j = blockIdx.x,
+//   One persistent 512-thread CTA per SM walks tiles j = blockIdx.x,
 //   += gridDim.x through a two-stage software pipeline: while tile j is
 //   accumulated, tile j+G's labels are being gathered and its row offsets
 //   staged (cp.async), and tile j+2G's arcs stream in (128-bit, L2
-//   evict-first).  Labels come from the hot tier (gee_hot.cu: shared-memory
-//   head, then an L2-resident rank-ordered table) or the packed array (L2
-//   evict-last).  Each thread finds its arcs' rows in the staged offsets by
-//   one binary search plus a forward walk.  Rows that run past their owner tile (hubs) are
+//   evict-first).  Targets are label-table slots (gee_common.cuh): the hot
+//   tier's head is staged in shared memory, the rest of the table is read
+//   through L2 (evict-last).  Rows use 32-bit tile-local offsets; a warp
+//   brackets its first arc with two 32-way ballots and each lane gallops to
+//   its own.  Rows that run past their owner tile (hubs) are
 //   summed exactly through 64-bit global atomics into the owner tile's slot
 //   and written by k_pull_finalize.
 #include "gee_common.cuh"
 
 namespace {
 
-constexpr int PT = 1024;                 // threads per CTA (one persistent CTA per SM)
-constexpr int APT = 4;                   // arcs per thread
+constexpr int PT = 512;                  // threads per CTA (one persistent CTA per SM)
+constexpr int APT = 8;                   // arcs per thread
 constexpr int TILE = PT * APT;           // 4096
 static_assert(TILE == GEE_TILE_ARCS, "tile size mismatch with header");
 constexpr int SMEM_BYTES = 227 * 1024;   // opt-in maximum per CTA on sm_100a
@@ -92,22 +93,25 @@ struct TileLabs {  // stage B: gathered labels of a tile
 template <bool WEIGHTED>
 __device__ __forceinline__ void load_arcs(TileArcs &A, int64_t j, int tid, const int32_t *__restrict__ targets,
                                           const float *__restrict__ w, int64_t arcs,
-                                          const int64_t *__restrict__ tile_row)
+                                          const int64_t *__restrict__ tile_row, int32_t sentinel)
 {
-    const int64_t a0 = j * (int64_t)TILE, a1 = min(a0 + (int64_t)TILE, arcs);
-    const int64_t e0 = a0 + (int64_t)tid * APT;
-    if (e0 + APT <= a1) {
-        const int4 t4 = __ldcs(reinterpret_cast<const int4 *>(targets + e0));
-        A.t[0] = t4.x; A.t[1] = t4.y; A.t[2] = t4.z; A.t[3] = t4.w;
+    const int64_t e0 = j * (int64_t)TILE + (int64_t)tid * APT;
+    if (e0 + APT <= arcs) {
+        const int4 t0 = __ldcs(reinterpret_cast<const int4 *>(targets + e0));
+        const int4 t1 = __ldcs(reinterpret_cast<const int4 *>(targets + e0 + 4));
+        A.t[0] = t0.x; A.t[1] = t0.y; A.t[2] = t0.z; A.t[3] = t0.w;
+        A.t[4] = t1.x; A.t[5] = t1.y; A.t[6] = t1.z; A.t[7] = t1.w;
         if (WEIGHTED) {
-            const float4 w4 = __ldcs(reinterpret_cast<const float4 *>(w + e0));
-            A.w[0] = w4.x; A.w[1] = w4.y; A.w[2] = w4.z; A.w[3] = w4.w;
+            const float4 w0 = __ldcs(reinterpret_cast<const float4 *>(w + e0));
+            const float4 w1 = __ldcs(reinterpret_cast<const float4 *>(w + e0 + 4));
+            A.w[0] = w0.x; A.w[1] = w0.y; A.w[2] = w0.z; A.w[3] = w0.w;
+            A.w[4] = w1.x; A.w[5] = w1.y; A.w[6] = w1.z; A.w[7] = w1.w;
         }
-    } else {
+    } else {  // last tile: padding arcs read the sentinel slot (label 0)
 #pragma unroll
         for (int i = 0; i < APT; i++) {
-            const bool ok = e0 + i < a1;
-            A.t[i] = ok ? __ldcs(targets + e0 + i) : 0;
+            const bool ok = e0 + i < arcs;
+            A.t[i] = ok ? __ldcs(targets + e0 + i) : sentinel;
             if (WEIGHTED) A.w[i] = ok ? __ldcs(w + e0 + i) : 0.f;
         }
     }
@@ -115,35 +119,19 @@ __device__ __forceinline__ void load_arcs(TileArcs &A, int64_t j, int tid, const
     A.r1 = (int32_t)tile_row[j + 1];
 }
 
-// Label of every arc of a tile.  Hot targets (t < 0) below hot0 read the
-// shared-memory head; other hot targets read the L2 hot table (as u32 words,
-// format hf: 8 or 16 bits); cold targets read the packed array (format lf).
-// Branch-free apart from the predicated global load.
-template <bool WEIGHTED, typename HT>
-__device__ __forceinline__ void gather_labs(TileLabs &B, const TileArcs &A, int64_t j, int tid, int64_t arcs,
-                                            const uint32_t *__restrict__ labels, const gee::LabelFmt &lf,
-                                            const uint32_t *__restrict__ hot_words, const gee::LabelFmt &hf,
-                                            const HT *__restrict__ hot_s, uint32_t hot0, uint32_t k, uint64_t pol)
+// Labels of this thread's arcs: slots below hot0 from shared memory, the
+// rest through L2 (one predicated load each; all APT in flight).
+template <bool WEIGHTED, typename LT>
+__device__ __forceinline__ void gather_labs(TileLabs &B, const TileArcs &A, const LT *__restrict__ table,
+                                            const LT *__restrict__ hot_s, uint32_t hot0, uint64_t pol)
 {
-    const int64_t e0 = j * (int64_t)TILE + (int64_t)tid * APT;
 #pragma unroll
     for (int i = 0; i < APT; i++) {
-        const int32_t t = A.t[i];
-        const bool hot = t < 0;
-        const uint32_t idx = (uint32_t)t & 0x7fffffffu;
-        const bool in_smem = hot && idx < hot0;
-        const uint32_t ls = (uint32_t)hot_s[in_smem ? idx : 0u];
-        const uint32_t magic = hot ? hf.magic : lf.magic, shift = hot ? hf.shift : lf.shift;
-        const uint32_t per = hot ? hf.per : lf.per, bits = hot ? hf.bits : lf.bits;
-        const uint32_t mask = hot ? hf.mask : lf.mask;
-        const uint32_t wi = (uint32_t)(((uint64_t)idx * magic) >> shift);
-        const uint32_t sh = (idx - wi * per) * bits;
-        const uint32_t *p = (hot ? hot_words : labels) + wi;
-        uint32_t word = 0u;
-        if (!in_smem && e0 + i < arcs) word = gee::ld_label_word(p, pol);
-        uint32_t lab = in_smem ? ls : ((word >> sh) & mask);
-        if (e0 + i >= arcs) lab = 0u;
-        B.l[i] = lab > k ? 0u : lab;  // raw int32 labels: drop out-of-range
+        const uint32_t t = (uint32_t)A.t[i];
+        const bool in_smem = t < hot0;
+        uint32_t lab = (uint32_t)hot_s[in_smem ? t : 0u];
+        if (!in_smem) lab = gee::ld_label<LT>(table + t, pol);
+        B.l[i] = lab;
         if (WEIGHTED) B.w[i] = A.w[i];
     }
     B.r0 = A.r0;
@@ -156,35 +144,35 @@ __device__ __forceinline__ void stage_offsets(int64_t *buf, const int64_t *__res
 {
     const int32_t start = r0 > 0 ? r0 - 1 : 0;
     const int32_t cnt = min(r1 - start + 1, OFF_MAX);
-    if (tid < cnt) cp_async8(buf + tid, offsets + start + tid);
+    for (int i = tid; i < cnt; i += PT) cp_async8(buf + i, offsets + start + i);
 }
 
-template <bool WEIGHTED, typename HT>
+template <bool WEIGHTED, typename LT>
 __global__ void __launch_bounds__(PT, 1)
 k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
        const float *__restrict__ w, int64_t arcs, const int64_t *__restrict__ tile_row, int64_t n_tiles,
-       float qscale, double dscale, const uint32_t *__restrict__ labels, gee::LabelFmt lf,
-       const HT *__restrict__ hot, gee::LabelFmt hf, int32_t hot0, const double *__restrict__ inv, int32_t k,
-       float *__restrict__ z, unsigned long long *__restrict__ slots, int win_rows)
+       float qscale, double dscale, const LT *__restrict__ table, int32_t sentinel, int32_t hot0,
+       const double *__restrict__ inv, int32_t k, float *__restrict__ z, unsigned long long *__restrict__ slots,
+       int win_rows)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    int64_t *off_buf = reinterpret_cast<int64_t *>(smem_raw);         // 2 x OFF_MAX
-    float *sc = reinterpret_cast<float *>(off_buf + 2 * OFF_MAX + 2);  // k+1 output scales
+    int64_t *off_buf = reinterpret_cast<int64_t *>(smem_raw);          // 2 x OFF_MAX int64
+    int32_t *ol = reinterpret_cast<int32_t *>(off_buf + 2 * OFF_MAX);  // OFF_MAX (+3) tile-local int32
+    float *sc = reinterpret_cast<float *>(ol + OFF_MAX + 3);           // k+1 output scales
     uint32_t *acc_lo = reinterpret_cast<uint32_t *>(sc + ((k + 4) & ~3));
-    const size_t plane = ((size_t)win_rows * k + 3) & ~(size_t)3;     // 16 B aligned planes
+    const size_t plane = ((size_t)win_rows * k + 3) & ~(size_t)3;      // 16 B aligned planes
     uint32_t *acc_hi = acc_lo + plane;                                 // weighted only
-    HT *hot_s = reinterpret_cast<HT *>(acc_lo + plane * (WEIGHTED ? 2 : 1));
+    LT *hot_s = reinterpret_cast<LT *>(acc_lo + plane * (WEIGHTED ? 2 : 1));
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int kk = k;
     const uint64_t pol = gee::policy_evict_last();
-    const uint32_t *hot_words = reinterpret_cast<const uint32_t *>(hot);
     // Z[x, c] = sum * sc[c+1]: inv folded with the fixed-point scale, fp32.
     for (int c = tid; c <= kk; c += PT) sc[c] = (float)(inv[c] * dscale);
-    {  // stage the head of the hot tier (hot0 * sizeof(HT) is a multiple of 16 B)
-        const int vec = (int)((size_t)hot0 * sizeof(HT) / 16);
-        const uint4 *src = reinterpret_cast<const uint4 *>(hot);
+    {  // stage the head of the label table (hot tier) with 16 B copies
+        const int vec = (int)(((size_t)hot0 * sizeof(LT) + 15) / 16);
+        const uint4 *src = reinterpret_cast<const uint4 *>(table);
         uint4 *dst = reinterpret_cast<uint4 *>(hot_s);
         for (int i = tid; i < vec; i += PT) dst[i] = __ldg(src + i);
     }
@@ -195,17 +183,17 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
     if (jA >= n_tiles) return;
     TileArcs A;
     TileLabs B;
-    // prologue: tile j0 gathered + staged, tile j0+G arcs in flight
-    load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row);
-    gather_labs<WEIGHTED>(B, A, jA, tid, arcs, labels, lf, hot_words, hf, hot_s, (uint32_t)hot0, (uint32_t)kk, pol);
+    // prologue: tile j0 gathered + offsets staged, tile j0+G arcs in flight
+    load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row, sentinel);
+    gather_labs<WEIGHTED, LT>(B, A, table, hot_s, (uint32_t)hot0, pol);
     stage_offsets(off_buf, offsets, B.r0, B.r1, tid);
     cp_async_commit();
     jA += G;
-    if (jA < n_tiles) load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row);
+    if (jA < n_tiles) load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row, sentinel);
     int buf = 0;
+    const int el0 = tid * APT;  // this thread's first arc, tile-local
 
     for (int64_t j = blockIdx.x; j < n_tiles; j += G) {
-        // current tile j: labels/weights from stage B
         uint32_t lab[APT];
         float wcur[APT];
 #pragma unroll
@@ -215,42 +203,51 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         }
         const int32_t R0 = B.r0, R1 = B.r1;
         // advance the pipeline: gather tile j+G, stage its offsets, load tile j+2G
-        const bool more = jA < n_tiles;
-        if (more) {
-            gather_labs<WEIGHTED>(B, A, jA, tid, arcs, labels, lf, hot_words, hf, hot_s, (uint32_t)hot0, (uint32_t)kk, pol);
+        if (jA < n_tiles) {
+            gather_labs<WEIGHTED, LT>(B, A, table, hot_s, (uint32_t)hot0, pol);
             stage_offsets(off_buf + (buf ^ 1) * OFF_MAX, offsets, B.r0, B.r1, tid);
         }
         cp_async_commit();
         jA += G;
-        if (jA < n_tiles) load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row);
+        if (jA < n_tiles) load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row, sentinel);
         cp_async_wait<1>();  // tile j's staged offsets have landed (tile j+G's may be in flight)
 
         // ---- process tile j
-        const int64_t a0 = j * (int64_t)TILE, a1 = min(a0 + (int64_t)TILE, arcs);
-        const int64_t e0 = a0 + (int64_t)tid * APT;
-        int64_t *off_s = off_buf + buf * OFF_MAX;
-        int32_t st0 = R0 > 0 ? R0 - 1 : 0;           // first staged row
-        int32_t scnt = min(R1 - st0 + 1, OFF_MAX);   // staged count
-        __syncthreads();                             // staged offsets visible to all threads
-        const int64_t offR0 = off_s[R0 - st0];
-        const bool has_head = offR0 > a0;            // also when R0 == n (offsets[n] = arcs > a0)
+        const int64_t a0 = j * (int64_t)TILE;
+        const int tlen = (int)min((int64_t)TILE, arcs - a0);
+        const int64_t *off_s = off_buf + buf * OFF_MAX;
+        const int32_t st0 = R0 > 0 ? R0 - 1 : 0;  // first staged row
+        int32_t scnt = min(R1 - st0 + 1, OFF_MAX);
+        __syncthreads();  // staged offsets visible; previous tile's smem reads done
+        // has_head: offsets[R0] > a0; tail_cut: offsets[R1] > a1 (read before ol is rewritten)
+        const bool has_head = off_s[R0 - st0] > a0;  // also when R0 == n (offsets[n] = arcs > a0)
         const int64_t offR1 = (R1 - st0 < scnt) ? off_s[R1 - st0] : __ldcs(offsets + R1);
-        const bool tail_cut = (R1 > R0) && (offR1 > a1);
+        const bool tail_cut = (R1 > R0) && (offR1 > a0 + tlen);
         const int32_t base = has_head ? R0 - 1 : R0;
         const int32_t rows_total = R1 - base;
+        int32_t ost = st0;  // row of ol[0]
 
         for (int32_t wo = 0; wo < rows_total; wo += win_rows) {
             const int nr = min(win_rows, rows_total - wo);
             const int32_t wrow0 = base + wo;
             const int words = nr * kk;
-            if (wrow0 - st0 + nr >= scnt) {
-                // window not (fully) staged: restage synchronously (large tiles only)
-                __syncthreads();
-                for (int i = tid; i <= nr; i += PT) off_s[i] = __ldcs(offsets + wrow0 + i);
-                st0 = wrow0;
+            if (wo > 0) __syncthreads();  // previous window's write-out done
+            if (wrow0 - ost + nr < scnt && wo == 0) {
+                // tile-local int32 offsets, clamped to [0, TILE+1]
+                for (int i = tid; i < scnt; i += PT) {
+                    const int64_t v = off_s[i] - a0;
+                    ol[i] = (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
+                }
+            } else {
+                // window not fully staged (large tiles): load it directly
+                for (int i = tid; i <= nr; i += PT) {
+                    const int64_t v = __ldcs(offsets + wrow0 + i) - a0;
+                    ol[i] = (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
+                }
+                ost = wrow0;
                 scnt = nr + 1;
             }
-            {  // zero the window: acc planes are 16 B aligned, words rounded up to 4
+            {  // zero the window
                 uint4 *a4 = reinterpret_cast<uint4 *>(acc_lo);
                 const int w4 = (words + 3) >> 2;
                 const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
@@ -261,44 +258,44 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 }
             }
             __syncthreads();
-            const int64_t *ow = off_s + (wrow0 - st0);  // ow[r] = offsets[wrow0 + r]
-            const int64_t wa0 = max(ow[0], a0), wa1 = min(ow[nr], a1);
-            const int64_t m0 = max(e0, wa0), m1 = min(e0 + APT, wa1);
-            // Row of this thread's first arc: the warp brackets its first arc
-            // with two 32-way ballots, then each lane gallops from there.
-            const int64_t ew = max(a0 + (int64_t)(tid & ~31) * APT, wa0);
+            const int32_t *ow = ol + (wrow0 - ost);  // ow[r] = offsets[wrow0 + r] - a0 (clamped)
+            const int wa0 = ow[0], wa1 = min(ow[nr], tlen);
+            const int m0 = max(el0, wa0), m1 = min(el0 + APT, wa1);
+            // Row of the warp's first arc: two 32-way ballots.
+            const int ew = max(el0 - lane * APT, wa0);
             int rw = 0;
-            if (ew < wa1) {
+            if (ew < wa1) {  // warp-uniform
                 const int step = (nr + 31) >> 5;  // <= 16
                 int cand = min(lane * step, nr);
                 unsigned bal = __ballot_sync(0xffffffffu, ow[cand] <= ew);
-                int b = (31 - __clz(bal)) * step;  // ow[b] <= ew
+                const int b = (31 - __clz(bal)) * step;  // ow[b] <= ew
                 cand = min(b + lane, nr);
                 bal = __ballot_sync(0xffffffffu, lane < step && ow[cand] <= ew);
                 rw = b + (31 - __clz(bal));
             }
             if (m0 < m1) {
-                // gallop from rw: find last r with ow[r] <= m0
+                // gallop from rw to the last r with ow[r] <= m0, then walk arcs
                 int lo = rw, g = 1;
                 while (lo + g < nr && ow[lo + g] <= m0) {
                     lo += g;
                     g <<= 1;
                 }
-                int hi = min(lo + g, nr);  // ow[lo] <= m0 < ow[hi] (ow[nr] >= m1 > m0)
+                int hi = min(lo + g, nr);  // ow[lo] <= m0 < ow[hi]
                 while (hi - lo > 1) {
                     const int mid = (lo + hi) >> 1;
                     if (ow[mid] <= m0) lo = mid;
                     else hi = mid;
                 }
                 int r = lo;
-                int64_t next = ow[r + 1];
+                int next = ow[r + 1];
 #pragma unroll
                 for (int i = 0; i < APT; i++) {
-                    const int64_t e = e0 + i;
+                    const int e = el0 + i;
                     if (e < m0 || e >= m1) continue;
                     while (e >= next) next = ow[++r + 1];
-                    if (lab[i] == 0u) continue;
-                    const int idx = r * kk + (int)lab[i] - 1;
+                    const uint32_t c = lab[i];
+                    if (c == 0u || c > (uint32_t)kk) continue;  // unlabeled (or out-of-range raw label)
+                    const int idx = r * kk + (int)c - 1;
                     if (WEIGHTED) {
                         const unsigned long long q = (unsigned long long)__float2ll_rn(wcur[i] * qscale);
                         const uint32_t lo32 = (uint32_t)q;
@@ -344,7 +341,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     row = R1 - 1;
                     if (row < wrow0 || row >= wrow0 + nr) continue;
                 }
-                const int64_t owner = part == 0 ? ow[0] / TILE : j;
+                const int64_t owner = part == 0 ? __ldg(offsets + row) / TILE : j;
                 const int lr = row - wrow0;
                 for (int c = tid; c < kk; c += PT) {
                     const int idx = lr * kk + c;
@@ -353,7 +350,6 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     if (v) atomicAdd(&slots[owner * kk + c], v);
                 }
             }
-            __syncthreads();
         }
         buf ^= 1;
     }
@@ -396,7 +392,7 @@ __global__ void k_zero_tail(const int64_t *__restrict__ first_row, int64_t n, in
 
 size_t pull_fixed_smem(int32_t k)
 {
-    return (2 * OFF_MAX + 2) * sizeof(int64_t) + (size_t)((k + 4) & ~3) * sizeof(float);
+    return 2 * OFF_MAX * sizeof(int64_t) + (OFF_MAX + 3) * sizeof(int32_t) + (size_t)((k + 4) & ~3) * sizeof(float);
 }
 
 struct PullShape {
@@ -405,45 +401,44 @@ struct PullShape {
     size_t smem;
 };
 
-PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int hot_bytes)
+PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes)
 {
     PullShape p{0, 0, 0};
     const size_t fixed = pull_fixed_smem(k);
     const size_t per_row = (size_t)k * sizeof(uint32_t) * (weighted ? 2 : 1);
-    if (fixed + per_row > SMEM_BYTES) return p;
+    if (fixed + per_row + 16 > SMEM_BYTES) return p;
     size_t win_bytes = per_row * (OFF_MAX - 1);
     if (win_bytes > WIN_BYTES_MAX) win_bytes = WIN_BYTES_MAX > per_row ? WIN_BYTES_MAX : per_row;
-    if (fixed + win_bytes > SMEM_BYTES) win_bytes = SMEM_BYTES - fixed;
+    if (fixed + win_bytes + 16 > SMEM_BYTES) win_bytes = SMEM_BYTES - fixed - 16;
     p.win_rows = (int)(win_bytes / per_row);
     if (p.win_rows > OFF_MAX - 1) p.win_rows = OFF_MAX - 1;
     const size_t plane = (((size_t)p.win_rows * k + 3) & ~(size_t)3) * sizeof(uint32_t);
-    const size_t used = fixed + plane * (weighted ? 2 : 1) + 16;  // + 16 B: hot_s is never empty
-    size_t hot_cap = (SMEM_BYTES - used) / (size_t)hot_bytes;
-    hot_cap &= ~(size_t)15;  // whole 16 B vectors (k_pull stages it with uint4 copies)
+    const size_t used = fixed + plane * (weighted ? 2 : 1);
+    size_t hot_cap = (SMEM_BYTES - used) / (size_t)label_bytes;
+    hot_cap &= ~(size_t)15;
     p.hot0 = (int)(n_hot < (int64_t)hot_cap ? n_hot : (int64_t)hot_cap);
-    p.hot0 &= ~15;  // the rest of the hot tier is read from the L2 table
-    p.smem = used + (size_t)p.hot0 * hot_bytes;
+    p.hot0 &= ~15;  // whole 16 B vectors; the rest of the hot tier is read through L2
+    p.smem = used + (((size_t)p.hot0 * label_bytes + 16 + 15) & ~(size_t)15);  // >= 16 B: slot 0 always readable
     return p;
 }
 
-template <bool WEIGHTED, typename HT>
-int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t arcs,
-                const int64_t *tile_row, int32_t scale_exp, const uint32_t *labels, gee::LabelFmt lf,
-                const HT *hot, int64_t n_hot, const double *inv, int32_t k, float *z, unsigned long long *slots,
-                cudaStream_t st)
+template <bool WEIGHTED, typename LT>
+int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n, int64_t arcs,
+                const int64_t *tile_row, int32_t scale_exp, const LT *table, int64_t n_hot, const double *inv,
+                int32_t k, float *z, unsigned long long *slots, cudaStream_t st)
 {
     const int64_t n_tiles = gee_pull_tiles(arcs);
-    const PullShape ps = pull_shape(k, WEIGHTED, hot ? n_hot : 0, (int)sizeof(HT));
+    const PullShape ps = pull_shape(k, WEIGHTED, n_hot, (int)sizeof(LT));
     GEE_REQUIRE(ps.win_rows >= 1, GEE_ERR_INVALID, "k=%d too large for the pull window", k);
-    auto kern = k_pull<WEIGHTED, HT>;
+    auto kern = k_pull<WEIGHTED, LT>;
     GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps.smem));
     const int64_t cap = (int64_t)gee::sm_count();
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = WEIGHTED ? ldexp(1.0, -scale_exp) : 1.0;
-    const gee::LabelFmt hf = gee::label_fmt(sizeof(HT) == 1 ? 8 : 16);
-    kern<<<grid, PT, ps.smem, st>>>(offsets, targets, w, arcs, tile_row, n_tiles, qscale, dscale, labels, lf, hot,
-                                    hf, ps.hot0, inv, k, z, slots, ps.win_rows);
+    const int32_t sentinel = (int32_t)(n_hot + n);
+    kern<<<grid, PT, ps.smem, st>>>(offsets, targets, w, arcs, tile_row, n_tiles, qscale, dscale, table, sentinel,
+                                    ps.hot0, inv, k, z, slots, ps.win_rows);
     int rc = gee::check_launch("k_pull");
     if (rc) return rc;
     const int64_t want = (n_tiles * 32 + 255) / 256;
@@ -493,19 +488,14 @@ int gee_pull_scale_exp(double max_row_abs, double min_abs_nz, int32_t *scale_exp
     return GEE_OK;
 }
 
-int gee_embed_csr_pull_hot(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n,
-                           int64_t arcs, const int64_t *tile_row, int32_t scale_exp, const uint32_t *labels,
-                           int32_t label_bits, const void *hot_labels, int64_t n_hot, const double *inv,
-                           int32_t k, float *z, void *slots, void *stream)
+int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n, int64_t arcs,
+                       const int64_t *tile_row, int32_t scale_exp, const void *table, int64_t n_hot,
+                       const double *inv, int32_t k, float *z, void *slots, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1, GEE_ERR_INVALID, "class count k must be positive (got %d)", k);
-    GEE_REQUIRE(n >= 0 && arcs >= 0, GEE_ERR_INVALID, "n and arcs must be nonnegative");
-    GEE_REQUIRE(n <= INT32_MAX, GEE_ERR_INVALID, "node count %lld exceeds int32 targets", (long long)n);
-    GEE_REQUIRE(label_bits == 32 || label_bits == gee_label_bits(k), GEE_ERR_INVALID,
-                "label_bits must be 32 (raw int32) or gee_label_bits(k)=%d (got %d)", gee_label_bits(k), label_bits);
-    GEE_REQUIRE(n_hot == 0 || (hot_labels && k <= 65535 && n_hot <= n), GEE_ERR_INVALID,
-                "hot tier needs hot_labels, k <= 65535 and n_hot <= n");
+    GEE_REQUIRE(n >= 0 && arcs >= 0 && n_hot >= 0, GEE_ERR_INVALID, "n, arcs and n_hot must be nonnegative");
+    GEE_REQUIRE(n + n_hot < INT32_MAX, GEE_ERR_INVALID, "label table exceeds int32 slots");
     cudaStream_t st = gee::as_stream(stream);
     if (n == 0) return GEE_OK;
     GEE_REQUIRE(offsets && tile_row && z, GEE_ERR_INVALID, "NULL array argument");
@@ -515,38 +505,33 @@ int gee_embed_csr_pull_hot(const int64_t *offsets, const int32_t *targets, const
         GEE_CUDA(cudaMemsetAsync(z, 0, sizeof(float) * (size_t)n * k, st));
         return GEE_OK;
     }
-    GEE_REQUIRE(targets && labels && inv && slots, GEE_ERR_INVALID, "NULL array argument");
-    GEE_REQUIRE(gee::aligned16(targets) && (!w || gee::aligned16(w)), GEE_ERR_INVALID,
-                "targets/weights must be 16-byte aligned");
+    GEE_REQUIRE(targets && table && inv && slots, GEE_ERR_INVALID, "NULL array argument");
+    GEE_REQUIRE(gee::aligned16(targets) && (!w || gee::aligned16(w)) && gee::aligned16(table), GEE_ERR_INVALID,
+                "targets/weights/table must be 16-byte aligned");
     {
         const int64_t n_tiles = gee_pull_tiles(arcs);
         k_zero_tail<<<gee::sm_count() * 2, 256, 0, st>>>(tile_row + n_tiles, n, k, z);
         int rc = gee::check_launch("k_zero_tail");
         if (rc) return rc;
     }
-    const gee::LabelFmt lf = gee::label_fmt(label_bits);
     auto *sl = reinterpret_cast<unsigned long long *>(slots);
-    if (k <= 255) {
-        const auto *h = static_cast<const uint8_t *>(hot_labels);
-        return w ? launch_pull<true, uint8_t>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, h, n_hot,
-                                              inv, k, z, sl, st)
-                 : launch_pull<false, uint8_t>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, h, n_hot,
-                                               inv, k, z, sl, st);
+    switch (gee_label_bytes(k)) {
+    case 1: {
+        const auto *t = static_cast<const uint8_t *>(table);
+        return w ? launch_pull<true, uint8_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st)
+                 : launch_pull<false, uint8_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st);
     }
-    const auto *h = static_cast<const uint16_t *>(hot_labels);
-    return w ? launch_pull<true, uint16_t>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, h, n_hot, inv,
-                                           k, z, sl, st)
-             : launch_pull<false, uint16_t>(offsets, targets, w, arcs, tile_row, scale_exp, labels, lf, h, n_hot, inv,
-                                            k, z, sl, st);
-}
-
-int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n,
-                       int64_t arcs, const int64_t *tile_row, int32_t scale_exp, const uint32_t *labels,
-                       int32_t label_bits, const double *inv, int32_t k, float *z, void *slots,
-                       void *stream)
-{
-    return gee_embed_csr_pull_hot(offsets, targets, w, n, arcs, tile_row, scale_exp, labels, label_bits, nullptr, 0,
-                                  inv, k, z, slots, stream);
+    case 2: {
+        const auto *t = static_cast<const uint16_t *>(table);
+        return w ? launch_pull<true, uint16_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st)
+                 : launch_pull<false, uint16_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st);
+    }
+    default: {
+        const auto *t = static_cast<const int32_t *>(table);
+        return w ? launch_pull<true, int32_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st)
+                 : launch_pull<false, int32_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st);
+    }
+    }
 }
 
 }  // extern "C"

@@ -11,8 +11,8 @@
 // The scatter is fp32 red.global.add (REDG.E.ADD.F32.FTZ.RN), the B200
 // equivalent of the reference's CAS-loop f64 atomic add (_kernels.py:92-106).
 // Edges stream in with 128-bit loads (4 edges per thread-iteration); labels
-// are bit-packed gathers (gee_common.cuh LabelFmt) kept in L2 with an
-// evict_last policy; inv[K+1] lives in shared memory.
+// are u8/u16 gathers from the label table (gee_common.cuh) kept in L2 with
+// an evict_last policy; inv[K+1] lives in shared memory.
 #include <cooperative_groups.h>
 #include <cooperative_groups/reduce.h>
 
@@ -40,10 +40,10 @@ __device__ __forceinline__ void scatter(float *z, int64_t idx, float val, bool a
     }
 }
 
-template <bool WEIGHTED, bool SRC_ONLY, bool VEC, bool PRECOMBINE>
+template <typename LT, bool WEIGHTED, bool SRC_ONLY, bool VEC, bool PRECOMBINE>
 __global__ void __launch_bounds__(PUSH_THREADS)
 k_push(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
-       const float *__restrict__ w, int64_t s, const uint32_t *__restrict__ labels, gee::LabelFmt lf,
+       const float *__restrict__ w, int64_t s, const LT *__restrict__ labels,
        const float *__restrict__ inv, int32_t k, float *__restrict__ z, bool inv_smem)
 {
     const uint64_t pol = gee::policy_evict_last();
@@ -55,8 +55,8 @@ k_push(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
     const float *tab = inv_smem ? sinv : inv;
 
     auto edge = [&](int32_t u, int32_t v, float wt, bool valid) {
-        uint32_t yv = valid ? gee::gather_label(labels, (uint32_t)v, lf, pol) : 0u;
-        uint32_t yu = (valid && !SRC_ONLY) ? gee::gather_label(labels, (uint32_t)u, lf, pol) : 0u;
+        uint32_t yv = valid ? gee::ld_label<LT>(labels + v, pol) : 0u;
+        uint32_t yu = (valid && !SRC_ONLY) ? gee::ld_label<LT>(labels + u, pol) : 0u;
         if (yv > (uint32_t)k) yv = 0;  // raw int32 labels: drop out-of-range
         if (yu > (uint32_t)k) yu = 0;
         float dv = yv ? tab[yv] * wt : 0.f;
@@ -101,9 +101,9 @@ k_push(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
     }
 }
 
-template <bool WEIGHTED, bool SRC_ONLY, bool VEC, bool PRE>
-int launch_push4(const int32_t *src, const int32_t *dst, const float *w, int64_t s, const uint32_t *labels,
-                 gee::LabelFmt lf, const float *inv, int32_t k, float *z, cudaStream_t st)
+template <typename LT, bool WEIGHTED, bool SRC_ONLY, bool VEC, bool PRE>
+int launch_push4(const int32_t *src, const int32_t *dst, const float *w, int64_t s, const void *labels,
+                 const float *inv, int32_t k, float *z, cudaStream_t st)
 {
     bool inv_smem = (size_t)(k + 1) * sizeof(float) <= 48 * 1024;
     size_t sh = inv_smem ? (size_t)(k + 1) * sizeof(float) : 0;
@@ -111,46 +111,61 @@ int launch_push4(const int32_t *src, const int32_t *dst, const float *w, int64_t
     int64_t want = (s + PUSH_THREADS * per - 1) / (PUSH_THREADS * per);
     int64_t cap = (int64_t)gee::sm_count() * 8;  // 8 resident CTAs of 256 per SM
     int grid = (int)(want < 1 ? 1 : (want > cap ? cap : want));
-    k_push<WEIGHTED, SRC_ONLY, VEC, PRE><<<grid, PUSH_THREADS, sh, st>>>(src, dst, w, s, labels, lf, inv, k, z,
-                                                                       inv_smem);
+    k_push<LT, WEIGHTED, SRC_ONLY, VEC, PRE><<<grid, PUSH_THREADS, sh, st>>>(
+        src, dst, w, s, static_cast<const LT *>(labels), inv, k, z, inv_smem);
     return gee::check_launch("k_push");
 }
 
-template <bool WEIGHTED, bool SRC_ONLY>
+template <typename LT, bool WEIGHTED, bool SRC_ONLY>
 int launch_push3(bool vec, bool pre, const int32_t *src, const int32_t *dst, const float *w, int64_t s,
-                 const uint32_t *labels, gee::LabelFmt lf, const float *inv, int32_t k, float *z, cudaStream_t st)
+                 const void *labels, const float *inv, int32_t k, float *z, cudaStream_t st)
 {
     if (vec)
-        return pre ? launch_push4<WEIGHTED, SRC_ONLY, true, true>(src, dst, w, s, labels, lf, inv, k, z, st)
-                   : launch_push4<WEIGHTED, SRC_ONLY, true, false>(src, dst, w, s, labels, lf, inv, k, z, st);
-    return pre ? launch_push4<WEIGHTED, SRC_ONLY, false, true>(src, dst, w, s, labels, lf, inv, k, z, st)
-               : launch_push4<WEIGHTED, SRC_ONLY, false, false>(src, dst, w, s, labels, lf, inv, k, z, st);
+        return pre ? launch_push4<LT, WEIGHTED, SRC_ONLY, true, true>(src, dst, w, s, labels, inv, k, z, st)
+                   : launch_push4<LT, WEIGHTED, SRC_ONLY, true, false>(src, dst, w, s, labels, inv, k, z, st);
+    return pre ? launch_push4<LT, WEIGHTED, SRC_ONLY, false, true>(src, dst, w, s, labels, inv, k, z, st)
+               : launch_push4<LT, WEIGHTED, SRC_ONLY, false, false>(src, dst, w, s, labels, inv, k, z, st);
+}
+
+template <typename LT>
+int launch_push2(bool weighted, bool src_only, bool vec, bool pre, const int32_t *src, const int32_t *dst,
+                 const float *w, int64_t s, const void *labels, const float *inv, int32_t k, float *z,
+                 cudaStream_t st)
+{
+    if (weighted)
+        return src_only ? launch_push3<LT, true, true>(vec, pre, src, dst, w, s, labels, inv, k, z, st)
+                        : launch_push3<LT, true, false>(vec, pre, src, dst, w, s, labels, inv, k, z, st);
+    return src_only ? launch_push3<LT, false, true>(vec, pre, src, dst, w, s, labels, inv, k, z, st)
+                    : launch_push3<LT, false, false>(vec, pre, src, dst, w, s, labels, inv, k, z, st);
 }
 
 }  // namespace
 
 extern "C" int gee_embed_coo(const int32_t *src, const int32_t *dst, const float *w, int64_t s,
-                             const uint32_t *labels, int32_t label_bits, const float *inv,
-                             int64_t n, int32_t k, float *z, uint32_t flags, void *stream)
+                             const void *table, int64_t label_off, const float *inv, int64_t n, int32_t k,
+                             float *z, uint32_t flags, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1, GEE_ERR_INVALID, "class count k must be positive (got %d)", k);
-    GEE_REQUIRE(n >= 0 && s >= 0, GEE_ERR_INVALID, "n and s must be nonnegative");
-    GEE_REQUIRE(label_bits == 32 || label_bits == gee_label_bits(k), GEE_ERR_INVALID,
-                "label_bits must be 32 (raw int32) or gee_label_bits(k)=%d (got %d)", gee_label_bits(k), label_bits);
+    GEE_REQUIRE(n >= 0 && s >= 0 && label_off >= 0, GEE_ERR_INVALID, "n, s and label_off must be nonnegative");
     cudaStream_t st = gee::as_stream(stream);
     if (flags & GEE_ZERO_Z) {
         if (n > 0) GEE_CUDA(cudaMemsetAsync(z, 0, sizeof(float) * (size_t)n * (size_t)k, st));
     }
     if (s == 0 || n == 0) return GEE_OK;
-    GEE_REQUIRE(src && dst && labels && inv && z, GEE_ERR_INVALID, "NULL array argument");
-    bool vec = gee::aligned16(src) && gee::aligned16(dst) && (!w || gee::aligned16(w));
-    bool src_only = (flags & GEE_SOURCE_ONLY) != 0;
-    bool pre = (flags & GEE_PRECOMBINE) != 0;
-    const gee::LabelFmt lf = gee::label_fmt(label_bits);
-    if (w)
-        return src_only ? launch_push3<true, true>(vec, pre, src, dst, w, s, labels, lf, inv, k, z, st)
-                        : launch_push3<true, false>(vec, pre, src, dst, w, s, labels, lf, inv, k, z, st);
-    return src_only ? launch_push3<false, true>(vec, pre, src, dst, w, s, labels, lf, inv, k, z, st)
-                    : launch_push3<false, false>(vec, pre, src, dst, w, s, labels, lf, inv, k, z, st);
+    GEE_REQUIRE(src && dst && table && inv && z, GEE_ERR_INVALID, "NULL array argument");
+    const bool vec = gee::aligned16(src) && gee::aligned16(dst) && (!w || gee::aligned16(w));
+    const bool src_only = (flags & GEE_SOURCE_ONLY) != 0;
+    const bool pre = (flags & GEE_PRECOMBINE) != 0;
+    switch (gee_label_bytes(k)) {
+    case 1:
+        return launch_push2<uint8_t>(w != nullptr, src_only, vec, pre, src, dst, w, s,
+                                     static_cast<const uint8_t *>(table) + label_off, inv, k, z, st);
+    case 2:
+        return launch_push2<uint16_t>(w != nullptr, src_only, vec, pre, src, dst, w, s,
+                                      static_cast<const uint16_t *>(table) + label_off, inv, k, z, st);
+    default:
+        return launch_push2<int32_t>(w != nullptr, src_only, vec, pre, src, dst, w, s,
+                                     static_cast<const int32_t *>(table) + label_off, inv, k, z, st);
+    }
 }

@@ -145,7 +145,7 @@ class DeviceGraph:
     # Hot-label tier (csrc/gee_hot.cu): worth it when the packed label array
     # outgrows what L2 keeps resident under random access and degrees are
     # skewed (R-MAT); ER graphs end up with few or no hot vertices.
-    HOT_MIN_PACKED_BYTES = 16 << 20
+    HOT_MIN_TABLE_BYTES = 16 << 20
     HOT_MAX = 16 << 20
 
     def prepare_hot(self, k, enable=None):
@@ -154,10 +154,9 @@ class DeviceGraph:
             return
         if self.hot_k is not None:
             raise ValidationError("hot tier already planned for a different k")
-        bits = int(lib.gee_label_bits(k))
-        packed_bytes = int(lib.gee_label_words(self.n_nodes, bits)) * 4
+        table_bytes = int(lib.gee_label_table_bytes(self.n_nodes, 0, k))
         if enable is None:
-            enable = packed_bytes > self.HOT_MIN_PACKED_BYTES and k <= 65535 and self.n == self.n_nodes
+            enable = table_bytes > self.HOT_MIN_TABLE_BYTES and k <= 65535 and self.n == self.n_nodes
         self.hot_k = k
         if not enable or self.arcs == 0:
             return
@@ -167,14 +166,15 @@ class DeviceGraph:
         n = self.n_nodes
         self.hot_rank = torch.empty(n, dtype=torch.int32, device=self.device)
         nh = ctypes.c_int64()
-        max_hot = min(n, self.HOT_MAX // int(lib.gee_hot_label_bytes(k)))
+        max_hot = min(n, self.HOT_MAX // int(lib.gee_label_bytes(k)))
         check(lib.gee_hot_plan(ptr(self.offsets), n, max_hot, 2, ptr(self.hot_rank), None, ctypes.byref(nh),
                                _stream()), "gee_hot_plan")
         self.n_hot = int(nh.value)
         if self.n_hot == 0:
             self.hot_rank = None
             return
-        check(lib.gee_hot_encode(ptr(self.targets), self.arcs, ptr(self.hot_rank), _stream()), "gee_hot_encode")
+        check(lib.gee_hot_encode(ptr(self.targets), self.arcs, ptr(self.hot_rank), self.n_hot, _stream()),
+              "gee_hot_encode")
 
     @property
     def arcs(self):
@@ -206,8 +206,8 @@ PULL_REL_ERR_MAX = 1e-5
 
 
 class Embedder:
-    """Reusable device state for one (n, k): projection buffers, compact
-    labels and the pull slot buffer.  `project` + `pull`/`push` is one edge
+    """Reusable device state for one (n, k): projection buffers, the label
+    table and the pull slot buffer.  `project` + `pull`/`push` is one edge
     pass; nothing is allocated on those calls once warm."""
 
     def __init__(self, n, k, device=None):
@@ -220,31 +220,28 @@ class Embedder:
         self.inv32 = torch.zeros(self.k + 1, dtype=torch.float32, device=dev)
         self.inv64 = torch.zeros(self.k + 1, dtype=torch.float64, device=dev)
         self.bad = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.label_bits = int(lib.gee_label_bits(self.k))
-        words = int(lib.gee_label_words(self.n, self.label_bits))
-        self.packed = torch.empty(max(words, 1), dtype=torch.int32, device=dev)
+        self.table = None
+        self.table_n_hot = None  # n_hot the current table was built with
         self.slots = None
-        self.hot_labels = None
-        self._hot_for = None
+
+    def _ensure_table(self, n_hot):
+        need = int(lib.gee_label_table_bytes(self.n, n_hot, self.k))
+        if self.table is None or self.table.numel() < need:
+            self.table = torch.empty(need, dtype=torch.uint8, device=self.device)
 
     # ------------------------------------------------------------------ K1
     def project(self, labels_d, validate=True, g=None):
-        """Histogram + inv + packed labels (build_projection); with a graph
-        that has a hot tier, also its rank-ordered hot label table."""
+        """Histogram + inv + label table (build_projection).  With a graph
+        whose pull layout has a hot tier, the table carries its hot prefix."""
         if labels_d.numel() != self.n:
             raise ValidationError(f"graph has {self.n} nodes but labels have {labels_d.numel()}")
-        hot_rank = None
-        if g is not None and g.hot_rank is not None:
-            hb = int(lib.gee_hot_label_bytes(self.k))
-            need = (g.n_hot * hb + 15) // 16 * 16
-            if self.hot_labels is None or self.hot_labels.numel() < need:
-                self.hot_labels = torch.zeros(need, dtype=torch.uint8, device=self.device)
-            hot_rank = g.hot_rank
-        check(lib.gee_build_projection_hot(ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.inv32),
-                                           ptr(self.inv64), ptr(self.packed), ptr(self.bad), ptr(hot_rank),
-                                           ptr(self.hot_labels) if hot_rank is not None else None, _stream()),
-              "gee_build_projection")
-        self._hot_for = g if hot_rank is not None else None
+        hot_rank = g.hot_rank if (g is not None and g.hot_rank is not None) else None
+        n_hot = g.n_hot if hot_rank is not None else 0
+        self._ensure_table(n_hot)
+        check(lib.gee_build_projection(ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.inv32),
+                                       ptr(self.inv64), ptr(self.table), ptr(hot_rank), n_hot, ptr(self.bad),
+                                       _stream()), "gee_build_projection")
+        self.table_n_hot = n_hot
         if validate and int(self.bad.item()):
             raise ValidationError(f"{int(self.bad.item())} labels outside [0, {self.k}]")
         return self.counts
@@ -262,23 +259,21 @@ class Embedder:
         if not g.has_pull:
             raise ValidationError("graph has no pull (symmetric CSR) layout")
         if g.n_nodes != self.n:
-            raise ValidationError(f"graph has {g.n} nodes but labels have {self.n}")
+            raise ValidationError(f"graph has {g.n_nodes} nodes but labels have {self.n}")
         if g.weighted and g.rel_err > PULL_REL_ERR_MAX:
             raise ValidationError(
                 f"weights span too wide a range for the exact fixed-point pull "
                 f"(rounding bound {g.rel_err:.2e}); use variant='push'")
         if g.hot_k != self.k:
-            raise ValidationError("call Embedder.project(labels, g=graph) (or graph.prepare_hot(k)) first")
-        if g.hot_rank is not None and (self.hot_labels is None or self._hot_for is not g):
-            raise ValidationError("hot label table not built for this graph: call project(labels, g=graph)")
+            raise ValidationError("call graph.prepare_hot(k) before the pull (Embedder.embed does)")
+        if self.table_n_hot != g.n_hot:
+            raise ValidationError("label table does not match the graph's hot tier: call project(labels, g=graph)")
         if z is None:
             z = torch.empty((g.n, self.k), dtype=torch.float32, device=self.device)
         self._ensure_slots(g.arcs)
-        check(lib.gee_embed_csr_pull_hot(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
-                                         ptr(g.tile_row), g.scale_exp, ptr(self.packed), self.label_bits,
-                                         ptr(self.hot_labels) if g.n_hot else None, g.n_hot, ptr(self.inv64),
-                                         self.k, ptr(z), ptr(self.slots), _stream()),
-              "gee_embed_csr_pull")
+        check(lib.gee_embed_csr_pull(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
+                                     ptr(g.tile_row), g.scale_exp, ptr(self.table), g.n_hot, ptr(self.inv64),
+                                     self.k, ptr(z), ptr(self.slots), _stream()), "gee_embed_csr_pull")
         return z
 
     # ------------------------------------------------------------------ K3
@@ -286,13 +281,15 @@ class Embedder:
         if not g.has_push:
             raise ValidationError("graph has no push (COO) layout")
         if g.n_nodes != self.n:
-            raise ValidationError(f"graph has {g.n} nodes but labels have {self.n}")
+            raise ValidationError(f"graph has {g.n_nodes} nodes but labels have {self.n}")
+        if self.table_n_hot is None:
+            raise ValidationError("call project(labels) before the push")
         z = self.new_z() if z is None else z
         flags = (_lib.GEE_ZERO_Z if zero else 0) | (_lib.GEE_SOURCE_ONLY if g.coo_source_only else 0)
         if precombine:
             flags |= _lib.GEE_PRECOMBINE
-        check(lib.gee_embed_coo(ptr(g.src), ptr(g.dst), ptr(g.w), int(g.src.numel()), ptr(self.packed),
-                                self.label_bits, ptr(self.inv32), g.n, self.k, ptr(z), flags, _stream()),
+        check(lib.gee_embed_coo(ptr(g.src), ptr(g.dst), ptr(g.w), int(g.src.numel()), ptr(self.table),
+                                self.table_n_hot, ptr(self.inv32), g.n, self.k, ptr(z), flags, _stream()),
               "gee_embed_coo")
         return z
 

@@ -36,9 +36,8 @@ def test_library_exports_every_declared_symbol():
 def test_pure_functions_without_gpu():
     L = _lib.lib
     assert L.gee_version() >= 100
-    assert [L.gee_label_bits(k) for k in (1, 3, 5, 50, 63, 64, 100, 255, 256, 1000, 1023, 1024, 65535, 65536)] == \
-        [1, 2, 3, 6, 6, 8, 8, 8, 10, 10, 10, 16, 16, 32]
-    assert L.gee_label_words(134217728, 6) == 26843546 and L.gee_label_words(10, 32) == 10
+    assert [L.gee_label_bytes(k) for k in (1, 255, 256, 65535, 65536)] == [1, 1, 2, 2, 4]
+    assert L.gee_label_table_bytes(100, 0, 50) == 112 and L.gee_label_table_bytes(100, 20, 300) == 256
     T = _lib.TILE_ARCS
     assert L.gee_pull_tiles(0) == 0 and L.gee_pull_tiles(1) == 1 and L.gee_pull_tiles(T + 1) == 2
     assert L.gee_pull_slots_bytes(2 * T, 10) == 2 * 10 * 8
@@ -48,10 +47,10 @@ def test_pure_functions_without_gpu():
     assert L.gee_pull_scale_exp(2.0 ** 20, 0.5, ctypes.byref(e), ctypes.byref(rel)) == 0
     assert 2.0 ** 20 * 2.0 ** e.value < 2.0 ** 62
     # argument validation happens before any CUDA call
-    assert L.gee_build_projection(None, 10, 0, None, None, None, None, None, None, None) == _lib.GEE_ERR_INVALID
+    assert L.gee_build_projection(None, 10, 0, None, None, None, None, None, 0, None, None) == _lib.GEE_ERR_INVALID
     assert b"positive" in L.gee_last_error()
     with pytest.raises(ValidationError):
-        _lib.check(L.gee_embed_coo(None, None, None, 1, None, 7, None, 1, 5, None, 0, None))
+        _lib.check(L.gee_embed_coo(None, None, None, 1, None, -1, None, 1, 5, None, 0, None))
 
 
 def test_synth_word_matches_numpy_restatement():
