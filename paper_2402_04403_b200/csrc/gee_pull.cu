@@ -42,7 +42,7 @@ constexpr int PT = 512;                  // threads per CTA (one persistent CTA 
 constexpr int APT = 8;                   // arcs per thread
 constexpr int TILE = PT * APT;           // 4096
 static_assert(TILE == GEE_TILE_ARCS, "tile size mismatch with header");
-constexpr int SMEM_BYTES = 227 * 1024;   // opt-in maximum per CTA on sm_100a
+constexpr int SMEM_BYTES_MAX = 227 * 1024;  // opt-in maximum per CTA on sm_100a (queried at launch)
 constexpr int OFF_MAX = 513;             // staged offsets per buffer (<= 512 rows)
 constexpr int WIN_BYTES_MAX = 120 * 1024;
 
@@ -401,7 +401,7 @@ struct PullShape {
     size_t smem;
 };
 
-PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes)
+PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes, size_t SMEM_BYTES)
 {
     PullShape p{0, 0, 0};
     const size_t fixed = pull_fixed_smem(k);
@@ -414,7 +414,7 @@ PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes)
     if (p.win_rows > OFF_MAX - 1) p.win_rows = OFF_MAX - 1;
     const size_t plane = (((size_t)p.win_rows * k + 3) & ~(size_t)3) * sizeof(uint32_t);
     const size_t used = fixed + plane * (weighted ? 2 : 1);
-    size_t hot_cap = (SMEM_BYTES - used) / (size_t)label_bytes;
+    size_t hot_cap = (SMEM_BYTES - used - 32) / (size_t)label_bytes;  // 32 B: rounding + the always-readable slot 0
     hot_cap &= ~(size_t)15;
     p.hot0 = (int)(n_hot < (int64_t)hot_cap ? n_hot : (int64_t)hot_cap);
     p.hot0 &= ~15;  // whole 16 B vectors; the rest of the hot tier is read through L2
@@ -428,10 +428,22 @@ int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, 
                 int32_t k, float *z, unsigned long long *slots, cudaStream_t st)
 {
     const int64_t n_tiles = gee_pull_tiles(arcs);
-    const PullShape ps = pull_shape(k, WEIGHTED, n_hot, (int)sizeof(LT));
+    static int optin = 0;
+    if (!optin) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
+            optin = 48 * 1024;
+    }
+    const size_t budget = (size_t)(optin < SMEM_BYTES_MAX ? optin : SMEM_BYTES_MAX);
+    const PullShape ps = pull_shape(k, WEIGHTED, n_hot, (int)sizeof(LT), budget);
     GEE_REQUIRE(ps.win_rows >= 1, GEE_ERR_INVALID, "k=%d too large for the pull window", k);
     auto kern = k_pull<WEIGHTED, LT>;
-    GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps.smem));
+    {
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps.smem);
+        GEE_REQUIRE(e == cudaSuccess, GEE_ERR_CUDA, "k_pull: %zu B dynamic smem (opt-in max %d, window %d rows, hot %d): %s",
+                    ps.smem, optin, ps.win_rows, ps.hot0, cudaGetErrorString(e));
+    }
     const int64_t cap = (int64_t)gee::sm_count();
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
     const float qscale = ldexpf(1.0f, scale_exp);
