@@ -38,13 +38,15 @@
 
 namespace {
 
-constexpr int PT = 512;                  // threads per CTA (one persistent CTA per SM)
-constexpr int APT = 8;                   // arcs per thread
-constexpr int TILE = PT * APT;           // 4096
+constexpr int GROUPS = 2;                // independent tile pipelines per CTA
+constexpr int GT = 256;                  // threads per group (8 warps)
+constexpr int PT = GROUPS * GT;          // threads per CTA (one persistent CTA per SM)
+constexpr int APT = 16;                  // arcs per thread
+constexpr int TILE = GT * APT;           // 4096 arcs per tile
 static_assert(TILE == GEE_TILE_ARCS, "tile size mismatch with header");
 constexpr int SMEM_BYTES_MAX = 227 * 1024;  // opt-in maximum per CTA on sm_100a (queried at launch)
-constexpr int OFF_MAX = 513;             // staged offsets per buffer (<= 512 rows)
-constexpr int WIN_BYTES_MAX = 120 * 1024;
+constexpr int OFF_MAX = 513;             // staged offsets per buffer (<= 512 rows per window)
+constexpr int WIN_HOT_BYTES = 40 * 1024; // per-group window when a hot tier wants the smem
 
 __device__ __forceinline__ int64_t lower_bound_i64(const int64_t *__restrict__ a, int64_t lo,
                                                    int64_t hi, int64_t key)
@@ -79,94 +81,89 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
-struct TileArcs {  // stage A: streamed arcs of a tile
-    int32_t t[APT];
-    float w[APT];
-    int32_t r0, r1;  // tile_row[j], tile_row[j+1]
-};
-struct TileLabs {  // stage B: gathered labels of a tile
-    uint32_t l[APT];
-    float w[APT];
-    int32_t r0, r1;
+__device__ __forceinline__ void group_sync(int g) { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(GT)); }
+
+struct GroupSmem {  // per-group shared state (carved from dynamic smem)
+    int64_t *off64;  // 2 x OFF_MAX staged offsets (cp.async double buffer)
+    int32_t *ol;     // OFF_MAX + 3 tile-local clamped offsets of the window
+    uint16_t *nzr;   // OFF_MAX rank of each nonempty row, 0xffff for empty rows
+    int32_t *wtot;   // 8 warp totals (+ 8 scratch)
+    uint32_t *lo;    // wnz * k
+    uint32_t *hi;    // wnz * k (weighted)
 };
 
 template <bool WEIGHTED>
-__device__ __forceinline__ void load_arcs(TileArcs &A, int64_t j, int tid, const int32_t *__restrict__ targets,
-                                          const float *__restrict__ w, int64_t arcs,
-                                          const int64_t *__restrict__ tile_row, int32_t sentinel)
+__device__ __forceinline__ void load_arcs(int32_t (&t)[APT], float (&w)[APT], int64_t j, int gt,
+                                          const int32_t *__restrict__ targets, const float *__restrict__ wts,
+                                          int64_t arcs, int32_t sentinel)
 {
-    const int64_t e0 = j * (int64_t)TILE + (int64_t)tid * APT;
+    const int64_t e0 = j * (int64_t)TILE + (int64_t)gt * APT;
     if (e0 + APT <= arcs) {
-        const int4 t0 = __ldcs(reinterpret_cast<const int4 *>(targets + e0));
-        const int4 t1 = __ldcs(reinterpret_cast<const int4 *>(targets + e0 + 4));
-        A.t[0] = t0.x; A.t[1] = t0.y; A.t[2] = t0.z; A.t[3] = t0.w;
-        A.t[4] = t1.x; A.t[5] = t1.y; A.t[6] = t1.z; A.t[7] = t1.w;
-        if (WEIGHTED) {
-            const float4 w0 = __ldcs(reinterpret_cast<const float4 *>(w + e0));
-            const float4 w1 = __ldcs(reinterpret_cast<const float4 *>(w + e0 + 4));
-            A.w[0] = w0.x; A.w[1] = w0.y; A.w[2] = w0.z; A.w[3] = w0.w;
-            A.w[4] = w1.x; A.w[5] = w1.y; A.w[6] = w1.z; A.w[7] = w1.w;
+#pragma unroll
+        for (int v = 0; v < APT / 4; v++) {
+            const int4 t4 = __ldcs(reinterpret_cast<const int4 *>(targets + e0) + v);
+            t[4 * v] = t4.x; t[4 * v + 1] = t4.y; t[4 * v + 2] = t4.z; t[4 * v + 3] = t4.w;
+            if (WEIGHTED) {
+                const float4 w4 = __ldcs(reinterpret_cast<const float4 *>(wts + e0) + v);
+                w[4 * v] = w4.x; w[4 * v + 1] = w4.y; w[4 * v + 2] = w4.z; w[4 * v + 3] = w4.w;
+            }
         }
     } else {  // last tile: padding arcs read the sentinel slot (label 0)
 #pragma unroll
         for (int i = 0; i < APT; i++) {
             const bool ok = e0 + i < arcs;
-            A.t[i] = ok ? __ldcs(targets + e0 + i) : sentinel;
-            if (WEIGHTED) A.w[i] = ok ? __ldcs(w + e0 + i) : 0.f;
+            t[i] = ok ? __ldcs(targets + e0 + i) : sentinel;
+            if (WEIGHTED) w[i] = ok ? __ldcs(wts + e0 + i) : 0.f;
         }
     }
-    A.r0 = (int32_t)tile_row[j];
-    A.r1 = (int32_t)tile_row[j + 1];
 }
 
-// Labels of this thread's arcs: slots below hot0 from shared memory, the
-// rest through L2 (one predicated load each; all APT in flight).
-template <bool WEIGHTED, typename LT>
-__device__ __forceinline__ void gather_labs(TileLabs &B, const TileArcs &A, const LT *__restrict__ table,
-                                            const LT *__restrict__ hot_s, uint32_t hot0, uint64_t pol)
-{
-#pragma unroll
-    for (int i = 0; i < APT; i++) {
-        const uint32_t t = (uint32_t)A.t[i];
-        const bool in_smem = t < hot0;
-        uint32_t lab = (uint32_t)hot_s[in_smem ? t : 0u];
-        if (!in_smem) lab = gee::ld_label<LT>(table + t, pol);
-        B.l[i] = lab;
-        if (WEIGHTED) B.w[i] = A.w[i];
-    }
-    B.r0 = A.r0;
-    B.r1 = A.r1;
-}
-
-// Stage offsets[start .. start+cnt) into smem with cp.async (one 8 B copy per thread).
+// Stage offsets[start .. start+cnt) into smem with cp.async (8 B per copy).
 __device__ __forceinline__ void stage_offsets(int64_t *buf, const int64_t *__restrict__ offsets, int32_t r0,
-                                              int32_t r1, int tid)
+                                              int32_t r1, int gt)
 {
     const int32_t start = r0 > 0 ? r0 - 1 : 0;
     const int32_t cnt = min(r1 - start + 1, OFF_MAX);
-    for (int i = tid; i < cnt; i += PT) cp_async8(buf + i, offsets + start + i);
+    for (int i = gt; i < cnt; i += GT) cp_async8(buf + i, offsets + start + i);
 }
 
 template <bool WEIGHTED, typename LT>
 __global__ void __launch_bounds__(PT, 1)
 k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
-       const float *__restrict__ w, int64_t arcs, const int64_t *__restrict__ tile_row, int64_t n_tiles,
+       const float *__restrict__ wts, int64_t arcs, const int64_t *__restrict__ tile_row, int64_t n_tiles,
        float qscale, double dscale, const LT *__restrict__ table, int32_t sentinel, int32_t hot0,
        const double *__restrict__ inv, int32_t k, float *__restrict__ z, unsigned long long *__restrict__ slots,
-       int win_rows)
+       int wnz)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    int64_t *off_buf = reinterpret_cast<int64_t *>(smem_raw);          // 2 x OFF_MAX int64
-    int32_t *ol = reinterpret_cast<int32_t *>(off_buf + 2 * OFF_MAX);  // OFF_MAX (+3) tile-local int32
-    float *sc = reinterpret_cast<float *>(ol + OFF_MAX + 3);           // k+1 output scales
-    uint32_t *acc_lo = reinterpret_cast<uint32_t *>(sc + ((k + 4) & ~3));
-    const size_t plane = ((size_t)win_rows * k + 3) & ~(size_t)3;      // 16 B aligned planes
-    uint32_t *acc_hi = acc_lo + plane;                                 // weighted only
-    LT *hot_s = reinterpret_cast<LT *>(acc_lo + plane * (WEIGHTED ? 2 : 1));
-
     const int tid = threadIdx.x;
-    const int lane = tid & 31;
+    const int g = tid / GT, gt = tid % GT;
+    const int lane = tid & 31, gw = gt >> 5;  // warp within the group
     const int kk = k;
+    // ---- carve shared memory
+    unsigned char *p = smem_raw;
+    float *sc = reinterpret_cast<float *>(p);
+    p += ((size_t)(kk + 4) & ~(size_t)3) * sizeof(float);
+    const size_t plane = ((size_t)wnz * kk + 3) & ~(size_t)3;
+    GroupSmem G;
+    for (int q = 0; q < GROUPS; q++) {
+        GroupSmem s;
+        s.off64 = reinterpret_cast<int64_t *>(p);
+        p += 2 * OFF_MAX * sizeof(int64_t);
+        s.ol = reinterpret_cast<int32_t *>(p);
+        p += (OFF_MAX + 3) * sizeof(int32_t);
+        s.nzr = reinterpret_cast<uint16_t *>(p);
+        p += ((OFF_MAX + 7) & ~7) * sizeof(uint16_t);
+        s.wtot = reinterpret_cast<int32_t *>(p);
+        p += 16 * sizeof(int32_t);
+        s.lo = reinterpret_cast<uint32_t *>(p);
+        p += plane * sizeof(uint32_t);
+        s.hi = reinterpret_cast<uint32_t *>(p);
+        if (WEIGHTED) p += plane * sizeof(uint32_t);
+        if (q == g) G = s;
+    }
+    LT *hot_s = reinterpret_cast<LT *>(p);
+
     const uint64_t pol = gee::policy_evict_last();
     // Z[x, c] = sum * sc[c+1]: inv folded with the fixed-point scale, fp32.
     for (int c = tid; c <= kk; c += PT) sc[c] = (float)(inv[c] * dscale);
@@ -176,111 +173,147 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         uint4 *dst = reinterpret_cast<uint4 *>(hot_s);
         for (int i = tid; i < vec; i += PT) dst[i] = __ldg(src + i);
     }
-    __syncthreads();
+    __syncthreads();  // the only CTA-wide barrier: groups run independently after this
 
-    const int64_t G = gridDim.x;
-    int64_t jA = blockIdx.x;
-    if (jA >= n_tiles) return;
-    TileArcs A;
-    TileLabs B;
-    // prologue: tile j0 gathered + offsets staged, tile j0+G arcs in flight
-    load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row, sentinel);
-    gather_labs<WEIGHTED, LT>(B, A, table, hot_s, (uint32_t)hot0, pol);
-    stage_offsets(off_buf, offsets, B.r0, B.r1, tid);
+    const int64_t stride = (int64_t)gridDim.x * GROUPS;
+    int64_t j = (int64_t)blockIdx.x * GROUPS + g;
+    if (j >= n_tiles) return;
+
+    // prologue: this tile's arcs + staged offsets
+    int32_t tn[APT];
+    float wn[APT];
+    load_arcs<WEIGHTED>(tn, wn, j, gt, targets, wts, arcs, sentinel);
+    int32_t R0 = (int32_t)tile_row[j], R1 = (int32_t)tile_row[j + 1];
+    stage_offsets(G.off64, offsets, R0, R1, gt);
     cp_async_commit();
-    jA += G;
-    if (jA < n_tiles) load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row, sentinel);
     int buf = 0;
-    const int el0 = tid * APT;  // this thread's first arc, tile-local
 
-    for (int64_t j = blockIdx.x; j < n_tiles; j += G) {
+    for (; j < n_tiles; j += stride) {
+        // ---- gather this tile's labels (their latency overlaps the row setup)
         uint32_t lab[APT];
         float wcur[APT];
 #pragma unroll
         for (int i = 0; i < APT; i++) {
-            lab[i] = B.l[i];
-            if (WEIGHTED) wcur[i] = B.w[i];
+            const uint32_t t = (uint32_t)tn[i];
+            const bool in_smem = t < (uint32_t)hot0;
+            uint32_t l = (uint32_t)hot_s[in_smem ? t : 0u];
+            if (!in_smem) l = gee::ld_label<LT>(table + t, pol);
+            lab[i] = l;
+            if (WEIGHTED) wcur[i] = wn[i];
         }
-        const int32_t R0 = B.r0, R1 = B.r1;
-        // advance the pipeline: gather tile j+G, stage its offsets, load tile j+2G
-        if (jA < n_tiles) {
-            gather_labs<WEIGHTED, LT>(B, A, table, hot_s, (uint32_t)hot0, pol);
-            stage_offsets(off_buf + (buf ^ 1) * OFF_MAX, offsets, B.r0, B.r1, tid);
+        // ---- prefetch the next tile's arcs (registers) and row range
+        const int64_t jn = j + stride;
+        int32_t R0n = 0, R1n = 0;
+        if (jn < n_tiles) {
+            load_arcs<WEIGHTED>(tn, wn, jn, gt, targets, wts, arcs, sentinel);
+            R0n = (int32_t)tile_row[jn];
+            R1n = (int32_t)tile_row[jn + 1];
         }
-        cp_async_commit();
-        jA += G;
-        if (jA < n_tiles) load_arcs<WEIGHTED>(A, jA, tid, targets, w, arcs, tile_row, sentinel);
-        cp_async_wait<1>();  // tile j's staged offsets have landed (tile j+G's may be in flight)
 
-        // ---- process tile j
         const int64_t a0 = j * (int64_t)TILE;
         const int tlen = (int)min((int64_t)TILE, arcs - a0);
-        const int64_t *off_s = off_buf + buf * OFF_MAX;
+        const int el0 = gt * APT;  // this thread's first arc, tile-local
+        int64_t *off_s = G.off64 + buf * OFF_MAX;
         const int32_t st0 = R0 > 0 ? R0 - 1 : 0;  // first staged row
-        int32_t scnt = min(R1 - st0 + 1, OFF_MAX);
-        __syncthreads();  // staged offsets visible; previous tile's smem reads done
-        // has_head: offsets[R0] > a0; tail_cut: offsets[R1] > a1 (read before ol is rewritten)
+        const int32_t scnt = min(R1 - st0 + 1, OFF_MAX);
+        cp_async_wait<0>();
+        group_sync(g);  // staged offsets visible; this group's previous tile fully written out
         const bool has_head = off_s[R0 - st0] > a0;  // also when R0 == n (offsets[n] = arcs > a0)
         const int64_t offR1 = (R1 - st0 < scnt) ? off_s[R1 - st0] : __ldcs(offsets + R1);
         const bool tail_cut = (R1 > R0) && (offR1 > a0 + tlen);
         const int32_t base = has_head ? R0 - 1 : R0;
         const int32_t rows_total = R1 - base;
-        int32_t ost = st0;  // row of ol[0]
 
-        for (int32_t wo = 0; wo < rows_total; wo += win_rows) {
-            const int nr = min(win_rows, rows_total - wo);
-            const int32_t wrow0 = base + wo;
-            const int words = nr * kk;
-            if (wo > 0) __syncthreads();  // previous window's write-out done
-            if (wrow0 - ost + nr < scnt && wo == 0) {
-                // tile-local int32 offsets, clamped to [0, TILE+1]
-                for (int i = tid; i < scnt; i += PT) {
-                    const int64_t v = off_s[i] - a0;
-                    ol[i] = (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
+        int32_t wrow0 = base;
+        bool first = true;
+        while (wrow0 < R1) {
+            // ---- window rows [wrow0, wrow0 + nr): tile-local int32 offsets
+            int nr = min(OFF_MAX - 1, R1 - wrow0);
+            if (first && wrow0 - st0 + nr < scnt) {
+                const int sh = wrow0 - st0;
+                for (int i = gt; i <= nr; i += GT) {
+                    const int64_t v = off_s[sh + i] - a0;
+                    G.ol[i] = (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
                 }
             } else {
-                // window not fully staged (large tiles): load it directly
-                for (int i = tid; i <= nr; i += PT) {
+                if (!first) group_sync(g);  // previous window fully consumed
+                for (int i = gt; i <= nr; i += GT) {
                     const int64_t v = __ldcs(offsets + wrow0 + i) - a0;
-                    ol[i] = (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
+                    G.ol[i] = (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
                 }
-                ost = wrow0;
-                scnt = nr + 1;
             }
-            {  // zero the window
-                uint4 *a4 = reinterpret_cast<uint4 *>(acc_lo);
-                const int w4 = (words + 3) >> 2;
+            group_sync(g);
+            // ---- ranks of nonempty rows (2 rows per thread, warp scan + group scan)
+            int f0 = 0, f1 = 0;
+            {
+                const int r = 2 * gt;
+                if (r < nr) f0 = G.ol[r + 1] > G.ol[r];
+                if (r + 1 < nr) f1 = G.ol[r + 2] > G.ol[r + 1];
+            }
+            int incl = f0 + f1;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            if (lane == 31) G.wtot[gw] = incl;
+            group_sync(g);
+            int wpre = 0, nnz = 0;
+#pragma unroll
+            for (int q = 0; q < GT / 32; q++) {
+                const int v = G.wtot[q];
+                wpre += q < gw ? v : 0;
+                nnz += v;
+            }
+            const int r0rank = wpre + incl - f0 - f1;  // rank of row 2*gt if nonempty
+            if (nnz > wnz) {
+                // shrink the window to the first wnz nonempty rows: find the row of rank wnz
+                if (f0 && r0rank == wnz) G.wtot[8] = 2 * gt;
+                if (f1 && r0rank + f0 == wnz) G.wtot[8] = 2 * gt + 1;
+            }
+            {
+                const int r = 2 * gt;
+                if (r < nr) G.nzr[r] = f0 ? (uint16_t)r0rank : (uint16_t)0xffff;
+                if (r + 1 < nr) G.nzr[r + 1] = f1 ? (uint16_t)(r0rank + f0) : (uint16_t)0xffff;
+            }
+            group_sync(g);
+            if (nnz > wnz) {
+                nr = G.wtot[8];  // rows [0, nr) hold exactly wnz nonempty rows
+                nnz = wnz;
+            }
+            {  // zero the compact window
+                uint4 *a4 = reinterpret_cast<uint4 *>(G.lo);
+                const int w4 = (nnz * kk + 3) >> 2;
                 const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-                for (int i = tid; i < w4; i += PT) a4[i] = zero4;
+                for (int i = gt; i < w4; i += GT) a4[i] = zero4;
                 if (WEIGHTED) {
-                    uint4 *h4 = reinterpret_cast<uint4 *>(acc_hi);
-                    for (int i = tid; i < w4; i += PT) h4[i] = zero4;
+                    uint4 *h4 = reinterpret_cast<uint4 *>(G.hi);
+                    for (int i = gt; i < w4; i += GT) h4[i] = zero4;
                 }
             }
-            __syncthreads();
-            const int32_t *ow = ol + (wrow0 - ost);  // ow[r] = offsets[wrow0 + r] - a0 (clamped)
+            group_sync(g);
+            // ---- accumulate this thread's arcs of the window
+            const int32_t *ow = G.ol;
             const int wa0 = ow[0], wa1 = min(ow[nr], tlen);
             const int m0 = max(el0, wa0), m1 = min(el0 + APT, wa1);
-            // Row of the warp's first arc: two 32-way ballots.
-            const int ew = max(el0 - lane * APT, wa0);
+            const int ew = max(el0 - lane * APT, wa0);  // the warp's first arc in the window
             int rw = 0;
-            if (ew < wa1) {  // warp-uniform
+            if (ew < wa1) {  // warp-uniform: bracket the warp's first arc with two 32-way ballots
                 const int step = (nr + 31) >> 5;  // <= 16
                 int cand = min(lane * step, nr);
                 unsigned bal = __ballot_sync(0xffffffffu, ow[cand] <= ew);
-                const int b = (31 - __clz(bal)) * step;  // ow[b] <= ew
+                const int b = (31 - __clz(bal)) * step;
                 cand = min(b + lane, nr);
                 bal = __ballot_sync(0xffffffffu, lane < step && ow[cand] <= ew);
                 rw = b + (31 - __clz(bal));
             }
             if (m0 < m1) {
-                // gallop from rw to the last r with ow[r] <= m0, then walk arcs
-                int lo = rw, g = 1;
-                while (lo + g < nr && ow[lo + g] <= m0) {
-                    lo += g;
-                    g <<= 1;
+                int lo = rw, gl = 1;  // gallop to the last r with ow[r] <= m0
+                while (lo + gl < nr && ow[lo + gl] <= m0) {
+                    lo += gl;
+                    gl <<= 1;
                 }
-                int hi = min(lo + g, nr);  // ow[lo] <= m0 < ow[hi]
+                int hi = min(lo + gl, nr);
                 while (hi - lo > 1) {
                     const int mid = (lo + hi) >> 1;
                     if (ow[mid] <= m0) lo = mid;
@@ -288,53 +321,79 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 }
                 int r = lo;
                 int next = ow[r + 1];
+                int slot = G.nzr[r];
 #pragma unroll
                 for (int i = 0; i < APT; i++) {
                     const int e = el0 + i;
                     if (e < m0 || e >= m1) continue;
-                    while (e >= next) next = ow[++r + 1];
+                    if (e >= next) {
+                        do next = ow[++r + 1];
+                        while (e >= next);
+                        slot = G.nzr[r];
+                    }
                     const uint32_t c = lab[i];
                     if (c == 0u || c > (uint32_t)kk) continue;  // unlabeled (or out-of-range raw label)
-                    const int idx = r * kk + (int)c - 1;
+                    const int idx = slot * kk + (int)c - 1;
                     if (WEIGHTED) {
                         const unsigned long long q = (unsigned long long)__float2ll_rn(wcur[i] * qscale);
                         const uint32_t lo32 = (uint32_t)q;
                         uint32_t hi32 = (uint32_t)(q >> 32);
-                        const uint32_t old = atomicAdd(&acc_lo[idx], lo32);
+                        const uint32_t old = atomicAdd(&G.lo[idx], lo32);
                         hi32 += (old + lo32 < old) ? 1u : 0u;  // carry out of the low plane
-                        if (hi32) atomicAdd(&acc_hi[idx], hi32);
+                        if (hi32) atomicAdd(&G.hi[idx], hi32);
                     } else {
-                        atomicAdd(&acc_lo[idx], 1u);
+                        atomicAdd(&G.lo[idx], 1u);
                     }
                 }
             }
-            __syncthreads();
+            // the next tile's offsets can be staged now (its buffer is free)
+            if (first && jn < n_tiles) stage_offsets(G.off64 + (buf ^ 1) * OFF_MAX, offsets, R0n, R1n, gt);
+            if (first) cp_async_commit();
+            group_sync(g);
 
-            // complete rows of this window -> Z (flat, coalesced, streaming stores)
+            // ---- write out complete rows of the window: one warp per row
             const int32_t fin_lo = max(wrow0, R0);  // a head row is partial
             const int32_t fin_hi = min(wrow0 + nr, tail_cut ? R1 - 1 : R1);
-            if (fin_hi > fin_lo) {
-                const int off = (fin_lo - wrow0) * kk;
-                const int total = (fin_hi - fin_lo) * kk;
-                float *zo = z + (int64_t)fin_lo * kk;
-                const uint32_t *plo = acc_lo + off;
-                const uint32_t *phi = acc_hi + off;
-                int c = tid % kk;
-                const int dc = PT % kk;
-                for (int e = tid; e < total; e += PT) {
-                    float v;
-                    if (WEIGHTED) v = (float)(long long)(((unsigned long long)phi[e] << 32) | plo[e]);
-                    else v = (float)plo[e];
-                    __stcs(zo + e, v * sc[c + 1]);
-                    c += dc;
-                    if (c >= kk) c -= kk;
+            for (int32_t row = fin_lo + gw; row < fin_hi; row += GT / 32) {
+                const int lr = row - wrow0;
+                const int slot = G.nzr[lr];
+                float *zr = z + (int64_t)row * kk;
+                if ((kk & 1) == 0) {
+                    float2 *z2 = reinterpret_cast<float2 *>(zr);
+                    for (int c2 = lane; c2 < (kk >> 1); c2 += 32) {
+                        float2 v = make_float2(0.f, 0.f);
+                        if (slot != 0xffff) {
+                            const int idx = slot * kk + 2 * c2;
+                            if (WEIGHTED) {
+                                v.x = (float)(long long)(((unsigned long long)G.hi[idx] << 32) | G.lo[idx]);
+                                v.y = (float)(long long)(((unsigned long long)G.hi[idx + 1] << 32) | G.lo[idx + 1]);
+                            } else {
+                                v.x = (float)G.lo[idx];
+                                v.y = (float)G.lo[idx + 1];
+                            }
+                            v.x *= sc[2 * c2 + 1];
+                            v.y *= sc[2 * c2 + 2];
+                        }
+                        __stcs(z2 + c2, v);
+                    }
+                } else {
+                    for (int c = lane; c < kk; c += 32) {
+                        float v = 0.f;
+                        if (slot != 0xffff) {
+                            const int idx = slot * kk + c;
+                            v = WEIGHTED ? (float)(long long)(((unsigned long long)G.hi[idx] << 32) | G.lo[idx])
+                                         : (float)G.lo[idx];
+                            v *= sc[c + 1];
+                        }
+                        __stcs(zr + c, v);
+                    }
                 }
             }
             // partial rows: the head (owned by an earlier tile) and a cut tail
             for (int part = 0; part < 2; part++) {
                 int32_t row;
                 if (part == 0) {
-                    if (!(has_head && wo == 0)) continue;
+                    if (!(has_head && first)) continue;
                     row = base;
                 } else {
                     if (!tail_cut) continue;
@@ -342,15 +401,20 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     if (row < wrow0 || row >= wrow0 + nr) continue;
                 }
                 const int64_t owner = part == 0 ? __ldg(offsets + row) / TILE : j;
-                const int lr = row - wrow0;
-                for (int c = tid; c < kk; c += PT) {
-                    const int idx = lr * kk + c;
+                const int slot = G.nzr[row - wrow0];
+                for (int c = gt; c < kk; c += GT) {
+                    const int idx = slot * kk + c;
                     const unsigned long long v =
-                        WEIGHTED ? (((unsigned long long)acc_hi[idx] << 32) | acc_lo[idx]) : (unsigned long long)acc_lo[idx];
+                        WEIGHTED ? (((unsigned long long)G.hi[idx] << 32) | G.lo[idx]) : (unsigned long long)G.lo[idx];
                     if (v) atomicAdd(&slots[owner * kk + c], v);
                 }
             }
+            wrow0 += nr;
+            first = false;
         }
+        (void)rows_total;
+        R0 = R0n;
+        R1 = R1n;
         buf ^= 1;
     }
     cp_async_wait<0>();
@@ -390,32 +454,34 @@ __global__ void k_zero_tail(const int64_t *__restrict__ first_row, int64_t n, in
         __stcs(zo + i, 0.f);
 }
 
-size_t pull_fixed_smem(int32_t k)
+size_t group_fixed_smem()
 {
-    return 2 * OFF_MAX * sizeof(int64_t) + (OFF_MAX + 3) * sizeof(int32_t) + (size_t)((k + 4) & ~3) * sizeof(float);
+    return 2 * OFF_MAX * sizeof(int64_t) + (OFF_MAX + 3) * sizeof(int32_t) + ((OFF_MAX + 7) & ~7) * sizeof(uint16_t) +
+           16 * sizeof(int32_t);
 }
 
 struct PullShape {
-    int win_rows;
+    int wnz;  // nonempty rows per window
     int hot0;
     size_t smem;
 };
 
-PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes, size_t SMEM_BYTES)
+PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes, size_t budget)
 {
     PullShape p{0, 0, 0};
-    const size_t fixed = pull_fixed_smem(k);
+    const size_t sc = ((size_t)(k + 4) & ~(size_t)3) * sizeof(float);
     const size_t per_row = (size_t)k * sizeof(uint32_t) * (weighted ? 2 : 1);
-    if (fixed + per_row + 16 > SMEM_BYTES) return p;
-    size_t win_bytes = per_row * (OFF_MAX - 1);
-    if (win_bytes > WIN_BYTES_MAX) win_bytes = WIN_BYTES_MAX > per_row ? WIN_BYTES_MAX : per_row;
-    if (fixed + win_bytes + 16 > SMEM_BYTES) win_bytes = SMEM_BYTES - fixed - 16;
-    p.win_rows = (int)(win_bytes / per_row);
-    if (p.win_rows > OFF_MAX - 1) p.win_rows = OFF_MAX - 1;
-    const size_t plane = (((size_t)p.win_rows * k + 3) & ~(size_t)3) * sizeof(uint32_t);
-    const size_t used = fixed + plane * (weighted ? 2 : 1);
-    size_t hot_cap = (SMEM_BYTES - used - 32) / (size_t)label_bytes;  // 32 B: rounding + the always-readable slot 0
+    const size_t fixed = sc + GROUPS * group_fixed_smem() + 64;
+    if (fixed + GROUPS * (per_row + 16) > budget) return p;
+    size_t win_bytes = (budget - fixed) / GROUPS;  // no hot tier: windows take everything
+    if (n_hot > 0 && win_bytes > WIN_HOT_BYTES) win_bytes = WIN_HOT_BYTES > per_row ? WIN_HOT_BYTES : per_row;
+    int wnz = (int)(win_bytes / per_row);
+    if (wnz > OFF_MAX - 1) wnz = OFF_MAX - 1;
+    const size_t plane = ((((size_t)wnz * k + 3) & ~(size_t)3) * sizeof(uint32_t));
+    const size_t used = fixed + GROUPS * plane * (weighted ? 2 : 1);
+    size_t hot_cap = used + 32 < budget ? (budget - used - 32) / (size_t)label_bytes : 0;
     hot_cap &= ~(size_t)15;
+    p.wnz = wnz;
     p.hot0 = (int)(n_hot < (int64_t)hot_cap ? n_hot : (int64_t)hot_cap);
     p.hot0 &= ~15;  // whole 16 B vectors; the rest of the hot tier is read through L2
     p.smem = used + (((size_t)p.hot0 * label_bytes + 16 + 15) & ~(size_t)15);  // >= 16 B: slot 0 always readable
@@ -437,20 +503,21 @@ int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, 
     }
     const size_t budget = (size_t)(optin < SMEM_BYTES_MAX ? optin : SMEM_BYTES_MAX);
     const PullShape ps = pull_shape(k, WEIGHTED, n_hot, (int)sizeof(LT), budget);
-    GEE_REQUIRE(ps.win_rows >= 1, GEE_ERR_INVALID, "k=%d too large for the pull window", k);
+    GEE_REQUIRE(ps.wnz >= 1, GEE_ERR_INVALID, "k=%d too large for the pull window", k);
     auto kern = k_pull<WEIGHTED, LT>;
     {
         const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps.smem);
         GEE_REQUIRE(e == cudaSuccess, GEE_ERR_CUDA, "k_pull: %zu B dynamic smem (opt-in max %d, window %d rows, hot %d): %s",
-                    ps.smem, optin, ps.win_rows, ps.hot0, cudaGetErrorString(e));
+                    ps.smem, optin, ps.wnz, ps.hot0, cudaGetErrorString(e));
     }
+    const int64_t ctas = (n_tiles + GROUPS - 1) / GROUPS;
     const int64_t cap = (int64_t)gee::sm_count();
-    const int grid = (int)(n_tiles < cap ? n_tiles : cap);
+    const int grid = (int)(ctas < cap ? ctas : cap);
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = WEIGHTED ? ldexp(1.0, -scale_exp) : 1.0;
     const int32_t sentinel = (int32_t)(n_hot + n);
     kern<<<grid, PT, ps.smem, st>>>(offsets, targets, w, arcs, tile_row, n_tiles, qscale, dscale, table, sentinel,
-                                    ps.hot0, inv, k, z, slots, ps.win_rows);
+                                    ps.hot0, inv, k, z, slots, ps.wnz);
     int rc = gee::check_launch("k_pull");
     if (rc) return rc;
     const int64_t want = (n_tiles * 32 + 255) / 256;
