@@ -173,6 +173,11 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         uint4 *dst = reinterpret_cast<uint4 *>(hot_s);
         for (int i = tid; i < vec; i += PT) dst[i] = __ldg(src + i);
     }
+    {  // windows start zeroed; the write-out clears every entry it reads
+        uint4 *a4 = reinterpret_cast<uint4 *>(G.lo);
+        const int w4 = (int)(plane * (WEIGHTED ? 2 : 1) / 4);
+        for (int i = gt; i < w4; i += GT) a4[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
     __syncthreads();  // the only CTA-wide barrier: groups run independently after this
 
     const int64_t stride = (int64_t)gridDim.x * GROUPS;
@@ -227,28 +232,32 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         int32_t wrow0 = base;
         bool first = true;
         while (wrow0 < R1) {
-            // ---- window rows [wrow0, wrow0 + nr): tile-local int32 offsets
+            // ---- window rows [wrow0, wrow0 + nr): tile-local int32 offsets and
+            // nonempty flags (2 rows per thread), ranks by warp + group scan
             int nr = min(OFF_MAX - 1, R1 - wrow0);
-            if (first && wrow0 - st0 + nr < scnt) {
-                const int sh = wrow0 - st0;
-                for (int i = gt; i <= nr; i += GT) {
-                    const int64_t v = off_s[sh + i] - a0;
-                    G.ol[i] = (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
-                }
-            } else {
-                if (!first) group_sync(g);  // previous window fully consumed
-                for (int i = gt; i <= nr; i += GT) {
-                    const int64_t v = __ldcs(offsets + wrow0 + i) - a0;
-                    G.ol[i] = (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
-                }
-            }
-            group_sync(g);
-            // ---- ranks of nonempty rows (2 rows per thread, warp scan + group scan)
             int f0 = 0, f1 = 0;
             {
                 const int r = 2 * gt;
-                if (r < nr) f0 = G.ol[r + 1] > G.ol[r];
-                if (r + 1 < nr) f1 = G.ol[r + 2] > G.ol[r + 1];
+                int64_t o0 = 0, o1 = 0, o2 = 0;
+                if (first && wrow0 - st0 + nr < scnt) {
+                    const int sh = wrow0 - st0;
+                    if (r <= nr) o0 = off_s[sh + r];
+                    if (r + 1 <= nr) o1 = off_s[sh + r + 1];
+                    if (r + 2 <= nr) o2 = off_s[sh + r + 2];
+                } else {
+                    if (!first) group_sync(g);  // previous window fully consumed
+                    if (r <= nr) o0 = __ldcs(offsets + wrow0 + r);
+                    if (r + 1 <= nr) o1 = __ldcs(offsets + wrow0 + r + 1);
+                    if (r + 2 <= nr) o2 = __ldcs(offsets + wrow0 + r + 2);
+                }
+                auto loc = [&](int64_t o) {
+                    const int64_t v = o - a0;
+                    return (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
+                };
+                if (r <= nr) G.ol[r] = loc(o0);
+                if (r + 1 <= nr) G.ol[r + 1] = loc(o1);
+                if (r < nr) f0 = o1 > o0;
+                if (r + 1 < nr) f1 = o2 > o1;
             }
             int incl = f0 + f1;
 #pragma unroll
@@ -277,21 +286,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 if (r + 1 < nr) G.nzr[r + 1] = f1 ? (uint16_t)(r0rank + f0) : (uint16_t)0xffff;
             }
             group_sync(g);
-            if (nnz > wnz) {
-                nr = G.wtot[8];  // rows [0, nr) hold exactly wnz nonempty rows
-                nnz = wnz;
-            }
-            {  // zero the compact window
-                uint4 *a4 = reinterpret_cast<uint4 *>(G.lo);
-                const int w4 = (nnz * kk + 3) >> 2;
-                const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-                for (int i = gt; i < w4; i += GT) a4[i] = zero4;
-                if (WEIGHTED) {
-                    uint4 *h4 = reinterpret_cast<uint4 *>(G.hi);
-                    for (int i = gt; i < w4; i += GT) h4[i] = zero4;
-                }
-            }
-            group_sync(g);
+            if (nnz > wnz) nr = G.wtot[8];  // rows [0, nr) hold exactly wnz nonempty rows
             // ---- accumulate this thread's arcs of the window
             const int32_t *ow = G.ol;
             const int wa0 = ow[0], wa1 = min(ow[nr], tlen);
@@ -351,41 +346,73 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
             if (first) cp_async_commit();
             group_sync(g);
 
-            // ---- write out complete rows of the window: one warp per row
+            // ---- write out complete rows of the window: flat over the Z region
+            // (coalesced, streaming); empty rows are zeros without smem reads;
+            // every window entry read is cleared for the next window
             const int32_t fin_lo = max(wrow0, R0);  // a head row is partial
             const int32_t fin_hi = min(wrow0 + nr, tail_cut ? R1 - 1 : R1);
-            for (int32_t row = fin_lo + gw; row < fin_hi; row += GT / 32) {
-                const int lr = row - wrow0;
-                const int slot = G.nzr[lr];
-                float *zr = z + (int64_t)row * kk;
+            if (fin_hi > fin_lo) {
+                const int lr0 = fin_lo - wrow0;
                 if ((kk & 1) == 0) {
-                    float2 *z2 = reinterpret_cast<float2 *>(zr);
-                    for (int c2 = lane; c2 < (kk >> 1); c2 += 32) {
+                    const int half = kk >> 1;
+                    const int total = (fin_hi - fin_lo) * half;
+                    float2 *zo = reinterpret_cast<float2 *>(z + (int64_t)fin_lo * kk);
+                    int c2 = gt % half, rr = lr0 + gt / half;
+                    const int dc = GT % half, dr = GT / half;
+#pragma unroll 2
+                    for (int e = gt; e < total; e += GT) {
+                        const int slot = G.nzr[rr];
                         float2 v = make_float2(0.f, 0.f);
                         if (slot != 0xffff) {
                             const int idx = slot * kk + 2 * c2;
+                            const uint2 l2 = *reinterpret_cast<const uint2 *>(G.lo + idx);
+                            *reinterpret_cast<uint2 *>(G.lo + idx) = make_uint2(0u, 0u);
                             if (WEIGHTED) {
-                                v.x = (float)(long long)(((unsigned long long)G.hi[idx] << 32) | G.lo[idx]);
-                                v.y = (float)(long long)(((unsigned long long)G.hi[idx + 1] << 32) | G.lo[idx + 1]);
+                                const uint2 h2 = *reinterpret_cast<const uint2 *>(G.hi + idx);
+                                *reinterpret_cast<uint2 *>(G.hi + idx) = make_uint2(0u, 0u);
+                                v.x = (float)(long long)(((unsigned long long)h2.x << 32) | l2.x);
+                                v.y = (float)(long long)(((unsigned long long)h2.y << 32) | l2.y);
                             } else {
-                                v.x = (float)G.lo[idx];
-                                v.y = (float)G.lo[idx + 1];
+                                v.x = (float)l2.x;
+                                v.y = (float)l2.y;
                             }
                             v.x *= sc[2 * c2 + 1];
                             v.y *= sc[2 * c2 + 2];
                         }
-                        __stcs(z2 + c2, v);
+                        __stcs(zo + e, v);
+                        c2 += dc;
+                        rr += dr;
+                        if (c2 >= half) {
+                            c2 -= half;
+                            rr++;
+                        }
                     }
                 } else {
-                    for (int c = lane; c < kk; c += 32) {
+                    const int total = (fin_hi - fin_lo) * kk;
+                    float *zo = z + (int64_t)fin_lo * kk;
+                    int c = gt % kk, rr = lr0 + gt / kk;
+                    const int dc = GT % kk, dr = GT / kk;
+                    for (int e = gt; e < total; e += GT) {
+                        const int slot = G.nzr[rr];
                         float v = 0.f;
                         if (slot != 0xffff) {
                             const int idx = slot * kk + c;
-                            v = WEIGHTED ? (float)(long long)(((unsigned long long)G.hi[idx] << 32) | G.lo[idx])
-                                         : (float)G.lo[idx];
+                            if (WEIGHTED) {
+                                v = (float)(long long)(((unsigned long long)G.hi[idx] << 32) | G.lo[idx]);
+                                G.hi[idx] = 0u;
+                            } else {
+                                v = (float)G.lo[idx];
+                            }
+                            G.lo[idx] = 0u;
                             v *= sc[c + 1];
                         }
-                        __stcs(zr + c, v);
+                        __stcs(zo + e, v);
+                        c += dc;
+                        rr += dr;
+                        if (c >= kk) {
+                            c -= kk;
+                            rr++;
+                        }
                     }
                 }
             }
@@ -406,6 +433,8 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     const int idx = slot * kk + c;
                     const unsigned long long v =
                         WEIGHTED ? (((unsigned long long)G.hi[idx] << 32) | G.lo[idx]) : (unsigned long long)G.lo[idx];
+                    G.lo[idx] = 0u;
+                    if (WEIGHTED) G.hi[idx] = 0u;
                     if (v) atomicAdd(&slots[owner * kk + c], v);
                 }
             }
