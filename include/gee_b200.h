@@ -53,6 +53,11 @@ extern "C" {
 /* Library version (major*10000 + minor*100 + patch). */
 int gee_version(void);
 
+/* Debug builds only (libgee_b200_debug.so, -DGEE_DEBUG): the first bounds
+ * violation a kernel recorded {check id, index, limit, thread}, then reset.
+ * Release builds return zeros. */
+int gee_debug_word(unsigned int *out4);
+
 /* Thread-local message of the last failing call ("" if none). */
 const char *gee_last_error(void);
 

@@ -30,17 +30,19 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_library(force=False, verbose=False):
-    """Compile every CUDA source into paper_2402_04403_b200/libgee_b200.so."""
+def build_library(force=False, verbose=False, debug=False):
+    """Compile every CUDA source into paper_2402_04403_b200/libgee_b200.so
+    (debug=True: libgee_b200_debug.so with -DGEE_DEBUG bounds checks)."""
+    lib = LIB.replace(".so", "_debug.so") if debug else LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(ROOT, "include", "gee_b200.h"), os.path.join(ROOT, "include", "gee_synth.h")]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    tmp = LIB + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, *srcs]
+    if not force and not _stale(lib, deps):
+        return lib
+    tmp = lib + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DGEE_DEBUG"] if debug else []), "-o", tmp, *srcs]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=CSRC)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib

@@ -10,7 +10,7 @@ import os
 from .errors import GeeError, ValidationError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgee_b200.so")
+LIB_PATH = os.path.join(_PKG, "libgee_b200_debug.so" if os.environ.get("GEE_DEBUG_LIB") else "libgee_b200.so")
 
 GEE_OK = 0
 GEE_ERR_INVALID = 1
@@ -39,6 +39,7 @@ P_i32 = ctypes.POINTER(ctypes.c_int32)
 SIGNATURES = {
     "gee_version": (c_int, []),
     "gee_last_error": (ctypes.c_char_p, []),
+    "gee_debug_word": (c_int, [ctypes.POINTER(ctypes.c_uint * 4)]),
     "gee_label_bytes": (c_int, [c_i32]),
     "gee_label_table_bytes": (c_size, [c_i64, c_i64, c_i32]),
     "gee_projection_work_bytes": (c_size, [c_i32]),

@@ -30,6 +30,7 @@ int check_launch(const char *what)
 
 }  // namespace gee
 
+
 extern "C" {
 
 int gee_version(void) { return 100; }

@@ -223,8 +223,8 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         const int32_t scnt = min(R1 - st0 + 1, OFF_MAX);
         cp_async_wait<0>();
         group_sync(g);  // staged offsets visible; this group's previous tile fully written out
-        const bool has_head = off_s[R0 - st0] > a0;  // also when R0 == n (offsets[n] = arcs > a0)
-        const int64_t offR1 = (R1 - st0 < scnt) ? off_s[R1 - st0] : __ldcs(offsets + R1);
+        const bool has_head = off_s[GEE_IDX(R0 - st0, OFF_MAX, 1)] > a0;  // also when R0 == n (offsets[n] = arcs > a0)
+        const int64_t offR1 = (R1 - st0 < scnt) ? off_s[GEE_IDX(R1 - st0, OFF_MAX, 2)] : __ldcs(offsets + R1);
         const bool tail_cut = (R1 > R0) && (offR1 > a0 + tlen);
         const int32_t base = has_head ? R0 - 1 : R0;
         const int32_t rows_total = R1 - base;
@@ -241,9 +241,9 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 int64_t o0 = 0, o1 = 0, o2 = 0;
                 if (first && wrow0 - st0 + nr < scnt) {
                     const int sh = wrow0 - st0;
-                    if (r <= nr) o0 = off_s[sh + r];
-                    if (r + 1 <= nr) o1 = off_s[sh + r + 1];
-                    if (r + 2 <= nr) o2 = off_s[sh + r + 2];
+                    if (r <= nr) o0 = off_s[GEE_IDX(sh + r, OFF_MAX, 3)];
+                    if (r + 1 <= nr) o1 = off_s[GEE_IDX(sh + r + 1, OFF_MAX, 3)];
+                    if (r + 2 <= nr) o2 = off_s[GEE_IDX(sh + r + 2, OFF_MAX, 3)];
                 } else {
                     if (!first) group_sync(g);  // previous window fully consumed
                     if (r <= nr) o0 = __ldcs(offsets + wrow0 + r);
@@ -256,6 +256,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 };
                 if (r <= nr) G.ol[r] = loc(o0);
                 if (r + 1 <= nr) G.ol[r + 1] = loc(o1);
+                if (r + 2 == nr) G.ol[nr] = loc(o2);  // nr == 2*GT: no thread starts there
                 if (r < nr) f0 = o1 > o0;
                 if (r + 1 < nr) f1 = o2 > o1;
             }
@@ -315,20 +316,20 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     else hi = mid;
                 }
                 int r = lo;
-                int next = ow[r + 1];
-                int slot = G.nzr[r];
+                int next = ow[GEE_IDX(r + 1, nr + 1, 4)];
+                int slot = G.nzr[GEE_IDX(r, nr, 5)];
 #pragma unroll
                 for (int i = 0; i < APT; i++) {
                     const int e = el0 + i;
                     if (e < m0 || e >= m1) continue;
                     if (e >= next) {
-                        do next = ow[++r + 1];
+                        do next = ow[GEE_IDX(++r + 1, nr + 1, 6)];
                         while (e >= next);
-                        slot = G.nzr[r];
+                        slot = G.nzr[GEE_IDX(r, nr, 7)];
                     }
                     const uint32_t c = lab[i];
                     if (c == 0u || c > (uint32_t)kk) continue;  // unlabeled (or out-of-range raw label)
-                    const int idx = slot * kk + (int)c - 1;
+                    const int idx = GEE_IDX(slot * kk + (int)c - 1, wnz * kk, 8);
                     if (WEIGHTED) {
                         const unsigned long long q = (unsigned long long)__float2ll_rn(wcur[i] * qscale);
                         const uint32_t lo32 = (uint32_t)q;
@@ -361,10 +362,10 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     const int dc = GT % half, dr = GT / half;
 #pragma unroll 2
                     for (int e = gt; e < total; e += GT) {
-                        const int slot = G.nzr[rr];
+                        const int slot = G.nzr[GEE_IDX(rr, nr, 9)];
                         float2 v = make_float2(0.f, 0.f);
                         if (slot != 0xffff) {
-                            const int idx = slot * kk + 2 * c2;
+                            const int idx = GEE_IDX(slot * kk + 2 * c2, wnz * kk, 10);
                             const uint2 l2 = *reinterpret_cast<const uint2 *>(G.lo + idx);
                             *reinterpret_cast<uint2 *>(G.lo + idx) = make_uint2(0u, 0u);
                             if (WEIGHTED) {
@@ -393,10 +394,10 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     int c = gt % kk, rr = lr0 + gt / kk;
                     const int dc = GT % kk, dr = GT / kk;
                     for (int e = gt; e < total; e += GT) {
-                        const int slot = G.nzr[rr];
+                        const int slot = G.nzr[GEE_IDX(rr, nr, 11)];
                         float v = 0.f;
                         if (slot != 0xffff) {
-                            const int idx = slot * kk + c;
+                            const int idx = GEE_IDX(slot * kk + c, wnz * kk, 12);
                             if (WEIGHTED) {
                                 v = (float)(long long)(((unsigned long long)G.hi[idx] << 32) | G.lo[idx]);
                                 G.hi[idx] = 0u;
@@ -428,9 +429,9 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     if (row < wrow0 || row >= wrow0 + nr) continue;
                 }
                 const int64_t owner = part == 0 ? __ldg(offsets + row) / TILE : j;
-                const int slot = G.nzr[row - wrow0];
+                const int slot = G.nzr[GEE_IDX(row - wrow0, nr, 13)];
                 for (int c = gt; c < kk; c += GT) {
-                    const int idx = slot * kk + c;
+                    const int idx = GEE_IDX(slot * kk + c, wnz * kk, 14);
                     const unsigned long long v =
                         WEIGHTED ? (((unsigned long long)G.hi[idx] << 32) | G.lo[idx]) : (unsigned long long)G.lo[idx];
                     G.lo[idx] = 0u;
@@ -559,6 +560,20 @@ int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, 
 }  // namespace
 
 extern "C" {
+
+/* Debug builds: first recorded bounds violation in the pull kernels. */
+int gee_debug_word(unsigned int *out4)
+{
+#ifdef GEE_DEBUG
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out4, g_gee_dbg, sizeof(unsigned int) * 4) != cudaSuccess) return GEE_ERR_CUDA;
+    unsigned int zero[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_gee_dbg, zero, sizeof(zero));
+#else
+    out4[0] = out4[1] = out4[2] = out4[3] = 0;
+#endif
+    return GEE_OK;
+}
 
 int64_t gee_pull_tiles(int64_t arcs) { return arcs <= 0 ? 0 : (arcs + TILE - 1) / TILE; }
 
