@@ -169,7 +169,7 @@ int gee_hot_encode(int32_t *targets, int64_t arcs, const int32_t *hot_rank, int6
  * zero_worker _kernels.py:124-135, arc_pass_worker _kernels.py:138-207)
  * for SOURCE_ONLY (symmetric) storage.
  */
-#define GEE_TILE_ARCS 4096
+#define GEE_TILE_ARCS 2048
 int64_t gee_pull_tiles(int64_t arcs);
 size_t gee_pull_slots_bytes(int64_t arcs, int32_t k);
 int gee_pull_plan(const int64_t *offsets, int64_t n, int64_t arcs, int64_t *tile_row,

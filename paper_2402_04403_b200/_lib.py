@@ -21,7 +21,7 @@ GEE_ZERO_Z = 1
 GEE_SOURCE_ONLY = 2
 GEE_PRECOMBINE = 4
 
-TILE_ARCS = 4096
+TILE_ARCS = 2048
 
 c_int = ctypes.c_int
 c_i32 = ctypes.c_int32

@@ -38,15 +38,16 @@
 
 namespace {
 
-constexpr int GROUPS = 2;                // independent tile pipelines per CTA
+constexpr int GROUPS = 4;                // independent tile pipelines per CTA
 constexpr int GT = 256;                  // threads per group (8 warps)
 constexpr int PT = GROUPS * GT;          // threads per CTA (one persistent CTA per SM)
-constexpr int APT = 16;                  // arcs per thread
-constexpr int TILE = GT * APT;           // 4096 arcs per tile
+constexpr int APT = 8;                   // arcs per thread
+constexpr int TILE = GT * APT;           // 2048 arcs per tile
 static_assert(TILE == GEE_TILE_ARCS, "tile size mismatch with header");
 constexpr int SMEM_BYTES_MAX = 227 * 1024;  // opt-in maximum per CTA on sm_100a (queried at launch)
-constexpr int OFF_MAX = 513;             // staged offsets per buffer (<= 512 rows per window)
-constexpr int WIN_HOT_BYTES = 40 * 1024; // per-group window when a hot tier wants the smem
+constexpr int WROWS = GT;                // rows per window (one per thread)
+constexpr int OFF_MAX = WROWS + 1;       // staged offsets per buffer
+constexpr int WIN_HOT_BYTES = 16 * 1024; // per-group window when a hot tier wants the smem
 
 __device__ __forceinline__ int64_t lower_bound_i64(const int64_t *__restrict__ a, int64_t lo,
                                                    int64_t hi, int64_t key)
@@ -61,8 +62,8 @@ __device__ __forceinline__ int64_t lower_bound_i64(const int64_t *__restrict__ a
 }
 
 // tile_row[j] = first row r in [0, n] with offsets[r] >= j*T (j < n_tiles);
-// tile_row[n_tiles] = first row with offsets[r] >= arcs (trailing empty rows
-// start there and are zero-filled by k_zero_tail).
+// tile_row[n_tiles] = first row with offsets[r] >= arcs (trailing rows have
+// no arcs; k_zero_empty zero-fills them with the other empty rows).
 __global__ void k_pull_plan(const int64_t *__restrict__ offsets, int64_t n, int64_t arcs,
                             int64_t n_tiles, int64_t *__restrict__ tile_row)
 {
@@ -86,7 +87,8 @@ __device__ __forceinline__ void group_sync(int g) { asm volatile("bar.sync %0, %
 struct GroupSmem {  // per-group shared state (carved from dynamic smem)
     int64_t *off64;  // 2 x OFF_MAX staged offsets (cp.async double buffer)
     int32_t *ol;     // OFF_MAX + 3 tile-local clamped offsets of the window
-    uint16_t *nzr;   // OFF_MAX rank of each nonempty row, 0xffff for empty rows
+    uint16_t *nzr;   // WROWS: rank of each nonempty row, 0xffff for empty rows
+    uint16_t *rrow;  // WROWS: window row of each rank
     int32_t *wtot;   // 8 warp totals (+ 8 scratch)
     uint32_t *lo;    // wnz * k
     uint32_t *hi;    // wnz * k (weighted)
@@ -149,11 +151,13 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
     for (int q = 0; q < GROUPS; q++) {
         GroupSmem s;
         s.off64 = reinterpret_cast<int64_t *>(p);
-        p += 2 * OFF_MAX * sizeof(int64_t);
+        p += 2 * ((OFF_MAX + 1) & ~1) * sizeof(int64_t);
         s.ol = reinterpret_cast<int32_t *>(p);
-        p += (OFF_MAX + 3) * sizeof(int32_t);
+        p += ((OFF_MAX + 3 + 3) & ~3) * sizeof(int32_t);
         s.nzr = reinterpret_cast<uint16_t *>(p);
-        p += ((OFF_MAX + 7) & ~7) * sizeof(uint16_t);
+        p += WROWS * sizeof(uint16_t);
+        s.rrow = reinterpret_cast<uint16_t *>(p);
+        p += WROWS * sizeof(uint16_t);
         s.wtot = reinterpret_cast<int32_t *>(p);
         p += 16 * sizeof(int32_t);
         s.lo = reinterpret_cast<uint32_t *>(p);
@@ -183,34 +187,30 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
     const int64_t stride = (int64_t)gridDim.x * GROUPS;
     int64_t j = (int64_t)blockIdx.x * GROUPS + g;
     if (j >= n_tiles) return;
-
-    // prologue: this tile's arcs + staged offsets
-    int32_t tn[APT];
-    float wn[APT];
-    load_arcs<WEIGHTED>(tn, wn, j, gt, targets, wts, arcs, sentinel);
     int32_t R0 = (int32_t)tile_row[j], R1 = (int32_t)tile_row[j + 1];
     stage_offsets(G.off64, offsets, R0, R1, gt);
     cp_async_commit();
     int buf = 0;
 
     for (; j < n_tiles; j += stride) {
-        // ---- gather this tile's labels (their latency overlaps the row setup)
+        // ---- this tile's arcs and labels (the gathers overlap the row setup)
         uint32_t lab[APT];
         float wcur[APT];
+        {
+            int32_t t[APT];
+            load_arcs<WEIGHTED>(t, wcur, j, gt, targets, wts, arcs, sentinel);
 #pragma unroll
-        for (int i = 0; i < APT; i++) {
-            const uint32_t t = (uint32_t)tn[i];
-            const bool in_smem = t < (uint32_t)hot0;
-            uint32_t l = (uint32_t)hot_s[in_smem ? t : 0u];
-            if (!in_smem) l = gee::ld_label<LT>(table + t, pol);
-            lab[i] = l;
-            if (WEIGHTED) wcur[i] = wn[i];
+            for (int i = 0; i < APT; i++) {
+                const uint32_t ti = (uint32_t)t[i];
+                const bool in_smem = ti < (uint32_t)hot0;
+                uint32_t l = (uint32_t)hot_s[in_smem ? ti : 0u];
+                if (!in_smem) l = gee::ld_label<LT>(table + ti, pol);
+                lab[i] = l;
+            }
         }
-        // ---- prefetch the next tile's arcs (registers) and row range
         const int64_t jn = j + stride;
         int32_t R0n = 0, R1n = 0;
         if (jn < n_tiles) {
-            load_arcs<WEIGHTED>(tn, wn, jn, gt, targets, wts, arcs, sentinel);
             R0n = (int32_t)tile_row[jn];
             R1n = (int32_t)tile_row[jn + 1];
         }
@@ -218,49 +218,43 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         const int64_t a0 = j * (int64_t)TILE;
         const int tlen = (int)min((int64_t)TILE, arcs - a0);
         const int el0 = gt * APT;  // this thread's first arc, tile-local
-        int64_t *off_s = G.off64 + buf * OFF_MAX;
+        int64_t *off_s = G.off64 + buf * ((OFF_MAX + 1) & ~1);
         const int32_t st0 = R0 > 0 ? R0 - 1 : 0;  // first staged row
         const int32_t scnt = min(R1 - st0 + 1, OFF_MAX);
         cp_async_wait<0>();
         group_sync(g);  // staged offsets visible; this group's previous tile fully written out
-        const bool has_head = off_s[GEE_IDX(R0 - st0, OFF_MAX, 1)] > a0;  // also when R0 == n (offsets[n] = arcs > a0)
+        const bool has_head = off_s[GEE_IDX(R0 - st0, OFF_MAX, 1)] > a0;  // also when R0 == n
         const int64_t offR1 = (R1 - st0 < scnt) ? off_s[GEE_IDX(R1 - st0, OFF_MAX, 2)] : __ldcs(offsets + R1);
         const bool tail_cut = (R1 > R0) && (offR1 > a0 + tlen);
         const int32_t base = has_head ? R0 - 1 : R0;
-        const int32_t rows_total = R1 - base;
 
         int32_t wrow0 = base;
         bool first = true;
         while (wrow0 < R1) {
-            // ---- window rows [wrow0, wrow0 + nr): tile-local int32 offsets and
-            // nonempty flags (2 rows per thread), ranks by warp + group scan
-            int nr = min(OFF_MAX - 1, R1 - wrow0);
-            int f0 = 0, f1 = 0;
+            // ---- window rows [wrow0, wrow0 + nr): tile-local int32 offsets,
+            // nonempty flags (one row per thread), ranks by warp + group scan
+            int nr = min(WROWS, R1 - wrow0);
+            int f = 0;
             {
-                const int r = 2 * gt;
-                int64_t o0 = 0, o1 = 0, o2 = 0;
+                int64_t o0 = 0, o1 = 0;
                 if (first && wrow0 - st0 + nr < scnt) {
                     const int sh = wrow0 - st0;
-                    if (r <= nr) o0 = off_s[GEE_IDX(sh + r, OFF_MAX, 3)];
-                    if (r + 1 <= nr) o1 = off_s[GEE_IDX(sh + r + 1, OFF_MAX, 3)];
-                    if (r + 2 <= nr) o2 = off_s[GEE_IDX(sh + r + 2, OFF_MAX, 3)];
+                    if (gt <= nr) o0 = off_s[GEE_IDX(sh + gt, OFF_MAX, 3)];
+                    if (gt + 1 <= nr) o1 = off_s[GEE_IDX(sh + gt + 1, OFF_MAX, 3)];
                 } else {
                     if (!first) group_sync(g);  // previous window fully consumed
-                    if (r <= nr) o0 = __ldcs(offsets + wrow0 + r);
-                    if (r + 1 <= nr) o1 = __ldcs(offsets + wrow0 + r + 1);
-                    if (r + 2 <= nr) o2 = __ldcs(offsets + wrow0 + r + 2);
+                    if (gt <= nr) o0 = __ldcs(offsets + wrow0 + gt);
+                    if (gt + 1 <= nr) o1 = __ldcs(offsets + wrow0 + gt + 1);
                 }
                 auto loc = [&](int64_t o) {
                     const int64_t v = o - a0;
                     return (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
                 };
-                if (r <= nr) G.ol[r] = loc(o0);
-                if (r + 1 <= nr) G.ol[r + 1] = loc(o1);
-                if (r + 2 == nr) G.ol[nr] = loc(o2);  // nr == 2*GT: no thread starts there
-                if (r < nr) f0 = o1 > o0;
-                if (r + 1 < nr) f1 = o2 > o1;
+                if (gt <= nr) G.ol[gt] = loc(o0);
+                if (gt + 1 == nr + 0 && nr == WROWS) G.ol[nr] = loc(o1);  // no thread starts at row WROWS
+                if (gt < nr) f = o1 > o0;
             }
-            int incl = f0 + f1;
+            int incl = f;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const int v = __shfl_up_sync(0xffffffffu, incl, d);
@@ -275,27 +269,25 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 wpre += q < gw ? v : 0;
                 nnz += v;
             }
-            const int r0rank = wpre + incl - f0 - f1;  // rank of row 2*gt if nonempty
-            if (nnz > wnz) {
-                // shrink the window to the first wnz nonempty rows: find the row of rank wnz
-                if (f0 && r0rank == wnz) G.wtot[8] = 2 * gt;
-                if (f1 && r0rank + f0 == wnz) G.wtot[8] = 2 * gt + 1;
-            }
-            {
-                const int r = 2 * gt;
-                if (r < nr) G.nzr[r] = f0 ? (uint16_t)r0rank : (uint16_t)0xffff;
-                if (r + 1 < nr) G.nzr[r + 1] = f1 ? (uint16_t)(r0rank + f0) : (uint16_t)0xffff;
+            const int rank = wpre + incl - f;  // rank of this thread's row if nonempty
+            if (gt < nr) {
+                G.nzr[gt] = f ? (uint16_t)rank : (uint16_t)0xffff;
+                if (f && rank < wnz) G.rrow[rank] = (uint16_t)gt;
+                if (f && rank == wnz) G.wtot[8] = gt;  // first row past a full window
             }
             group_sync(g);
-            if (nnz > wnz) nr = G.wtot[8];  // rows [0, nr) hold exactly wnz nonempty rows
+            if (nnz > wnz) {
+                nr = G.wtot[8];  // rows [0, nr) hold exactly wnz nonempty rows
+                nnz = wnz;
+            }
             // ---- accumulate this thread's arcs of the window
             const int32_t *ow = G.ol;
-            const int wa0 = ow[0], wa1 = min(ow[nr], tlen);
+            const int wa0 = ow[0], wa1 = min(ow[GEE_IDX(nr, OFF_MAX, 15)], tlen);
             const int m0 = max(el0, wa0), m1 = min(el0 + APT, wa1);
             const int ew = max(el0 - lane * APT, wa0);  // the warp's first arc in the window
             int rw = 0;
             if (ew < wa1) {  // warp-uniform: bracket the warp's first arc with two 32-way ballots
-                const int step = (nr + 31) >> 5;  // <= 16
+                const int step = (nr + 31) >> 5;  // <= 8
                 int cand = min(lane * step, nr);
                 unsigned bal = __ballot_sync(0xffffffffu, ow[cand] <= ew);
                 const int b = (31 - __clz(bal)) * step;
@@ -343,77 +335,38 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 }
             }
             // the next tile's offsets can be staged now (its buffer is free)
-            if (first && jn < n_tiles) stage_offsets(G.off64 + (buf ^ 1) * OFF_MAX, offsets, R0n, R1n, gt);
+            if (first && jn < n_tiles)
+                stage_offsets(G.off64 + (buf ^ 1) * ((OFF_MAX + 1) & ~1), offsets, R0n, R1n, gt);
             if (first) cp_async_commit();
             group_sync(g);
 
-            // ---- write out complete rows of the window: flat over the Z region
-            // (coalesced, streaming); empty rows are zeros without smem reads;
-            // every window entry read is cleared for the next window
-            const int32_t fin_lo = max(wrow0, R0);  // a head row is partial
-            const int32_t fin_hi = min(wrow0 + nr, tail_cut ? R1 - 1 : R1);
-            if (fin_hi > fin_lo) {
-                const int lr0 = fin_lo - wrow0;
-                if ((kk & 1) == 0) {
-                    const int half = kk >> 1;
-                    const int total = (fin_hi - fin_lo) * half;
-                    float2 *zo = reinterpret_cast<float2 *>(z + (int64_t)fin_lo * kk);
-                    int c2 = gt % half, rr = lr0 + gt / half;
-                    const int dc = GT % half, dr = GT / half;
-#pragma unroll 2
-                    for (int e = gt; e < total; e += GT) {
-                        const int slot = G.nzr[GEE_IDX(rr, nr, 9)];
-                        float2 v = make_float2(0.f, 0.f);
-                        if (slot != 0xffff) {
-                            const int idx = GEE_IDX(slot * kk + 2 * c2, wnz * kk, 10);
-                            const uint2 l2 = *reinterpret_cast<const uint2 *>(G.lo + idx);
-                            *reinterpret_cast<uint2 *>(G.lo + idx) = make_uint2(0u, 0u);
-                            if (WEIGHTED) {
-                                const uint2 h2 = *reinterpret_cast<const uint2 *>(G.hi + idx);
-                                *reinterpret_cast<uint2 *>(G.hi + idx) = make_uint2(0u, 0u);
-                                v.x = (float)(long long)(((unsigned long long)h2.x << 32) | l2.x);
-                                v.y = (float)(long long)(((unsigned long long)h2.y << 32) | l2.y);
-                            } else {
-                                v.x = (float)l2.x;
-                                v.y = (float)l2.y;
-                            }
-                            v.x *= sc[2 * c2 + 1];
-                            v.y *= sc[2 * c2 + 2];
+            // ---- write out the window's complete nonempty rows (empty rows are
+            // zeroed by k_zero_empty); flat over nnz x k, clearing what it reads
+            {
+                const int32_t lr_lo = max(wrow0, R0) - wrow0;                       // a head row is partial
+                const int32_t lr_hi = min(wrow0 + nr, tail_cut ? R1 - 1 : R1) - wrow0;  // so is a cut tail
+                const int total = nnz * kk;
+                int c = gt % kk, s = gt / kk;
+                const int dc = GT % kk, ds = GT / kk;
+                for (int e = gt; e < total; e += GT) {
+                    const int lr = G.rrow[GEE_IDX(s, wnz, 9)];
+                    if (lr >= lr_lo && lr < lr_hi) {
+                        const int idx = GEE_IDX(s * kk + c, wnz * kk, 10);
+                        float v;
+                        if (WEIGHTED) {
+                            v = (float)(long long)(((unsigned long long)G.hi[idx] << 32) | G.lo[idx]);
+                            G.hi[idx] = 0u;
+                        } else {
+                            v = (float)G.lo[idx];
                         }
-                        __stcs(zo + e, v);
-                        c2 += dc;
-                        rr += dr;
-                        if (c2 >= half) {
-                            c2 -= half;
-                            rr++;
-                        }
+                        G.lo[idx] = 0u;
+                        __stcs(z + (int64_t)(wrow0 + lr) * kk + c, v * sc[c + 1]);
                     }
-                } else {
-                    const int total = (fin_hi - fin_lo) * kk;
-                    float *zo = z + (int64_t)fin_lo * kk;
-                    int c = gt % kk, rr = lr0 + gt / kk;
-                    const int dc = GT % kk, dr = GT / kk;
-                    for (int e = gt; e < total; e += GT) {
-                        const int slot = G.nzr[GEE_IDX(rr, nr, 11)];
-                        float v = 0.f;
-                        if (slot != 0xffff) {
-                            const int idx = GEE_IDX(slot * kk + c, wnz * kk, 12);
-                            if (WEIGHTED) {
-                                v = (float)(long long)(((unsigned long long)G.hi[idx] << 32) | G.lo[idx]);
-                                G.hi[idx] = 0u;
-                            } else {
-                                v = (float)G.lo[idx];
-                            }
-                            G.lo[idx] = 0u;
-                            v *= sc[c + 1];
-                        }
-                        __stcs(zo + e, v);
-                        c += dc;
-                        rr += dr;
-                        if (c >= kk) {
-                            c -= kk;
-                            rr++;
-                        }
+                    c += dc;
+                    s += ds;
+                    if (c >= kk) {
+                        c -= kk;
+                        s++;
                     }
                 }
             }
@@ -442,7 +395,6 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
             wrow0 += nr;
             first = false;
         }
-        (void)rows_total;
         R0 = R0n;
         R1 = R1n;
         buf ^= 1;
@@ -473,21 +425,39 @@ __global__ void k_pull_finalize(const int64_t *__restrict__ offsets, const int64
     }
 }
 
-__global__ void k_zero_tail(const int64_t *__restrict__ first_row, int64_t n, int32_t k,
-                            float *__restrict__ z)
+// Zero the Z rows with no arcs (the pull kernel writes only nonempty rows).
+// One warp per 32 consecutive rows: a ballot marks the empty ones, then the
+// warp writes their k floats as one coalesced flat range.
+__global__ void k_zero_empty(const int64_t *__restrict__ offsets, int64_t n, int32_t k, float *__restrict__ z)
 {
-    const int64_t r0 = *first_row;
-    const int64_t total = (n - r0) * (int64_t)k;
-    float *zo = z + r0 * (int64_t)k;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x)
-        __stcs(zo + i, 0.f);
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r0 = ((((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5) * 32; r0 < n; r0 += warps * 32) {
+        const int64_t r = r0 + lane;
+        const bool empty = r < n && __ldcs(offsets + r + 1) == __ldcs(offsets + r);
+        const unsigned mask = __ballot_sync(0xffffffffu, empty);
+        if (!mask) continue;
+        const int rows = (int)min((int64_t)32, n - r0);
+        const int total = rows * k;
+        float *zo = z + r0 * (int64_t)k;
+        int c = lane % k, rr = lane / k;
+        const int dc = 32 % k, dr = 32 / k;
+        for (int e = lane; e < total; e += 32) {
+            if ((mask >> rr) & 1u) __stcs(zo + e, 0.f);
+            c += dc;
+            rr += dr;
+            if (c >= k) {
+                c -= k;
+                rr++;
+            }
+        }
+    }
 }
 
 size_t group_fixed_smem()
 {
-    return 2 * OFF_MAX * sizeof(int64_t) + (OFF_MAX + 3) * sizeof(int32_t) + ((OFF_MAX + 7) & ~7) * sizeof(uint16_t) +
-           16 * sizeof(int32_t);
+    return 2 * ((OFF_MAX + 1) & ~1) * sizeof(int64_t) + ((OFF_MAX + 3 + 3) & ~3) * sizeof(int32_t) +
+           2 * WROWS * sizeof(uint16_t) + 16 * sizeof(int32_t);
 }
 
 struct PullShape {
@@ -506,7 +476,7 @@ PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes, s
     size_t win_bytes = (budget - fixed) / GROUPS;  // no hot tier: windows take everything
     if (n_hot > 0 && win_bytes > WIN_HOT_BYTES) win_bytes = WIN_HOT_BYTES > per_row ? WIN_HOT_BYTES : per_row;
     int wnz = (int)(win_bytes / per_row);
-    if (wnz > OFF_MAX - 1) wnz = OFF_MAX - 1;
+    if (wnz > WROWS) wnz = WROWS;
     const size_t plane = ((((size_t)wnz * k + 3) & ~(size_t)3) * sizeof(uint32_t));
     const size_t used = fixed + GROUPS * plane * (weighted ? 2 : 1);
     size_t hot_cap = used + 32 < budget ? (budget - used - 32) / (size_t)label_bytes : 0;
@@ -622,8 +592,8 @@ int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const flo
     cudaStream_t st = gee::as_stream(stream);
     if (n == 0) return GEE_OK;
     GEE_REQUIRE(offsets && tile_row && z, GEE_ERR_INVALID, "NULL array argument");
-    // Trailing rows with no arcs belong to no tile: zero them (the first such
-    // row is tile_row[n_tiles], read on the device; no host sync).
+    // Rows with no arcs (isolated vertices, trailing rows) are zeroed by
+    // k_zero_empty; the pull kernel writes exactly the nonempty rows.
     if (arcs == 0) {
         GEE_CUDA(cudaMemsetAsync(z, 0, sizeof(float) * (size_t)n * k, st));
         return GEE_OK;
@@ -632,9 +602,11 @@ int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const flo
     GEE_REQUIRE(gee::aligned16(targets) && (!w || gee::aligned16(w)) && gee::aligned16(table), GEE_ERR_INVALID,
                 "targets/weights/table must be 16-byte aligned");
     {
-        const int64_t n_tiles = gee_pull_tiles(arcs);
-        k_zero_tail<<<gee::sm_count() * 2, 256, 0, st>>>(tile_row + n_tiles, n, k, z);
-        int rc = gee::check_launch("k_zero_tail");
+        const int64_t warps = (n + 31) / 32;
+        const int64_t want = (warps * 32 + 255) / 256;
+        const int64_t cap = (int64_t)gee::sm_count() * 8;
+        k_zero_empty<<<(int)(want < cap ? (want < 1 ? 1 : want) : cap), 256, 0, st>>>(offsets, n, k, z);
+        int rc = gee::check_launch("k_zero_empty");
         if (rc) return rc;
     }
     auto *sl = reinterpret_cast<unsigned long long *>(slots);
