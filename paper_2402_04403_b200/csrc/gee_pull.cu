@@ -34,6 +34,8 @@
 //   its own.  Rows that run past their owner tile (hubs) are
 //   summed exactly through 64-bit global atomics into the owner tile's slot
 //   and written by k_pull_finalize.
+#include <cstdlib>
+
 #include "gee_common.cuh"
 
 namespace {
@@ -135,8 +137,10 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
        const float *__restrict__ wts, int64_t arcs, const int64_t *__restrict__ tile_row, int64_t n_tiles,
        float qscale, double dscale, const LT *__restrict__ table, int32_t sentinel, int32_t hot0,
        const double *__restrict__ inv, int32_t k, float *__restrict__ z, unsigned long long *__restrict__ slots,
-       int wnz)
+       int wnz, int skip)
 {
+    // skip: experiment mask (GEE_PULL_SKIP; results are wrong when set):
+    // 1 no label gathers, 2 no accumulation, 4 no Z write-out, 8 no row search
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid % GT;
@@ -198,13 +202,22 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         float wcur[APT];
         {
             int32_t t[APT];
-            load_arcs<WEIGHTED>(t, wcur, j, gt, targets, wts, arcs, sentinel);
+            if (skip & 32) {
+#pragma unroll
+                for (int i = 0; i < APT; i++) {
+                    t[i] = sentinel;
+                    wcur[i] = 1.f;
+                }
+            } else {
+                load_arcs<WEIGHTED>(t, wcur, j, gt, targets, wts, arcs, sentinel);
+            }
 #pragma unroll
             for (int i = 0; i < APT; i++) {
                 const uint32_t ti = (uint32_t)t[i];
                 const bool in_smem = ti < (uint32_t)hot0;
                 uint32_t l = (uint32_t)hot_s[in_smem ? ti : 0u];
-                if (!in_smem) l = gee::ld_label<LT>(table + ti, pol);
+                if (!in_smem && !(skip & 1)) l = gee::ld_label<LT>(table + ti, pol);
+                if (skip & 1) l = 1u + (ti & 1u);
                 lab[i] = l;
             }
         }
@@ -295,7 +308,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 bal = __ballot_sync(0xffffffffu, lane < step && ow[cand] <= ew);
                 rw = b + (31 - __clz(bal));
             }
-            if (m0 < m1) {
+            if (m0 < m1 && !(skip & 8)) {
                 int lo = rw, gl = 1;  // gallop to the last r with ow[r] <= m0
                 while (lo + gl < nr && ow[lo + gl] <= m0) {
                     lo += gl;
@@ -320,7 +333,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                         slot = G.nzr[GEE_IDX(r, nr, 7)];
                     }
                     const uint32_t c = lab[i];
-                    if (c == 0u || c > (uint32_t)kk) continue;  // unlabeled (or out-of-range raw label)
+                    if (c == 0u || c > (uint32_t)kk || (skip & 2)) continue;  // unlabeled (or out-of-range raw label)
                     const int idx = GEE_IDX(slot * kk + (int)c - 1, wnz * kk, 8);
                     if (WEIGHTED) {
                         const unsigned long long q = (unsigned long long)__float2ll_rn(wcur[i] * qscale);
@@ -345,7 +358,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
             {
                 const int32_t lr_lo = max(wrow0, R0) - wrow0;                       // a head row is partial
                 const int32_t lr_hi = min(wrow0 + nr, tail_cut ? R1 - 1 : R1) - wrow0;  // so is a cut tail
-                const int total = nnz * kk;
+                const int total = (skip & 4) ? 0 : nnz * kk;
                 int c = gt % kk, s = gt / kk;
                 const int dc = GT % kk, ds = GT / kk;
                 for (int e = gt; e < total; e += GT) {
@@ -381,6 +394,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     row = R1 - 1;
                     if (row < wrow0 || row >= wrow0 + nr) continue;
                 }
+                if (skip & 16) continue;
                 const int64_t owner = part == 0 ? __ldg(offsets + row) / TILE : j;
                 const int slot = G.nzr[GEE_IDX(row - wrow0, nr, 13)];
                 for (int c = gt; c < kk; c += GT) {
@@ -516,8 +530,12 @@ int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, 
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = WEIGHTED ? ldexp(1.0, -scale_exp) : 1.0;
     const int32_t sentinel = (int32_t)(n_hot + n);
+    static const int skip = getenv("GEE_PULL_SKIP") ? atoi(getenv("GEE_PULL_SKIP")) : 0;
+    if (getenv("GEE_PULL_VERBOSE"))
+        fprintf(stderr, "k_pull grid %d x %d smem %zu wnz %d hot0 %d tiles %lld skip %d\n", grid, PT, ps.smem, ps.wnz,
+                ps.hot0, (long long)n_tiles, skip);
     kern<<<grid, PT, ps.smem, st>>>(offsets, targets, w, arcs, tile_row, n_tiles, qscale, dscale, table, sentinel,
-                                    ps.hot0, inv, k, z, slots, ps.wnz);
+                                    ps.hot0, inv, k, z, slots, ps.wnz, skip);
     int rc = gee::check_launch("k_pull");
     if (rc) return rc;
     const int64_t want = (n_tiles * 32 + 255) / 256;
