@@ -460,7 +460,7 @@ def run_e2e(g, y, emb, z, s, args):
             g.hot_rank.copy_(h_hot, non_blocking=True)
         g2 = DeviceGraph(g.n, g.s, dev)
         g2.offsets, g2.targets, g2.weights = d_off, d_tgt, d_w
-        g2._plan()  # tile plan + weight statistics (host sync for the exponent)
+        g2._plan()  # tile/chunk plan, cut list, weight statistics (host sync)
         g2.hot_rank, g2.n_hot, g2.hot_k = g.hot_rank, g.n_hot, g.hot_k  # targets arrive hot-encoded
         emb.project(d_y, validate=False, g=g2)
         emb.pull(g2, z)

@@ -156,8 +156,12 @@ int gee_hot_encode(int32_t *targets, int64_t arcs, const int32_t *hot_rank, int6
 /* ---------------------------------------------------------------- K4 ----
  * Pull (row-owner) edge map over a symmetric CSR whose targets are
  * label-table slots.  Tile j covers arcs [j*GEE_TILE_ARCS, (j+1)*GEE_TILE_ARCS)
- * and owns the rows whose first arc position offsets[r] falls in it;
- * tile_row[j] = first such row (gee_pull_plan).  Per row x:
+ * and owns the rows whose first arc position offsets[r] falls in it.
+ * gee_pull_plan (graph preparation) writes tile_row[n_tiles+1] (first owned
+ * row of each tile), chunk_row[gee_pull_chunks(arcs)] (u16: row of the first
+ * arc of each 16-arc chunk relative to the tile's first row) and the list of
+ * tiles whose last row continues past them (cut_tiles[n_tiles], count in
+ * *n_cut, host).  Per row x:
  *     Z[x, c] = inv[c+1] * sum_{arcs x->v, Y[v]=c+1} w
  * accumulated exactly in integers (unit weights: counts; weighted: fixed
  * point w*2^scale_exp rounded to int64), so Z is bit-stable run to run and
@@ -169,15 +173,17 @@ int gee_hot_encode(int32_t *targets, int64_t arcs, const int32_t *hot_rank, int6
  * zero_worker _kernels.py:124-135, arc_pass_worker _kernels.py:138-207)
  * for SOURCE_ONLY (symmetric) storage.
  */
-#define GEE_TILE_ARCS 2048
+#define GEE_TILE_ARCS 4096
 int64_t gee_pull_tiles(int64_t arcs);
+int64_t gee_pull_chunks(int64_t arcs);
 size_t gee_pull_slots_bytes(int64_t arcs, int32_t k);
 int gee_pull_plan(const int64_t *offsets, int64_t n, int64_t arcs, int64_t *tile_row,
-                  void *stream);
+                  uint16_t *chunk_row, int32_t *cut_tiles, int64_t *n_cut, void *stream);
 int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const float *w,
-                       int64_t n, int64_t arcs, const int64_t *tile_row, int32_t scale_exp,
-                       const void *table, int64_t n_hot, const double *inv, int32_t k,
-                       float *z, void *slots, void *stream);
+                       int64_t n, int64_t arcs, const int64_t *tile_row,
+                       const uint16_t *chunk_row, const int32_t *cut_tiles, int64_t n_cut,
+                       int32_t scale_exp, const void *table, int64_t n_hot, const double *inv,
+                       int32_t k, float *z, void *slots, void *stream);
 
 /* Choose the fixed-point exponent for a weighted pull: the largest e with
  * max_row_abs * 2^e < 2^62.  Returns the relative quantisation bound

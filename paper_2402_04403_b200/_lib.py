@@ -21,7 +21,7 @@ GEE_ZERO_Z = 1
 GEE_SOURCE_ONLY = 2
 GEE_PRECOMBINE = 4
 
-TILE_ARCS = 2048
+TILE_ARCS = 4096
 
 c_int = ctypes.c_int
 c_i32 = ctypes.c_int32
@@ -54,9 +54,11 @@ SIGNATURES = {
     "gee_hot_plan": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, ctypes.POINTER(c_i64), vp]),
     "gee_hot_encode": (c_int, [vp, c_i64, vp, c_i64, vp]),
     "gee_pull_tiles": (c_i64, [c_i64]),
+    "gee_pull_chunks": (c_i64, [c_i64]),
     "gee_pull_slots_bytes": (c_size, [c_i64, c_i32]),
-    "gee_pull_plan": (c_int, [vp, c_i64, c_i64, vp, vp]),
-    "gee_embed_csr_pull": (c_int, [vp, vp, vp, c_i64, c_i64, vp, c_i32, vp, c_i64, vp, c_i32, vp, vp, vp]),
+    "gee_pull_plan": (c_int, [vp, c_i64, c_i64, vp, vp, vp, ctypes.POINTER(c_i64), vp]),
+    "gee_embed_csr_pull": (c_int, [vp, vp, vp, c_i64, c_i64, vp, vp, vp, c_i64, c_i32, vp, c_i64, vp, c_i32, vp, vp,
+                                   vp]),
     "gee_pull_scale_exp": (c_int, [c_dbl, c_dbl, P_i32, P_dbl]),
     "gee_synth_word": (c_u64, [c_u64, c_u64, c_u64]),
     "gee_synth_rmat": (c_int, [vp, vp, vp, c_i64, c_i64, c_i32, c_dbl, c_dbl, c_dbl, c_u64, c_i32, vp]),

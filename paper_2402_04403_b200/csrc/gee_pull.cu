@@ -20,36 +20,43 @@
 //                   sm_100a, 64-bit shared atomics are CAS loops).
 //
 // Work decomposition (balanced by arcs, hub rows split for free):
-//   tile j = arcs [j*T, (j+1)*T), T = GEE_TILE_ARCS = 512 threads x 8 arcs;
+//   tile j = arcs [j*T, (j+1)*T), T = GEE_TILE_ARCS = 256 threads x 16 arcs;
 //   tile j OWNS the rows whose first-arc position offsets[r] lies in it;
-//   tile_row[j] = first owned row (gee_pull_plan, a lower_bound per tile).
-//   One persistent 512-thread CTA per SM walks tiles j = blockIdx.x,
-//   += gridDim.x through a two-stage software pipeline: while tile j is
-//   accumulated, tile j+G's labels are being gathered and its row offsets
-//   staged (cp.async), and tile j+2G's arcs stream in (128-bit, L2
-//   evict-first).  Targets are label-table slots (gee_common.cuh): the hot
-//   tier's head is staged in shared memory, the rest of the table is read
-//   through L2 (evict-last).  Rows use 32-bit tile-local offsets; a warp
-//   brackets its first arc with two 32-way ballots and each lane gallops to
-//   its own.  Rows that run past their owner tile (hubs) are
-//   summed exactly through 64-bit global atomics into the owner tile's slot
-//   and written by k_pull_finalize.
+//   tile_row[j] = first owned row, chunk_row[c] = row of the first arc of
+//   each 16-arc chunk relative to the tile's first row (gee_pull_plan).
+//
+// Pipeline.  One persistent CTA per SM runs GROUPS independent 256-thread
+// groups (named barriers), each walking its own tiles.  While a group
+// accumulates tile j it already has tile j+1's labels in flight (cp.async
+// 4-byte gathers into shared memory; hot-tier labels copied from the
+// shared-memory head) and tile j+2's arcs in flight (128-bit streaming loads
+// into registers).  Measured on C4 (profiles/): label gathers dominate, and
+// they only approach the L1TEX limit (~1 random gather/clk/SM) when their
+// latency is hidden this way.
+//
+// Only nonempty rows are written here, from a compact window of their
+// accumulators; k_zero_empty zero-fills the rows without arcs (55% of C4's
+// rows).  Rows that run past their owner tile (hubs) are summed exactly
+// through 64-bit global atomics into the owner tile's slot and written by
+// k_pull_finalize over the planned list of cut tiles.
+#include <cstdio>
 #include <cstdlib>
 
 #include "gee_common.cuh"
 
 namespace {
 
-constexpr int GROUPS = 4;                // independent tile pipelines per CTA
+constexpr int GROUPS = 2;                // independent tile pipelines per CTA
 constexpr int GT = 256;                  // threads per group (8 warps)
 constexpr int PT = GROUPS * GT;          // threads per CTA (one persistent CTA per SM)
-constexpr int APT = 8;                   // arcs per thread
-constexpr int TILE = GT * APT;           // 2048 arcs per tile
+constexpr int APT = 16;                  // arcs per thread (one chunk)
+constexpr int TILE = GT * APT;           // 4096 arcs per tile
 static_assert(TILE == GEE_TILE_ARCS, "tile size mismatch with header");
 constexpr int SMEM_BYTES_MAX = 227 * 1024;  // opt-in maximum per CTA on sm_100a (queried at launch)
-constexpr int WROWS = GT;                // rows per window (one per thread)
+constexpr int WROWS = 2 * GT;            // rows per window (two per thread)
 constexpr int OFF_MAX = WROWS + 1;       // staged offsets per buffer
-constexpr int WIN_HOT_BYTES = 16 * 1024; // per-group window when a hot tier wants the smem
+constexpr int WIN_HOT_BYTES = 24 * 1024; // per-group window when a hot tier wants the smem
+constexpr uint16_t CHUNK_FAR = 0xffff;   // chunk_row overflow: search instead
 
 __device__ __forceinline__ int64_t lower_bound_i64(const int64_t *__restrict__ a, int64_t lo,
                                                    int64_t hi, int64_t key)
@@ -75,6 +82,48 @@ __global__ void k_pull_plan(const int64_t *__restrict__ offsets, int64_t n, int6
     tile_row[j] = lower_bound_i64(offsets, 0, n + 1, key);
 }
 
+// First row of tile j including a head row that started in an earlier tile.
+__device__ __forceinline__ int64_t tile_base(const int64_t *__restrict__ offsets,
+                                             const int64_t *__restrict__ tile_row, int64_t j)
+{
+    const int64_t r0 = tile_row[j];
+    return offsets[r0] > j * (int64_t)TILE ? r0 - 1 : r0;
+}
+
+// chunk_row[c] = (row holding arc c*APT) - tile_base, or CHUNK_FAR.
+__global__ void k_chunk_rows(const int64_t *__restrict__ offsets, const int64_t *__restrict__ tile_row,
+                             int64_t arcs, uint16_t *__restrict__ chunk_row)
+{
+    const int64_t chunks = (arcs + APT - 1) / APT;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = c * APT, j = e / TILE;
+        const int64_t base = tile_base(offsets, tile_row, j);
+        // last row r in [base, tile_row[j+1]] with offsets[r] <= e
+        const int64_t row = lower_bound_i64(offsets, base, tile_row[j + 1] + 1, e + 1) - 1;
+        const int64_t rel = row - base;
+        chunk_row[c] = (rel >= 0 && rel < CHUNK_FAR) ? (uint16_t)rel : CHUNK_FAR;
+    }
+}
+
+// Tiles whose last owned row continues into later tiles (finalize list).
+__global__ void k_cut_tiles(const int64_t *__restrict__ offsets, const int64_t *__restrict__ tile_row,
+                            int64_t arcs, int64_t n_tiles, int32_t *__restrict__ cut,
+                            unsigned long long *__restrict__ count)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_tiles;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r0 = tile_row[j], r1 = tile_row[j + 1];
+        const int64_t a1 = min((j + 1) * (int64_t)TILE, arcs);
+        if (r1 > r0 && offsets[r1] > a1) cut[atomicAdd(count, 1ull)] = (int32_t)j;
+    }
+}
+
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem, uint64_t pol)
+{
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(s), "l"(gmem), "l"(pol));
+}
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem)
 {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -87,39 +136,82 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __device__ __forceinline__ void group_sync(int g) { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(GT)); }
 
 struct GroupSmem {  // per-group shared state (carved from dynamic smem)
-    int64_t *off64;  // 2 x OFF_MAX staged offsets (cp.async double buffer)
-    int32_t *ol;     // OFF_MAX + 3 tile-local clamped offsets of the window
-    uint16_t *nzr;   // WROWS: rank of each nonempty row, 0xffff for empty rows
-    uint16_t *rrow;  // WROWS: window row of each rank
-    int32_t *wtot;   // 8 warp totals (+ 8 scratch)
-    uint32_t *lo;    // wnz * k
-    uint32_t *hi;    // wnz * k (weighted)
+    int64_t *off64;   // 2 x OFF_MAX staged offsets (cp.async double buffer)
+    uint32_t *lab;    // 2 x TILE label words (cp.async double buffer)
+    int32_t *ol;      // OFF_MAX + 3 tile-local clamped offsets of the window
+    uint16_t *nzr;    // WROWS: rank of each nonempty row, 0xffff for empty rows
+    uint16_t *rrow;   // WROWS: window row of each rank
+    int32_t *wtot;    // 8 warp totals (+ 8 scratch)
+    uint32_t *lo;     // wnz * k
+    uint32_t *hi;     // wnz * k (weighted)
+};
+
+struct Arcs {  // one tile's arcs for this thread (registers)
+    int32_t t[APT];
+    float w[APT];
+    int32_t r0, r1;  // tile_row[j], tile_row[j+1]
+    int32_t crow;    // chunk_row of this thread's chunk
 };
 
 template <bool WEIGHTED>
-__device__ __forceinline__ void load_arcs(int32_t (&t)[APT], float (&w)[APT], int64_t j, int gt,
-                                          const int32_t *__restrict__ targets, const float *__restrict__ wts,
-                                          int64_t arcs, int32_t sentinel)
+__device__ __forceinline__ void load_arcs(Arcs &A, int64_t j, int gt, const int32_t *__restrict__ targets,
+                                          const float *__restrict__ wts, const int64_t *__restrict__ tile_row,
+                                          const uint16_t *__restrict__ chunk_row, int64_t arcs, int32_t sentinel)
 {
     const int64_t e0 = j * (int64_t)TILE + (int64_t)gt * APT;
     if (e0 + APT <= arcs) {
 #pragma unroll
         for (int v = 0; v < APT / 4; v++) {
             const int4 t4 = __ldcs(reinterpret_cast<const int4 *>(targets + e0) + v);
-            t[4 * v] = t4.x; t[4 * v + 1] = t4.y; t[4 * v + 2] = t4.z; t[4 * v + 3] = t4.w;
+            A.t[4 * v] = t4.x; A.t[4 * v + 1] = t4.y; A.t[4 * v + 2] = t4.z; A.t[4 * v + 3] = t4.w;
             if (WEIGHTED) {
                 const float4 w4 = __ldcs(reinterpret_cast<const float4 *>(wts + e0) + v);
-                w[4 * v] = w4.x; w[4 * v + 1] = w4.y; w[4 * v + 2] = w4.z; w[4 * v + 3] = w4.w;
+                A.w[4 * v] = w4.x; A.w[4 * v + 1] = w4.y; A.w[4 * v + 2] = w4.z; A.w[4 * v + 3] = w4.w;
             }
         }
     } else {  // last tile: padding arcs read the sentinel slot (label 0)
 #pragma unroll
         for (int i = 0; i < APT; i++) {
             const bool ok = e0 + i < arcs;
-            t[i] = ok ? __ldcs(targets + e0 + i) : sentinel;
-            if (WEIGHTED) w[i] = ok ? __ldcs(wts + e0 + i) : 0.f;
+            A.t[i] = ok ? __ldcs(targets + e0 + i) : sentinel;
+            if (WEIGHTED) A.w[i] = ok ? __ldcs(wts + e0 + i) : 0.f;
         }
     }
+    A.crow = e0 < arcs ? (int32_t)__ldcs(chunk_row + e0 / APT) : 0;
+    A.r0 = (int32_t)tile_row[j];
+    A.r1 = (int32_t)tile_row[j + 1];
+}
+
+// Issue this thread's label fetches for a tile: hot-tier head labels are
+// copied from shared memory now, everything else lands via cp.async as the
+// containing aligned 4-byte word; returns the position of each label in its
+// word (2 bits per arc).
+template <typename LT>
+__device__ __forceinline__ uint32_t fetch_labels(uint32_t *buf, const Arcs &A, const LT *__restrict__ table,
+                                                 const LT *__restrict__ hot_s, uint32_t hot0, uint64_t pol)
+{
+    uint32_t pos = 0;
+#pragma unroll
+    for (int i = 0; i < APT; i++) {
+        const uint32_t t = (uint32_t)A.t[i];
+        if (t < hot0) {
+            buf[i] = (uint32_t)hot_s[t];
+        } else {
+            const uintptr_t addr = reinterpret_cast<uintptr_t>(table + t);
+            cp_async4(buf + i, reinterpret_cast<const void *>(addr & ~(uintptr_t)3), pol);
+            pos |= (uint32_t)((addr & 3) / sizeof(LT)) << (2 * i);
+        }
+    }
+    return pos;
+}
+
+template <typename LT>
+__device__ __forceinline__ uint32_t extract_label(uint32_t word, uint32_t pos, int i)
+{
+    const uint32_t p = (pos >> (2 * i)) & 3u;
+    if (sizeof(LT) == 1) return (word >> (8 * p)) & 0xffu;
+    if (sizeof(LT) == 2) return (word >> (16 * p)) & 0xffffu;
+    return word;
 }
 
 // Stage offsets[start .. start+cnt) into smem with cp.async (8 B per copy).
@@ -134,13 +226,13 @@ __device__ __forceinline__ void stage_offsets(int64_t *buf, const int64_t *__res
 template <bool WEIGHTED, typename LT>
 __global__ void __launch_bounds__(PT, 1)
 k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
-       const float *__restrict__ wts, int64_t arcs, const int64_t *__restrict__ tile_row, int64_t n_tiles,
-       float qscale, double dscale, const LT *__restrict__ table, int32_t sentinel, int32_t hot0,
-       const double *__restrict__ inv, int32_t k, float *__restrict__ z, unsigned long long *__restrict__ slots,
-       int wnz, int skip)
+       const float *__restrict__ wts, int64_t arcs, const int64_t *__restrict__ tile_row,
+       const uint16_t *__restrict__ chunk_row, int64_t n_tiles, float qscale, double dscale,
+       const LT *__restrict__ table, int32_t sentinel, int32_t hot0, const double *__restrict__ inv, int32_t k,
+       float *__restrict__ z, unsigned long long *__restrict__ slots, int wnz, int skip)
 {
     // skip: experiment mask (GEE_PULL_SKIP; results are wrong when set):
-    // 1 no label gathers, 2 no accumulation, 4 no Z write-out, 8 no row search
+    // 1 no label gathers, 2 no accumulation, 4 no Z write-out, 16 no partials
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid % GT;
@@ -156,6 +248,8 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         GroupSmem s;
         s.off64 = reinterpret_cast<int64_t *>(p);
         p += 2 * ((OFF_MAX + 1) & ~1) * sizeof(int64_t);
+        s.lab = reinterpret_cast<uint32_t *>(p);
+        p += 2 * TILE * sizeof(uint32_t);
         s.ol = reinterpret_cast<int32_t *>(p);
         p += ((OFF_MAX + 3 + 3) & ~3) * sizeof(int32_t);
         s.nzr = reinterpret_cast<uint16_t *>(p);
@@ -191,51 +285,50 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
     const int64_t stride = (int64_t)gridDim.x * GROUPS;
     int64_t j = (int64_t)blockIdx.x * GROUPS + g;
     if (j >= n_tiles) return;
-    int32_t R0 = (int32_t)tile_row[j], R1 = (int32_t)tile_row[j + 1];
+    const uint32_t uhot0 = (uint32_t)hot0;
+
+    // ---- prologue: tile j's labels + offsets in flight, tile j+stride's arcs loading
+    Arcs A;  // arcs two tiles ahead of the one being accumulated
+    load_arcs<WEIGHTED>(A, j, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
+    float wcur[APT], wnext[APT];
+    int32_t R0 = A.r0, R1 = A.r1, crow = A.crow;
+    uint32_t pos = 0, npos = 0;
+    int32_t nR0 = 0, nR1 = 0, ncrow = 0;
+    if (!(skip & 1)) pos = fetch_labels<LT>(G.lab + gt * APT, A, table, hot_s, uhot0, pol);
+#pragma unroll
+    for (int i = 0; i < APT; i++) wcur[i] = A.w[i];
     stage_offsets(G.off64, offsets, R0, R1, gt);
     cp_async_commit();
+    if (j + stride < n_tiles)
+        load_arcs<WEIGHTED>(A, j + stride, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
     int buf = 0;
 
     for (; j < n_tiles; j += stride) {
-        // ---- this tile's arcs and labels (the gathers overlap the row setup)
-        uint32_t lab[APT];
-        float wcur[APT];
-        {
-            int32_t t[APT];
-            if (skip & 32) {
-#pragma unroll
-                for (int i = 0; i < APT; i++) {
-                    t[i] = sentinel;
-                    wcur[i] = 1.f;
-                }
-            } else {
-                load_arcs<WEIGHTED>(t, wcur, j, gt, targets, wts, arcs, sentinel);
-            }
-#pragma unroll
-            for (int i = 0; i < APT; i++) {
-                const uint32_t ti = (uint32_t)t[i];
-                const bool in_smem = ti < (uint32_t)hot0;
-                uint32_t l = (uint32_t)hot_s[in_smem ? ti : 0u];
-                if (!in_smem && !(skip & 1)) l = gee::ld_label<LT>(table + ti, pol);
-                if (skip & 1) l = 1u + (ti & 1u);
-                lab[i] = l;
-            }
-        }
         const int64_t jn = j + stride;
-        int32_t R0n = 0, R1n = 0;
+        // ---- advance the pipeline: tile jn's labels + offsets, tile jn+stride's arcs
         if (jn < n_tiles) {
-            R0n = (int32_t)tile_row[jn];
-            R1n = (int32_t)tile_row[jn + 1];
+            if (!(skip & 1))
+                npos = fetch_labels<LT>(G.lab + (buf ^ 1) * TILE + gt * APT, A, table, hot_s, uhot0, pol);
+            nR0 = A.r0;
+            nR1 = A.r1;
+            ncrow = A.crow;
+#pragma unroll
+            for (int i = 0; i < APT; i++) wnext[i] = A.w[i];
+            stage_offsets(G.off64 + (buf ^ 1) * ((OFF_MAX + 1) & ~1), offsets, nR0, nR1, gt);
         }
+        cp_async_commit();
+        if (jn + stride < n_tiles)
+            load_arcs<WEIGHTED>(A, jn + stride, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
+        cp_async_wait<1>();  // tile j's labels and offsets have landed
 
         const int64_t a0 = j * (int64_t)TILE;
         const int tlen = (int)min((int64_t)TILE, arcs - a0);
         const int el0 = gt * APT;  // this thread's first arc, tile-local
-        int64_t *off_s = G.off64 + buf * ((OFF_MAX + 1) & ~1);
+        const int64_t *off_s = G.off64 + buf * ((OFF_MAX + 1) & ~1);
+        const uint32_t *labw = G.lab + buf * TILE + gt * APT;
         const int32_t st0 = R0 > 0 ? R0 - 1 : 0;  // first staged row
         const int32_t scnt = min(R1 - st0 + 1, OFF_MAX);
-        cp_async_wait<0>();
-        group_sync(g);  // staged offsets visible; this group's previous tile fully written out
+        group_sync(g);  // staged data visible; this group's previous tile fully written out
         const bool has_head = off_s[GEE_IDX(R0 - st0, OFF_MAX, 1)] > a0;  // also when R0 == n
         const int64_t offR1 = (R1 - st0 < scnt) ? off_s[GEE_IDX(R1 - st0, OFF_MAX, 2)] : __ldcs(offsets + R1);
         const bool tail_cut = (R1 > R0) && (offR1 > a0 + tlen);
@@ -244,30 +337,35 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         int32_t wrow0 = base;
         bool first = true;
         while (wrow0 < R1) {
-            // ---- window rows [wrow0, wrow0 + nr): tile-local int32 offsets,
-            // nonempty flags (one row per thread), ranks by warp + group scan
+            // ---- window rows [wrow0, wrow0 + nr): tile-local int32 offsets and
+            // nonempty flags (2 rows per thread), ranks by warp + group scan
             int nr = min(WROWS, R1 - wrow0);
-            int f = 0;
+            int f0 = 0, f1 = 0;
             {
-                int64_t o0 = 0, o1 = 0;
+                const int r = 2 * gt;
+                int64_t o0 = 0, o1 = 0, o2 = 0;
                 if (first && wrow0 - st0 + nr < scnt) {
                     const int sh = wrow0 - st0;
-                    if (gt <= nr) o0 = off_s[GEE_IDX(sh + gt, OFF_MAX, 3)];
-                    if (gt + 1 <= nr) o1 = off_s[GEE_IDX(sh + gt + 1, OFF_MAX, 3)];
+                    if (r <= nr) o0 = off_s[GEE_IDX(sh + r, OFF_MAX, 3)];
+                    if (r + 1 <= nr) o1 = off_s[GEE_IDX(sh + r + 1, OFF_MAX, 3)];
+                    if (r + 2 <= nr) o2 = off_s[GEE_IDX(sh + r + 2, OFF_MAX, 3)];
                 } else {
                     if (!first) group_sync(g);  // previous window fully consumed
-                    if (gt <= nr) o0 = __ldcs(offsets + wrow0 + gt);
-                    if (gt + 1 <= nr) o1 = __ldcs(offsets + wrow0 + gt + 1);
+                    if (r <= nr) o0 = __ldcs(offsets + wrow0 + r);
+                    if (r + 1 <= nr) o1 = __ldcs(offsets + wrow0 + r + 1);
+                    if (r + 2 <= nr) o2 = __ldcs(offsets + wrow0 + r + 2);
                 }
                 auto loc = [&](int64_t o) {
                     const int64_t v = o - a0;
                     return (int32_t)(v < 0 ? 0 : (v > TILE + 1 ? TILE + 1 : v));
                 };
-                if (gt <= nr) G.ol[gt] = loc(o0);
-                if (gt + 1 == nr + 0 && nr == WROWS) G.ol[nr] = loc(o1);  // no thread starts at row WROWS
-                if (gt < nr) f = o1 > o0;
+                if (r <= nr) G.ol[r] = loc(o0);
+                if (r + 1 <= nr) G.ol[r + 1] = loc(o1);
+                if (r + 2 == nr) G.ol[nr] = loc(o2);  // nr == WROWS: no thread starts there
+                if (r < nr) f0 = o1 > o0;
+                if (r + 1 < nr) f1 = o2 > o1;
             }
-            int incl = f;
+            int incl = f0 + f1;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const int v = __shfl_up_sync(0xffffffffu, incl, d);
@@ -282,11 +380,19 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                 wpre += q < gw ? v : 0;
                 nnz += v;
             }
-            const int rank = wpre + incl - f;  // rank of this thread's row if nonempty
-            if (gt < nr) {
-                G.nzr[gt] = f ? (uint16_t)rank : (uint16_t)0xffff;
-                if (f && rank < wnz) G.rrow[rank] = (uint16_t)gt;
-                if (f && rank == wnz) G.wtot[8] = gt;  // first row past a full window
+            {
+                const int r = 2 * gt;
+                const int rk0 = wpre + incl - f0 - f1, rk1 = rk0 + f0;
+                if (r < nr) {
+                    G.nzr[r] = f0 ? (uint16_t)rk0 : (uint16_t)0xffff;
+                    if (f0 && rk0 < wnz) G.rrow[rk0] = (uint16_t)r;
+                    if (f0 && rk0 == wnz) G.wtot[8] = r;  // first row past a full window
+                }
+                if (r + 1 < nr) {
+                    G.nzr[r + 1] = f1 ? (uint16_t)rk1 : (uint16_t)0xffff;
+                    if (f1 && rk1 < wnz) G.rrow[rk1] = (uint16_t)(r + 1);
+                    if (f1 && rk1 == wnz) G.wtot[8] = r + 1;
+                }
             }
             group_sync(g);
             if (nnz > wnz) {
@@ -297,31 +403,24 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
             const int32_t *ow = G.ol;
             const int wa0 = ow[0], wa1 = min(ow[GEE_IDX(nr, OFF_MAX, 15)], tlen);
             const int m0 = max(el0, wa0), m1 = min(el0 + APT, wa1);
-            const int ew = max(el0 - lane * APT, wa0);  // the warp's first arc in the window
-            int rw = 0;
-            if (ew < wa1) {  // warp-uniform: bracket the warp's first arc with two 32-way ballots
-                const int step = (nr + 31) >> 5;  // <= 8
-                int cand = min(lane * step, nr);
-                unsigned bal = __ballot_sync(0xffffffffu, ow[cand] <= ew);
-                const int b = (31 - __clz(bal)) * step;
-                cand = min(b + lane, nr);
-                bal = __ballot_sync(0xffffffffu, lane < step && ow[cand] <= ew);
-                rw = b + (31 - __clz(bal));
-            }
-            if (m0 < m1 && !(skip & 8)) {
-                int lo = rw, gl = 1;  // gallop to the last r with ow[r] <= m0
-                while (lo + gl < nr && ow[lo + gl] <= m0) {
-                    lo += gl;
-                    gl <<= 1;
+            if (m0 < m1) {
+                // row of m0: start from the planned chunk row, walk forward
+                int r = 0;
+                if (crow != CHUNK_FAR) {
+                    r = crow - (wrow0 - base);
+                    r = r < 0 ? 0 : (r >= nr ? nr - 1 : r);
                 }
-                int hi = min(lo + gl, nr);
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (ow[mid] <= m0) lo = mid;
-                    else hi = mid;
+                if (ow[GEE_IDX(r, OFF_MAX, 16)] > m0) {  // planned row beyond m0: search (rare)
+                    int lo = 0, hi = r;
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (ow[mid] <= m0) lo = mid;
+                        else hi = mid;
+                    }
+                    r = lo;
                 }
-                int r = lo;
                 int next = ow[GEE_IDX(r + 1, nr + 1, 4)];
+                while (m0 >= next) next = ow[GEE_IDX(++r + 1, nr + 1, 6)];
                 int slot = G.nzr[GEE_IDX(r, nr, 5)];
 #pragma unroll
                 for (int i = 0; i < APT; i++) {
@@ -332,8 +431,8 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                         while (e >= next);
                         slot = G.nzr[GEE_IDX(r, nr, 7)];
                     }
-                    const uint32_t c = lab[i];
-                    if (c == 0u || c > (uint32_t)kk || (skip & 2)) continue;  // unlabeled (or out-of-range raw label)
+                    const uint32_t c = (skip & 1) ? 1u + (i & 1) : extract_label<LT>(labw[i], pos, i);
+                    if (c == 0u || c > (uint32_t)kk || (skip & 2)) continue;  // unlabeled / out-of-range raw label
                     const int idx = GEE_IDX(slot * kk + (int)c - 1, wnz * kk, 8);
                     if (WEIGHTED) {
                         const unsigned long long q = (unsigned long long)__float2ll_rn(wcur[i] * qscale);
@@ -347,16 +446,12 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                     }
                 }
             }
-            // the next tile's offsets can be staged now (its buffer is free)
-            if (first && jn < n_tiles)
-                stage_offsets(G.off64 + (buf ^ 1) * ((OFF_MAX + 1) & ~1), offsets, R0n, R1n, gt);
-            if (first) cp_async_commit();
             group_sync(g);
 
             // ---- write out the window's complete nonempty rows (empty rows are
             // zeroed by k_zero_empty); flat over nnz x k, clearing what it reads
             {
-                const int32_t lr_lo = max(wrow0, R0) - wrow0;                       // a head row is partial
+                const int32_t lr_lo = max(wrow0, R0) - wrow0;                           // a head row is partial
                 const int32_t lr_hi = min(wrow0 + nr, tail_cut ? R1 - 1 : R1) - wrow0;  // so is a cut tail
                 const int total = (skip & 4) ? 0 : nnz * kk;
                 int c = gt % kk, s = gt / kk;
@@ -409,8 +504,13 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
             wrow0 += nr;
             first = false;
         }
-        R0 = R0n;
-        R1 = R1n;
+        // rotate the pipeline registers
+        R0 = nR0;
+        R1 = nR1;
+        crow = ncrow;
+        pos = npos;
+#pragma unroll
+        for (int i = 0; i < APT; i++) wcur[i] = wnext[i];
         buf ^= 1;
     }
     cp_async_wait<0>();
@@ -418,18 +518,15 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
 
 // Write the rows that spanned tiles from their owner's slot; re-zero slots.
 template <bool WEIGHTED>
-__global__ void k_pull_finalize(const int64_t *__restrict__ offsets, const int64_t *__restrict__ tile_row,
-                                int64_t arcs, int64_t n_tiles, unsigned long long *__restrict__ slots,
-                                const double *__restrict__ inv, int32_t k, double dscale,
-                                float *__restrict__ z)
+__global__ void k_pull_finalize(const int32_t *__restrict__ cut, int64_t n_cut, const int64_t *__restrict__ tile_row,
+                                unsigned long long *__restrict__ slots, const double *__restrict__ inv, int32_t k,
+                                double dscale, float *__restrict__ z)
 {
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
-    for (int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; j < n_tiles; j += warps) {
-        const int64_t R0 = tile_row[j], R1 = tile_row[j + 1];
-        const int64_t a1 = min((j + 1) * (int64_t)TILE, arcs);
-        if (!(R1 > R0 && offsets[R1] > a1)) continue;
-        const int64_t row = R1 - 1;
+    for (int64_t i = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; i < n_cut; i += warps) {
+        const int64_t j = cut[i];
+        const int64_t row = tile_row[j + 1] - 1;
         for (int c = lane; c < k; c += 32) {
             const unsigned long long v = slots[j * k + c];
             slots[j * k + c] = 0ull;
@@ -446,6 +543,8 @@ __global__ void k_zero_empty(const int64_t *__restrict__ offsets, int64_t n, int
 {
     const int lane = threadIdx.x & 31;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int c0 = lane % k, r0l = lane / k;
+    const int dc = 32 % k, dr = 32 / k;
     for (int64_t r0 = ((((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5) * 32; r0 < n; r0 += warps * 32) {
         const int64_t r = r0 + lane;
         const bool empty = r < n && __ldcs(offsets + r + 1) == __ldcs(offsets + r);
@@ -454,8 +553,7 @@ __global__ void k_zero_empty(const int64_t *__restrict__ offsets, int64_t n, int
         const int rows = (int)min((int64_t)32, n - r0);
         const int total = rows * k;
         float *zo = z + r0 * (int64_t)k;
-        int c = lane % k, rr = lane / k;
-        const int dc = 32 % k, dr = 32 / k;
+        int c = c0, rr = r0l;
         for (int e = lane; e < total; e += 32) {
             if ((mask >> rr) & 1u) __stcs(zo + e, 0.f);
             c += dc;
@@ -470,8 +568,8 @@ __global__ void k_zero_empty(const int64_t *__restrict__ offsets, int64_t n, int
 
 size_t group_fixed_smem()
 {
-    return 2 * ((OFF_MAX + 1) & ~1) * sizeof(int64_t) + ((OFF_MAX + 3 + 3) & ~3) * sizeof(int32_t) +
-           2 * WROWS * sizeof(uint16_t) + 16 * sizeof(int32_t);
+    return 2 * ((OFF_MAX + 1) & ~1) * sizeof(int64_t) + 2 * TILE * sizeof(uint32_t) +
+           ((OFF_MAX + 3 + 3) & ~3) * sizeof(int32_t) + 2 * WROWS * sizeof(uint16_t) + 16 * sizeof(int32_t);
 }
 
 struct PullShape {
@@ -504,8 +602,9 @@ PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes, s
 
 template <bool WEIGHTED, typename LT>
 int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n, int64_t arcs,
-                const int64_t *tile_row, int32_t scale_exp, const LT *table, int64_t n_hot, const double *inv,
-                int32_t k, float *z, unsigned long long *slots, cudaStream_t st)
+                const int64_t *tile_row, const uint16_t *chunk_row, const int32_t *cut, int64_t n_cut,
+                int32_t scale_exp, const LT *table, int64_t n_hot, const double *inv, int32_t k, float *z,
+                unsigned long long *slots, cudaStream_t st)
 {
     const int64_t n_tiles = gee_pull_tiles(arcs);
     static int optin = 0;
@@ -532,17 +631,27 @@ int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, 
     const int32_t sentinel = (int32_t)(n_hot + n);
     static const int skip = getenv("GEE_PULL_SKIP") ? atoi(getenv("GEE_PULL_SKIP")) : 0;
     if (getenv("GEE_PULL_VERBOSE"))
-        fprintf(stderr, "k_pull grid %d x %d smem %zu wnz %d hot0 %d tiles %lld skip %d\n", grid, PT, ps.smem, ps.wnz,
-                ps.hot0, (long long)n_tiles, skip);
-    kern<<<grid, PT, ps.smem, st>>>(offsets, targets, w, arcs, tile_row, n_tiles, qscale, dscale, table, sentinel,
-                                    ps.hot0, inv, k, z, slots, ps.wnz, skip);
+        fprintf(stderr, "k_pull grid %d x %d smem %zu wnz %d hot0 %d tiles %lld cut %lld skip %d\n", grid, PT, ps.smem,
+                ps.wnz, ps.hot0, (long long)n_tiles, (long long)n_cut, skip);
+    kern<<<grid, PT, ps.smem, st>>>(offsets, targets, w, arcs, tile_row, chunk_row, n_tiles, qscale, dscale, table,
+                                    sentinel, ps.hot0, inv, k, z, slots, ps.wnz, skip);
     int rc = gee::check_launch("k_pull");
     if (rc) return rc;
-    const int64_t want = (n_tiles * 32 + 255) / 256;
-    const int64_t fcap = (int64_t)gee::sm_count() * 16;
-    const int fgrid = (int)(want < 1 ? 1 : (want > fcap ? fcap : want));
-    k_pull_finalize<WEIGHTED><<<fgrid, 256, 0, st>>>(offsets, tile_row, arcs, n_tiles, slots, inv, k, dscale, z);
-    return gee::check_launch("k_pull_finalize");
+    if (n_cut > 0) {
+        const int64_t want = (n_cut * 32 + 255) / 256;
+        const int64_t fcap = (int64_t)gee::sm_count() * 16;
+        const int fgrid = (int)(want < 1 ? 1 : (want > fcap ? fcap : want));
+        k_pull_finalize<WEIGHTED><<<fgrid, 256, 0, st>>>(cut, n_cut, tile_row, slots, inv, k, dscale, z);
+        rc = gee::check_launch("k_pull_finalize");
+    }
+    return rc;
+}
+
+int grid_for(int64_t items)
+{
+    int64_t want = (items + 255) / 256;
+    int64_t cap = (int64_t)gee::sm_count() * 16;
+    return (int)(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
 }  // namespace
@@ -565,20 +674,40 @@ int gee_debug_word(unsigned int *out4)
 
 int64_t gee_pull_tiles(int64_t arcs) { return arcs <= 0 ? 0 : (arcs + TILE - 1) / TILE; }
 
+int64_t gee_pull_chunks(int64_t arcs) { return arcs <= 0 ? 0 : (arcs + APT - 1) / APT; }
+
 size_t gee_pull_slots_bytes(int64_t arcs, int32_t k)
 {
     int64_t t = gee_pull_tiles(arcs);
     return (size_t)(t ? t : 1) * (size_t)(k > 0 ? k : 1) * sizeof(unsigned long long);
 }
 
-int gee_pull_plan(const int64_t *offsets, int64_t n, int64_t arcs, int64_t *tile_row, void *stream)
+int gee_pull_plan(const int64_t *offsets, int64_t n, int64_t arcs, int64_t *tile_row, uint16_t *chunk_row,
+                  int32_t *cut_tiles, int64_t *n_cut, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(n >= 0 && arcs >= 0, GEE_ERR_INVALID, "n and arcs must be nonnegative");
+    GEE_REQUIRE(n_cut != nullptr, GEE_ERR_INVALID, "n_cut must not be NULL");
     const int64_t n_tiles = gee_pull_tiles(arcs);
     cudaStream_t st = gee::as_stream(stream);
+    *n_cut = 0;
     k_pull_plan<<<(unsigned)((n_tiles + 1 + 255) / 256), 256, 0, st>>>(offsets, n, arcs, n_tiles, tile_row);
-    return gee::check_launch("k_pull_plan");
+    int rc = gee::check_launch("k_pull_plan");
+    if (rc || n_tiles == 0) return rc;
+    GEE_REQUIRE(chunk_row && cut_tiles, GEE_ERR_INVALID, "chunk_row / cut_tiles must not be NULL");
+    k_chunk_rows<<<grid_for(gee_pull_chunks(arcs)), 256, 0, st>>>(offsets, tile_row, arcs, chunk_row);
+    if ((rc = gee::check_launch("k_chunk_rows"))) return rc;
+    unsigned long long *cnt = nullptr;
+    unsigned long long h = 0;
+    GEE_CUDA(cudaMallocAsync((void **)&cnt, sizeof(unsigned long long), st));
+    GEE_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+    k_cut_tiles<<<grid_for(n_tiles), 256, 0, st>>>(offsets, tile_row, arcs, n_tiles, cut_tiles, cnt);
+    rc = gee::check_launch("k_cut_tiles");
+    cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(cnt, st);
+    GEE_CUDA(cudaStreamSynchronize(st));
+    *n_cut = (int64_t)h;
+    return rc;
 }
 
 int gee_pull_scale_exp(double max_row_abs, double min_abs_nz, int32_t *scale_exp, double *rel_err)
@@ -600,26 +729,29 @@ int gee_pull_scale_exp(double max_row_abs, double min_abs_nz, int32_t *scale_exp
 }
 
 int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n, int64_t arcs,
-                       const int64_t *tile_row, int32_t scale_exp, const void *table, int64_t n_hot,
-                       const double *inv, int32_t k, float *z, void *slots, void *stream)
+                       const int64_t *tile_row, const uint16_t *chunk_row, const int32_t *cut_tiles, int64_t n_cut,
+                       int32_t scale_exp, const void *table, int64_t n_hot, const double *inv, int32_t k, float *z,
+                       void *slots, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1, GEE_ERR_INVALID, "class count k must be positive (got %d)", k);
-    GEE_REQUIRE(n >= 0 && arcs >= 0 && n_hot >= 0, GEE_ERR_INVALID, "n, arcs and n_hot must be nonnegative");
+    GEE_REQUIRE(n >= 0 && arcs >= 0 && n_hot >= 0 && n_cut >= 0, GEE_ERR_INVALID,
+                "n, arcs, n_hot and n_cut must be nonnegative");
     GEE_REQUIRE(n + n_hot < INT32_MAX, GEE_ERR_INVALID, "label table exceeds int32 slots");
     cudaStream_t st = gee::as_stream(stream);
     if (n == 0) return GEE_OK;
     GEE_REQUIRE(offsets && tile_row && z, GEE_ERR_INVALID, "NULL array argument");
-    // Rows with no arcs (isolated vertices, trailing rows) are zeroed by
-    // k_zero_empty; the pull kernel writes exactly the nonempty rows.
     if (arcs == 0) {
         GEE_CUDA(cudaMemsetAsync(z, 0, sizeof(float) * (size_t)n * k, st));
         return GEE_OK;
     }
-    GEE_REQUIRE(targets && table && inv && slots, GEE_ERR_INVALID, "NULL array argument");
+    GEE_REQUIRE(targets && chunk_row && table && inv && slots && (n_cut == 0 || cut_tiles), GEE_ERR_INVALID,
+                "NULL array argument");
     GEE_REQUIRE(gee::aligned16(targets) && (!w || gee::aligned16(w)) && gee::aligned16(table), GEE_ERR_INVALID,
                 "targets/weights/table must be 16-byte aligned");
     {
+        // Rows with no arcs (isolated vertices, trailing rows) are zeroed
+        // here; the pull kernel writes exactly the nonempty rows.
         const int64_t warps = (n + 31) / 32;
         const int64_t want = (warps * 32 + 255) / 256;
         const int64_t cap = (int64_t)gee::sm_count() * 8;
@@ -631,18 +763,24 @@ int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const flo
     switch (gee_label_bytes(k)) {
     case 1: {
         const auto *t = static_cast<const uint8_t *>(table);
-        return w ? launch_pull<true, uint8_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st)
-                 : launch_pull<false, uint8_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st);
+        return w ? launch_pull<true, uint8_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+                                              scale_exp, t, n_hot, inv, k, z, sl, st)
+                 : launch_pull<false, uint8_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+                                               scale_exp, t, n_hot, inv, k, z, sl, st);
     }
     case 2: {
         const auto *t = static_cast<const uint16_t *>(table);
-        return w ? launch_pull<true, uint16_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st)
-                 : launch_pull<false, uint16_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st);
+        return w ? launch_pull<true, uint16_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+                                               scale_exp, t, n_hot, inv, k, z, sl, st)
+                 : launch_pull<false, uint16_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+                                                scale_exp, t, n_hot, inv, k, z, sl, st);
     }
     default: {
         const auto *t = static_cast<const int32_t *>(table);
-        return w ? launch_pull<true, int32_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st)
-                 : launch_pull<false, int32_t>(offsets, targets, w, n, arcs, tile_row, scale_exp, t, n_hot, inv, k, z, sl, st);
+        return w ? launch_pull<true, int32_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+                                              scale_exp, t, n_hot, inv, k, z, sl, st)
+                 : launch_pull<false, int32_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+                                               scale_exp, t, n_hot, inv, k, z, sl, st);
     }
     }
 }

@@ -54,6 +54,9 @@ class DeviceGraph:
         self.device = device
         self.offsets = self.targets = self.weights = None
         self.tile_row = None
+        self.chunk_row = None  # u16 per 16-arc chunk (gee_pull_plan)
+        self.cut_tiles = None  # tiles whose last row continues into later tiles
+        self.n_cut = 0
         self.scale_exp = 0
         self.rel_err = 0.0
         self.max_row_abs = 0.0
@@ -129,7 +132,12 @@ class DeviceGraph:
         arcs = self.arcs
         n_tiles = int(lib.gee_pull_tiles(arcs))
         self.tile_row = torch.empty(n_tiles + 1, dtype=torch.int64, device=self.device)
-        check(lib.gee_pull_plan(ptr(self.offsets), self.n, arcs, ptr(self.tile_row), _stream()), "gee_pull_plan")
+        self.chunk_row = torch.empty(max(int(lib.gee_pull_chunks(arcs)), 1), dtype=torch.int16, device=self.device)
+        self.cut_tiles = torch.empty(max(n_tiles, 1), dtype=torch.int32, device=self.device)
+        nc = ctypes.c_int64()
+        check(lib.gee_pull_plan(ptr(self.offsets), self.n, arcs, ptr(self.tile_row), ptr(self.chunk_row),
+                                ptr(self.cut_tiles), ctypes.byref(nc), _stream()), "gee_pull_plan")
+        self.n_cut = int(nc.value)
         mx, mn, mxa = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         nf = ctypes.c_int32()
         check(lib.gee_graph_stats(ptr(self.offsets), ptr(self.weights), self.n, arcs, ctypes.byref(mx),
@@ -272,8 +280,9 @@ class Embedder:
             z = torch.empty((g.n, self.k), dtype=torch.float32, device=self.device)
         self._ensure_slots(g.arcs)
         check(lib.gee_embed_csr_pull(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
-                                     ptr(g.tile_row), g.scale_exp, ptr(self.table), g.n_hot, ptr(self.inv64),
-                                     self.k, ptr(z), ptr(self.slots), _stream()), "gee_embed_csr_pull")
+                                     ptr(g.tile_row), ptr(g.chunk_row), ptr(g.cut_tiles), g.n_cut, g.scale_exp,
+                                     ptr(self.table), g.n_hot, ptr(self.inv64), self.k, ptr(z), ptr(self.slots),
+                                     _stream()), "gee_embed_csr_pull")
         return z
 
     # ------------------------------------------------------------------ K3
