@@ -185,6 +185,20 @@ int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const flo
                        int32_t scale_exp, const void *table, int64_t n_hot, const double *inv,
                        int32_t k, float *z, void *slots, void *stream);
 
+/* Class stream: cls[e] = table[targets[e]] (u8, k <= 255) for every arc of
+ * a pull layout -- the random half of the pull pass on its own (label-table
+ * head staged in shared memory; measurement and split-pass use). */
+int gee_gather_labels(const int32_t *targets, int64_t arcs, const void *table, int64_t n_hot,
+                      int32_t k, uint8_t *cls, void *stream);
+
+/* Split pull: the same edge map over the class stream from
+ * gee_gather_labels (cls[e] = label of arc e's target, k <= 255) instead
+ * of gathering labels itself. */
+int gee_embed_csr_pull_cls(const int64_t *offsets, const uint8_t *cls, const float *w, int64_t n,
+                           int64_t arcs, const int64_t *tile_row, const uint16_t *chunk_row,
+                           const int32_t *cut_tiles, int64_t n_cut, int32_t scale_exp,
+                           const double *inv, int32_t k, float *z, void *slots, void *stream);
+
 /* Choose the fixed-point exponent for a weighted pull: the largest e with
  * max_row_abs * 2^e < 2^62.  Returns the relative quantisation bound
  * 2^-(e+1)/min_abs_nz through *rel_err (host). */

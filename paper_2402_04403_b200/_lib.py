@@ -60,6 +60,8 @@ SIGNATURES = {
     "gee_embed_csr_pull": (c_int, [vp, vp, vp, c_i64, c_i64, vp, vp, vp, c_i64, c_i32, vp, c_i64, vp, c_i32, vp, vp,
                                    vp]),
     "gee_pull_scale_exp": (c_int, [c_dbl, c_dbl, P_i32, P_dbl]),
+    "gee_gather_labels": (c_int, [vp, c_i64, vp, c_i64, c_i32, vp, vp]),
+    "gee_embed_csr_pull_cls": (c_int, [vp, vp, vp, c_i64, c_i64, vp, vp, vp, c_i64, c_i32, vp, c_i32, vp, vp, vp]),
     "gee_synth_word": (c_u64, [c_u64, c_u64, c_u64]),
     "gee_synth_rmat": (c_int, [vp, vp, vp, c_i64, c_i64, c_i32, c_dbl, c_dbl, c_dbl, c_u64, c_i32, vp]),
     "gee_synth_er": (c_int, [vp, vp, vp, c_i64, c_i64, c_i64, c_u64, vp]),

@@ -153,12 +153,41 @@ struct Arcs {  // one tile's arcs for this thread (registers)
     int32_t crow;    // chunk_row of this thread's chunk
 };
 
-template <bool WEIGHTED>
+template <bool WEIGHTED, bool CLS>
 __device__ __forceinline__ void load_arcs(Arcs &A, int64_t j, int gt, const int32_t *__restrict__ targets,
                                           const float *__restrict__ wts, const int64_t *__restrict__ tile_row,
                                           const uint16_t *__restrict__ chunk_row, int64_t arcs, int32_t sentinel)
 {
     const int64_t e0 = j * (int64_t)TILE + (int64_t)gt * APT;
+    if (CLS) {  // class stream (gee_gather_labels): 16 class bytes per chunk, 0 past the end
+        const uint8_t *cls = reinterpret_cast<const uint8_t *>(targets);
+        if (e0 + APT <= arcs) {
+            const uint4 c4 = __ldcs(reinterpret_cast<const uint4 *>(cls + e0));
+            A.t[0] = (int32_t)c4.x; A.t[1] = (int32_t)c4.y; A.t[2] = (int32_t)c4.z; A.t[3] = (int32_t)c4.w;
+        } else {
+            uint32_t wd[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int i = 0; i < APT; i++)
+                if (e0 + i < arcs) wd[i >> 2] |= (uint32_t)cls[e0 + i] << (8 * (i & 3));
+            A.t[0] = (int32_t)wd[0]; A.t[1] = (int32_t)wd[1]; A.t[2] = (int32_t)wd[2]; A.t[3] = (int32_t)wd[3];
+        }
+        if (WEIGHTED) {
+            if (e0 + APT <= arcs) {
+#pragma unroll
+                for (int v = 0; v < APT / 4; v++) {
+                    const float4 w4 = __ldcs(reinterpret_cast<const float4 *>(wts + e0) + v);
+                    A.w[4 * v] = w4.x; A.w[4 * v + 1] = w4.y; A.w[4 * v + 2] = w4.z; A.w[4 * v + 3] = w4.w;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < APT; i++) A.w[i] = e0 + i < arcs ? __ldcs(wts + e0 + i) : 0.f;
+            }
+        }
+        A.crow = e0 < arcs ? (int32_t)__ldcs(chunk_row + e0 / APT) : 0;
+        A.r0 = (int32_t)tile_row[j];
+        A.r1 = (int32_t)tile_row[j + 1];
+        return;
+    }
     if (e0 + APT <= arcs) {
 #pragma unroll
         for (int v = 0; v < APT / 4; v++) {
@@ -223,7 +252,7 @@ __device__ __forceinline__ void stage_offsets(int64_t *buf, const int64_t *__res
     for (int i = gt; i < cnt; i += GT) cp_async8(buf + i, offsets + start + i);
 }
 
-template <bool WEIGHTED, typename LT>
+template <bool WEIGHTED, typename LT, bool CLS>
 __global__ void __launch_bounds__(PT, 1)
 k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
        const float *__restrict__ wts, int64_t arcs, const int64_t *__restrict__ tile_row,
@@ -289,26 +318,36 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
 
     // ---- prologue: tile j's labels + offsets in flight, tile j+stride's arcs loading
     Arcs A;  // arcs two tiles ahead of the one being accumulated
-    load_arcs<WEIGHTED>(A, j, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
+    load_arcs<WEIGHTED, CLS>(A, j, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
     float wcur[APT], wnext[APT];
+    uint32_t cw[4] = {0u, 0u, 0u, 0u}, ncw[4] = {0u, 0u, 0u, 0u};  // class words (CLS mode)
     int32_t R0 = A.r0, R1 = A.r1, crow = A.crow;
     uint32_t pos = 0, npos = 0;
     int32_t nR0 = 0, nR1 = 0, ncrow = 0;
-    if (!(skip & 1)) pos = fetch_labels<LT>(G.lab + gt * APT, A, table, hot_s, uhot0, pol);
+    if (CLS) {
+#pragma unroll
+        for (int v = 0; v < 4; v++) cw[v] = (uint32_t)A.t[v];
+    } else if (!(skip & 1)) {
+        pos = fetch_labels<LT>(G.lab + gt * APT, A, table, hot_s, uhot0, pol);
+    }
 #pragma unroll
     for (int i = 0; i < APT; i++) wcur[i] = A.w[i];
     stage_offsets(G.off64, offsets, R0, R1, gt);
     cp_async_commit();
     if (j + stride < n_tiles)
-        load_arcs<WEIGHTED>(A, j + stride, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
+        load_arcs<WEIGHTED, CLS>(A, j + stride, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
     int buf = 0;
 
     for (; j < n_tiles; j += stride) {
         const int64_t jn = j + stride;
         // ---- advance the pipeline: tile jn's labels + offsets, tile jn+stride's arcs
         if (jn < n_tiles) {
-            if (!(skip & 1))
+            if (CLS) {
+#pragma unroll
+                for (int v = 0; v < 4; v++) ncw[v] = (uint32_t)A.t[v];
+            } else if (!(skip & 1)) {
                 npos = fetch_labels<LT>(G.lab + (buf ^ 1) * TILE + gt * APT, A, table, hot_s, uhot0, pol);
+            }
             nR0 = A.r0;
             nR1 = A.r1;
             ncrow = A.crow;
@@ -318,7 +357,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         }
         cp_async_commit();
         if (jn + stride < n_tiles)
-            load_arcs<WEIGHTED>(A, jn + stride, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
+            load_arcs<WEIGHTED, CLS>(A, jn + stride, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
         cp_async_wait<1>();  // tile j's labels and offsets have landed
 
         const int64_t a0 = j * (int64_t)TILE;
@@ -431,7 +470,8 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
                         while (e >= next);
                         slot = G.nzr[GEE_IDX(r, nr, 7)];
                     }
-                    const uint32_t c = (skip & 1) ? 1u + (i & 1) : extract_label<LT>(labw[i], pos, i);
+                    const uint32_t c = CLS ? ((cw[i >> 2] >> (8 * (i & 3))) & 0xffu)
+                                           : ((skip & 1) ? 1u + (i & 1) : extract_label<LT>(labw[i], pos, i));
                     if (c == 0u || c > (uint32_t)kk || (skip & 2)) continue;  // unlabeled / out-of-range raw label
                     const int idx = GEE_IDX(slot * kk + (int)c - 1, wnz * kk, 8);
                     if (WEIGHTED) {
@@ -509,6 +549,8 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         R1 = nR1;
         crow = ncrow;
         pos = npos;
+#pragma unroll
+        for (int v = 0; v < 4; v++) cw[v] = ncw[v];
 #pragma unroll
         for (int i = 0; i < APT; i++) wcur[i] = wnext[i];
         buf ^= 1;
@@ -600,7 +642,7 @@ PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes, s
     return p;
 }
 
-template <bool WEIGHTED, typename LT>
+template <bool WEIGHTED, typename LT, bool CLS>
 int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, int64_t n, int64_t arcs,
                 const int64_t *tile_row, const uint16_t *chunk_row, const int32_t *cut, int64_t n_cut,
                 int32_t scale_exp, const LT *table, int64_t n_hot, const double *inv, int32_t k, float *z,
@@ -615,9 +657,13 @@ int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, 
             optin = 48 * 1024;
     }
     const size_t budget = (size_t)(optin < SMEM_BYTES_MAX ? optin : SMEM_BYTES_MAX);
-    const PullShape ps = pull_shape(k, WEIGHTED, n_hot, (int)sizeof(LT), budget);
+    // The hot tier is read through L1/L2: staging its head in shared memory
+    // measured 3x slower on C4 (skewed LDS bank conflicts, and the carve-out
+    // starves L1); GEE_PULL_SMEM_HOT=1 re-enables it for experiments.
+    static const bool smem_hot = getenv("GEE_PULL_SMEM_HOT") != nullptr;
+    const PullShape ps = pull_shape(k, WEIGHTED, (CLS || !smem_hot) ? 0 : n_hot, (int)sizeof(LT), budget);
     GEE_REQUIRE(ps.wnz >= 1, GEE_ERR_INVALID, "k=%d too large for the pull window", k);
-    auto kern = k_pull<WEIGHTED, LT>;
+    auto kern = k_pull<WEIGHTED, LT, CLS>;
     {
         const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps.smem);
         GEE_REQUIRE(e == cudaSuccess, GEE_ERR_CUDA, "k_pull: %zu B dynamic smem (opt-in max %d, window %d rows, hot %d): %s",
@@ -763,26 +809,60 @@ int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const flo
     switch (gee_label_bytes(k)) {
     case 1: {
         const auto *t = static_cast<const uint8_t *>(table);
-        return w ? launch_pull<true, uint8_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+        return w ? launch_pull<true, uint8_t, false>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
                                               scale_exp, t, n_hot, inv, k, z, sl, st)
-                 : launch_pull<false, uint8_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+                 : launch_pull<false, uint8_t, false>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
                                                scale_exp, t, n_hot, inv, k, z, sl, st);
     }
     case 2: {
         const auto *t = static_cast<const uint16_t *>(table);
-        return w ? launch_pull<true, uint16_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+        return w ? launch_pull<true, uint16_t, false>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
                                                scale_exp, t, n_hot, inv, k, z, sl, st)
-                 : launch_pull<false, uint16_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+                 : launch_pull<false, uint16_t, false>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
                                                 scale_exp, t, n_hot, inv, k, z, sl, st);
     }
     default: {
         const auto *t = static_cast<const int32_t *>(table);
-        return w ? launch_pull<true, int32_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+        return w ? launch_pull<true, int32_t, false>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
                                               scale_exp, t, n_hot, inv, k, z, sl, st)
-                 : launch_pull<false, int32_t>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
+                 : launch_pull<false, int32_t, false>(offsets, targets, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut,
                                                scale_exp, t, n_hot, inv, k, z, sl, st);
     }
     }
+}
+
+int gee_embed_csr_pull_cls(const int64_t *offsets, const uint8_t *cls, const float *w, int64_t n, int64_t arcs,
+                           const int64_t *tile_row, const uint16_t *chunk_row, const int32_t *cut_tiles,
+                           int64_t n_cut, int32_t scale_exp, const double *inv, int32_t k, float *z, void *slots,
+                           void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs 1 <= k <= 255 (got %d)", k);
+    GEE_REQUIRE(n >= 0 && arcs >= 0 && n_cut >= 0, GEE_ERR_INVALID, "n, arcs and n_cut must be nonnegative");
+    cudaStream_t st = gee::as_stream(stream);
+    if (n == 0) return GEE_OK;
+    GEE_REQUIRE(offsets && tile_row && z, GEE_ERR_INVALID, "NULL array argument");
+    if (arcs == 0) {
+        GEE_CUDA(cudaMemsetAsync(z, 0, sizeof(float) * (size_t)n * k, st));
+        return GEE_OK;
+    }
+    GEE_REQUIRE(cls && chunk_row && inv && slots && (n_cut == 0 || cut_tiles), GEE_ERR_INVALID, "NULL array argument");
+    GEE_REQUIRE(gee::aligned16(cls) && (!w || gee::aligned16(w)), GEE_ERR_INVALID, "cls/weights must be 16-byte aligned");
+    {
+        const int64_t warps = (n + 31) / 32;
+        const int64_t want = (warps * 32 + 255) / 256;
+        const int64_t cap = (int64_t)gee::sm_count() * 8;
+        k_zero_empty<<<(int)(want < cap ? (want < 1 ? 1 : want) : cap), 256, 0, st>>>(offsets, n, k, z);
+        int rc = gee::check_launch("k_zero_empty");
+        if (rc) return rc;
+    }
+    auto *sl = reinterpret_cast<unsigned long long *>(slots);
+    const auto *tg = reinterpret_cast<const int32_t *>(cls);
+    const uint8_t *no_table = nullptr;
+    return w ? launch_pull<true, uint8_t, true>(offsets, tg, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut, scale_exp,
+                                                no_table, 0, inv, k, z, sl, st)
+             : launch_pull<false, uint8_t, true>(offsets, tg, w, n, arcs, tile_row, chunk_row, cut_tiles, n_cut, scale_exp,
+                                                 no_table, 0, inv, k, z, sl, st);
 }
 
 }  // extern "C"

@@ -7,6 +7,7 @@ to the CPU: without a CUDA device the calls raise.
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -231,6 +232,8 @@ class Embedder:
         self.table = None
         self.table_n_hot = None  # n_hot the current table was built with
         self.slots = None
+        self.cls = None  # class stream of the split pull
+        self.split = os.environ.get("GEE_PULL_FUSED") is None
 
     def _ensure_table(self, n_hot):
         need = int(lib.gee_label_table_bytes(self.n, n_hot, self.k))
@@ -279,6 +282,18 @@ class Embedder:
         if z is None:
             z = torch.empty((g.n, self.k), dtype=torch.float32, device=self.device)
         self._ensure_slots(g.arcs)
+        if self.split and self.k <= 255:
+            # split pass: class stream (random gathers, full occupancy), then
+            # the gather-free segmented reduction
+            if self.cls is None or self.cls.numel() < g.arcs + 16:
+                self.cls = torch.empty(g.arcs + 16, dtype=torch.uint8, device=self.device)
+            check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
+                                        _stream()), "gee_gather_labels")
+            check(lib.gee_embed_csr_pull_cls(ptr(g.offsets), ptr(self.cls), ptr(g.weights), g.n, g.arcs,
+                                             ptr(g.tile_row), ptr(g.chunk_row), ptr(g.cut_tiles), g.n_cut,
+                                             g.scale_exp, ptr(self.inv64), self.k, ptr(z), ptr(self.slots),
+                                             _stream()), "gee_embed_csr_pull_cls")
+            return z
         check(lib.gee_embed_csr_pull(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
                                      ptr(g.tile_row), ptr(g.chunk_row), ptr(g.cut_tiles), g.n_cut, g.scale_exp,
                                      ptr(self.table), g.n_hot, ptr(self.inv64), self.k, ptr(z), ptr(self.slots),
