@@ -1,8 +1,11 @@
 // Label-gather stream: cls[e] = table[targets[e]] for every arc (the random
-// half of the pull pass, isolated).  One persistent 1024-thread CTA per SM
-// stages the head of the label table (hot tier) in shared memory; each
-// thread streams 16 targets (4 x 128-bit), issues 16 independent gathers and
-// writes 16 class bytes (one 128-bit store).  No barriers after the prologue.
+// half of the pull pass, isolated).  One persistent 1024-thread CTA per SM;
+// each thread streams 16 targets (4 x 128-bit), issues 16 independent
+// gathers through L1/L2 (evict-last) and writes 16 class bytes (one 128-bit
+// store).  Nothing synchronises, so the gathers' latency is hidden by
+// occupancy and per-thread memory-level parallelism.
+#include <cstdlib>
+
 #include "gee_common.cuh"
 
 namespace {
@@ -72,8 +75,15 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
         if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
             optin = 48 * 1024;
     }
-    int64_t hot0 = (optin - 64) & ~15;
-    if (hot0 > n_hot) hot0 = n_hot & ~15;
+    // Hot labels are read through L1/L2: staging the hot tier's head in
+    // shared memory measured 3x slower on C4 (33 ms vs 10.8 ms for 3.6e9
+    // lookups: skewed LDS bank conflicts, and the carve-out starves L1).
+    // GEE_GATHER_SMEM_HOT=1 re-enables it for experiments.
+    int64_t hot0 = 0;
+    if (getenv("GEE_GATHER_SMEM_HOT")) {
+        hot0 = (optin - 64) & ~15;
+        if (hot0 > n_hot) hot0 = n_hot & ~15;
+    }
     const size_t sh = (size_t)hot0 + 16;
     auto kern = k_gather<uint8_t>;
     GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));

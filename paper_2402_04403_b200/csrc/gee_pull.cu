@@ -46,16 +46,18 @@
 
 namespace {
 
-constexpr int GROUPS = 2;                // independent tile pipelines per CTA
 constexpr int GT = 256;                  // threads per group (8 warps)
-constexpr int PT = GROUPS * GT;          // threads per CTA (one persistent CTA per SM)
+// independent tile pipelines per CTA: 2 when the kernel gathers labels
+// itself (128 registers per thread), 4 in the gather-free class-stream mode
+template <bool CLS>
+__host__ __device__ constexpr int groups_for() { return CLS ? 2 : 2; }
 constexpr int APT = 16;                  // arcs per thread (one chunk)
 constexpr int TILE = GT * APT;           // 4096 arcs per tile
 static_assert(TILE == GEE_TILE_ARCS, "tile size mismatch with header");
 constexpr int SMEM_BYTES_MAX = 227 * 1024;  // opt-in maximum per CTA on sm_100a (queried at launch)
 constexpr int WROWS = 2 * GT;            // rows per window (two per thread)
 constexpr int OFF_MAX = WROWS + 1;       // staged offsets per buffer
-constexpr int WIN_HOT_BYTES = 24 * 1024; // per-group window when a hot tier wants the smem
+constexpr int WIN_HOT_BYTES = 32 * 1024; // per-group window cap (the rest of smem is L1 or hot tier)
 constexpr uint16_t CHUNK_FAR = 0xffff;   // chunk_row overflow: search instead
 
 __device__ __forceinline__ int64_t lower_bound_i64(const int64_t *__restrict__ a, int64_t lo,
@@ -253,7 +255,7 @@ __device__ __forceinline__ void stage_offsets(int64_t *buf, const int64_t *__res
 }
 
 template <bool WEIGHTED, typename LT, bool CLS>
-__global__ void __launch_bounds__(PT, 1)
+__global__ void __launch_bounds__(groups_for<CLS>() * GT, 1)
 k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
        const float *__restrict__ wts, int64_t arcs, const int64_t *__restrict__ tile_row,
        const uint16_t *__restrict__ chunk_row, int64_t n_tiles, float qscale, double dscale,
@@ -262,6 +264,8 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
 {
     // skip: experiment mask (GEE_PULL_SKIP; results are wrong when set):
     // 1 no label gathers, 2 no accumulation, 4 no Z write-out, 16 no partials
+    constexpr int GROUPS = groups_for<CLS>();
+    constexpr int PT = GROUPS * GT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid % GT;
@@ -278,7 +282,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
         s.off64 = reinterpret_cast<int64_t *>(p);
         p += 2 * ((OFF_MAX + 1) & ~1) * sizeof(int64_t);
         s.lab = reinterpret_cast<uint32_t *>(p);
-        p += 2 * TILE * sizeof(uint32_t);
+        if (!CLS) p += 2 * TILE * sizeof(uint32_t);
         s.ol = reinterpret_cast<int32_t *>(p);
         p += ((OFF_MAX + 3 + 3) & ~3) * sizeof(int32_t);
         s.nzr = reinterpret_cast<uint16_t *>(p);
@@ -320,7 +324,7 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
     Arcs A;  // arcs two tiles ahead of the one being accumulated
     load_arcs<WEIGHTED, CLS>(A, j, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
     float wcur[APT], wnext[APT];
-    uint32_t cw[4] = {0u, 0u, 0u, 0u}, ncw[4] = {0u, 0u, 0u, 0u};  // class words (CLS mode)
+    uint32_t cw[4] = {0u, 0u, 0u, 0u};  // class words (CLS mode)
     int32_t R0 = A.r0, R1 = A.r1, crow = A.crow;
     uint32_t pos = 0, npos = 0;
     int32_t nR0 = 0, nR1 = 0, ncrow = 0;
@@ -341,23 +345,27 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
     for (; j < n_tiles; j += stride) {
         const int64_t jn = j + stride;
         // ---- advance the pipeline: tile jn's labels + offsets, tile jn+stride's arcs
-        if (jn < n_tiles) {
-            if (CLS) {
+        if constexpr (CLS) {
+            // class-stream mode keeps one register stage: A holds tile jn
+            // (classes, weights) and is rotated into the current stage at the
+            // end of this iteration, when tile jn+stride's load is issued
+            if (jn < n_tiles) stage_offsets(G.off64 + (buf ^ 1) * ((OFF_MAX + 1) & ~1), offsets, A.r0, A.r1, gt);
+            cp_async_commit();
+        } else {
+            if (jn < n_tiles) {
+                if (!(skip & 1))
+                    npos = fetch_labels<LT>(G.lab + (buf ^ 1) * TILE + gt * APT, A, table, hot_s, uhot0, pol);
+                nR0 = A.r0;
+                nR1 = A.r1;
+                ncrow = A.crow;
 #pragma unroll
-                for (int v = 0; v < 4; v++) ncw[v] = (uint32_t)A.t[v];
-            } else if (!(skip & 1)) {
-                npos = fetch_labels<LT>(G.lab + (buf ^ 1) * TILE + gt * APT, A, table, hot_s, uhot0, pol);
+                for (int i = 0; i < APT; i++) wnext[i] = A.w[i];
+                stage_offsets(G.off64 + (buf ^ 1) * ((OFF_MAX + 1) & ~1), offsets, nR0, nR1, gt);
             }
-            nR0 = A.r0;
-            nR1 = A.r1;
-            ncrow = A.crow;
-#pragma unroll
-            for (int i = 0; i < APT; i++) wnext[i] = A.w[i];
-            stage_offsets(G.off64 + (buf ^ 1) * ((OFF_MAX + 1) & ~1), offsets, nR0, nR1, gt);
+            cp_async_commit();
+            if (jn + stride < n_tiles)
+                load_arcs<WEIGHTED, CLS>(A, jn + stride, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
         }
-        cp_async_commit();
-        if (jn + stride < n_tiles)
-            load_arcs<WEIGHTED, CLS>(A, jn + stride, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
         cp_async_wait<1>();  // tile j's labels and offsets have landed
 
         const int64_t a0 = j * (int64_t)TILE;
@@ -545,14 +553,26 @@ k_pull(const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
             first = false;
         }
         // rotate the pipeline registers
-        R0 = nR0;
-        R1 = nR1;
-        crow = ncrow;
-        pos = npos;
+        if constexpr (CLS) {
+            if (jn < n_tiles) {
+                R0 = A.r0;
+                R1 = A.r1;
+                crow = A.crow;
 #pragma unroll
-        for (int v = 0; v < 4; v++) cw[v] = ncw[v];
+                for (int v = 0; v < 4; v++) cw[v] = (uint32_t)A.t[v];
 #pragma unroll
-        for (int i = 0; i < APT; i++) wcur[i] = wnext[i];
+                for (int i = 0; i < APT; i++) wcur[i] = A.w[i];
+                if (jn + stride < n_tiles)
+                    load_arcs<WEIGHTED, CLS>(A, jn + stride, gt, targets, wts, tile_row, chunk_row, arcs, sentinel);
+            }
+        } else {
+            R0 = nR0;
+            R1 = nR1;
+            crow = ncrow;
+            pos = npos;
+#pragma unroll
+            for (int i = 0; i < APT; i++) wcur[i] = wnext[i];
+        }
         buf ^= 1;
     }
     cp_async_wait<0>();
@@ -608,9 +628,9 @@ __global__ void k_zero_empty(const int64_t *__restrict__ offsets, int64_t n, int
     }
 }
 
-size_t group_fixed_smem()
+size_t group_fixed_smem(bool cls)
 {
-    return 2 * ((OFF_MAX + 1) & ~1) * sizeof(int64_t) + 2 * TILE * sizeof(uint32_t) +
+    return 2 * ((OFF_MAX + 1) & ~1) * sizeof(int64_t) + (cls ? 0 : 2 * TILE * sizeof(uint32_t)) +
            ((OFF_MAX + 3 + 3) & ~3) * sizeof(int32_t) + 2 * WROWS * sizeof(uint16_t) + 16 * sizeof(int32_t);
 }
 
@@ -620,15 +640,18 @@ struct PullShape {
     size_t smem;
 };
 
-PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes, size_t budget)
+PullShape pull_shape(int32_t k, bool weighted, int64_t n_hot, int label_bytes, size_t budget, bool cls)
 {
     PullShape p{0, 0, 0};
+    const int GROUPS = cls ? groups_for<true>() : groups_for<false>();
     const size_t sc = ((size_t)(k + 4) & ~(size_t)3) * sizeof(float);
     const size_t per_row = (size_t)k * sizeof(uint32_t) * (weighted ? 2 : 1);
-    const size_t fixed = sc + GROUPS * group_fixed_smem() + 64;
+    const size_t fixed = sc + GROUPS * group_fixed_smem(cls) + 64;
     if (fixed + GROUPS * (per_row + 16) > budget) return p;
-    size_t win_bytes = (budget - fixed) / GROUPS;  // no hot tier: windows take everything
-    if (n_hot > 0 && win_bytes > WIN_HOT_BYTES) win_bytes = WIN_HOT_BYTES > per_row ? WIN_HOT_BYTES : per_row;
+    size_t win_bytes = (budget - fixed) / GROUPS;
+    // windows hold a tile's nonempty rows; beyond ~WIN_HOT_BYTES per group the
+    // smem is worth more as L1 (the gathers go through it)
+    if (win_bytes > WIN_HOT_BYTES) win_bytes = WIN_HOT_BYTES > per_row ? WIN_HOT_BYTES : per_row;
     int wnz = (int)(win_bytes / per_row);
     if (wnz > WROWS) wnz = WROWS;
     const size_t plane = ((((size_t)wnz * k + 3) & ~(size_t)3) * sizeof(uint32_t));
@@ -661,7 +684,9 @@ int launch_pull(const int64_t *offsets, const int32_t *targets, const float *w, 
     // measured 3x slower on C4 (skewed LDS bank conflicts, and the carve-out
     // starves L1); GEE_PULL_SMEM_HOT=1 re-enables it for experiments.
     static const bool smem_hot = getenv("GEE_PULL_SMEM_HOT") != nullptr;
-    const PullShape ps = pull_shape(k, WEIGHTED, (CLS || !smem_hot) ? 0 : n_hot, (int)sizeof(LT), budget);
+    const PullShape ps = pull_shape(k, WEIGHTED, (CLS || !smem_hot) ? 0 : n_hot, (int)sizeof(LT), budget, CLS);
+    constexpr int GROUPS = groups_for<CLS>();
+    constexpr int PT = GROUPS * GT;
     GEE_REQUIRE(ps.wnz >= 1, GEE_ERR_INVALID, "k=%d too large for the pull window", k);
     auto kern = k_pull<WEIGHTED, LT, CLS>;
     {
