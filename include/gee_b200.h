@@ -199,6 +199,21 @@ int gee_embed_csr_pull_cls(const int64_t *offsets, const uint8_t *cls, const flo
                            const int32_t *cut_tiles, int64_t n_cut, int32_t scale_exp,
                            const double *inv, int32_t k, float *z, void *slots, void *stream);
 
+/* Row-per-warp segmented reduction over the class stream (the second half
+ * of the split pull; gee_reduce.cu).  Writes every row of Z: rows with no
+ * arcs as zeros, rows with at most heavy_arcs arcs directly, heavier rows
+ * (gee_reduce_heavy_plan lists them) through chunks of heavy_arcs arcs whose
+ * exact int64 partials meet in heavy_acc[n_heavy*k] (zero on first use, left
+ * zero).  chunk_first[q] / chunk_heavy[q]: first arc and heavy-row index of
+ * chunk q.  k <= 255. */
+int gee_reduce_heavy_plan(const int64_t *offsets, int64_t n, int64_t heavy_arcs,
+                          int32_t *heavy_rows, int64_t *n_heavy, void *stream);
+int gee_reduce_rows(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
+                    int32_t scale_exp, const double *inv, int32_t k, int64_t heavy_arcs,
+                    const int32_t *heavy_rows, int64_t n_heavy, const int64_t *chunk_first,
+                    const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
+                    void *stream);
+
 /* Choose the fixed-point exponent for a weighted pull: the largest e with
  * max_row_abs * 2^e < 2^62.  Returns the relative quantisation bound
  * 2^-(e+1)/min_abs_nz through *rel_err (host). */

@@ -58,6 +58,10 @@ class DeviceGraph:
         self.chunk_row = None  # u16 per 16-arc chunk (gee_pull_plan)
         self.cut_tiles = None  # tiles whose last row continues into later tiles
         self.n_cut = 0
+        # row-per-warp reducer (split pull): rows heavier than HEAVY_ARCS are
+        # split into chunks
+        self.heavy_rows = self.chunk_first = self.chunk_heavy = None
+        self.n_heavy = self.n_chunks = 0
         self.scale_exp = 0
         self.rel_err = 0.0
         self.max_row_abs = 0.0
@@ -139,6 +143,7 @@ class DeviceGraph:
         check(lib.gee_pull_plan(ptr(self.offsets), self.n, arcs, ptr(self.tile_row), ptr(self.chunk_row),
                                 ptr(self.cut_tiles), ctypes.byref(nc), _stream()), "gee_pull_plan")
         self.n_cut = int(nc.value)
+        self._plan_heavy()
         mx, mn, mxa = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         nf = ctypes.c_int32()
         check(lib.gee_graph_stats(ptr(self.offsets), ptr(self.weights), self.n, arcs, ctypes.byref(mx),
@@ -150,6 +155,33 @@ class DeviceGraph:
         e, rel = ctypes.c_int32(), ctypes.c_double()
         check(lib.gee_pull_scale_exp(mx.value, mn.value, ctypes.byref(e), ctypes.byref(rel)), "gee_pull_scale_exp")
         self.scale_exp, self.rel_err = e.value, rel.value
+
+    HEAVY_ARCS = 4096
+
+    def _plan_heavy(self):
+        """Heavy-row chunk list for gee_reduce_rows (graph preparation)."""
+        n = self.n
+        rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        nh = ctypes.c_int64()
+        check(lib.gee_reduce_heavy_plan(ptr(self.offsets), n, self.HEAVY_ARCS, ptr(rows), ctypes.byref(nh),
+                                        _stream()), "gee_reduce_heavy_plan")
+        self.n_heavy = int(nh.value)
+        if self.n_heavy == 0:
+            self.heavy_rows = self.chunk_first = self.chunk_heavy = None
+            self.n_chunks = 0
+            return
+        rows = rows[:self.n_heavy].clone()
+        r64 = rows.to(torch.int64)
+        first = self.offsets[r64].cpu()
+        deg = (self.offsets[r64 + 1] - self.offsets[r64]).cpu()
+        per = (deg + self.HEAVY_ARCS - 1) // self.HEAVY_ARCS
+        heavy_idx = torch.repeat_interleave(torch.arange(self.n_heavy), per)
+        start = torch.repeat_interleave(first, per)
+        within = torch.arange(int(per.sum())) - torch.repeat_interleave(torch.cumsum(per, 0) - per, per)
+        self.heavy_rows = rows
+        self.chunk_first = (start + within * self.HEAVY_ARCS).to(self.device)
+        self.chunk_heavy = heavy_idx.to(torch.int32).to(self.device)
+        self.n_chunks = int(per.sum())
 
     # Hot-label tier (csrc/gee_hot.cu): worth it when the packed label array
     # outgrows what L2 keeps resident under random access and degrees are
@@ -233,7 +265,9 @@ class Embedder:
         self.table_n_hot = None  # n_hot the current table was built with
         self.slots = None
         self.cls = None  # class stream of the split pull
+        self.heavy_acc = None  # heavy-row partial sums (row reducer)
         self.split = os.environ.get("GEE_PULL_FUSED") is None
+        self.reducer = os.environ.get("GEE_PULL_REDUCER", "rows")  # rows | tiles
 
     def _ensure_table(self, n_hot):
         need = int(lib.gee_label_table_bytes(self.n, n_hot, self.k))
@@ -289,6 +323,15 @@ class Embedder:
                 self.cls = torch.empty(g.arcs + 16, dtype=torch.uint8, device=self.device)
             check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
                                         _stream()), "gee_gather_labels")
+            if self.reducer == "rows":
+                if g.n_heavy and (self.heavy_acc is None or self.heavy_acc.numel() < g.n_heavy * self.k):
+                    self.heavy_acc = torch.zeros(g.n_heavy * self.k, dtype=torch.int64, device=self.device)
+                check(lib.gee_reduce_rows(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                          ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(g.heavy_rows), g.n_heavy,
+                                          ptr(g.chunk_first), ptr(g.chunk_heavy), g.n_chunks,
+                                          ptr(self.heavy_acc) if g.n_heavy else None, ptr(z), _stream()),
+                      "gee_reduce_rows")
+                return z
             check(lib.gee_embed_csr_pull_cls(ptr(g.offsets), ptr(self.cls), ptr(g.weights), g.n, g.arcs,
                                              ptr(g.tile_row), ptr(g.chunk_row), ptr(g.cut_tiles), g.n_cut,
                                              g.scale_exp, ptr(self.inv64), self.k, ptr(z), ptr(self.slots),
