@@ -214,6 +214,21 @@ int gee_reduce_rows(const int64_t *offsets, int64_t n, const uint8_t *cls, const
                     const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
                     void *stream);
 
+/* Degree-binned reduction: gee_reduce_bins lists the rows with at most
+ * small_arcs arcs (empty rows included) and those with more but at most
+ * heavy_arcs, each in row order; gee_reduce_lists reduces them with 8-lane
+ * groups (small) and whole warps (medium) and the heavy rows in chunks, as
+ * gee_reduce_rows does.  Every row of Z is written. */
+int gee_reduce_bins(const int64_t *offsets, int64_t n, int64_t small_arcs, int64_t heavy_arcs,
+                    int32_t *small_rows, int32_t *medium_rows, int64_t *n_small, int64_t *n_medium,
+                    void *stream);
+int gee_reduce_lists(const int64_t *offsets, const int32_t *small_rows, int64_t n_small,
+                     const int32_t *medium_rows, int64_t n_medium, const uint8_t *cls,
+                     const float *w, int32_t scale_exp, const double *inv, int32_t k,
+                     int64_t heavy_arcs, const int32_t *heavy_rows, int64_t n_heavy,
+                     const int64_t *chunk_first, const int32_t *chunk_heavy, int64_t n_chunks,
+                     void *heavy_acc, float *z, void *stream);
+
 /* Choose the fixed-point exponent for a weighted pull: the largest e with
  * max_row_abs * 2^e < 2^62.  Returns the relative quantisation bound
  * 2^-(e+1)/min_abs_nz through *rel_err (host). */

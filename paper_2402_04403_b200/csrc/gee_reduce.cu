@@ -171,6 +171,170 @@ k_reduce_rows(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__r
     }
 }
 
+// Degree-binned variant: rows come from a prepared list (gee_reduce_bins);
+// groups of GS lanes each own one row at a time (GS = 8 for rows of <= 32
+// arcs, so a warp has 4 rows in flight; GS = 32 for medium rows, with the
+// next 32*UNR-arc round loaded while the current one accumulates).  Each
+// group prefetches its next row's offsets and first round.
+template <bool WEIGHTED, int GS>
+__global__ void __launch_bounds__(RT)
+k_reduce_list(const int64_t *__restrict__ offsets, const int32_t *__restrict__ rows, int64_t n_rows,
+              const uint8_t *__restrict__ cls, const float *__restrict__ w, float qscale, double dscale,
+              const double *__restrict__ inv, int32_t k, float *__restrict__ z)
+{
+    constexpr int GPW = 32 / GS;  // groups per warp
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float *sc = reinterpret_cast<float *>(smem_raw);
+    const int kk = k;
+    const int pk = (kk + 3) & ~3;
+    const int vecw = pk * Acc<WEIGHTED>::planes;
+    uint32_t *vbase = reinterpret_cast<uint32_t *>(sc + ((kk + 4) & ~3));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int gid = lane / GS, gl = lane % GS;
+    const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1u) << (gid * GS));
+    uint32_t *v = vbase + (wid * GPW + gid) * vecw;
+    for (int c = threadIdx.x; c <= kk; c += RT) sc[c] = (float)(inv[c] * dscale);
+    for (int i = threadIdx.x; i < RW * GPW * vecw; i += RT) vbase[i] = 0u;
+    __syncthreads();
+    const bool even = (kk & 1) == 0;
+    const int64_t G0 = ((int64_t)blockIdx.x * RW + wid) * GPW + gid;
+    const int64_t GG = (int64_t)gridDim.x * RW * GPW;
+    constexpr int ROUND = GS * UNR;
+
+    int64_t i = G0;
+    int64_t ob = 0, oe = 0, r = 0;
+    if (i < n_rows) {
+        r = rows[i];
+        ob = __ldcs(offsets + r);
+        oe = __ldcs(offsets + r + 1);
+    }
+    uint32_t c0[UNR];
+    float w0[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+        const int64_t e = ob + gl + GS * u;
+        c0[u] = (i < n_rows && e < oe) ? __ldcs(cls + e) : 0u;
+        w0[u] = (WEIGHTED && i < n_rows && e < oe) ? __ldcs(w + e) : 0.f;
+    }
+    int64_t rn = 0, obn = 0, oen = 0;
+    if (i + GG < n_rows) {
+        rn = rows[i + GG];
+        obn = __ldcs(offsets + rn);
+        oen = __ldcs(offsets + rn + 1);
+    }
+    for (; i < n_rows; i += GG) {
+        // prefetch the next row's first round and the row after's offsets
+        uint32_t c1[UNR];
+        float w1[UNR];
+        const bool has_next = i + GG < n_rows;
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+            const int64_t e = obn + gl + GS * u;
+            c1[u] = (has_next && e < oen) ? __ldcs(cls + e) : 0u;
+            w1[u] = (WEIGHTED && has_next && e < oen) ? __ldcs(w + e) : 0.f;
+        }
+        int64_t rnn = 0, obnn = 0, oenn = 0;
+        if (i + 2 * GG < n_rows) {
+            rnn = rows[i + 2 * GG];
+            obnn = __ldcs(offsets + rnn);
+            oenn = __ldcs(offsets + rnn + 1);
+        }
+        float *zr = z + r * (int64_t)kk;
+        if (oe == ob) {
+            if (even) {
+                float2 *z2 = reinterpret_cast<float2 *>(zr);
+                for (int c = gl; c < (kk >> 1); c += GS) __stcs(z2 + c, make_float2(0.f, 0.f));
+            } else {
+                for (int c = gl; c < kk; c += GS) __stcs(zr + c, 0.f);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < UNR; u++)
+                if (c0[u] != 0u && c0[u] <= (uint32_t)kk) acc_add<WEIGHTED>(v, pk, c0[u], w0[u], qscale);
+            if (oe - ob > ROUND) {  // longer rows: rounds with the next one in flight
+                uint32_t ca[UNR];
+                float wa[UNR];
+                int64_t e0 = ob + ROUND;
+#pragma unroll
+                for (int u = 0; u < UNR; u++) {
+                    const int64_t e = e0 + gl + GS * u;
+                    ca[u] = e < oe ? __ldcs(cls + e) : 0u;
+                    wa[u] = (WEIGHTED && e < oe) ? __ldcs(w + e) : 0.f;
+                }
+                for (; e0 < oe; e0 += ROUND) {
+                    uint32_t cb[UNR];
+                    float wb[UNR];
+#pragma unroll
+                    for (int u = 0; u < UNR; u++) {
+                        const int64_t e = e0 + ROUND + gl + GS * u;
+                        cb[u] = e < oe ? __ldcs(cls + e) : 0u;
+                        wb[u] = (WEIGHTED && e < oe) ? __ldcs(w + e) : 0.f;
+                    }
+#pragma unroll
+                    for (int u = 0; u < UNR; u++)
+                        if (ca[u] != 0u && ca[u] <= (uint32_t)kk) acc_add<WEIGHTED>(v, pk, ca[u], wa[u], qscale);
+#pragma unroll
+                    for (int u = 0; u < UNR; u++) {
+                        ca[u] = cb[u];
+                        wa[u] = wb[u];
+                    }
+                }
+            }
+            __syncwarp(gmask);
+            if (even) {
+                float2 *z2 = reinterpret_cast<float2 *>(zr);
+                for (int c2 = gl; c2 < (kk >> 1); c2 += GS) {
+                    const float a = (float)acc_take<WEIGHTED>(v, pk, 2 * c2) * sc[2 * c2 + 1];
+                    const float b = (float)acc_take<WEIGHTED>(v, pk, 2 * c2 + 1) * sc[2 * c2 + 2];
+                    __stcs(z2 + c2, make_float2(a, b));
+                }
+            } else {
+                for (int c = gl; c < kk; c += GS) __stcs(zr + c, (float)acc_take<WEIGHTED>(v, pk, c) * sc[c + 1]);
+            }
+            __syncwarp(gmask);
+        }
+        r = rn;
+        ob = obn;
+        oe = oen;
+        rn = rnn;
+        obn = obnn;
+        oen = oenn;
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+            c0[u] = c1[u];
+            w0[u] = w1[u];
+        }
+    }
+}
+
+// Bin rows by degree: small (<= small_arcs, incl. empty) and medium
+// (<= heavy_arcs); heavier rows are left to the chunked path.
+__global__ void k_bin_rows(const int64_t *__restrict__ offsets, int64_t n, int64_t small_arcs, int64_t heavy_arcs,
+                           int32_t *__restrict__ small_rows, int32_t *__restrict__ medium_rows,
+                           unsigned long long *__restrict__ counts)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; base < n;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = base + lane;
+        int64_t d = -1;
+        if (r < n) d = offsets[r + 1] - offsets[r];
+        const bool sm = r < n && d <= small_arcs, md = r < n && d > small_arcs && d <= heavy_arcs;
+        // warp-aggregated appends keep each warp's rows consecutive in the lists
+        const unsigned bs = __ballot_sync(0xffffffffu, sm), bm = __ballot_sync(0xffffffffu, md);
+        unsigned long long ps = 0, pm = 0;
+        if (lane == 0) {
+            if (bs) ps = atomicAdd(&counts[0], (unsigned long long)__popc(bs));
+            if (bm) pm = atomicAdd(&counts[1], (unsigned long long)__popc(bm));
+        }
+        ps = __shfl_sync(0xffffffffu, ps, 0);
+        pm = __shfl_sync(0xffffffffu, pm, 0);
+        const unsigned below = (1u << lane) - 1u;
+        if (sm) small_rows[ps + __popc(bs & below)] = (int32_t)r;
+        if (md) medium_rows[pm + __popc(bm & below)] = (int32_t)r;
+    }
+}
+
 // Heavy rows: one warp per chunk of GEE_HEAVY_ARCS arcs; exact int64 partial
 // sums meet in acc[h][c] through 64-bit global atomics.
 template <bool WEIGHTED>
@@ -305,6 +469,91 @@ int gee_reduce_rows(const int64_t *offsets, int64_t n, const uint8_t *cls, const
     int rc = gee::check_launch("k_reduce_rows");
     if (rc || n_heavy == 0) return rc;
     const size_t shh = (size_t)RW * (((size_t)k + 3) & ~(size_t)3) * (weighted ? 2 : 1) * sizeof(uint32_t);
+    const int hgrid = grid_for(n_chunks * 32, RT, 8);
+    if (weighted)
+        k_reduce_heavy<true><<<hgrid, RT, shh, st>>>(offsets, heavy_rows, chunk_first, chunk_heavy, n_chunks, heavy_arcs,
+                                                     cls, w, qscale, k, acc);
+    else
+        k_reduce_heavy<false><<<hgrid, RT, shh, st>>>(offsets, heavy_rows, chunk_first, chunk_heavy, n_chunks,
+                                                      heavy_arcs, cls, w, qscale, k, acc);
+    if ((rc = gee::check_launch("k_reduce_heavy"))) return rc;
+    const int fgrid = grid_for(n_heavy * k, 256, 4);
+    if (weighted)
+        k_heavy_finalize<true><<<fgrid, 256, 0, st>>>(heavy_rows, n_heavy, k, acc, inv, dscale, z);
+    else
+        k_heavy_finalize<false><<<fgrid, 256, 0, st>>>(heavy_rows, n_heavy, k, acc, inv, dscale, z);
+    return gee::check_launch("k_heavy_finalize");
+}
+
+int gee_reduce_bins(const int64_t *offsets, int64_t n, int64_t small_arcs, int64_t heavy_arcs, int32_t *small_rows,
+                    int32_t *medium_rows, int64_t *n_small, int64_t *n_medium, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(n >= 0 && small_arcs >= 0 && heavy_arcs >= small_arcs, GEE_ERR_INVALID, "bad bin sizes");
+    GEE_REQUIRE(n_small && n_medium, GEE_ERR_INVALID, "NULL count argument");
+    *n_small = *n_medium = 0;
+    if (n == 0) return GEE_OK;
+    GEE_REQUIRE(offsets && small_rows && medium_rows, GEE_ERR_INVALID, "NULL array argument");
+    cudaStream_t st = gee::as_stream(stream);
+    unsigned long long *cnt = nullptr, h[2] = {0, 0};
+    GEE_CUDA(cudaMallocAsync((void **)&cnt, 2 * sizeof(unsigned long long), st));
+    GEE_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), st));
+    k_bin_rows<<<grid_for(n, 256, 16), 256, 0, st>>>(offsets, n, small_arcs, heavy_arcs, small_rows, medium_rows, cnt);
+    int rc = gee::check_launch("k_bin_rows");
+    cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(cnt, st);
+    GEE_CUDA(cudaStreamSynchronize(st));
+    *n_small = (int64_t)h[0];
+    *n_medium = (int64_t)h[1];
+    return rc;
+}
+
+int gee_reduce_lists(const int64_t *offsets, const int32_t *small_rows, int64_t n_small, const int32_t *medium_rows,
+                     int64_t n_medium, const uint8_t *cls, const float *w, int32_t scale_exp, const double *inv,
+                     int32_t k, int64_t heavy_arcs, const int32_t *heavy_rows, int64_t n_heavy,
+                     const int64_t *chunk_first, const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
+                     void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs 1 <= k <= 255 (got %d)", k);
+    GEE_REQUIRE(n_small >= 0 && n_medium >= 0 && n_heavy >= 0 && n_chunks >= 0, GEE_ERR_INVALID, "bad sizes");
+    GEE_REQUIRE(offsets && z && inv, GEE_ERR_INVALID, "NULL array argument");
+    GEE_REQUIRE(n_heavy == 0 || (heavy_rows && chunk_first && chunk_heavy && heavy_acc), GEE_ERR_INVALID,
+                "heavy rows need their chunk list and accumulator");
+    cudaStream_t st = gee::as_stream(stream);
+    const bool weighted = w != nullptr;
+    const float qscale = ldexpf(1.0f, scale_exp);
+    const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
+    const size_t vec = (((size_t)k + 3) & ~(size_t)3) * (weighted ? 2 : 1) * sizeof(uint32_t);
+    const size_t scb = ((size_t)(k + 4) & ~(size_t)3) * sizeof(float);
+    int rc = GEE_OK;
+    if (n_small > 0) {
+        const size_t sh = scb + (size_t)RW * 4 * vec;
+        const int grid = grid_for((n_small + 3) / 4 * 32, RT, 8);
+        if (weighted) {
+            GEE_CUDA(cudaFuncSetAttribute(k_reduce_list<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+            k_reduce_list<true, 8><<<grid, RT, sh, st>>>(offsets, small_rows, n_small, cls, w, qscale, dscale, inv, k, z);
+        } else {
+            GEE_CUDA(cudaFuncSetAttribute(k_reduce_list<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+            k_reduce_list<false, 8><<<grid, RT, sh, st>>>(offsets, small_rows, n_small, cls, w, qscale, dscale, inv, k, z);
+        }
+        if ((rc = gee::check_launch("k_reduce_list<8>"))) return rc;
+    }
+    if (n_medium > 0) {
+        const size_t sh = scb + (size_t)RW * vec;
+        const int grid = grid_for(n_medium * 32, RT, 8);
+        if (weighted) {
+            GEE_CUDA(cudaFuncSetAttribute(k_reduce_list<true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+            k_reduce_list<true, 32><<<grid, RT, sh, st>>>(offsets, medium_rows, n_medium, cls, w, qscale, dscale, inv, k, z);
+        } else {
+            GEE_CUDA(cudaFuncSetAttribute(k_reduce_list<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+            k_reduce_list<false, 32><<<grid, RT, sh, st>>>(offsets, medium_rows, n_medium, cls, w, qscale, dscale, inv, k, z);
+        }
+        if ((rc = gee::check_launch("k_reduce_list<32>"))) return rc;
+    }
+    if (n_heavy == 0) return GEE_OK;
+    const size_t shh = (size_t)RW * vec;
+    auto *acc = static_cast<unsigned long long *>(heavy_acc);
     const int hgrid = grid_for(n_chunks * 32, RT, 8);
     if (weighted)
         k_reduce_heavy<true><<<hgrid, RT, shh, st>>>(offsets, heavy_rows, chunk_first, chunk_heavy, n_chunks, heavy_arcs,

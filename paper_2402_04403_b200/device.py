@@ -62,6 +62,8 @@ class DeviceGraph:
         # split into chunks
         self.heavy_rows = self.chunk_first = self.chunk_heavy = None
         self.n_heavy = self.n_chunks = 0
+        self.small_rows = self.medium_rows = None
+        self.n_small = self.n_medium = 0
         self.scale_exp = 0
         self.rel_err = 0.0
         self.max_row_abs = 0.0
@@ -157,10 +159,18 @@ class DeviceGraph:
         self.scale_exp, self.rel_err = e.value, rel.value
 
     HEAVY_ARCS = 4096
+    SMALL_ARCS = 32
 
     def _plan_heavy(self):
-        """Heavy-row chunk list for gee_reduce_rows (graph preparation)."""
+        """Degree bins + heavy-row chunk list for the row reducers (graph preparation)."""
         n = self.n
+        self.small_rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        self.medium_rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        ns, nm = ctypes.c_int64(), ctypes.c_int64()
+        check(lib.gee_reduce_bins(ptr(self.offsets), n, self.SMALL_ARCS, self.HEAVY_ARCS, ptr(self.small_rows),
+                                  ptr(self.medium_rows), ctypes.byref(ns), ctypes.byref(nm), _stream()),
+              "gee_reduce_bins")
+        self.n_small, self.n_medium = int(ns.value), int(nm.value)
         rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         nh = ctypes.c_int64()
         check(lib.gee_reduce_heavy_plan(ptr(self.offsets), n, self.HEAVY_ARCS, ptr(rows), ctypes.byref(nh),
@@ -267,7 +277,7 @@ class Embedder:
         self.cls = None  # class stream of the split pull
         self.heavy_acc = None  # heavy-row partial sums (row reducer)
         self.split = os.environ.get("GEE_PULL_FUSED") is None
-        self.reducer = os.environ.get("GEE_PULL_REDUCER", "rows")  # rows | tiles
+        self.reducer = os.environ.get("GEE_PULL_REDUCER", "lists")  # lists | rows | tiles
 
     def _ensure_table(self, n_hot):
         need = int(lib.gee_label_table_bytes(self.n, n_hot, self.k))
@@ -323,6 +333,16 @@ class Embedder:
                 self.cls = torch.empty(g.arcs + 16, dtype=torch.uint8, device=self.device)
             check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
                                         _stream()), "gee_gather_labels")
+            if self.reducer == "lists":
+                if g.n_heavy and (self.heavy_acc is None or self.heavy_acc.numel() < g.n_heavy * self.k):
+                    self.heavy_acc = torch.zeros(g.n_heavy * self.k, dtype=torch.int64, device=self.device)
+                check(lib.gee_reduce_lists(ptr(g.offsets), ptr(g.small_rows), g.n_small, ptr(g.medium_rows),
+                                           g.n_medium, ptr(self.cls), ptr(g.weights), g.scale_exp, ptr(self.inv64),
+                                           self.k, g.HEAVY_ARCS, ptr(g.heavy_rows), g.n_heavy, ptr(g.chunk_first),
+                                           ptr(g.chunk_heavy), g.n_chunks,
+                                           ptr(self.heavy_acc) if g.n_heavy else None, ptr(z), _stream()),
+                      "gee_reduce_lists")
+                return z
             if self.reducer == "rows":
                 if g.n_heavy and (self.heavy_acc is None or self.heavy_acc.numel() < g.n_heavy * self.k):
                     self.heavy_acc = torch.zeros(g.n_heavy * self.k, dtype=torch.int64, device=self.device)
