@@ -229,6 +229,15 @@ int gee_reduce_lists(const int64_t *offsets, const int32_t *small_rows, int64_t 
                      const int64_t *chunk_first, const int32_t *chunk_heavy, int64_t n_chunks,
                      void *heavy_acc, float *z, void *stream);
 
+/* Block reduction: one warp per 32 consecutive rows (coalesced offsets,
+ * streamed arcs, one flat coalesced write of the block's Z rows); heavy rows
+ * as in gee_reduce_rows.  k <= 255. */
+int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
+                      int32_t scale_exp, const double *inv, int32_t k, int64_t heavy_arcs,
+                      const int32_t *heavy_rows, int64_t n_heavy, const int64_t *chunk_first,
+                      const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
+                      void *stream);
+
 /* Choose the fixed-point exponent for a weighted pull: the largest e with
  * max_row_abs * 2^e < 2^62.  Returns the relative quantisation bound
  * 2^-(e+1)/min_abs_nz through *rel_err (host). */

@@ -307,6 +307,189 @@ k_reduce_list(const int64_t *__restrict__ offsets, const int32_t *__restrict__ r
     }
 }
 
+// Block variant: one warp per block of 32 consecutive rows.  Lane i loads
+// offsets[r0+i] (one coalesced load per block).  The block's arcs stream in
+// rounds of 32 x 8 contiguous arcs (one 8-byte class load and two 16-byte
+// weight loads per lane, the next round in flight); a lane finds the row of
+// its first arc with a 5-step shuffle search over the lanes' offsets and
+// walks forward from there.  Nonempty rows get compact slots (ballot rank)
+// in a warp-private window.  The block's Z range is zero-filled with 16-byte
+// stores when it holds empty rows, then each nonempty row is written from its
+// slot; heavy rows are left to the chunked path (k_heavy_finalize runs
+// after).  Blocks with more than `nslots` nonempty rows take several passes.
+constexpr int BU = 8;            // contiguous arcs per lane per round
+constexpr int BROUND = 32 * BU;  // arcs per warp round
+constexpr int BMETA = 72;        // per-warp ints: 33 local offsets + 32 slots (+pad)
+
+template <bool WEIGHTED>
+__device__ __forceinline__ void block_round(const uint8_t *__restrict__ cls, const float *__restrict__ w, int64_t e,
+                                            int64_t arcs, bool vec, uint2 &c, float (&wt)[BU])
+{
+    if (vec && e + BU <= arcs) {
+        c = __ldcs(reinterpret_cast<const uint2 *>(cls + e));
+        if (WEIGHTED) {
+            const float4 a = __ldcs(reinterpret_cast<const float4 *>(w + e));
+            const float4 b = __ldcs(reinterpret_cast<const float4 *>(w + e + 4));
+            wt[0] = a.x, wt[1] = a.y, wt[2] = a.z, wt[3] = a.w;
+            wt[4] = b.x, wt[5] = b.y, wt[6] = b.z, wt[7] = b.w;
+        }
+    } else {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int u = 0; u < BU; u++) {
+            const bool ok = e + u < arcs;
+            const uint32_t cv = ok ? (uint32_t)cls[e + u] : 0u;
+            if (u < 4)
+                lo |= cv << (8 * u);
+            else
+                hi |= cv << (8 * (u - 4));
+            if (WEIGHTED) wt[u] = ok ? w[e + u] : 0.f;
+        }
+        c = make_uint2(lo, hi);
+    }
+}
+
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(RT)
+k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
+                const float *__restrict__ w, float qscale, double dscale, const double *__restrict__ inv, int32_t k,
+                int64_t heavy_arcs, int nslots, bool vec, float *__restrict__ z)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float *sc = reinterpret_cast<float *>(smem_raw);
+    const int kk = k;
+    const int pk = (kk + 3) & ~3;
+    const int vecw = pk * Acc<WEIGHTED>::planes;
+    int32_t *meta = reinterpret_cast<int32_t *>(sc + ((kk + 4) & ~3));
+    uint32_t *vbase = reinterpret_cast<uint32_t *>(meta + RW * BMETA);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t *s_off = meta + wid * BMETA;  // [0, 33)
+    int32_t *s_slot = s_off + 36;         // [0, 32)
+    uint32_t *v = vbase + wid * nslots * vecw;  // slot s: lo plane at v + s*pk, hi plane at + nslots*pk
+    const int hoff = nslots * pk;
+    for (int c = threadIdx.x; c <= kk; c += RT) sc[c] = (float)(inv[c] * dscale);
+    for (int i = threadIdx.x; i < RW * nslots * vecw; i += RT) vbase[i] = 0u;
+    __syncthreads();
+    const unsigned below = (1u << lane) - 1u;
+    const int64_t nblocks = (n + 31) / 32;
+    const int64_t gw = (int64_t)blockIdx.x * RW + wid, GW = (int64_t)gridDim.x * RW;
+    const int64_t arcs = offsets[n];
+
+    int64_t b = gw;
+    int64_t o_lo = 0;
+    if (b < nblocks) o_lo = __ldcs(offsets + min(32 * b + lane, n));
+    for (; b < nblocks; b += GW) {
+        const int64_t r0 = 32 * b;
+        int64_t o_hi = __shfl_down_sync(0xffffffffu, o_lo, 1);
+        if (lane == 31) o_hi = r0 + 32 <= n ? __ldcs(offsets + r0 + 32) : arcs;
+        const int64_t o_nx = (b + GW < nblocks) ? __ldcs(offsets + min(32 * (b + GW) + lane, n)) : 0;
+        const bool valid = r0 + lane < n;
+        const int64_t d = valid ? o_hi - o_lo : 0;
+        const bool heavy = d > heavy_arcs;
+        const bool nz = d > 0 && !heavy;
+        const unsigned nzm = __ballot_sync(0xffffffffu, nz), hvm = __ballot_sync(0xffffffffu, heavy);
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        const int rank = __popc(nzm & below);
+        const int nnz = __popc(nzm);
+        const int64_t base = __shfl_sync(0xffffffffu, o_lo, 0);
+        const int64_t bend = __shfl_sync(0xffffffffu, o_hi, 31);
+        const int32_t ol = (int32_t)(o_lo - base);  // local start of this lane's row
+        const int32_t lend = (int32_t)(bend - base);
+        const int rows = (int)min((int64_t)32, n - r0);
+        float *zb = z + r0 * (int64_t)kk;
+        if ((nzm | hvm) != vm) {  // the block holds empty rows: zero-fill its Z range
+            const int total = rows * kk;
+            const int q4 = total >> 2;
+            float4 *z4 = reinterpret_cast<float4 *>(zb);
+            for (int q = lane; q < q4; q += 32) z4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int e = 4 * q4 + lane; e < total; e += 32) zb[e] = 0.f;
+        }
+        s_off[lane] = ol;
+        if (lane == 31) s_off[32] = lend;
+        for (int p0 = 0; p0 < nnz; p0 += nslots) {
+            const bool mine = nz && rank >= p0 && rank < p0 + nslots;
+            s_slot[lane] = mine ? rank - p0 : -1;
+            const unsigned pm0 = __ballot_sync(0xffffffffu, mine);
+            __syncwarp();
+            int64_t e0 = base & ~(int64_t)(BU - 1);
+            uint2 ca;
+            float wa[BU];
+            block_round<WEIGHTED>(cls, w, e0 + lane * BU, arcs, vec, ca, wa);
+            while (e0 < bend) {
+                if (hvm) {  // skip a heavy row's arcs wholesale (warp-uniform)
+                    const int32_t ls = (int32_t)max(e0 - base, (int64_t)0);
+                    int j = 0;
+#pragma unroll
+                    for (int st = 16; st; st >>= 1) {
+                        const int32_t oc = __shfl_sync(0xffffffffu, ol, (j + st) & 31);
+                        if (j + st < 32 && oc <= ls) j += st;
+                    }
+                    const int64_t hend = base + s_off[j + 1];
+                    if (((hvm >> j) & 1u) && hend >= e0 + BROUND) {  // whole round inside the heavy row
+                        e0 = hend & ~(int64_t)(BU - 1);
+                        block_round<WEIGHTED>(cls, w, e0 + lane * BU, arcs, vec, ca, wa);
+                        continue;
+                    }
+                }
+                const int64_t e1 = e0 + BROUND;
+                uint2 cb = make_uint2(0u, 0u);
+                float wb[BU];
+                if (e1 < bend) block_round<WEIGHTED>(cls, w, e1 + lane * BU, arcs, vec, cb, wb);
+                const int32_t le = (int32_t)(e0 + lane * BU - base);
+                const int32_t ls = max(le, 0);
+                int j = 0;  // row of this lane's first arc: last lane j with ol[j] <= ls
+#pragma unroll
+                for (int st = 16; st; st >>= 1) {
+                    const int32_t oc = __shfl_sync(0xffffffffu, ol, (j + st) & 31);
+                    if (j + st < 32 && oc <= ls) j += st;
+                }
+                if (le < lend) {
+                    int32_t nxt = s_off[j + 1];
+                    int slot = s_slot[j];
+#pragma unroll
+                    for (int u = 0; u < BU; u++) {
+                        const int32_t a = le + u;
+                        while (a >= nxt && j < 31) {
+                            j++;
+                            nxt = s_off[j + 1];
+                            slot = s_slot[j];
+                        }
+                        const uint32_t c = ((u < 4 ? ca.x : ca.y) >> (8 * (u & 3))) & 0xffu;
+                        if (a >= 0 && a < nxt && slot >= 0 && c != 0u && c <= (uint32_t)kk)
+                            acc_add<WEIGHTED>(v + slot * pk, hoff, c, WEIGHTED ? wa[u] : 1.f, qscale);
+                    }
+                }
+                ca = cb;
+#pragma unroll
+                for (int u = 0; u < BU; u++) wa[u] = wb[u];
+                e0 = e1;
+            }
+            __syncwarp();
+            // write this pass's rows from their slots
+            unsigned pm = pm0;
+            while (pm) {
+                const int rr = __ffs(pm) - 1;
+                pm &= pm - 1;
+                const int slot = __popc(nzm & ((1u << rr) - 1u)) - p0;
+                uint32_t *vs = v + slot * pk;
+                float *zr = zb + (int64_t)rr * kk;
+                if ((kk & 1) == 0) {
+                    float2 *z2 = reinterpret_cast<float2 *>(zr);
+                    for (int c2 = lane; c2 < (kk >> 1); c2 += 32) {
+                        const float x0 = (float)acc_take<WEIGHTED>(vs, hoff, 2 * c2) * sc[2 * c2 + 1];
+                        const float x1 = (float)acc_take<WEIGHTED>(vs, hoff, 2 * c2 + 1) * sc[2 * c2 + 2];
+                        __stcs(z2 + c2, make_float2(x0, x1));
+                    }
+                } else {
+                    for (int c = lane; c < kk; c += 32) __stcs(zr + c, (float)acc_take<WEIGHTED>(vs, hoff, c) * sc[c + 1]);
+                }
+            }
+            __syncwarp();
+        }
+        o_lo = o_nx;
+    }
+}
+
 // Bin rows by degree: small (<= small_arcs, incl. empty) and medium
 // (<= heavy_arcs); heavier rows are left to the chunked path.
 __global__ void k_bin_rows(const int64_t *__restrict__ offsets, int64_t n, int64_t small_arcs, int64_t heavy_arcs,
@@ -551,6 +734,61 @@ int gee_reduce_lists(const int64_t *offsets, const int32_t *small_rows, int64_t 
         }
         if ((rc = gee::check_launch("k_reduce_list<32>"))) return rc;
     }
+    if (n_heavy == 0) return GEE_OK;
+    const size_t shh = (size_t)RW * vec;
+    auto *acc = static_cast<unsigned long long *>(heavy_acc);
+    const int hgrid = grid_for(n_chunks * 32, RT, 8);
+    if (weighted)
+        k_reduce_heavy<true><<<hgrid, RT, shh, st>>>(offsets, heavy_rows, chunk_first, chunk_heavy, n_chunks, heavy_arcs,
+                                                     cls, w, qscale, k, acc);
+    else
+        k_reduce_heavy<false><<<hgrid, RT, shh, st>>>(offsets, heavy_rows, chunk_first, chunk_heavy, n_chunks,
+                                                      heavy_arcs, cls, w, qscale, k, acc);
+    if ((rc = gee::check_launch("k_reduce_heavy"))) return rc;
+    const int fgrid = grid_for(n_heavy * k, 256, 4);
+    if (weighted)
+        k_heavy_finalize<true><<<fgrid, 256, 0, st>>>(heavy_rows, n_heavy, k, acc, inv, dscale, z);
+    else
+        k_heavy_finalize<false><<<fgrid, 256, 0, st>>>(heavy_rows, n_heavy, k, acc, inv, dscale, z);
+    return gee::check_launch("k_heavy_finalize");
+}
+
+int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
+                      const double *inv, int32_t k, int64_t heavy_arcs, const int32_t *heavy_rows, int64_t n_heavy,
+                      const int64_t *chunk_first, const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc,
+                      float *z, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs 1 <= k <= 255 (got %d)", k);
+    GEE_REQUIRE(n >= 0 && n_heavy >= 0 && n_chunks >= 0 && heavy_arcs >= 1, GEE_ERR_INVALID, "bad sizes");
+    if (n == 0) return GEE_OK;
+    GEE_REQUIRE(offsets && z && inv && cls, GEE_ERR_INVALID, "NULL array argument");
+    GEE_REQUIRE(n_heavy == 0 || (heavy_rows && chunk_first && chunk_heavy && heavy_acc), GEE_ERR_INVALID,
+                "heavy rows need their chunk list and accumulator");
+    cudaStream_t st = gee::as_stream(stream);
+    const bool weighted = w != nullptr;
+    const float qscale = ldexpf(1.0f, scale_exp);
+    const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
+    const size_t vec = (((size_t)k + 3) & ~(size_t)3) * (weighted ? 2 : 1) * sizeof(uint32_t);
+    const size_t scb = ((size_t)(k + 4) & ~(size_t)3) * sizeof(float);
+    // slots per warp: up to 16, within ~64 KB per CTA so several CTAs fit per SM
+    int nslots = (int)((56 * 1024) / (RW * vec));
+    if (nslots > 16) nslots = 16;
+    if (nslots < 1) nslots = 1;
+    const size_t sh = scb + (size_t)RW * BMETA * sizeof(int32_t) + (size_t)RW * nslots * vec;
+    const bool vld = (reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0);
+    GEE_REQUIRE((reinterpret_cast<uintptr_t>(z) & 15) == 0, GEE_ERR_INVALID, "z must be 16-byte aligned");
+    const int64_t nblocks = (n + 31) / 32;
+    const int grid = grid_for(nblocks * 32, RT, 8);
+    int rc;
+    if (weighted) {
+        GEE_CUDA(cudaFuncSetAttribute(k_reduce_blocks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        k_reduce_blocks<true><<<grid, RT, sh, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, nslots, vld, z);
+    } else {
+        GEE_CUDA(cudaFuncSetAttribute(k_reduce_blocks<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        k_reduce_blocks<false><<<grid, RT, sh, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, nslots, vld, z);
+    }
+    if ((rc = gee::check_launch("k_reduce_blocks"))) return rc;
     if (n_heavy == 0) return GEE_OK;
     const size_t shh = (size_t)RW * vec;
     auto *acc = static_cast<unsigned long long *>(heavy_acc);

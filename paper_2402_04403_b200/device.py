@@ -64,6 +64,7 @@ class DeviceGraph:
         self.n_heavy = self.n_chunks = 0
         self.small_rows = self.medium_rows = None
         self.n_small = self.n_medium = 0
+        self.max_block_arcs = 0
         self.scale_exp = 0
         self.rel_err = 0.0
         self.max_row_abs = 0.0
@@ -146,6 +147,10 @@ class DeviceGraph:
                                 ptr(self.cut_tiles), ctypes.byref(nc), _stream()), "gee_pull_plan")
         self.n_cut = int(nc.value)
         self._plan_heavy()
+        # arc span of the widest 32-row block (gee_reduce_blocks keeps
+        # block-local offsets in int32)
+        ends = self.offsets[torch.arange(0, self.n + 32, 32, device=self.device).clamp_(max=self.n)]
+        self.max_block_arcs = int((ends[1:] - ends[:-1]).max().item()) if self.n else 0
         mx, mn, mxa = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         nf = ctypes.c_int32()
         check(lib.gee_graph_stats(ptr(self.offsets), ptr(self.weights), self.n, arcs, ctypes.byref(mx),
@@ -277,7 +282,7 @@ class Embedder:
         self.cls = None  # class stream of the split pull
         self.heavy_acc = None  # heavy-row partial sums (row reducer)
         self.split = os.environ.get("GEE_PULL_FUSED") is None
-        self.reducer = os.environ.get("GEE_PULL_REDUCER", "lists")  # lists | rows | tiles
+        self.reducer = os.environ.get("GEE_PULL_REDUCER", "blocks")  # blocks | lists | rows | tiles
 
     def _ensure_table(self, n_hot):
         need = int(lib.gee_label_table_bytes(self.n, n_hot, self.k))
@@ -329,28 +334,28 @@ class Embedder:
         if self.split and self.k <= 255:
             # split pass: class stream (random gathers, full occupancy), then
             # the gather-free segmented reduction
-            if self.cls is None or self.cls.numel() < g.arcs + 16:
-                self.cls = torch.empty(g.arcs + 16, dtype=torch.uint8, device=self.device)
+            if self.cls is None or self.cls.numel() < g.arcs + 64:
+                self.cls = torch.empty(g.arcs + 64, dtype=torch.uint8, device=self.device)
             check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
                                         _stream()), "gee_gather_labels")
-            if self.reducer == "lists":
+            reducer = self.reducer
+            if reducer == "blocks" and (g.max_block_arcs >= 2**31 or z.data_ptr() % 16):
+                reducer = "lists"
+            if reducer in ("blocks", "lists", "rows"):
                 if g.n_heavy and (self.heavy_acc is None or self.heavy_acc.numel() < g.n_heavy * self.k):
                     self.heavy_acc = torch.zeros(g.n_heavy * self.k, dtype=torch.int64, device=self.device)
-                check(lib.gee_reduce_lists(ptr(g.offsets), ptr(g.small_rows), g.n_small, ptr(g.medium_rows),
-                                           g.n_medium, ptr(self.cls), ptr(g.weights), g.scale_exp, ptr(self.inv64),
-                                           self.k, g.HEAVY_ARCS, ptr(g.heavy_rows), g.n_heavy, ptr(g.chunk_first),
-                                           ptr(g.chunk_heavy), g.n_chunks,
-                                           ptr(self.heavy_acc) if g.n_heavy else None, ptr(z), _stream()),
-                      "gee_reduce_lists")
-                return z
-            if self.reducer == "rows":
-                if g.n_heavy and (self.heavy_acc is None or self.heavy_acc.numel() < g.n_heavy * self.k):
-                    self.heavy_acc = torch.zeros(g.n_heavy * self.k, dtype=torch.int64, device=self.device)
-                check(lib.gee_reduce_rows(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                          ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(g.heavy_rows), g.n_heavy,
-                                          ptr(g.chunk_first), ptr(g.chunk_heavy), g.n_chunks,
-                                          ptr(self.heavy_acc) if g.n_heavy else None, ptr(z), _stream()),
-                      "gee_reduce_rows")
+                heavy = (g.HEAVY_ARCS, ptr(g.heavy_rows), g.n_heavy, ptr(g.chunk_first), ptr(g.chunk_heavy),
+                         g.n_chunks, ptr(self.heavy_acc) if g.n_heavy else None, ptr(z), _stream())
+                if reducer == "blocks":
+                    check(lib.gee_reduce_blocks(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                                ptr(self.inv64), self.k, *heavy), "gee_reduce_blocks")
+                elif reducer == "lists":
+                    check(lib.gee_reduce_lists(ptr(g.offsets), ptr(g.small_rows), g.n_small, ptr(g.medium_rows),
+                                               g.n_medium, ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                               ptr(self.inv64), self.k, *heavy), "gee_reduce_lists")
+                else:
+                    check(lib.gee_reduce_rows(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                              ptr(self.inv64), self.k, *heavy), "gee_reduce_rows")
                 return z
             check(lib.gee_embed_csr_pull_cls(ptr(g.offsets), ptr(self.cls), ptr(g.weights), g.n, g.arcs,
                                              ptr(g.tile_row), ptr(g.chunk_row), ptr(g.cut_tiles), g.n_cut,

@@ -293,3 +293,31 @@ def test_hot_plan_ranks_by_degree():
     for r, v in enumerate(hot):
         assert rank[v] == r
     assert all(rank[v] == -1 for v in range(6) if deg[v] < 2)
+
+
+@pytest.mark.parametrize("k,weighted", [(50, True), (7, False), (2, True), (255, False)])
+def test_pull_reducers_agree_bitwise(k, weighted):
+    # every exact pull reducer (32-row blocks, degree lists, row-per-warp,
+    # tiles) sums the same integers: their Z must match bit for bit.  The
+    # graph mixes empty rows, dense blocks (> 16 nonempty rows: several
+    # passes), a heavy row inside a block and ragged tails.
+    rng = np.random.default_rng(k)
+    n = 40_003
+    hub = np.full(30_000, 37, np.int64)
+    src = np.concatenate([hub, rng.integers(0, n // 3, 200_000), np.arange(n - 50, n)])
+    dst = np.concatenate([rng.integers(0, n, 30_000), rng.integers(0, n // 3, 200_000), np.arange(n - 50, n)])
+    w = (1.0 - rng.random(src.size)).astype(np.float32) if weighted else None
+    y = gb.random_labels(n, k, 0.8, seed=k + 1)
+    dev = torch.device("cuda")
+    g = DeviceGraph.from_edges(torch.from_numpy(src).int(), torch.from_numpy(dst).int(),
+                               None if w is None else torch.from_numpy(w), n, device=dev, pull=True)
+    assert g.n_heavy >= 1
+    exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
+    out = {}
+    for red in ("blocks", "lists", "rows", "tiles"):
+        emb = Embedder(n, k, dev)
+        emb.reducer = red
+        out[red] = emb.embed(g, torch.from_numpy(y.labels).to(dev), variant="pull").cpu().numpy()
+        assert rel_err(out[red], exp) <= TOL, red
+    for red in ("lists", "rows"):
+        assert np.array_equal(out["blocks"].view(np.uint32), out[red].view(np.uint32)), red
