@@ -310,16 +310,19 @@ k_reduce_list(const int64_t *__restrict__ offsets, const int32_t *__restrict__ r
 // Block variant: one warp per block of 32 consecutive rows.  Lane i loads
 // offsets[r0+i] (one coalesced load per block).  The block's arcs stream in
 // rounds of 32 x 8 contiguous arcs (one 8-byte class load and two 16-byte
-// weight loads per lane, the next round in flight); a lane finds the row of
-// its first arc with a 5-step shuffle search over the lanes' offsets and
-// walks forward from there.  Nonempty rows get compact slots (ballot rank)
-// in a warp-private window.  The block's Z range is zero-filled with 16-byte
-// stores when it holds empty rows, then each nonempty row is written from its
-// slot; heavy rows are left to the chunked path (k_heavy_finalize runs
-// after).  Blocks with more than `nslots` nonempty rows take several passes.
+// weight loads per lane; the next round, and the next block's first round,
+// in flight).  Arc -> row mapping is branch-free: the lanes whose rows start
+// inside the round set bits in a 256-bit start mask (shared memory, three
+// rotating buffers so one __syncwarp per round suffices); a lane's arcs then
+// take the owner rank "rows started at or before the round" + popcounts.
+// Nonempty rows get compact slots in a warp-private window.  The block's Z
+// range is zero-filled with 16-byte stores when it holds empty rows, then the
+// nonempty rows are written from their slots in one flat loop; heavy rows are
+// left to the chunked path (k_heavy_finalize runs after).  Blocks with more
+// than `nslots` nonempty rows take several passes.
 constexpr int BU = 8;            // contiguous arcs per lane per round
 constexpr int BROUND = 32 * BU;  // arcs per warp round
-constexpr int BMETA = 72;        // per-warp ints: 33 local offsets + 32 slots (+pad)
+constexpr int BMETA = 96;        // per-warp ints: 3 x 8 mask words, 32 slots, 32 rows (+pad)
 
 template <bool WEIGHTED>
 __device__ __forceinline__ void block_round(const uint8_t *__restrict__ cls, const float *__restrict__ w, int64_t e,
@@ -350,82 +353,90 @@ __device__ __forceinline__ void block_round(const uint8_t *__restrict__ cls, con
 }
 
 template <bool WEIGHTED>
-__global__ void __launch_bounds__(RT)
+__global__ void __launch_bounds__(RT, 4)
 k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
                 const float *__restrict__ w, float qscale, double dscale, const double *__restrict__ inv, int32_t k,
                 int64_t heavy_arcs, int nslots, bool vec, float *__restrict__ z)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float *sc = reinterpret_cast<float *>(smem_raw);
     const int kk = k;
     const int pk = (kk + 3) & ~3;
     const int vecw = pk * Acc<WEIGHTED>::planes;
-    int32_t *meta = reinterpret_cast<int32_t *>(sc + ((kk + 4) & ~3));
+    float *sc1 = reinterpret_cast<float *>(smem_raw);  // sc1[c] = inv[c+1] * dscale
+    int32_t *meta = reinterpret_cast<int32_t *>(sc1 + pk);
     uint32_t *vbase = reinterpret_cast<uint32_t *>(meta + RW * BMETA);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int32_t *s_off = meta + wid * BMETA;  // [0, 33)
-    int32_t *s_slot = s_off + 36;         // [0, 32)
+    uint32_t *s_mask = reinterpret_cast<uint32_t *>(meta + wid * BMETA);  // 3 x 8 words
+    int32_t *s_slot = meta + wid * BMETA + 24;                              // by owner rank
+    int32_t *s_row = s_slot + 32;                                           // by slot
     uint32_t *v = vbase + wid * nslots * vecw;  // slot s: lo plane at v + s*pk, hi plane at + nslots*pk
     const int hoff = nslots * pk;
-    for (int c = threadIdx.x; c <= kk; c += RT) sc[c] = (float)(inv[c] * dscale);
+    for (int c = threadIdx.x; c < pk; c += RT) sc1[c] = c < kk ? (float)(inv[c + 1] * dscale) : 0.f;
     for (int i = threadIdx.x; i < RW * nslots * vecw; i += RT) vbase[i] = 0u;
+    for (int i = threadIdx.x; i < RW * BMETA; i += RT) meta[i] = 0;
     __syncthreads();
     const unsigned below = (1u << lane) - 1u;
     const int64_t nblocks = (n + 31) / 32;
     const int64_t gw = (int64_t)blockIdx.x * RW + wid, GW = (int64_t)gridDim.x * RW;
     const int64_t arcs = offsets[n];
+    const int half = kk >> 1;
 
     int64_t b = gw;
     int64_t o_lo = 0;
-    if (b < nblocks) o_lo = __ldcs(offsets + min(32 * b + lane, n));
+    uint2 ca = make_uint2(0u, 0u);
+    float wa[BU];
+    if (b < nblocks) {
+        o_lo = __ldcs(offsets + min(32 * b + lane, n));
+        const int64_t b0 = __shfl_sync(0xffffffffu, o_lo, 0) & ~(int64_t)(BU - 1);
+        block_round<WEIGHTED>(cls, w, b0 + lane * BU, arcs, vec, ca, wa);
+    }
+    int rot = 0;  // mask buffer rotation
     for (; b < nblocks; b += GW) {
         const int64_t r0 = 32 * b;
         int64_t o_hi = __shfl_down_sync(0xffffffffu, o_lo, 1);
         if (lane == 31) o_hi = r0 + 32 <= n ? __ldcs(offsets + r0 + 32) : arcs;
-        const int64_t o_nx = (b + GW < nblocks) ? __ldcs(offsets + min(32 * (b + GW) + lane, n)) : 0;
+        const bool more = b + GW < nblocks;
+        const int64_t o_nx = more ? __ldcs(offsets + min(32 * (b + GW) + lane, n)) : 0;
         const bool valid = r0 + lane < n;
         const int64_t d = valid ? o_hi - o_lo : 0;
         const bool heavy = d > heavy_arcs;
         const bool nz = d > 0 && !heavy;
         const unsigned nzm = __ballot_sync(0xffffffffu, nz), hvm = __ballot_sync(0xffffffffu, heavy);
+        const unsigned anym = nzm | hvm;
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
-        const int rank = __popc(nzm & below);
+        const int rank = __popc(nzm & below);  // slot order among light nonempty rows
+        const int orank = __popc(anym & below);  // owner order among all nonempty rows
         const int nnz = __popc(nzm);
         const int64_t base = __shfl_sync(0xffffffffu, o_lo, 0);
         const int64_t bend = __shfl_sync(0xffffffffu, o_hi, 31);
         const int32_t ol = (int32_t)(o_lo - base);  // local start of this lane's row
+        const bool owner = (anym >> lane) & 1u;
         const int32_t lend = (int32_t)(bend - base);
         const int rows = (int)min((int64_t)32, n - r0);
         float *zb = z + r0 * (int64_t)kk;
-        if ((nzm | hvm) != vm) {  // the block holds empty rows: zero-fill its Z range
+        if ((anym) != vm) {  // the block holds empty rows: zero-fill its Z range
             const int total = rows * kk;
             const int q4 = total >> 2;
             float4 *z4 = reinterpret_cast<float4 *>(zb);
             for (int q = lane; q < q4; q += 32) z4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int e = 4 * q4 + lane; e < total; e += 32) zb[e] = 0.f;
         }
-        s_off[lane] = ol;
-        if (lane == 31) s_off[32] = lend;
         for (int p0 = 0; p0 < nnz; p0 += nslots) {
             const bool mine = nz && rank >= p0 && rank < p0 + nslots;
-            s_slot[lane] = mine ? rank - p0 : -1;
-            const unsigned pm0 = __ballot_sync(0xffffffffu, mine);
+            if (owner) s_slot[orank] = mine ? rank - p0 : -1;
+            if (mine) s_row[rank - p0] = lane;
+            const int npass = min(nslots, nnz - p0);
             __syncwarp();
             int64_t e0 = base & ~(int64_t)(BU - 1);
-            uint2 ca;
-            float wa[BU];
-            block_round<WEIGHTED>(cls, w, e0 + lane * BU, arcs, vec, ca, wa);
+            if (p0 > 0) block_round<WEIGHTED>(cls, w, e0 + lane * BU, arcs, vec, ca, wa);
             while (e0 < bend) {
-                if (hvm) {  // skip a heavy row's arcs wholesale (warp-uniform)
-                    const int32_t ls = (int32_t)max(e0 - base, (int64_t)0);
-                    int j = 0;
-#pragma unroll
-                    for (int st = 16; st; st >>= 1) {
-                        const int32_t oc = __shfl_sync(0xffffffffu, ol, (j + st) & 31);
-                        if (j + st < 32 && oc <= ls) j += st;
-                    }
-                    const int64_t hend = base + s_off[j + 1];
-                    if (((hvm >> j) & 1u) && hend >= e0 + BROUND) {  // whole round inside the heavy row
+                const int32_t lr = (int32_t)(e0 - base);  // >= -(BU-1)
+                // rows started at or before the round's first arc
+                const unsigned startm = __ballot_sync(0xffffffffu, owner && ol <= lr);
+                if (hvm && startm) {  // skip a heavy row's arcs wholesale (warp-uniform)
+                    const int jr = 31 - __clz(startm);
+                    const int64_t hend = __shfl_sync(0xffffffffu, o_hi, jr);
+                    if (((hvm >> jr) & 1u) && hend >= e0 + BROUND) {
                         e0 = hend & ~(int64_t)(BU - 1);
                         block_round<WEIGHTED>(cls, w, e0 + lane * BU, arcs, vec, ca, wa);
                         continue;
@@ -435,28 +446,33 @@ k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *_
                 uint2 cb = make_uint2(0u, 0u);
                 float wb[BU];
                 if (e1 < bend) block_round<WEIGHTED>(cls, w, e1 + lane * BU, arcs, vec, cb, wb);
-                const int32_t le = (int32_t)(e0 + lane * BU - base);
-                const int32_t ls = max(le, 0);
-                int j = 0;  // row of this lane's first arc: last lane j with ol[j] <= ls
+                // start mask of the rows beginning inside the round
+                uint32_t *mk = s_mask + 8 * rot;
+                const int32_t pos = ol - lr;
+                if (owner && pos > 0 && pos < BROUND) atomicOr(mk + (pos >> 5), 1u << (pos & 31));
+                __syncwarp();
+                const uint32_t word = mk[lane >> 2];
+                const uint32_t mb = (word >> (8 * (lane & 3))) & 0xffu;
+                if (lane < 8) s_mask[8 * (rot == 0 ? 2 : rot - 1) + lane] = 0u;  // buffer read last round
+                rot = rot == 2 ? 0 : rot + 1;
+                // starts in earlier lanes' arcs: exclusive scan of popc(mb)
+                const int pc = __popc(mb);
+                int incl = pc;
 #pragma unroll
-                for (int st = 16; st; st >>= 1) {
-                    const int32_t oc = __shfl_sync(0xffffffffu, ol, (j + st) & 31);
-                    if (j + st < 32 && oc <= ls) j += st;
+                for (int st = 1; st < 32; st <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, st);
+                    if (lane >= st) incl += t;
                 }
-                if (le < lend) {
-                    int32_t nxt = s_off[j + 1];
-                    int slot = s_slot[j];
+                int r = __popc(startm) - 1 + incl - pc;  // owner rank before this lane's first arc
+                const int32_t a0 = lr + lane * BU;
 #pragma unroll
-                    for (int u = 0; u < BU; u++) {
-                        const int32_t a = le + u;
-                        while (a >= nxt && j < 31) {
-                            j++;
-                            nxt = s_off[j + 1];
-                            slot = s_slot[j];
-                        }
-                        const uint32_t c = ((u < 4 ? ca.x : ca.y) >> (8 * (u & 3))) & 0xffu;
-                        if (a >= 0 && a < nxt && slot >= 0 && c != 0u && c <= (uint32_t)kk)
-                            acc_add<WEIGHTED>(v + slot * pk, hoff, c, WEIGHTED ? wa[u] : 1.f, qscale);
+                for (int u = 0; u < BU; u++) {
+                    r += (mb >> u) & 1u;
+                    const int32_t a = a0 + u;
+                    const uint32_t c = ((u < 4 ? ca.x : ca.y) >> (8 * (u & 3))) & 0xffu;
+                    if (r >= 0 && a < lend && c != 0u && c <= (uint32_t)kk) {
+                        const int slot = s_slot[r];
+                        if (slot >= 0) acc_add<WEIGHTED>(v + slot * pk, hoff, c, WEIGHTED ? wa[u] : 1.f, qscale);
                     }
                 }
                 ca = cb;
@@ -465,28 +481,54 @@ k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *_
                 e0 = e1;
             }
             __syncwarp();
-            // write this pass's rows from their slots
-            unsigned pm = pm0;
-            while (pm) {
-                const int rr = __ffs(pm) - 1;
-                pm &= pm - 1;
-                const int slot = __popc(nzm & ((1u << rr) - 1u)) - p0;
-                uint32_t *vs = v + slot * pk;
-                float *zr = zb + (int64_t)rr * kk;
-                if ((kk & 1) == 0) {
-                    float2 *z2 = reinterpret_cast<float2 *>(zr);
-                    for (int c2 = lane; c2 < (kk >> 1); c2 += 32) {
-                        const float x0 = (float)acc_take<WEIGHTED>(vs, hoff, 2 * c2) * sc[2 * c2 + 1];
-                        const float x1 = (float)acc_take<WEIGHTED>(vs, hoff, 2 * c2 + 1) * sc[2 * c2 + 2];
-                        __stcs(z2 + c2, make_float2(x0, x1));
+            // write this pass's rows from their slots: flat over (row, column pair)
+            if ((kk & 1) == 0) {
+                const int total = npass * half;
+                int sl = lane / half, c2 = lane - sl * half;
+                const int dsl = 32 / half, dc2 = 32 - dsl * half;
+                for (int q = lane; q < total; q += 32) {
+                    uint32_t *vs = v + sl * pk + 2 * c2;
+                    const uint2 lo = *reinterpret_cast<uint2 *>(vs);
+                    *reinterpret_cast<uint2 *>(vs) = make_uint2(0u, 0u);
+                    long long s0 = (long long)lo.x, s1 = (long long)lo.y;
+                    if (WEIGHTED) {
+                        const uint2 hi = *reinterpret_cast<uint2 *>(vs + hoff);
+                        *reinterpret_cast<uint2 *>(vs + hoff) = make_uint2(0u, 0u);
+                        s0 = (long long)(((unsigned long long)hi.x << 32) | lo.x);
+                        s1 = (long long)(((unsigned long long)hi.y << 32) | lo.y);
                     }
-                } else {
-                    for (int c = lane; c < kk; c += 32) __stcs(zr + c, (float)acc_take<WEIGHTED>(vs, hoff, c) * sc[c + 1]);
+                    const float2 f = *reinterpret_cast<const float2 *>(sc1 + 2 * c2);
+                    float2 *zr = reinterpret_cast<float2 *>(zb + (int64_t)s_row[sl] * kk);
+                    __stcs(zr + c2, make_float2((float)s0 * f.x, (float)s1 * f.y));
+                    sl += dsl;
+                    c2 += dc2;
+                    if (c2 >= half) {
+                        c2 -= half;
+                        sl++;
+                    }
+                }
+            } else {
+                const int total = npass * kk;
+                int sl = lane / kk, c = lane - sl * kk;
+                const int dsl = 32 / kk, dc = 32 - dsl * kk;
+                for (int q = lane; q < total; q += 32) {
+                    __stcs(zb + (int64_t)s_row[sl] * kk + c, (float)acc_take<WEIGHTED>(v + sl * pk, hoff, c) * sc1[c]);
+                    sl += dsl;
+                    c += dc;
+                    if (c >= kk) {
+                        c -= kk;
+                        sl++;
+                    }
                 }
             }
             __syncwarp();
         }
+        // next block: its first round in flight while this one finishes
         o_lo = o_nx;
+        if (more) {
+            const int64_t b0 = __shfl_sync(0xffffffffu, o_nx, 0) & ~(int64_t)(BU - 1);
+            block_round<WEIGHTED>(cls, w, b0 + lane * BU, arcs, vec, ca, wa);
+        }
     }
 }
 
@@ -770,12 +812,13 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
     const size_t vec = (((size_t)k + 3) & ~(size_t)3) * (weighted ? 2 : 1) * sizeof(uint32_t);
-    const size_t scb = ((size_t)(k + 4) & ~(size_t)3) * sizeof(float);
     // slots per warp: up to 16, within ~64 KB per CTA so several CTAs fit per SM
-    int nslots = (int)((56 * 1024) / (RW * vec));
+    // slots per warp: up to 16, within ~48 KB per CTA so four CTAs fit per SM
+    const size_t fixed = (((size_t)k + 3) & ~(size_t)3) * sizeof(float) + (size_t)RW * BMETA * sizeof(int32_t);
+    int nslots = (int)((48 * 1024 - fixed) / (RW * vec));
     if (nslots > 16) nslots = 16;
     if (nslots < 1) nslots = 1;
-    const size_t sh = scb + (size_t)RW * BMETA * sizeof(int32_t) + (size_t)RW * nslots * vec;
+    const size_t sh = fixed + (size_t)RW * nslots * vec;
     const bool vld = (reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0);
     GEE_REQUIRE((reinterpret_cast<uintptr_t>(z) & 15) == 0, GEE_ERR_INVALID, "z must be 16-byte aligned");
     const int64_t nblocks = (n + 31) / 32;
