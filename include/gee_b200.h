@@ -231,12 +231,19 @@ int gee_reduce_lists(const int64_t *offsets, const int32_t *small_rows, int64_t 
 
 /* Block reduction: one warp per 32 consecutive rows (coalesced offsets,
  * streamed arcs, one flat coalesced write of the block's Z rows); heavy rows
- * as in gee_reduce_rows.  k <= 255. */
+ * as in gee_reduce_rows.  k <= 255; heavy_arcs <= 2048; weighted graphs need
+ * the exponent from gee_block_scale_exp (carry-free split accumulators). */
 int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
                       int32_t scale_exp, const double *inv, int32_t k, int64_t heavy_arcs,
                       const int32_t *heavy_rows, int64_t n_heavy, const int64_t *chunk_first,
                       const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
                       void *stream);
+
+/* Fixed-point exponent valid for every pull reducer, gee_reduce_blocks
+ * included: the largest e with max_row_abs * 2^e < 2^62 and
+ * max_abs * 2^e < 2^42.  *rel_err = 2^-(e+1)/min_abs_nz (host). */
+int gee_block_scale_exp(double max_row_abs, double max_abs, double min_abs_nz, int32_t *scale_exp,
+                        double *rel_err);
 
 /* Choose the fixed-point exponent for a weighted pull: the largest e with
  * max_row_abs * 2^e < 2^62.  Returns the relative quantisation bound

@@ -10,7 +10,10 @@ import os
 from .errors import GeeError, ValidationError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgee_b200_debug.so" if os.environ.get("GEE_DEBUG_LIB") else "libgee_b200.so")
+# GEE_LIB_VARIANT=<tag> loads libgee_b200_<tag>.so from the package (build
+# experiments); GEE_DEBUG_LIB=1 the bounds-checked debug build.
+_VARIANT = os.environ.get("GEE_LIB_VARIANT") or ("debug" if os.environ.get("GEE_DEBUG_LIB") else "")
+LIB_PATH = os.path.join(_PKG, f"libgee_b200_{_VARIANT}.so" if _VARIANT else "libgee_b200.so")
 
 GEE_OK = 0
 GEE_ERR_INVALID = 1
@@ -63,6 +66,7 @@ SIGNATURES = {
     "gee_gather_labels": (c_int, [vp, c_i64, vp, c_i64, c_i32, vp, vp]),
     "gee_reduce_heavy_plan": (c_int, [vp, c_i64, c_i64, vp, ctypes.POINTER(c_i64), vp]),
     "gee_reduce_blocks": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, c_i64, vp, vp, c_i64, vp, vp, vp]),
+    "gee_block_scale_exp": (c_int, [c_dbl, c_dbl, c_dbl, P_i32, P_dbl]),
     "gee_reduce_bins": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), vp]),
     "gee_reduce_lists": (c_int, [vp, vp, c_i64, vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, c_i64, vp, vp, c_i64,
                                  vp, vp, vp]),

@@ -29,6 +29,19 @@ inline int sm_count()
     return sms;
 }
 
+// Shared memory per SM (bytes) available to resident CTAs.
+inline int smem_per_sm()
+{
+    static int b = 0;
+    if (!b) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&b, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        if (b <= 0) b = 228 * 1024;
+    }
+    return b;
+}
+
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 template <typename T>

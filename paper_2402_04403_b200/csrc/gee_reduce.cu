@@ -320,9 +320,14 @@ k_reduce_list(const int64_t *__restrict__ offsets, const int32_t *__restrict__ r
 // nonempty rows are written from their slots in one flat loop; heavy rows are
 // left to the chunked path (k_heavy_finalize runs after).  Blocks with more
 // than `nslots` nonempty rows take several passes.
+#ifndef BLOCKS_MINB
+#define BLOCKS_MINB 3  // CTAs per SM the block reducer is register-capped for
+#endif
 constexpr int BU = 8;            // contiguous arcs per lane per round
+constexpr int BLOCK_SPLIT = 21;  // weighted: low plane takes q's low 21 bits
+constexpr int64_t BLOCK_ROW_MAX = 2048;  // longest row the block kernel takes (longer: heavy path)
 constexpr int BROUND = 32 * BU;  // arcs per warp round
-constexpr int BMETA = 96;        // per-warp ints: 3 x 8 mask words, 32 slots, 32 rows (+pad)
+constexpr int BMETA = 96;        // per-warp ints: 3 x 8 mask words, 33 slot offsets, 32 rows (+pad)
 
 template <bool WEIGHTED>
 __device__ __forceinline__ void block_round(const uint8_t *__restrict__ cls, const float *__restrict__ w, int64_t e,
@@ -352,29 +357,82 @@ __device__ __forceinline__ void block_round(const uint8_t *__restrict__ cls, con
     }
 }
 
+// Window of one warp: per plane [nslots x vector | 32 trash words]; a slot's
+// vector is [3 pad | unused | bin 1 .. bin k | pad] so that bin pairs
+// (2j+1, 2j+2) are 8-byte aligned for the write-out.  Masked arcs (class 0,
+// past the block, rows outside this pass) add into the lane's own trash
+// word: no branch, and no two lanes on one address.
+__host__ __device__ constexpr int block_vec_words(int k) { return 4 + ((k + 3) & ~3); }
+
+// One round of arcs already in registers: start mask -> owner ranks -> slots.
 template <bool WEIGHTED>
-__global__ void __launch_bounds__(RT, 4)
+__device__ __forceinline__ void block_round_acc(uint32_t *__restrict__ vw, const int32_t *__restrict__ s_soff,
+                                                uint32_t *__restrict__ s_mask, int &rot, int lane, bool owner,
+                                                int32_t ol, int32_t lr, int32_t lend, int hoff, int trash,
+                                                float qscale, const uint2 &ca, const float (&wa)[BU])
+{
+    const unsigned startm = __ballot_sync(0xffffffffu, owner && ol <= lr);
+    uint32_t *mk = s_mask + 8 * rot;
+    const int32_t pos = ol - lr;
+    if (owner && pos > 0 && pos < BROUND) atomicOr(mk + (pos >> 5), 1u << (pos & 31));
+    __syncwarp();
+    const uint32_t mb = (mk[lane >> 2] >> (8 * (lane & 3))) & 0xffu;
+    if (lane < 8) s_mask[8 * (rot == 0 ? 2 : rot - 1) + lane] = 0u;  // buffer read last round
+    rot = rot == 2 ? 0 : rot + 1;
+    const int pc = __popc(mb);
+    int incl = pc;
+#pragma unroll
+    for (int st = 1; st < 32; st <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, st);
+        incl += lane >= st ? t : 0;
+    }
+    int r = __popc(startm) + incl - pc;  // owner rank + 1 before this lane's first arc
+    const int nvalid = lend - (lr + lane * BU);
+#pragma unroll
+    for (int u = 0; u < BU; u++) {
+        r += (mb >> u) & 1u;
+        const uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
+        const int so = s_soff[r];
+        const int idx = (c != 0u && u < nvalid && so >= 0) ? so + (int)c : trash;
+        if (WEIGHTED) {
+            // carry-free split q = A * 2^21 + B: both plane sums stay below
+            // 2^32 (rows <= BLOCK_ROW_MAX arcs, q < 2^42), so neither add
+            // needs its return value
+            const unsigned long long q = (unsigned long long)__float2ll_rn(wa[u] * qscale);
+            atomicAdd(vw + idx, (uint32_t)q & ((1u << BLOCK_SPLIT) - 1u));
+            atomicAdd(vw + hoff + idx, (uint32_t)(q >> BLOCK_SPLIT));
+        } else {
+            atomicAdd(vw + idx, 1u);
+        }
+    }
+}
+
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(RT, BLOCKS_MINB)
 k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
                 const float *__restrict__ w, float qscale, double dscale, const double *__restrict__ inv, int32_t k,
                 int64_t heavy_arcs, int nslots, bool vec, float *__restrict__ z)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int kk = k;
-    const int pk = (kk + 3) & ~3;
-    const int vecw = pk * Acc<WEIGHTED>::planes;
+    const int pkb = block_vec_words(kk);
+    const int hoff = nslots * pkb + 32;  // hi plane offset
+    const int wwords = hoff * Acc<WEIGHTED>::planes;
     float *sc1 = reinterpret_cast<float *>(smem_raw);  // sc1[c] = inv[c+1] * dscale
-    int32_t *meta = reinterpret_cast<int32_t *>(sc1 + pk);
+    int32_t *meta = reinterpret_cast<int32_t *>(sc1 + pkb);
     uint32_t *vbase = reinterpret_cast<uint32_t *>(meta + RW * BMETA);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t *s_mask = reinterpret_cast<uint32_t *>(meta + wid * BMETA);  // 3 x 8 words
-    int32_t *s_slot = meta + wid * BMETA + 24;                              // by owner rank
-    int32_t *s_row = s_slot + 32;                                           // by slot
-    uint32_t *v = vbase + wid * nslots * vecw;  // slot s: lo plane at v + s*pk, hi plane at + nslots*pk
-    const int hoff = nslots * pk;
-    for (int c = threadIdx.x; c < pk; c += RT) sc1[c] = c < kk ? (float)(inv[c + 1] * dscale) : 0.f;
-    for (int i = threadIdx.x; i < RW * nslots * vecw; i += RT) vbase[i] = 0u;
-    for (int i = threadIdx.x; i < RW * BMETA; i += RT) meta[i] = 0;
+    int32_t *s_soff = meta + wid * BMETA + 24;                              // [owner rank + 1] -> slot offset
+    int32_t *s_row = s_soff + 36;                                           // [slot] -> row in block
+    uint32_t *vw = vbase + wid * wwords;
+    for (int c = threadIdx.x; c < pkb; c += RT) sc1[c] = c < kk ? (float)(inv[c + 1] * dscale) : 0.f;
+    for (int i = threadIdx.x; i < RW * wwords; i += RT) vbase[i] = 0u;
+    for (int i = threadIdx.x; i < RW * BMETA; i += RT) meta[i] = -1;
     __syncthreads();
+    if (lane < 24) s_mask[lane] = 0u;
+    __syncwarp();
+    const int trash = nslots * pkb + lane;
     const unsigned below = (1u << lane) - 1u;
     const int64_t nblocks = (n + 31) / 32;
     const int64_t gw = (int64_t)blockIdx.x * RW + wid, GW = (int64_t)gridDim.x * RW;
@@ -383,8 +441,10 @@ k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *_
 
     int64_t b = gw;
     int64_t o_lo = 0;
-    uint2 ca = make_uint2(0u, 0u);
-    float wa[BU];
+    uint2 ca = make_uint2(0u, 0u), cb = make_uint2(0u, 0u);
+    float wa[BU], wb[BU];
+#pragma unroll
+    for (int u = 0; u < BU; u++) wa[u] = wb[u] = 0.f;
     if (b < nblocks) {
         o_lo = __ldcs(offsets + min(32 * b + lane, n));
         const int64_t b0 = __shfl_sync(0xffffffffu, o_lo, 0) & ~(int64_t)(BU - 1);
@@ -404,17 +464,19 @@ k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *_
         const unsigned nzm = __ballot_sync(0xffffffffu, nz), hvm = __ballot_sync(0xffffffffu, heavy);
         const unsigned anym = nzm | hvm;
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
-        const int rank = __popc(nzm & below);  // slot order among light nonempty rows
+        const int rank = __popc(nzm & below);    // slot order among light nonempty rows
         const int orank = __popc(anym & below);  // owner order among all nonempty rows
         const int nnz = __popc(nzm);
         const int64_t base = __shfl_sync(0xffffffffu, o_lo, 0);
-        const int64_t bend = __shfl_sync(0xffffffffu, o_hi, 31);
+        const int64_t abase = base & ~(int64_t)(BU - 1);
         const int32_t ol = (int32_t)(o_lo - base);  // local start of this lane's row
+        const int32_t oh = (int32_t)(o_hi - base);
         const bool owner = (anym >> lane) & 1u;
-        const int32_t lend = (int32_t)(bend - base);
+        const int32_t lend = __shfl_sync(0xffffffffu, oh, 31);
+        const int32_t lr0 = (int32_t)(abase - base);  // in [-(BU-1), 0]
         const int rows = (int)min((int64_t)32, n - r0);
         float *zb = z + r0 * (int64_t)kk;
-        if ((anym) != vm) {  // the block holds empty rows: zero-fill its Z range
+        if (anym != vm) {  // the block holds empty rows: zero-fill its Z range
             const int total = rows * kk;
             const int q4 = total >> 2;
             float4 *z4 = reinterpret_cast<float4 *>(zb);
@@ -423,62 +485,49 @@ k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *_
         }
         for (int p0 = 0; p0 < nnz; p0 += nslots) {
             const bool mine = nz && rank >= p0 && rank < p0 + nslots;
-            if (owner) s_slot[orank] = mine ? rank - p0 : -1;
+            if (owner) s_soff[orank + 1] = mine ? (rank - p0) * pkb + 3 : -1;
             if (mine) s_row[rank - p0] = lane;
             const int npass = min(nslots, nnz - p0);
             __syncwarp();
-            int64_t e0 = base & ~(int64_t)(BU - 1);
-            if (p0 > 0) block_round<WEIGHTED>(cls, w, e0 + lane * BU, arcs, vec, ca, wa);
-            while (e0 < bend) {
-                const int32_t lr = (int32_t)(e0 - base);  // >= -(BU-1)
-                // rows started at or before the round's first arc
-                const unsigned startm = __ballot_sync(0xffffffffu, owner && ol <= lr);
-                if (hvm && startm) {  // skip a heavy row's arcs wholesale (warp-uniform)
-                    const int jr = 31 - __clz(startm);
-                    const int64_t hend = __shfl_sync(0xffffffffu, o_hi, jr);
-                    if (((hvm >> jr) & 1u) && hend >= e0 + BROUND) {
-                        e0 = hend & ~(int64_t)(BU - 1);
-                        block_round<WEIGHTED>(cls, w, e0 + lane * BU, arcs, vec, ca, wa);
-                        continue;
+            int32_t lr = lr0;
+            if (p0 > 0) block_round<WEIGHTED>(cls, w, abase + lane * BU, arcs, vec, ca, wa);
+            // rounds, ping-ponging between the (ca, wa) and (cb, wb) buffers
+            while (lr < lend) {
+                if (hvm) {  // skip a heavy row's arcs wholesale (warp-uniform)
+                    const unsigned sm = __ballot_sync(0xffffffffu, owner && ol <= lr);
+                    if (sm) {
+                        const int jr = 31 - __clz(sm);
+                        const int32_t hend = __shfl_sync(0xffffffffu, oh, jr);
+                        if (((hvm >> jr) & 1u) && hend >= lr + BROUND) {
+                            lr = ((hend - lr0) & ~(BU - 1)) + lr0;
+                            block_round<WEIGHTED>(cls, w, abase + (lr - lr0) + lane * BU, arcs, vec, ca, wa);
+                            continue;
+                        }
                     }
                 }
-                const int64_t e1 = e0 + BROUND;
-                uint2 cb = make_uint2(0u, 0u);
-                float wb[BU];
-                if (e1 < bend) block_round<WEIGHTED>(cls, w, e1 + lane * BU, arcs, vec, cb, wb);
-                // start mask of the rows beginning inside the round
-                uint32_t *mk = s_mask + 8 * rot;
-                const int32_t pos = ol - lr;
-                if (owner && pos > 0 && pos < BROUND) atomicOr(mk + (pos >> 5), 1u << (pos & 31));
-                __syncwarp();
-                const uint32_t word = mk[lane >> 2];
-                const uint32_t mb = (word >> (8 * (lane & 3))) & 0xffu;
-                if (lane < 8) s_mask[8 * (rot == 0 ? 2 : rot - 1) + lane] = 0u;  // buffer read last round
-                rot = rot == 2 ? 0 : rot + 1;
-                // starts in earlier lanes' arcs: exclusive scan of popc(mb)
-                const int pc = __popc(mb);
-                int incl = pc;
-#pragma unroll
-                for (int st = 1; st < 32; st <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, st);
-                    if (lane >= st) incl += t;
-                }
-                int r = __popc(startm) - 1 + incl - pc;  // owner rank before this lane's first arc
-                const int32_t a0 = lr + lane * BU;
-#pragma unroll
-                for (int u = 0; u < BU; u++) {
-                    r += (mb >> u) & 1u;
-                    const int32_t a = a0 + u;
-                    const uint32_t c = ((u < 4 ? ca.x : ca.y) >> (8 * (u & 3))) & 0xffu;
-                    if (r >= 0 && a < lend && c != 0u && c <= (uint32_t)kk) {
-                        const int slot = s_slot[r];
-                        if (slot >= 0) acc_add<WEIGHTED>(v + slot * pk, hoff, c, WEIGHTED ? wa[u] : 1.f, qscale);
+                int32_t l1 = lr + BROUND;
+                if (l1 < lend) block_round<WEIGHTED>(cls, w, abase + (l1 - lr0) + lane * BU, arcs, vec, cb, wb);
+                block_round_acc<WEIGHTED>(vw, s_soff, s_mask, rot, lane, owner, ol, lr, lend, hoff, trash, qscale,
+                                          ca, wa);
+                lr = l1;
+                if (lr >= lend) break;
+                if (hvm) {
+                    const unsigned sm = __ballot_sync(0xffffffffu, owner && ol <= lr);
+                    if (sm) {
+                        const int jr = 31 - __clz(sm);
+                        const int32_t hend = __shfl_sync(0xffffffffu, oh, jr);
+                        if (((hvm >> jr) & 1u) && hend >= lr + BROUND) {
+                            lr = ((hend - lr0) & ~(BU - 1)) + lr0;
+                            block_round<WEIGHTED>(cls, w, abase + (lr - lr0) + lane * BU, arcs, vec, ca, wa);
+                            continue;
+                        }
                     }
                 }
-                ca = cb;
-#pragma unroll
-                for (int u = 0; u < BU; u++) wa[u] = wb[u];
-                e0 = e1;
+                l1 = lr + BROUND;
+                if (l1 < lend) block_round<WEIGHTED>(cls, w, abase + (l1 - lr0) + lane * BU, arcs, vec, ca, wa);
+                block_round_acc<WEIGHTED>(vw, s_soff, s_mask, rot, lane, owner, ol, lr, lend, hoff, trash, qscale,
+                                          cb, wb);
+                lr = l1;
             }
             __syncwarp();
             // write this pass's rows from their slots: flat over (row, column pair)
@@ -487,19 +536,22 @@ k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *_
                 int sl = lane / half, c2 = lane - sl * half;
                 const int dsl = 32 / half, dc2 = 32 - dsl * half;
                 for (int q = lane; q < total; q += 32) {
-                    uint32_t *vs = v + sl * pk + 2 * c2;
+                    uint32_t *vs = vw + sl * pkb + 4 + 2 * c2;
                     const uint2 lo = *reinterpret_cast<uint2 *>(vs);
                     *reinterpret_cast<uint2 *>(vs) = make_uint2(0u, 0u);
-                    long long s0 = (long long)lo.x, s1 = (long long)lo.y;
+                    float s0, s1;
                     if (WEIGHTED) {
                         const uint2 hi = *reinterpret_cast<uint2 *>(vs + hoff);
                         *reinterpret_cast<uint2 *>(vs + hoff) = make_uint2(0u, 0u);
-                        s0 = (long long)(((unsigned long long)hi.x << 32) | lo.x);
-                        s1 = (long long)(((unsigned long long)hi.y << 32) | lo.y);
+                        s0 = (float)(long long)(((unsigned long long)hi.x << BLOCK_SPLIT) + lo.x);
+                        s1 = (float)(long long)(((unsigned long long)hi.y << BLOCK_SPLIT) + lo.y);
+                    } else {
+                        s0 = (float)lo.x;
+                        s1 = (float)lo.y;
                     }
                     const float2 f = *reinterpret_cast<const float2 *>(sc1 + 2 * c2);
-                    float2 *zr = reinterpret_cast<float2 *>(zb + (int64_t)s_row[sl] * kk);
-                    __stcs(zr + c2, make_float2((float)s0 * f.x, (float)s1 * f.y));
+                    float2 *zr = reinterpret_cast<float2 *>(zb + s_row[sl] * kk);
+                    __stcs(zr + c2, make_float2(s0 * f.x, s1 * f.y));
                     sl += dsl;
                     c2 += dc2;
                     if (c2 >= half) {
@@ -512,7 +564,18 @@ k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *_
                 int sl = lane / kk, c = lane - sl * kk;
                 const int dsl = 32 / kk, dc = 32 - dsl * kk;
                 for (int q = lane; q < total; q += 32) {
-                    __stcs(zb + (int64_t)s_row[sl] * kk + c, (float)acc_take<WEIGHTED>(v + sl * pk, hoff, c) * sc1[c]);
+                    uint32_t *vs = vw + sl * pkb + 4 + c;
+                    const uint32_t lo = *vs;
+                    *vs = 0u;
+                    float s0;
+                    if (WEIGHTED) {
+                        const uint32_t hi = vs[hoff];
+                        vs[hoff] = 0u;
+                        s0 = (float)(long long)(((unsigned long long)hi << BLOCK_SPLIT) + lo);
+                    } else {
+                        s0 = (float)lo;
+                    }
+                    __stcs(zb + s_row[sl] * kk + c, s0 * sc1[c]);
                     sl += dsl;
                     c += dc;
                     if (c >= kk) {
@@ -813,14 +876,22 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
     const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
     const size_t vec = (((size_t)k + 3) & ~(size_t)3) * (weighted ? 2 : 1) * sizeof(uint32_t);
     // slots per warp: up to 16, within ~64 KB per CTA so several CTAs fit per SM
-    // slots per warp: up to 16, within ~48 KB per CTA so four CTAs fit per SM
-    const size_t fixed = (((size_t)k + 3) & ~(size_t)3) * sizeof(float) + (size_t)RW * BMETA * sizeof(int32_t);
-    int nslots = (int)((48 * 1024 - fixed) / (RW * vec));
-    if (nslots > 16) nslots = 16;
+    // slots per warp: up to 24 (+32 trash words), within the shared memory
+    // share of one of the BLOCKS_MINB CTAs per SM
+    const size_t planes = weighted ? 2 : 1;
+    const size_t fixed = (size_t)block_vec_words(k) * sizeof(float) + (size_t)RW * BMETA * sizeof(int32_t) +
+                         (size_t)RW * planes * 32 * sizeof(uint32_t);
+    const size_t vecb = (size_t)block_vec_words(k) * planes * sizeof(uint32_t);
+    const size_t budget = (size_t)(gee::smem_per_sm() / BLOCKS_MINB) - 1024;
+    int nslots = (int)((budget - fixed) / (RW * vecb));
+    if (nslots > 24) nslots = 24;
     if (nslots < 1) nslots = 1;
-    const size_t sh = fixed + (size_t)RW * nslots * vec;
+    const size_t sh = fixed + (size_t)RW * nslots * vecb;
     const bool vld = (reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0);
     GEE_REQUIRE((reinterpret_cast<uintptr_t>(z) & 15) == 0, GEE_ERR_INVALID, "z must be 16-byte aligned");
+    GEE_REQUIRE(heavy_arcs <= BLOCK_ROW_MAX, GEE_ERR_INVALID,
+                "block reducer takes rows of at most %lld arcs (heavy_arcs %lld)", (long long)BLOCK_ROW_MAX,
+                (long long)heavy_arcs);
     const int64_t nblocks = (n + 31) / 32;
     const int grid = grid_for(nblocks * 32, RT, 8);
     int rc;
@@ -849,6 +920,27 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
     else
         k_heavy_finalize<false><<<fgrid, 256, 0, st>>>(heavy_rows, n_heavy, k, acc, inv, dscale, z);
     return gee::check_launch("k_heavy_finalize");
+}
+
+int gee_block_scale_exp(double max_row_abs, double max_abs, double min_abs_nz, int32_t *scale_exp, double *rel_err)
+{
+    gee::clear_error();
+    GEE_REQUIRE(scale_exp != nullptr, GEE_ERR_INVALID, "scale_exp must not be NULL");
+    int e = 126;
+    int ex;
+    if (max_row_abs > 0) {  // max_row_abs * 2^e < 2^62 (64-bit row sums, heavy path)
+        frexp(max_row_abs, &ex);
+        e = min(e, 62 - ex);
+    }
+    if (max_abs > 0) {  // max|w| * 2^e < 2^(BLOCK_SPLIT + 21): the split planes stay below 2^32
+        frexp(max_abs, &ex);
+        e = min(e, BLOCK_SPLIT + 21 - ex);
+    }
+    if (max_row_abs <= 0 && max_abs <= 0) e = 0;
+    if (e < -126) e = -126;
+    *scale_exp = e;
+    if (rel_err) *rel_err = min_abs_nz > 0 ? ldexp(1.0, -(e + 1)) / min_abs_nz : 0.0;
+    return GEE_OK;
 }
 
 }  // extern "C"

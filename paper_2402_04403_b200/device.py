@@ -160,10 +160,11 @@ class DeviceGraph:
             raise ValidationError("arc weights must be finite")
         self.max_row_abs = mx.value
         e, rel = ctypes.c_int32(), ctypes.c_double()
-        check(lib.gee_pull_scale_exp(mx.value, mn.value, ctypes.byref(e), ctypes.byref(rel)), "gee_pull_scale_exp")
+        check(lib.gee_block_scale_exp(mx.value, mxa.value, mn.value, ctypes.byref(e), ctypes.byref(rel)),
+              "gee_block_scale_exp")
         self.scale_exp, self.rel_err = e.value, rel.value
 
-    HEAVY_ARCS = 4096
+    HEAVY_ARCS = 2048  # rows above go to the chunked heavy path (<= the block reducer's limit)
     SMALL_ARCS = 32
 
     def _plan_heavy(self):
