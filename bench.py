@@ -7,7 +7,8 @@ on; it fits one B200): C4 = R-MAT(.57,.19,.19,.05) scale 27 (134M nodes),
 
 A step = one edge pass over the whole graph:
     K1 class histogram + inv + compact labels   (labels are an input)
-    K4 pull edge map (+ trailing-row zero fill + cross-tile finalize)
+    K4 pull edge pass: class gather (k_gather), 32-row block reduction
+       (k_reduce_blocks), heavy-row chunks + finalize (k_reduce_heavy)
 Graph preparation (symmetric CSR build, tile plan, weight statistics) is
 outside the timed region, as the reference's bench keeps build_csr out
 (reference bench.py:1-7).  Inputs (30 GB CSR) are far larger than the
@@ -17,7 +18,8 @@ outside the timed region, as the reference's bench keeps build_csr out
     e2e      same metric through the host-buffer path: pinned host CSR +
              labels -> H2D, weight stats + tile plan, the step, Z -> pinned
              host, all inside the timed region
-    roofline the pull kernel: algorithmic bytes / its CUDA-event time
+    roofline the dominant kernel of the step: its algorithmic bytes / its
+             CUDA-event time (every phase is listed under roofline.phases)
     cpu_baseline  the reference's parallel CPU edge map (oracle/ pthreads
              port of embed_parallel, CAS f64 atomics), all host threads, on a
              1/16 self-similar sample of C4 (R-MAT scale 23, same edge
@@ -76,14 +78,14 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic(workload):
-    """dram bytes per pull launch from the committed ncu capture, if any."""
+def load_traffic(workload, kernel):
+    """dram bytes per launch of `kernel` from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
             t = json.load(fh)
         if t.get("workload") == workload:
-            return float(t["dram_bytes_per_launch"])
+            return float(t["kernels"][kernel]["dram_bytes_per_launch"])
     except Exception:
         pass
     return None
@@ -323,18 +325,19 @@ def main():
         step(z)
     torch.cuda.synchronize()
 
-    ev_pull = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = []  # (phase, event) after each phase of every timed step
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
+        emb.launches = 0
+        emb.phase_events = marks
         start.record(stream)
         for i in range(args.steps):
-            emb.project(y, validate=False, g=g)
-            ev_pull[i][0].record(stream)
-            emb.pull(g, z)
-            ev_pull[i][1].record(stream)
+            step(z)
         end.record(stream)
+        emb.phase_events = None
+        launches = emb.launches
         torch.cuda.synchronize()
         # short timed regions get few nvidia-smi samples: keep the same load
         # running (untimed) for another second so the clock record covers it
@@ -346,19 +349,37 @@ def main():
     ms_total = start.elapsed_time(end)
     ms_total = max_over_ranks(ms_total, world)
     ms_step = ms_total / args.steps
-    ms_pull = float(np.mean([a.elapsed_time(b) for a, b in ev_pull]))
     clk = clocks.summary()
 
-    # launches of OUR kernels per step: k_label_hist, k_inv, k_zero_tail, k_pull, k_pull_finalize
-    launches_per_step = 5
+    # per-phase device time (CUDA events on the launching stream, between
+    # consecutive phase boundaries; the first phase of a step is measured
+    # from the previous step's last boundary / the start event)
+    phase_ms = {}
+    prev = start
+    for name, ev in marks:
+        phase_ms.setdefault(name, []).append(prev.elapsed_time(ev))
+        prev = ev
+    phase_ms = {kx: float(np.mean(v)) for kx, v in phase_ms.items()}
 
-    # roofline of the pull kernel (algorithmic bytes: its edges once as COO-
-    # equivalent listed edges, compact labels once, Z once)
-    peak_gbs, peak_kind = load_peaks()
+    # algorithmic bytes per launch of each phase (SURVEY.md section 8(d)
+    # per-unit figures x the units one launch processes)
     weighted = g.weighted
-    s_local = g.arcs // 2 if world > 1 else s
-    pull_bytes = s_local * (8 + 4 * weighted) + n * 1 + rows * k * 4
-    achieved = pull_bytes / (ms_pull * 1e-3) / 1e9
+    arcs = g.arcs
+    heavy_arcs = g.heavy_arc_total
+    light_arcs = arcs - heavy_arcs
+    heavy_rows = g.n_heavy
+    lb = 1 if k <= 255 else (2 if k <= 65535 else 4)
+    phase_bytes = {
+        "project": 4 * rows + lb * rows + (4 * rows + lb * g.n_hot if g.n_hot else 0),
+        "gather": arcs * (4 + 1),
+        "blocks": 8 * (rows + 1) + light_arcs * (1 + 4 * weighted) + 4 * k * (rows - heavy_rows),
+        "heavy": heavy_arcs * (1 + 4 * weighted) + 4 * k * heavy_rows,
+    }
+    peak_gbs, peak_kind = load_peaks()
+    dominant = max((p for p in phase_ms if p in phase_bytes), key=lambda p: phase_ms[p])
+    kernel_of = {"project": "k_label_hist", "gather": "k_gather", "blocks": "k_reduce_blocks",
+                 "heavy": "k_reduce_heavy"}
+    achieved = phase_bytes[dominant] / (phase_ms[dominant] * 1e-3) / 1e9
     step_bmin = s * (8 + 4 * weighted) + 4 * n + 4 * n * k  # SURVEY 8(d) B_min, whole graph
     workload = cfg.name if not (args.scale or args.edges) else f"{cfg.name}-reduced(scale={args.scale},s={s})"
 
@@ -373,21 +394,25 @@ def main():
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32 (exact int64 fixed-point accumulation)" if weighted else "f32 (exact u32 counts)",
+        "dtype": "f32 (exact integer fixed-point accumulation)" if weighted else "f32 (exact u32 counts)",
         "data": "synthetic (seeded R-MAT; Friendster unavailable)",
         "config": {"workload": workload, "n": n, "s_listed_edges": s, "k": k, "weighted": bool(weighted),
-                   "directed": bool(directed), "variant": "pull", "sym_arcs": g.arcs,
+                   "directed": bool(directed), "variant": "pull", "reducer": emb.reducer, "sym_arcs": arcs,
                    "parallelism": f"row-range x{world}" if world > 1 else "single GPU",
                    "l2": "inputs (CSR %.1f GB) >> 126 MB L2; no flush needed" % (g.csr_bytes() / 1e9),
                    "gen_s": round(t_gen, 3), "prep_s": round(t_prep, 3), "hot_prep_s": round(t_hot, 3),
-                   "hot_vertices": g.n_hot},
+                   "hot_vertices": g.n_hot, "heavy_rows": heavy_rows},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-                     "frac": achieved / peak_gbs, "traffic": load_traffic(workload), "kernel": "k_pull",
-                     "peak_kind": peak_kind, "algorithmic_bytes_per_launch": pull_bytes,
-                     "pull_ms": ms_pull, "step_bmin_bytes": step_bmin,
-                     "step_frac": step_bmin / (ms_step * 1e-3) / 1e9 / (peak_gbs * world)},
+                     "frac": achieved / peak_gbs, "traffic": load_traffic(workload, kernel_of[dominant]),
+                     "kernel": kernel_of[dominant], "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": phase_bytes[dominant],
+                     "kernel_ms": phase_ms[dominant], "step_bmin_bytes": step_bmin,
+                     "step_frac": step_bmin / (ms_step * 1e-3) / 1e9 / (peak_gbs * world),
+                     "phases": {p: {"ms": phase_ms[p], "bytes": phase_bytes.get(p),
+                                    "gbs": (phase_bytes[p] / (phase_ms[p] * 1e-3) / 1e9) if p in phase_bytes else None}
+                                for p in phase_ms}},
         "clocks": clk,
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches,
     }
 
     # ---- variant measurement: push on the same graph (chosen by measurement)
@@ -460,7 +485,7 @@ def run_e2e(g, y, emb, z, s, args):
             g.hot_rank.copy_(h_hot, non_blocking=True)
         g2 = DeviceGraph(g.n, g.s, dev)
         g2.offsets, g2.targets, g2.weights = d_off, d_tgt, d_w
-        g2._plan()  # tile/chunk plan, cut list, weight statistics (host sync)
+        g2._plan()  # weight statistics, exponent, heavy-row chunk list (host sync)
         g2.hot_rank, g2.n_hot, g2.hot_k = g.hot_rank, g.n_hot, g.hot_k  # targets arrive hot-encoded
         emb.project(d_y, validate=False, g=g2)
         emb.pull(g2, z)
@@ -478,7 +503,8 @@ def run_e2e(g, y, emb, z, s, args):
     return {"value": s / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "steps": args.e2e_steps,
             "path": "host pinned prepared graph (CSR with hot-encoded targets, hot ranks) + labels -> "
-                    "gee_graph_stats/gee_pull_plan/gee_build_projection_hot/gee_embed_csr_pull_hot -> host pinned Z"}
+                    "gee_graph_stats/gee_reduce_heavy_plan/gee_build_projection/gee_gather_labels/"
+                    "gee_reduce_blocks/gee_reduce_heavy -> host pinned Z"}
 
 
 if __name__ == "__main__":

@@ -239,6 +239,15 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
                       const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
                       void *stream);
 
+/* Heavy rows alone (rows longer than heavy_arcs, chunk list from
+ * graph preparation): int64 chunk partials, then the finalize that writes
+ * their Z rows.  gee_reduce_blocks with n_heavy = 0 followed by this call
+ * equals gee_reduce_blocks with the heavy arguments. */
+int gee_reduce_heavy(const int64_t *offsets, const uint8_t *cls, const float *w, int32_t scale_exp,
+                     const double *inv, int32_t k, int64_t heavy_arcs, const int32_t *heavy_rows,
+                     int64_t n_heavy, const int64_t *chunk_first, const int32_t *chunk_heavy,
+                     int64_t n_chunks, void *heavy_acc, float *z, void *stream);
+
 /* Fixed-point exponent valid for every pull reducer, gee_reduce_blocks
  * included: the largest e with max_row_abs * 2^e < 2^62 and
  * max_abs * 2^e < 2^42.  *rel_err = 2^-(e+1)/min_abs_nz (host). */

@@ -922,6 +922,40 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
     return gee::check_launch("k_heavy_finalize");
 }
 
+int gee_reduce_heavy(const int64_t *offsets, const uint8_t *cls, const float *w, int32_t scale_exp,
+                     const double *inv, int32_t k, int64_t heavy_arcs, const int32_t *heavy_rows, int64_t n_heavy,
+                     const int64_t *chunk_first, const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc,
+                     float *z, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs 1 <= k <= 255 (got %d)", k);
+    GEE_REQUIRE(n_heavy >= 0 && n_chunks >= 0 && heavy_arcs >= 1, GEE_ERR_INVALID, "bad sizes");
+    if (n_heavy == 0) return GEE_OK;
+    GEE_REQUIRE(offsets && cls && inv && z && heavy_rows && chunk_first && chunk_heavy && heavy_acc, GEE_ERR_INVALID,
+                "NULL array argument");
+    cudaStream_t st = gee::as_stream(stream);
+    const bool weighted = w != nullptr;
+    const float qscale = ldexpf(1.0f, scale_exp);
+    const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
+    const size_t shh = (size_t)RW * (((size_t)k + 3) & ~(size_t)3) * (weighted ? 2 : 1) * sizeof(uint32_t);
+    auto *acc = static_cast<unsigned long long *>(heavy_acc);
+    const int hgrid = grid_for(n_chunks * 32, RT, 8);
+    if (weighted)
+        k_reduce_heavy<true><<<hgrid, RT, shh, st>>>(offsets, heavy_rows, chunk_first, chunk_heavy, n_chunks, heavy_arcs,
+                                                     cls, w, qscale, k, acc);
+    else
+        k_reduce_heavy<false><<<hgrid, RT, shh, st>>>(offsets, heavy_rows, chunk_first, chunk_heavy, n_chunks,
+                                                      heavy_arcs, cls, w, qscale, k, acc);
+    int rc;
+    if ((rc = gee::check_launch("k_reduce_heavy"))) return rc;
+    const int fgrid = grid_for(n_heavy * k, 256, 4);
+    if (weighted)
+        k_heavy_finalize<true><<<fgrid, 256, 0, st>>>(heavy_rows, n_heavy, k, acc, inv, dscale, z);
+    else
+        k_heavy_finalize<false><<<fgrid, 256, 0, st>>>(heavy_rows, n_heavy, k, acc, inv, dscale, z);
+    return gee::check_launch("k_heavy_finalize");
+}
+
 int gee_block_scale_exp(double max_row_abs, double max_abs, double min_abs_nz, int32_t *scale_exp, double *rel_err)
 {
     gee::clear_error();

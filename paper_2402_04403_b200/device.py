@@ -71,6 +71,7 @@ class DeviceGraph:
         self.src = self.dst = self.w = None
         self.coo_source_only = False
         self.hot_rank = None  # int32[n_nodes]: degree rank of hot vertices, -1 cold
+        self.global_offsets = None  # row shard: global symmetric offsets until the hot plan
         self.n_hot = 0
         self.hot_k = None  # k the hot tier was planned for (None = not planned)
         self._owns_targets = False
@@ -137,20 +138,13 @@ class DeviceGraph:
         self._plan()
 
     def _plan(self):
+        """Pull planning (graph preparation): weight statistics + fixed-point
+        exponent, heavy-row chunk list, block arc spans.  The tile plan and
+        degree bins of the alternative reducers are built on first use."""
         arcs = self.arcs
-        n_tiles = int(lib.gee_pull_tiles(arcs))
-        self.tile_row = torch.empty(n_tiles + 1, dtype=torch.int64, device=self.device)
-        self.chunk_row = torch.empty(max(int(lib.gee_pull_chunks(arcs)), 1), dtype=torch.int16, device=self.device)
-        self.cut_tiles = torch.empty(max(n_tiles, 1), dtype=torch.int32, device=self.device)
-        nc = ctypes.c_int64()
-        check(lib.gee_pull_plan(ptr(self.offsets), self.n, arcs, ptr(self.tile_row), ptr(self.chunk_row),
-                                ptr(self.cut_tiles), ctypes.byref(nc), _stream()), "gee_pull_plan")
-        self.n_cut = int(nc.value)
+        self.tile_row = self.chunk_row = self.cut_tiles = None
+        self.small_rows = self.medium_rows = None
         self._plan_heavy()
-        # arc span of the widest 32-row block (gee_reduce_blocks keeps
-        # block-local offsets in int32)
-        ends = self.offsets[torch.arange(0, self.n + 32, 32, device=self.device).clamp_(max=self.n)]
-        self.max_block_arcs = int((ends[1:] - ends[:-1]).max().item()) if self.n else 0
         mx, mn, mxa = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         nf = ctypes.c_int32()
         check(lib.gee_graph_stats(ptr(self.offsets), ptr(self.weights), self.n, arcs, ctypes.byref(mx),
@@ -163,12 +157,29 @@ class DeviceGraph:
         check(lib.gee_block_scale_exp(mx.value, mxa.value, mn.value, ctypes.byref(e), ctypes.byref(rel)),
               "gee_block_scale_exp")
         self.scale_exp, self.rel_err = e.value, rel.value
+        # arc span of the widest 32-row block (gee_reduce_blocks keeps
+        # block-local offsets in int32)
+        ends = self.offsets[torch.arange(0, self.n + 32, 32, device=self.device).clamp_(max=self.n)]
+        self.max_block_arcs = int((ends[1:] - ends[:-1]).max().item()) if self.n else 0
 
-    HEAVY_ARCS = 2048  # rows above go to the chunked heavy path (<= the block reducer's limit)
-    SMALL_ARCS = 32
+    def ensure_tile_plan(self):
+        """Tile / chunk / cut plan of the tile reducers (gee_pull_plan)."""
+        if self.tile_row is not None:
+            return
+        arcs = self.arcs
+        n_tiles = int(lib.gee_pull_tiles(arcs))
+        self.tile_row = torch.empty(n_tiles + 1, dtype=torch.int64, device=self.device)
+        self.chunk_row = torch.empty(max(int(lib.gee_pull_chunks(arcs)), 1), dtype=torch.int16, device=self.device)
+        self.cut_tiles = torch.empty(max(n_tiles, 1), dtype=torch.int32, device=self.device)
+        nc = ctypes.c_int64()
+        check(lib.gee_pull_plan(ptr(self.offsets), self.n, arcs, ptr(self.tile_row), ptr(self.chunk_row),
+                                ptr(self.cut_tiles), ctypes.byref(nc), _stream()), "gee_pull_plan")
+        self.n_cut = int(nc.value)
 
-    def _plan_heavy(self):
-        """Degree bins + heavy-row chunk list for the row reducers (graph preparation)."""
+    def ensure_bins(self):
+        """Degree bins of the list reducer (gee_reduce_bins)."""
+        if self.small_rows is not None:
+            return
         n = self.n
         self.small_rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         self.medium_rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
@@ -177,11 +188,19 @@ class DeviceGraph:
                                   ptr(self.medium_rows), ctypes.byref(ns), ctypes.byref(nm), _stream()),
               "gee_reduce_bins")
         self.n_small, self.n_medium = int(ns.value), int(nm.value)
+
+    HEAVY_ARCS = 2048  # rows above go to the chunked heavy path (<= the block reducer's limit)
+    SMALL_ARCS = 32
+
+    def _plan_heavy(self):
+        """Heavy-row chunk list for the row reducers (graph preparation)."""
+        n = self.n
         rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         nh = ctypes.c_int64()
         check(lib.gee_reduce_heavy_plan(ptr(self.offsets), n, self.HEAVY_ARCS, ptr(rows), ctypes.byref(nh),
                                         _stream()), "gee_reduce_heavy_plan")
         self.n_heavy = int(nh.value)
+        self.heavy_arc_total = 0
         if self.n_heavy == 0:
             self.heavy_rows = self.chunk_first = self.chunk_heavy = None
             self.n_chunks = 0
@@ -194,6 +213,7 @@ class DeviceGraph:
         heavy_idx = torch.repeat_interleave(torch.arange(self.n_heavy), per)
         start = torch.repeat_interleave(first, per)
         within = torch.arange(int(per.sum())) - torch.repeat_interleave(torch.cumsum(per, 0) - per, per)
+        self.heavy_arc_total = int(deg.sum())
         self.heavy_rows = rows
         self.chunk_first = (start + within * self.HEAVY_ARCS).to(self.device)
         self.chunk_heavy = heavy_idx.to(torch.int32).to(self.device)
@@ -212,10 +232,13 @@ class DeviceGraph:
         if self.hot_k is not None:
             raise ValidationError("hot tier already planned for a different k")
         table_bytes = int(lib.gee_label_table_bytes(self.n_nodes, 0, k))
+        # a row shard ranks the GLOBAL vertices by their global degree
+        deg_off = self.offsets if self.n == self.n_nodes else self.global_offsets
         if enable is None:
-            enable = table_bytes > self.HOT_MIN_TABLE_BYTES and k <= 65535 and self.n == self.n_nodes
+            enable = table_bytes > self.HOT_MIN_TABLE_BYTES and k <= 65535 and deg_off is not None
         self.hot_k = k
-        if not enable or self.arcs == 0:
+        if not enable or self.arcs == 0 or deg_off is None:
+            self.global_offsets = None
             return
         if not self._owns_targets:
             self.targets = self.targets.clone()
@@ -224,8 +247,9 @@ class DeviceGraph:
         self.hot_rank = torch.empty(n, dtype=torch.int32, device=self.device)
         nh = ctypes.c_int64()
         max_hot = min(n, self.HOT_MAX // int(lib.gee_label_bytes(k)))
-        check(lib.gee_hot_plan(ptr(self.offsets), n, max_hot, 2, ptr(self.hot_rank), None, ctypes.byref(nh),
+        check(lib.gee_hot_plan(ptr(deg_off), n, max_hot, 2, ptr(self.hot_rank), None, ctypes.byref(nh),
                                _stream()), "gee_hot_plan")
+        self.global_offsets = None
         self.n_hot = int(nh.value)
         if self.n_hot == 0:
             self.hot_rank = None
@@ -284,6 +308,8 @@ class Embedder:
         self.heavy_acc = None  # heavy-row partial sums (row reducer)
         self.split = os.environ.get("GEE_PULL_FUSED") is None
         self.reducer = os.environ.get("GEE_PULL_REDUCER", "blocks")  # blocks | lists | rows | tiles
+        self.phase_events = None  # list -> (phase, cuda event) after each phase (bench)
+        self.launches = 0  # our kernels launched so far (bench accounting)
 
     def _ensure_table(self, n_hot):
         need = int(lib.gee_label_table_bytes(self.n, n_hot, self.k))
@@ -302,6 +328,7 @@ class Embedder:
         check(lib.gee_build_projection(ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.inv32),
                                        ptr(self.inv64), ptr(self.table), ptr(hot_rank), n_hot, ptr(self.bad),
                                        _stream()), "gee_build_projection")
+        self._mark("project", 2)
         self.table_n_hot = n_hot
         if validate and int(self.bad.item()):
             raise ValidationError(f"{int(self.bad.item())} labels outside [0, {self.k}]")
@@ -331,7 +358,6 @@ class Embedder:
             raise ValidationError("label table does not match the graph's hot tier: call project(labels, g=graph)")
         if z is None:
             z = torch.empty((g.n, self.k), dtype=torch.float32, device=self.device)
-        self._ensure_slots(g.arcs)
         if self.split and self.k <= 255:
             # split pass: class stream (random gathers, full occupancy), then
             # the gather-free segmented reduction
@@ -339,6 +365,7 @@ class Embedder:
                 self.cls = torch.empty(g.arcs + 64, dtype=torch.uint8, device=self.device)
             check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
                                         _stream()), "gee_gather_labels")
+            self._mark("gather", 1)
             reducer = self.reducer
             if reducer == "blocks" and (g.max_block_arcs >= 2**31 or z.data_ptr() % 16):
                 reducer = "lists"
@@ -349,25 +376,48 @@ class Embedder:
                          g.n_chunks, ptr(self.heavy_acc) if g.n_heavy else None, ptr(z), _stream())
                 if reducer == "blocks":
                     check(lib.gee_reduce_blocks(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                                ptr(self.inv64), self.k, *heavy), "gee_reduce_blocks")
+                                                ptr(self.inv64), self.k, g.HEAVY_ARCS, None, 0, None, None, 0, None,
+                                                ptr(z), _stream()), "gee_reduce_blocks")
+                    self._mark("blocks", 1)
+                    check(lib.gee_reduce_heavy(ptr(g.offsets), ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                               ptr(self.inv64), self.k, *heavy), "gee_reduce_heavy")
+                    self._mark("heavy", 2 if g.n_heavy else 0)
                 elif reducer == "lists":
+                    g.ensure_bins()
                     check(lib.gee_reduce_lists(ptr(g.offsets), ptr(g.small_rows), g.n_small, ptr(g.medium_rows),
                                                g.n_medium, ptr(self.cls), ptr(g.weights), g.scale_exp,
                                                ptr(self.inv64), self.k, *heavy), "gee_reduce_lists")
+                    self._mark("lists", 2 + (2 if g.n_heavy else 0))
                 else:
                     check(lib.gee_reduce_rows(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
                                               ptr(self.inv64), self.k, *heavy), "gee_reduce_rows")
+                    self._mark("rows", 1 + (2 if g.n_heavy else 0))
                 return z
+            g.ensure_tile_plan()
+            self._ensure_slots(g.arcs)
             check(lib.gee_embed_csr_pull_cls(ptr(g.offsets), ptr(self.cls), ptr(g.weights), g.n, g.arcs,
                                              ptr(g.tile_row), ptr(g.chunk_row), ptr(g.cut_tiles), g.n_cut,
                                              g.scale_exp, ptr(self.inv64), self.k, ptr(z), ptr(self.slots),
                                              _stream()), "gee_embed_csr_pull_cls")
+            self._mark("tiles", 3)
             return z
+        g.ensure_tile_plan()
+        self._ensure_slots(g.arcs)
         check(lib.gee_embed_csr_pull(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
                                      ptr(g.tile_row), ptr(g.chunk_row), ptr(g.cut_tiles), g.n_cut, g.scale_exp,
                                      ptr(self.table), g.n_hot, ptr(self.inv64), self.k, ptr(z), ptr(self.slots),
                                      _stream()), "gee_embed_csr_pull")
+        self._mark("fused", 3)
         return z
+
+    def _mark(self, phase, launches):
+        """Phase bookkeeping for measurement: kernels launched, and a CUDA
+        event on the current stream when `phase_events` is a list."""
+        self.launches += launches
+        if self.phase_events is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(torch.cuda.current_stream(self.device))
+            self.phase_events.append((phase, ev))
 
     # ------------------------------------------------------------------ K3
     def push(self, g: DeviceGraph, z=None, precombine=False, zero=True):

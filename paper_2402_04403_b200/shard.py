@@ -75,9 +75,9 @@ def build_row_shard(src, dst, w, n, world, rank, k=None):
     g.weights = torch.empty(arcs, dtype=torch.float32, device=dev) if w is not None else None
     check(lib.gee_build_sym_csr_rows(ptr(src), ptr(dst), ptr(w), s, n, lo, hi, ptr(full), ptr(g.offsets),
                                      ptr(g.targets), ptr(g.weights), _lib.stream_handle()), "gee_build_sym_csr_rows")
-    del full
     g._plan()
     g.n_nodes = n
+    g.global_offsets = full  # global degrees for the hot-label plan (freed by prepare_hot)
     return g, lo, hi
 
 

@@ -321,3 +321,80 @@ def test_pull_reducers_agree_bitwise(k, weighted):
         assert rel_err(out[red], exp) <= TOL, red
     for red in ("lists", "rows"):
         assert np.array_equal(out["blocks"].view(np.uint32), out[red].view(np.uint32)), red
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_shards_tile_the_full_pull(world):
+    # row-range sharding (shard.build_row_shard): each rank's pull over its
+    # rows, with the hot tier planned on GLOBAL degrees, run one after the
+    # other on this GPU (ranks never wait on each other); the slices tile Z
+    from paper_2402_04403_b200 import shard
+
+    scale, s, k = 16, 600_000, 50
+    src, dst, w = synth.rmat_edges(scale, s, seed=21, weighted=True)
+    n = 1 << scale
+    y = synth.uniform_labels(n, k, seed=22)
+    exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), w.cpu().numpy(), y.cpu().numpy(), n, k)
+    dev = torch.device("cuda")
+    parts, bounds = [], []
+    for rank in range(world):
+        g, lo, hi = shard.build_row_shard(src, dst, w, n, world, rank, k=k)
+        g.prepare_hot(k, enable=True)
+        assert g.n_hot > 0 and g.global_offsets is None
+        emb = Embedder(n, k, dev)
+        z = torch.empty((hi - lo, k), dtype=torch.float32, device=dev)
+        emb.project(y, g=g)
+        parts.append(emb.pull(g, z).cpu().numpy())
+        bounds.append((lo, hi))
+    assert bounds[0][0] == 0 and bounds[-1][1] == n
+    assert all(bounds[i][1] == bounds[i + 1][0] for i in range(world - 1))
+    assert rel_err(np.concatenate(parts), exp) <= TOL
+
+
+def test_raw_ctypes_binding_without_torch():
+    # the C ABI bound with plain ctypes and
+    # cuda-python device memory (no torch on the path) reproduces the oracle
+    import ctypes
+
+    from cuda.bindings import runtime as rt
+
+    from paper_2402_04403_b200 import _lib
+
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    L.gee_last_error.restype = ctypes.c_char_p
+    L.gee_build_projection.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, i64, vp, vp]
+    L.gee_embed_coo.argtypes = [vp, vp, vp, i64, vp, i64, vp, i64, i32, vp, ctypes.c_uint32, vp]
+    L.gee_label_table_bytes.restype = ctypes.c_size_t
+
+    def check(rc):
+        assert rc == 0, L.gee_last_error().decode()
+
+    def dev(a):
+        err, p = rt.cudaMalloc(max(a.nbytes, 1))
+        assert err == rt.cudaError_t.cudaSuccess
+        rt.cudaMemcpy(p, a.ctypes.data, a.nbytes, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+        return p
+
+    rng = np.random.default_rng(31)
+    n, k, s = 5000, 9, 60_000
+    src, dst = rng.integers(0, n, s), rng.integers(0, n, s)
+    w = (1.0 - rng.random(s)).astype(np.float32)
+    y = gb.random_labels(n, k, 0.6, seed=32).labels
+    d_src, d_dst, d_w, d_y = dev(src.astype(np.int32)), dev(dst.astype(np.int32)), dev(w), dev(y.astype(np.int32))
+    d_counts = rt.cudaMalloc(8 * (k + 1))[1]
+    d_inv = rt.cudaMalloc(4 * (k + 1))[1]
+    d_tab = rt.cudaMalloc(L.gee_label_table_bytes(n, 0, k))[1]
+    d_z = rt.cudaMalloc(4 * n * k)[1]
+    try:
+        check(L.gee_build_projection(d_y, n, k, d_counts, d_inv, None, d_tab, None, 0, None, None))
+        check(L.gee_embed_coo(d_src, d_dst, d_w, s, d_tab, 0, d_inv, n, k, d_z, 1, None))
+        z = np.empty((n, k), np.float32)
+        rt.cudaMemcpy(z.ctypes.data, d_z, z.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+        counts = np.empty(k + 1, np.int64)
+        rt.cudaMemcpy(counts.ctypes.data, d_counts, counts.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+    finally:
+        for p in (d_src, d_dst, d_w, d_y, d_counts, d_inv, d_tab, d_z):
+            rt.cudaFree(p)
+    assert np.array_equal(counts, np.bincount(y, minlength=k + 1))
+    assert rel_err(z, oracle.serial_embed(src, dst, w, y, n, k)) <= TOL

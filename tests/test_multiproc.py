@@ -1,0 +1,117 @@
+"""Multi-process sharding logic on CPU (gloo, world_size 2).
+
+The device path of a shard is the single-GPU pull on a row range
+(shard.build_row_shard); what multi-GPU adds is the partitioning and, for
+edge-range sharding, the reduce-scatter.  Both are exercised here with the
+oracle standing in for each rank's device pass:
+
+* row-range: every rank plans the same bounds from the same offsets, takes
+  its rows of the symmetric CSR and computes their Z rows with the
+  SOURCE_ONLY rule; the gathered slices equal the full oracle Z.
+* edge-range: every rank embeds its contiguous slice of the listed edges
+  into a full partial Z; shard.reduce_scatter_rows leaves each rank its row
+  slice of the sum.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2402_04403_b200 import shard
+
+WORLD = 2
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _graph(seed, n=3000, s=20000, k=7):
+    rng = np.random.default_rng(seed)
+    # skewed sources so that an arc-balanced split differs from an even one
+    src = (rng.pareto(1.5, s) * 50).astype(np.int64) % n
+    dst = rng.integers(0, n, s)
+    w = (1.0 - rng.random(s)).astype(np.float32).astype(np.float64)
+    y = rng.integers(0, k + 1, n).astype(np.int64)
+    return src, dst, w, y, n, k
+
+
+def _worker(rank, port, seed, mode, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        src, dst, w, y, n, k = _graph(seed)
+        _, _, row = oracle.projection(y, k)
+        full = oracle.serial_embed(src, dst, w, y, n, k)
+        if mode == "rows":
+            off, tgt, wts = oracle.build_csr(src, dst, w, n, directed=False)  # symmetric CSR
+            bounds = shard.plan_rows(off, WORLD, k, weighted=True)
+            got = [torch.zeros(WORLD + 1, dtype=torch.int64) for _ in range(WORLD)]
+            dist.all_gather(got, torch.from_numpy(bounds))
+            assert all(torch.equal(g, got[0]) for g in got), "ranks disagree on the plan"
+            lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+            loc_off = off[lo:hi + 1] - off[lo]
+            a, b = int(off[lo]), int(off[hi])
+            z = oracle.parallel_embed(loc_off, tgt[a:b], wts[a:b], y, k, False, 1,
+                                      row_value=row, label32=y.astype(np.int32))
+            np.testing.assert_allclose(z, full[lo:hi], rtol=1e-12, atol=1e-15)
+            # the slices tile [0, n) exactly
+            sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(WORLD)]
+            dist.all_gather(sizes, torch.tensor([hi - lo]))
+            assert sum(int(x) for x in sizes) == n
+            q.put((rank, "ok", hi - lo))
+        else:
+            e = shard.plan_edges(src.size, WORLD)
+            a, b = int(e[rank]), int(e[rank + 1])
+            part = oracle.serial_embed(src[a:b], dst[a:b], w[a:b], y, n, k)
+            mine = shard.reduce_scatter_rows(torch.from_numpy(part), WORLD)
+            per = -(-n // WORLD)
+            lo, hi = rank * per, min(n, (rank + 1) * per)
+            np.testing.assert_allclose(mine[:hi - lo].numpy(), full[lo:hi], rtol=1e-12, atol=1e-15)
+            assert not mine[hi - lo:].any()  # padding rows stay zero
+            q.put((rank, "ok", hi - lo))
+    except Exception as ex:  # pragma: no cover - reported to the parent
+        q.put((rank, f"fail: {type(ex).__name__}: {ex}", 0))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["rows", "edges"])
+def test_sharding_world2_gloo(mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, 11, mode, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = sorted(q.get(timeout=10) for _ in range(WORLD))
+    assert all(p.exitcode == 0 for p in procs), res
+    assert all(r[1] == "ok" for r in res), res
+    if mode == "rows":
+        # arc-balanced: the skewed head gets fewer rows than an even split
+        assert res[0][2] != res[1][2]
+
+
+def test_plan_rows_balances_cost():
+    src, dst, w, y, n, k = _graph(3, n=20000, s=200000, k=50)
+    off, _, _ = oracle.build_csr(src, dst, w, n, directed=False)
+    for world in (1, 2, 4, 8):
+        b = shard.plan_rows(off, world, k, weighted=True)
+        assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
+        cost = off[b] * 8 + b * 4 * k
+        per = np.diff(cost)
+        # within one row's worth of cost of the ideal share
+        row_max = int(np.max(np.diff(off))) * 8 + 4 * k
+        assert per.max() - per.min() <= 2 * row_max
+    assert list(shard.plan_edges(10, 4)) == [0, 2, 5, 7, 10]

@@ -19,7 +19,7 @@ for enable in (False, True):
         rows = np.unique(bad[:, 0])
         print(" bad rows", rows[:20], len(rows))
         off = g.offsets.cpu().numpy()
-        tr = g.tile_row.cpu().numpy()
+        tr = (g.ensure_tile_plan() or g.tile_row).cpu().numpy()
         for r in rows[:5]:
             print("  row", r, "deg", off[r+1]-off[r], "start", off[r], "tile", off[r] // 4096, "z", z[r], "exp", exp[r])
         print(" tile_row around:", [(j, tr[j]) for j in range(len(tr)) if tr[j] in rows[:5] or (j+1 < len(tr) and tr[j] <= rows[0] < tr[j+1])][:5])

@@ -13,7 +13,9 @@ h = r[1]
 ai, ii = h.index('Source'), h.index('Instructions Executed')
 b, cnt, ops = collections.Counter(), collections.Counter(), collections.defaultdict(collections.Counter)
 for x in r[2:]:
-    n = int(x[ii] or 0)
+    if len(x) != len(h) or not x[ii].replace(',', '').isdigit():
+        continue
+    n = int(x[ii].replace(',', '') or 0)
     if n == 0:
         continue
     key = float(f'{n:.2g}')

@@ -31,7 +31,9 @@ def main(rep, kregex=None, top=20):
     op = collections.Counter()
     rows = []
     for x in r[2:]:
-        n = int(x[ii] or 0)
+        if len(x) != len(h) or not x[ii].replace(',', '').isdigit():
+            continue
+        n = int(x[ii].replace(',', '') or 0)
         tot += n
         t = x[ai].split()
         o = (t[1] if t and t[0].startswith('@') and len(t) > 1 else (t[0] if t else '')).split('.')[0]

@@ -6,7 +6,7 @@ scale = int(sys.argv[1]) if len(sys.argv) > 1 else 27
 src, dst, w, y, n, k, directed = synth.make_config(4, scale_override=scale if scale != 27 else None)
 g = DeviceGraph.from_edges(src, dst, w, n, pull=True)
 del src, dst, w
-tr = g.tile_row.cpu().numpy().astype(np.int64)
+tr = (g.ensure_tile_plan() or g.tile_row).cpu().numpy().astype(np.int64)
 off = g.offsets
 rows = np.diff(tr)
 deg = (off[1:] - off[:-1])
