@@ -239,14 +239,19 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
                       const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
                       void *stream);
 
-/* Heavy rows alone (rows longer than heavy_arcs, chunk list from
- * graph preparation): int64 chunk partials, then the finalize that writes
- * their Z rows.  gee_reduce_blocks with n_heavy = 0 followed by this call
- * equals gee_reduce_blocks with the heavy arguments. */
-int gee_reduce_heavy(const int64_t *offsets, const uint8_t *cls, const float *w, int32_t scale_exp,
-                     const double *inv, int32_t k, int64_t heavy_arcs, const int32_t *heavy_rows,
-                     int64_t n_heavy, const int64_t *chunk_first, const int32_t *chunk_heavy,
-                     int64_t n_chunks, void *heavy_acc, float *z, void *stream);
+/* Heavy rows (longer than the block reducer's heavy_arcs) as work items:
+ * item i covers arcs [item_first[i], item_end[i]) of row item_row[i]
+ * (at most 65536 arcs).  item_slot[i] < 0: the item is its row's only one and
+ * writes the Z row; otherwise it adds into mega_acc[item_slot[i]] (int64
+ * [n_mega x k], zero on entry, left zero on exit) and a finalize writes the
+ * Z rows of mega_rows.  Items are fetched dynamically through *counter
+ * (device int64 scratch), so list them largest first.  Weighted graphs need
+ * gee_block_scale_exp's exponent.  Graph preparation builds the items (device.py
+ * DeviceGraph._plan_heavy). */
+int gee_reduce_heavy(const uint8_t *cls, const float *w, int32_t scale_exp, const double *inv, int32_t k,
+                     const int64_t *item_first, const int64_t *item_end, const int32_t *item_row,
+                     const int32_t *item_slot, int64_t n_items, const int32_t *mega_rows, int64_t n_mega,
+                     void *mega_acc, int64_t *counter, float *z, void *stream);
 
 /* Fixed-point exponent valid for every pull reducer, gee_reduce_blocks
  * included: the largest e with max_row_abs * 2^e < 2^62 and

@@ -1,9 +1,11 @@
 // Label-gather stream: cls[e] = table[targets[e]] for every arc (the random
 // half of the pull pass, isolated).  One persistent 1024-thread CTA per SM;
-// each thread streams 16 targets (4 x 128-bit), issues 16 independent
-// gathers through L1/L2 (evict-last) and writes 16 class bytes (one 128-bit
-// store).  Nothing synchronises, so the gathers' latency is hidden by
-// occupancy and per-thread memory-level parallelism.
+// each thread streams 16 targets (2 x 256-bit loads that bypass L1), issues
+// 16 independent predicated gathers through L1/L2 (L2 evict-last) and writes
+// 16 class bytes (one 128-bit store).  Nothing synchronises, so the gathers'
+// latency is hidden by occupancy and per-thread memory-level parallelism.
+// Bound: L2->SM sector bandwidth (each L1-missing 1-byte lookup moves a
+// 32-byte sector; C4 moves ~3.7e9 sectors).
 #include <cstdlib>
 
 #include "gee_common.cuh"
@@ -13,15 +15,54 @@ namespace {
 constexpr int GTHREADS = 1024;
 constexpr int GAPT = 16;
 
-template <typename LT>
+// Label load of a cold-or-L2 slot, issued only when `on` (predicated, so
+// the 16 lookups of a thread stay independent and in flight together).
+// L1MODE 0: default L1 policy; 1: L1::evict_last (keep the hot prefix).
+template <int L1MODE>
+__device__ __forceinline__ uint32_t ld_label_pred(const uint8_t *p, bool on, uint64_t pol)
+{
+    uint32_t v = 0;
+    if (L1MODE == 1)
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                     "@q ld.global.nc.L1::evict_last.L2::cache_hint.u8 %0, [%1], %3;\n\t}"
+                     : "+r"(v) : "l"(p), "r"((uint32_t)on), "l"(pol));
+    else
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                     "@q ld.global.nc.L2::cache_hint.u8 %0, [%1], %3;\n\t}"
+                     : "+r"(v) : "l"(p), "r"((uint32_t)on), "l"(pol));
+    return v;
+}
+
+// Target stream: TMODE 0 = ld.global.cs, 4 x 128-bit; 1 = 2 x 256-bit
+// ld.global.nc.L1::no_allocate.L2::evict_first (sm_100 .v8.b32 loads).
+template <int TMODE>
+__device__ __forceinline__ void ld_targets16(const int32_t *p, int32_t (&t)[16])
+{
+    if (TMODE == 0) {
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const int4 t4 = __ldcs(reinterpret_cast<const int4 *>(p) + v);
+            t[4 * v] = t4.x, t[4 * v + 1] = t4.y, t[4 * v + 2] = t4.z, t[4 * v + 3] = t4.w;
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < 2; v++)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=r"(t[8 * v]), "=r"(t[8 * v + 1]), "=r"(t[8 * v + 2]), "=r"(t[8 * v + 3]),
+                           "=r"(t[8 * v + 4]), "=r"(t[8 * v + 5]), "=r"(t[8 * v + 6]), "=r"(t[8 * v + 7])
+                         : "l"(p + 8 * v));
+    }
+}
+
+template <int L1MODE, int TMODE>
 __global__ void __launch_bounds__(GTHREADS, 1)
-k_gather(const int32_t *__restrict__ targets, int64_t arcs, const LT *__restrict__ table, int32_t hot0,
+k_gather(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t *__restrict__ table, int32_t hot0,
          uint8_t *__restrict__ cls)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    LT *hot_s = reinterpret_cast<LT *>(smem_raw);
+    uint8_t *hot_s = smem_raw;  // table[0, hot0): the hottest ranks
     {
-        const int vec = (int)(((size_t)hot0 * sizeof(LT) + 15) / 16);
+        const int vec = (hot0 + 15) / 16;
         const uint4 *src = reinterpret_cast<const uint4 *>(table);
         uint4 *dst = reinterpret_cast<uint4 *>(hot_s);
         for (int i = threadIdx.x; i < vec; i += GTHREADS) dst[i] = __ldg(src + i);
@@ -32,18 +73,15 @@ k_gather(const int32_t *__restrict__ targets, int64_t arcs, const LT *__restrict
     const int64_t chunks = arcs / GAPT;
     for (int64_t c = (int64_t)blockIdx.x * GTHREADS + threadIdx.x; c < chunks; c += (int64_t)gridDim.x * GTHREADS) {
         int32_t t[GAPT];
-#pragma unroll
-        for (int v = 0; v < GAPT / 4; v++) {
-            const int4 t4 = __ldcs(reinterpret_cast<const int4 *>(targets + c * GAPT) + v);
-            t[4 * v] = t4.x; t[4 * v + 1] = t4.y; t[4 * v + 2] = t4.z; t[4 * v + 3] = t4.w;
-        }
+        ld_targets16<TMODE>(targets + c * GAPT, t);
         uint32_t l[GAPT];
 #pragma unroll
         for (int i = 0; i < GAPT; i++) {
             const uint32_t ti = (uint32_t)t[i];
             const bool in_smem = ti < h0;
-            l[i] = (uint32_t)hot_s[in_smem ? ti : 0u];
-            if (!in_smem) l[i] = gee::ld_label<LT>(table + ti, pol);
+            const uint32_t g = ld_label_pred<L1MODE>(table + ti, !in_smem, pol);
+            const uint32_t sv = hot_s[in_smem ? ti : 0u];
+            l[i] = in_smem ? sv : g;
         }
         uint4 o;
         o.x = l[0] | l[1] << 8 | l[2] << 16 | l[3] << 24;
@@ -54,7 +92,7 @@ k_gather(const int32_t *__restrict__ targets, int64_t arcs, const LT *__restrict
     }
     for (int64_t e = chunks * GAPT + (int64_t)blockIdx.x * GTHREADS + threadIdx.x; e < arcs;
          e += (int64_t)gridDim.x * GTHREADS)
-        cls[e] = (uint8_t)table[targets[e]];
+        cls[e] = table[targets[e]];
 }
 
 }  // namespace
@@ -66,8 +104,8 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
     GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs k <= 255");
     if (arcs <= 0) return GEE_OK;
     GEE_REQUIRE(targets && table && cls, GEE_ERR_INVALID, "NULL array argument");
-    GEE_REQUIRE(gee::aligned16(targets) && gee::aligned16(cls) && gee::aligned16(table), GEE_ERR_INVALID,
-                "targets/cls/table must be 16-byte aligned");
+    GEE_REQUIRE(((uintptr_t)targets & 31) == 0 && gee::aligned16(cls) && gee::aligned16(table), GEE_ERR_INVALID,
+                "targets must be 32-byte aligned, cls/table 16-byte aligned");
     static int optin = 0;
     if (!optin) {
         int dev = 0;
@@ -75,17 +113,20 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
         if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
             optin = 48 * 1024;
     }
-    // Hot labels are read through L1/L2: staging the hot tier's head in
-    // shared memory measured 3x slower on C4 (33 ms vs 10.8 ms for 3.6e9
-    // lookups: skewed LDS bank conflicts, and the carve-out starves L1).
-    // GEE_GATHER_SMEM_HOT=1 re-enables it for experiments.
+    // Shared-memory head of the hot tier: GEE_GATHER_SMEM_HOT=<bytes> (experiment; default 0).
+    // GEE_GATHER_MODE=<L1MODE*2 + TMODE> selects the L1 policies (experiment).
     int64_t hot0 = 0;
-    if (getenv("GEE_GATHER_SMEM_HOT")) {
-        hot0 = (optin - 64) & ~15;
-        if (hot0 > n_hot) hot0 = n_hot & ~15;
-    }
+    if (const char *e = getenv("GEE_GATHER_SMEM_HOT")) hot0 = atoll(e);
+    if (hot0 > optin - 64) hot0 = optin - 64;
+    if (hot0 > n_hot) hot0 = n_hot;
+    hot0 &= ~(int64_t)15;
+    // default mode 1: 256-bit L1::no_allocate target loads keep L1 for the
+    // labels (10.55 ms vs 11.15 ms on C4); an smem head did not pay (L2->SM
+    // sector bandwidth, not L1 misses, bounds the lookups; profiles/)
+    int mode = 1;
+    if (const char *e = getenv("GEE_GATHER_MODE")) mode = atoi(e);
     const size_t sh = (size_t)hot0 + 16;
-    auto kern = k_gather<uint8_t>;
+    auto kern = mode == 1 ? k_gather<0, 1> : mode == 2 ? k_gather<1, 0> : mode == 3 ? k_gather<1, 1> : k_gather<0, 0>;
     GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     kern<<<gee::sm_count(), GTHREADS, sh, gee::as_stream(stream)>>>(targets, arcs, static_cast<const uint8_t *>(table),
                                                                      (int32_t)hot0, cls);

@@ -16,6 +16,9 @@
 // partials meet in a global accumulator, written by gee_reduce_heavy's
 // finalize.  Z therefore is bit-stable and independent of arc order, like
 // the tiled pull kernel (gee_pull.cu).
+#include <algorithm>
+#include <cstdlib>
+
 #include "gee_common.cuh"
 
 namespace {
@@ -595,6 +598,288 @@ k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *_
     }
 }
 
+// ---------------------------------------------------------------------------
+// Ring variant of the block reducer.  The same 32-row blocks, slot windows,
+// start-mask row mapping and write-out, but the arc stream (classes and
+// weights) is fetched by cp.async into a per-warp ring of RING rounds in
+// shared memory: RING rounds per warp are in flight without holding
+// registers (the register-fed kernel keeps one), and the ring is primed
+// across passes and blocks so a block's first rounds arrive while the
+// previous block is written out.  Each lane copies and consumes the same 8
+// arcs of a round, so cp.async.wait_group alone orders them.
+constexpr int RING = 4;
+constexpr int RING_CLS = BROUND;                        // bytes per round
+constexpr int RING_W = BROUND * (int)sizeof(float);     // bytes per round (weighted)
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Per-block view shared by the warp (uniform fields) and per lane.
+struct RingBlk {
+    int64_t base, bend;      // arc range of the block
+    unsigned nzm, hvm, anym, vm;
+    int32_t ol, oh;          // this lane's row bounds, block-local
+};
+
+__device__ __forceinline__ RingBlk ring_open(int64_t r0, int64_t n, int64_t o_lo, int64_t o_hi31, int64_t heavy_arcs,
+                                             int lane)
+{
+    RingBlk B;
+    int64_t o_hi = __shfl_down_sync(0xffffffffu, o_lo, 1);
+    if (lane == 31) o_hi = o_hi31;
+    const bool valid = r0 + lane < n;
+    const int64_t d = valid ? o_hi - o_lo : 0;
+    const bool heavy = d > heavy_arcs;
+    B.nzm = __ballot_sync(0xffffffffu, d > 0 && !heavy);
+    B.hvm = __ballot_sync(0xffffffffu, heavy);
+    B.vm = __ballot_sync(0xffffffffu, valid);
+    B.anym = B.nzm | B.hvm;
+    B.base = __shfl_sync(0xffffffffu, o_lo, 0);
+    B.bend = __shfl_sync(0xffffffffu, o_hi, 31);
+    B.ol = (int32_t)(o_lo - B.base);
+    B.oh = (int32_t)(o_hi - B.base);
+    return B;
+}
+
+// First round at or after arc e that is not entirely inside a heavy row
+// (warp-uniform).
+__device__ __forceinline__ int64_t ring_skip(const RingBlk &B, int64_t e, int lane)
+{
+    if (!B.hvm || e >= B.bend) return e;
+    const int32_t lr = (int32_t)(e - B.base);
+    const unsigned sm = __ballot_sync(0xffffffffu, ((B.anym >> lane) & 1u) && B.ol <= lr);
+    if (!sm) return e;
+    const int jr = 31 - __clz(sm);
+    const int32_t hend = __shfl_sync(0xffffffffu, B.oh, jr);
+    if (((B.hvm >> jr) & 1u) && B.base + hend >= e + BROUND) return (B.base + hend) & ~(int64_t)(BU - 1);
+    return e;
+}
+
+template <bool WEIGHTED>
+__device__ __forceinline__ void ring_issue(uint8_t *ring, int slot, int64_t e, int64_t bend, int64_t arcs,
+                                           const uint8_t *__restrict__ cls, const float *__restrict__ w, int lane)
+{
+    if (e < bend) {
+        const int64_t a = e + lane * BU;
+        const int64_t left = arcs - a;
+        const uint32_t nc = left <= 0 ? 0u : (left >= BU ? (uint32_t)BU : (uint32_t)left);
+        uint8_t *rs = ring + slot * (RING_CLS + (WEIGHTED ? RING_W : 0));
+        cp_async8(smem_u32(rs + lane * BU), nc ? (const void *)(cls + a) : (const void *)cls, nc);
+        if (WEIGHTED) {
+            const uint32_t n0 = nc >= 4 ? 16u : nc * 4u;
+            const uint32_t n1 = nc > 4 ? (nc - 4) * 4u : 0u;
+            uint8_t *rw = rs + RING_CLS + lane * BU * 4;
+            cp_async16(smem_u32(rw), n0 ? (const void *)(w + a) : (const void *)w, n0);
+            cp_async16(smem_u32(rw + 16), n1 ? (const void *)(w + a + 4) : (const void *)w, n1);
+        }
+    }
+    cp_commit();
+}
+
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(RT, 2)
+k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
+                     const float *__restrict__ w, float qscale, double dscale, const double *__restrict__ inv,
+                     int32_t k, int64_t heavy_arcs, int nslots, float *__restrict__ z)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int kk = k;
+    const int pkb = block_vec_words(kk);
+    const int hoff = nslots * pkb + 32;
+    const int wwords = hoff * Acc<WEIGHTED>::planes;
+    constexpr int RSLOT = RING_CLS + (WEIGHTED ? RING_W : 0);
+    uint8_t *ring_base = smem_raw;  // RW x RING x RSLOT (16-byte aligned)
+    float *sc1 = reinterpret_cast<float *>(smem_raw + RW * RING * RSLOT);
+    int32_t *meta = reinterpret_cast<int32_t *>(sc1 + pkb);
+    uint32_t *vbase = reinterpret_cast<uint32_t *>(meta + RW * BMETA);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint8_t *ring = ring_base + wid * RING * RSLOT;
+    uint32_t *s_mask = reinterpret_cast<uint32_t *>(meta + wid * BMETA);
+    int32_t *s_soff = meta + wid * BMETA + 24;
+    int32_t *s_row = s_soff + 36;
+    uint32_t *vw = vbase + wid * wwords;
+    for (int c = threadIdx.x; c < pkb; c += RT) sc1[c] = c < kk ? (float)(inv[c + 1] * dscale) : 0.f;
+    for (int i = threadIdx.x; i < RW * wwords; i += RT) vbase[i] = 0u;
+    for (int i = threadIdx.x; i < RW * BMETA; i += RT) meta[i] = -1;
+    __syncthreads();
+    if (lane < 24) s_mask[lane] = 0u;
+    __syncwarp();
+    const int trash = nslots * pkb + lane;
+    const unsigned below = (1u << lane) - 1u;
+    const int64_t nblocks = (n + 31) / 32;
+    const int64_t gw = (int64_t)blockIdx.x * RW + wid, GW = (int64_t)gridDim.x * RW;
+    const int64_t arcs = offsets[n];
+    const int half = kk >> 1;
+    int rot = 0;
+
+    int64_t b = gw;
+    if (b >= nblocks) return;
+    // open the first block and prime its first rounds
+    RingBlk B;
+    {
+        const int64_t r0 = 32 * b;
+        const int64_t o_lo = __ldcs(offsets + min(r0 + lane, n));
+        const int64_t o_31 = lane == 31 ? __ldcs(offsets + min(r0 + 32, n)) : 0;
+        B = ring_open(r0, n, o_lo, o_31, heavy_arcs, lane);
+    }
+    int64_t ep = ring_skip(B, B.base & ~(int64_t)(BU - 1), lane);  // next round to issue
+#pragma unroll
+    for (int i = 0; i < RING; i++) {
+        ring_issue<WEIGHTED>(ring, i, ep, B.bend, arcs, cls, w, lane);
+        if (ep < B.bend) ep = ring_skip(B, ep + BROUND, lane);
+    }
+    int slot0 = 0;  // ring slot of the pass's first round
+    for (; b < nblocks; b += GW) {
+        const int64_t r0 = 32 * b;
+        const bool more = b + GW < nblocks;
+        // next block's offsets, in flight during this block
+        const int64_t nr0 = 32 * (b + GW);
+        const int64_t o_lo_n = more ? __ldcs(offsets + min(nr0 + lane, n)) : 0;
+        const int64_t o_31_n = (more && lane == 31) ? __ldcs(offsets + min(nr0 + 32, n)) : 0;
+        const int rank = __popc(B.nzm & below);
+        const int orank = __popc(B.anym & below);
+        const int nnz = __popc(B.nzm);
+        const bool owner = (B.anym >> lane) & 1u;
+        const bool nz = (B.nzm >> lane) & 1u;
+        const int32_t lend = (int32_t)(B.bend - B.base);
+        const int rows = (int)min((int64_t)32, n - r0);
+        float *zb = z + r0 * (int64_t)kk;
+        if (B.anym != B.vm) {  // the block holds empty rows: zero-fill its Z range
+            const int total = rows * kk;
+            const int q4 = total >> 2;
+            float4 *z4 = reinterpret_cast<float4 *>(zb);
+            for (int q = lane; q < q4; q += 32) z4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int e = 4 * q4 + lane; e < total; e += 32) zb[e] = 0.f;
+        }
+        RingBlk NB;
+        bool opened = false;
+        for (int p0 = 0; p0 < max(nnz, 1); p0 += nslots) {
+            const bool mine = nz && rank >= p0 && rank < p0 + nslots;
+            if (owner) s_soff[orank + 1] = mine ? (rank - p0) * pkb + 3 : -1;
+            if (mine) s_row[rank - p0] = lane;
+            const int npass = min(nslots, nnz - p0);
+            __syncwarp();
+            int64_t ec = ring_skip(B, B.base & ~(int64_t)(BU - 1), lane);  // next round to consume
+            int slot = slot0;
+            while (ec < B.bend) {
+                cp_wait<RING - 1>();
+                const uint8_t *rs = ring + slot * RSLOT;
+                const uint2 ca = *reinterpret_cast<const uint2 *>(rs + lane * BU);
+                float wa[BU];
+                if (WEIGHTED) {
+                    const float4 x0 = *reinterpret_cast<const float4 *>(rs + RING_CLS + lane * BU * 4);
+                    const float4 x1 = *reinterpret_cast<const float4 *>(rs + RING_CLS + lane * BU * 4 + 16);
+                    wa[0] = x0.x, wa[1] = x0.y, wa[2] = x0.z, wa[3] = x0.w;
+                    wa[4] = x1.x, wa[5] = x1.y, wa[6] = x1.z, wa[7] = x1.w;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < BU; u++) wa[u] = 1.f;
+                }
+                if (nnz > 0)
+                    block_round_acc<WEIGHTED>(vw, s_soff, s_mask, rot, lane, owner, B.ol, (int32_t)(ec - B.base), lend,
+                                              hoff, trash, qscale, ca, wa);
+                __syncwarp();
+                // refill the slot just consumed with the round RING ahead
+                ring_issue<WEIGHTED>(ring, slot, ep, B.bend, arcs, cls, w, lane);
+                if (ep < B.bend) ep = ring_skip(B, ep + BROUND, lane);
+                slot = slot + 1 == RING ? 0 : slot + 1;
+                ec = ring_skip(B, ec + BROUND, lane);
+            }
+            // prime the ring for what comes next: this block's next pass, or
+            // the next block's first rounds (in flight during the write-out)
+            const bool last = p0 + nslots >= nnz;
+            if (!last) {
+                ep = ring_skip(B, B.base & ~(int64_t)(BU - 1), lane);
+            } else if (more) {
+                NB = ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
+                opened = true;
+                ep = ring_skip(NB, NB.base & ~(int64_t)(BU - 1), lane);
+            }
+            if (!last || more) {
+                const RingBlk &P = last ? NB : B;
+#pragma unroll
+                for (int i = 0; i < RING; i++) {
+                    ring_issue<WEIGHTED>(ring, (slot + i) % RING, ep, P.bend, arcs, cls, w, lane);
+                    if (ep < P.bend) ep = ring_skip(P, ep + BROUND, lane);
+                }
+                slot0 = slot;
+            }
+            if (nnz == 0) break;
+            // write this pass's rows from their slots: flat over (row, column pair)
+            if ((kk & 1) == 0) {
+                const int total = npass * half;
+                int sl = lane / half, c2 = lane - sl * half;
+                const int dsl = 32 / half, dc2 = 32 - dsl * half;
+                for (int q = lane; q < total; q += 32) {
+                    uint32_t *vs = vw + sl * pkb + 4 + 2 * c2;
+                    const uint2 lo = *reinterpret_cast<uint2 *>(vs);
+                    *reinterpret_cast<uint2 *>(vs) = make_uint2(0u, 0u);
+                    float s0, s1;
+                    if (WEIGHTED) {
+                        const uint2 hi = *reinterpret_cast<uint2 *>(vs + hoff);
+                        *reinterpret_cast<uint2 *>(vs + hoff) = make_uint2(0u, 0u);
+                        s0 = (float)(long long)(((unsigned long long)hi.x << BLOCK_SPLIT) + lo.x);
+                        s1 = (float)(long long)(((unsigned long long)hi.y << BLOCK_SPLIT) + lo.y);
+                    } else {
+                        s0 = (float)lo.x;
+                        s1 = (float)lo.y;
+                    }
+                    const float2 f = *reinterpret_cast<const float2 *>(sc1 + 2 * c2);
+                    float2 *zr = reinterpret_cast<float2 *>(zb + s_row[sl] * kk);
+                    __stcs(zr + c2, make_float2(s0 * f.x, s1 * f.y));
+                    sl += dsl;
+                    c2 += dc2;
+                    if (c2 >= half) {
+                        c2 -= half;
+                        sl++;
+                    }
+                }
+            } else {
+                const int total = npass * kk;
+                int sl = lane / kk, c = lane - sl * kk;
+                const int dsl = 32 / kk, dc = 32 - dsl * kk;
+                for (int q = lane; q < total; q += 32) {
+                    uint32_t *vs = vw + sl * pkb + 4 + c;
+                    const uint32_t lo = *vs;
+                    *vs = 0u;
+                    float s0;
+                    if (WEIGHTED) {
+                        const uint32_t hi = vs[hoff];
+                        vs[hoff] = 0u;
+                        s0 = (float)(long long)(((unsigned long long)hi << BLOCK_SPLIT) + lo);
+                    } else {
+                        s0 = (float)lo;
+                    }
+                    __stcs(zb + s_row[sl] * kk + c, s0 * sc1[c]);
+                    sl += dsl;
+                    c += dc;
+                    if (c >= kk) {
+                        c -= kk;
+                        sl++;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (!more) break;
+        B = opened ? NB : ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
+    }
+    cp_wait<0>();
+}
+
 // Bin rows by degree: small (<= small_arcs, incl. empty) and medium
 // (<= heavy_arcs); heavier rows are left to the chunked path.
 __global__ void k_bin_rows(const int64_t *__restrict__ offsets, int64_t n, int64_t small_arcs, int64_t heavy_arcs,
@@ -663,6 +948,136 @@ k_reduce_heavy(const int64_t *__restrict__ offsets, const int32_t *__restrict__ 
             if (s) atomicAdd(&acc[(int64_t)h * kk + c], (unsigned long long)s);
         }
         __syncwarp();
+    }
+}
+
+// Heavy rows for gee_reduce_heavy, one warp per work item: an item is a
+// run of up to HEAVY_ITEM_ARCS arcs of one heavy row.  Lanes take 8
+// contiguous arcs per round (one 8-byte class load, two 16-byte weight
+// loads; the next round in flight) into the carry-free split window of the
+// block kernel; every BLOCK_ROW_MAX arcs the window is folded into per-lane
+// 64-bit column sums in registers.  An item that is its row's only item
+// writes the Z row itself; the items of longer (mega) rows meet in acc[m]
+// through 64-bit atomics and a small finalize.
+constexpr int HCOL = 8;  // columns per lane: k <= 256
+
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(RT)
+k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__restrict__ item_end,
+                     const int32_t *__restrict__ item_row, const int32_t *__restrict__ item_slot, int64_t n_items,
+                     const uint8_t *__restrict__ cls, const float *__restrict__ w, float qscale, double dscale,
+                     const double *__restrict__ inv, int32_t k, bool vec, unsigned long long *__restrict__ acc,
+                     unsigned long long *__restrict__ counter, float *__restrict__ z)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int kk = k;
+    const int pkb = block_vec_words(kk);  // [3 pad | trash | bins 1..k | pad]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float *sc1 = reinterpret_cast<float *>(smem_raw);  // sc1[c] = inv[c+1] * dscale
+    uint32_t *v = reinterpret_cast<uint32_t *>(sc1 + pkb) + wid * pkb * Acc<WEIGHTED>::planes;
+    for (int c = threadIdx.x; c < pkb; c += RT) sc1[c] = c < kk ? (float)(inv[c + 1] * dscale) : 0.f;
+    for (int i = lane; i < pkb * Acc<WEIGHTED>::planes; i += 32) v[i] = 0u;
+    __syncthreads();
+    // items come largest first; warps fetch them dynamically
+    for (;;) {
+        int64_t it = 0;
+        if (lane == 0) it = (int64_t)atomicAdd(counter, 1ull);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= n_items) break;
+        const int64_t b0 = item_first[it], e1 = item_end[it];
+        unsigned long long sum[HCOL];
+#pragma unroll
+        for (int j = 0; j < HCOL; j++) sum[j] = 0ull;
+        // carry-free windows of at most BLOCK_ROW_MAX arcs, aligned in the
+        // arc array so every full window is exactly BLOCK_ROW_MAX/BROUND rounds
+        for (int64_t wb0 = b0; wb0 < e1;) {
+            const int64_t we = min((wb0 & ~(BLOCK_ROW_MAX - 1)) + BLOCK_ROW_MAX, e1);
+            int64_t e0 = wb0 & ~(int64_t)(BU - 1);
+            uint2 ca;
+            float wa[BU];
+            block_round<WEIGHTED>(cls, w, e0 + lane * BU, we, vec, ca, wa);
+            while (e0 < we) {
+                const int64_t en = e0 + BROUND;
+                uint2 cb = make_uint2(0u, 0u);
+                float wb[BU];
+#pragma unroll
+                for (int u = 0; u < BU; u++) wb[u] = 0.f;
+                if (en < we) block_round<WEIGHTED>(cls, w, en + lane * BU, we, vec, cb, wb);
+                const int64_t a0 = e0 + lane * BU;
+#pragma unroll
+                for (int u = 0; u < BU; u++) {
+                    uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
+                    if (a0 + u < wb0 || a0 + u >= we) c = 0u;
+                    if (c == 0u) continue;
+                    uint32_t *p = v + 3 + c;
+                    if (WEIGHTED) {
+                        const unsigned long long qv = (unsigned long long)__float2ll_rn(wa[u] * qscale);
+                        atomicAdd(p, (uint32_t)qv & ((1u << BLOCK_SPLIT) - 1u));
+                        atomicAdd(p + pkb, (uint32_t)(qv >> BLOCK_SPLIT));
+                    } else {
+                        atomicAdd(p, 1u);
+                    }
+                }
+                ca = cb;
+#pragma unroll
+                for (int u = 0; u < BU; u++) wa[u] = wb[u];
+                e0 = en;
+            }
+            __syncwarp();
+            wb0 = we;
+#pragma unroll
+            for (int j = 0; j < HCOL; j++) {
+                const int c = lane + 32 * j;
+                if (c < kk) {
+                    uint32_t *p = v + 4 + c;
+                    unsigned long long t = *p;
+                    *p = 0u;
+                    if (WEIGHTED) {
+                        t += (unsigned long long)p[pkb] << BLOCK_SPLIT;
+                        p[pkb] = 0u;
+                    }
+                    sum[j] += t;
+                }
+            }
+            __syncwarp();
+        }
+        const int32_t slot = item_slot[it];
+        if (slot < 0) {  // the row's only item: write its Z row
+            float *zr = z + (int64_t)item_row[it] * kk;
+#pragma unroll
+            for (int j = 0; j < HCOL; j++) {
+                const int c = lane + 32 * j;
+                if (c < kk) zr[c] = (WEIGHTED ? (float)(long long)sum[j] : (float)sum[j]) * sc1[c];
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < HCOL; j++) {
+                const int c = lane + 32 * j;
+                if (c < kk && sum[j]) atomicAdd(&acc[(int64_t)slot * kk + c], sum[j]);
+            }
+        }
+    }
+}
+
+// Heavy-row finalize, one warp per heavy row: Z[row] = acc[h] * inv (and
+// acc cleared for the next call).
+template <bool WEIGHTED>
+__global__ void k_heavy_finalize_rows(const int32_t *__restrict__ heavy_rows, int64_t n_heavy, int32_t k,
+                                      unsigned long long *__restrict__ acc, const double *__restrict__ inv,
+                                      double dscale, float *__restrict__ z)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t h = gw; h < n_heavy; h += GW) {
+        unsigned long long *a = acc + h * k;
+        float *zr = z + (int64_t)heavy_rows[h] * k;
+        for (int c = lane; c < k; c += 32) {
+            const unsigned long long s = a[c];
+            a[c] = 0ull;
+            const float f = WEIGHTED ? (float)(long long)s : (float)s;
+            zr[c] = f * (float)(inv[c + 1] * dscale);
+        }
     }
 }
 
@@ -895,6 +1310,31 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
     const int64_t nblocks = (n + 31) / 32;
     const int grid = grid_for(nblocks * 32, RT, 8);
     int rc;
+    const char *ringenv = getenv("GEE_BLOCKS_RING");
+    if (!ringenv || atoi(ringenv) != 0) {
+        // ring variant: RING rounds per warp in shared memory, 2 CTAs per SM
+        const size_t ring = (size_t)RW * RING * (RING_CLS + (weighted ? RING_W : 0));
+        const size_t budget2 = (size_t)(gee::smem_per_sm() / 2) - 1024;
+        int ns = (int)((budget2 - fixed - ring) / (RW * vecb));
+        if (ns > 24) ns = 24;
+        if (ns >= 4) {
+            const size_t shr = ring + fixed + (size_t)RW * ns * vecb;
+            const int rgrid = (int)std::min<int64_t>((nblocks + RW - 1) / RW, (int64_t)gee::sm_count() * 2);
+            if (weighted) {
+                GEE_CUDA(cudaFuncSetAttribute(k_reduce_blocks_ring<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)shr));
+                k_reduce_blocks_ring<true><<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k,
+                                                                  heavy_arcs, ns, z);
+            } else {
+                GEE_CUDA(cudaFuncSetAttribute(k_reduce_blocks_ring<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)shr));
+                k_reduce_blocks_ring<false><<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k,
+                                                                   heavy_arcs, ns, z);
+            }
+            if ((rc = gee::check_launch("k_reduce_blocks_ring"))) return rc;
+            goto heavy;
+        }
+    }
     if (weighted) {
         GEE_CUDA(cudaFuncSetAttribute(k_reduce_blocks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
         k_reduce_blocks<true><<<grid, RT, sh, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, nslots, vld, z);
@@ -903,6 +1343,7 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
         k_reduce_blocks<false><<<grid, RT, sh, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, nslots, vld, z);
     }
     if ((rc = gee::check_launch("k_reduce_blocks"))) return rc;
+heavy:
     if (n_heavy == 0) return GEE_OK;
     const size_t shh = (size_t)RW * vec;
     auto *acc = static_cast<unsigned long long *>(heavy_acc);
@@ -922,38 +1363,45 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
     return gee::check_launch("k_heavy_finalize");
 }
 
-int gee_reduce_heavy(const int64_t *offsets, const uint8_t *cls, const float *w, int32_t scale_exp,
-                     const double *inv, int32_t k, int64_t heavy_arcs, const int32_t *heavy_rows, int64_t n_heavy,
-                     const int64_t *chunk_first, const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc,
-                     float *z, void *stream)
+int gee_reduce_heavy(const uint8_t *cls, const float *w, int32_t scale_exp, const double *inv, int32_t k,
+                     const int64_t *item_first, const int64_t *item_end, const int32_t *item_row,
+                     const int32_t *item_slot, int64_t n_items, const int32_t *mega_rows, int64_t n_mega,
+                     void *mega_acc, int64_t *counter, float *z, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs 1 <= k <= 255 (got %d)", k);
-    GEE_REQUIRE(n_heavy >= 0 && n_chunks >= 0 && heavy_arcs >= 1, GEE_ERR_INVALID, "bad sizes");
-    if (n_heavy == 0) return GEE_OK;
-    GEE_REQUIRE(offsets && cls && inv && z && heavy_rows && chunk_first && chunk_heavy && heavy_acc, GEE_ERR_INVALID,
+    GEE_REQUIRE(n_items >= 0 && n_mega >= 0, GEE_ERR_INVALID, "bad sizes");
+    if (n_items == 0) return GEE_OK;
+    GEE_REQUIRE(cls && inv && z && item_first && item_end && item_row && item_slot, GEE_ERR_INVALID,
                 "NULL array argument");
+    GEE_REQUIRE(n_mega == 0 || (mega_rows && mega_acc), GEE_ERR_INVALID, "mega rows need their accumulator");
+    GEE_REQUIRE(counter != nullptr, GEE_ERR_INVALID, "counter must not be NULL");
     cudaStream_t st = gee::as_stream(stream);
     const bool weighted = w != nullptr;
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
-    const size_t shh = (size_t)RW * (((size_t)k + 3) & ~(size_t)3) * (weighted ? 2 : 1) * sizeof(uint32_t);
-    auto *acc = static_cast<unsigned long long *>(heavy_acc);
-    const int hgrid = grid_for(n_chunks * 32, RT, 8);
+    const size_t sh = (size_t)block_vec_words(k) * sizeof(float) +
+                      (size_t)RW * block_vec_words(k) * (weighted ? 2 : 1) * sizeof(uint32_t);
+    const bool vld = (reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0);
+    auto *acc = static_cast<unsigned long long *>(mega_acc);
+    auto *ctr = reinterpret_cast<unsigned long long *>(counter);
+    GEE_CUDA(cudaMemsetAsync(ctr, 0, sizeof(*ctr), st));
+    const int hgrid = grid_for(n_items * 32, RT, 8);
     if (weighted)
-        k_reduce_heavy<true><<<hgrid, RT, shh, st>>>(offsets, heavy_rows, chunk_first, chunk_heavy, n_chunks, heavy_arcs,
-                                                     cls, w, qscale, k, acc);
+        k_reduce_heavy_items<true><<<hgrid, RT, sh, st>>>(item_first, item_end, item_row, item_slot, n_items, cls, w,
+                                                          qscale, dscale, inv, k, vld, acc, ctr, z);
     else
-        k_reduce_heavy<false><<<hgrid, RT, shh, st>>>(offsets, heavy_rows, chunk_first, chunk_heavy, n_chunks,
-                                                      heavy_arcs, cls, w, qscale, k, acc);
+        k_reduce_heavy_items<false><<<hgrid, RT, sh, st>>>(item_first, item_end, item_row, item_slot, n_items, cls, w,
+                                                           qscale, dscale, inv, k, vld, acc, ctr, z);
     int rc;
-    if ((rc = gee::check_launch("k_reduce_heavy"))) return rc;
-    const int fgrid = grid_for(n_heavy * k, 256, 4);
+    if ((rc = gee::check_launch("k_reduce_heavy_items"))) return rc;
+    if (n_mega == 0) return GEE_OK;
+    const int fgrid = grid_for(n_mega * 32, 256, 8);
     if (weighted)
-        k_heavy_finalize<true><<<fgrid, 256, 0, st>>>(heavy_rows, n_heavy, k, acc, inv, dscale, z);
+        k_heavy_finalize_rows<true><<<fgrid, 256, 0, st>>>(mega_rows, n_mega, k, acc, inv, dscale, z);
     else
-        k_heavy_finalize<false><<<fgrid, 256, 0, st>>>(heavy_rows, n_heavy, k, acc, inv, dscale, z);
-    return gee::check_launch("k_heavy_finalize");
+        k_heavy_finalize_rows<false><<<fgrid, 256, 0, st>>>(mega_rows, n_mega, k, acc, inv, dscale, z);
+    return gee::check_launch("k_heavy_finalize_rows");
 }
 
 int gee_block_scale_exp(double max_row_abs, double max_abs, double min_abs_nz, int32_t *scale_exp, double *rel_err)

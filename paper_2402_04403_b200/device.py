@@ -189,7 +189,8 @@ class DeviceGraph:
               "gee_reduce_bins")
         self.n_small, self.n_medium = int(ns.value), int(nm.value)
 
-    HEAVY_ARCS = 2048  # rows above go to the chunked heavy path (<= the block reducer's limit)
+    HEAVY_ARCS = 2048  # rows above go to the heavy path (<= the block reducer's limit)
+    HEAVY_ITEM_ARCS = 65536  # arcs per heavy work item (one warp)
     SMALL_ARCS = 32
 
     def _plan_heavy(self):
@@ -201,11 +202,16 @@ class DeviceGraph:
                                         _stream()), "gee_reduce_heavy_plan")
         self.n_heavy = int(nh.value)
         self.heavy_arc_total = 0
+        self.item_first = self.item_end = self.item_row = self.item_slot = self.mega_rows = None
+        self.n_items = self.n_mega = 0
         if self.n_heavy == 0:
             self.heavy_rows = self.chunk_first = self.chunk_heavy = None
             self.n_chunks = 0
             return
-        rows = rows[:self.n_heavy].clone()
+        # ascending row order: the chunk pass then streams the CSR and the
+        # finalize sweeps Z in address order (k_mark_heavy appends in
+        # atomic order, which scatters both over 30 GB)
+        rows = torch.sort(rows[:self.n_heavy])[0].contiguous()
         r64 = rows.to(torch.int64)
         first = self.offsets[r64].cpu()
         deg = (self.offsets[r64 + 1] - self.offsets[r64]).cpu()
@@ -214,6 +220,27 @@ class DeviceGraph:
         start = torch.repeat_interleave(first, per)
         within = torch.arange(int(per.sum())) - torch.repeat_interleave(torch.cumsum(per, 0) - per, per)
         self.heavy_arc_total = int(deg.sum())
+        # work items of gee_reduce_heavy: runs of <= HEAVY_ITEM_ARCS arcs;
+        # rows with several items ("mega" rows) combine through acc + finalize
+        nit = (deg + self.HEAVY_ITEM_ARCS - 1) // self.HEAVY_ITEM_ARCS
+        it_row = torch.repeat_interleave(torch.arange(self.n_heavy), nit)
+        it_j = torch.arange(int(nit.sum())) - torch.repeat_interleave(torch.cumsum(nit, 0) - nit, nit)
+        it_first = first[it_row] + it_j * self.HEAVY_ITEM_ARCS
+        it_end = torch.minimum(it_first + self.HEAVY_ITEM_ARCS, first[it_row] + deg[it_row])
+        mega = nit > 1
+        mega_idx = torch.full((self.n_heavy,), -1, dtype=torch.int64)
+        mega_idx[mega] = torch.arange(int(mega.sum()))
+        rows_cpu = rows.cpu()
+        # largest items first (the kernel fetches them dynamically)
+        order = torch.argsort(it_end - it_first, descending=True, stable=True)
+        it_row, it_first, it_end = it_row[order], it_first[order], it_end[order]
+        self.item_first = it_first.to(self.device)
+        self.item_end = it_end.to(self.device)
+        self.item_row = rows_cpu[it_row].to(torch.int32).to(self.device)
+        self.item_slot = mega_idx[it_row].to(torch.int32).to(self.device)
+        self.n_items = int(it_row.numel())
+        self.mega_rows = rows_cpu[mega].to(torch.int32).to(self.device)
+        self.n_mega = int(mega.sum())
         self.heavy_rows = rows
         self.chunk_first = (start + within * self.HEAVY_ARCS).to(self.device)
         self.chunk_heavy = heavy_idx.to(torch.int32).to(self.device)
@@ -305,7 +332,9 @@ class Embedder:
         self.table_n_hot = None  # n_hot the current table was built with
         self.slots = None
         self.cls = None  # class stream of the split pull
-        self.heavy_acc = None  # heavy-row partial sums (row reducer)
+        self.heavy_acc = None  # heavy-row partial sums (list / row reducers)
+        self.mega_acc = None  # mega-row partial sums (block reducer's heavy items)
+        self.counter = torch.zeros(1, dtype=torch.int64, device=dev)  # heavy-item work counter
         self.split = os.environ.get("GEE_PULL_FUSED") is None
         self.reducer = os.environ.get("GEE_PULL_REDUCER", "blocks")  # blocks | lists | rows | tiles
         self.phase_events = None  # list -> (phase, cuda event) after each phase (bench)
@@ -379,9 +408,15 @@ class Embedder:
                                                 ptr(self.inv64), self.k, g.HEAVY_ARCS, None, 0, None, None, 0, None,
                                                 ptr(z), _stream()), "gee_reduce_blocks")
                     self._mark("blocks", 1)
-                    check(lib.gee_reduce_heavy(ptr(g.offsets), ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                               ptr(self.inv64), self.k, *heavy), "gee_reduce_heavy")
-                    self._mark("heavy", 2 if g.n_heavy else 0)
+                    if g.n_mega and (self.mega_acc is None or self.mega_acc.numel() < g.n_mega * self.k):
+                        self.mega_acc = torch.zeros(g.n_mega * self.k, dtype=torch.int64, device=self.device)
+                    check(lib.gee_reduce_heavy(ptr(self.cls), ptr(g.weights), g.scale_exp, ptr(self.inv64), self.k,
+                                               ptr(g.item_first), ptr(g.item_end), ptr(g.item_row), ptr(g.item_slot),
+                                               g.n_items, ptr(g.mega_rows), g.n_mega,
+                                               ptr(self.mega_acc) if g.n_mega else None, ptr(self.counter), ptr(z),
+                                               _stream()),
+                          "gee_reduce_heavy")
+                    self._mark("heavy", (1 if g.n_items else 0) + (1 if g.n_mega else 0))
                 elif reducer == "lists":
                     g.ensure_bins()
                     check(lib.gee_reduce_lists(ptr(g.offsets), ptr(g.small_rows), g.n_small, ptr(g.medium_rows),
