@@ -818,57 +818,45 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
                 slot0 = slot;
             }
             if (nnz == 0) break;
-            // write this pass's rows from their slots: flat over (row, column pair)
+            // write this pass's rows from their slots: each lane owns column
+            // pairs (scale factors hoisted), rows loop with uniform addresses
             if ((kk & 1) == 0) {
-                const int total = npass * half;
-                int sl = lane / half, c2 = lane - sl * half;
-                const int dsl = 32 / half, dc2 = 32 - dsl * half;
-                for (int q = lane; q < total; q += 32) {
-                    uint32_t *vs = vw + sl * pkb + 4 + 2 * c2;
-                    const uint2 lo = *reinterpret_cast<uint2 *>(vs);
-                    *reinterpret_cast<uint2 *>(vs) = make_uint2(0u, 0u);
-                    float s0, s1;
-                    if (WEIGHTED) {
-                        const uint2 hi = *reinterpret_cast<uint2 *>(vs + hoff);
-                        *reinterpret_cast<uint2 *>(vs + hoff) = make_uint2(0u, 0u);
-                        s0 = (float)(long long)(((unsigned long long)hi.x << BLOCK_SPLIT) + lo.x);
-                        s1 = (float)(long long)(((unsigned long long)hi.y << BLOCK_SPLIT) + lo.y);
-                    } else {
-                        s0 = (float)lo.x;
-                        s1 = (float)lo.y;
-                    }
+                for (int c2 = lane; c2 < half; c2 += 32) {
                     const float2 f = *reinterpret_cast<const float2 *>(sc1 + 2 * c2);
-                    float2 *zr = reinterpret_cast<float2 *>(zb + s_row[sl] * kk);
-                    __stcs(zr + c2, make_float2(s0 * f.x, s1 * f.y));
-                    sl += dsl;
-                    c2 += dc2;
-                    if (c2 >= half) {
-                        c2 -= half;
-                        sl++;
+                    uint32_t *vs = vw + 4 + 2 * c2;
+                    float *zc = zb + 2 * c2;
+                    for (int sl = 0; sl < npass; sl++, vs += pkb) {
+                        const uint2 lo = *reinterpret_cast<uint2 *>(vs);
+                        *reinterpret_cast<uint2 *>(vs) = make_uint2(0u, 0u);
+                        float s0, s1;
+                        if (WEIGHTED) {
+                            const uint2 hi = *reinterpret_cast<uint2 *>(vs + hoff);
+                            *reinterpret_cast<uint2 *>(vs + hoff) = make_uint2(0u, 0u);
+                            s0 = (float)(long long)(((unsigned long long)hi.x << BLOCK_SPLIT) + lo.x);
+                            s1 = (float)(long long)(((unsigned long long)hi.y << BLOCK_SPLIT) + lo.y);
+                        } else {
+                            s0 = (float)lo.x;
+                            s1 = (float)lo.y;
+                        }
+                        __stcs(reinterpret_cast<float2 *>(zc + s_row[sl] * kk), make_float2(s0 * f.x, s1 * f.y));
                     }
                 }
             } else {
-                const int total = npass * kk;
-                int sl = lane / kk, c = lane - sl * kk;
-                const int dsl = 32 / kk, dc = 32 - dsl * kk;
-                for (int q = lane; q < total; q += 32) {
-                    uint32_t *vs = vw + sl * pkb + 4 + c;
-                    const uint32_t lo = *vs;
-                    *vs = 0u;
-                    float s0;
-                    if (WEIGHTED) {
-                        const uint32_t hi = vs[hoff];
-                        vs[hoff] = 0u;
-                        s0 = (float)(long long)(((unsigned long long)hi << BLOCK_SPLIT) + lo);
-                    } else {
-                        s0 = (float)lo;
-                    }
-                    __stcs(zb + s_row[sl] * kk + c, s0 * sc1[c]);
-                    sl += dsl;
-                    c += dc;
-                    if (c >= kk) {
-                        c -= kk;
-                        sl++;
+                for (int c = lane; c < kk; c += 32) {
+                    const float f = sc1[c];
+                    uint32_t *vs = vw + 4 + c;
+                    for (int sl = 0; sl < npass; sl++, vs += pkb) {
+                        const uint32_t lo = *vs;
+                        *vs = 0u;
+                        float s0;
+                        if (WEIGHTED) {
+                            const uint32_t hi = vs[hoff];
+                            vs[hoff] = 0u;
+                            s0 = (float)(long long)(((unsigned long long)hi << BLOCK_SPLIT) + lo);
+                        } else {
+                            s0 = (float)lo;
+                        }
+                        __stcs(zb + s_row[sl] * kk + c, s0 * f);
                     }
                 }
             }

@@ -1,0 +1,154 @@
+"""Host-resident graph -> host Z, streamed through the GPU in row chunks.
+
+A user of the reference calls ``embed_parallel(g, y)`` with a CSR graph and
+labels in host memory and gets Z back in host memory (encoder.py:123-194).
+With a graph of C4's size the PCIe copies dominate that call:
+- about 31 GB of prepared CSR goes in;
+- about 27 GB of Z comes out.
+
+PCIe is full duplex, so this module overlaps the two. It splits the prepared
+symmetric CSR into row chunks balanced by bytes. Then, on three CUDA streams:
+- copy-in: H2D of chunk i+1 into one of two device slots;
+- compute: the pull of chunk i (gather + block / heavy reduction), into one
+  of two Z slots;
+- copy-out: D2H of chunk i-1's Z rows into the caller's pinned host Z.
+
+Events order the slot reuse, and each chunk's pull is exactly the
+single-GPU pull on a row range (the same kernels as the row-range shards).
+
+Graph preparation (CSR build, hot-label plan, per-chunk heavy-row items,
+pinned host copies) happens once in ``HostPipeline(...)``. It is outside
+the timed region, as the reference's ``build_csr`` is (bench.py:1-7 there).
+"""
+
+import numpy as np
+import torch
+
+from .device import DeviceGraph, Embedder
+from .errors import ValidationError
+from .shard import plan_rows
+
+
+class HostPipeline:
+    """Streams a prepared graph held in pinned host memory through one GPU."""
+
+    def __init__(self, g: DeviceGraph, k, chunks=16, device=None):
+        if not g.has_pull or g.hot_k != k:
+            raise ValidationError("HostPipeline needs a pull graph prepared for k (prepare_hot)")
+        if g.n != g.n_nodes:
+            raise ValidationError("HostPipeline takes a whole graph, not a row shard")
+        self.device = device or g.device
+        self.n, self.k, self.s = g.n, k, g.s
+        self.weighted = g.weighted
+        dev = self.device
+        off = g.offsets.cpu().numpy()
+        self.bounds = plan_rows(off, max(1, chunks), k, self.weighted)
+        pin = lambda t: None if t is None else t.cpu().pin_memory()  # noqa: E731
+        # host copies of the prepared layout (the "stored graph")
+        self.h_tgt = pin(g.targets)
+        self.h_w = pin(g.weights)
+        self.h_hot = pin(g.hot_rank)
+        self.n_hot = g.n_hot
+        self.h_off = []
+        self.views = []
+        max_rows = max_arcs = 0
+        for c in range(len(self.bounds) - 1):
+            lo, hi = int(self.bounds[c]), int(self.bounds[c + 1])
+            a0, a1 = int(off[lo]), int(off[hi])
+            self.h_off.append(torch.from_numpy(off[lo:hi + 1] - off[lo]).pin_memory())
+            v = DeviceGraph(hi - lo, 0, dev)
+            v.n_nodes = g.n_nodes
+            # plan the chunk's heavy rows / block spans on a temporary device
+            # copy of its rebased offsets (graph preparation)
+            v.offsets = self.h_off[c].to(dev)
+            v.targets = torch.empty(a1 - a0, dtype=torch.int32, device=dev)  # shape only
+            v.weights = None
+            v._plan_heavy()
+            ends = v.offsets[torch.arange(0, v.n + 32, 32, device=dev).clamp_(max=v.n)]
+            v.max_block_arcs = int((ends[1:] - ends[:-1]).max().item()) if v.n else 0
+            v.scale_exp, v.rel_err, v.max_row_abs = g.scale_exp, g.rel_err, g.max_row_abs
+            v.hot_k, v.n_hot, v.hot_rank = k, g.n_hot, None
+            v.offsets = v.targets = None
+            v.span = (lo, hi, a0, a1)
+            self.views.append(v)
+            max_rows, max_arcs = max(max_rows, hi - lo), max(max_arcs, a1 - a0)
+        # device slots (double-buffered) and the labels / hot ranks
+        self.d_off = [torch.empty(max_rows + 1, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.d_tgt = [torch.empty(max_arcs, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.d_w = [torch.empty(max_arcs, dtype=torch.float32, device=dev) if self.weighted else None
+                    for _ in range(2)]
+        self.d_z = [torch.empty(max_rows * k, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.d_y = torch.empty(self.n, dtype=torch.int32, device=dev)
+        self.d_hot = torch.empty(self.n, dtype=torch.int32, device=dev) if self.h_hot is not None else None
+        self.proj = DeviceGraph(self.n, 0, dev)  # what project() needs: hot ranks of the whole graph
+        self.proj.hot_rank, self.proj.n_hot = self.d_hot, self.n_hot
+        self.s_in = torch.cuda.Stream(dev)
+        self.s_cmp = torch.cuda.Stream(dev)
+        self.s_out = torch.cuda.Stream(dev)
+
+    @property
+    def n_chunks(self):
+        return len(self.views)
+
+    def h2d_bytes(self, h_labels):
+        b = h_labels.numel() * h_labels.element_size()
+        b += sum(t.numel() * 8 for t in self.h_off) + self.h_tgt.numel() * 4
+        if self.h_w is not None:
+            b += self.h_w.numel() * 4
+        if self.h_hot is not None:
+            b += self.h_hot.numel() * 4
+        return int(b)
+
+    def run(self, h_labels, h_z, emb: Embedder):
+        """labels (pinned host int32[n]) -> h_z (pinned host float32[n, k])."""
+        if h_z.shape != (self.n, self.k) or h_z.dtype != torch.float32:
+            raise ValidationError("h_z must be a float32 (n, k) host tensor")
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        e_lab = ev()
+        with torch.cuda.stream(self.s_in):
+            self.d_y.copy_(h_labels, non_blocking=True)
+            if self.d_hot is not None:
+                self.d_hot.copy_(self.h_hot, non_blocking=True)
+            e_lab.record(self.s_in)
+        self.s_cmp.wait_event(e_lab)
+        with torch.cuda.stream(self.s_cmp):
+            emb.project(self.d_y, validate=False, g=self.proj)
+        e_in = [ev() for _ in self.views]
+        e_cmp = [ev() for _ in self.views]
+        e_out = [ev() for _ in self.views]
+        for i, v in enumerate(self.views):
+            b = i & 1
+            lo, hi, a0, a1 = v.span
+            with torch.cuda.stream(self.s_in):
+                if i >= 2:
+                    self.s_in.wait_event(e_cmp[i - 2])  # slot b's CSR is free
+                self.d_off[b][:hi - lo + 1].copy_(self.h_off[i], non_blocking=True)
+                self.d_tgt[b][:a1 - a0].copy_(self.h_tgt[a0:a1], non_blocking=True)
+                if self.weighted:
+                    self.d_w[b][:a1 - a0].copy_(self.h_w[a0:a1], non_blocking=True)
+                e_in[i].record(self.s_in)
+            self.s_cmp.wait_event(e_in[i])
+            if i >= 2:
+                self.s_cmp.wait_event(e_out[i - 2])  # Z slot b has been copied out
+            with torch.cuda.stream(self.s_cmp):
+                v.offsets = self.d_off[b][:hi - lo + 1]
+                v.targets = self.d_tgt[b][:a1 - a0]
+                v.weights = self.d_w[b][:a1 - a0] if self.weighted else None
+                z = self.d_z[b][:(hi - lo) * self.k].view(hi - lo, self.k)
+                emb.pull(v, z)
+                e_cmp[i].record(self.s_cmp)
+            self.s_out.wait_event(e_cmp[i])
+            with torch.cuda.stream(self.s_out):
+                h_z[lo:hi].copy_(z, non_blocking=True)
+                e_out[i].record(self.s_out)
+        self.s_out.synchronize()
+        for v in self.views:
+            v.offsets = v.targets = v.weights = None
+        return h_z
+
+
+def pinned_like(shape, dtype=torch.float32):
+    return torch.empty(shape, dtype=dtype).pin_memory()
+
+
+__all__ = ["HostPipeline", "pinned_like", "np"]

@@ -398,3 +398,30 @@ def test_raw_ctypes_binding_without_torch():
             rt.cudaFree(p)
     assert np.array_equal(counts, np.bincount(y, minlength=k + 1))
     assert rel_err(z, oracle.serial_embed(src, dst, w, y, n, k)) <= TOL
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 7])
+def test_host_pipeline_matches_resident_pull(chunks):
+    # stream.HostPipeline: pinned host graph + labels -> pinned host Z via
+    # row chunks on three streams; every chunk's pull sums the same integers
+    # as the resident pull, so Z is bit-identical
+    from paper_2402_04403_b200.stream import HostPipeline, pinned_like
+
+    scale, s, k = 17, 1_500_000, 50
+    src, dst, w = synth.rmat_edges(scale, s, seed=41, weighted=True)
+    n = 1 << scale
+    y = synth.uniform_labels(n, k, seed=42)
+    dev = torch.device("cuda")
+    g = DeviceGraph.from_edges(src, dst, w, n, device=dev, pull=True)
+    g.prepare_hot(k, enable=True)
+    emb = Embedder(n, k, dev)
+    emb.project(y, g=g)
+    z_ref = emb.pull(g).cpu()
+    pipe = HostPipeline(g, k, chunks=chunks)
+    assert pipe.n_chunks == chunks
+    h_z = pinned_like((n, k))
+    h_z.fill_(float("nan"))
+    pipe.run(y.cpu().pin_memory(), h_z, emb)
+    assert torch.equal(h_z, z_ref)
+    exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), w.cpu().numpy(), y.cpu().numpy(), n, k)
+    assert rel_err(h_z.numpy(), exp) <= TOL
