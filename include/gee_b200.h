@@ -135,6 +135,12 @@ int gee_build_sym_csr_rows(const int32_t *src, const int32_t *dst, const float *
  * gee_build_csr or gee_embed_coo.  rows[arcs] int32. */
 int gee_csr_rows(const int64_t *offsets, int64_t n, int64_t arcs, int32_t *rows, void *stream);
 
+/* Graph preparation: sort every row's arcs by target (stable, weights
+ * follow).  The pull's sums are exact integers, so Z is unchanged; sorted
+ * targets (label-table slots after gee_hot_encode) let a warp's 32
+ * consecutive label lookups share sectors.  Allocates scratch; blocks. */
+int gee_sort_rows(const int64_t *offsets, int64_t n, int32_t *targets, float *w, void *stream);
+
 /* Graph statistics that size the pull accumulator (host outputs):
  * max over rows of sum |w| (or max degree if w NULL), min nonzero |w|,
  * max |w|, and whether any weight is non-finite. */
@@ -241,6 +247,7 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
 
 /* Heavy rows (longer than the block reducer's heavy_arcs) as work items:
  * item i covers arcs [item_first[i], item_end[i]) of row item_row[i]
+ * (cls / w hold `arcs` entries)
  * (at most 65536 arcs).  item_slot[i] < 0: the item is its row's only one and
  * writes the Z row; otherwise it adds into mega_acc[item_slot[i]] (int64
  * [n_mega x k], zero on entry, left zero on exit) and a finalize writes the
@@ -248,8 +255,8 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
  * (device int64 scratch), so list them largest first.  Weighted graphs need
  * gee_block_scale_exp's exponent.  Graph preparation builds the items (device.py
  * DeviceGraph._plan_heavy). */
-int gee_reduce_heavy(const uint8_t *cls, const float *w, int32_t scale_exp, const double *inv, int32_t k,
-                     const int64_t *item_first, const int64_t *item_end, const int32_t *item_row,
+int gee_reduce_heavy(const uint8_t *cls, const float *w, int64_t arcs, int32_t scale_exp, const double *inv,
+                     int32_t k, const int64_t *item_first, const int64_t *item_end, const int32_t *item_row,
                      const int32_t *item_slot, int64_t n_items, const int32_t *mega_rows, int64_t n_mega,
                      void *mega_acc, int64_t *counter, float *z, void *stream);
 

@@ -95,6 +95,35 @@ k_gather(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t *__res
         cls[e] = table[targets[e]];
 }
 
+// Lane-contiguous variant: a warp takes 512 consecutive arcs per step and
+// each of its 16 gather instructions covers 32 consecutive arcs, so when
+// rows are sorted by slot (gee_sort_rows) a warp's lookups share sectors.
+template <int L1MODE>
+__global__ void __launch_bounds__(GTHREADS, 1)
+k_gather_contig(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t *__restrict__ table,
+                uint8_t *__restrict__ cls)
+{
+    const uint64_t pol = gee::policy_evict_last();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (GTHREADS / 32);
+    const int64_t gw = (int64_t)blockIdx.x * (GTHREADS / 32) + (threadIdx.x >> 5);
+    const int64_t steps = arcs / 512;
+    for (int64_t st = gw; st < steps; st += warps) {
+        const int32_t *tp = targets + st * 512 + lane;
+        uint32_t t[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++)
+            asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(t[i]) : "l"(tp + 32 * i));
+        uint32_t l[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) l[i] = ld_label_pred<L1MODE>(table + t[i], true, pol);
+        uint8_t *cp = cls + st * 512 + lane;
+#pragma unroll
+        for (int i = 0; i < 16; i++) cp[32 * i] = (uint8_t)l[i];
+    }
+    for (int64_t e = steps * 512 + gw * 32 + lane; e < arcs; e += warps * 32) cls[e] = table[targets[e]];
+}
+
 }  // namespace
 
 extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const void *table, int64_t n_hot, int32_t k,
@@ -120,11 +149,19 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
     if (hot0 > optin - 64) hot0 = optin - 64;
     if (hot0 > n_hot) hot0 = n_hot;
     hot0 &= ~(int64_t)15;
-    // default mode 1: 256-bit L1::no_allocate target loads keep L1 for the
-    // labels (10.55 ms vs 11.15 ms on C4); an smem head did not pay (L2->SM
-    // sector bandwidth, not L1 misses, bounds the lookups; profiles/)
-    int mode = 1;
+    // default mode 4: lane-contiguous lookups, which share sectors when rows
+    // are sorted by slot (DeviceGraph sorts them: C4 9.67 ms vs 10.43 ms for
+    // mode 1, the 16-arcs-per-thread layout with 256-bit no-allocate target
+    // loads; mode 0 = 11.15 ms).  An smem head did not pay: the L1->L2
+    // request rate for missing sectors bounds the lookups (profiles/).
+    int mode = 4;
     if (const char *e = getenv("GEE_GATHER_MODE")) mode = atoi(e);
+    if (mode >= 4) {  // lane-contiguous lookups (rows sorted by slot)
+        auto kc = mode == 5 ? k_gather_contig<1> : k_gather_contig<0>;
+        kc<<<gee::sm_count(), GTHREADS, 0, gee::as_stream(stream)>>>(targets, arcs, static_cast<const uint8_t *>(table),
+                                                                     cls);
+        return gee::check_launch("k_gather_contig");
+    }
     const size_t sh = (size_t)hot0 + 16;
     auto kern = mode == 1 ? k_gather<0, 1> : mode == 2 ? k_gather<1, 0> : mode == 3 ? k_gather<1, 1> : k_gather<0, 0>;
     GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));

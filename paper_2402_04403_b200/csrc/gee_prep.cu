@@ -9,8 +9,12 @@
 //                      updates per listed edge (encoder.py:106-120).
 //   gee_csr_rows       per-arc source row of a stored CSR (COO expansion).
 //   gee_graph_stats    weight statistics that size the pull fixed point.
+#include <algorithm>
+#include <vector>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include "gee_common.cuh"
 
@@ -188,6 +192,29 @@ int grid_for(int64_t items, int per_block, int waves)
     int64_t want = (items + per_block - 1) / per_block;
     int64_t cap = (int64_t)gee::sm_count() * waves;
     return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+// first row r in [0, n] with offsets[r] >= target, one thread per target
+__global__ void k_row_bounds(const int64_t *__restrict__ offsets, int64_t n, int64_t step, int64_t m,
+                             int64_t *__restrict__ rows)
+{
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j > m) return;
+    const int64_t t = j * step;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (offsets[mid] < t) lo = mid + 1;
+        else hi = mid;
+    }
+    rows[j] = j == m ? n : lo;
+}
+
+__global__ void k_rebase(const int64_t *__restrict__ offsets, int64_t r0, int64_t rows, int32_t *__restrict__ out)
+{
+    const int64_t base = offsets[r0];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= rows; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int32_t)(offsets[r0 + i] - base);
 }
 
 }  // namespace
@@ -374,6 +401,110 @@ int gee_graph_stats(const int64_t *offsets, const float *w, int64_t n, int64_t a
     if (max_abs) *max_abs = h.max_abs;
     if (nonfinite) *nonfinite = h.nonfinite;
     return GEE_OK;
+}
+
+int gee_sort_rows(const int64_t *offsets, int64_t n, int32_t *targets, float *w, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(n >= 0, GEE_ERR_INVALID, "n must be nonnegative");
+    if (n == 0) return GEE_OK;
+    GEE_REQUIRE(offsets && targets, GEE_ERR_INVALID, "NULL array argument");
+    cudaStream_t st = gee::as_stream(stream);
+    int64_t arcs = 0;
+    GEE_CUDA(cudaMemcpyAsync(&arcs, offsets + n, sizeof(arcs), cudaMemcpyDeviceToHost, st));
+    GEE_CUDA(cudaStreamSynchronize(st));
+    if (arcs == 0) return GEE_OK;
+    // row chunks of at most STEP arcs (plus one row) for the int-sized CUB calls
+    const int64_t STEP = (int64_t)1 << 29;
+    const int64_t m = (arcs + STEP - 1) / STEP;
+    int64_t *d_rows = nullptr;
+    int32_t *d_off = nullptr, *k_out = nullptr;
+    float *v_out = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    std::vector<int64_t> rows(m + 1);
+    int rc = GEE_OK;
+    int64_t max_rows = 0, max_arcs = 0;
+    auto fail = [&](const char *what) {
+        gee::set_error("%s", what);
+        rc = GEE_ERR_CUDA;
+    };
+    if (cudaMallocAsync((void **)&d_rows, sizeof(int64_t) * (m + 1), st) != cudaSuccess) {
+        fail("gee_sort_rows: alloc failed");
+        goto out;
+    }
+    k_row_bounds<<<(int)((m + 1 + 255) / 256), 256, 0, st>>>(offsets, n, STEP, m, d_rows);
+    if ((rc = gee::check_launch("k_row_bounds"))) goto out;
+    cudaMemcpyAsync(rows.data(), d_rows, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+        fail("gee_sort_rows: sync failed");
+        goto out;
+    }
+    {
+        std::vector<int64_t> off_h(m + 1);
+        for (int64_t j = 0; j <= m; j++)
+            cudaMemcpyAsync(&off_h[j], offsets + rows[j], sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        for (int64_t j = 0; j < m; j++) {
+            max_rows = std::max(max_rows, rows[j + 1] - rows[j]);
+            max_arcs = std::max(max_arcs, off_h[j + 1] - off_h[j]);
+        }
+        GEE_REQUIRE(max_arcs < INT32_MAX, GEE_ERR_RANGE, "a row exceeds 2^31 arcs");
+        if (cudaMallocAsync((void **)&d_off, sizeof(int32_t) * (max_rows + 1), st) != cudaSuccess ||
+            cudaMallocAsync((void **)&k_out, sizeof(int32_t) * max_arcs, st) != cudaSuccess ||
+            (w && cudaMallocAsync((void **)&v_out, sizeof(float) * max_arcs, st) != cudaSuccess)) {
+            fail("gee_sort_rows: scratch alloc failed");
+            goto out;
+        }
+        for (int64_t j = 0; j < m; j++) {
+            const int64_t r0 = rows[j], nr = rows[j + 1] - rows[j];
+            const int64_t a0 = off_h[j], na = off_h[j + 1] - off_h[j];
+            if (nr == 0 || na == 0) continue;
+            k_rebase<<<(int)std::min<int64_t>((nr + 256) / 256, 4096), 256, 0, st>>>(offsets, r0, nr, d_off);
+            if ((rc = gee::check_launch("k_rebase"))) goto out;
+            size_t need = 0;
+            if (w)
+                cub::DeviceSegmentedSort::StableSortPairs(nullptr, need, targets + a0, k_out, w + a0, v_out, (int)na,
+                                                          (int)nr, d_off, d_off + 1, st);
+            else
+                cub::DeviceSegmentedSort::StableSortKeys(nullptr, need, targets + a0, k_out, (int)na, (int)nr, d_off,
+                                                         d_off + 1, st);
+            if (need > tmp_bytes) {
+                if (tmp) cudaFreeAsync(tmp, st);
+                tmp = nullptr;
+                if (cudaMallocAsync(&tmp, need, st) != cudaSuccess) {
+                    fail("gee_sort_rows: sort scratch alloc failed");
+                    goto out;
+                }
+                tmp_bytes = need;
+            }
+            cudaError_t e;
+            if (w)
+                e = cub::DeviceSegmentedSort::StableSortPairs(tmp, need, targets + a0, k_out, w + a0, v_out, (int)na,
+                                                              (int)nr, d_off, d_off + 1, st);
+            else
+                e = cub::DeviceSegmentedSort::StableSortKeys(tmp, need, targets + a0, k_out, (int)na, (int)nr, d_off,
+                                                             d_off + 1, st);
+            if (e != cudaSuccess) {
+                fail("gee_sort_rows: segmented sort failed");
+                goto out;
+            }
+            cudaMemcpyAsync(targets + a0, k_out, sizeof(int32_t) * na, cudaMemcpyDeviceToDevice, st);
+            if (w) cudaMemcpyAsync(w + a0, v_out, sizeof(float) * na, cudaMemcpyDeviceToDevice, st);
+        }
+        if ((rc = gee::check_launch("gee_sort_rows"))) goto out;
+    }
+out:
+    if (tmp) cudaFreeAsync(tmp, st);
+    if (d_rows) cudaFreeAsync(d_rows, st);
+    if (d_off) cudaFreeAsync(d_off, st);
+    if (k_out) cudaFreeAsync(k_out, st);
+    if (v_out) cudaFreeAsync(v_out, st);
+    if (rc == GEE_OK && cudaStreamSynchronize(st) != cudaSuccess) {
+        gee::set_error("gee_sort_rows: sync failed");
+        rc = GEE_ERR_CUDA;
+    }
+    return rc;
 }
 
 }  // extern "C"

@@ -947,26 +947,36 @@ k_reduce_heavy(const int64_t *__restrict__ offsets, const int32_t *__restrict__ 
 // 64-bit column sums in registers.  An item that is its row's only item
 // writes the Z row itself; the items of longer (mega) rows meet in acc[m]
 // through 64-bit atomics and a small finalize.
-constexpr int HCOL = 8;  // columns per lane: k <= 256
+constexpr int HCOL = 8;   // columns per lane: k <= 256
+constexpr int HCOPY = 4;  // private window copies per warp (heavy items)
 
 template <bool WEIGHTED>
 __global__ void __launch_bounds__(RT)
 k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__restrict__ item_end,
                      const int32_t *__restrict__ item_row, const int32_t *__restrict__ item_slot, int64_t n_items,
                      const uint8_t *__restrict__ cls, const float *__restrict__ w, float qscale, double dscale,
-                     const double *__restrict__ inv, int32_t k, bool vec, unsigned long long *__restrict__ acc,
+                     const double *__restrict__ inv, int32_t k, int64_t arcs, unsigned long long *__restrict__ acc,
                      unsigned long long *__restrict__ counter, float *__restrict__ z)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int kk = k;
     const int pkb = block_vec_words(kk);  // [3 pad | trash | bins 1..k | pad]
+    constexpr int RSLOT = RING_CLS + (WEIGHTED ? RING_W : 0);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    float *sc1 = reinterpret_cast<float *>(smem_raw);  // sc1[c] = inv[c+1] * dscale
-    uint32_t *v = reinterpret_cast<uint32_t *>(sc1 + pkb) + wid * pkb * Acc<WEIGHTED>::planes;
+    uint8_t *ring = smem_raw + wid * RING * RSLOT;
+    float *sc1 = reinterpret_cast<float *>(smem_raw + RW * RING * RSLOT);  // sc1[c] = inv[c+1] * dscale
+    // HCOPY private copies of the window per warp (lane groups of 32/HCOPY):
+    // all lanes add into one row, so a single copy serialises on equal
+    // classes; the copy stride (== 4 mod 32 words) puts copies on other banks
+    const int cs = pkb * Acc<WEIGHTED>::planes + 4;
+    uint32_t *vw = reinterpret_cast<uint32_t *>(sc1 + pkb) + wid * HCOPY * cs;
+    uint32_t *v = vw + (lane / (32 / HCOPY)) * cs;
     for (int c = threadIdx.x; c < pkb; c += RT) sc1[c] = c < kk ? (float)(inv[c + 1] * dscale) : 0.f;
-    for (int i = lane; i < pkb * Acc<WEIGHTED>::planes; i += 32) v[i] = 0u;
+    for (int i = lane; i < HCOPY * cs; i += 32) vw[i] = 0u;
     __syncthreads();
-    // items come largest first; warps fetch them dynamically
+    // items come largest first; warps fetch them dynamically.  Rounds are
+    // 256-arc aligned, so each aligned BLOCK_ROW_MAX window holds whole
+    // rounds; RING rounds stay in flight (cp.async ring) within an item.
     for (;;) {
         int64_t it = 0;
         if (lane == 0) it = (int64_t)atomicAdd(counter, 1ull);
@@ -976,61 +986,70 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
         unsigned long long sum[HCOL];
 #pragma unroll
         for (int j = 0; j < HCOL; j++) sum[j] = 0ull;
-        // carry-free windows of at most BLOCK_ROW_MAX arcs, aligned in the
-        // arc array so every full window is exactly BLOCK_ROW_MAX/BROUND rounds
-        for (int64_t wb0 = b0; wb0 < e1;) {
-            const int64_t we = min((wb0 & ~(BLOCK_ROW_MAX - 1)) + BLOCK_ROW_MAX, e1);
-            int64_t e0 = wb0 & ~(int64_t)(BU - 1);
-            uint2 ca;
-            float wa[BU];
-            block_round<WEIGHTED>(cls, w, e0 + lane * BU, we, vec, ca, wa);
-            while (e0 < we) {
-                const int64_t en = e0 + BROUND;
-                uint2 cb = make_uint2(0u, 0u);
-                float wb[BU];
+        int64_t ep = b0 & ~(int64_t)(BROUND - 1);
 #pragma unroll
-                for (int u = 0; u < BU; u++) wb[u] = 0.f;
-                if (en < we) block_round<WEIGHTED>(cls, w, en + lane * BU, we, vec, cb, wb);
-                const int64_t a0 = e0 + lane * BU;
-#pragma unroll
-                for (int u = 0; u < BU; u++) {
-                    uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
-                    if (a0 + u < wb0 || a0 + u >= we) c = 0u;
-                    if (c == 0u) continue;
-                    uint32_t *p = v + 3 + c;
-                    if (WEIGHTED) {
-                        const unsigned long long qv = (unsigned long long)__float2ll_rn(wa[u] * qscale);
-                        atomicAdd(p, (uint32_t)qv & ((1u << BLOCK_SPLIT) - 1u));
-                        atomicAdd(p + pkb, (uint32_t)(qv >> BLOCK_SPLIT));
-                    } else {
-                        atomicAdd(p, 1u);
-                    }
-                }
-                ca = cb;
-#pragma unroll
-                for (int u = 0; u < BU; u++) wa[u] = wb[u];
-                e0 = en;
-            }
-            __syncwarp();
-            wb0 = we;
-#pragma unroll
-            for (int j = 0; j < HCOL; j++) {
-                const int c = lane + 32 * j;
-                if (c < kk) {
-                    uint32_t *p = v + 4 + c;
-                    unsigned long long t = *p;
-                    *p = 0u;
-                    if (WEIGHTED) {
-                        t += (unsigned long long)p[pkb] << BLOCK_SPLIT;
-                        p[pkb] = 0u;
-                    }
-                    sum[j] += t;
-                }
-            }
-            __syncwarp();
+        for (int i = 0; i < RING; i++) {
+            ring_issue<WEIGHTED>(ring, i, ep, e1, arcs, cls, w, lane);
+            ep += BROUND;
         }
-        const int32_t slot = item_slot[it];
-        if (slot < 0) {  // the row's only item: write its Z row
+        int slot = 0;
+        for (int64_t e0 = b0 & ~(int64_t)(BROUND - 1); e0 < e1; e0 += BROUND) {
+            cp_wait<RING - 1>();
+            const uint8_t *rs = ring + slot * RSLOT;
+            const uint2 ca = *reinterpret_cast<const uint2 *>(rs + lane * BU);
+            float wa[BU];
+            if (WEIGHTED) {
+                const float4 x0 = *reinterpret_cast<const float4 *>(rs + RING_CLS + lane * BU * 4);
+                const float4 x1 = *reinterpret_cast<const float4 *>(rs + RING_CLS + lane * BU * 4 + 16);
+                wa[0] = x0.x, wa[1] = x0.y, wa[2] = x0.z, wa[3] = x0.w;
+                wa[4] = x1.x, wa[5] = x1.y, wa[6] = x1.z, wa[7] = x1.w;
+            }
+            const int64_t a0 = e0 + lane * BU;
+            const bool full = a0 >= b0 && a0 + BU <= e1;
+#pragma unroll
+            for (int u = 0; u < BU; u++) {
+                uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
+                if (!full && (a0 + u < b0 || a0 + u >= e1)) c = 0u;
+                if (c == 0u) continue;
+                uint32_t *p = v + 3 + c;
+                if (WEIGHTED) {
+                    const unsigned long long qv = (unsigned long long)__float2ll_rn(wa[u] * qscale);
+                    atomicAdd(p, (uint32_t)qv & ((1u << BLOCK_SPLIT) - 1u));
+                    atomicAdd(p + pkb, (uint32_t)(qv >> BLOCK_SPLIT));
+                } else {
+                    atomicAdd(p, 1u);
+                }
+            }
+            ring_issue<WEIGHTED>(ring, slot, ep, e1, arcs, cls, w, lane);
+            ep += BROUND;
+            slot = slot + 1 == RING ? 0 : slot + 1;
+            // fold the window into the 64-bit sums at each aligned window end
+            const int64_t en = e0 + BROUND;
+            if ((en & (BLOCK_ROW_MAX - 1)) == 0 || en >= e1) {
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < HCOL; j++) {
+                    const int c = lane + 32 * j;
+                    if (c < kk) {
+#pragma unroll
+                        for (int q = 0; q < HCOPY; q++) {
+                            uint32_t *p = vw + q * cs + 4 + c;
+                            unsigned long long t = *p;
+                            *p = 0u;
+                            if (WEIGHTED) {
+                                t += (unsigned long long)p[pkb] << BLOCK_SPLIT;
+                                p[pkb] = 0u;
+                            }
+                            sum[j] += t;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        cp_wait<0>();
+        const int32_t slotm = item_slot[it];
+        if (slotm < 0) {  // the row's only item: write its Z row
             float *zr = z + (int64_t)item_row[it] * kk;
 #pragma unroll
             for (int j = 0; j < HCOL; j++) {
@@ -1041,7 +1060,7 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
 #pragma unroll
             for (int j = 0; j < HCOL; j++) {
                 const int c = lane + 32 * j;
-                if (c < kk && sum[j]) atomicAdd(&acc[(int64_t)slot * kk + c], sum[j]);
+                if (c < kk && sum[j]) atomicAdd(&acc[(int64_t)slotm * kk + c], sum[j]);
             }
         }
     }
@@ -1351,8 +1370,8 @@ heavy:
     return gee::check_launch("k_heavy_finalize");
 }
 
-int gee_reduce_heavy(const uint8_t *cls, const float *w, int32_t scale_exp, const double *inv, int32_t k,
-                     const int64_t *item_first, const int64_t *item_end, const int32_t *item_row,
+int gee_reduce_heavy(const uint8_t *cls, const float *w, int64_t arcs, int32_t scale_exp, const double *inv,
+                     int32_t k, const int64_t *item_first, const int64_t *item_end, const int32_t *item_row,
                      const int32_t *item_slot, int64_t n_items, const int32_t *mega_rows, int64_t n_mega,
                      void *mega_acc, int64_t *counter, float *z, void *stream)
 {
@@ -1368,19 +1387,25 @@ int gee_reduce_heavy(const uint8_t *cls, const float *w, int32_t scale_exp, cons
     const bool weighted = w != nullptr;
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
-    const size_t sh = (size_t)block_vec_words(k) * sizeof(float) +
-                      (size_t)RW * block_vec_words(k) * (weighted ? 2 : 1) * sizeof(uint32_t);
-    const bool vld = (reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0);
+    const size_t sh = (size_t)RW * RING * (RING_CLS + (weighted ? RING_W : 0)) +
+                      (size_t)block_vec_words(k) * sizeof(float) +
+                      (size_t)RW * HCOPY * (block_vec_words(k) * (weighted ? 2 : 1) + 4) * sizeof(uint32_t);
+    GEE_REQUIRE((reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0),
+                GEE_ERR_INVALID, "cls must be 8-byte and w 16-byte aligned");
     auto *acc = static_cast<unsigned long long *>(mega_acc);
     auto *ctr = reinterpret_cast<unsigned long long *>(counter);
     GEE_CUDA(cudaMemsetAsync(ctr, 0, sizeof(*ctr), st));
     const int hgrid = grid_for(n_items * 32, RT, 8);
     if (weighted)
+        GEE_CUDA(cudaFuncSetAttribute(k_reduce_heavy_items<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+    else
+        GEE_CUDA(cudaFuncSetAttribute(k_reduce_heavy_items<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+    if (weighted)
         k_reduce_heavy_items<true><<<hgrid, RT, sh, st>>>(item_first, item_end, item_row, item_slot, n_items, cls, w,
-                                                          qscale, dscale, inv, k, vld, acc, ctr, z);
+                                                          qscale, dscale, inv, k, arcs, acc, ctr, z);
     else
         k_reduce_heavy_items<false><<<hgrid, RT, sh, st>>>(item_first, item_end, item_row, item_slot, n_items, cls, w,
-                                                           qscale, dscale, inv, k, vld, acc, ctr, z);
+                                                           qscale, dscale, inv, k, arcs, acc, ctr, z);
     int rc;
     if ((rc = gee::check_launch("k_reduce_heavy_items"))) return rc;
     if (n_mega == 0) return GEE_OK;

@@ -75,6 +75,7 @@ class DeviceGraph:
         self.n_hot = 0
         self.hot_k = None  # k the hot tier was planned for (None = not planned)
         self._owns_targets = False
+        self._owns_weights = False
 
     # ---------------------------------------------------------------- build
     @classmethod
@@ -110,6 +111,8 @@ class DeviceGraph:
             g = cls(n, arcs // 2, dev)
             g.offsets, g.targets, g.weights = off_d, tgt_d, w_d
             g._owns_targets = not (isinstance(targets, torch.Tensor) and targets.data_ptr() == tgt_d.data_ptr())
+            g._owns_weights = w_d is not None and not (isinstance(weights, torch.Tensor) and
+                                                       weights.data_ptr() == w_d.data_ptr())
             g._plan()
             if keep_coo or not pull:
                 rows = torch.empty(arcs, dtype=torch.int32, device=dev)
@@ -135,6 +138,7 @@ class DeviceGraph:
                                 ptr(self.offsets), ptr(self.targets), ptr(self.weights), _stream()),
               "gee_build_csr")
         self._owns_targets = True
+        self._owns_weights = True
         self._plan()
 
     def _plan(self):
@@ -270,10 +274,9 @@ class DeviceGraph:
         self.hot_k = k
         if not enable or self.arcs == 0 or deg_off is None:
             self.global_offsets = None
+            self._sort_rows()
             return
-        if not self._owns_targets:
-            self.targets = self.targets.clone()
-            self._owns_targets = True
+        self._own_pull_arrays()
         n = self.n_nodes
         self.hot_rank = torch.empty(n, dtype=torch.int32, device=self.device)
         nh = ctypes.c_int64()
@@ -289,6 +292,30 @@ class DeviceGraph:
             return
         check(lib.gee_hot_encode(ptr(self.targets), self.arcs, ptr(self.hot_rank), self.n_hot, _stream()),
               "gee_hot_encode")
+        self._sort_rows()
+
+    SORT_ROWS = True
+
+    def _own_pull_arrays(self):
+        """Private copies of the pull targets / weights before they are
+        rewritten in place (hot encoding, row sort): never the caller's
+        tensors, never the push layout's."""
+        shared = lambda a, b: a is not None and b is not None and a.data_ptr() == b.data_ptr()  # noqa: E731
+        if not self._owns_targets or shared(self.targets, self.dst):
+            self.targets = self.targets.clone()
+            self._owns_targets = True
+        if self.weights is not None and (not self._owns_weights or shared(self.weights, self.w)):
+            self.weights = self.weights.clone()
+            self._owns_weights = True
+
+    def _sort_rows(self):
+        """Sort each row's arcs by label-table slot (graph preparation; the
+        pull's integer sums do not depend on arc order)."""
+        if not (self.SORT_ROWS and os.environ.get("GEE_SORT_ROWS", "1") != "0") or self.arcs == 0:
+            return
+        self._own_pull_arrays()
+        check(lib.gee_sort_rows(ptr(self.offsets), self.n, ptr(self.targets), ptr(self.weights), _stream()),
+              "gee_sort_rows")
 
     @property
     def arcs(self):
@@ -416,7 +443,7 @@ class Embedder:
                     self._mark("blocks", 1)
                     if g.n_mega and (self.mega_acc is None or self.mega_acc.numel() < g.n_mega * self.k):
                         self.mega_acc = torch.zeros(g.n_mega * self.k, dtype=torch.int64, device=self.device)
-                    check(lib.gee_reduce_heavy(ptr(self.cls), ptr(g.weights), g.scale_exp, ptr(self.inv64), self.k,
+                    check(lib.gee_reduce_heavy(ptr(self.cls), ptr(g.weights), g.arcs, g.scale_exp, ptr(self.inv64), self.k,
                                                ptr(g.item_first), ptr(g.item_end), ptr(g.item_row), ptr(g.item_slot),
                                                g.n_items, ptr(g.mega_rows), g.n_mega,
                                                ptr(self.mega_acc) if g.n_mega else None, ptr(self.counter), ptr(z),

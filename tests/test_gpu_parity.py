@@ -425,3 +425,26 @@ def test_host_pipeline_matches_resident_pull(chunks):
     assert torch.equal(h_z, z_ref)
     exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), w.cpu().numpy(), y.cpu().numpy(), n, k)
     assert rel_err(h_z.numpy(), exp) <= TOL
+
+
+def test_graph_prep_never_mutates_caller_or_push_arrays():
+    # hot encoding and the row sort rewrite the pull targets / weights in
+    # place: a caller's CUDA tensors and the push layout must keep theirs
+    n, k = 4000, 6
+    rng = np.random.default_rng(51)
+    el = gb.EdgeList(n=n, src=rng.integers(0, n, 30_000), dst=rng.integers(0, n, 30_000),
+                     w=(1.0 - rng.random(30_000)).astype(np.float32), directed=False)
+    csr = gb.build_csr(el)
+    dev = torch.device("cuda")
+    off, tgt, w = (torch.from_numpy(np.asarray(a)).to(dev) for a in (csr.offsets, csr.targets, csr.weights))
+    tgt0, w0 = tgt.clone(), w.clone()
+    g = DeviceGraph.from_csr(off, tgt, w, n, symmetric=True, device=dev, pull=True, keep_coo=True)
+    g.prepare_hot(k, enable=True)
+    assert torch.equal(tgt, tgt0) and torch.equal(w, w0)
+    assert torch.equal(g.dst, tgt0) and torch.equal(g.w, w0)
+    y = gb.random_labels(n, k, 0.8, seed=52)
+    yd = torch.from_numpy(y.labels).to(dev)
+    emb = Embedder(n, k, dev)
+    zp = emb.embed(g, yd, variant="pull").cpu().numpy()
+    zq = emb.embed(g, yd, variant="push").cpu().numpy()
+    assert rel_err(zp, zq.astype(np.float64)) <= TOL
