@@ -390,13 +390,20 @@ __device__ __forceinline__ void block_round_acc(uint32_t *__restrict__ vw, const
         incl += lane >= st ? t : 0;
     }
     int r = __popc(startm) + incl - pc;  // owner rank + 1 before this lane's first arc
+    // arcs past the block end get class 0 (masked), once per round
     const int nvalid = lend - (lr + lane * BU);
+    uint2 cm = ca;
+    if (nvalid < BU) {
+        const uint32_t nv = nvalid <= 0 ? 0u : (uint32_t)nvalid;
+        cm.x &= nv >= 4 ? 0xffffffffu : ((1u << (8 * nv)) - 1u);
+        cm.y &= nv >= 8 ? 0xffffffffu : (nv <= 4 ? 0u : ((1u << (8 * (nv - 4))) - 1u));
+    }
 #pragma unroll
     for (int u = 0; u < BU; u++) {
         r += (mb >> u) & 1u;
-        const uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
+        const uint32_t c = __byte_perm(u < 4 ? cm.x : cm.y, 0u, 0x4440 + (u & 3));
         const int so = s_soff[r];
-        const int idx = (c != 0u && u < nvalid && so >= 0) ? so + (int)c : trash;
+        const int idx = (c != 0u && so >= 0) ? so + (int)c : trash;
         if (WEIGHTED) {
             // carry-free split q = A * 2^21 + B: both plane sums stay below
             // 2^32 (rows <= BLOCK_ROW_MAX arcs, q < 2^42), so neither add
@@ -674,16 +681,25 @@ __device__ __forceinline__ void ring_issue(uint8_t *ring, int slot, int64_t e, i
 {
     if (e < bend) {
         const int64_t a = e + lane * BU;
-        const int64_t left = arcs - a;
-        const uint32_t nc = left <= 0 ? 0u : (left >= BU ? (uint32_t)BU : (uint32_t)left);
         uint8_t *rs = ring + slot * (RING_CLS + (WEIGHTED ? RING_W : 0));
-        cp_async8(smem_u32(rs + lane * BU), nc ? (const void *)(cls + a) : (const void *)cls, nc);
-        if (WEIGHTED) {
-            const uint32_t n0 = nc >= 4 ? 16u : nc * 4u;
-            const uint32_t n1 = nc > 4 ? (nc - 4) * 4u : 0u;
-            uint8_t *rw = rs + RING_CLS + lane * BU * 4;
-            cp_async16(smem_u32(rw), n0 ? (const void *)(w + a) : (const void *)w, n0);
-            cp_async16(smem_u32(rw + 16), n1 ? (const void *)(w + a + 4) : (const void *)w, n1);
+        const uint32_t dc = smem_u32(rs + lane * BU);
+        const uint32_t dw = smem_u32(rs + RING_CLS + lane * BU * 4);
+        if (e + BROUND <= arcs) {  // whole round inside the arrays (warp-uniform)
+            cp_async8(dc, cls + a, BU);
+            if (WEIGHTED) {
+                cp_async16(dw, w + a, 16u);
+                cp_async16(dw + 16, w + a + 4, 16u);
+            }
+        } else {
+            const int64_t left = arcs - a;
+            const uint32_t nc = left <= 0 ? 0u : (left >= BU ? (uint32_t)BU : (uint32_t)left);
+            cp_async8(dc, nc ? (const void *)(cls + a) : (const void *)cls, nc);
+            if (WEIGHTED) {
+                const uint32_t n0 = nc >= 4 ? 16u : nc * 4u;
+                const uint32_t n1 = nc > 4 ? (nc - 4) * 4u : 0u;
+                cp_async16(dw, n0 ? (const void *)(w + a) : (const void *)w, n0);
+                cp_async16(dw + 16, n1 ? (const void *)(w + a + 4) : (const void *)w, n1);
+            }
         }
     }
     cp_commit();

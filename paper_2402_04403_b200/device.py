@@ -254,10 +254,11 @@ class DeviceGraph:
     # outgrows what L2 keeps resident under random access and degrees are
     # skewed (R-MAT); ER graphs end up with few or no hot vertices.
     HOT_MIN_TABLE_BYTES = 16 << 20
-    # rank every vertex with an arc (degree >= 1), up to 64M: the whole table
-    # is then popularity-ordered and L2 keeps its used lines (C4: lookup DRAM
-    # reads 25.6 -> 18.5 GB per pass)
-    HOT_MAX = 64 << 20
+    # the top 16M vertices by degree: with rows sorted by slot, ranking more
+    # (up to all 60M with an arc) trims the lookups' DRAM reads but the
+    # histogram's rank scatter grows more (C4 step: 16M 21.32 ms, 32M 21.39,
+    # 64M 21.53)
+    HOT_MAX = 16 << 20
     HOT_MIN_DEGREE = 1
 
     def prepare_hot(self, k, enable=None):
