@@ -365,9 +365,9 @@ def main():
     # algorithmic bytes per launch of each phase (SURVEY.md section 8(d)
     # per-unit figures x the units one launch processes)
     weighted = g.weighted
-    arcs = g.arcs
+    arcs = g.arcs_unpadded or g.arcs  # algorithmic: the real arcs (row padding is our overhead)
     heavy_arcs = g.heavy_arc_total
-    light_arcs = arcs - heavy_arcs
+    light_arcs = g.arcs - heavy_arcs - (g.arcs - arcs)
     heavy_rows = g.n_heavy
     lb = 1 if k <= 255 else (2 if k <= 65535 else 4)
     phase_bytes = {
@@ -399,6 +399,7 @@ def main():
         "data": "synthetic (seeded R-MAT; Friendster unavailable)",
         "config": {"workload": workload, "n": n, "s_listed_edges": s, "k": k, "weighted": bool(weighted),
                    "directed": bool(directed), "variant": "pull", "reducer": emb.reducer, "sym_arcs": arcs,
+                   "padded_arcs": g.arcs, "row_pad": g.padded,
                    "parallelism": f"row-range x{world}" if world > 1 else "single GPU",
                    "l2": "inputs (CSR %.1f GB) >> 126 MB L2; no flush needed" % (g.csr_bytes() / 1e9),
                    "gen_s": round(t_gen, 3), "prep_s": round(t_prep, 3), "hot_prep_s": round(t_hot, 3),

@@ -141,6 +141,17 @@ int gee_csr_rows(const int64_t *offsets, int64_t n, int64_t arcs, int32_t *rows,
  * consecutive label lookups share sectors.  Allocates scratch; blocks. */
 int gee_sort_rows(const int64_t *offsets, int64_t n, int32_t *targets, float *w, void *stream);
 
+/* Graph preparation: pad every row to a multiple of `align` arcs with
+ * (sentinel slot, weight 0) arcs.  The sentinel slot's label is 0
+ * (unlabeled: gee_build_projection writes it), so pads add nothing.  With
+ * align = 8 every lane of the block reducer owns arcs of a single row.
+ * gee_pad_offsets writes the padded offsets and returns the padded arc
+ * count (blocks); gee_pad_rows copies the arcs. */
+int gee_pad_offsets(const int64_t *offsets, int64_t n, int64_t align, int64_t *padded_offsets,
+                    int64_t *padded_arcs, void *stream);
+int gee_pad_rows(const int64_t *offsets, const int64_t *padded_offsets, int64_t n, const int32_t *targets,
+                 const float *w, int32_t sentinel, int32_t *padded_targets, float *padded_w, void *stream);
+
 /* Graph statistics that size the pull accumulator (host outputs):
  * max over rows of sum |w| (or max degree if w NULL), min nonzero |w|,
  * max |w|, and whether any weight is non-finite. */
@@ -244,6 +255,12 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
                       const int32_t *heavy_rows, int64_t n_heavy, const int64_t *chunk_first,
                       const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
                       void *stream);
+
+/* gee_reduce_blocks for PADDED rows (gee_pad_rows, align 8): light rows
+ * only (heavy rows are left to gee_reduce_heavy). */
+int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
+                           int32_t scale_exp, const double *inv, int32_t k, int64_t heavy_arcs, float *z,
+                           void *stream);
 
 /* Heavy rows (longer than the block reducer's heavy_arcs) as work items:
  * item i covers arcs [item_first[i], item_end[i]) of row item_row[i]

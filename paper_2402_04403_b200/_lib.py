@@ -66,7 +66,10 @@ SIGNATURES = {
     "gee_gather_labels": (c_int, [vp, c_i64, vp, c_i64, c_i32, vp, vp]),
     "gee_reduce_heavy_plan": (c_int, [vp, c_i64, c_i64, vp, ctypes.POINTER(c_i64), vp]),
     "gee_reduce_blocks": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, c_i64, vp, vp, c_i64, vp, vp, vp]),
+    "gee_pad_offsets": (c_int, [vp, c_i64, c_i64, vp, vp, vp]),
+    "gee_pad_rows": (c_int, [vp, vp, c_i64, vp, vp, c_i32, vp, vp, vp]),
     "gee_sort_rows": (c_int, [vp, c_i64, vp, vp, vp]),
+    "gee_reduce_blocks_pad8": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, vp]),
     "gee_reduce_heavy": (c_int, [vp, vp, c_i64, c_i32, vp, c_i32, vp, vp, vp, vp, c_i64, vp, c_i64, vp, vp, vp, vp]),
     "gee_block_scale_exp": (c_int, [c_dbl, c_dbl, c_dbl, P_i32, P_dbl]),
     "gee_reduce_bins": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), vp]),

@@ -217,6 +217,35 @@ __global__ void k_rebase(const int64_t *__restrict__ offsets, int64_t r0, int64_
         out[i] = (int32_t)(offsets[r0 + i] - base);
 }
 
+// padded offsets: pout[r+1] = round_up(offsets[r+1] - offsets[r], align)
+__global__ void k_pad_degrees(const int64_t *__restrict__ offsets, int64_t n, int64_t align, int64_t *__restrict__ pout)
+{
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = offsets[r + 1] - offsets[r];
+        pout[r + 1] = (d + align - 1) / align * align;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) pout[0] = 0;
+}
+
+// one warp per row: copy its arcs, then fill the pad with (sentinel, 0)
+__global__ void k_pad_copy(const int64_t *__restrict__ offsets, const int64_t *__restrict__ poff, int64_t n,
+                           const int32_t *__restrict__ tin, const float *__restrict__ win, int32_t sentinel,
+                           int32_t *__restrict__ tout, float *__restrict__ wout)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = gw; r < n; r += GW) {
+        const int64_t a0 = offsets[r], d = offsets[r + 1] - a0;
+        const int64_t b0 = poff[r], pd = poff[r + 1] - b0;
+        for (int64_t j = lane; j < pd; j += 32) {
+            const bool in = j < d;
+            tout[b0 + j] = in ? tin[a0 + j] : sentinel;
+            if (wout) wout[b0 + j] = in ? win[a0 + j] : 0.f;
+        }
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -505,6 +534,48 @@ out:
         rc = GEE_ERR_CUDA;
     }
     return rc;
+}
+
+int gee_pad_offsets(const int64_t *offsets, int64_t n, int64_t align, int64_t *padded_offsets, int64_t *padded_arcs,
+                    void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(n >= 0 && align >= 1, GEE_ERR_INVALID, "bad n / align");
+    GEE_REQUIRE(offsets && padded_offsets && padded_arcs, GEE_ERR_INVALID, "NULL argument");
+    cudaStream_t st = gee::as_stream(stream);
+    *padded_arcs = 0;
+    if (n == 0) {
+        GEE_CUDA(cudaMemsetAsync(padded_offsets, 0, sizeof(int64_t), st));
+        return GEE_OK;
+    }
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)gee::sm_count() * 16);
+    k_pad_degrees<<<grid, 256, 0, st>>>(offsets, n, align, padded_offsets);
+    int rc;
+    if ((rc = gee::check_launch("k_pad_degrees"))) return rc;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, padded_offsets + 1, padded_offsets + 1, n, st);
+    GEE_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, padded_offsets + 1, padded_offsets + 1, n, st);
+    cudaFreeAsync(tmp, st);
+    if ((rc = gee::check_launch("DeviceScan::InclusiveSum"))) return rc;
+    GEE_CUDA(cudaMemcpyAsync(padded_arcs, padded_offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GEE_CUDA(cudaStreamSynchronize(st));
+    return GEE_OK;
+}
+
+int gee_pad_rows(const int64_t *offsets, const int64_t *padded_offsets, int64_t n, const int32_t *targets,
+                 const float *w, int32_t sentinel, int32_t *padded_targets, float *padded_w, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(n >= 0, GEE_ERR_INVALID, "n must be nonnegative");
+    if (n == 0) return GEE_OK;
+    GEE_REQUIRE(offsets && padded_offsets && targets && padded_targets && (!w || padded_w), GEE_ERR_INVALID,
+                "NULL array argument");
+    const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, (int64_t)gee::sm_count() * 16);
+    k_pad_copy<<<grid, 256, 0, gee::as_stream(stream)>>>(offsets, padded_offsets, n, targets, w, sentinel,
+                                                         padded_targets, w ? padded_w : nullptr);
+    return gee::check_launch("k_pad_copy");
 }
 
 }  // extern "C"

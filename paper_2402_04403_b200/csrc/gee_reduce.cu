@@ -417,6 +417,36 @@ __device__ __forceinline__ void block_round_acc(uint32_t *__restrict__ vw, const
     }
 }
 
+// One round over PADDED rows (every row's arc run is a multiple of BU, so
+// each lane's 8 arcs belong to one row): the lane's owner rank is the count
+// of rows started before the round plus the row starts at lane chunks <= its
+// own -- one ballot, one OR-reduction, two popcounts, no shared masks.
+template <bool WEIGHTED>
+__device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const int32_t *__restrict__ s_soff, int lane,
+                                                bool owner, int32_t ol, int32_t lr, int32_t lend, int hoff, int trash,
+                                                float qscale, const uint2 &ca, const float (&wa)[BU])
+{
+    const unsigned startm = __ballot_sync(0xffffffffu, owner && ol <= lr);
+    const int32_t pos = ol - lr;
+    const unsigned m = __reduce_or_sync(0xffffffffu, (owner && pos > 0 && pos < BROUND) ? 1u << (pos >> 3) : 0u);
+    const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+    const int r = __popc(startm) + __popc(m & upto);  // owner rank + 1 (0: before the block)
+    const int so = s_soff[r];
+    const bool ok = so >= 0 && lr + lane * BU < lend;
+#pragma unroll
+    for (int u = 0; u < BU; u++) {
+        const uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
+        const int idx = (ok && c != 0u) ? so + (int)c : trash;
+        if (WEIGHTED) {
+            const unsigned long long q = (unsigned long long)__float2ll_rn(wa[u] * qscale);
+            atomicAdd(vw + idx, (uint32_t)q & ((1u << BLOCK_SPLIT) - 1u));
+            atomicAdd(vw + hoff + idx, (uint32_t)(q >> BLOCK_SPLIT));
+        } else {
+            atomicAdd(vw + idx, 1u);
+        }
+    }
+}
+
 template <bool WEIGHTED>
 __global__ void __launch_bounds__(RT, BLOCKS_MINB)
 k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
@@ -705,7 +735,7 @@ __device__ __forceinline__ void ring_issue(uint8_t *ring, int slot, int64_t e, i
     cp_commit();
 }
 
-template <bool WEIGHTED>
+template <bool WEIGHTED, bool PAD>
 __global__ void __launch_bounds__(RT, 2)
 k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
                      const float *__restrict__ w, float qscale, double dscale, const double *__restrict__ inv,
@@ -804,9 +834,14 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
 #pragma unroll
                     for (int u = 0; u < BU; u++) wa[u] = 1.f;
                 }
-                if (nnz > 0)
-                    block_round_acc<WEIGHTED>(vw, s_soff, s_mask, rot, lane, owner, B.ol, (int32_t)(ec - B.base), lend,
-                                              hoff, trash, qscale, ca, wa);
+                if (nnz > 0) {
+                    if (PAD)
+                        block_round_pad<WEIGHTED>(vw, s_soff, lane, owner, B.ol, (int32_t)(ec - B.base), lend, hoff,
+                                                  trash, qscale, ca, wa);
+                    else
+                        block_round_acc<WEIGHTED>(vw, s_soff, s_mask, rot, lane, owner, B.ol, (int32_t)(ec - B.base),
+                                                  lend, hoff, trash, qscale, ca, wa);
+                }
                 __syncwarp();
                 // refill the slot just consumed with the round RING ahead
                 ring_issue<WEIGHTED>(ring, slot, ep, B.bend, arcs, cls, w, lane);
@@ -1296,10 +1331,31 @@ int gee_reduce_lists(const int64_t *offsets, const int32_t *small_rows, int64_t 
     return gee::check_launch("k_heavy_finalize");
 }
 
+static int reduce_blocks_impl(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
+                              const double *inv, int32_t k, int64_t heavy_arcs, const int32_t *heavy_rows,
+                              int64_t n_heavy, const int64_t *chunk_first, const int32_t *chunk_heavy,
+                              int64_t n_chunks, void *heavy_acc, float *z, void *stream, bool pad);
+
 int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
                       const double *inv, int32_t k, int64_t heavy_arcs, const int32_t *heavy_rows, int64_t n_heavy,
                       const int64_t *chunk_first, const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc,
                       float *z, void *stream)
+{
+    return reduce_blocks_impl(offsets, n, cls, w, scale_exp, inv, k, heavy_arcs, heavy_rows, n_heavy, chunk_first,
+                              chunk_heavy, n_chunks, heavy_acc, z, stream, false);
+}
+
+int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
+                           const double *inv, int32_t k, int64_t heavy_arcs, float *z, void *stream)
+{
+    return reduce_blocks_impl(offsets, n, cls, w, scale_exp, inv, k, heavy_arcs, nullptr, 0, nullptr, nullptr, 0,
+                              nullptr, z, stream, true);
+}
+
+static int reduce_blocks_impl(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
+                              const double *inv, int32_t k, int64_t heavy_arcs, const int32_t *heavy_rows,
+                              int64_t n_heavy, const int64_t *chunk_first, const int32_t *chunk_heavy,
+                              int64_t n_chunks, void *heavy_acc, float *z, void *stream, bool pad)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs 1 <= k <= 255 (got %d)", k);
@@ -1334,7 +1390,8 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
     const int grid = grid_for(nblocks * 32, RT, 8);
     int rc;
     const char *ringenv = getenv("GEE_BLOCKS_RING");
-    if (!ringenv || atoi(ringenv) != 0) {
+    GEE_REQUIRE(!pad || !ringenv || atoi(ringenv) != 0, GEE_ERR_INVALID, "padded rows need the ring reducer");
+    if (pad || !ringenv || atoi(ringenv) != 0) {
         // ring variant: RING rounds per warp in shared memory, 2 CTAs per SM
         const size_t ring = (size_t)RW * RING * (RING_CLS + (weighted ? RING_W : 0));
         const size_t budget2 = (size_t)(gee::smem_per_sm() / 2) - 1024;
@@ -1343,17 +1400,10 @@ int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, con
         if (ns >= 4) {
             const size_t shr = ring + fixed + (size_t)RW * ns * vecb;
             const int rgrid = (int)std::min<int64_t>((nblocks + RW - 1) / RW, (int64_t)gee::sm_count() * 2);
-            if (weighted) {
-                GEE_CUDA(cudaFuncSetAttribute(k_reduce_blocks_ring<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)shr));
-                k_reduce_blocks_ring<true><<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k,
-                                                                  heavy_arcs, ns, z);
-            } else {
-                GEE_CUDA(cudaFuncSetAttribute(k_reduce_blocks_ring<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)shr));
-                k_reduce_blocks_ring<false><<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k,
-                                                                   heavy_arcs, ns, z);
-            }
+            auto kern = weighted ? (pad ? k_reduce_blocks_ring<true, true> : k_reduce_blocks_ring<true, false>)
+                                 : (pad ? k_reduce_blocks_ring<false, true> : k_reduce_blocks_ring<false, false>);
+            GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shr));
+            kern<<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, ns, z);
             if ((rc = gee::check_launch("k_reduce_blocks_ring"))) return rc;
             goto heavy;
         }

@@ -76,6 +76,8 @@ class DeviceGraph:
         self.hot_k = None  # k the hot tier was planned for (None = not planned)
         self._owns_targets = False
         self._owns_weights = False
+        self.padded = 0  # rows padded to a multiple of this many arcs (0: not padded)
+        self.arcs_unpadded = None
 
     # ---------------------------------------------------------------- build
     @classmethod
@@ -276,6 +278,7 @@ class DeviceGraph:
         if not enable or self.arcs == 0 or deg_off is None:
             self.global_offsets = None
             self._sort_rows()
+            self._pad_rows()
             return
         self._own_pull_arrays()
         n = self.n_nodes
@@ -294,8 +297,33 @@ class DeviceGraph:
         check(lib.gee_hot_encode(ptr(self.targets), self.arcs, ptr(self.hot_rank), self.n_hot, _stream()),
               "gee_hot_encode")
         self._sort_rows()
+        self._pad_rows()
 
     SORT_ROWS = True
+    PAD_ROWS = 8  # pad every row to a multiple of 8 arcs (0: off)
+
+    def _pad_rows(self):
+        """Pad each row's arc run to a multiple of PAD_ROWS with (sentinel
+        slot, weight 0) arcs (graph preparation): every lane of the block
+        reducer then owns arcs of one row.  The sentinel slot's label is 0."""
+        align = int(os.environ.get("GEE_PAD_ROWS", self.PAD_ROWS))
+        if align <= 1 or self.arcs == 0 or self.padded:
+            return
+        poff = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
+        pa = ctypes.c_int64()
+        check(lib.gee_pad_offsets(ptr(self.offsets), self.n, align, ptr(poff), ctypes.byref(pa), _stream()),
+              "gee_pad_offsets")
+        pa = int(pa.value)
+        tgt = torch.empty(pa, dtype=torch.int32, device=self.device)
+        wts = torch.empty(pa, dtype=torch.float32, device=self.device) if self.weights is not None else None
+        sentinel = self.n_hot + self.n_nodes
+        check(lib.gee_pad_rows(ptr(self.offsets), ptr(poff), self.n, ptr(self.targets), ptr(self.weights), sentinel,
+                               ptr(tgt), ptr(wts), _stream()), "gee_pad_rows")
+        self.arcs_unpadded = self.arcs
+        self.offsets, self.targets, self.weights = poff, tgt, wts
+        self._owns_targets = self._owns_weights = True
+        self.padded = align
+        self._plan()
 
     def _own_pull_arrays(self):
         """Private copies of the pull targets / weights before they are
@@ -438,13 +466,19 @@ class Embedder:
                 heavy = (g.HEAVY_ARCS, ptr(g.heavy_rows), g.n_heavy, ptr(g.chunk_first), ptr(g.chunk_heavy),
                          g.n_chunks, ptr(self.heavy_acc) if g.n_heavy else None, ptr(z), _stream())
                 if reducer == "blocks":
-                    check(lib.gee_reduce_blocks(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                                ptr(self.inv64), self.k, g.HEAVY_ARCS, None, 0, None, None, 0, None,
-                                                ptr(z), _stream()), "gee_reduce_blocks")
+                    if g.padded == 8:
+                        check(lib.gee_reduce_blocks_pad8(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights),
+                                                         g.scale_exp, ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(z),
+                                                         _stream()), "gee_reduce_blocks_pad8")
+                    else:
+                        check(lib.gee_reduce_blocks(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                                    ptr(self.inv64), self.k, g.HEAVY_ARCS, None, 0, None, None, 0,
+                                                    None, ptr(z), _stream()), "gee_reduce_blocks")
                     self._mark("blocks", 1)
                     if g.n_mega and (self.mega_acc is None or self.mega_acc.numel() < g.n_mega * self.k):
                         self.mega_acc = torch.zeros(g.n_mega * self.k, dtype=torch.int64, device=self.device)
-                    check(lib.gee_reduce_heavy(ptr(self.cls), ptr(g.weights), g.arcs, g.scale_exp, ptr(self.inv64), self.k,
+                    check(lib.gee_reduce_heavy(ptr(self.cls), ptr(g.weights), g.arcs, g.scale_exp, ptr(self.inv64),
+                                               self.k,
                                                ptr(g.item_first), ptr(g.item_end), ptr(g.item_row), ptr(g.item_slot),
                                                g.n_items, ptr(g.mega_rows), g.n_mega,
                                                ptr(self.mega_acc) if g.n_mega else None, ptr(self.counter), ptr(z),

@@ -68,6 +68,7 @@ class HostPipeline:
             v.max_block_arcs = int((ends[1:] - ends[:-1]).max().item()) if v.n else 0
             v.scale_exp, v.rel_err, v.max_row_abs = g.scale_exp, g.rel_err, g.max_row_abs
             v.hot_k, v.n_hot, v.hot_rank = k, g.n_hot, None
+            v.padded = g.padded
             v.offsets = v.targets = None
             v.span = (lo, hi, a0, a1)
             self.views.append(v)
