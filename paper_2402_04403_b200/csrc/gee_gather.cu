@@ -105,8 +105,8 @@ k_gather_contig(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
 {
     const uint64_t pol = gee::policy_evict_last();
     const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (GTHREADS / 32);
-    const int64_t gw = (int64_t)blockIdx.x * (GTHREADS / 32) + (threadIdx.x >> 5);
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int64_t steps = arcs / 512;
     for (int64_t st = gw; st < steps; st += warps) {
         const int32_t *tp = targets + st * 512 + lane;
@@ -158,8 +158,12 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
     if (const char *e = getenv("GEE_GATHER_MODE")) mode = atoi(e);
     if (mode >= 4) {  // lane-contiguous lookups (rows sorted by slot)
         auto kc = mode == 5 ? k_gather_contig<1> : k_gather_contig<0>;
-        kc<<<gee::sm_count(), GTHREADS, 0, gee::as_stream(stream)>>>(targets, arcs, static_cast<const uint8_t *>(table),
-                                                                     cls);
+        // GEE_GATHER_BLOCK / GEE_GATHER_CTAS (per SM): co-residency experiments
+        int bt = GTHREADS, per = 1;
+        if (const char *e = getenv("GEE_GATHER_BLOCK")) bt = atoi(e);
+        if (const char *e = getenv("GEE_GATHER_CTAS")) per = atoi(e);
+        kc<<<gee::sm_count() * per, bt, 0, gee::as_stream(stream)>>>(targets, arcs,
+                                                                     static_cast<const uint8_t *>(table), cls);
         return gee::check_launch("k_gather_contig");
     }
     const size_t sh = (size_t)hot0 + 16;

@@ -436,6 +436,9 @@ __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const
 #pragma unroll
     for (int u = 0; u < BU; u++) {
         const uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
+        // masked arcs (pads, unlabeled, other passes, past the block) add into
+        // the lane's trash word: branch-free (predicating the atomics off
+        // measured slower: 8.20 vs 8.01 ms on C4)
         const int idx = (ok && c != 0u) ? so + (int)c : trash;
         if (WEIGHTED) {
             const unsigned long long q = (unsigned long long)__float2ll_rn(wa[u] * qscale);
@@ -443,6 +446,43 @@ __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const
             atomicAdd(vw + hoff + idx, (uint32_t)(q >> BLOCK_SPLIT));
         } else {
             atomicAdd(vw + idx, 1u);
+        }
+    }
+}
+
+// A padded row of exactly one 8-arc chunk (<= 8 real arcs) is reduced by the
+// lane that owns it, in registers: equal classes combine exactly (integer
+// sums, as in the window), and only the nonzero entries are stored into the
+// zero-filled Z row.
+template <bool WEIGHTED>
+__device__ __forceinline__ void single_row(const uint8_t *__restrict__ cls, const float *__restrict__ w, int64_t a,
+                                           float qscale, const float *__restrict__ sc1, float *__restrict__ zr)
+{
+    const uint2 c8 = *reinterpret_cast<const uint2 *>(cls + a);
+    uint32_t c[BU];
+    unsigned long long q[BU];
+    float wv[BU];
+    if (WEIGHTED) {
+        const float4 x0 = *reinterpret_cast<const float4 *>(w + a);
+        const float4 x1 = *reinterpret_cast<const float4 *>(w + a + 4);
+        wv[0] = x0.x, wv[1] = x0.y, wv[2] = x0.z, wv[3] = x0.w;
+        wv[4] = x1.x, wv[5] = x1.y, wv[6] = x1.z, wv[7] = x1.w;
+    }
+#pragma unroll
+    for (int u = 0; u < BU; u++) {
+        c[u] = __byte_perm(u < 4 ? c8.x : c8.y, 0u, 0x4440 + (u & 3));
+        q[u] = WEIGHTED ? (unsigned long long)__float2ll_rn(wv[u] * qscale) : 1ull;
+    }
+#pragma unroll
+    for (int u = 0; u < BU; u++) {
+        bool first = c[u] != 0u;
+#pragma unroll
+        for (int v = 0; v < u; v++) first = first && c[v] != c[u];
+        if (first) {
+            unsigned long long sum = q[u];
+#pragma unroll
+            for (int v = u + 1; v < BU; v++) sum += c[v] == c[u] ? q[v] : 0ull;
+            zr[c[u] - 1] = (WEIGHTED ? (float)(long long)sum : (float)sum) * sc1[c[u] - 1];
         }
     }
 }
@@ -645,6 +685,12 @@ k_reduce_blocks(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *_
 // previous block is written out.  Each lane copies and consumes the same 8
 // arcs of a round, so cp.async.wait_group alone orders them.
 constexpr int RING = 4;
+// Single-chunk rows reduced in registers after the block (single_row):
+// measured slower on C4 (9.09 vs 8.01 ms: each block then waits on the L2
+// reloads of its short rows), so off.
+#ifndef BLOCK_SINGLE_ROWS
+#define BLOCK_SINGLE_ROWS 0
+#endif
 constexpr int RING_CLS = BROUND;                        // bytes per round
 constexpr int RING_W = BROUND * (int)sizeof(float);     // bytes per round (weighted)
 
@@ -795,15 +841,20 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         const int64_t nr0 = 32 * (b + GW);
         const int64_t o_lo_n = more ? __ldcs(offsets + min(nr0 + lane, n)) : 0;
         const int64_t o_31_n = (more && lane == 31) ? __ldcs(offsets + min(nr0 + 32, n)) : 0;
-        const int rank = __popc(B.nzm & below);
+        // PAD: single-chunk rows (padded length BU) go to single_row, not to
+        // the window
+        const unsigned singlem =
+            (PAD && BLOCK_SINGLE_ROWS) ? __ballot_sync(0xffffffffu, ((B.nzm >> lane) & 1u) && B.oh - B.ol == BU) : 0u;
+        const unsigned winm = B.nzm & ~singlem;
+        const int rank = __popc(winm & below);
         const int orank = __popc(B.anym & below);
-        const int nnz = __popc(B.nzm);
+        const int nnz = __popc(winm);
         const bool owner = (B.anym >> lane) & 1u;
-        const bool nz = (B.nzm >> lane) & 1u;
+        const bool nz = (winm >> lane) & 1u;
         const int32_t lend = (int32_t)(B.bend - B.base);
         const int rows = (int)min((int64_t)32, n - r0);
         float *zb = z + r0 * (int64_t)kk;
-        if (B.anym != B.vm) {  // the block holds empty rows: zero-fill its Z range
+        if ((winm | B.hvm) != B.vm) {  // empty or single rows: zero-fill the block's Z range
             const int total = rows * kk;
             const int q4 = total >> 2;
             float4 *z4 = reinterpret_cast<float4 *>(zb);
@@ -912,6 +963,11 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
                 }
             }
             __syncwarp();
+        }
+        if (PAD && singlem) {
+            __syncwarp();  // the zero fill lands before the single rows' entries
+            if ((singlem >> lane) & 1u)
+                single_row<WEIGHTED>(cls, w, B.base + B.ol, qscale, sc1, zb + (int64_t)lane * kk);
         }
         if (!more) break;
         B = opened ? NB : ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
