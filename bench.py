@@ -378,8 +378,8 @@ def main():
     }
     peak_gbs, peak_kind = load_peaks()
     dominant = max((p for p in phase_ms if p in phase_bytes), key=lambda p: phase_ms[p])
-    kernel_of = {"project": "k_label_hist", "gather": "k_gather", "blocks": "k_reduce_blocks",
-                 "heavy": "k_reduce_heavy"}
+    kernel_of = {"project": "k_label_hist", "gather": "k_gather_contig", "blocks": "k_reduce_blocks_ring",
+                 "heavy": "k_reduce_heavy_items"}
     achieved = phase_bytes[dominant] / (phase_ms[dominant] * 1e-3) / 1e9
     step_bmin = s * (8 + 4 * weighted) + 4 * n + 4 * n * k  # SURVEY 8(d) B_min, whole graph
     workload = cfg.name if not (args.scale or args.edges) else f"{cfg.name}-reduced(scale={args.scale},s={s})"
