@@ -158,8 +158,17 @@ def dist_setup(n_gpus):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # GEE_BENCH_BACKEND=gloo: a code-path check of the multi-rank bench on
+        # a box with fewer GPUs than ranks (ranks share devices; nothing in
+        # the timed region waits on another rank).  Timing runs use NCCL.
+        backend = os.environ.get("GEE_BENCH_BACKEND", "nccl")
+        dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+        local = dev
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
@@ -170,7 +179,10 @@ def barrier(world):
         import torch
         import torch.distributed as dist
 
-        dist.barrier(device_ids=[torch.cuda.current_device()])
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[torch.cuda.current_device()])
+        else:
+            dist.barrier()
 
 
 def max_over_ranks(x, world):
@@ -179,8 +191,19 @@ def max_over_ranks(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
 
@@ -286,7 +309,7 @@ def build_shard(args, world, rank):
         g = DeviceGraph.from_edges(src, dst, w, n, pull=True, keep_coo=not args.no_push)
         row_lo, row_hi = 0, n
     else:
-        g, row_lo, row_hi = shard_mod.build_row_shard(src, dst, w, n, world, rank)
+        g, row_lo, row_hi = shard_mod.build_row_shard(src, dst, w, n, world, rank, k=k)
         del src, dst, w
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t0
@@ -435,9 +458,9 @@ def main():
         g.src = g.dst = g.w = None
         torch.cuda.empty_cache()
 
-    # ---- e2e through host buffers
-    if not args.no_e2e and world == 1:
-        result["e2e"] = run_e2e(g, y, emb, z, s, args)
+    # ---- e2e through host buffers (every rank streams its own rows)
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(g, y, emb, z, s, args, world)
 
     # ---- CPU baseline (rank 0, N=1 only)
     if not args.no_cpu and world == 1 and rank == 0:
@@ -459,7 +482,7 @@ def main():
     return 0
 
 
-def run_e2e(g, y, emb, z, s, args):
+def run_e2e(g, y, emb, z, s, args, world=1):
     """Host buffers in, host Z out, through stream.HostPipeline: the prepared
     graph (symmetric CSR with hot-encoded targets, hot ranks) and the labels
     sit in pinned host memory; each step copies them in (row chunks), runs
@@ -469,22 +492,25 @@ def run_e2e(g, y, emb, z, s, args):
 
     from paper_2402_04403_b200.stream import HostPipeline, pinned_like
 
-    pipe = HostPipeline(g, emb.k, chunks=args.e2e_chunks)
+    pipe = HostPipeline(g, emb.k, chunks=max(1, args.e2e_chunks // world))
     h_y = y.cpu().pin_memory()
     h_z = pinned_like((g.n, emb.k))
     pipe.run(h_y, h_z, emb)  # warm-up (sizes the scratch buffers)
     torch.cuda.synchronize()
     times = []
     for _ in range(args.e2e_steps):
+        barrier(world)
         t0 = time.perf_counter()
         pipe.run(h_y, h_z, emb)
-        times.append(time.perf_counter() - t0)
+        times.append(max_over_ranks(time.perf_counter() - t0, world))
     ms = float(np.median(times)) * 1e3
     # spot check: the streamed Z equals the resident pull's Z (exact integer sums)
     rows = torch.randint(0, g.n, (4096,), device=z.device)
     same = bool(torch.equal(h_z[rows.cpu()].to(z.device), z[rows]))
-    return {"value": s / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": pipe.h2d_bytes(h_y),
-            "d2h_bytes_per_step": int(h_z.numel() * 4), "ms_per_step": ms, "steps": args.e2e_steps,
+    h2d = int(sum_over_ranks(pipe.h2d_bytes(h_y), world))
+    d2h = int(sum_over_ranks(h_z.numel() * 4, world))
+    return {"value": s / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": args.e2e_steps,
             "chunks": pipe.n_chunks, "matches_resident_pull": same, "timing": "wall clock, median",
             "path": "pinned host prepared graph + labels -> HostPipeline.run (H2D row chunks | "
                     "gee_build_projection, gee_gather_labels, gee_reduce_blocks, gee_reduce_heavy | D2H Z) "

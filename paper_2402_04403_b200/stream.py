@@ -35,10 +35,9 @@ class HostPipeline:
     def __init__(self, g: DeviceGraph, k, chunks=16, device=None):
         if not g.has_pull or g.hot_k != k:
             raise ValidationError("HostPipeline needs a pull graph prepared for k (prepare_hot)")
-        if g.n != g.n_nodes:
-            raise ValidationError("HostPipeline takes a whole graph, not a row shard")
         self.device = device or g.device
-        self.n, self.k, self.s = g.n, k, g.s
+        # a row shard streams its own rows; labels and hot ranks cover all nodes
+        self.n, self.n_nodes, self.k, self.s = g.n, g.n_nodes, k, g.s
         self.weighted = g.weighted
         dev = self.device
         off = g.offsets.cpu().numpy()
@@ -79,9 +78,9 @@ class HostPipeline:
         self.d_w = [torch.empty(max_arcs, dtype=torch.float32, device=dev) if self.weighted else None
                     for _ in range(2)]
         self.d_z = [torch.empty(max_rows * k, dtype=torch.float32, device=dev) for _ in range(2)]
-        self.d_y = torch.empty(self.n, dtype=torch.int32, device=dev)
-        self.d_hot = torch.empty(self.n, dtype=torch.int32, device=dev) if self.h_hot is not None else None
-        self.proj = DeviceGraph(self.n, 0, dev)  # what project() needs: hot ranks of the whole graph
+        self.d_y = torch.empty(self.n_nodes, dtype=torch.int32, device=dev)
+        self.d_hot = torch.empty(self.n_nodes, dtype=torch.int32, device=dev) if self.h_hot is not None else None
+        self.proj = DeviceGraph(self.n_nodes, 0, dev)  # what project() needs: hot ranks of all nodes
         self.proj.hot_rank, self.proj.n_hot = self.d_hot, self.n_hot
         self.s_in = torch.cuda.Stream(dev)
         self.s_cmp = torch.cuda.Stream(dev)
