@@ -342,6 +342,10 @@ def main():
     # warm-up (also validates labels once); the hot-label tier is graph prep
     t0 = time.perf_counter()
     g.prepare_hot(k)
+    if world > 1:  # every rank rounds weights with the whole graph's exponent
+        from paper_2402_04403_b200.shard import unify_scale_distributed
+
+        unify_scale_distributed(g)
     torch.cuda.synchronize()
     t_hot = time.perf_counter() - t0
     emb.project(y, validate=True, g=g)

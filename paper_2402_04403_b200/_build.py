@@ -30,6 +30,27 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+IO_LIB = os.path.join(PKG, "libgee_io.so")
+IO_SOURCES = ["gee_io.cpp"]
+CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra", "-static-libstdc++", "-static-libgcc"]
+
+
+def build_io_library(force=False, verbose=False):
+    """Compile the host IO library (text parsers, GEECSR1/GEEEMB1 readers and
+    writers; pure C++, no CUDA) into paper_2402_04403_b200/libgee_io.so."""
+    srcs = [os.path.join(CSRC, s) for s in IO_SOURCES]
+    deps = srcs + [os.path.join(ROOT, "include", "gee_io.h")]
+    if not force and not _stale(IO_LIB, deps):
+        return IO_LIB
+    tmp = IO_LIB + ".tmp"
+    cmd = [os.environ.get("CXX", "g++"), *CXX_FLAGS, "-o", tmp, *srcs]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    os.replace(tmp, IO_LIB)
+    return IO_LIB
+
+
 def build_library(force=False, verbose=False, debug=False):
     """Compile every CUDA source into paper_2402_04403_b200/libgee_b200.so
     (debug=True: libgee_b200_debug.so with -DGEE_DEBUG bounds checks)."""

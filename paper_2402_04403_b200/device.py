@@ -19,7 +19,7 @@ from .errors import ValidationError
 
 def require_cuda(device=None):
     if not torch.cuda.is_available():
-        raise RuntimeError("the GEE edge pass runs on a CUDA device (sm_100a); none is visible")
+        raise _lib.CudaError("the GEE edge pass runs on a CUDA device (sm_100a); none is visible")
     return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
 
 
@@ -67,7 +67,7 @@ class DeviceGraph:
         self.max_block_arcs = 0
         self.scale_exp = 0
         self.rel_err = 0.0
-        self.max_row_abs = 0.0
+        self.max_row_abs = self.max_abs = self.min_abs = 0.0
         self.src = self.dst = self.w = None
         self.coo_source_only = False
         self.hot_rank = None  # int32[n_nodes]: degree rank of hot vertices, -1 cold
@@ -158,11 +158,8 @@ class DeviceGraph:
               "gee_graph_stats")
         if nf.value:
             raise ValidationError("arc weights must be finite")
-        self.max_row_abs = mx.value
-        e, rel = ctypes.c_int32(), ctypes.c_double()
-        check(lib.gee_block_scale_exp(mx.value, mxa.value, mn.value, ctypes.byref(e), ctypes.byref(rel)),
-              "gee_block_scale_exp")
-        self.scale_exp, self.rel_err = e.value, rel.value
+        self.max_row_abs, self.max_abs, self.min_abs = mx.value, mxa.value, mn.value
+        self._set_scale(mx.value, mxa.value, mn.value)
         # arc span of the widest 32-row block (gee_reduce_blocks keeps
         # block-local offsets in int32)
         ends = self.offsets[torch.arange(0, self.n + 32, 32, device=self.device).clamp_(max=self.n)]
@@ -198,6 +195,25 @@ class DeviceGraph:
     HEAVY_ARCS = 2048  # rows above go to the heavy path (<= the block reducer's limit)
     HEAVY_ITEM_ARCS = 65536  # arcs per heavy work item (one warp)
     SMALL_ARCS = 32
+
+    def _set_scale(self, max_row_abs, max_abs, min_abs):
+        e, rel = ctypes.c_int32(), ctypes.c_double()
+        check(lib.gee_block_scale_exp(max_row_abs, max_abs, min_abs, ctypes.byref(e), ctypes.byref(rel)),
+              "gee_block_scale_exp")
+        self.scale_exp, self.rel_err = e.value, rel.value
+
+    def weight_stats(self):
+        """(max row |w| sum, max |w|, min nonzero |w|) of this layout's arcs."""
+        return self.max_row_abs, self.max_abs, self.min_abs
+
+    def adopt_scale(self, stats):
+        """Use the fixed-point exponent of the whole graph this layout is a row
+        shard of.  `stats` = (max over shards of max_row_abs and max_abs, min
+        over shards of the nonzero min_abs); the exponent it gives is <= this
+        shard's own, so no sum can overflow, and every shard then rounds
+        each weight exactly as the single-GPU pull does (bit-identical rows)."""
+        mx, mxa, mn = (float(v) for v in stats)
+        self._set_scale(mx, mxa, mn)
 
     def _plan_heavy(self):
         """Heavy-row chunk list for the row reducers (graph preparation)."""

@@ -207,13 +207,23 @@ def generate_erdos_renyi(n, s, seed, device=None) -> EdgeList:
     """G(n, s): exactly s directed unit-weight edges with uniform endpoints.
 
     Same contract as graph.py:187-201 (self-loops and duplicates kept,
-    deterministic in (n, s, seed)); the stream is the counter-based
-    generator in gee_synth.cu, so values differ from numpy's.
+    deterministic in (n, s, seed)).  With ``device=None`` the endpoints are
+    the reference's own numpy stream (default_rng(seed).integers twice), so
+    a seed gives the reference's edge sequence; with a CUDA ``device`` they
+    come from the counter-based generator in gee_synth.cu (a different
+    stream, generated in HBM at memory speed).
     """
     if n < 1:
         raise ValidationError("n must be at least 1")
     if s < 0:
         raise ValidationError("s must be nonnegative")
+    if device is None:
+        if n - 1 > MAX_NODES:
+            raise ValidationError(f"node count {n} exceeds int32 limit {MAX_NODES}")
+        rng = np.random.default_rng(seed)
+        src = rng.integers(0, n, size=s, dtype=np.int64)
+        dst = rng.integers(0, n, size=s, dtype=np.int64)
+        return EdgeList(n=n, src=src, dst=dst, w=None, directed=True)
     from . import synth
 
     src, dst, _ = synth.er_edges(n, s, seed, weighted=False, device=device)

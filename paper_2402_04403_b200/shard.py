@@ -81,6 +81,31 @@ def build_row_shard(src, dst, w, n, world, rank, k=None):
     return g, lo, hi
 
 
+def merge_weight_stats(stats):
+    """Whole-graph weight statistics from per-shard (max_row_abs, max_abs,
+    min_abs) triples: max, max, and min over the shards' nonzero minima."""
+    stats = list(stats)
+    mins = [s[2] for s in stats if s[2] > 0]
+    return (max((s[0] for s in stats), default=0.0), max((s[1] for s in stats), default=0.0),
+            min(mins) if mins else 0.0)
+
+
+def unify_scale_distributed(g, group=None):
+    """All ranks adopt the whole graph's fixed-point exponent (one 3-value
+    all-reduce at graph preparation; nothing on the data path)."""
+    import torch
+    import torch.distributed as dist
+
+    mx, mxa, mn = g.weight_stats()
+    dev = g.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    hi = torch.tensor([mx, mxa], dtype=torch.float64, device=dev)
+    lo = torch.tensor([mn if mn > 0 else float("inf")], dtype=torch.float64, device=dev)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    mn_all = float(lo[0])
+    g.adopt_scale((float(hi[0]), float(hi[1]), 0.0 if mn_all == float("inf") else mn_all))
+
+
 def reduce_scatter_rows(z_partial, world, group=None):
     """Edge-range combine: sum the (n, k) partials across ranks and return
     this rank's contiguous row slice (rows padded to a multiple of world)."""

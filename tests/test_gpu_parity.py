@@ -336,19 +336,29 @@ def test_row_shards_tile_the_full_pull(world):
     y = synth.uniform_labels(n, k, seed=22)
     exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), w.cpu().numpy(), y.cpu().numpy(), n, k)
     dev = torch.device("cuda")
-    parts, bounds = [], []
+    shards, bounds = [], []
     for rank in range(world):
         g, lo, hi = shard.build_row_shard(src, dst, w, n, world, rank, k=k)
         g.prepare_hot(k, enable=True)
         assert g.n_hot > 0 and g.global_offsets is None
+        shards.append(g)
+        bounds.append((lo, hi))
+    # the whole graph's fixed-point exponent (bench: one all-reduce) makes
+    # the tiled shards bit-identical to the single-GPU pull
+    stats = shard.merge_weight_stats(g.weight_stats() for g in shards)
+    parts = []
+    for g, (lo, hi) in zip(shards, bounds):
+        g.adopt_scale(stats)
         emb = Embedder(n, k, dev)
         z = torch.empty((hi - lo, k), dtype=torch.float32, device=dev)
         emb.project(y, g=g)
         parts.append(emb.pull(g, z).cpu().numpy())
-        bounds.append((lo, hi))
     assert bounds[0][0] == 0 and bounds[-1][1] == n
     assert all(bounds[i][1] == bounds[i + 1][0] for i in range(world - 1))
-    assert rel_err(np.concatenate(parts), exp) <= TOL
+    z_all = np.concatenate(parts)
+    assert rel_err(z_all, exp) <= TOL
+    single = gb.embed(src, dst, y, n, k, weights=w, directed=True, variant="pull").cpu().numpy()
+    assert np.array_equal(z_all, single)
 
 
 def test_raw_ctypes_binding_without_torch():

@@ -51,7 +51,21 @@ def _worker(rank, port, seed, mode, q):
         src, dst, w, y, n, k = _graph(seed)
         _, _, row = oracle.projection(y, k)
         full = oracle.serial_embed(src, dst, w, y, n, k)
-        if mode == "rows":
+        if mode == "scale":
+            # every rank adopts the whole graph's fixed-point exponent
+            from paper_2402_04403_b200.device import DeviceGraph
+
+            g = DeviceGraph(10, 10, torch.device("cpu"))
+            mine = [(12.5, 0.75, 1e-3), (3.0, 0.999, 2e-6)][rank]
+            g.max_row_abs, g.max_abs, g.min_abs = mine
+            g.adopt_scale(mine)
+            own = g.scale_exp
+            shard.unify_scale_distributed(g)
+            ref = DeviceGraph(10, 10, torch.device("cpu"))
+            ref.adopt_scale(shard.merge_weight_stats([(12.5, 0.75, 1e-3), (3.0, 0.999, 2e-6)]))
+            assert g.scale_exp == ref.scale_exp <= own and g.rel_err == ref.rel_err
+            q.put((rank, "ok", g.scale_exp))
+        elif mode == "rows":
             off, tgt, wts = oracle.build_csr(src, dst, w, n, directed=False)  # symmetric CSR
             bounds = shard.plan_rows(off, WORLD, k, weighted=True)
             got = [torch.zeros(WORLD + 1, dtype=torch.int64) for _ in range(WORLD)]
@@ -85,7 +99,7 @@ def _worker(rank, port, seed, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["rows", "edges"])
+@pytest.mark.parametrize("mode", ["rows", "edges", "scale"])
 def test_sharding_world2_gloo(mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
