@@ -402,11 +402,14 @@ def main():
         "gather": arcs * (4 + 1),
         "blocks": 8 * (rows + 1) + light_arcs * (1 + 4 * weighted) + 4 * k * (rows - heavy_rows),
         "heavy": heavy_arcs * (1 + 4 * weighted) + 4 * k * heavy_rows,
+        # wide K: label gather fused with the row windows (targets + weights
+        # in, whole Z rows out; the label table is L2-resident)
+        "wide": 8 * (rows + 1) + arcs * (4 + 4 * weighted) + 4 * k * rows,
     }
     peak_gbs, peak_kind = load_peaks()
     dominant = max((p for p in phase_ms if p in phase_bytes), key=lambda p: phase_ms[p])
     kernel_of = {"project": "k_label_hist", "gather": "k_gather_contig", "blocks": "k_reduce_blocks_ring",
-                 "heavy": "k_reduce_heavy_items"}
+                 "heavy": "k_reduce_heavy_items", "wide": "k_wide_rows"}
     achieved = phase_bytes[dominant] / (phase_ms[dominant] * 1e-3) / 1e9
     step_bmin = s * (8 + 4 * weighted) + 4 * n + 4 * n * k  # SURVEY 8(d) B_min, whole graph
     workload = cfg.name if not (args.scale or args.edges) else f"{cfg.name}-reduced(scale={args.scale},s={s})"

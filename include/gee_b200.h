@@ -202,6 +202,20 @@ int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const flo
                        int32_t scale_exp, const void *table, int64_t n_hot, const double *inv,
                        int32_t k, float *z, void *slots, void *stream);
 
+/* Wide-embedding pull (any k; the default for k > 255, BASELINE C5): the
+ * label gather fused with a per-row class window.  Replaces the parallel
+ * arc wave of embed_parallel (_kernels.py:138-207, SOURCE_ONLY arcs of the
+ * symmetric CSR) for wide K: one warp per row of <= 2048 arcs (shared-memory
+ * K-bin window, whole Z row written with 16-byte streaming stores), one CTA
+ * per heavy row listed in heavy_rows (rows > 2048 arcs, u64 window).  Every
+ * Z row is written exactly once, zeros included; exact integer sums (unit:
+ * counts, weighted: q = rint(w 2^scale_exp) from gee_block_scale_exp), so Z
+ * is bit-identical to the other pull reducers.  Targets are label-table
+ * slots (gee_hot_encode), w == NULL for unit weights. */
+int gee_reduce_wide(const int64_t *offsets, int64_t n, const int32_t *targets, const float *w,
+                    const void *table, int32_t k, int32_t scale_exp, const double *inv,
+                    const int32_t *heavy_rows, int64_t n_heavy, float *z, void *stream);
+
 /* Class stream: cls[e] = table[targets[e]] (u8, k <= 255) for every arc of
  * a pull layout -- the random half of the pull pass on its own (label-table
  * head staged in shared memory; measurement and split-pass use). */

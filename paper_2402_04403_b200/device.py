@@ -465,6 +465,13 @@ class Embedder:
             raise ValidationError("label table does not match the graph's hot tier: call project(labels, g=graph)")
         if z is None:
             z = torch.empty((g.n, self.k), dtype=torch.float32, device=self.device)
+        if self.k > 255 and os.environ.get("GEE_WIDE", "1") != "0" or self.reducer == "wide":
+            # wide K: label gather fused with a per-row class window
+            check(lib.gee_reduce_wide(ptr(g.offsets), g.n, ptr(g.targets), ptr(g.weights), ptr(self.table), self.k,
+                                      g.scale_exp, ptr(self.inv64), ptr(g.heavy_rows), g.n_heavy, ptr(z), _stream()),
+                  "gee_reduce_wide")
+            self._mark("wide", 1 + (1 if g.n_heavy else 0))
+            return z
         if self.split and self.k <= 255:
             # split pass: class stream (random gathers, full occupancy), then
             # the gather-free segmented reduction

@@ -314,13 +314,41 @@ def test_pull_reducers_agree_bitwise(k, weighted):
     assert g.n_heavy >= 1
     exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
     out = {}
-    for red in ("blocks", "lists", "rows", "tiles"):
+    for red in ("blocks", "lists", "rows", "tiles", "wide"):
         emb = Embedder(n, k, dev)
         emb.reducer = red
         out[red] = emb.embed(g, torch.from_numpy(y.labels).to(dev), variant="pull").cpu().numpy()
         assert rel_err(out[red], exp) <= TOL, red
-    for red in ("lists", "rows"):
+    for red in ("lists", "rows", "wide"):
         assert np.array_equal(out["blocks"].view(np.uint32), out[red].view(np.uint32)), red
+
+
+@pytest.mark.parametrize("k,weighted", [(1000, False), (1000, True), (301, False), (1001, True), (4096, False)])
+def test_wide_k_pull(k, weighted, monkeypatch):
+    # K > 255 (BASELINE C5 is K = 1000): the fused wide reducer (warp per
+    # light row, CTA per heavy row; vector and scalar write-outs for
+    # k % 4 == 0 / != 0) against the oracle, bit-stable, and bit-identical to
+    # the tiled pull it replaced
+    rng = np.random.default_rng(k + weighted)
+    n = 30_011
+    hub = np.full(9_000, 11, np.int64)
+    src = np.concatenate([hub, rng.integers(0, n, 150_000), np.arange(n - 40, n)])
+    dst = np.concatenate([rng.integers(0, n, 9_000), rng.integers(0, n, 150_000), np.arange(n - 40, n)])
+    w = (1.0 - rng.random(src.size)).astype(np.float32) if weighted else None
+    y = gb.random_labels(n, k, 0.9, seed=k)
+    dev = torch.device("cuda")
+    g = DeviceGraph.from_edges(torch.from_numpy(src).int(), torch.from_numpy(dst).int(),
+                               None if w is None else torch.from_numpy(w), n, device=dev, pull=True)
+    assert g.n_heavy >= 1
+    exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
+    lab = torch.from_numpy(y.labels).to(dev)
+    emb = Embedder(n, k, dev)
+    z = emb.embed(g, lab, variant="pull").cpu().numpy()
+    assert rel_err(z, exp) <= TOL
+    assert np.array_equal(z, emb.embed(g, lab, variant="pull").cpu().numpy())
+    monkeypatch.setenv("GEE_WIDE", "0")
+    old = Embedder(n, k, dev).embed(g, lab, variant="pull").cpu().numpy()
+    assert np.array_equal(z.view(np.uint32), old.view(np.uint32))
 
 
 @pytest.mark.parametrize("world", [2, 3])
