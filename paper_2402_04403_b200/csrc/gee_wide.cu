@@ -27,7 +27,7 @@ constexpr int WT = 256;        // threads per CTA (8 warps)
 constexpr int WW = WT / 32;
 constexpr int SPLIT = 21;      // == BLOCK_SPLIT of gee_reduce.cu (gee_block_scale_exp bounds q < 2^42)
 constexpr int LIGHT_MAX = 2048;
-constexpr int UNR = 4;         // 32-arc rounds in flight per warp
+constexpr int UNR = 8;         // 32-arc rounds in flight per warp (256 arcs)
 
 template <typename LT>
 __device__ __forceinline__ uint32_t ld_lab(const LT *t, uint32_t slot)
@@ -35,12 +35,61 @@ __device__ __forceinline__ uint32_t ld_lab(const LT *t, uint32_t slot)
     return (uint32_t)__ldg(t + slot);
 }
 
-// window layout per warp: planes x kp u32 (kp = k rounded up to 4)
+// Labels of a loaded segment (predicated gathers; 0 for lanes past the row).
+template <typename LT>
+__device__ __forceinline__ void wide_labels(const int32_t (&t)[UNR], const LT *__restrict__ table, uint32_t (&lab)[UNR])
+{
+#pragma unroll
+    for (int u = 0; u < UNR; u++) lab[u] = t[u] >= 0 ? ld_lab(table, (uint32_t)t[u]) : 0u;
+}
+
+// Add a segment's arcs (labels + weights) into the window.
+template <bool WEIGHTED>
+__device__ __forceinline__ void wide_add(const uint32_t (&lab)[UNR], const float (&wt)[UNR], uint32_t *win,
+                                         int32_t kp, float qscale, int skip, uint32_t &sink)
+{
+    if (skip & 4) {
+#pragma unroll
+        for (int u = 0; u < UNR; u++) sink += lab[u];
+        return;
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+        if (lab[u] == 0u) continue;
+        uint32_t *p = win + (lab[u] - 1);
+        if (WEIGHTED) {
+            const unsigned long long q = (unsigned long long)__float2ll_rn(wt[u] * qscale);
+            atomicAdd(p, (uint32_t)q & ((1u << SPLIT) - 1u));
+            atomicAdd(p + kp, (uint32_t)(q >> SPLIT));
+        } else {
+            atomicAdd(p, 1u);
+        }
+    }
+}
+
+template <bool WEIGHTED>
+__device__ __forceinline__ void wide_load(const int32_t *__restrict__ targets, const float *__restrict__ w, int64_t e0,
+                                          int64_t e1, int lane, int32_t (&t)[UNR], float (&wt)[UNR])
+{
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+        const int64_t e = e0 + 32 * u + lane;
+        t[u] = e < e1 ? __ldcs(targets + e) : -1;
+        if (WEIGHTED) wt[u] = e < e1 ? __ldcs(w + e) : 0.f;
+    }
+}
+
+// window layout per warp: planes x kp u32 (kp = k rounded up to 4).
+// Software pipeline per warp (rows r, r+GW, r+2GW, ...): while row i's Z row
+// is written out, row i+1's labels and row i+2's targets (+ weights) and
+// offsets are in flight, so the write-out hides both dependent latencies.
+// Only a row's first 32 * UNR arcs are pipelined; longer rows finish their
+// remaining segments in place.
 template <typename LT, bool WEIGHTED, bool VEC>
-__global__ void __launch_bounds__(WT)
+__global__ void __launch_bounds__(WT, WEIGHTED ? 3 : 5)
 k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__restrict__ targets,
             const float *__restrict__ w, const LT *__restrict__ table, float qscale, double dscale,
-            const double *__restrict__ inv, int32_t k, int32_t kp, float *__restrict__ z)
+            const double *__restrict__ inv, int32_t k, int32_t kp, float *__restrict__ z, int skip)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *sc = reinterpret_cast<float *>(smem_raw);  // sc[c] = inv[c+1] * dscale, c < kp
@@ -50,82 +99,101 @@ k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__res
     for (int c = threadIdx.x; c < kp; c += WT) sc[c] = c < k ? (float)(inv[c + 1] * dscale) : 0.f;
     for (int i = lane; i < planes * kp; i += 32) win[i] = 0u;
     __syncthreads();
-    const int64_t gw = (int64_t)blockIdx.x * WW + wid;
     const int64_t GW = (int64_t)gridDim.x * WW;
-    for (int64_t r = gw; r < n; r += GW) {
-        const int64_t a0 = offsets[r], a1 = offsets[r + 1];
-        if (a1 - a0 > LIGHT_MAX) continue;  // heavy row: k_wide_heavy writes it
-        for (int64_t e0 = a0; e0 < a1; e0 += 32 * UNR) {
-            int32_t t[UNR];
-            float wt[UNR];
-#pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                const int64_t e = e0 + 32 * u + lane;
-                t[u] = e < a1 ? __ldcs(targets + e) : -1;
-                if (WEIGHTED) wt[u] = e < a1 ? __ldcs(w + e) : 0.f;
-            }
-            uint32_t lab[UNR];
-#pragma unroll
-            for (int u = 0; u < UNR; u++) lab[u] = t[u] >= 0 ? ld_lab(table, (uint32_t)t[u]) : 0u;
-#pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                if (lab[u] == 0u) continue;
-                uint32_t *p = win + (lab[u] - 1);
-                if (WEIGHTED) {
-                    const unsigned long long q = (unsigned long long)__float2ll_rn(wt[u] * qscale);
-                    atomicAdd(p, (uint32_t)q & ((1u << SPLIT) - 1u));
-                    atomicAdd(p + kp, (uint32_t)(q >> SPLIT));
-                } else {
-                    atomicAdd(p, 1u);
-                }
-            }
-        }
-        __syncwarp();
-        float *zr = z + r * (int64_t)k;
-        if (VEC) {  // k % 4 == 0 and z 16-byte aligned: whole row in 16-byte stores
-            const int groups = kp >> 2;
-            uint4 *w4 = reinterpret_cast<uint4 *>(win);
-            float4 *z4 = reinterpret_cast<float4 *>(zr);
-            for (int g = lane; g < groups; g += 32) {
-                const uint4 lo = w4[g];
-                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-                uint4 hi = make_uint4(0u, 0u, 0u, 0u);
-                if (WEIGHTED) hi = w4[g + (kp >> 2)];
-                if ((lo.x | lo.y | lo.z | lo.w | hi.x | hi.y | hi.z | hi.w) != 0u) {
-                    const float4 s4 = reinterpret_cast<const float4 *>(sc)[g];
-                    if (WEIGHTED) {
-                        o.x = (float)(long long)(((unsigned long long)hi.x << SPLIT) + lo.x) * s4.x;
-                        o.y = (float)(long long)(((unsigned long long)hi.y << SPLIT) + lo.y) * s4.y;
-                        o.z = (float)(long long)(((unsigned long long)hi.z << SPLIT) + lo.z) * s4.z;
-                        o.w = (float)(long long)(((unsigned long long)hi.w << SPLIT) + lo.w) * s4.w;
-                        w4[g + (kp >> 2)] = make_uint4(0u, 0u, 0u, 0u);
-                    } else {
-                        o.x = (float)lo.x * s4.x, o.y = (float)lo.y * s4.y;
-                        o.z = (float)lo.z * s4.z, o.w = (float)lo.w * s4.w;
-                    }
-                    w4[g] = make_uint4(0u, 0u, 0u, 0u);
-                }
-                __stcs(z4 + g, o);
-            }
-        } else {
-            for (int c = lane; c < k; c += 32) {
-                const uint32_t lo = win[c];
-                float o = 0.f;
-                if (WEIGHTED) {
-                    const uint32_t hi = win[c + kp];
-                    if (lo | hi) {
-                        o = (float)(long long)(((unsigned long long)hi << SPLIT) + lo) * sc[c];
-                        win[c] = 0u, win[c + kp] = 0u;
-                    }
-                } else if (lo) {
-                    o = (float)lo * sc[c];
-                    win[c] = 0u;
-                }
-                __stcs(zr + c, o);
-            }
-        }
-        __syncwarp();
+    int64_t r = (int64_t)blockIdx.x * WW + wid;
+    if (r >= n) return;
+    uint32_t sink = 0;
+    auto seg_end = [](int64_t b0, int64_t b1) { return b1 - b0 <= LIGHT_MAX ? (b1 < b0 + 32 * UNR ? b1 : b0 + 32 * UNR) : b0; };
+    // stage 0 (row r): labels in flight; stage 1 (row r+GW): targets in flight
+    int64_t a0 = offsets[r], a1 = offsets[r + 1];
+    int32_t t[UNR];
+    float wt[UNR], wt1[UNR];
+    uint32_t lab[UNR];
+    wide_load<WEIGHTED>(targets, w, a0, seg_end(a0, a1), lane, t, wt);
+    wide_labels<LT>(t, table, lab);
+    int64_t b0 = 0, b1 = 0;
+    if (r + GW < n) {
+        b0 = offsets[r + GW], b1 = offsets[r + GW + 1];
+        wide_load<WEIGHTED>(targets, w, b0, seg_end(b0, b1), lane, t, wt1);
     }
+    while (true) {
+        const bool light = a1 - a0 <= LIGHT_MAX;  // heavy rows: k_wide_heavy writes them
+        if (light && !(skip & 1)) {
+            wide_add<WEIGHTED>(lab, wt, win, kp, qscale, skip, sink);
+            for (int64_t e0 = a0 + 32 * UNR; e0 < a1; e0 += 32 * UNR) {  // rows longer than one segment
+                int32_t tx[UNR];
+                uint32_t lx[UNR];
+                wide_load<WEIGHTED>(targets, w, e0, a1, lane, tx, wt);
+                wide_labels<LT>(tx, table, lx);
+                wide_add<WEIGHTED>(lx, wt, win, kp, qscale, skip, sink);
+            }
+        }
+        const int64_t rn = r + GW;
+        // advance the pipeline: labels of rn, targets (+ offsets) of rn + GW
+        int64_t c0 = 0, c1 = 0;
+        if (rn < n) {
+            wide_labels<LT>(t, table, lab);
+#pragma unroll
+            for (int u = 0; u < UNR; u++) wt[u] = wt1[u];
+            const int64_t rnn = rn + GW;
+            if (rnn < n) {
+                c0 = offsets[rnn], c1 = offsets[rnn + 1];
+                wide_load<WEIGHTED>(targets, w, c0, seg_end(c0, c1), lane, t, wt1);
+            }
+        }
+        if (light && !(skip & 2)) {
+            __syncwarp();
+            float *zr = z + r * (int64_t)k;
+            if (VEC) {  // k % 4 == 0 and z 16-byte aligned: whole row in 16-byte streaming stores
+                // (a TMA bulk store of the converted row measured slower: 4.99 vs 4.58 ms on C5)
+                const int groups = kp >> 2;
+                uint4 *w4 = reinterpret_cast<uint4 *>(win);
+                float4 *z4 = reinterpret_cast<float4 *>(zr);
+#pragma unroll 4
+                for (int g = lane; g < groups; g += 32) {
+                    const uint4 lo = w4[g];
+                    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                    uint4 hi = make_uint4(0u, 0u, 0u, 0u);
+                    if (WEIGHTED) hi = w4[g + (kp >> 2)];
+                    if ((lo.x | lo.y | lo.z | lo.w | hi.x | hi.y | hi.z | hi.w) != 0u) {
+                        const float4 s4 = reinterpret_cast<const float4 *>(sc)[g];
+                        if (WEIGHTED) {
+                            o.x = (float)(long long)(((unsigned long long)hi.x << SPLIT) + lo.x) * s4.x;
+                            o.y = (float)(long long)(((unsigned long long)hi.y << SPLIT) + lo.y) * s4.y;
+                            o.z = (float)(long long)(((unsigned long long)hi.z << SPLIT) + lo.z) * s4.z;
+                            o.w = (float)(long long)(((unsigned long long)hi.w << SPLIT) + lo.w) * s4.w;
+                            w4[g + (kp >> 2)] = make_uint4(0u, 0u, 0u, 0u);
+                        } else {
+                            o.x = (float)lo.x * s4.x, o.y = (float)lo.y * s4.y;
+                            o.z = (float)lo.z * s4.z, o.w = (float)lo.w * s4.w;
+                        }
+                        w4[g] = make_uint4(0u, 0u, 0u, 0u);
+                    }
+                    __stcs(z4 + g, o);
+                }
+            } else {
+                for (int c = lane; c < k; c += 32) {
+                    const uint32_t lo = win[c];
+                    float o = 0.f;
+                    if (WEIGHTED) {
+                        const uint32_t hi = win[c + kp];
+                        if (lo | hi) {
+                            o = (float)(long long)(((unsigned long long)hi << SPLIT) + lo) * sc[c];
+                            win[c] = 0u, win[c + kp] = 0u;
+                        }
+                    } else if (lo) {
+                        o = (float)lo * sc[c];
+                        win[c] = 0u;
+                    }
+                    __stcs(zr + c, o);
+                }
+            }
+            __syncwarp();
+        }
+        if (rn >= n) break;
+        r = rn, a0 = b0, a1 = b1, b0 = c0, b1 = c1;
+    }
+    if (sink == 0x9e3779b9u) z[0] = 0.f;  // keeps the skip-4 experiment's loads alive
 }
 
 // Heavy rows (> LIGHT_MAX arcs): one CTA per row, u64 window, any length.
@@ -188,7 +256,9 @@ int launch_wide(const int64_t *offsets, int64_t n, const int32_t *targets, const
         int64_t want = (n + WW - 1) / WW;
         int64_t grid = (int64_t)gee::sm_count() * per_sm;
         if (grid > want) grid = want;
-        kern<<<(int)grid, WT, smem, st>>>(offsets, n, targets, w, tab, qscale, dscale, inv, k, kp, z);
+        int skip = 0;  // GEE_WIDE_SKIP (experiment): 1 = no gather/atomics, 2 = no write-out
+        if (const char *e = getenv("GEE_WIDE_SKIP")) skip = atoi(e);
+        kern<<<(int)grid, WT, smem, st>>>(offsets, n, targets, w, tab, qscale, dscale, inv, k, kp, z, skip);
         if (int rc = gee::check_launch("k_wide_rows")) return rc;
     }
     if (n_heavy > 0) {
