@@ -493,35 +493,46 @@ def run_e2e(g, y, emb, z, s, args, world=1):
     """Host buffers in, host Z out, through stream.HostPipeline: the prepared
     graph (symmetric CSR with hot-encoded targets, hot ranks) and the labels
     sit in pinned host memory; each step copies them in (row chunks), runs
-    the histogram and the chunked pull, and copies Z out -- H2D, compute and
-    D2H overlapping on three streams.  Wall clock around the whole call."""
+    the histogram and the chunked pull, compacts each chunk's Z rows on the
+    device and copies them out row-sparse, and the host rebuilds the dense
+    rows in the caller's pinned Z -- H2D, compute, D2H and host expansion
+    overlapping.  Wall clock around the whole call.  GEE_E2E_DENSE=1 copies
+    dense Z instead (the previous path, for comparison)."""
     import torch
 
     from paper_2402_04403_b200.stream import HostPipeline, pinned_like
 
+    sparse = os.environ.get("GEE_E2E_DENSE") is None
     pipe = HostPipeline(g, emb.k, chunks=max(1, args.e2e_chunks // world))
     h_y = y.cpu().pin_memory()
     h_z = pinned_like((g.n, emb.k))
-    pipe.run(h_y, h_z, emb)  # warm-up (sizes the scratch buffers)
+    pipe.run(h_y, h_z, emb, sparse=sparse)  # warm-up (sizes the scratch buffers)
     torch.cuda.synchronize()
     times = []
     for _ in range(args.e2e_steps):
+        h_z.fill_(float("nan"))  # untimed: every entry must be rewritten by the call
         barrier(world)
         t0 = time.perf_counter()
-        pipe.run(h_y, h_z, emb)
+        pipe.run(h_y, h_z, emb, sparse=sparse)
         times.append(max_over_ranks(time.perf_counter() - t0, world))
     ms = float(np.median(times)) * 1e3
     # spot check: the streamed Z equals the resident pull's Z (exact integer sums)
     rows = torch.randint(0, g.n, (4096,), device=z.device)
     same = bool(torch.equal(h_z[rows.cpu()].to(z.device), z[rows]))
+    step = max(1, (1 << 28) // emb.k)  # whole-Z check in 1 GB row slices (untimed)
+    for r0 in range(0, g.n, step):
+        same = same and bool(torch.equal(h_z[r0:r0 + step].to(z.device), z[r0:r0 + step]))
     h2d = int(sum_over_ranks(pipe.h2d_bytes(h_y), world))
-    d2h = int(sum_over_ranks(h_z.numel() * 4, world))
+    d2h = int(sum_over_ranks(pipe.d2h_bytes if sparse else h_z.numel() * 4, world))
     return {"value": s / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": args.e2e_steps,
             "chunks": pipe.n_chunks, "matches_resident_pull": same, "timing": "wall clock, median",
             "path": "pinned host prepared graph + labels -> HostPipeline.run (H2D row chunks | "
+                    "gee_build_projection, gee_gather_labels, gee_reduce_blocks, gee_reduce_heavy, gee_z_compact | "
+                    "D2H row-sparse Z | gee_io_expand_rows on the host threads) -> pinned host Z"
+                    if sparse else "pinned host prepared graph + labels -> HostPipeline.run (H2D row chunks | "
                     "gee_build_projection, gee_gather_labels, gee_reduce_blocks, gee_reduce_heavy | D2H Z) "
-                    "-> pinned host Z"}
+                    "-> pinned host Z", "z_transfer": "row-sparse" if sparse else "dense"}
 
 
 if __name__ == "__main__":

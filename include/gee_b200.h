@@ -216,6 +216,24 @@ int gee_reduce_wide(const int64_t *offsets, int64_t n, const int32_t *targets, c
                     const void *table, int32_t k, int32_t scale_exp, const double *inv,
                     const int32_t *heavy_rows, int64_t n_heavy, float *z, void *stream);
 
+/* Row-sparse Z for the device -> host copy of a streamed pass (the
+ * caller-owned dense `out` of embed_parallel, encoder.py:143-194, rebuilt on
+ * the host by gee_io_expand_rows in include/gee_io.h).  For rows [0, rows)
+ * of a row-major (rows, k) f32 Z:
+ *   mask[r * mw + j] (u64, mw = ceil(k / 64)): bit c set iff Z[r, 64 j + c]
+ *                    has a nonzero bit pattern;
+ *   vals:            the nonzero values, row-major (capacity rows * k);
+ *   block_off[b]:    index in vals of the first value of row
+ *                    b * GEE_ZC_BLOCK_ROWS (gee_zc_blocks(rows) + 1 entries;
+ *                    the last one is the nonzero count).
+ * Three launches (mask + counts, scan, scatter); no allocation. */
+#ifndef GEE_ZC_BLOCK_ROWS
+#define GEE_ZC_BLOCK_ROWS 1024
+#endif
+int64_t gee_zc_blocks(int64_t rows);
+int gee_z_compact(const float *z, int64_t rows, int32_t k, unsigned long long *mask, int64_t *block_off,
+                  float *vals, void *stream);
+
 /* Class stream: cls[e] = table[targets[e]] (u8, k <= 255) for every arc of
  * a pull layout -- the random half of the pull pass on its own (label-table
  * head staged in shared memory; measurement and split-pass use). */

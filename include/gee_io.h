@@ -105,6 +105,17 @@ int gee_io_emb_read(const char *path, int64_t n, int64_t k, double *z, int threa
  * 1 = binary.  f32 values are written as their exact f64 value. */
 int gee_io_emb_write(const char *path, const void *z, int z_is_f64, int64_t n, int64_t k, int fmt, int threads);
 
+/* ---- row-sparse Z -> dense host rows (the streamed pass's D2H) --------
+ * Inverse of gee_z_compact (include/gee_b200.h): writes rows [0, rows) of
+ * the dense row-major (rows, k) f32 Z from the u64 row masks, the packed
+ * nonzero values and the per-block value offsets (GEE_ZC_BLOCK_ROWS rows
+ * per block), zeros included, with streaming stores; blocks in parallel. */
+#ifndef GEE_ZC_BLOCK_ROWS
+#define GEE_ZC_BLOCK_ROWS 1024
+#endif
+int gee_io_expand_rows(const uint64_t *mask, const float *vals, const int64_t *block_off, int64_t rows, int32_t k,
+                       float *z, int threads);
+
 #ifdef __cplusplus
 }
 #endif

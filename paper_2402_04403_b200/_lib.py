@@ -64,6 +64,8 @@ SIGNATURES = {
                                    vp]),
     "gee_pull_scale_exp": (c_int, [c_dbl, c_dbl, P_i32, P_dbl]),
     "gee_gather_labels": (c_int, [vp, c_i64, vp, c_i64, c_i32, vp, vp]),
+    "gee_zc_blocks": (c_i64, [c_i64]),
+    "gee_z_compact": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp]),
     "gee_reduce_wide": (c_int, [vp, c_i64, vp, vp, vp, c_i32, c_i32, vp, vp, c_i64, vp, vp]),
     "gee_reduce_heavy_plan": (c_int, [vp, c_i64, c_i64, vp, ctypes.POINTER(c_i64), vp]),
     "gee_reduce_blocks": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, c_i64, vp, vp, c_i64, vp, vp, vp]),

@@ -34,6 +34,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <emmintrin.h>
 #include <functional>
 #include <string>
 #include <thread>
@@ -1058,5 +1059,59 @@ extern "C" int gee_io_emb_write(const char *path, const void *z, int z_is_f64, i
     int fd = f.fd;
     f.fd = -1;
     if (close(fd) != 0) return fail_os(path);
+    return GEE_IO_OK;
+}
+
+// ===================================================== row-sparse Z expand
+namespace {
+
+// dst <- src (bytes), 16-byte non-temporal stores where dst is aligned
+inline void stream_copy(char *dst, const char *src, size_t bytes)
+{
+    size_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+    if (head > bytes) head = bytes;
+    memcpy(dst, src, head);
+    dst += head, src += head, bytes -= head;
+    size_t body = bytes & ~(size_t)15;
+    for (size_t i = 0; i < body; i += 16)
+        _mm_stream_si128(reinterpret_cast<__m128i *>(dst + i), _mm_loadu_si128(reinterpret_cast<const __m128i *>(src + i)));
+    memcpy(dst + body, src + body, bytes - body);
+}
+
+}  // namespace
+
+extern "C" int gee_io_expand_rows(const uint64_t *mask, const float *vals, const int64_t *block_off, int64_t rows,
+                                  int32_t k, float *z, int threads)
+{
+    clear_error();
+    if (rows <= 0) return GEE_IO_OK;
+    if (k < 1 || !mask || !block_off || !z) return fail(GEE_IO_ERR_INVALID, "bad arguments");
+    const int mw = (k + 63) / 64;
+    const int64_t nb = (rows + GEE_ZC_BLOCK_ROWS - 1) / GEE_ZC_BLOCK_ROWS;
+    if (block_off[nb] > 0 && !vals) return fail(GEE_IO_ERR_INVALID, "NULL vals");
+    constexpr int SUB = 32;  // rows staged per streaming copy
+    parallel_for(nb, threads, [&](int64_t b) {
+        std::vector<float> stage((size_t)SUB * k);
+        int64_t pos = block_off[b];
+        const int64_t r0 = b * GEE_ZC_BLOCK_ROWS;
+        const int64_t r1 = std::min(rows, r0 + GEE_ZC_BLOCK_ROWS);
+        for (int64_t s0 = r0; s0 < r1; s0 += SUB) {
+            const int64_t s1 = std::min(r1, s0 + SUB);
+            std::fill(stage.begin(), stage.begin() + (s1 - s0) * k, 0.0f);
+            for (int64_t r = s0; r < s1; r++) {
+                float *row = stage.data() + (r - s0) * k;
+                for (int j = 0; j < mw; j++) {
+                    uint64_t m = mask[r * mw + j];
+                    while (m) {
+                        row[64 * j + __builtin_ctzll(m)] = vals[pos++];
+                        m &= m - 1;
+                    }
+                }
+            }
+            stream_copy(reinterpret_cast<char *>(z + s0 * k), reinterpret_cast<const char *>(stage.data()),
+                        (size_t)(s1 - s0) * k * sizeof(float));
+        }
+    });
+    _mm_sfence();
     return GEE_IO_OK;
 }

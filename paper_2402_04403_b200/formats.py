@@ -62,6 +62,7 @@ IO_SIGNATURES = {
     "gee_io_emb_header": (_int, [_cs, _P_i64, _P_i64]),
     "gee_io_emb_read": (_int, [_cs, _i64, _i64, _vp, _int]),
     "gee_io_emb_write": (_int, [_cs, _vp, _int, _i64, _i64, _int, _int]),
+    "gee_io_expand_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _int]),
 }
 
 

@@ -235,3 +235,28 @@ def test_weight_repr_matches_python(tmp_path):
     gb.write_edge_list(el, p, threads=4)
     got = [ln.split(" ")[2] for ln in p.read_text().splitlines()]
     assert got == [repr(float(x)) for x in w]
+
+
+@pytest.mark.parametrize("rows,k", [(1, 1), (3000, 50), (2048, 64), (1500, 130), (0, 5)])
+def test_expand_rows_rebuilds_dense_z(rows, k):
+    """gee_io_expand_rows (the host half of the streamed pass's row-sparse
+    Z copy) from the format built in numpy: u64 row masks, packed nonzeros,
+    per-1024-row value offsets; every bit pattern survives, -0.0 included."""
+    rng = np.random.default_rng(rows * 7 + k)
+    z = np.where(rng.random((rows, k)) < 0.2, rng.standard_normal((rows, k)), 0.0).astype(np.float32)
+    if rows:
+        z[0, -1] = -0.0
+    nz = z.view(np.uint32) != 0
+    mw = (k + 63) // 64
+    bits = np.zeros((rows, mw * 64), bool)
+    bits[:, :k] = nz
+    mask = np.packbits(bits.reshape(rows, mw, 64)[..., ::-1], axis=-1).view(">u8").reshape(rows, mw).astype(np.uint64)
+    vals = z[nz].copy()
+    nb = (rows + 1023) // 1024
+    boff = np.concatenate([[0], np.cumsum(nz.sum(1))])[::1024][:nb].astype(np.int64)
+    boff = np.concatenate([boff, [nz.sum()]]).astype(np.int64)
+    out = np.full((rows, k), np.nan, np.float32)
+    lib = formats.io_lib()
+    assert lib.gee_io_expand_rows(mask.ctypes.data, vals.ctypes.data, boff.ctypes.data, rows, k, out.ctypes.data,
+                                  4) == 0
+    assert np.array_equal(out.view(np.uint32), z.view(np.uint32))

@@ -458,11 +458,51 @@ def test_host_pipeline_matches_resident_pull(chunks):
     pipe = HostPipeline(g, k, chunks=chunks)
     assert pipe.n_chunks == chunks
     h_z = pinned_like((n, k))
-    h_z.fill_(float("nan"))
-    pipe.run(y.cpu().pin_memory(), h_z, emb)
-    assert torch.equal(h_z, z_ref)
+    for sparse in (True, False):
+        h_z.fill_(float("nan"))
+        pipe.run(y.cpu().pin_memory(), h_z, emb, sparse=sparse)
+        assert torch.equal(h_z, z_ref), sparse
+    assert 0 < pipe.d2h_bytes < n * k * 4  # the row-sparse copy-out is smaller than dense Z
     exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), w.cpu().numpy(), y.cpu().numpy(), n, k)
     assert rel_err(h_z.numpy(), exp) <= TOL
+
+
+@pytest.mark.parametrize("rows,k", [(1, 1), (1023, 50), (1024, 64), (5000, 65), (3001, 1000), (0, 7)])
+def test_z_compact_round_trip(rows, k):
+    # gee_z_compact (device) -> gee_io_expand_rows (host) rebuilds Z bit for
+    # bit; the format matches its numpy definition (u64 row masks, packed
+    # nonzeros, per-1024-row value offsets); -0.0 counts as a value
+    from paper_2402_04403_b200 import _lib
+    from paper_2402_04403_b200.formats import io_lib
+
+    rng = np.random.default_rng(rows + k)
+    zh = np.where(rng.random((rows, k)) < 0.15, rng.standard_normal((rows, k)), 0.0).astype(np.float32)
+    if rows:
+        zh[0, 0] = -0.0
+        zh[rows // 2] = 0.0
+    z = torch.from_numpy(zh).cuda()
+    mw = (k + 63) // 64
+    nb = int(_lib.lib.gee_zc_blocks(rows))
+    mask = torch.empty(max(1, rows * mw), dtype=torch.int64, device="cuda")
+    boff = torch.empty(nb + 1, dtype=torch.int64, device="cuda")
+    vals = torch.empty(max(1, rows * k), dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib.gee_z_compact(_lib.ptr(z), rows, k, _lib.ptr(mask), _lib.ptr(boff), _lib.ptr(vals),
+                                      _lib.stream_handle()))
+    torch.cuda.synchronize()
+    nz = zh.view(np.uint32) != 0
+    bits = np.zeros((rows, mw * 64), bool)
+    bits[:, :k] = nz
+    exp_mask = np.packbits(bits.reshape(rows, mw, 64)[..., ::-1], axis=-1).view(">u8").reshape(rows, mw)
+    assert np.array_equal(mask.cpu().numpy()[:rows * mw].view(np.uint64).reshape(rows, mw), exp_mask.astype(np.uint64))
+    per_row = nz.sum(1)
+    exp_off = np.concatenate([[0], np.cumsum(per_row)])[::1024][:nb]
+    assert np.array_equal(boff.cpu().numpy()[:nb], exp_off) and int(boff[nb]) == int(nz.sum())
+    assert np.array_equal(vals.cpu().numpy()[:int(nz.sum())].view(np.uint32), zh.view(np.uint32)[nz])
+    out = np.full((rows, k), np.nan, np.float32)
+    m_h, b_h, v_h = mask.cpu().numpy(), boff.cpu().numpy(), vals.cpu().numpy()
+    assert io_lib().gee_io_expand_rows(m_h.ctypes.data, v_h.ctypes.data, b_h.ctypes.data, rows, k,
+                                       out.ctypes.data, 3) == 0
+    assert np.array_equal(out.view(np.uint32), zh.view(np.uint32))
 
 
 def test_graph_prep_never_mutates_caller_or_push_arrays():
