@@ -124,6 +124,59 @@ k_gather_contig(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
     for (int64_t e = steps * 512 + gw * 32 + lane; e < arcs; e += warps * 32) cls[e] = table[targets[e]];
 }
 
+// Tiered lane-contiguous gather: slots [0, hs) come from a shared-memory copy
+// of the table head (immune to the L1 churn of the cold lookups), slots
+// [hs, hl1) through L1 with evict_last, and the rest with L1::no_allocate so
+// the cold tail does not evict the warm tier.  Lanes of one lookup
+// instruction take consecutive arcs as in k_gather_contig.
+template <bool SMEM>
+__global__ void __launch_bounds__(GTHREADS, 1)
+k_gather_tiered(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t *__restrict__ table, uint32_t hs,
+                uint32_t hl1, uint8_t *__restrict__ cls)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (SMEM) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(table);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem_raw);
+        for (uint32_t i = threadIdx.x; i < hs / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+        __syncthreads();
+    }
+    const uint64_t pol = gee::policy_evict_last();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int64_t steps = arcs / 512;
+    for (int64_t st = gw; st < steps; st += warps) {
+        const int32_t *tp = targets + st * 512 + lane;
+        uint32_t t[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++)
+            asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(t[i]) : "l"(tp + 32 * i));
+        uint32_t l[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const uint32_t ti = t[i];
+            const bool in_s = SMEM && ti < hs;
+            const bool warm = !in_s && ti < hl1;
+            const bool cold = ti >= hl1 && !in_s;
+            uint32_t a = 0, b = 0;
+            asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                         "@q ld.global.nc.L1::evict_last.L2::cache_hint.u8 %0, [%1], %3;\n\t}"
+                         : "+r"(a) : "l"(table + ti), "r"((uint32_t)warm), "l"(pol));
+            asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                         "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %3;\n\t}"
+                         : "+r"(b) : "l"(table + ti), "r"((uint32_t)cold), "l"(pol));
+            uint32_t sv = 0;
+            if (SMEM) sv = smem_raw[in_s ? ti : 0u];
+            l[i] = in_s ? sv : (a | b);
+        }
+        uint8_t *cp = cls + st * 512 + lane;
+#pragma unroll
+        for (int i = 0; i < 16; i++) cp[32 * i] = (uint8_t)l[i];
+    }
+    for (int64_t e = steps * 512 + gw * 32 + lane; e < arcs; e += warps * 32) cls[e] = table[targets[e]];
+}
+
 }  // namespace
 
 extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const void *table, int64_t n_hot, int32_t k,
@@ -156,6 +209,19 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
     // request rate for missing sectors bounds the lookups (profiles/).
     int mode = 4;
     if (const char *e = getenv("GEE_GATHER_MODE")) mode = atoi(e);
+    if (mode == 6 || mode == 7) {  // tiered: smem head (mode 7) + L1 evict_last warm tier + no-allocate tail
+        int64_t hl1 = 1 << 18;
+        if (const char *e = getenv("GEE_GATHER_L1_HOT")) hl1 = atoll(e);
+        if (hl1 < hot0) hl1 = hot0;
+        if (hl1 > 0x7fffffff) hl1 = 0x7fffffff;
+        if (mode == 6 || hot0 < 16) mode = 6, hot0 = 0;
+        const size_t sh = mode == 7 ? (size_t)hot0 : 0;
+        auto kern = mode == 7 ? k_gather_tiered<true> : k_gather_tiered<false>;
+        GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        kern<<<gee::sm_count(), GTHREADS, sh, gee::as_stream(stream)>>>(
+            targets, arcs, static_cast<const uint8_t *>(table), (uint32_t)hot0, (uint32_t)hl1, cls);
+        return gee::check_launch("k_gather_tiered");
+    }
     if (mode >= 4) {  // lane-contiguous lookups (rows sorted by slot)
         auto kc = mode == 5 ? k_gather_contig<1> : k_gather_contig<0>;
         // GEE_GATHER_BLOCK / GEE_GATHER_CTAS (per SM): co-residency experiments

@@ -182,6 +182,7 @@ class HostPipeline:
                 with torch.cuda.stream(self.s_out):
                     h_z[lo:hi].copy_(z, non_blocking=True)
                     e_out[i].record(self.s_out)
+                self.d2h_bytes += z.numel() * 4
                 continue
             if i >= 1:
                 self._drain(i - 1, e_cmp, e_out)
