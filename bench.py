@@ -408,7 +408,7 @@ def main():
     }
     peak_gbs, peak_kind = load_peaks()
     dominant = max((p for p in phase_ms if p in phase_bytes), key=lambda p: phase_ms[p])
-    kernel_of = {"project": "k_label_hist", "gather": "k_gather_contig", "blocks": "k_reduce_blocks_ring",
+    kernel_of = {"project": "k_label_hist", "gather": "k_gather_tiered", "blocks": "k_reduce_blocks_ring",
                  "heavy": "k_reduce_heavy_items", "wide": "k_wide_rows"}
     achieved = phase_bytes[dominant] / (phase_ms[dominant] * 1e-3) / 1e9
     step_bmin = s * (8 + 4 * weighted) + 4 * n + 4 * n * k  # SURVEY 8(d) B_min, whole graph
@@ -503,7 +503,8 @@ def run_e2e(g, y, emb, z, s, args, world=1):
     from paper_2402_04403_b200.stream import HostPipeline, pinned_like
 
     sparse = os.environ.get("GEE_E2E_DENSE") is None
-    pipe = HostPipeline(g, emb.k, chunks=max(1, args.e2e_chunks // world))
+    packed = None if os.environ.get("GEE_E2E_UNPACKED") is None else False
+    pipe = HostPipeline(g, emb.k, chunks=max(1, args.e2e_chunks // world), packed=packed)
     h_y = y.cpu().pin_memory()
     h_z = pinned_like((g.n, emb.k))
     pipe.run(h_y, h_z, emb, sparse=sparse)  # warm-up (sizes the scratch buffers)
@@ -528,11 +529,13 @@ def run_e2e(g, y, emb, z, s, args, world=1):
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": args.e2e_steps,
             "chunks": pipe.n_chunks, "matches_resident_pull": same, "timing": "wall clock, median",
             "path": "pinned host prepared graph + labels -> HostPipeline.run (H2D row chunks | "
-                    "gee_build_projection, gee_gather_labels, gee_reduce_blocks, gee_reduce_heavy, gee_z_compact | "
+                    "gee_unpack_targets, gee_build_projection, gee_gather_labels, gee_reduce_blocks, gee_reduce_heavy, gee_z_compact | "
                     "D2H row-sparse Z | gee_io_expand_rows on the host threads) -> pinned host Z"
                     if sparse else "pinned host prepared graph + labels -> HostPipeline.run (H2D row chunks | "
                     "gee_build_projection, gee_gather_labels, gee_reduce_blocks, gee_reduce_heavy | D2H Z) "
-                    "-> pinned host Z", "z_transfer": "row-sparse" if sparse else "dense"}
+                    "-> pinned host Z", "z_transfer": "row-sparse" if sparse else "dense",
+            "graph_transfer": "packed targets (gee_pack_targets / gee_unpack_targets), unpadded weights"
+            if pipe.packed else "padded CSR as stored"}
 
 
 if __name__ == "__main__":

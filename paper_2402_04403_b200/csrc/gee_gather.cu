@@ -129,7 +129,7 @@ k_gather_contig(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
 // [hs, hl1) through L1 with evict_last, and the rest with L1::no_allocate so
 // the cold tail does not evict the warm tier.  Lanes of one lookup
 // instruction take consecutive arcs as in k_gather_contig.
-template <bool SMEM>
+template <bool SMEM, int SPLIT>
 __global__ void __launch_bounds__(GTHREADS, 1)
 k_gather_tiered(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t *__restrict__ table, uint32_t hs,
                 uint32_t hl1, uint8_t *__restrict__ cls)
@@ -160,12 +160,18 @@ k_gather_tiered(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
             const bool warm = !in_s && ti < hl1;
             const bool cold = ti >= hl1 && !in_s;
             uint32_t a = 0, b = 0;
+            if (SPLIT == 0) {  // one load, default L1 policy
+                a = ld_label_pred<0>(table + ti, !in_s, pol);
+            } else if (SPLIT == 1) {  // one load, L1 evict_last
+                a = ld_label_pred<1>(table + ti, !in_s, pol);
+            } else {
             asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
                          "@q ld.global.nc.L1::evict_last.L2::cache_hint.u8 %0, [%1], %3;\n\t}"
                          : "+r"(a) : "l"(table + ti), "r"((uint32_t)warm), "l"(pol));
             asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
                          "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %3;\n\t}"
                          : "+r"(b) : "l"(table + ti), "r"((uint32_t)cold), "l"(pol));
+            }
             uint32_t sv = 0;
             if (SMEM) sv = smem_raw[in_s ? ti : 0u];
             l[i] = in_s ? sv : (a | b);
@@ -195,28 +201,34 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
         if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
             optin = 48 * 1024;
     }
-    // Shared-memory head of the hot tier: GEE_GATHER_SMEM_HOT=<bytes> (experiment; default 0).
-    // GEE_GATHER_MODE=<L1MODE*2 + TMODE> selects the L1 policies (experiment).
-    int64_t hot0 = 0;
+    // Default (mode 9): lane-contiguous lookups, which share sectors when rows
+    // are sorted by slot, with the hottest 96 KB of the degree-ranked tier in
+    // shared memory and the rest through L1 (evict_last) / L2 (evict_last).
+    // C4: 9.23 ms against 9.77 ms without the head (mode 4) and 10.43 ms for
+    // the 16-arcs-per-thread layout (mode 1); larger heads shrink the L1 that
+    // holds the in-flight misses (160 KB: 10.5 ms, 180 KB: 13.3 ms;
+    // profiles/r01_gather_tiers*.txt).  Without a hot tier: mode 4.
+    // Experiments: GEE_GATHER_MODE (0-3 per-thread layouts, 4/5 contiguous,
+    // 6-9 tiered), GEE_GATHER_SMEM_HOT=<bytes>, GEE_GATHER_L1_HOT=<slots>.
+    int64_t hot0 = 98304;
     if (const char *e = getenv("GEE_GATHER_SMEM_HOT")) hot0 = atoll(e);
     if (hot0 > optin - 64) hot0 = optin - 64;
     if (hot0 > n_hot) hot0 = n_hot;
     hot0 &= ~(int64_t)15;
-    // default mode 4: lane-contiguous lookups, which share sectors when rows
-    // are sorted by slot (DeviceGraph sorts them: C4 9.67 ms vs 10.43 ms for
-    // mode 1, the 16-arcs-per-thread layout with 256-bit no-allocate target
-    // loads; mode 0 = 11.15 ms).  An smem head did not pay: the L1->L2
-    // request rate for missing sectors bounds the lookups (profiles/).
-    int mode = 4;
+    int mode = hot0 >= 16384 ? 9 : 4;
     if (const char *e = getenv("GEE_GATHER_MODE")) mode = atoi(e);
-    if (mode == 6 || mode == 7) {  // tiered: smem head (mode 7) + L1 evict_last warm tier + no-allocate tail
+    if (mode >= 6 && mode <= 9) {  // tiered: smem head (mode 7) + L1 evict_last warm tier + no-allocate tail
         int64_t hl1 = 1 << 18;
         if (const char *e = getenv("GEE_GATHER_L1_HOT")) hl1 = atoll(e);
         if (hl1 < hot0) hl1 = hot0;
         if (hl1 > 0x7fffffff) hl1 = 0x7fffffff;
         if (mode == 6 || hot0 < 16) mode = 6, hot0 = 0;
-        const size_t sh = mode == 7 ? (size_t)hot0 : 0;
-        auto kern = mode == 7 ? k_gather_tiered<true> : k_gather_tiered<false>;
+        const size_t sh = mode == 6 ? 0 : (size_t)hot0;
+        // 6: L1 tiers only; 7: smem head + L1 tiers; 8 / 9: smem head + one load (L1 default / evict_last)
+        auto kern = mode == 7   ? k_gather_tiered<true, 2>
+                    : mode == 8 ? k_gather_tiered<true, 0>
+                    : mode == 9 ? k_gather_tiered<true, 1>
+                                : k_gather_tiered<false, 2>;
         GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
         kern<<<gee::sm_count(), GTHREADS, sh, gee::as_stream(stream)>>>(
             targets, arcs, static_cast<const uint8_t *>(table), (uint32_t)hot0, (uint32_t)hl1, cls);

@@ -1,0 +1,291 @@
+// Byte-width delta coding of the prepared targets, for shipping the graph
+// over PCIe (stream.HostPipeline, the e2e path).  The reference hands its
+// CsrGraph to embed_parallel in host memory (encoder.py:123-194, graph.py:54-91);
+// on C4 the targets are 15.5 GB of the 33 GB that cross PCIe per call, and
+// rows sorted by slot (gee_sort_rows) make them compressible.
+//
+// Layout.  The padded CSR (gee_pad_rows: rows are multiples of 8 arcs, pads
+// are the sentinel slot at the row's end) is cut into groups of 8 arcs; a
+// group never spans two rows.  Per group:
+//   ctl[g]  = (W - 1) | pads << 2 | row_start << 6
+//             W in 1..4 bytes per value, pads 0..7 trailing sentinel arcs
+//   payload = the group's 8 - pads real values as W-byte little-endian
+//             deltas (mod 2^32): the first arc of a row is stored absolute,
+//             every other arc relative to the previous arc of its row.
+// The payload of group g starts at the sum of the earlier groups' sizes.
+// Unsorted rows still round-trip (deltas wrap mod 2^32); they compress less.
+//
+// Decode (gee_unpack_targets, inside the timed e2e region; no allocation):
+//   1. exclusive scan over (payload bytes, pads) per group -> the group's
+//      payload offset and real-arc index (for the weight copy);
+//   2. per group, the sum of its deltas; an inclusive segmented scan over
+//      (sum, row_start) gives each group's last target;
+//   3. per group, rebuild the 8 padded targets (sentinel for pads) and copy
+//      the row's real weights into the padded weight layout (pads 0).
+#include <cub/cub.cuh>
+#include <thrust/iterator/transform_iterator.h>
+
+#include "gee_common.cuh"
+
+namespace {
+
+constexpr int PT = 256;
+
+struct SegSum {  // segmented-scan element: running value, "a row starts here"
+    uint32_t val;
+    uint32_t flag;
+};
+
+struct SegOp {
+    __device__ __forceinline__ SegSum operator()(const SegSum &a, const SegSum &b) const
+    {
+        return b.flag ? b : SegSum{a.val + b.val, a.flag};
+    }
+};
+
+struct Pos {  // payload bytes and pad arcs before a group
+    uint64_t bytes;
+    uint64_t pads;
+};
+
+struct PosSum {
+    __host__ __device__ __forceinline__ Pos operator()(const Pos &a, const Pos &b) const
+    {
+        return Pos{a.bytes + b.bytes, a.pads + b.pads};
+    }
+};
+
+struct CtlToPos {  // ctl byte -> (payload bytes, pads) of the group
+    __host__ __device__ __forceinline__ Pos operator()(uint8_t c) const
+    {
+        const uint32_t w = (c & 3u) + 1u, pads = (c >> 2) & 15u;
+        return Pos{(uint64_t)((8u - pads) * w), (uint64_t)pads};
+    }
+};
+
+__device__ __forceinline__ uint32_t width_of(uint32_t d) { return d < 0x100u ? 1u : d < 0x10000u ? 2u : d < 0x1000000u ? 3u : 4u; }
+
+__global__ void k_mark_row_starts(const int64_t *__restrict__ off, int64_t rows, uint8_t *__restrict__ start)
+{
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = off[r];
+        if (off[r + 1] > a) start[a >> 3] = 1;
+    }
+}
+
+// ctl byte per group (start[] holds the row-start flags, 0/1)
+__global__ void k_pack_ctl(const int32_t *__restrict__ t, int64_t groups, uint32_t sentinel, uint8_t *__restrict__ ctl,
+                           const uint8_t *__restrict__ start, int *__restrict__ bad)
+{
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+        const bool rs = start[g] != 0;
+        uint32_t prev = rs ? 0u : (uint32_t)t[8 * g - 1];
+        uint32_t pads = 0, w = 1;
+        for (int i = 0; i < 8; i++) {
+            const uint32_t v = (uint32_t)t[8 * g + i];
+            if (v == sentinel) {
+                pads++;
+                continue;
+            }
+            if (pads) atomicExch(bad, 1);  // a real arc after a pad: not the padded layout
+            w = max(w, width_of(v - prev));
+            prev = v;
+        }
+        if (pads == 8) atomicExch(bad, 1);  // whole-pad group: not the padded layout
+        ctl[g] = (uint8_t)((w - 1) | pads << 2 | (rs ? 64u : 0u));
+    }
+}
+
+__global__ void k_pack_payload(const int32_t *__restrict__ t, int64_t groups, const uint8_t *__restrict__ ctl,
+                               const Pos *__restrict__ pos, uint8_t *__restrict__ payload)
+{
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = ctl[g], w = (c & 3u) + 1u, real = 8u - ((c >> 2) & 15u);
+        uint8_t *p = payload + pos[g].bytes;
+        uint32_t prev = (c & 64u) ? 0u : (uint32_t)t[8 * g - 1];
+        for (uint32_t i = 0; i < real; i++) {
+            const uint32_t v = (uint32_t)t[8 * g + i];
+            const uint32_t d = v - prev;
+            prev = v;
+            for (uint32_t b = 0; b < w; b++) *p++ = (uint8_t)(d >> (8 * b));
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t ld_delta(const uint8_t *p, uint32_t w)
+{
+    uint32_t d = p[0];
+    if (w > 1) d |= (uint32_t)p[1] << 8;
+    if (w > 2) d |= (uint32_t)p[2] << 16;
+    if (w > 3) d |= (uint32_t)p[3] << 24;
+    return d;
+}
+
+__global__ void __launch_bounds__(PT) k_unpack_sums(const uint8_t *__restrict__ ctl, const uint8_t *__restrict__ payload,
+                                                    int64_t groups, const Pos *__restrict__ pos,
+                                                    SegSum *__restrict__ seg)
+{
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = ctl[g], w = (c & 3u) + 1u, real = 8u - ((c >> 2) & 15u);
+        const uint8_t *p = payload + pos[g].bytes;
+        uint32_t s = 0;
+        for (uint32_t i = 0; i < real; i++) s += ld_delta(p + i * w, w);
+        seg[g] = SegSum{s, (c >> 6) & 1u};
+    }
+}
+
+__global__ void __launch_bounds__(PT) k_unpack_rows(const uint8_t *__restrict__ ctl, const uint8_t *__restrict__ payload,
+                                                    int64_t groups, const Pos *__restrict__ pos,
+                                                    const SegSum *__restrict__ last, const float *__restrict__ w_real,
+                                                    uint32_t sentinel, int32_t *__restrict__ t, float *__restrict__ w_pad)
+{
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = ctl[g], w = (c & 3u) + 1u, pads = (c >> 2) & 15u, real = 8u - pads;
+        const Pos ps = pos[g];
+        const uint8_t *p = payload + ps.bytes;
+        uint32_t v = ((c & 64u) || g == 0) ? 0u : last[g - 1].val;
+        uint32_t o[8];
+#pragma unroll
+        for (uint32_t i = 0; i < 8; i++) {
+            if (i < real) {
+                v += ld_delta(p + i * w, w);
+                o[i] = v;
+            } else {
+                o[i] = sentinel;
+            }
+        }
+        int4 *tp = reinterpret_cast<int4 *>(t + 8 * g);
+        __stcs(tp, make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]));
+        __stcs(tp + 1, make_int4((int)o[4], (int)o[5], (int)o[6], (int)o[7]));
+        if (w_real) {
+            const float *src = w_real + (8 * g - (int64_t)ps.pads);  // real arcs before this group
+            float x[8];
+#pragma unroll
+            for (uint32_t i = 0; i < 8; i++) x[i] = i < real ? __ldcs(src + i) : 0.f;
+            float4 *wp = reinterpret_cast<float4 *>(w_pad + 8 * g);
+            __stcs(wp, make_float4(x[0], x[1], x[2], x[3]));
+            __stcs(wp + 1, make_float4(x[4], x[5], x[6], x[7]));
+        }
+    }
+}
+
+inline int grid_of(int64_t items) { return (int)std::min<int64_t>((items + PT - 1) / PT, (int64_t)gee::sm_count() * 16); }
+
+size_t cub_scan_bytes(int64_t groups)
+{
+    size_t a = 0, b = 0;
+    auto it = thrust::make_transform_iterator((const uint8_t *)nullptr, CtlToPos());
+    cub::DeviceScan::ExclusiveScan(nullptr, a, it, (Pos *)nullptr, PosSum(), Pos{0, 0}, groups);
+    cub::DeviceScan::InclusiveScan(nullptr, b, (SegSum *)nullptr, (SegSum *)nullptr, SegOp(), groups);
+    return std::max(a, b);
+}
+
+inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+}  // namespace
+
+extern "C" {
+
+size_t gee_unpack_scratch_bytes(int64_t groups)
+{
+    if (groups <= 0) return 0;
+    return align256((size_t)groups * sizeof(Pos)) + align256((size_t)groups * sizeof(SegSum)) +
+           align256(cub_scan_bytes(groups));
+}
+
+int gee_pack_targets(const int64_t *padded_offsets, int64_t rows, const int32_t *targets, int64_t padded_arcs,
+                     int32_t sentinel, uint8_t *ctl, uint8_t *payload, int64_t *payload_bytes, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(rows >= 0 && padded_arcs >= 0 && (padded_arcs & 7) == 0, GEE_ERR_INVALID,
+                "padded_arcs must be a nonnegative multiple of 8");
+    GEE_REQUIRE(payload_bytes != nullptr, GEE_ERR_INVALID, "payload_bytes must not be NULL");
+    *payload_bytes = 0;
+    const int64_t groups = padded_arcs / 8;
+    if (groups == 0) return GEE_OK;
+    GEE_REQUIRE(padded_offsets && targets && ctl && payload, GEE_ERR_INVALID, "NULL array argument");
+    cudaStream_t st = gee::as_stream(stream);
+    uint8_t *start = nullptr;
+    Pos *pos = nullptr;
+    int *bad = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int rc = GEE_OK, hbad = 0;
+    Pos tail[1];
+    auto it = thrust::make_transform_iterator((const uint8_t *)ctl, CtlToPos());
+    auto fail = [&](int code, const char *msg) {
+        gee::set_error("gee_pack_targets: %s", msg);
+        rc = code;
+    };
+    if (cudaMallocAsync(&start, groups, st) != cudaSuccess || cudaMallocAsync(&pos, groups * sizeof(Pos), st) != cudaSuccess ||
+        cudaMallocAsync(&bad, sizeof(int), st) != cudaSuccess) {
+        fail(GEE_ERR_CUDA, "scratch alloc failed");
+        goto out;
+    }
+    cudaMemsetAsync(start, 0, groups, st);
+    cudaMemsetAsync(bad, 0, sizeof(int), st);
+    k_mark_row_starts<<<grid_of(rows), PT, 0, st>>>(padded_offsets, rows, start);
+    k_pack_ctl<<<grid_of(groups), PT, 0, st>>>(targets, groups, (uint32_t)sentinel, ctl, start, bad);
+    cub::DeviceScan::ExclusiveScan(nullptr, tmp_bytes, it, pos, PosSum(), Pos{0, 0}, groups, st);
+    if (cudaMallocAsync(&tmp, tmp_bytes, st) != cudaSuccess) {
+        fail(GEE_ERR_CUDA, "scan scratch alloc failed");
+        goto out;
+    }
+    cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, it, pos, PosSum(), Pos{0, 0}, groups, st);
+    k_pack_payload<<<grid_of(groups), PT, 0, st>>>(targets, groups, ctl, pos, payload);
+    if ((rc = gee::check_launch("k_pack_payload"))) goto out;
+    cudaMemcpyAsync(tail, pos + groups - 1, sizeof(Pos), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+        fail(GEE_ERR_CUDA, "sync failed");
+        goto out;
+    }
+    if (hbad) {
+        fail(GEE_ERR_INVALID, "targets are not in the padded layout (pads must end a row, < 8 per row)");
+        goto out;
+    }
+    {
+        uint8_t last = 0;
+        cudaMemcpy(&last, ctl + groups - 1, 1, cudaMemcpyDeviceToHost);
+        *payload_bytes = (int64_t)(tail[0].bytes + CtlToPos()(last).bytes);
+    }
+out:
+    if (tmp) cudaFreeAsync(tmp, st);
+    if (start) cudaFreeAsync(start, st);
+    if (pos) cudaFreeAsync(pos, st);
+    if (bad) cudaFreeAsync(bad, st);
+    return rc;
+}
+
+int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t groups, const float *w_real,
+                       int32_t sentinel, int32_t *targets, float *w_padded, void *scratch, size_t scratch_bytes,
+                       void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(groups >= 0, GEE_ERR_INVALID, "groups must be nonnegative");
+    if (groups == 0) return GEE_OK;
+    GEE_REQUIRE(ctl && payload && targets && (!w_real || w_padded) && scratch, GEE_ERR_INVALID,
+                "NULL array argument");
+    GEE_REQUIRE(((uintptr_t)targets & 15) == 0 && (!w_padded || ((uintptr_t)w_padded & 15) == 0), GEE_ERR_INVALID,
+                "targets / w_padded must be 16-byte aligned");
+    GEE_REQUIRE(scratch_bytes >= gee_unpack_scratch_bytes(groups), GEE_ERR_INVALID,
+                "scratch too small (gee_unpack_scratch_bytes)");
+    cudaStream_t st = gee::as_stream(stream);
+    auto *pos = static_cast<Pos *>(scratch);
+    const size_t pos_b = align256((size_t)groups * sizeof(Pos));
+    auto *seg = reinterpret_cast<SegSum *>(static_cast<char *>(scratch) + pos_b);
+    void *tmp = static_cast<char *>(scratch) + pos_b + align256((size_t)groups * sizeof(SegSum));
+    size_t tmp_bytes = cub_scan_bytes(groups);
+    auto it = thrust::make_transform_iterator((const uint8_t *)ctl, CtlToPos());
+    GEE_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, it, pos, PosSum(), Pos{0, 0}, groups, st));
+    k_unpack_sums<<<grid_of(groups), PT, 0, st>>>(ctl, payload, groups, pos, seg);
+    int rc;
+    if ((rc = gee::check_launch("k_unpack_sums"))) return rc;
+    tmp_bytes = cub_scan_bytes(groups);
+    GEE_CUDA(cub::DeviceScan::InclusiveScan(tmp, tmp_bytes, seg, seg, SegOp(), groups, st));
+    k_unpack_rows<<<grid_of(groups), PT, 0, st>>>(ctl, payload, groups, pos, seg, w_real, (uint32_t)sentinel, targets,
+                                                  w_real ? w_padded : nullptr);
+    return gee::check_launch("k_unpack_rows");
+}
+
+}  // extern "C"

@@ -9,6 +9,7 @@ Bar (BASELINE.json north_star):
   * the pull variant bit-stable run to run.
 """
 
+import ctypes
 import numpy as np
 import pytest
 
@@ -439,7 +440,8 @@ def test_raw_ctypes_binding_without_torch():
 
 
 @pytest.mark.parametrize("chunks", [1, 3, 7])
-def test_host_pipeline_matches_resident_pull(chunks):
+@pytest.mark.parametrize("packed", [True, False])
+def test_host_pipeline_matches_resident_pull(chunks, packed):
     # stream.HostPipeline: pinned host graph + labels -> pinned host Z via
     # row chunks on three streams; every chunk's pull sums the same integers
     # as the resident pull, so Z is bit-identical
@@ -455,8 +457,8 @@ def test_host_pipeline_matches_resident_pull(chunks):
     emb = Embedder(n, k, dev)
     emb.project(y, g=g)
     z_ref = emb.pull(g).cpu()
-    pipe = HostPipeline(g, k, chunks=chunks)
-    assert pipe.n_chunks == chunks
+    pipe = HostPipeline(g, k, chunks=chunks, packed=packed)
+    assert pipe.n_chunks == chunks and pipe.packed == packed
     h_z = pinned_like((n, k))
     for sparse in (True, False):
         h_z.fill_(float("nan"))
@@ -529,3 +531,101 @@ def test_graph_prep_never_mutates_caller_or_push_arrays():
     zp = emb.embed(g, yd, variant="pull").cpu().numpy()
     zq = emb.embed(g, yd, variant="push").cpu().numpy()
     assert rel_err(zp, zq.astype(np.float64)) <= TOL
+
+
+def _pack_round_trip(off, tgt, w, sentinel):
+    from paper_2402_04403_b200 import _lib
+
+    dev = torch.device("cuda")
+    off_d = torch.as_tensor(off, dtype=torch.int64, device=dev)
+    t_d = torch.as_tensor(tgt, dtype=torch.int32, device=dev)
+    arcs = t_d.numel()
+    groups = arcs // 8
+    ctl = torch.empty(max(1, groups), dtype=torch.uint8, device=dev)
+    pay = torch.empty(max(1, 4 * arcs), dtype=torch.uint8, device=dev)
+    nb = ctypes.c_int64()
+    _lib.check(_lib.lib.gee_pack_targets(_lib.ptr(off_d), off_d.numel() - 1, _lib.ptr(t_d), arcs, sentinel,
+                                         _lib.ptr(ctl), _lib.ptr(pay), ctypes.byref(nb), _lib.stream_handle()),
+               "pack")
+    real = t_d != sentinel
+    w_real = torch.as_tensor(w, dtype=torch.float32, device=dev)[real] if w is not None else None
+    sb = int(_lib.lib.gee_unpack_scratch_bytes(groups))
+    scratch = torch.empty(max(1, sb), dtype=torch.uint8, device=dev)
+    out_t = torch.full((arcs + 8,), -7, dtype=torch.int32, device=dev)
+    out_w = torch.full((arcs + 8,), -7.0, dtype=torch.float32, device=dev) if w is not None else None
+    # the payload a PCIe copy would deliver: exactly nb bytes, followed by junk
+    pay2 = torch.full((int(nb.value) + 64,), 0xAB, dtype=torch.uint8, device=dev)
+    pay2[:int(nb.value)] = pay[:int(nb.value)]
+    _lib.check(_lib.lib.gee_unpack_targets(_lib.ptr(ctl), _lib.ptr(pay2), groups, _lib.ptr(w_real), sentinel,
+                                           _lib.ptr(out_t), _lib.ptr(out_w), _lib.ptr(scratch), sb,
+                                           _lib.stream_handle()), "unpack")
+    torch.cuda.synchronize()
+    assert torch.equal(out_t[:arcs], t_d) and bool((out_t[arcs:] == -7).all())
+    if w is not None:
+        exp_w = torch.as_tensor(w, dtype=torch.float32, device=dev)
+        assert torch.equal(out_w[:arcs], torch.where(real, exp_w, torch.zeros_like(exp_w)))
+        assert bool((out_w[arcs:] == -7.0).all())
+    return int(nb.value)
+
+
+def _padded_rows(degs, rng, sentinel, sort=True, big=False):
+    off, tgt, w = [0], [], []
+    for d in degs:
+        hi = sentinel if big else min(sentinel, 1 << 20)
+        row = rng.integers(0, hi, d)
+        if sort:
+            row = np.sort(row)
+        pad = (-d) % 8
+        tgt += list(row) + [sentinel] * pad
+        w += list(rng.random(d).astype(np.float32) + 0.25) + [0.0] * pad
+        off.append(len(tgt))
+    return np.array(off), np.array(tgt, dtype=np.int64), np.array(w, dtype=np.float32)
+
+
+@pytest.mark.parametrize("case", ["mixed", "unsorted", "wide", "single", "empty_rows"])
+def test_pack_targets_round_trip(case):
+    # gee_pack_targets -> gee_unpack_targets rebuilds the padded targets and
+    # weights bit for bit: rows of every length (0, 1, 8, 9, heavy), pads,
+    # unsorted rows (deltas wrap mod 2^32) and 4-byte deltas
+    rng = np.random.default_rng(len(case))
+    sentinel = (1 << 31) - 2 if case == "wide" else 5_000_000
+    if case == "single":
+        degs = [3]
+    elif case == "empty_rows":
+        degs = [0, 0, 5, 0, 8, 0, 0, 17, 0]
+    else:
+        degs = list(rng.integers(0, 40, 3000)) + [0, 1, 8, 9, 7, 16, 5000, 70_000]
+        rng.shuffle(degs)
+    off, tgt, w = _padded_rows(degs, rng, sentinel, sort=case != "unsorted", big=case == "wide")
+    nb = _pack_round_trip(off, tgt, w, sentinel)
+    _pack_round_trip(off, tgt, None, sentinel)
+    if case == "mixed":  # sorted rows code in well under 4 bytes per real arc
+        assert nb < 3 * int((tgt != sentinel).sum())
+
+
+def test_pack_targets_many_pads():
+    # more than 2^24 pad arcs in one call (C4's chunks hold ~18M): the
+    # real-arc index of every group (for the weight copy) stays exact
+    rows = 2_500_000
+    rng = np.random.default_rng(5)
+    sentinel = 1 << 27
+    tgt = np.full((rows, 8), sentinel, dtype=np.int64)
+    tgt[:, 0] = rng.integers(0, sentinel, rows)
+    w = np.zeros((rows, 8), dtype=np.float32)
+    w[:, 0] = rng.random(rows, dtype=np.float32) + 0.5
+    off = np.arange(0, 8 * rows + 1, 8)
+    _pack_round_trip(off, tgt.ravel(), w.ravel(), sentinel)
+
+
+def test_pack_targets_rejects_unpadded():
+    from paper_2402_04403_b200 import _lib
+
+    dev = torch.device("cuda")
+    off = torch.tensor([0, 16], dtype=torch.int64, device=dev)
+    t = torch.tensor([1, 2, 3, 9, 9, 9, 9, 9, 9, 9, 9, 9, 9, 9, 9, 9], dtype=torch.int32, device=dev)  # 13 pads
+    ctl = torch.empty(2, dtype=torch.uint8, device=dev)
+    pay = torch.empty(64, dtype=torch.uint8, device=dev)
+    nb = ctypes.c_int64()
+    rc = _lib.lib.gee_pack_targets(_lib.ptr(off), 1, _lib.ptr(t), 16, 9, _lib.ptr(ctl), _lib.ptr(pay),
+                                   ctypes.byref(nb), _lib.stream_handle())
+    assert rc != 0 and b"padded layout" in _lib.lib.gee_last_error()
