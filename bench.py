@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (smaller runs)")
     ap.add_argument("--edges", type=int, default=None, help="edge-count override")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-chunks", type=int, default=16)
+    ap.add_argument("--e2e-chunks", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-push", action="store_true")

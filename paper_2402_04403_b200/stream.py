@@ -38,6 +38,7 @@ the timed region, as the reference's ``build_csr`` is (bench.py:1-7 there).
 """
 
 import ctypes
+import threading
 
 import numpy as np
 import torch
@@ -55,6 +56,7 @@ class HostPipeline:
         if not g.has_pull or g.hot_k != k:
             raise ValidationError("HostPipeline needs a pull graph prepared for k (prepare_hot)")
         self.device = device or g.device
+        self.dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         # a row shard streams its own rows; labels and hot ranks cover all nodes
         self.n, self.n_nodes, self.k, self.s = g.n, g.n_nodes, k, g.s
         self.weighted = g.weighted
@@ -198,67 +200,108 @@ class HostPipeline:
         e_cmp = [ev() for _ in self.views]
         e_out = [ev() for _ in self.views]
         self.d2h_bytes = 0
-        for i, v in enumerate(self.views):
-            b = i & 1
-            lo, hi, a0, a1 = v.span
-            with torch.cuda.stream(self.s_in):
-                if i >= 2:
-                    self.s_in.wait_event(e_cmp[i - 2])  # slot b's CSR is free
-                self.d_off[b][:hi - lo + 1].copy_(self.h_off[i], non_blocking=True)
-                if self.packed:
-                    self.d_ctl[b][:self.h_ctl[i].numel()].copy_(self.h_ctl[i], non_blocking=True)
-                    self.d_pay[b][:self.h_pay[i].numel()].copy_(self.h_pay[i], non_blocking=True)
-                    if self.weighted:
-                        self.d_wr[b][:self.h_wr[i].numel()].copy_(self.h_wr[i], non_blocking=True)
-                else:
-                    self.d_tgt[b][:a1 - a0].copy_(self.h_tgt[a0:a1], non_blocking=True)
-                    if self.weighted:
-                        self.d_w[b][:a1 - a0].copy_(self.h_w[a0:a1], non_blocking=True)
-                e_in[i].record(self.s_in)
-            self.s_cmp.wait_event(e_in[i])
-            if i >= 2 and not sparse:
-                self.s_cmp.wait_event(e_out[i - 2])  # Z slot b has been copied out
-            with torch.cuda.stream(self.s_cmp):
-                if self.packed:
-                    _lib.check(_lib.lib.gee_unpack_targets(
-                        _lib.ptr(self.d_ctl[b]), _lib.ptr(self.d_pay[b]), (a1 - a0) // 8,
-                        _lib.ptr(self.d_wr[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
-                        _lib.ptr(self.d_w[b]) if self.weighted else None, _lib.ptr(self.d_scratch),
-                        self.scratch_bytes, _lib.stream_handle(self.s_cmp)), "gee_unpack_targets")
-                v.offsets = self.d_off[b][:hi - lo + 1]
-                v.targets = self.d_tgt[b][:a1 - a0]
-                v.weights = self.d_w[b][:a1 - a0] if self.weighted else None
-                z = self.d_z[b][:(hi - lo) * self.k].view(hi - lo, self.k)
-                emb.pull(v, z)
-                if sparse:
-                    if i >= 2:
-                        self.s_cmp.wait_event(e_out[i - 2])  # compact slot b has been copied out
-                    _lib.check(_lib.lib.gee_z_compact(_lib.ptr(z), hi - lo, self.k, _lib.ptr(self.cm[b]),
-                                                      _lib.ptr(self.cb[b]), _lib.ptr(self.cv[b]),
-                                                      _lib.stream_handle(self.s_cmp)), "gee_z_compact")
-                    nb = int(_lib.lib.gee_zc_blocks(hi - lo))
-                    self.h_tot[i:i + 1].copy_(self.cb[b][nb:nb + 1], non_blocking=True)
-                e_cmp[i].record(self.s_cmp)
-            if not sparse:
-                self.s_out.wait_event(e_cmp[i])
-                with torch.cuda.stream(self.s_out):
-                    h_z[lo:hi].copy_(z, non_blocking=True)
-                    e_out[i].record(self.s_out)
-                self.d2h_bytes += z.numel() * 4
-                continue
-            if i >= 1:
-                self._drain(i - 1, e_cmp, e_out)
-            if i >= 2:
-                self._expand(i - 2, e_out, h_z)
-        if sparse:
-            if nv >= 1:
-                self._drain(nv - 1, e_cmp, e_out)
-            for j in range(max(0, nv - 2), nv):
-                self._expand(j, e_out, h_z)
+        # sparse copy-out: a host worker drains chunk i (its size is known once
+        # the chunk is compacted) and expands chunk i-1 into h_z, so the main
+        # thread keeps the copy-in and compute queues fed meanwhile
+        recorded = [threading.Event() for _ in self.views]
+        drained = [threading.Event() for _ in self.views]
+        errors = []
+        worker = None
+        if sparse and nv:
+            worker = threading.Thread(target=self._sparse_worker,
+                                      args=(e_cmp, e_out, h_z, recorded, drained, errors), daemon=True)
+            worker.start()
+        try:
+            for i, v in enumerate(self.views):
+                self._issue_chunk(i, v, emb, h_z, sparse, e_in, e_cmp, e_out, drained, errors)
+                recorded[i].set()
+        except BaseException as e:
+            errors.append(e)  # stops the worker before it drains an unissued chunk
+            raise
+        finally:
+            for r in recorded:
+                r.set()  # a failed issue must not leave the worker waiting
+            if worker is not None:
+                worker.join()
+        if errors:
+            raise errors[0]
         self.s_out.synchronize()
         for v in self.views:
             v.offsets = v.targets = v.weights = None
         return h_z
+
+    def _issue_chunk(self, i, v, emb, h_z, sparse, e_in, e_cmp, e_out, drained, errors):
+        """Main thread: queue chunk i's copy-in, decode, pull and compaction."""
+        b = i & 1
+        lo, hi, a0, a1 = v.span
+        with torch.cuda.stream(self.s_in):
+            if i >= 2:
+                self.s_in.wait_event(e_cmp[i - 2])  # slot b's CSR is free
+            self.d_off[b][:hi - lo + 1].copy_(self.h_off[i], non_blocking=True)
+            if self.packed:
+                self.d_ctl[b][:self.h_ctl[i].numel()].copy_(self.h_ctl[i], non_blocking=True)
+                self.d_pay[b][:self.h_pay[i].numel()].copy_(self.h_pay[i], non_blocking=True)
+                if self.weighted:
+                    self.d_wr[b][:self.h_wr[i].numel()].copy_(self.h_wr[i], non_blocking=True)
+            else:
+                self.d_tgt[b][:a1 - a0].copy_(self.h_tgt[a0:a1], non_blocking=True)
+                if self.weighted:
+                    self.d_w[b][:a1 - a0].copy_(self.h_w[a0:a1], non_blocking=True)
+            e_in[i].record(self.s_in)
+        self.s_cmp.wait_event(e_in[i])
+        if i >= 2 and not sparse:
+            self.s_cmp.wait_event(e_out[i - 2])  # Z slot b has been copied out
+        with torch.cuda.stream(self.s_cmp):
+            if self.packed:
+                _lib.check(_lib.lib.gee_unpack_targets(
+                    _lib.ptr(self.d_ctl[b]), _lib.ptr(self.d_pay[b]), (a1 - a0) // 8,
+                    _lib.ptr(self.d_wr[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
+                    _lib.ptr(self.d_w[b]) if self.weighted else None, _lib.ptr(self.d_scratch),
+                    self.scratch_bytes, _lib.stream_handle(self.s_cmp)), "gee_unpack_targets")
+            v.offsets = self.d_off[b][:hi - lo + 1]
+            v.targets = self.d_tgt[b][:a1 - a0]
+            v.weights = self.d_w[b][:a1 - a0] if self.weighted else None
+            z = self.d_z[b][:(hi - lo) * self.k].view(hi - lo, self.k)
+            emb.pull(v, z)
+            if sparse:
+                if i >= 2:
+                    drained[i - 2].wait()  # the worker has queued chunk i-2's copy-out
+                    if errors:
+                        raise errors[0]
+                    self.s_cmp.wait_event(e_out[i - 2])  # compact slot b has been copied out
+                _lib.check(_lib.lib.gee_z_compact(_lib.ptr(z), hi - lo, self.k, _lib.ptr(self.cm[b]),
+                                                  _lib.ptr(self.cb[b]), _lib.ptr(self.cv[b]),
+                                                  _lib.stream_handle(self.s_cmp)), "gee_z_compact")
+                nb = int(_lib.lib.gee_zc_blocks(hi - lo))
+                self.h_tot[i:i + 1].copy_(self.cb[b][nb:nb + 1], non_blocking=True)
+            e_cmp[i].record(self.s_cmp)
+        if not sparse:
+            self.s_out.wait_event(e_cmp[i])
+            with torch.cuda.stream(self.s_out):
+                h_z[lo:hi].copy_(z, non_blocking=True)
+                e_out[i].record(self.s_out)
+            self.d2h_bytes += z.numel() * 4
+
+    def _sparse_worker(self, e_cmp, e_out, h_z, recorded, drained, errors):
+        """Host worker: drain chunk i, then expand chunk i-1 (slot reuse:
+        drain(i) overwrites the host slot that expand(i-2) has finished with)."""
+        try:
+            torch.cuda.set_device(self.dev_index)
+            nv = len(self.views)
+            for i in range(nv):
+                recorded[i].wait()
+                if errors:
+                    return
+                self._drain(i, e_cmp, e_out)
+                drained[i].set()
+                if i >= 1:
+                    self._expand(i - 1, e_out, h_z)
+            self._expand(nv - 1, e_out, h_z)
+        except BaseException as e:  # surfaced by run()
+            errors.append(e)
+        finally:
+            for d in drained:
+                d.set()
 
     def _drain(self, i, e_cmp, e_out):
         """Host: once chunk i is compacted, copy its sparse Z out (size now known)."""
