@@ -64,3 +64,38 @@ print(f"full run sparse: {timed(lambda: pipe.run(h_y, h_z, emb)):.1f} ms")
 t0 = time.perf_counter()
 h_z.fill_(0.0)
 print(f"host fill of Z ({h_z.numel() * 4 / 1e9:.1f} GB): {(time.perf_counter() - t0) * 1e3:.1f} ms")
+import threading  # noqa: E402
+
+
+def expand_all():
+    # every chunk's expansion from slot 0's compacted rows (host write rate)
+    from paper_2402_04403_b200.formats import io_lib
+    import ctypes
+    from paper_2402_04403_b200 import _lib
+    lo, hi, _, _ = pipe.views[0].span
+    for i in range(len(pipe.views)):
+        io_lib().gee_io_expand_rows(_lib.ptr(pipe.hm[0]), _lib.ptr(pipe.hv[0]), _lib.ptr(pipe.hb[0]), hi - lo, k,
+                                    ctypes.c_void_p(h_z.data_ptr()), 0)
+
+
+print(f"expand x{len(pipe.views)} chunks alone: {timed(expand_all):.1f} ms")
+
+
+def copy_in_with_fill():
+    t = threading.Thread(target=lambda: h_z.fill_(0.0))
+    t.start()
+    copy_in()
+    t.join()
+
+
+print(f"copy-in + host fill of Z concurrently: {timed(copy_in_with_fill):.1f} ms")
+
+
+def copy_in_with_expand():
+    t = threading.Thread(target=expand_all)
+    t.start()
+    copy_in()
+    t.join()
+
+
+print(f"copy-in + expand concurrently: {timed(copy_in_with_expand):.1f} ms")
