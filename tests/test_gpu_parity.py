@@ -629,3 +629,32 @@ def test_pack_targets_rejects_unpadded():
     rc = _lib.lib.gee_pack_targets(_lib.ptr(off), 1, _lib.ptr(t), 16, 9, _lib.ptr(ctl), _lib.ptr(pay),
                                    ctypes.byref(nb), _lib.stream_handle())
     assert rc != 0 and b"padded layout" in _lib.lib.gee_last_error()
+
+
+@pytest.mark.parametrize("mode,head", [(None, None), ("10", "40000"), ("9", None), ("4", None), ("1", None)])
+@pytest.mark.parametrize("k", [5, 20, 50, 63, 64, 200])
+def test_gather_labels_modes(k, mode, head, monkeypatch):
+    # gee_gather_labels equals a plain gather for every kernel variant: the
+    # packed shared-memory head (5 / 6 / 8 labels per word by k), the byte
+    # head, contiguous and per-thread layouts; skewed slots hit the head,
+    # the hot tier and the cold tier; ragged lengths exercise the tails
+    from paper_2402_04403_b200 import _lib
+
+    if mode:
+        monkeypatch.setenv("GEE_GATHER_MODE", mode)
+    if head:
+        monkeypatch.setenv("GEE_GATHER_SMEM_HOT", head)
+    gen = torch.Generator(device="cuda").manual_seed(k)
+    n_hot, n = 300_000, 2_000_000
+    table = torch.randint(0, k + 1, (n_hot + n + 1,), dtype=torch.uint8, device="cuda", generator=gen)
+    for arcs in (5, 512 * 148 * 32 + 77, 3_000_001):
+        u = torch.rand(arcs, device="cuda", generator=gen)
+        t = torch.where(u < 0.5, (u * 200_000).long(), torch.where(
+            u < 0.75, (u * n_hot).long() % n_hot, torch.randint(0, n_hot + n + 1, (arcs,), device="cuda",
+                                                                 generator=gen))).int()
+        cls = torch.full((arcs + 16,), 255, dtype=torch.uint8, device="cuda")
+        _lib.check(_lib.lib.gee_gather_labels(_lib.ptr(t), arcs, _lib.ptr(table), n_hot, k, _lib.ptr(cls),
+                                              _lib.stream_handle()), "gee_gather_labels")
+        torch.cuda.synchronize()
+        assert torch.equal(cls[:arcs], table[t.long()]), arcs
+        assert bool((cls[arcs:] == 255).all()), arcs
