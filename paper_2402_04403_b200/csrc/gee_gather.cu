@@ -278,7 +278,9 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
         auto kern = per == 8 ? k_gather_packed<8> : per == 6 ? k_gather_packed<6> : per == 5 ? k_gather_packed<5>
                                                                                            : k_gather_packed<4>;
         GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-        kern<<<gee::sm_count(), GTHREADS, sh, gee::as_stream(stream)>>>(
+        int bt = GTHREADS;  // GEE_GATHER_BLOCK: fewer lookups in flight (experiment)
+        if (const char *e = getenv("GEE_GATHER_BLOCK")) bt = atoi(e);
+        kern<<<gee::sm_count(), bt, sh, gee::as_stream(stream)>>>(
             targets, arcs, static_cast<const uint8_t *>(table), (uint32_t)hl, cls);
         return gee::check_launch("k_gather_packed");
     }

@@ -6,7 +6,6 @@ run() {
   env "$@" python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-push 2>/dev/null |
     python -c "import json,sys; d=json.loads(sys.stdin.readline()); p=d['roofline']['phases']; print('$*', 'gather %.3f' % p['gather']['ms'], 'step %.3f' % d['ms_per_step'])"
 }
-run GEE_GATHER_MODE=9
-for m in ${MODES:-10}; do
-  for sm in ${SMEMS:-65536 81920 98304 114688 131072}; do run GEE_GATHER_MODE=$m GEE_GATHER_SMEM_HOT=$sm; done
+for bt in ${BLOCKS:-512 768 1024}; do
+  for sm in ${SMEMS:-98304 131072 163840 196608}; do run GEE_GATHER_BLOCK=$bt GEE_GATHER_SMEM_HOT=$sm; done
 done
