@@ -234,24 +234,31 @@ int64_t gee_zc_blocks(int64_t rows);
 int gee_z_compact(const float *z, int64_t rows, int32_t k, unsigned long long *mask, int64_t *block_off,
                   float *vals, void *stream);
 
-/* Compressed targets for the host -> device path (csrc/gee_pack.cu).  The
+/* Compressed graph for the host -> device path (csrc/gee_pack.cu).  The
  * reference passes its CsrGraph to embed_parallel in host memory
  * (encoder.py:123-194, graph.py:54-91); these code the prepared, padded,
- * slot-sorted targets as per-8-arc groups of byte-width deltas so fewer bytes
- * cross PCIe.  ctl: one byte per group ((W-1) | pads << 2 | row_start << 6);
- * payload: the groups' real values as W-byte little-endian deltas (a row's
- * first arc absolute).  gee_pack_targets (graph preparation; allocates,
- * synchronises) writes ctl[padded_arcs/8] and up to 4*padded_arcs payload
- * bytes and returns the payload size.  gee_unpack_targets (stream-ordered,
- * no allocation; scratch >= gee_unpack_scratch_bytes(groups)) rebuilds the
- * padded targets (pads = sentinel) and, given the real arcs' weights in
- * order, the padded weights (pads 0). */
+ * slot-sorted CSR in groups of 8 arcs so fewer bytes cross PCIe:
+ *   ctl:  one byte per group ((W-1) | pads << 2 | row_start << 6);
+ *   payload: the real arcs' targets as W-byte little-endian deltas (a row's
+ *         first arc absolute);
+ *   wctl: one byte per group (B | e << 2): B = 1..3 bytes per weight of an
+ *         integer k with w = k * 2^-e exactly (lossless group fixed point),
+ *         B = 0 raw f32 bits;
+ *   wpayload: the real arcs' weights (no pads).
+ * gee_pack_targets (graph preparation; allocates, synchronises) writes
+ * ctl[padded_arcs/8], up to 4*padded_arcs payload bytes and, given the
+ * padded weights, wctl[padded_arcs/8] and up to 4*padded_arcs wpayload bytes,
+ * returning both sizes.  gee_unpack_targets (stream-ordered, no allocation;
+ * scratch >= gee_unpack_scratch_bytes(groups)) rebuilds the padded targets
+ * (pads = sentinel) and, given wctl/wpayload, the padded weights (pads 0),
+ * bit for bit. */
 size_t gee_unpack_scratch_bytes(int64_t groups);
-int gee_pack_targets(const int64_t *padded_offsets, int64_t rows, const int32_t *targets, int64_t padded_arcs,
-                     int32_t sentinel, uint8_t *ctl, uint8_t *payload, int64_t *payload_bytes, void *stream);
-int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t groups, const float *w_real,
-                       int32_t sentinel, int32_t *targets, float *w_padded, void *scratch, size_t scratch_bytes,
-                       void *stream);
+int gee_pack_targets(const int64_t *padded_offsets, int64_t rows, const int32_t *targets, const float *w_padded,
+                     int64_t padded_arcs, int32_t sentinel, uint8_t *ctl, uint8_t *payload, int64_t *payload_bytes,
+                     uint8_t *wctl, uint8_t *wpayload, int64_t *wpayload_bytes, void *stream);
+int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t groups, const uint8_t *wctl,
+                       const uint8_t *wpayload, int32_t sentinel, int32_t *targets, float *w_padded, void *scratch,
+                       size_t scratch_bytes, void *stream);
 
 /* Class stream: cls[e] = table[targets[e]] (u8, k <= 255) for every arc of
  * a pull layout -- the random half of the pull pass on its own (label-table

@@ -15,6 +15,14 @@
 // The payload of group g starts at the sum of the earlier groups' sizes.
 // Unsorted rows still round-trip (deltas wrap mod 2^32); they compress less.
 //
+// Weights (weighted graphs) travel per group too, without the pads:
+//   wctl[g] = B | e << 2: B = 0 raw f32 bits (4 bytes per real weight), or
+//             B = 1..3 bytes per weight of an integer k with w = k * 2^-e
+//             exactly (e in 0..63; all real weights of the group >= +0,
+//             normal, and exactly representable that way) -- lossless
+//             group fixed point; seeded (0,1] weights with 24-bit mantissas
+//             take 3 bytes.
+//
 // Decode (gee_unpack_targets, inside the timed e2e region; no allocation):
 //   1. exclusive scan over (payload bytes, pads) per group -> the group's
 //      payload offset and real-arc index (for the weight copy);
@@ -23,6 +31,7 @@
 //   3. per group, rebuild the 8 padded targets (sentinel for pads) and copy
 //      the row's real weights into the padded weight layout (pads 0).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
 #include "gee_common.cuh"
@@ -43,23 +52,31 @@ struct SegOp {
     }
 };
 
-struct Pos {  // payload bytes and pad arcs before a group
+struct Pos {  // target payload bytes, pad arcs and weight payload bytes before a group
     uint64_t bytes;
     uint64_t pads;
+    uint64_t wbytes;
 };
 
 struct PosSum {
     __host__ __device__ __forceinline__ Pos operator()(const Pos &a, const Pos &b) const
     {
-        return Pos{a.bytes + b.bytes, a.pads + b.pads};
+        return Pos{a.bytes + b.bytes, a.pads + b.pads, a.wbytes + b.wbytes};
     }
 };
 
-struct CtlToPos {  // ctl byte -> (payload bytes, pads) of the group
-    __host__ __device__ __forceinline__ Pos operator()(uint8_t c) const
+__host__ __device__ __forceinline__ Pos group_pos(uint8_t c, uint8_t wc, bool weighted)
+{
+    const uint32_t w = (c & 3u) + 1u, pads = (c >> 2) & 15u, real = 8u - pads;
+    const uint32_t wb = (wc & 3u) ? (wc & 3u) : 4u;
+    return Pos{(uint64_t)(real * w), (uint64_t)pads, weighted ? (uint64_t)(real * wb) : 0ull};
+}
+
+struct GroupToPos {  // group index -> its (payload bytes, pads, weight bytes)
+    const uint8_t *ctl, *wctl;
+    __device__ __forceinline__ Pos operator()(int64_t g) const
     {
-        const uint32_t w = (c & 3u) + 1u, pads = (c >> 2) & 15u;
-        return Pos{(uint64_t)((8u - pads) * w), (uint64_t)pads};
+        return group_pos(ctl[g], wctl ? wctl[g] : 0, wctl != nullptr);
     }
 };
 
@@ -112,6 +129,62 @@ __global__ void k_pack_payload(const int32_t *__restrict__ t, int64_t groups, co
     }
 }
 
+// Group fixed point: the smallest e (<= 63) with every real weight an integer
+// multiple of 2^-e, and the bytes of the largest multiple; B = 0 (raw) when
+// a weight is negative, -0.0, denormal, inf/nan or needs 4 bytes.
+__device__ __forceinline__ uint32_t weight_ctl(const float *w, uint32_t real)
+{
+    int e = 0;
+    bool ok = true;
+    for (uint32_t i = 0; i < real; i++) {
+        const uint32_t u = __float_as_uint(w[i]);
+        if (u == 0u) continue;
+        const uint32_t ef = u >> 23;  // sign bit set -> ef >= 256
+        if (ef == 0u || ef >= 255u) {
+            ok = false;
+            continue;
+        }
+        const uint32_t sig = (u & 0x7fffffu) | 0x800000u;
+        const int ei = 150 - (int)ef - (__ffs(sig) - 1);
+        e = max(e, ei);
+    }
+    if (!ok || e > 63) return 0u;
+    uint32_t kmax = 0;
+    for (uint32_t i = 0; i < real; i++) {
+        const uint32_t u = __float_as_uint(w[i]);
+        if (u == 0u) continue;
+        const int sh = (int)(u >> 23) - 150 + e;  // k = sig * 2^sh
+        if (sh > 0) return 0u;                    // k >= 2^24
+        kmax = max(kmax, ((u & 0x7fffffu) | 0x800000u) >> (-sh));
+    }
+    const uint32_t b = kmax < 0x100u ? 1u : kmax < 0x10000u ? 2u : kmax < 0x1000000u ? 3u : 0u;
+    return b ? (b | (uint32_t)e << 2) : 0u;
+}
+
+__global__ void k_pack_wctl(const float *__restrict__ w, const uint8_t *__restrict__ ctl, int64_t groups,
+                            uint8_t *__restrict__ wctl)
+{
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x)
+        wctl[g] = (uint8_t)weight_ctl(w + 8 * g, 8u - ((ctl[g] >> 2) & 15u));
+}
+
+__global__ void k_pack_wpayload(const float *__restrict__ w, const uint8_t *__restrict__ ctl,
+                                const uint8_t *__restrict__ wctl, int64_t groups, const Pos *__restrict__ pos,
+                                uint8_t *__restrict__ wpay)
+{
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t real = 8u - ((ctl[g] >> 2) & 15u), wc = wctl[g], b = wc & 3u, e = wc >> 2;
+        uint8_t *p = wpay + pos[g].wbytes;
+        for (uint32_t i = 0; i < real; i++) {
+            const uint32_t u = __float_as_uint(w[8 * g + i]);
+            uint32_t v = u;
+            if (b) v = u ? ((u & 0x7fffffu) | 0x800000u) >> (150 - (int)(u >> 23) - (int)e) : 0u;
+            const uint32_t nb = b ? b : 4u;
+            for (uint32_t q = 0; q < nb; q++) *p++ = (uint8_t)(v >> (8 * q));
+        }
+    }
+}
+
 __device__ __forceinline__ uint32_t ld_delta(const uint8_t *p, uint32_t w)
 {
     uint32_t d = p[0];
@@ -136,8 +209,9 @@ __global__ void __launch_bounds__(PT) k_unpack_sums(const uint8_t *__restrict__ 
 
 __global__ void __launch_bounds__(PT) k_unpack_rows(const uint8_t *__restrict__ ctl, const uint8_t *__restrict__ payload,
                                                     int64_t groups, const Pos *__restrict__ pos,
-                                                    const SegSum *__restrict__ last, const float *__restrict__ w_real,
-                                                    uint32_t sentinel, int32_t *__restrict__ t, float *__restrict__ w_pad)
+                                                    const SegSum *__restrict__ last, const uint8_t *__restrict__ wctl,
+                                                    const uint8_t *__restrict__ wpay, uint32_t sentinel,
+                                                    int32_t *__restrict__ t, float *__restrict__ w_pad)
 {
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t c = ctl[g], w = (c & 3u) + 1u, pads = (c >> 2) & 15u, real = 8u - pads;
@@ -157,11 +231,18 @@ __global__ void __launch_bounds__(PT) k_unpack_rows(const uint8_t *__restrict__ 
         int4 *tp = reinterpret_cast<int4 *>(t + 8 * g);
         __stcs(tp, make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]));
         __stcs(tp + 1, make_int4((int)o[4], (int)o[5], (int)o[6], (int)o[7]));
-        if (w_real) {
-            const float *src = w_real + (8 * g - (int64_t)ps.pads);  // real arcs before this group
+        if (wctl) {
+            const uint32_t wc = wctl[g], b = wc & 3u;
+            const uint8_t *q = wpay + ps.wbytes;
+            // w = k * 2^-e (exact: k < 2^24, e <= 63), or the raw bits
+            const float scale = __uint_as_float((127u - (wc >> 2)) << 23);
             float x[8];
 #pragma unroll
-            for (uint32_t i = 0; i < 8; i++) x[i] = i < real ? __ldcs(src + i) : 0.f;
+            for (uint32_t i = 0; i < 8; i++) {
+                float v = 0.f;
+                if (i < real) v = b ? (float)ld_delta(q + i * b, b) * scale : __uint_as_float(ld_delta(q + 4 * i, 4));
+                x[i] = v;
+            }
             float4 *wp = reinterpret_cast<float4 *>(w_pad + 8 * g);
             __stcs(wp, make_float4(x[0], x[1], x[2], x[3]));
             __stcs(wp + 1, make_float4(x[4], x[5], x[6], x[7]));
@@ -171,11 +252,16 @@ __global__ void __launch_bounds__(PT) k_unpack_rows(const uint8_t *__restrict__ 
 
 inline int grid_of(int64_t items) { return (int)std::min<int64_t>((items + PT - 1) / PT, (int64_t)gee::sm_count() * 16); }
 
+inline auto pos_iter(const uint8_t *ctl, const uint8_t *wctl)
+{
+    return thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), GroupToPos{ctl, wctl});
+}
+
 size_t cub_scan_bytes(int64_t groups)
 {
     size_t a = 0, b = 0;
-    auto it = thrust::make_transform_iterator((const uint8_t *)nullptr, CtlToPos());
-    cub::DeviceScan::ExclusiveScan(nullptr, a, it, (Pos *)nullptr, PosSum(), Pos{0, 0}, groups);
+    auto it = pos_iter(nullptr, nullptr);
+    cub::DeviceScan::ExclusiveScan(nullptr, a, it, (Pos *)nullptr, PosSum(), Pos{0, 0, 0}, groups);
     cub::DeviceScan::InclusiveScan(nullptr, b, (SegSum *)nullptr, (SegSum *)nullptr, SegOp(), groups);
     return std::max(a, b);
 }
@@ -193,17 +279,21 @@ size_t gee_unpack_scratch_bytes(int64_t groups)
            align256(cub_scan_bytes(groups));
 }
 
-int gee_pack_targets(const int64_t *padded_offsets, int64_t rows, const int32_t *targets, int64_t padded_arcs,
-                     int32_t sentinel, uint8_t *ctl, uint8_t *payload, int64_t *payload_bytes, void *stream)
+int gee_pack_targets(const int64_t *padded_offsets, int64_t rows, const int32_t *targets, const float *w_padded,
+                     int64_t padded_arcs, int32_t sentinel, uint8_t *ctl, uint8_t *payload, int64_t *payload_bytes,
+                     uint8_t *wctl, uint8_t *wpayload, int64_t *wpayload_bytes, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(rows >= 0 && padded_arcs >= 0 && (padded_arcs & 7) == 0, GEE_ERR_INVALID,
                 "padded_arcs must be a nonnegative multiple of 8");
     GEE_REQUIRE(payload_bytes != nullptr, GEE_ERR_INVALID, "payload_bytes must not be NULL");
     *payload_bytes = 0;
+    if (wpayload_bytes) *wpayload_bytes = 0;
     const int64_t groups = padded_arcs / 8;
     if (groups == 0) return GEE_OK;
     GEE_REQUIRE(padded_offsets && targets && ctl && payload, GEE_ERR_INVALID, "NULL array argument");
+    GEE_REQUIRE(!w_padded || (wctl && wpayload && wpayload_bytes), GEE_ERR_INVALID,
+                "weights need wctl, wpayload and wpayload_bytes");
     cudaStream_t st = gee::as_stream(stream);
     uint8_t *start = nullptr;
     Pos *pos = nullptr;
@@ -212,7 +302,7 @@ int gee_pack_targets(const int64_t *padded_offsets, int64_t rows, const int32_t 
     size_t tmp_bytes = 0;
     int rc = GEE_OK, hbad = 0;
     Pos tail[1];
-    auto it = thrust::make_transform_iterator((const uint8_t *)ctl, CtlToPos());
+    auto it = pos_iter(ctl, w_padded ? wctl : nullptr);
     auto fail = [&](int code, const char *msg) {
         gee::set_error("gee_pack_targets: %s", msg);
         rc = code;
@@ -226,13 +316,15 @@ int gee_pack_targets(const int64_t *padded_offsets, int64_t rows, const int32_t 
     cudaMemsetAsync(bad, 0, sizeof(int), st);
     k_mark_row_starts<<<grid_of(rows), PT, 0, st>>>(padded_offsets, rows, start);
     k_pack_ctl<<<grid_of(groups), PT, 0, st>>>(targets, groups, (uint32_t)sentinel, ctl, start, bad);
-    cub::DeviceScan::ExclusiveScan(nullptr, tmp_bytes, it, pos, PosSum(), Pos{0, 0}, groups, st);
+    if (w_padded) k_pack_wctl<<<grid_of(groups), PT, 0, st>>>(w_padded, ctl, groups, wctl);
+    cub::DeviceScan::ExclusiveScan(nullptr, tmp_bytes, it, pos, PosSum(), Pos{0, 0, 0}, groups, st);
     if (cudaMallocAsync(&tmp, tmp_bytes, st) != cudaSuccess) {
         fail(GEE_ERR_CUDA, "scan scratch alloc failed");
         goto out;
     }
-    cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, it, pos, PosSum(), Pos{0, 0}, groups, st);
+    cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, it, pos, PosSum(), Pos{0, 0, 0}, groups, st);
     k_pack_payload<<<grid_of(groups), PT, 0, st>>>(targets, groups, ctl, pos, payload);
+    if (w_padded) k_pack_wpayload<<<grid_of(groups), PT, 0, st>>>(w_padded, ctl, wctl, groups, pos, wpayload);
     if ((rc = gee::check_launch("k_pack_payload"))) goto out;
     cudaMemcpyAsync(tail, pos + groups - 1, sizeof(Pos), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -245,9 +337,12 @@ int gee_pack_targets(const int64_t *padded_offsets, int64_t rows, const int32_t 
         goto out;
     }
     {
-        uint8_t last = 0;
+        uint8_t last = 0, wlast = 0;
         cudaMemcpy(&last, ctl + groups - 1, 1, cudaMemcpyDeviceToHost);
-        *payload_bytes = (int64_t)(tail[0].bytes + CtlToPos()(last).bytes);
+        if (w_padded) cudaMemcpy(&wlast, wctl + groups - 1, 1, cudaMemcpyDeviceToHost);
+        const Pos lp = group_pos(last, wlast, w_padded != nullptr);
+        *payload_bytes = (int64_t)(tail[0].bytes + lp.bytes);
+        if (w_padded) *wpayload_bytes = (int64_t)(tail[0].wbytes + lp.wbytes);
     }
 out:
     if (tmp) cudaFreeAsync(tmp, st);
@@ -257,14 +352,14 @@ out:
     return rc;
 }
 
-int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t groups, const float *w_real,
-                       int32_t sentinel, int32_t *targets, float *w_padded, void *scratch, size_t scratch_bytes,
-                       void *stream)
+int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t groups, const uint8_t *wctl,
+                       const uint8_t *wpayload, int32_t sentinel, int32_t *targets, float *w_padded, void *scratch,
+                       size_t scratch_bytes, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(groups >= 0, GEE_ERR_INVALID, "groups must be nonnegative");
     if (groups == 0) return GEE_OK;
-    GEE_REQUIRE(ctl && payload && targets && (!w_real || w_padded) && scratch, GEE_ERR_INVALID,
+    GEE_REQUIRE(ctl && payload && targets && (!wctl || (wpayload && w_padded)) && scratch, GEE_ERR_INVALID,
                 "NULL array argument");
     GEE_REQUIRE(((uintptr_t)targets & 15) == 0 && (!w_padded || ((uintptr_t)w_padded & 15) == 0), GEE_ERR_INVALID,
                 "targets / w_padded must be 16-byte aligned");
@@ -276,15 +371,15 @@ int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t group
     auto *seg = reinterpret_cast<SegSum *>(static_cast<char *>(scratch) + pos_b);
     void *tmp = static_cast<char *>(scratch) + pos_b + align256((size_t)groups * sizeof(SegSum));
     size_t tmp_bytes = cub_scan_bytes(groups);
-    auto it = thrust::make_transform_iterator((const uint8_t *)ctl, CtlToPos());
-    GEE_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, it, pos, PosSum(), Pos{0, 0}, groups, st));
+    auto it = pos_iter(ctl, wctl);
+    GEE_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, it, pos, PosSum(), Pos{0, 0, 0}, groups, st));
     k_unpack_sums<<<grid_of(groups), PT, 0, st>>>(ctl, payload, groups, pos, seg);
     int rc;
     if ((rc = gee::check_launch("k_unpack_sums"))) return rc;
     tmp_bytes = cub_scan_bytes(groups);
     GEE_CUDA(cub::DeviceScan::InclusiveScan(tmp, tmp_bytes, seg, seg, SegOp(), groups, st));
-    k_unpack_rows<<<grid_of(groups), PT, 0, st>>>(ctl, payload, groups, pos, seg, w_real, (uint32_t)sentinel, targets,
-                                                  w_real ? w_padded : nullptr);
+    k_unpack_rows<<<grid_of(groups), PT, 0, st>>>(ctl, payload, groups, pos, seg, wctl, wpayload, (uint32_t)sentinel,
+                                                  targets, wctl ? w_padded : nullptr);
     return gee::check_launch("k_unpack_rows");
 }
 

@@ -27,10 +27,12 @@ queue stays ahead of both.
 
 The targets cross PCIe packed (``packed=True``, the default for the padded
 layout): gee_pack_targets codes each chunk's slot-sorted targets as groups of
-8 byte-width deltas at preparation time, the weights travel without the row
-padding, and gee_unpack_targets rebuilds the padded targets and weights on
-the compute stream before the chunk's pull (C4: 15.5 GB of targets become
-about 9 GB; the rebuilt arrays are bit-identical, so Z is too).
+8 byte-width deltas at preparation time and its weights, without the row
+padding, as lossless group fixed point (1-3 bytes per weight when the group's
+weights are exact multiples of a common power of two, else raw f32);
+gee_unpack_targets rebuilds the padded targets and weights on the compute
+stream before the chunk's pull (C4: 31 GB of targets and weights become
+about 20 GB; the rebuilt arrays are bit-identical, so Z is too).
 
 Graph preparation (CSR build, hot-label plan, per-chunk heavy-row items,
 pinned host copies) happens once in ``HostPipeline(...)``. It is outside
@@ -75,7 +77,7 @@ class HostPipeline:
         self.sentinel = g.n_hot + g.n_nodes
         self.h_tgt = None if self.packed else pin(g.targets)
         self.h_w = None if self.packed else pin(g.weights)
-        self.h_ctl, self.h_pay, self.h_wr = [], [], []
+        self.h_ctl, self.h_pay, self.h_wctl, self.h_wpay = [], [], [], []
         self.h_off = []
         self.views = []
         max_rows = max_arcs = 0
@@ -107,8 +109,10 @@ class HostPipeline:
             self.d_ctl = [torch.empty(max(1, max_arcs // 8), dtype=torch.uint8, device=dev) for _ in range(2)]
             self.d_pay = [torch.empty(max(1, max(t.numel() for t in self.h_pay)), dtype=torch.uint8, device=dev)
                           for _ in range(2)]
-            self.d_wr = [torch.empty(max(1, max(t.numel() for t in self.h_wr)), dtype=torch.float32, device=dev)
-                         if self.weighted else None for _ in range(2)]
+            self.d_wctl = [torch.empty(max(1, max_arcs // 8), dtype=torch.uint8, device=dev)
+                           if self.weighted else None for _ in range(2)]
+            self.d_wpay = [torch.empty(max(1, max(t.numel() for t in self.h_wpay)), dtype=torch.uint8, device=dev)
+                           if self.weighted else None for _ in range(2)]
             self.scratch_bytes = int(_lib.lib.gee_unpack_scratch_bytes(max_arcs // 8))
             self.d_scratch = torch.empty(max(1, self.scratch_bytes), dtype=torch.uint8, device=dev)
         self.d_off = [torch.empty(max_rows + 1, dtype=torch.int64, device=dev) for _ in range(2)]
@@ -125,25 +129,27 @@ class HostPipeline:
         self.s_out = torch.cuda.Stream(dev)
 
     def _pack_chunk(self, g, lo, hi, a0, a1):
-        """Graph preparation: code chunk [lo, hi)'s padded targets (device) and
-        keep the packed stream and the real arcs' weights in pinned memory."""
+        """Graph preparation: code chunk [lo, hi)'s padded targets and weights
+        (device) and keep the packed streams in pinned memory."""
         dev = g.device
         groups = (a1 - a0) // 8
         off = g.offsets[lo:hi + 1] - g.offsets[lo]
         tgt = g.targets[a0:a1]
-        ctl = torch.empty(max(1, groups), dtype=torch.uint8, device=dev)
-        pay = torch.empty(max(1, 4 * (a1 - a0)), dtype=torch.uint8, device=dev)
-        nb = ctypes.c_int64()
-        _lib.check(_lib.lib.gee_pack_targets(_lib.ptr(off), hi - lo, _lib.ptr(tgt), a1 - a0, self.sentinel,
-                                             _lib.ptr(ctl), _lib.ptr(pay), ctypes.byref(nb),
+        wts = g.weights[a0:a1] if self.weighted else None
+        u8 = lambda m: torch.empty(max(1, m), dtype=torch.uint8, device=dev)  # noqa: E731
+        ctl, pay = u8(groups), u8(4 * (a1 - a0))
+        wctl, wpay = (u8(groups), u8(4 * (a1 - a0))) if self.weighted else (None, None)
+        nb, nwb = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib.gee_pack_targets(_lib.ptr(off), hi - lo, _lib.ptr(tgt), _lib.ptr(wts), a1 - a0,
+                                             self.sentinel, _lib.ptr(ctl), _lib.ptr(pay), ctypes.byref(nb),
+                                             _lib.ptr(wctl), _lib.ptr(wpay), ctypes.byref(nwb),
                                              _lib.stream_handle()), "gee_pack_targets")
         self.h_ctl.append(ctl[:groups].cpu().pin_memory())
         self.h_pay.append(pay[:int(nb.value)].cpu().pin_memory())
-        if self.weighted:
-            self.h_wr.append(g.weights[a0:a1][tgt != self.sentinel].cpu().pin_memory())
-        else:
-            self.h_wr.append(torch.empty(0, dtype=torch.float32))
-        del pay
+        empty = torch.empty(0, dtype=torch.uint8)
+        self.h_wctl.append(wctl[:groups].cpu().pin_memory() if self.weighted else empty)
+        self.h_wpay.append(wpay[:int(nwb.value)].cpu().pin_memory() if self.weighted else empty)
+        del pay, wpay
 
     @property
     def n_chunks(self):
@@ -154,7 +160,7 @@ class HostPipeline:
         b += sum(t.numel() * 8 for t in self.h_off)
         if self.packed:
             b += sum(t.numel() for t in self.h_ctl) + sum(t.numel() for t in self.h_pay)
-            b += sum(t.numel() * 4 for t in self.h_wr)
+            b += sum(t.numel() for t in self.h_wctl) + sum(t.numel() for t in self.h_wpay)
         else:
             b += self.h_tgt.numel() * 4
             if self.h_w is not None:
@@ -242,7 +248,8 @@ class HostPipeline:
                 self.d_ctl[b][:self.h_ctl[i].numel()].copy_(self.h_ctl[i], non_blocking=True)
                 self.d_pay[b][:self.h_pay[i].numel()].copy_(self.h_pay[i], non_blocking=True)
                 if self.weighted:
-                    self.d_wr[b][:self.h_wr[i].numel()].copy_(self.h_wr[i], non_blocking=True)
+                    self.d_wctl[b][:self.h_wctl[i].numel()].copy_(self.h_wctl[i], non_blocking=True)
+                    self.d_wpay[b][:self.h_wpay[i].numel()].copy_(self.h_wpay[i], non_blocking=True)
             else:
                 self.d_tgt[b][:a1 - a0].copy_(self.h_tgt[a0:a1], non_blocking=True)
                 if self.weighted:
@@ -255,7 +262,8 @@ class HostPipeline:
             if self.packed:
                 _lib.check(_lib.lib.gee_unpack_targets(
                     _lib.ptr(self.d_ctl[b]), _lib.ptr(self.d_pay[b]), (a1 - a0) // 8,
-                    _lib.ptr(self.d_wr[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
+                    _lib.ptr(self.d_wctl[b]) if self.weighted else None,
+                    _lib.ptr(self.d_wpay[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
                     _lib.ptr(self.d_w[b]) if self.weighted else None, _lib.ptr(self.d_scratch),
                     self.scratch_bytes, _lib.stream_handle(self.s_cmp)), "gee_unpack_targets")
             v.offsets = self.d_off[b][:hi - lo + 1]

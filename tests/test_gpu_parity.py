@@ -539,33 +539,40 @@ def _pack_round_trip(off, tgt, w, sentinel):
     dev = torch.device("cuda")
     off_d = torch.as_tensor(off, dtype=torch.int64, device=dev)
     t_d = torch.as_tensor(tgt, dtype=torch.int32, device=dev)
+    w_d = torch.as_tensor(w, dtype=torch.float32, device=dev) if w is not None else None
     arcs = t_d.numel()
     groups = arcs // 8
-    ctl = torch.empty(max(1, groups), dtype=torch.uint8, device=dev)
-    pay = torch.empty(max(1, 4 * arcs), dtype=torch.uint8, device=dev)
-    nb = ctypes.c_int64()
-    _lib.check(_lib.lib.gee_pack_targets(_lib.ptr(off_d), off_d.numel() - 1, _lib.ptr(t_d), arcs, sentinel,
-                                         _lib.ptr(ctl), _lib.ptr(pay), ctypes.byref(nb), _lib.stream_handle()),
-               "pack")
+    u8 = lambda m: torch.empty(max(1, m), dtype=torch.uint8, device=dev)  # noqa: E731
+    ctl, pay = u8(groups), u8(4 * arcs)
+    wctl, wpay = (u8(groups), u8(4 * arcs)) if w is not None else (None, None)
+    nb, nwb = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.lib.gee_pack_targets(_lib.ptr(off_d), off_d.numel() - 1, _lib.ptr(t_d), _lib.ptr(w_d), arcs,
+                                         sentinel, _lib.ptr(ctl), _lib.ptr(pay), ctypes.byref(nb), _lib.ptr(wctl),
+                                         _lib.ptr(wpay), ctypes.byref(nwb), _lib.stream_handle()), "pack")
     real = t_d != sentinel
-    w_real = torch.as_tensor(w, dtype=torch.float32, device=dev)[real] if w is not None else None
     sb = int(_lib.lib.gee_unpack_scratch_bytes(groups))
     scratch = torch.empty(max(1, sb), dtype=torch.uint8, device=dev)
     out_t = torch.full((arcs + 8,), -7, dtype=torch.int32, device=dev)
     out_w = torch.full((arcs + 8,), -7.0, dtype=torch.float32, device=dev) if w is not None else None
-    # the payload a PCIe copy would deliver: exactly nb bytes, followed by junk
-    pay2 = torch.full((int(nb.value) + 64,), 0xAB, dtype=torch.uint8, device=dev)
-    pay2[:int(nb.value)] = pay[:int(nb.value)]
-    _lib.check(_lib.lib.gee_unpack_targets(_lib.ptr(ctl), _lib.ptr(pay2), groups, _lib.ptr(w_real), sentinel,
-                                           _lib.ptr(out_t), _lib.ptr(out_w), _lib.ptr(scratch), sb,
+
+    def exact(b, n):  # the bytes a PCIe copy would deliver: exactly n, then junk
+        x = torch.full((n + 64,), 0xAB, dtype=torch.uint8, device=dev)
+        x[:n] = b[:n]
+        return x
+
+    pay2 = exact(pay, int(nb.value))
+    wpay2 = exact(wpay, int(nwb.value)) if w is not None else None
+    _lib.check(_lib.lib.gee_unpack_targets(_lib.ptr(ctl), _lib.ptr(pay2), groups, _lib.ptr(wctl), _lib.ptr(wpay2),
+                                           sentinel, _lib.ptr(out_t), _lib.ptr(out_w), _lib.ptr(scratch), sb,
                                            _lib.stream_handle()), "unpack")
     torch.cuda.synchronize()
     assert torch.equal(out_t[:arcs], t_d) and bool((out_t[arcs:] == -7).all())
     if w is not None:
-        exp_w = torch.as_tensor(w, dtype=torch.float32, device=dev)
-        assert torch.equal(out_w[:arcs], torch.where(real, exp_w, torch.zeros_like(exp_w)))
+        exp_w = torch.where(real, w_d, torch.zeros_like(w_d))
+        assert torch.equal(out_w[:arcs].view(torch.int32), exp_w.view(torch.int32))
         assert bool((out_w[arcs:] == -7.0).all())
-    return int(nb.value)
+        return int(nb.value), int(nwb.value)
+    return int(nb.value), 0
 
 
 def _padded_rows(degs, rng, sentinel, sort=True, big=False):
@@ -597,17 +604,53 @@ def test_pack_targets_round_trip(case):
         degs = list(rng.integers(0, 40, 3000)) + [0, 1, 8, 9, 7, 16, 5000, 70_000]
         rng.shuffle(degs)
     off, tgt, w = _padded_rows(degs, rng, sentinel, sort=case != "unsorted", big=case == "wide")
-    nb = _pack_round_trip(off, tgt, w, sentinel)
+    nb, nwb = _pack_round_trip(off, tgt, w, sentinel)
     _pack_round_trip(off, tgt, None, sentinel)
+    real = int((tgt != sentinel).sum())
     if case == "mixed":  # sorted rows code in well under 4 bytes per real arc
-        assert nb < 3 * int((tgt != sentinel).sum())
+        assert nb < 3 * real
+    # weights of 1 - U[0,1) with 24-bit U: 3 bytes each (groups holding w = 1.0 raw)
+    w24 = np.where(tgt != sentinel, 1.0 - rng.integers(0, 1 << 24, tgt.size) / float(1 << 24), 0.0).astype(np.float32)
+    _, nwb24 = _pack_round_trip(off, tgt, w24, sentinel)
+    assert nwb24 <= 3 * real + real // 8 * 2 + 64
+
+
+@pytest.mark.parametrize("kind", ["integers", "halves", "mixed_signs", "specials", "tiny", "big"])
+def test_pack_weights_lossless(kind):
+    # group fixed point is lossless for every f32 pattern: integer and
+    # dyadic weights take 1-3 bytes, negatives / -0.0 / denormals / inf /
+    # nan / values needing 2^-64 or 4 bytes fall back to raw bits
+    rng = np.random.default_rng(len(kind))
+    degs = list(rng.integers(0, 30, 2000)) + [1, 8, 9, 300]
+    sentinel = 1 << 20
+    off, tgt, _ = _padded_rows(degs, rng, sentinel)
+    m = tgt.size
+    if kind == "integers":
+        w = rng.integers(0, 70_000, m).astype(np.float32)
+    elif kind == "halves":
+        w = (rng.integers(0, 512, m) / 2.0).astype(np.float32)
+    elif kind == "mixed_signs":
+        w = rng.standard_normal(m).astype(np.float32)
+    elif kind == "specials":
+        pool = np.array([0.0, -0.0, 1.0, np.inf, -np.inf, np.nan, 1e-45, 3.4e38, 2.0 ** -63, 2.0 ** -64, 0.75],
+                        dtype=np.float32)
+        w = pool[rng.integers(0, pool.size, m)]
+    elif kind == "tiny":
+        w = (rng.integers(1, 1 << 20, m) * 2.0 ** -60).astype(np.float32)
+    else:
+        w = (rng.integers(1, 1 << 24, m).astype(np.float64) * 2.0 ** 30).astype(np.float32)
+    w = np.where(tgt != sentinel, w, np.float32(0.0)).astype(np.float32)
+    _, nwb = _pack_round_trip(off, tgt, w, sentinel)
+    real = int((tgt != sentinel).sum())
+    if kind in ("integers", "halves"):
+        assert nwb <= 3 * real
 
 
 def test_pack_targets_many_pads():
     # more than 2^24 pad arcs in one call (C4's chunks hold ~18M): the
     # real-arc index of every group (for the weight copy) stays exact
     rows = 2_500_000
-    rng = np.random.default_rng(5)
+    rng = np.random.default_rng(5)  # (weights: raw or fixed point, per group)
     sentinel = 1 << 27
     tgt = np.full((rows, 8), sentinel, dtype=np.int64)
     tgt[:, 0] = rng.integers(0, sentinel, rows)
@@ -626,8 +669,8 @@ def test_pack_targets_rejects_unpadded():
     ctl = torch.empty(2, dtype=torch.uint8, device=dev)
     pay = torch.empty(64, dtype=torch.uint8, device=dev)
     nb = ctypes.c_int64()
-    rc = _lib.lib.gee_pack_targets(_lib.ptr(off), 1, _lib.ptr(t), 16, 9, _lib.ptr(ctl), _lib.ptr(pay),
-                                   ctypes.byref(nb), _lib.stream_handle())
+    rc = _lib.lib.gee_pack_targets(_lib.ptr(off), 1, _lib.ptr(t), None, 16, 9, _lib.ptr(ctl), _lib.ptr(pay),
+                                   ctypes.byref(nb), None, None, None, _lib.stream_handle())
     assert rc != 0 and b"padded layout" in _lib.lib.gee_last_error()
 
 
