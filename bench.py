@@ -408,9 +408,9 @@ def main():
     }
     peak_gbs, peak_kind = load_peaks()
     dominant = max((p for p in phase_ms if p in phase_bytes), key=lambda p: phase_ms[p])
-    # gee_gather_labels' default kernel: packed shared-memory head for k <= 63,
-    # byte head otherwise, plain contiguous lookups without a hot tier
-    gather_kernel = ("k_gather_contig" if g.n_hot < 16384 else "k_gather_packed" if k <= 63 else "k_gather_tiered")
+    # gee_gather_labels: packed shared-memory head of the hot tier, or
+    # plain contiguous lookups without one
+    gather_kernel = "k_gather_contig" if g.n_hot < 16384 else "k_gather_packed"
     kernel_of = {"project": "k_label_hist", "gather": gather_kernel, "blocks": "k_reduce_blocks_ring",
                  "heavy": "k_reduce_heavy_items", "wide": "k_wide_rows"}
     achieved = phase_bytes[dominant] / (phase_ms[dominant] * 1e-3) / 1e9

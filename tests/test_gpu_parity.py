@@ -674,17 +674,15 @@ def test_pack_targets_rejects_unpadded():
     assert rc != 0 and b"padded layout" in _lib.lib.gee_last_error()
 
 
-@pytest.mark.parametrize("mode,head", [(None, None), ("10", "40000"), ("9", None), ("4", None), ("1", None)])
+@pytest.mark.parametrize("head", [None, "40000", "0"])
 @pytest.mark.parametrize("k", [5, 20, 50, 63, 64, 200])
-def test_gather_labels_modes(k, mode, head, monkeypatch):
+def test_gather_labels_heads(k, head, monkeypatch):
     # gee_gather_labels equals a plain gather for every kernel variant: the
-    # packed shared-memory head (5 / 6 / 8 labels per word by k), the byte
-    # head, contiguous and per-thread layouts; skewed slots hit the head,
+    # shared-memory head packed 8 / 6 / 5 / 4 labels per word by k (full and
+    # partial heads) and plain contiguous lookups; skewed slots hit the head,
     # the hot tier and the cold tier; ragged lengths exercise the tails
     from paper_2402_04403_b200 import _lib
 
-    if mode:
-        monkeypatch.setenv("GEE_GATHER_MODE", mode)
     if head:
         monkeypatch.setenv("GEE_GATHER_SMEM_HOT", head)
     gen = torch.Generator(device="cuda").manual_seed(k)
