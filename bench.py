@@ -438,7 +438,7 @@ def main():
                    "gen_s": round(t_gen, 3), "prep_s": round(t_prep, 3), "hot_prep_s": round(t_hot, 3),
                    "hot_vertices": g.n_hot, "heavy_rows": heavy_rows},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-                     "frac": achieved / peak_gbs, "traffic": load_traffic(workload, kernel_of[dominant]),
+                     "frac": achieved / peak_gbs, "traffic": load_traffic(workload, kernel_of[dominant]) if world == 1 else None,
                      "kernel": kernel_of[dominant], "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": phase_bytes[dominant],
                      "kernel_ms": phase_ms[dominant], "step_bmin_bytes": step_bmin,
