@@ -756,25 +756,31 @@ __device__ __forceinline__ void ring_issue(uint8_t *ring, int slot, int64_t e, i
                                            const uint8_t *__restrict__ cls, const float *__restrict__ w, int lane)
 {
     if (e < bend) {
+        // classes: lane l copies arcs [8l, 8l + 8); weights: each of the two
+        // copies moves 512 contiguous bytes (lane l: arcs [4l, 4l + 4), then
+        // [128 + 4l, 128 + 4l + 4)), so every 32-byte sector is read once
+        // (a lane-owns-its-8-arcs split halves each sector per instruction)
         const int64_t a = e + lane * BU;
         uint8_t *rs = ring + slot * (RING_CLS + (WEIGHTED ? RING_W : 0));
         const uint32_t dc = smem_u32(rs + lane * BU);
-        const uint32_t dw = smem_u32(rs + RING_CLS + lane * BU * 4);
+        const uint32_t dw = smem_u32(rs + RING_CLS + lane * 16);
+        const int64_t a0 = e + lane * 4, a1 = e + 128 + lane * 4;
         if (e + BROUND <= arcs) {  // whole round inside the arrays (warp-uniform)
             cp_async8(dc, cls + a, BU);
             if (WEIGHTED) {
-                cp_async16(dw, w + a, 16u);
-                cp_async16(dw + 16, w + a + 4, 16u);
+                cp_async16(dw, w + a0, 16u);
+                cp_async16(dw + 512, w + a1, 16u);
             }
         } else {
             const int64_t left = arcs - a;
             const uint32_t nc = left <= 0 ? 0u : (left >= BU ? (uint32_t)BU : (uint32_t)left);
             cp_async8(dc, nc ? (const void *)(cls + a) : (const void *)cls, nc);
             if (WEIGHTED) {
-                const uint32_t n0 = nc >= 4 ? 16u : nc * 4u;
-                const uint32_t n1 = nc > 4 ? (nc - 4) * 4u : 0u;
-                cp_async16(dw, n0 ? (const void *)(w + a) : (const void *)w, n0);
-                cp_async16(dw + 16, n1 ? (const void *)(w + a + 4) : (const void *)w, n1);
+                const int64_t l0 = arcs - a0, l1 = arcs - a1;
+                const uint32_t n0 = l0 <= 0 ? 0u : (l0 >= 4 ? 16u : (uint32_t)l0 * 4u);
+                const uint32_t n1 = l1 <= 0 ? 0u : (l1 >= 4 ? 16u : (uint32_t)l1 * 4u);
+                cp_async16(dw, n0 ? (const void *)(w + a0) : (const void *)w, n0);
+                cp_async16(dw + 512, n1 ? (const void *)(w + a1) : (const void *)w, n1);
             }
         }
     }
