@@ -751,25 +751,28 @@ __device__ __forceinline__ int64_t ring_skip(const RingBlk &B, int64_t e, int la
     return e;
 }
 
-template <bool WEIGHTED>
+// SPANS: the two weight copies of a round each move 512 contiguous bytes
+// (lane l: arcs [4l, 4l + 4), then [128 + 4l, 128 + 4l + 4)), so every
+// 32-byte sector is read once; otherwise lane l copies its own 8 arcs' 32
+// bytes as two 16-byte halves, and each copy instruction reads every sector
+// of the round half-used (2x the L2->SM bytes; blocks: 8.00 -> 7.81 ms with
+// spans, the heavy kernel 2.52 vs 2.61 ms the other way round).
+template <bool WEIGHTED, bool SPANS = true>
 __device__ __forceinline__ void ring_issue(uint8_t *ring, int slot, int64_t e, int64_t bend, int64_t arcs,
                                            const uint8_t *__restrict__ cls, const float *__restrict__ w, int lane)
 {
     if (e < bend) {
-        // classes: lane l copies arcs [8l, 8l + 8); weights: each of the two
-        // copies moves 512 contiguous bytes (lane l: arcs [4l, 4l + 4), then
-        // [128 + 4l, 128 + 4l + 4)), so every 32-byte sector is read once
-        // (a lane-owns-its-8-arcs split halves each sector per instruction)
-        const int64_t a = e + lane * BU;
+        const int64_t a = e + lane * BU;  // classes: lane l copies arcs [8l, 8l + 8)
         uint8_t *rs = ring + slot * (RING_CLS + (WEIGHTED ? RING_W : 0));
         const uint32_t dc = smem_u32(rs + lane * BU);
-        const uint32_t dw = smem_u32(rs + RING_CLS + lane * 16);
-        const int64_t a0 = e + lane * 4, a1 = e + 128 + lane * 4;
+        const uint32_t dw = smem_u32(rs + RING_CLS + lane * (SPANS ? 16 : 32));
+        const int64_t a0 = SPANS ? e + lane * 4 : a, a1 = SPANS ? e + 128 + lane * 4 : a + 4;
+        const uint32_t d1 = SPANS ? 512u : 16u;
         if (e + BROUND <= arcs) {  // whole round inside the arrays (warp-uniform)
             cp_async8(dc, cls + a, BU);
             if (WEIGHTED) {
                 cp_async16(dw, w + a0, 16u);
-                cp_async16(dw + 512, w + a1, 16u);
+                cp_async16(dw + d1, w + a1, 16u);
             }
         } else {
             const int64_t left = arcs - a;
@@ -780,7 +783,7 @@ __device__ __forceinline__ void ring_issue(uint8_t *ring, int slot, int64_t e, i
                 const uint32_t n0 = l0 <= 0 ? 0u : (l0 >= 4 ? 16u : (uint32_t)l0 * 4u);
                 const uint32_t n1 = l1 <= 0 ? 0u : (l1 >= 4 ? 16u : (uint32_t)l1 * 4u);
                 cp_async16(dw, n0 ? (const void *)(w + a0) : (const void *)w, n0);
-                cp_async16(dw + 512, n1 ? (const void *)(w + a1) : (const void *)w, n1);
+                cp_async16(dw + d1, n1 ? (const void *)(w + a1) : (const void *)w, n1);
             }
         }
     }
@@ -1102,7 +1105,7 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
         int64_t ep = b0 & ~(int64_t)(BROUND - 1);
 #pragma unroll
         for (int i = 0; i < RING; i++) {
-            ring_issue<WEIGHTED>(ring, i, ep, e1, arcs, cls, w, lane);
+            ring_issue<WEIGHTED, false>(ring, i, ep, e1, arcs, cls, w, lane);
             ep += BROUND;
         }
         int slot = 0;
@@ -1133,7 +1136,7 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
                     atomicAdd(p, 1u);
                 }
             }
-            ring_issue<WEIGHTED>(ring, slot, ep, e1, arcs, cls, w, lane);
+            ring_issue<WEIGHTED, false>(ring, slot, ep, e1, arcs, cls, w, lane);
             ep += BROUND;
             slot = slot + 1 == RING ? 0 : slot + 1;
             // fold the window into the 64-bit sums at each aligned window end
