@@ -35,15 +35,20 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned 
     LT *cold = table ? table + n_hot : nullptr;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
 
-    auto one = [&](int64_t i, int32_t c, int32_t r) {
+    // count label c (checked) and return it (0 when out of range)
+    auto count = [&](int32_t c) -> int32_t {
         if ((uint32_t)c > (uint32_t)k) {  // outside [0, k] (LabelVector, labeling.py:24-29)
             nbad++;
-            c = 0;
-        } else if (smem) {
-            atomicAdd(&mine[c], 1u);
-        } else {
-            atomicAdd(&counts[c], 1ull);
+            return 0;
         }
+        if (smem)
+            atomicAdd(&mine[c], 1u);
+        else
+            atomicAdd(&counts[c], 1ull);
+        return c;
+    };
+    auto one = [&](int64_t i, int32_t c, int32_t r) {
+        c = count(c);
         if (cold) {
             cold[i] = (LT)c;
             if (r >= 0) table[r] = (LT)c;  // hot tier copy (gee_hot.cu)
@@ -53,14 +58,26 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned 
     int64_t done = 0;
     if ((reinterpret_cast<uintptr_t>(labels) & 15) == 0 && (!hot_rank || (reinterpret_cast<uintptr_t>(hot_rank) & 15) == 0)) {
         const int64_t n4 = n >> 2;
+        // u8 table with a 4-byte aligned cold tier: one 32-bit store per 4 labels
+        const bool pack4 = sizeof(LT) == 1 && cold && (reinterpret_cast<uintptr_t>(cold) & 3) == 0;
         for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
             const int4 v = __ldcs(reinterpret_cast<const int4 *>(labels) + q);
             int4 r = make_int4(-1, -1, -1, -1);
             if (hot_rank) r = __ldcs(reinterpret_cast<const int4 *>(hot_rank) + q);
-            one(4 * q + 0, v.x, r.x);
-            one(4 * q + 1, v.y, r.y);
-            one(4 * q + 2, v.z, r.z);
-            one(4 * q + 3, v.w, r.w);
+            if (pack4) {
+                const int32_t c0 = count(v.x), c1 = count(v.y), c2 = count(v.z), c3 = count(v.w);
+                reinterpret_cast<uint32_t *>(cold)[q] = (uint32_t)c0 | (uint32_t)c1 << 8 | (uint32_t)c2 << 16 |
+                                                        (uint32_t)c3 << 24;
+                if (r.x >= 0) table[r.x] = (LT)c0;
+                if (r.y >= 0) table[r.y] = (LT)c1;
+                if (r.z >= 0) table[r.z] = (LT)c2;
+                if (r.w >= 0) table[r.w] = (LT)c3;
+            } else {
+                one(4 * q + 0, v.x, r.x);
+                one(4 * q + 1, v.y, r.y);
+                one(4 * q + 2, v.z, r.z);
+                one(4 * q + 3, v.w, r.w);
+            }
         }
         done = n4 << 2;
     }
