@@ -398,7 +398,9 @@ def main():
     heavy_rows = g.n_heavy
     lb = 1 if k <= 255 else (2 if k <= 65535 else 4)
     phase_bytes = {
-        "project": 4 * rows + lb * rows + (4 * rows + lb * g.n_hot if g.n_hot else 0),
+        # labels in, label table out; the compact hot tier (bitmap + prefix
+        # per 32 vertices, ranks of the hot ones) in, their labels out again
+        "project": 4 * rows + lb * rows + (rows // 4 + 4 * g.n_hot + lb * g.n_hot if g.n_hot else 0),
         "gather": arcs * (4 + 1),
         "blocks": 8 * (rows + 1) + light_arcs * (1 + 4 * weighted) + 4 * k * (rows - heavy_rows),
         "heavy": heavy_arcs * (1 + 4 * weighted) + 4 * k * heavy_rows,

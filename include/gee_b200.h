@@ -84,6 +84,16 @@ int gee_build_projection(const int32_t *labels, int64_t n, int32_t k,
                          void *table, const int32_t *hot_rank, int64_t n_hot,
                          int64_t *bad, void *stream);
 
+/* gee_build_projection with the hot tier in compact form (built once per
+ * graph by the caller): hot_bits[(n+31)/32] marks the hot vertices,
+ * hot_pref[w] counts the hot vertices before word w, and hot_list holds
+ * their degree ranks in vertex order: about n/4 + 4*n_hot bytes instead of
+ * the 4*n of hot_rank (C4: 0.10 GB instead of 0.54 GB per call, also over
+ * PCIe on the streamed path). */
+int gee_build_projection_hotc(const int32_t *labels, int64_t n, int32_t k, int64_t *counts, float *inv_f32,
+                              double *inv_f64, void *table, const uint32_t *hot_bits, const int32_t *hot_pref,
+                              const int32_t *hot_list, int64_t n_hot, int64_t *bad, void *stream);
+
 /* ---------------------------------------------------------------- K3 ----
  * Push edge map over a listed edge list (COO, structure of arrays).
  * Replaces serial_pass (_kernels.py:210-226, via embed_serial,

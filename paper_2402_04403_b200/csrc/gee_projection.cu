@@ -22,7 +22,8 @@ template <typename LT>
 __global__ void __launch_bounds__(HIST_THREADS)
 k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned long long *__restrict__ counts,
              LT *__restrict__ table, const int32_t *__restrict__ hot_rank, int64_t n_hot,
-             unsigned long long *__restrict__ bad, int copies)
+             unsigned long long *__restrict__ bad, int copies, const uint32_t *__restrict__ hot_bits,
+             const int32_t *__restrict__ hot_pref, const int32_t *__restrict__ hot_list)
 {
     extern __shared__ uint32_t hist[];  // copies * (k+1) bins
     const int bins = k + 1;
@@ -64,6 +65,18 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned 
             const int4 v = __ldcs(reinterpret_cast<const int4 *>(labels) + q);
             int4 r = make_int4(-1, -1, -1, -1);
             if (hot_rank) r = __ldcs(reinterpret_cast<const int4 *>(hot_rank) + q);
+            if (hot_bits) {  // compact hot tier: bitmap word, its prefix, ranks in vertex order
+                const uint32_t word = __ldg(hot_bits + (q >> 3)), sh = (uint32_t)(4 * q) & 31u;
+                const uint32_t b4 = (word >> sh) & 15u;
+                if (b4) {
+                    const int32_t *lp = hot_list + __ldg(hot_pref + (q >> 3)) + __popc(word & ((1u << sh) - 1u));
+                    int j = 0;
+                    if (b4 & 1u) r.x = lp[j++];
+                    if (b4 & 2u) r.y = lp[j++];
+                    if (b4 & 4u) r.z = lp[j++];
+                    if (b4 & 8u) r.w = lp[j++];
+                }
+            }
             if (pack4) {
                 const int32_t c0 = count(v.x), c1 = count(v.y), c2 = count(v.z), c3 = count(v.w);
                 reinterpret_cast<uint32_t *>(cold)[q] = (uint32_t)c0 | (uint32_t)c1 << 8 | (uint32_t)c2 << 16 |
@@ -81,8 +94,14 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned 
         }
         done = n4 << 2;
     }
-    for (int64_t i = done + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        one(i, __ldcs(labels + i), hot_rank ? __ldcs(hot_rank + i) : -1);
+    for (int64_t i = done + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        int32_t r = hot_rank ? __ldcs(hot_rank + i) : -1;
+        if (hot_bits) {
+            const uint32_t word = hot_bits[i >> 5], bit = (uint32_t)i & 31u;
+            if ((word >> bit) & 1u) r = hot_list[hot_pref[i >> 5] + __popc(word & ((1u << bit) - 1u))];
+        }
+        one(i, __ldcs(labels + i), r);
+    }
     if (table && blockIdx.x == 0 && threadIdx.x == 0) table[n_hot + n] = (LT)0;  // sentinel slot
     __syncthreads();
     if (smem) {
@@ -108,7 +127,9 @@ __global__ void k_inv(const unsigned long long *__restrict__ counts, int32_t k,
 
 template <typename LT>
 int launch_hist(const int32_t *labels, int64_t n, int32_t k, unsigned long long *counts, void *table,
-                const int32_t *hot_rank, int64_t n_hot, unsigned long long *bad, cudaStream_t st)
+                const int32_t *hot_rank, int64_t n_hot, unsigned long long *bad, cudaStream_t st,
+                const uint32_t *hot_bits = nullptr, const int32_t *hot_pref = nullptr,
+                const int32_t *hot_list = nullptr)
 {
     const int bins = k + 1;
     int copies = HIST_SMEM_WORDS / bins;
@@ -118,7 +139,7 @@ int launch_hist(const int32_t *labels, int64_t n, int32_t k, unsigned long long 
     const int64_t cap = (int64_t)gee::sm_count() * 4;
     const int grid = (int)(want < 1 ? 1 : (want > cap ? cap : want));
     k_label_hist<LT><<<grid, HIST_THREADS, sh, st>>>(labels, n, k, counts, static_cast<LT *>(table), hot_rank, n_hot,
-                                                     bad, copies);
+                                                     bad, copies, hot_bits, hot_pref, hot_list);
     return gee::check_launch("k_label_hist");
 }
 
@@ -161,6 +182,37 @@ int gee_build_projection(const int32_t *labels, int64_t n, int32_t k, int64_t *c
         }
         if (rc) return rc;
     }
+    if (inv_f32 || inv_f64) {
+        k_inv<<<(k + 1 + 255) / 256, 256, 0, st>>>(cnt, k, inv_f32, inv_f64);
+        return gee::check_launch("k_inv");
+    }
+    return GEE_OK;
+}
+
+int gee_build_projection_hotc(const int32_t *labels, int64_t n, int32_t k, int64_t *counts, float *inv_f32,
+                              double *inv_f64, void *table, const uint32_t *hot_bits, const int32_t *hot_pref,
+                              const int32_t *hot_list, int64_t n_hot, int64_t *bad, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(k >= 1, GEE_ERR_INVALID, "class count k must be positive (got %d)", k);
+    GEE_REQUIRE(n >= 0 && n_hot >= 0, GEE_ERR_INVALID, "n and n_hot must be nonnegative");
+    GEE_REQUIRE(n + n_hot < INT32_MAX, GEE_ERR_INVALID, "label table exceeds int32 slots");
+    GEE_REQUIRE(counts != nullptr && table != nullptr, GEE_ERR_INVALID, "counts and table must not be NULL");
+    GEE_REQUIRE(n == 0 || labels != nullptr, GEE_ERR_INVALID, "labels must not be NULL");
+    GEE_REQUIRE(hot_bits && hot_pref && hot_list && n_hot > 0, GEE_ERR_INVALID,
+                "the compact hot tier needs its bitmap, prefix and rank list and n_hot > 0");
+    cudaStream_t st = gee::as_stream(stream);
+    GEE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t)(k + 1), st));
+    if (bad) GEE_CUDA(cudaMemsetAsync(bad, 0, sizeof(int64_t), st));
+    auto *cnt = reinterpret_cast<unsigned long long *>(counts);
+    auto *nb = reinterpret_cast<unsigned long long *>(bad);
+    int rc;
+    switch (gee_label_bytes(k)) {
+    case 1: rc = launch_hist<uint8_t>(labels, n, k, cnt, table, nullptr, n_hot, nb, st, hot_bits, hot_pref, hot_list); break;
+    case 2: rc = launch_hist<uint16_t>(labels, n, k, cnt, table, nullptr, n_hot, nb, st, hot_bits, hot_pref, hot_list); break;
+    default: rc = launch_hist<int32_t>(labels, n, k, cnt, table, nullptr, n_hot, nb, st, hot_bits, hot_pref, hot_list); break;
+    }
+    if (rc) return rc;
     if (inv_f32 || inv_f64) {
         k_inv<<<(k + 1 + 255) / 256, 256, 0, st>>>(cnt, k, inv_f32, inv_f64);
         return gee::check_launch("k_inv");

@@ -71,6 +71,8 @@ class DeviceGraph:
         self.src = self.dst = self.w = None
         self.coo_source_only = False
         self.hot_rank = None  # int32[n_nodes]: degree rank of hot vertices, -1 cold
+        # the same tier in compact form for the per-call projection (compact_hot)
+        self.hot_bits = self.hot_pref = self.hot_list = None
         self.global_offsets = None  # row shard: global symmetric offsets until the hot plan
         self.n_hot = 0
         self.hot_k = None  # k the hot tier was planned for (None = not planned)
@@ -312,8 +314,27 @@ class DeviceGraph:
             return
         check(lib.gee_hot_encode(ptr(self.targets), self.arcs, ptr(self.hot_rank), self.n_hot, _stream()),
               "gee_hot_encode")
+        self.compact_hot()
         self._sort_rows()
         self._pad_rows()
+
+    def compact_hot(self):
+        """hot_rank (int32 per vertex) -> hot_bits (u32 bitmap of the hot
+        vertices), hot_pref (hot vertices before each word) and hot_list (their
+        ranks in vertex order): what gee_build_projection_hotc reads each call
+        (graph preparation)."""
+        hr = self.hot_rank
+        n = hr.numel()
+        nw = (n + 31) // 32
+        hot = torch.zeros(nw * 32, dtype=torch.bool, device=hr.device)
+        hot[:n] = hr >= 0
+        hv = hot.view(nw, 32).to(torch.int64)
+        bits = (hv << torch.arange(32, device=hr.device, dtype=torch.int64)).sum(1)
+        self.hot_bits = torch.where(bits >= 2**31, bits - 2**32, bits).to(torch.int32)  # u32 bit pattern
+        cnt = hv.sum(1)
+        self.hot_pref = (torch.cumsum(cnt, 0) - cnt).to(torch.int32)
+        self.hot_list = hr[hot[:n]].contiguous()
+        del hv, bits, cnt, hot
 
     SORT_ROWS = True
     PAD_ROWS = 8  # pad every row to a multiple of 8 arcs (0: off)
@@ -430,11 +451,18 @@ class Embedder:
         if labels_d.numel() != self.n:
             raise ValidationError(f"graph has {self.n} nodes but labels have {labels_d.numel()}")
         hot_rank = g.hot_rank if (g is not None and g.hot_rank is not None) else None
-        n_hot = g.n_hot if hot_rank is not None else 0
+        compact = g is not None and getattr(g, "hot_bits", None) is not None and g.n_hot > 0
+        n_hot = g.n_hot if (hot_rank is not None or compact) else 0
         self._ensure_table(n_hot)
-        check(lib.gee_build_projection(ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.inv32),
-                                       ptr(self.inv64), ptr(self.table), ptr(hot_rank), n_hot, ptr(self.bad),
-                                       _stream()), "gee_build_projection")
+        if compact:
+            check(lib.gee_build_projection_hotc(ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.inv32),
+                                                ptr(self.inv64), ptr(self.table), ptr(g.hot_bits), ptr(g.hot_pref),
+                                                ptr(g.hot_list), n_hot, ptr(self.bad), _stream()),
+                  "gee_build_projection_hotc")
+        else:
+            check(lib.gee_build_projection(ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.inv32),
+                                           ptr(self.inv64), ptr(self.table), ptr(hot_rank), n_hot, ptr(self.bad),
+                                           _stream()), "gee_build_projection")
         self._mark("project", 2)
         self.table_n_hot = n_hot
         if validate and int(self.bad.item()):

@@ -67,7 +67,12 @@ class HostPipeline:
         self.bounds = plan_rows(off, max(1, chunks), k, self.weighted)
         pin = lambda t: None if t is None else t.cpu().pin_memory()  # noqa: E731
         # host copies of the prepared layout (the "stored graph")
-        self.h_hot = pin(g.hot_rank)
+        # the hot tier travels in compact form (bitmap, prefix, ranks)
+        self.h_hot = None
+        if g.hot_rank is not None:
+            if g.hot_bits is None:
+                g.compact_hot()
+            self.h_hot = [pin(g.hot_bits), pin(g.hot_pref), pin(g.hot_list)]
         self.n_hot = g.n_hot
         # packed targets (gee_pack_targets): per-8-arc-group byte-width deltas
         # and the real arcs' weights (pads rebuilt on the device)
@@ -84,12 +89,17 @@ class HostPipeline:
         for c in range(len(self.bounds) - 1):
             lo, hi = int(self.bounds[c]), int(self.bounds[c + 1])
             a0, a1 = int(off[lo]), int(off[hi])
-            self.h_off.append(torch.from_numpy(off[lo:hi + 1] - off[lo]).pin_memory())
+            # chunk-relative offsets travel as int32 when the chunk allows it
+            # (widened on the device): C4 saves 0.54 GB of H2D per call
+            rel = off[lo:hi + 1] - off[lo]
+            if rel[-1] < 2**31:
+                rel = rel.astype(np.int32)
+            self.h_off.append(torch.from_numpy(rel).pin_memory())
             v = DeviceGraph(hi - lo, 0, dev)
             v.n_nodes = g.n_nodes
             # plan the chunk's heavy rows / block spans on a temporary device
             # copy of its rebased offsets (graph preparation)
-            v.offsets = self.h_off[c].to(dev)
+            v.offsets = self.h_off[c].to(dev).long()
             v.targets = torch.empty(a1 - a0, dtype=torch.int32, device=dev)  # shape only
             v.weights = None
             v._plan_heavy()
@@ -116,14 +126,17 @@ class HostPipeline:
             self.scratch_bytes = int(_lib.lib.gee_unpack_scratch_bytes(max_arcs // 8))
             self.d_scratch = torch.empty(max(1, self.scratch_bytes), dtype=torch.uint8, device=dev)
         self.d_off = [torch.empty(max_rows + 1, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.d_off32 = [torch.empty(max_rows + 1, dtype=torch.int32, device=dev) for _ in range(2)]
         self.d_tgt = [torch.empty(max_arcs, dtype=torch.int32, device=dev) for _ in range(2)]
         self.d_w = [torch.empty(max_arcs, dtype=torch.float32, device=dev) if self.weighted else None
                     for _ in range(2)]
         self.d_z = [torch.empty(max_rows * k, dtype=torch.float32, device=dev) for _ in range(2)]
         self.d_y = torch.empty(self.n_nodes, dtype=torch.int32, device=dev)
-        self.d_hot = torch.empty(self.n_nodes, dtype=torch.int32, device=dev) if self.h_hot is not None else None
-        self.proj = DeviceGraph(self.n_nodes, 0, dev)  # what project() needs: hot ranks of all nodes
-        self.proj.hot_rank, self.proj.n_hot = self.d_hot, self.n_hot
+        self.d_hot = [torch.empty_like(t, device=dev) for t in self.h_hot] if self.h_hot is not None else None
+        self.proj = DeviceGraph(self.n_nodes, 0, dev)  # what project() needs: the hot tier of all nodes
+        if self.d_hot is not None:
+            self.proj.hot_bits, self.proj.hot_pref, self.proj.hot_list = self.d_hot
+            self.proj.n_hot = self.n_hot
         self.s_in = torch.cuda.Stream(dev)
         self.s_cmp = torch.cuda.Stream(dev)
         self.s_out = torch.cuda.Stream(dev)
@@ -157,7 +170,7 @@ class HostPipeline:
 
     def h2d_bytes(self, h_labels):
         b = h_labels.numel() * h_labels.element_size()
-        b += sum(t.numel() * 8 for t in self.h_off)
+        b += sum(t.numel() * t.element_size() for t in self.h_off)
         if self.packed:
             b += sum(t.numel() for t in self.h_ctl) + sum(t.numel() for t in self.h_pay)
             b += sum(t.numel() for t in self.h_wctl) + sum(t.numel() for t in self.h_wpay)
@@ -166,7 +179,7 @@ class HostPipeline:
             if self.h_w is not None:
                 b += self.h_w.numel() * 4
         if self.h_hot is not None:
-            b += self.h_hot.numel() * 4
+            b += sum(t.numel() * 4 for t in self.h_hot)
         return int(b)
 
     def _sparse_slots(self):
@@ -196,7 +209,8 @@ class HostPipeline:
         with torch.cuda.stream(self.s_in):
             self.d_y.copy_(h_labels, non_blocking=True)
             if self.d_hot is not None:
-                self.d_hot.copy_(self.h_hot, non_blocking=True)
+                for d, h in zip(self.d_hot, self.h_hot):
+                    d.copy_(h, non_blocking=True)
             e_lab.record(self.s_in)
         self.s_cmp.wait_event(e_lab)
         with torch.cuda.stream(self.s_cmp):
@@ -243,7 +257,8 @@ class HostPipeline:
         with torch.cuda.stream(self.s_in):
             if i >= 2:
                 self.s_in.wait_event(e_cmp[i - 2])  # slot b's CSR is free
-            self.d_off[b][:hi - lo + 1].copy_(self.h_off[i], non_blocking=True)
+            ho = self.h_off[i]
+            (self.d_off32 if ho.dtype == torch.int32 else self.d_off)[b][:hi - lo + 1].copy_(ho, non_blocking=True)
             if self.packed:
                 self.d_ctl[b][:self.h_ctl[i].numel()].copy_(self.h_ctl[i], non_blocking=True)
                 self.d_pay[b][:self.h_pay[i].numel()].copy_(self.h_pay[i], non_blocking=True)
@@ -266,6 +281,8 @@ class HostPipeline:
                     _lib.ptr(self.d_wpay[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
                     _lib.ptr(self.d_w[b]) if self.weighted else None, _lib.ptr(self.d_scratch),
                     self.scratch_bytes, _lib.stream_handle(self.s_cmp)), "gee_unpack_targets")
+            if self.h_off[i].dtype == torch.int32:
+                self.d_off[b][:hi - lo + 1].copy_(self.d_off32[b][:hi - lo + 1])  # widen on the device
             v.offsets = self.d_off[b][:hi - lo + 1]
             v.targets = self.d_tgt[b][:a1 - a0]
             v.weights = self.d_w[b][:a1 - a0] if self.weighted else None

@@ -699,3 +699,47 @@ def test_gather_labels_heads(k, head, monkeypatch):
         torch.cuda.synchronize()
         assert torch.equal(cls[:arcs], table[t.long()]), arcs
         assert bool((cls[arcs:] == 255).all()), arcs
+
+
+@pytest.mark.parametrize("k", [50, 300, 70_000])
+def test_projection_compact_hot_tier(k):
+    # gee_build_projection_hotc (bitmap + prefix + ranks in vertex order)
+    # writes the same label table and counts as the hot_rank form, for u8,
+    # u16 and int32 tables, with a ragged n (not a multiple of 4 or 32)
+    from paper_2402_04403_b200 import _lib
+
+    n = 1_000_003
+    dev = torch.device("cuda")
+    gen = torch.Generator(device="cuda").manual_seed(k)
+    hot = torch.rand(n, device=dev, generator=gen) < 0.2
+    n_hot = int(hot.sum())
+    hot_rank = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    hot_rank[hot] = torch.randperm(n_hot, device=dev, generator=gen).int()
+    labels = torch.randint(0, k + 1, (n,), dtype=torch.int32, device=dev, generator=gen)
+    g = DeviceGraph(n, 0, dev)
+    g.hot_rank = hot_rank
+    g.compact_hot()
+    lb = int(_lib.lib.gee_label_bytes(k))
+    tb = int(_lib.lib.gee_label_table_bytes(n, n_hot, k))
+    out = []
+    for compact in (False, True):
+        table = torch.full((tb,), 0xEE, dtype=torch.uint8, device=dev)
+        counts = torch.zeros(k + 1, dtype=torch.int64, device=dev)
+        if compact:
+            rc = _lib.lib.gee_build_projection_hotc(_lib.ptr(labels), n, k, _lib.ptr(counts), None, None,
+                                                    _lib.ptr(table), _lib.ptr(g.hot_bits), _lib.ptr(g.hot_pref),
+                                                    _lib.ptr(g.hot_list), n_hot, None, _lib.stream_handle())
+        else:
+            rc = _lib.lib.gee_build_projection(_lib.ptr(labels), n, k, _lib.ptr(counts), None, None,
+                                               _lib.ptr(table), _lib.ptr(hot_rank), n_hot, None,
+                                               _lib.stream_handle())
+        assert rc == 0, _lib.lib.gee_last_error()
+        torch.cuda.synchronize()
+        out.append((table.cpu().numpy(), counts.cpu().numpy()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[1][1], np.bincount(labels.cpu().numpy(), minlength=k + 1))
+    # the hot prefix holds each hot vertex's label at its rank
+    tab = out[1][0][:(n_hot + n + 1) * lb].view({1: np.uint8, 2: np.uint16, 4: np.int32}[lb])
+    hv = np.flatnonzero(hot.cpu().numpy())
+    assert np.array_equal(tab[hot_rank.cpu().numpy()[hv]], labels.cpu().numpy()[hv])
+    assert np.array_equal(tab[n_hot:n_hot + n], labels.cpu().numpy())
