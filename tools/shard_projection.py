@@ -1,0 +1,84 @@
+"""Row-shard step times of C4 at N = 1, 2, 4, 8 shards, measured one shard at
+a time on one B200 (dev / profiles tool).
+
+Row-range sharding (shard.build_row_shard) has no
+collective in the timed region: each rank runs the histogram of all labels
+and the pull of its own rows, and the step's time is the max over ranks.
+This box exposes one GPU, so every rank's step is timed here in turn: it
+builds that rank's shard, warms it up, and times `--steps` steps with CUDA
+events on the launching stream, exactly as bench.py does for each rank. The
+projection value = listed edges / max-over-ranks step time assumes that
+ranks on separate GPUs do not slow each other down. Nothing crosses NVLink
+or PCIe in the timed region, so only the host would be shared.
+
+Usage: python tools/shard_projection.py [--shards 1,2,4,8] [--steps 10]
+Prints one JSON line.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shards", default="1,2,4,8")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    args = ap.parse_args()
+
+    import torch
+
+    from paper_2402_04403_b200 import shard as shard_mod
+    from paper_2402_04403_b200 import synth
+    from paper_2402_04403_b200.device import DeviceGraph, Embedder
+
+    torch.cuda.set_device(0)
+    src, dst, w, y, n, k, _ = synth.make_config(args.config)
+    s = int(src.numel())
+    cfg = synth.CONFIGS[args.config]
+    out = {"workload": cfg.name, "s_listed_edges": s, "steps": args.steps, "warmup": args.warmup, "per_n": {}}
+    for nshards in (int(x) for x in args.shards.split(",")):
+        ranks = []
+        for rank in range(nshards):
+            if nshards == 1:
+                g = DeviceGraph.from_edges(src, dst, w, n, pull=True)
+                lo, hi = 0, n
+            else:
+                g, lo, hi = shard_mod.build_row_shard(src, dst, w, n, nshards, rank, k=k)
+            g.prepare_hot(k)
+            emb = Embedder(n, k)
+            z = torch.empty((hi - lo, k), dtype=torch.float32, device="cuda")
+            emb.project(y, validate=True, g=g)
+            for _ in range(args.warmup):
+                emb.project(y, validate=False, g=g)
+                emb.pull(g, z)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(args.steps):
+                emb.project(y, validate=False, g=g)
+                emb.pull(g, z)
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / args.steps
+            ranks.append({"rank": rank, "rows": hi - lo, "arcs": int(g.arcs), "ms_per_step": ms})
+            del g, emb, z
+            torch.cuda.empty_cache()
+        worst = max(r["ms_per_step"] for r in ranks)
+        mean = sum(r["ms_per_step"] for r in ranks) / len(ranks)
+        out["per_n"][nshards] = {"max_ms": worst, "mean_ms": mean, "balance": mean / worst,
+                                 "projected_geps": s / (worst * 1e-3) / 1e9, "ranks": ranks}
+    base = out["per_n"].get(1)
+    if base:
+        for nshards, r in out["per_n"].items():
+            r["projected_efficiency"] = base["max_ms"] / (nshards * r["max_ms"])
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
