@@ -743,3 +743,30 @@ def test_projection_compact_hot_tier(k):
     hv = np.flatnonzero(hot.cpu().numpy())
     assert np.array_equal(tab[hot_rank.cpu().numpy()[hv]], labels.cpu().numpy()[hv])
     assert np.array_equal(tab[n_hot:n_hot + n], labels.cpu().numpy())
+
+
+@pytest.mark.parametrize("k", [5, 300])
+def test_projection_counts_out_of_range_labels(k):
+    # labels outside [0, k] (LabelVector rejects them, labeling.py:24-29) are
+    # reported through `bad`, left out of the counts and stored as 0
+    from paper_2402_04403_b200 import _lib
+
+    dev = torch.device("cuda")
+    lab = torch.tensor([1, -1, k, k + 1, 0, 2**31 - 1, 3, -(2**31)] * 1001, dtype=torch.int32, device=dev)
+    n = lab.numel()
+    tb = int(_lib.lib.gee_label_table_bytes(n, 0, k))
+    table = torch.full((tb,), 0xEE, dtype=torch.uint8, device=dev)
+    counts = torch.zeros(k + 1, dtype=torch.int64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    rc = _lib.lib.gee_build_projection(_lib.ptr(lab), n, k, _lib.ptr(counts), None, None, _lib.ptr(table), None, 0,
+                                       _lib.ptr(bad), _lib.stream_handle())
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 4 * 1001
+    exp = np.zeros(k + 1, dtype=np.int64)
+    exp[[1, k, 0, 3]] += 1001
+    assert np.array_equal(counts.cpu().numpy(), exp)
+    lb = int(_lib.lib.gee_label_bytes(k))
+    tab = table.cpu().numpy()[:(n + 1) * lb].view({1: np.uint8, 2: np.uint16}[lb])
+    want = np.where((lab.cpu().numpy() >= 0) & (lab.cpu().numpy() <= k), lab.cpu().numpy(), 0)
+    assert np.array_equal(tab[:n], want) and tab[n] == 0
