@@ -770,3 +770,30 @@ def test_projection_counts_out_of_range_labels(k):
     tab = table.cpu().numpy()[:(n + 1) * lb].view({1: np.uint8, 2: np.uint16}[lb])
     want = np.where((lab.cpu().numpy() >= 0) & (lab.cpu().numpy() <= k), lab.cpu().numpy(), 0)
     assert np.array_equal(tab[:n], want) and tab[n] == 0
+
+
+@pytest.mark.parametrize("k,labeled", [(100, 0.1), (5, 1.0)])
+def test_host_pipeline_unit_weights(k, labeled):
+    # the streamed pass on an unweighted graph (packed targets, no weight
+    # streams; C3-like 10% labeled K=100 and a small-K table): Z equals the
+    # resident pull bit for bit, and the oracle within tolerance
+    from paper_2402_04403_b200.stream import HostPipeline, pinned_like
+
+    scale, s = 16, 600_000
+    n = 1 << scale
+    src, dst, _ = synth.rmat_edges(scale, s, seed=k, weighted=False)
+    y = torch.from_numpy(gb.random_labels(n, k, labeled, seed=k).labels).cuda()
+    dev = torch.device("cuda")
+    g = DeviceGraph.from_edges(src, dst, None, n, device=dev, pull=True)
+    g.prepare_hot(k, enable=True)
+    emb = Embedder(n, k, dev)
+    emb.project(y, g=g)
+    z_ref = emb.pull(g).cpu()
+    pipe = HostPipeline(g, k, chunks=3)
+    assert pipe.packed and not pipe.weighted
+    h_z = pinned_like((n, k))
+    h_z.fill_(float("nan"))
+    pipe.run(y.cpu().pin_memory(), h_z, emb)
+    assert torch.equal(h_z, z_ref)
+    exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), None, y.cpu().numpy(), n, k)
+    assert rel_err(h_z.numpy(), exp) <= TOL
