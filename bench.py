@@ -433,7 +433,7 @@ def main():
         "dtype": "f32 (exact integer fixed-point accumulation)" if weighted else "f32 (exact u32 counts)",
         "data": "synthetic (seeded R-MAT; Friendster unavailable)",
         "config": {"workload": workload, "n": n, "s_listed_edges": s, "k": k, "weighted": bool(weighted),
-                   "directed": bool(directed), "variant": "pull", "reducer": "wide" if k > 255 else emb.reducer, "sym_arcs": arcs,
+                   "directed": bool(directed), "variant": "pull", "reducer": emb.reducer_for(g), "sym_arcs": arcs,
                    "padded_arcs": g.arcs, "row_pad": g.padded,
                    "parallelism": f"row-range x{world}" if world > 1 else "single GPU",
                    "l2": "inputs (CSR %.1f GB) >> 126 MB L2; no flush needed" % (g.csr_bytes() / 1e9),

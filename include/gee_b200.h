@@ -17,8 +17,8 @@
  *     (labeling.py:10-26, encoder.py:3-10).
  *   - Z is a dense row-major (n, k) float32 array.  Its accumulator is exact
  *     integer arithmetic in the pull path and fp32 red.global in the push path.
- *   - Hot-path calls (gee_build_projection, gee_embed_coo, gee_embed_csr_pull)
- *     never allocate; graph-preparation calls (gee_build_csr, gee_hot_plan,
+ *   - Hot-path calls (gee_build_projection*, gee_embed_coo, gee_gather_labels,
+ *     gee_reduce_blocks_pad8, gee_reduce_heavy, gee_reduce_wide) never allocate; graph-preparation calls (gee_build_csr, gee_hot_plan,
  *     gee_graph_stats, ...) may allocate stream-ordered scratch with
  *     cudaMallocAsync and free it before returning.
  *
@@ -52,11 +52,6 @@ extern "C" {
 
 /* Library version (major*10000 + minor*100 + patch). */
 int gee_version(void);
-
-/* Debug builds only (libgee_b200_debug.so, -DGEE_DEBUG): the first bounds
- * violation a kernel recorded {check id, index, limit, thread}, then reset.
- * Release builds return zeros. */
-int gee_debug_word(unsigned int *out4);
 
 /* Thread-local message of the last failing call ("" if none). */
 const char *gee_last_error(void);
@@ -180,38 +175,6 @@ int gee_hot_plan(const int64_t *offsets, int64_t n, int64_t max_hot, int64_t min
 int gee_hot_encode(int32_t *targets, int64_t arcs, const int32_t *hot_rank, int64_t n_hot,
                    void *stream);
 
-/* ---------------------------------------------------------------- K4 ----
- * Pull (row-owner) edge map over a symmetric CSR whose targets are
- * label-table slots.  Tile j covers arcs [j*GEE_TILE_ARCS, (j+1)*GEE_TILE_ARCS)
- * and owns the rows whose first arc position offsets[r] falls in it.
- * gee_pull_plan (graph preparation) writes tile_row[n_tiles+1] (first owned
- * row of each tile), chunk_row[gee_pull_chunks(arcs)] (u16: row of the first
- * arc of each 16-arc chunk relative to the tile's first row) and the list of
- * tiles whose last row continues past them (cut_tiles[n_tiles], count in
- * *n_cut, host).  Per row x:
- *     Z[x, c] = inv[c+1] * sum_{arcs x->v, Y[v]=c+1} w
- * accumulated exactly in integers (unit weights: counts; weighted: fixed
- * point w*2^scale_exp rounded to int64), so Z is bit-stable run to run and
- * independent of arc order.  Every row of Z is written exactly once; no
- * zeroing is needed.  Rows that span tiles are combined through `slots`
- * (gee_pull_slots_bytes bytes, zero on first use, left zero on return).
- *   w == NULL means unit weights (scale_exp ignored).  inv: inv_f64[k+1].
- * Replaces embed_parallel's zero wave + arc wave (encoder.py:123-194,
- * zero_worker _kernels.py:124-135, arc_pass_worker _kernels.py:138-207)
- * for SOURCE_ONLY (symmetric) storage.
- */
-#define GEE_TILE_ARCS 4096
-int64_t gee_pull_tiles(int64_t arcs);
-int64_t gee_pull_chunks(int64_t arcs);
-size_t gee_pull_slots_bytes(int64_t arcs, int32_t k);
-int gee_pull_plan(const int64_t *offsets, int64_t n, int64_t arcs, int64_t *tile_row,
-                  uint16_t *chunk_row, int32_t *cut_tiles, int64_t *n_cut, void *stream);
-int gee_embed_csr_pull(const int64_t *offsets, const int32_t *targets, const float *w,
-                       int64_t n, int64_t arcs, const int64_t *tile_row,
-                       const uint16_t *chunk_row, const int32_t *cut_tiles, int64_t n_cut,
-                       int32_t scale_exp, const void *table, int64_t n_hot, const double *inv,
-                       int32_t k, float *z, void *slots, void *stream);
-
 /* Wide-embedding pull (any k; the default for k > 255, BASELINE C5): the
  * label gather fused with a per-row class window.  Replaces the parallel
  * arc wave of embed_parallel (_kernels.py:138-207, SOURCE_ONLY arcs of the
@@ -271,61 +234,36 @@ int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t group
                        size_t scratch_bytes, void *stream);
 
 /* Class stream: cls[e] = table[targets[e]] (u8, k <= 255) for every arc of
- * a pull layout -- the random half of the pull pass on its own (label-table
- * head staged in shared memory; measurement and split-pass use). */
+ * a pull layout -- the random half of the pull pass (the hottest label-table
+ * slots staged in a packed shared-memory head of head_bytes, -1 = the tuned
+ * default of 96 KB, 0 = none). */
 int gee_gather_labels(const int32_t *targets, int64_t arcs, const void *table, int64_t n_hot,
                       int32_t k, uint8_t *cls, void *stream);
+int gee_gather_labels_head(const int32_t *targets, int64_t arcs, const void *table, int64_t n_hot,
+                           int32_t k, int64_t head_bytes, uint8_t *cls, void *stream);
 
-/* Split pull: the same edge map over the class stream from
- * gee_gather_labels (cls[e] = label of arc e's target, k <= 255) instead
- * of gathering labels itself. */
-int gee_embed_csr_pull_cls(const int64_t *offsets, const uint8_t *cls, const float *w, int64_t n,
-                           int64_t arcs, const int64_t *tile_row, const uint16_t *chunk_row,
-                           const int32_t *cut_tiles, int64_t n_cut, int32_t scale_exp,
-                           const double *inv, int32_t k, float *z, void *slots, void *stream);
-
-/* Row-per-warp segmented reduction over the class stream (the second half
- * of the split pull; gee_reduce.cu).  Writes every row of Z: rows with no
- * arcs as zeros, rows with at most heavy_arcs arcs directly, heavier rows
- * (gee_reduce_heavy_plan lists them) through chunks of heavy_arcs arcs whose
- * exact int64 partials meet in heavy_acc[n_heavy*k] (zero on first use, left
- * zero).  chunk_first[q] / chunk_heavy[q]: first arc and heavy-row index of
- * chunk q.  k <= 255. */
+/* Graph preparation for the split pull: list the rows with more than
+ * heavy_arcs arcs (heavy_rows[n], count in *n_heavy, host; allocates,
+ * synchronises). */
 int gee_reduce_heavy_plan(const int64_t *offsets, int64_t n, int64_t heavy_arcs,
                           int32_t *heavy_rows, int64_t *n_heavy, void *stream);
-int gee_reduce_rows(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
-                    int32_t scale_exp, const double *inv, int32_t k, int64_t heavy_arcs,
-                    const int32_t *heavy_rows, int64_t n_heavy, const int64_t *chunk_first,
-                    const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
-                    void *stream);
-
-/* Degree-binned reduction: gee_reduce_bins lists the rows with at most
- * small_arcs arcs (empty rows included) and those with more but at most
- * heavy_arcs, each in row order; gee_reduce_lists reduces them with 8-lane
- * groups (small) and whole warps (medium) and the heavy rows in chunks, as
- * gee_reduce_rows does.  Every row of Z is written. */
-int gee_reduce_bins(const int64_t *offsets, int64_t n, int64_t small_arcs, int64_t heavy_arcs,
-                    int32_t *small_rows, int32_t *medium_rows, int64_t *n_small, int64_t *n_medium,
-                    void *stream);
-int gee_reduce_lists(const int64_t *offsets, const int32_t *small_rows, int64_t n_small,
-                     const int32_t *medium_rows, int64_t n_medium, const uint8_t *cls,
-                     const float *w, int32_t scale_exp, const double *inv, int32_t k,
-                     int64_t heavy_arcs, const int32_t *heavy_rows, int64_t n_heavy,
-                     const int64_t *chunk_first, const int32_t *chunk_heavy, int64_t n_chunks,
-                     void *heavy_acc, float *z, void *stream);
-
-/* Block reduction: one warp per 32 consecutive rows (coalesced offsets,
- * streamed arcs, one flat coalesced write of the block's Z rows); heavy rows
- * as in gee_reduce_rows.  k <= 255; heavy_arcs <= 2048; weighted graphs need
- * the exponent from gee_block_scale_exp (carry-free split accumulators). */
-int gee_reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
-                      int32_t scale_exp, const double *inv, int32_t k, int64_t heavy_arcs,
-                      const int32_t *heavy_rows, int64_t n_heavy, const int64_t *chunk_first,
-                      const int32_t *chunk_heavy, int64_t n_chunks, void *heavy_acc, float *z,
-                      void *stream);
-
-/* gee_reduce_blocks for PADDED rows (gee_pad_rows, align 8): light rows
- * only (heavy rows are left to gee_reduce_heavy). */
+/* ---------------------------------------------------------------- K4 ----
+ * Pull (row-owner) edge map, split in two: gee_gather_labels (class stream)
+ * then the segmented class reduction below.  Together they replace
+ * embed_parallel's zero wave + arc wave (encoder.py:123-194, zero_worker
+ * _kernels.py:124-135, arc_pass_worker _kernels.py:138-207) for SOURCE_ONLY
+ * (symmetric) storage, k <= 255 (wider k: gee_reduce_wide).  Per row x:
+ *     Z[x, c] = inv[c+1] * sum_{arcs x->v, Y[v]=c+1} w
+ * accumulated exactly in integers (unit weights: counts; weighted: fixed
+ * point q = rint(w * 2^scale_exp), scale_exp from gee_block_scale_exp, signed
+ * weights allowed), so Z is bit-stable run to run and independent of arc
+ * order.
+ *
+ * Block reduction over PADDED rows (gee_pad_rows, align 8): one warp per 32
+ * consecutive rows (coalesced offsets, arcs streamed through a cp.async
+ * ring, slot windows of shared-memory atomics); writes every row with at
+ * most heavy_arcs (<= 2048) arcs, empty rows as zeros, and leaves the longer
+ * rows to gee_reduce_heavy.  z 16-byte aligned. */
 int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
                            int32_t scale_exp, const double *inv, int32_t k, int64_t heavy_arcs, float *z,
                            void *stream);
@@ -345,17 +283,13 @@ int gee_reduce_heavy(const uint8_t *cls, const float *w, int64_t arcs, int32_t s
                      const int32_t *item_slot, int64_t n_items, const int32_t *mega_rows, int64_t n_mega,
                      void *mega_acc, int64_t *counter, float *z, void *stream);
 
-/* Fixed-point exponent valid for every pull reducer, gee_reduce_blocks
- * included: the largest e with max_row_abs * 2^e < 2^62 and
- * max_abs * 2^e < 2^42.  *rel_err = 2^-(e+1)/min_abs_nz (host). */
+/* Fixed-point exponent valid for every pull reducer: the largest e with
+ * max_row_abs * 2^e < 2^62 (64-bit row sums) and max_abs * 2^e < 2^41 (the
+ * signed split planes of a 2048-arc row cannot overflow).
+ * *rel_err = 2^-(e+1)/min_abs_nz (host): the worst per-term rounding,
+ * relative to the smallest nonzero |w|. */
 int gee_block_scale_exp(double max_row_abs, double max_abs, double min_abs_nz, int32_t *scale_exp,
                         double *rel_err);
-
-/* Choose the fixed-point exponent for a weighted pull: the largest e with
- * max_row_abs * 2^e < 2^62.  Returns the relative quantisation bound
- * 2^-(e+1)/min_abs_nz through *rel_err (host). */
-int gee_pull_scale_exp(double max_row_abs, double min_abs_nz, int32_t *scale_exp,
-                       double *rel_err);
 
 #ifdef __cplusplus
 }

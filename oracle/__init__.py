@@ -54,6 +54,13 @@ def lib():
         L.oracle_atomic_hammer.restype = None
         L.oracle_sampled_rows.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, i64]
         L.oracle_sampled_rows.restype = None
+        u64 = ctypes.c_uint64
+        L.oracle_rmat.argtypes = [vp, vp, vp, i64, i64, i32, dbl, dbl, dbl, u64, i32, i32]
+        L.oracle_rmat.restype = None
+        L.oracle_uniform_labels.argtypes = [vp, i64, i64, u64]
+        L.oracle_uniform_labels.restype = None
+        L.oracle_build_csr_directed_par.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, i32]
+        L.oracle_build_csr_directed_par.restype = None
         _lib = L
     return _lib
 
@@ -172,3 +179,44 @@ def numpy_reference(src, dst, w, labels, n, k):
     m = ys > 0
     np.add.at(z, (dst[m], ys[m] - 1), wrow[src[m]] * w[m])
     return z
+
+
+# ------------------------------------------------ CPU arm inputs (bench.py)
+RMAT_ABC = (0.57, 0.19, 0.19)
+
+
+def rmat_edges(scale, s, seed, weighted=False, first=0, threads=None, scramble=True):
+    """C restatement of synth.rmat_edges_numpy: int32 src/dst (+ f32 w), all
+    host threads.  The reference arm builds its inputs with this, so it never
+    loads the product library."""
+    src = np.empty(s, dtype=np.int32)
+    dst = np.empty(s, dtype=np.int32)
+    w = np.empty(s, dtype=np.float32) if weighted else None
+    a, b, c = RMAT_ABC
+    lib().oracle_rmat(_p(src), _p(dst), None if w is None else _p(w), first, s, scale, a, b, c,
+                      seed & ((1 << 64) - 1), 1 if scramble else 0, threads or os.cpu_count() or 1)
+    return src, dst, w
+
+
+def uniform_labels(n, k, seed):
+    """C restatement of synth.uniform_labels_numpy (int32, 1..k)."""
+    y = np.empty(n, dtype=np.int32)
+    lib().oracle_uniform_labels(_p(y), n, k, seed & ((1 << 64) - 1))
+    return y
+
+
+def build_csr_directed_par(src, dst, w, n, threads=None):
+    """Directed build_csr (graph.py:159-184) in the reference dtypes (int64
+    offsets, int32 targets, f64 weights or None for unit), threaded; arc
+    order within a row unspecified."""
+    src = np.ascontiguousarray(src, dtype=np.int32)
+    dst = np.ascontiguousarray(dst, dtype=np.int32)
+    s = src.size
+    offsets = np.empty(n + 1, dtype=np.int64)
+    targets = np.empty(s, dtype=np.int32)
+    weights = np.empty(s, dtype=np.float64) if w is not None else None
+    wf = None if w is None else np.ascontiguousarray(w, dtype=np.float32)
+    lib().oracle_build_csr_directed_par(_p(src), _p(dst), None if wf is None else _p(wf), s, n, _p(offsets),
+                                        _p(targets), None if weights is None else _p(weights),
+                                        threads or os.cpu_count() or 1)
+    return offsets, targets, weights

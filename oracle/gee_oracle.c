@@ -279,3 +279,160 @@ void oracle_sampled_rows(const int32_t *src, const int32_t *dst, const float *w,
         }
     }
 }
+
+/* ---- seeded synthetic inputs for the CPU arm (bench.py --impl reference) ----
+ *
+ * A C restatement of the counter-based generator the workload uses
+ * (paper_2402_04403_b200/synth.py: word_numpy, rmat_edges_numpy,
+ * uniform_labels_numpy), so the reference arm builds the SAME C4 graph on the
+ * host without loading the product library.  Pinned bit for bit against the
+ * numpy restatement (tests/test_oracle.py) and, on the GPU, against
+ * gee_synth_rmat (tests/test_gpu_parity.py). */
+static inline uint64_t sm64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+static inline uint64_t synth_word(uint64_t seed, uint64_t tag, uint64_t ctr)
+{
+    return sm64(sm64(seed ^ (tag * 0xD1B54A32D192ED03ull)) + ctr);
+}
+
+static inline uint64_t scramble(uint64_t x, int scale, uint64_t m1, uint64_t m2)
+{
+    const uint64_t mask = (scale >= 64) ? ~0ull : ((1ull << scale) - 1ull);
+    const int h = scale / 2 > 1 ? scale / 2 : 1;
+    x = (x * m1) & mask;
+    x ^= x >> h;
+    x = (x * m2) & mask;
+    x ^= x >> (h + (scale & 1));
+    return (x * m1) & mask;
+}
+
+typedef struct {
+    int32_t *src, *dst;
+    float *w;
+    int64_t first, s;
+    int scale, scramble;
+    uint64_t seed, ta, tab, tabc, m1, m2;
+    int64_t lo, hi;
+} rmat_job;
+
+static void *rmat_worker(void *arg)
+{
+    rmat_job *j = (rmat_job *)arg;
+    for (int64_t q = j->lo; q < j->hi; q++) {
+        const uint64_t i = (uint64_t)(j->first + q);
+        uint64_t u = 0, v = 0, bits = 0;
+        for (int lvl = 0; lvl < j->scale; lvl++) {
+            if ((lvl & 1) == 0)
+                bits = synth_word(j->seed, 1, i * 32u + (uint64_t)(lvl >> 1));
+            const uint64_t r = (lvl & 1) ? (bits >> 32) : (bits & 0xFFFFFFFFull);
+            const uint64_t bu = r >= j->tab;
+            const uint64_t bv = ((r >= j->ta) && (r < j->tab)) || (r >= j->tabc);
+            u = (u << 1) | bu;
+            v = (v << 1) | bv;
+        }
+        if (j->scramble) {
+            u = scramble(u, j->scale, j->m1, j->m2);
+            v = scramble(v, j->scale, j->m1, j->m2);
+        }
+        j->src[q] = (int32_t)u;
+        j->dst[q] = (int32_t)v;
+        if (j->w)
+            j->w[q] = 1.0f - (float)(synth_word(j->seed, 2, i) >> 40) * (1.0f / 16777216.0f);
+    }
+    return NULL;
+}
+
+/* rmat_edges_numpy(scale, s, seed, weighted, a, b, c, scramble, first). */
+void oracle_rmat(int32_t *src, int32_t *dst, float *w, int64_t first, int64_t s, int scale, double a,
+                 double b, double c, uint64_t seed, int do_scramble, int threads)
+{
+    const double two32 = 4294967296.0;
+    rmat_job base = {src, dst, w, first, s, scale, do_scramble, seed,
+                     (uint64_t)(a * two32), (uint64_t)((a + b) * two32), (uint64_t)((a + b + c) * two32),
+                     sm64(seed ^ 0x5EED1ull) | 1ull, sm64(seed ^ 0x5EED2ull) | 1ull, 0, 0};
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t t[256];
+    rmat_job jobs[256];
+    for (int i = 0; i < threads; i++) {
+        jobs[i] = base;
+        jobs[i].lo = s * i / threads;
+        jobs[i].hi = s * (i + 1) / threads;
+        pthread_create(&t[i], NULL, rmat_worker, &jobs[i]);
+    }
+    for (int i = 0; i < threads; i++) pthread_join(t[i], NULL);
+}
+
+/* uniform_labels_numpy(n, k, seed): 1 + ((word(seed, 4, i) >> 32) * k >> 32). */
+void oracle_uniform_labels(int32_t *y, int64_t n, int64_t k, uint64_t seed)
+{
+    for (int64_t i = 0; i < n; i++)
+        y[i] = (int32_t)(1 + (((synth_word(seed, 4, (uint64_t)i) >> 32) * (uint64_t)k) >> 32));
+}
+
+/* ---- build_csr for the CPU arm at full size ----
+ *
+ * graph.py:159-184 (directed storage: one arc per listed edge) with the
+ * degree count and the fill spread over threads (atomic per-row cursors),
+ * in the reference's dtypes: int64 offsets, int32 targets, f64 weights.
+ * Arc order inside a row is not the reference's (that one is serial and
+ * stable, oracle_build_csr above); it only changes the f64 summation order
+ * of the timed pass, not its work.  Graph construction is outside the
+ * reference's timed region (bench.py:1-7). */
+typedef struct {
+    const int32_t *src, *dst;
+    const float *w;
+    int64_t lo, hi;
+    int64_t *cnt;
+    int32_t *targets;
+    double *weights;
+} csr_job;
+
+static void *csr_count(void *arg)
+{
+    csr_job *j = (csr_job *)arg;
+    for (int64_t i = j->lo; i < j->hi; i++)
+        __atomic_fetch_add(&j->cnt[j->src[i]], 1, __ATOMIC_RELAXED);
+    return NULL;
+}
+
+static void *csr_fill_par(void *arg)
+{
+    csr_job *j = (csr_job *)arg;
+    for (int64_t i = j->lo; i < j->hi; i++) {
+        const int64_t p = __atomic_fetch_add(&j->cnt[j->src[i]], 1, __ATOMIC_RELAXED);
+        j->targets[p] = j->dst[i];
+        if (j->weights) j->weights[p] = j->w ? (double)j->w[i] : 1.0;
+    }
+    return NULL;
+}
+
+void oracle_build_csr_directed_par(const int32_t *src, const int32_t *dst, const float *w, int64_t s, int64_t n,
+                                   int64_t *offsets, int32_t *targets, double *weights, int threads)
+{
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    int64_t *cnt = (int64_t *)calloc((size_t)(n + 1), sizeof(int64_t));
+    pthread_t t[256];
+    csr_job jobs[256];
+    for (int i = 0; i < threads; i++) {
+        csr_job jb = {src, dst, w, s * i / threads, s * (i + 1) / threads, cnt, targets, weights};
+        jobs[i] = jb;
+        pthread_create(&t[i], NULL, csr_count, &jobs[i]);
+    }
+    for (int i = 0; i < threads; i++) pthread_join(t[i], NULL);
+    offsets[0] = 0;
+    for (int64_t r = 0; r < n; r++) {
+        offsets[r + 1] = offsets[r] + cnt[r];
+        cnt[r] = offsets[r];
+    }
+    for (int i = 0; i < threads; i++) pthread_create(&t[i], NULL, csr_fill_par, &jobs[i]);
+    for (int i = 0; i < threads; i++) pthread_join(t[i], NULL);
+    free(cnt);
+}

@@ -7,7 +7,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libgee_b200.so")
-SOURCES = ["gee_capi.cu", "gee_projection.cu", "gee_push.cu", "gee_pull.cu", "gee_prep.cu", "gee_hot.cu", "gee_gather.cu", "gee_reduce.cu", "gee_wide.cu", "gee_compact.cu", "gee_pack.cu", "gee_synth.cu"]
+SOURCES = ["gee_capi.cu", "gee_projection.cu", "gee_push.cu", "gee_prep.cu", "gee_hot.cu", "gee_gather.cu", "gee_reduce.cu", "gee_wide.cu", "gee_compact.cu", "gee_pack.cu", "gee_synth.cu"]
 HEADERS = ["gee_common.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -51,17 +51,35 @@ def build_io_library(force=False, verbose=False):
     return IO_LIB
 
 
-def build_library(force=False, verbose=False, debug=False):
+def build_library(force=False, verbose=False):
     """Compile every CUDA source into paper_2402_04403_b200/libgee_b200.so
-    (debug=True: libgee_b200_debug.so with -DGEE_DEBUG bounds checks)."""
-    lib = LIB.replace(".so", "_debug.so") if debug else LIB
+    (one nvcc process per source, in parallel, then one link)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    lib = LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(ROOT, "include", "gee_b200.h"), os.path.join(ROOT, "include", "gee_synth.h")]
-    if not force and not _stale(lib, deps):
+    if not force and not _stale(lib, srcs + hdrs):
         return lib
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def obj(src):
+        o = os.path.join(objdir, os.path.basename(src) + ".o")
+        if force or _stale(o, [src] + hdrs):
+            cmd = [_nvcc(), *compile_flags, "-c", "-o", o + ".tmp", src]
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.run(cmd, check=True, cwd=CSRC)
+            os.replace(o + ".tmp", o)
+        return o
+
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(obj, srcs))
     tmp = lib + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DGEE_DEBUG"] if debug else []), "-o", tmp, *srcs]
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=CSRC)

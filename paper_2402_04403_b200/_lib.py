@@ -10,10 +10,7 @@ import os
 from .errors import GeeError, ValidationError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-# GEE_LIB_VARIANT=<tag> loads libgee_b200_<tag>.so from the package (build
-# experiments); GEE_DEBUG_LIB=1 the bounds-checked debug build.
-_VARIANT = os.environ.get("GEE_LIB_VARIANT") or ("debug" if os.environ.get("GEE_DEBUG_LIB") else "")
-LIB_PATH = os.path.join(_PKG, f"libgee_b200_{_VARIANT}.so" if _VARIANT else "libgee_b200.so")
+LIB_PATH = os.path.join(_PKG, "libgee_b200.so")
 
 GEE_OK = 0
 GEE_ERR_INVALID = 1
@@ -23,8 +20,6 @@ GEE_ERR_RANGE = 3
 GEE_ZERO_Z = 1
 GEE_SOURCE_ONLY = 2
 GEE_PRECOMBINE = 4
-
-TILE_ARCS = 4096
 
 c_int = ctypes.c_int
 c_i32 = ctypes.c_int32
@@ -42,7 +37,6 @@ P_i32 = ctypes.POINTER(ctypes.c_int32)
 SIGNATURES = {
     "gee_version": (c_int, []),
     "gee_last_error": (ctypes.c_char_p, []),
-    "gee_debug_word": (c_int, [ctypes.POINTER(ctypes.c_uint * 4)]),
     "gee_label_bytes": (c_int, [c_i32]),
     "gee_label_table_bytes": (c_size, [c_i64, c_i64, c_i32]),
     "gee_projection_work_bytes": (c_size, [c_i32]),
@@ -57,14 +51,8 @@ SIGNATURES = {
     "gee_graph_stats": (c_int, [vp, vp, c_i64, c_i64, P_dbl, P_dbl, P_dbl, P_i32, vp]),
     "gee_hot_plan": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, ctypes.POINTER(c_i64), vp]),
     "gee_hot_encode": (c_int, [vp, c_i64, vp, c_i64, vp]),
-    "gee_pull_tiles": (c_i64, [c_i64]),
-    "gee_pull_chunks": (c_i64, [c_i64]),
-    "gee_pull_slots_bytes": (c_size, [c_i64, c_i32]),
-    "gee_pull_plan": (c_int, [vp, c_i64, c_i64, vp, vp, vp, ctypes.POINTER(c_i64), vp]),
-    "gee_embed_csr_pull": (c_int, [vp, vp, vp, c_i64, c_i64, vp, vp, vp, c_i64, c_i32, vp, c_i64, vp, c_i32, vp, vp,
-                                   vp]),
-    "gee_pull_scale_exp": (c_int, [c_dbl, c_dbl, P_i32, P_dbl]),
     "gee_gather_labels": (c_int, [vp, c_i64, vp, c_i64, c_i32, vp, vp]),
+    "gee_gather_labels_head": (c_int, [vp, c_i64, vp, c_i64, c_i32, c_i64, vp, vp]),
     "gee_zc_blocks": (c_i64, [c_i64]),
     "gee_z_compact": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp]),
     "gee_unpack_scratch_bytes": (c_size, [c_i64]),
@@ -73,18 +61,12 @@ SIGNATURES = {
     "gee_unpack_targets": (c_int, [vp, vp, c_i64, vp, vp, c_i32, vp, vp, vp, c_size, vp]),
     "gee_reduce_wide": (c_int, [vp, c_i64, vp, vp, vp, c_i32, c_i32, vp, vp, c_i64, vp, vp]),
     "gee_reduce_heavy_plan": (c_int, [vp, c_i64, c_i64, vp, ctypes.POINTER(c_i64), vp]),
-    "gee_reduce_blocks": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, c_i64, vp, vp, c_i64, vp, vp, vp]),
     "gee_pad_offsets": (c_int, [vp, c_i64, c_i64, vp, vp, vp]),
     "gee_pad_rows": (c_int, [vp, vp, c_i64, vp, vp, c_i32, vp, vp, vp]),
     "gee_sort_rows": (c_int, [vp, c_i64, vp, vp, vp]),
     "gee_reduce_blocks_pad8": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, vp]),
     "gee_reduce_heavy": (c_int, [vp, vp, c_i64, c_i32, vp, c_i32, vp, vp, vp, vp, c_i64, vp, c_i64, vp, vp, vp, vp]),
     "gee_block_scale_exp": (c_int, [c_dbl, c_dbl, c_dbl, P_i32, P_dbl]),
-    "gee_reduce_bins": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), vp]),
-    "gee_reduce_lists": (c_int, [vp, vp, c_i64, vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, c_i64, vp, vp, c_i64,
-                                 vp, vp, vp]),
-    "gee_reduce_rows": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, c_i64, vp, vp, c_i64, vp, vp, vp]),
-    "gee_embed_csr_pull_cls": (c_int, [vp, vp, vp, c_i64, c_i64, vp, vp, vp, c_i64, c_i32, vp, c_i32, vp, vp, vp]),
     "gee_synth_word": (c_u64, [c_u64, c_u64, c_u64]),
     "gee_synth_rmat": (c_int, [vp, vp, vp, c_i64, c_i64, c_i32, c_dbl, c_dbl, c_dbl, c_u64, c_i32, vp]),
     "gee_synth_er": (c_int, [vp, vp, vp, c_i64, c_i64, c_i64, c_u64, vp]),

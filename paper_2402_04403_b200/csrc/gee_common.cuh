@@ -91,28 +91,6 @@ __device__ __forceinline__ uint64_t policy_evict_last()
 
 }  // namespace gee
 
-// Debug builds (-DGEE_DEBUG, libgee_b200_debug.so): bounds checks that
-// record the first violation in gee_debug_word and clamp the index, so an
-// out-of-range access is reported instead of faulting.
-#ifdef GEE_DEBUG
-static __device__ unsigned int g_gee_dbg[4];  // per translation unit (no -rdc)
-__device__ __forceinline__ int gee_dclamp(long long i, long long lim, unsigned id)
-{
-    if (i < 0 || i >= lim) {
-        if (atomicCAS(&g_gee_dbg[0], 0u, id) == 0u) {
-            g_gee_dbg[1] = (unsigned)i;
-            g_gee_dbg[2] = (unsigned)lim;
-            g_gee_dbg[3] = blockIdx.x * 1024 + threadIdx.x;
-        }
-        return i < 0 ? 0 : (int)(lim - 1);
-    }
-    return (int)i;
-}
-#define GEE_IDX(i, lim, id) gee_dclamp((long long)(i), (long long)(lim), (unsigned)(id))
-#else
-#define GEE_IDX(i, lim, id) (i)
-#endif
-
 #define GEE_REQUIRE(cond, code, ...)      \
     do {                                  \
         if (!(cond)) {                    \

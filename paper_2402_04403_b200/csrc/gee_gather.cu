@@ -115,8 +115,8 @@ k_gather_packed(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
 
 }  // namespace
 
-extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const void *table, int64_t n_hot, int32_t k,
-                                 uint8_t *cls, void *stream)
+extern "C" int gee_gather_labels_head(const int32_t *targets, int64_t arcs, const void *table, int64_t n_hot,
+                                      int32_t k, int64_t head_bytes, uint8_t *cls, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs k <= 255");
@@ -138,9 +138,8 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
     // evict_last in L2).  Larger heads shrink the L1 that holds the lines of
     // the ~16K lookups in flight per SM (byte head 160 KB: 10.5 ms, 180 KB:
     // 13.3 ms; profiles/r01_gather_tiers*.txt).  Without a hot tier (or
-    // GEE_GATHER_SMEM_HOT=0): plain contiguous lookups.
-    int64_t head = 98304;
-    if (const char *e = getenv("GEE_GATHER_SMEM_HOT")) head = atoll(e);
+    // head_bytes = 0): plain contiguous lookups.
+    int64_t head = head_bytes < 0 ? 98304 : head_bytes;
     if (head > optin - 64) head = optin - 64;
     const int per = k <= 15 ? 8 : k <= 31 ? 6 : k <= 63 ? 5 : 4;
     int64_t hl = (head / 4) * per;
@@ -157,4 +156,10 @@ extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const voi
     GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     kern<<<gee::sm_count(), GTHREADS, sh, gee::as_stream(stream)>>>(targets, arcs, tab, (uint32_t)hl, cls);
     return gee::check_launch("k_gather_packed");
+}
+
+extern "C" int gee_gather_labels(const int32_t *targets, int64_t arcs, const void *table, int64_t n_hot, int32_t k,
+                                 uint8_t *cls, void *stream)
+{
+    return gee_gather_labels_head(targets, arcs, table, n_hot, k, -1, cls, stream);
 }

@@ -9,8 +9,9 @@
 //     u16/int32 labels through L1/L2 (the table is small and stays in L2) and
 //     add the arc into a warp-private K-bin window in shared memory with
 //     fire-and-forget shared atomics (u32 counts; weighted arcs as the
-//     carry-free split fixed point of the block reducer: q = rint(w 2^e) =
-//     A 2^21 + B, two u32 planes, rows <= 2048 arcs so neither plane wraps);
+//     signed split fixed point of the block reducer: q = rint(w 2^e) =
+//     A 2^21 + B, two u32 planes, rows <= 2048 arcs so neither plane
+//     overflows, the A plane decoded with sign extension);
 //   * the warp then writes the WHOLE Z row with 16-byte streaming stores
 //     (zeros included: no separate zero fill), reading each 4-class group of
 //     the window once and clearing only the groups that were touched.
@@ -25,9 +26,16 @@ namespace {
 
 constexpr int WT = 256;        // threads per CTA (8 warps)
 constexpr int WW = WT / 32;
-constexpr int SPLIT = 21;      // == BLOCK_SPLIT of gee_reduce.cu (gee_block_scale_exp bounds q < 2^42)
+constexpr int SPLIT = 21;      // == BLOCK_SPLIT of gee_reduce.cu (gee_block_scale_exp bounds |q| < 2^41)
 constexpr int LIGHT_MAX = 2048;
 constexpr int UNR = 8;         // 32-arc rounds in flight per warp (256 arcs)
+
+// Signed split decode (see gee_reduce.cu): the high plane holds the two's
+// complement of a sum in [-2^31, 2^31).
+__device__ __forceinline__ long long plane_sum(uint32_t lo, uint32_t hi)
+{
+    return (long long)(int32_t)hi * (1ll << SPLIT) + (long long)lo;
+}
 
 template <typename LT>
 __device__ __forceinline__ uint32_t ld_lab(const LT *t, uint32_t slot)
@@ -46,13 +54,8 @@ __device__ __forceinline__ void wide_labels(const int32_t (&t)[UNR], const LT *_
 // Add a segment's arcs (labels + weights) into the window.
 template <bool WEIGHTED>
 __device__ __forceinline__ void wide_add(const uint32_t (&lab)[UNR], const float (&wt)[UNR], uint32_t *win,
-                                         int32_t kp, float qscale, int skip, uint32_t &sink)
+                                         int32_t kp, float qscale)
 {
-    if (skip & 4) {
-#pragma unroll
-        for (int u = 0; u < UNR; u++) sink += lab[u];
-        return;
-    }
 #pragma unroll
     for (int u = 0; u < UNR; u++) {
         if (lab[u] == 0u) continue;
@@ -89,7 +92,7 @@ template <typename LT, bool WEIGHTED, bool VEC>
 __global__ void __launch_bounds__(WT, WEIGHTED ? 3 : 5)
 k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__restrict__ targets,
             const float *__restrict__ w, const LT *__restrict__ table, float qscale, double dscale,
-            const double *__restrict__ inv, int32_t k, int32_t kp, float *__restrict__ z, int skip)
+            const double *__restrict__ inv, int32_t k, int32_t kp, float *__restrict__ z)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *sc = reinterpret_cast<float *>(smem_raw);  // sc[c] = inv[c+1] * dscale, c < kp
@@ -102,7 +105,6 @@ k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__res
     const int64_t GW = (int64_t)gridDim.x * WW;
     int64_t r = (int64_t)blockIdx.x * WW + wid;
     if (r >= n) return;
-    uint32_t sink = 0;
     auto seg_end = [](int64_t b0, int64_t b1) { return b1 - b0 <= LIGHT_MAX ? (b1 < b0 + 32 * UNR ? b1 : b0 + 32 * UNR) : b0; };
     // stage 0 (row r): labels in flight; stage 1 (row r+GW): targets in flight
     int64_t a0 = offsets[r], a1 = offsets[r + 1];
@@ -118,14 +120,14 @@ k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__res
     }
     while (true) {
         const bool light = a1 - a0 <= LIGHT_MAX;  // heavy rows: k_wide_heavy writes them
-        if (light && !(skip & 1)) {
-            wide_add<WEIGHTED>(lab, wt, win, kp, qscale, skip, sink);
+        if (light) {
+            wide_add<WEIGHTED>(lab, wt, win, kp, qscale);
             for (int64_t e0 = a0 + 32 * UNR; e0 < a1; e0 += 32 * UNR) {  // rows longer than one segment
                 int32_t tx[UNR];
                 uint32_t lx[UNR];
                 wide_load<WEIGHTED>(targets, w, e0, a1, lane, tx, wt);
                 wide_labels<LT>(tx, table, lx);
-                wide_add<WEIGHTED>(lx, wt, win, kp, qscale, skip, sink);
+                wide_add<WEIGHTED>(lx, wt, win, kp, qscale);
             }
         }
         const int64_t rn = r + GW;
@@ -141,7 +143,7 @@ k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__res
                 wide_load<WEIGHTED>(targets, w, c0, seg_end(c0, c1), lane, t, wt1);
             }
         }
-        if (light && !(skip & 2)) {
+        if (light) {
             __syncwarp();
             float *zr = z + r * (int64_t)k;
             if (VEC) {  // k % 4 == 0 and z 16-byte aligned: whole row in 16-byte streaming stores
@@ -158,10 +160,10 @@ k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__res
                     if ((lo.x | lo.y | lo.z | lo.w | hi.x | hi.y | hi.z | hi.w) != 0u) {
                         const float4 s4 = reinterpret_cast<const float4 *>(sc)[g];
                         if (WEIGHTED) {
-                            o.x = (float)(long long)(((unsigned long long)hi.x << SPLIT) + lo.x) * s4.x;
-                            o.y = (float)(long long)(((unsigned long long)hi.y << SPLIT) + lo.y) * s4.y;
-                            o.z = (float)(long long)(((unsigned long long)hi.z << SPLIT) + lo.z) * s4.z;
-                            o.w = (float)(long long)(((unsigned long long)hi.w << SPLIT) + lo.w) * s4.w;
+                            o.x = (float)plane_sum(lo.x, hi.x) * s4.x;
+                            o.y = (float)plane_sum(lo.y, hi.y) * s4.y;
+                            o.z = (float)plane_sum(lo.z, hi.z) * s4.z;
+                            o.w = (float)plane_sum(lo.w, hi.w) * s4.w;
                             w4[g + (kp >> 2)] = make_uint4(0u, 0u, 0u, 0u);
                         } else {
                             o.x = (float)lo.x * s4.x, o.y = (float)lo.y * s4.y;
@@ -178,7 +180,7 @@ k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__res
                     if (WEIGHTED) {
                         const uint32_t hi = win[c + kp];
                         if (lo | hi) {
-                            o = (float)(long long)(((unsigned long long)hi << SPLIT) + lo) * sc[c];
+                            o = (float)plane_sum(lo, hi) * sc[c];
                             win[c] = 0u, win[c + kp] = 0u;
                         }
                     } else if (lo) {
@@ -193,7 +195,6 @@ k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__res
         if (rn >= n) break;
         r = rn, a0 = b0, a1 = b1, b0 = c0, b1 = c1;
     }
-    if (sink == 0x9e3779b9u) z[0] = 0.f;  // keeps the skip-4 experiment's loads alive
 }
 
 // Heavy rows (> LIGHT_MAX arcs): one CTA per row, u64 window, any length.
@@ -256,9 +257,7 @@ int launch_wide(const int64_t *offsets, int64_t n, const int32_t *targets, const
         int64_t want = (n + WW - 1) / WW;
         int64_t grid = (int64_t)gee::sm_count() * per_sm;
         if (grid > want) grid = want;
-        int skip = 0;  // GEE_WIDE_SKIP (experiment): 1 = no gather/atomics, 2 = no write-out
-        if (const char *e = getenv("GEE_WIDE_SKIP")) skip = atoi(e);
-        kern<<<(int)grid, WT, smem, st>>>(offsets, n, targets, w, tab, qscale, dscale, inv, k, kp, z, skip);
+        kern<<<(int)grid, WT, smem, st>>>(offsets, n, targets, w, tab, qscale, dscale, inv, k, kp, z);
         if (int rc = gee::check_launch("k_wide_rows")) return rc;
     }
     if (n_heavy > 0) {

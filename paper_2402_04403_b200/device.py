@@ -6,8 +6,6 @@ to the CPU: without a CUDA device the calls raise.
 """
 
 import ctypes
-import math
-import os
 
 import numpy as np
 import torch
@@ -54,16 +52,10 @@ class DeviceGraph:
         self.s = int(s_listed)  # listed edges: the GEPS numerator
         self.device = device
         self.offsets = self.targets = self.weights = None
-        self.tile_row = None
-        self.chunk_row = None  # u16 per 16-arc chunk (gee_pull_plan)
-        self.cut_tiles = None  # tiles whose last row continues into later tiles
-        self.n_cut = 0
-        # row-per-warp reducer (split pull): rows heavier than HEAVY_ARCS are
-        # split into chunks
-        self.heavy_rows = self.chunk_first = self.chunk_heavy = None
-        self.n_heavy = self.n_chunks = 0
-        self.small_rows = self.medium_rows = None
-        self.n_small = self.n_medium = 0
+        # rows heavier than HEAVY_ARCS: the heavy-item reducer (k <= 255) or
+        # the wide kernel's CTA-per-row path (k > 255)
+        self.heavy_rows = None
+        self.n_heavy = 0
         self.max_block_arcs = 0
         self.scale_exp = 0
         self.rel_err = 0.0
@@ -147,11 +139,8 @@ class DeviceGraph:
 
     def _plan(self):
         """Pull planning (graph preparation): weight statistics + fixed-point
-        exponent, heavy-row chunk list, block arc spans.  The tile plan and
-        degree bins of the alternative reducers are built on first use."""
+        exponent, heavy-row work items, block arc spans."""
         arcs = self.arcs
-        self.tile_row = self.chunk_row = self.cut_tiles = None
-        self.small_rows = self.medium_rows = None
         self._plan_heavy()
         mx, mn, mxa = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         nf = ctypes.c_int32()
@@ -167,36 +156,8 @@ class DeviceGraph:
         ends = self.offsets[torch.arange(0, self.n + 32, 32, device=self.device).clamp_(max=self.n)]
         self.max_block_arcs = int((ends[1:] - ends[:-1]).max().item()) if self.n else 0
 
-    def ensure_tile_plan(self):
-        """Tile / chunk / cut plan of the tile reducers (gee_pull_plan)."""
-        if self.tile_row is not None:
-            return
-        arcs = self.arcs
-        n_tiles = int(lib.gee_pull_tiles(arcs))
-        self.tile_row = torch.empty(n_tiles + 1, dtype=torch.int64, device=self.device)
-        self.chunk_row = torch.empty(max(int(lib.gee_pull_chunks(arcs)), 1), dtype=torch.int16, device=self.device)
-        self.cut_tiles = torch.empty(max(n_tiles, 1), dtype=torch.int32, device=self.device)
-        nc = ctypes.c_int64()
-        check(lib.gee_pull_plan(ptr(self.offsets), self.n, arcs, ptr(self.tile_row), ptr(self.chunk_row),
-                                ptr(self.cut_tiles), ctypes.byref(nc), _stream()), "gee_pull_plan")
-        self.n_cut = int(nc.value)
-
-    def ensure_bins(self):
-        """Degree bins of the list reducer (gee_reduce_bins)."""
-        if self.small_rows is not None:
-            return
-        n = self.n
-        self.small_rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
-        self.medium_rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
-        ns, nm = ctypes.c_int64(), ctypes.c_int64()
-        check(lib.gee_reduce_bins(ptr(self.offsets), n, self.SMALL_ARCS, self.HEAVY_ARCS, ptr(self.small_rows),
-                                  ptr(self.medium_rows), ctypes.byref(ns), ctypes.byref(nm), _stream()),
-              "gee_reduce_bins")
-        self.n_small, self.n_medium = int(ns.value), int(nm.value)
-
     HEAVY_ARCS = 2048  # rows above go to the heavy path (<= the block reducer's limit)
     HEAVY_ITEM_ARCS = 65536  # arcs per heavy work item (one warp)
-    SMALL_ARCS = 32
 
     def _set_scale(self, max_row_abs, max_abs, min_abs):
         e, rel = ctypes.c_int32(), ctypes.c_double()
@@ -218,7 +179,7 @@ class DeviceGraph:
         self._set_scale(mx, mxa, mn)
 
     def _plan_heavy(self):
-        """Heavy-row chunk list for the row reducers (graph preparation)."""
+        """Heavy-row work items (graph preparation)."""
         n = self.n
         rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         nh = ctypes.c_int64()
@@ -229,8 +190,7 @@ class DeviceGraph:
         self.item_first = self.item_end = self.item_row = self.item_slot = self.mega_rows = None
         self.n_items = self.n_mega = 0
         if self.n_heavy == 0:
-            self.heavy_rows = self.chunk_first = self.chunk_heavy = None
-            self.n_chunks = 0
+            self.heavy_rows = None
             return
         # ascending row order: the chunk pass then streams the CSR and the
         # finalize sweeps Z in address order (k_mark_heavy appends in
@@ -239,10 +199,6 @@ class DeviceGraph:
         r64 = rows.to(torch.int64)
         first = self.offsets[r64].cpu()
         deg = (self.offsets[r64 + 1] - self.offsets[r64]).cpu()
-        per = (deg + self.HEAVY_ARCS - 1) // self.HEAVY_ARCS
-        heavy_idx = torch.repeat_interleave(torch.arange(self.n_heavy), per)
-        start = torch.repeat_interleave(first, per)
-        within = torch.arange(int(per.sum())) - torch.repeat_interleave(torch.cumsum(per, 0) - per, per)
         self.heavy_arc_total = int(deg.sum())
         # work items of gee_reduce_heavy: runs of <= HEAVY_ITEM_ARCS arcs;
         # rows with several items ("mega" rows) combine through acc + finalize
@@ -266,9 +222,6 @@ class DeviceGraph:
         self.mega_rows = rows_cpu[mega].to(torch.int32).to(self.device)
         self.n_mega = int(mega.sum())
         self.heavy_rows = rows
-        self.chunk_first = (start + within * self.HEAVY_ARCS).to(self.device)
-        self.chunk_heavy = heavy_idx.to(torch.int32).to(self.device)
-        self.n_chunks = int(per.sum())
 
     # Hot-label tier (csrc/gee_hot.cu): worth it when the packed label array
     # outgrows what L2 keeps resident under random access and degrees are
@@ -302,10 +255,15 @@ class DeviceGraph:
         n = self.n_nodes
         self.hot_rank = torch.empty(n, dtype=torch.int32, device=self.device)
         nh = ctypes.c_int64()
-        hot_max = int(os.environ.get("GEE_HOT_MAX", self.HOT_MAX))
-        min_deg = int(os.environ.get("GEE_HOT_MIN_DEG", self.HOT_MIN_DEGREE))
-        max_hot = min(n, hot_max // int(lib.gee_label_bytes(k)))
-        check(lib.gee_hot_plan(ptr(deg_off), n, max_hot, min_deg, ptr(self.hot_rank), None, ctypes.byref(nh),
+        # slots are int32: every slot n_hot + v, and the sentinel n_hot + n,
+        # must stay below 2^31
+        max_hot = min(n, self.HOT_MAX // int(lib.gee_label_bytes(k)), 2**31 - 1 - n - 1)
+        if max_hot <= 0:
+            self.hot_rank = None
+            self._sort_rows()
+            self._pad_rows()
+            return
+        check(lib.gee_hot_plan(ptr(deg_off), n, max_hot, self.HOT_MIN_DEGREE, ptr(self.hot_rank), None, ctypes.byref(nh),
                                _stream()), "gee_hot_plan")
         self.global_offsets = None
         self.n_hot = int(nh.value)
@@ -336,15 +294,14 @@ class DeviceGraph:
         self.hot_list = hr[hot[:n]].contiguous()
         del hv, bits, cnt, hot
 
-    SORT_ROWS = True
-    PAD_ROWS = 8  # pad every row to a multiple of 8 arcs (0: off)
+    PAD_ROWS = 8  # every row padded to a multiple of 8 arcs (the block reducer's lane unit)
 
     def _pad_rows(self):
         """Pad each row's arc run to a multiple of PAD_ROWS with (sentinel
         slot, weight 0) arcs (graph preparation): every lane of the block
         reducer then owns arcs of one row.  The sentinel slot's label is 0."""
-        align = int(os.environ.get("GEE_PAD_ROWS", self.PAD_ROWS))
-        if align <= 1 or self.arcs == 0 or self.padded:
+        align = self.PAD_ROWS
+        if self.arcs == 0 or self.padded:
             return
         poff = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
         pa = ctypes.c_int64()
@@ -377,7 +334,7 @@ class DeviceGraph:
     def _sort_rows(self):
         """Sort each row's arcs by label-table slot (graph preparation; the
         pull's integer sums do not depend on arc order)."""
-        if not (self.SORT_ROWS and os.environ.get("GEE_SORT_ROWS", "1") != "0") or self.arcs == 0:
+        if self.arcs == 0:
             return
         self._own_pull_arrays()
         check(lib.gee_sort_rows(ptr(self.offsets), self.n, ptr(self.targets), ptr(self.weights), _stream()),
@@ -429,13 +386,9 @@ class Embedder:
         self.bad = torch.zeros(1, dtype=torch.int64, device=dev)
         self.table = None
         self.table_n_hot = None  # n_hot the current table was built with
-        self.slots = None
         self.cls = None  # class stream of the split pull
-        self.heavy_acc = None  # heavy-row partial sums (list / row reducers)
-        self.mega_acc = None  # mega-row partial sums (block reducer's heavy items)
+        self.mega_acc = None  # mega-row partial sums (heavy items)
         self.counter = torch.zeros(1, dtype=torch.int64, device=dev)  # heavy-item work counter
-        self.split = os.environ.get("GEE_PULL_FUSED") is None
-        self.reducer = os.environ.get("GEE_PULL_REDUCER", "blocks")  # blocks | lists | rows | tiles
         self.phase_events = None  # list -> (phase, cuda event) after each phase (bench)
         self.launches = 0  # our kernels launched so far (bench accounting)
 
@@ -445,9 +398,11 @@ class Embedder:
             self.table = torch.empty(need, dtype=torch.uint8, device=self.device)
 
     # ------------------------------------------------------------------ K1
-    def project(self, labels_d, validate=True, g=None):
+    def project(self, labels_d, validate=True, g=None, inv=None):
         """Histogram + inv + label table (build_projection).  With a graph
-        whose pull layout has a hot tier, the table carries its hot prefix."""
+        whose pull layout has a hot tier, the table carries its hot prefix.
+        ``inv`` (float64[k+1], device or host) replaces the per-class values
+        1/count: a caller-supplied ProjectionMatrix (encoder.py:116,155)."""
         if labels_d.numel() != self.n:
             raise ValidationError(f"graph has {self.n} nodes but labels have {labels_d.numel()}")
         hot_rank = g.hot_rank if (g is not None and g.hot_rank is not None) else None
@@ -465,18 +420,26 @@ class Embedder:
                                            _stream()), "gee_build_projection")
         self._mark("project", 2)
         self.table_n_hot = n_hot
+        if inv is not None:
+            self.inv64.copy_(torch.as_tensor(inv, dtype=torch.float64))
+            self.inv32.copy_(self.inv64)
         if validate and int(self.bad.item()):
             raise ValidationError(f"{int(self.bad.item())} labels outside [0, {self.k}]")
         return self.counts
 
     # ------------------------------------------------------------------ K4
-    def _ensure_slots(self, arcs):
-        need = int(lib.gee_pull_slots_bytes(arcs, self.k))
-        if self.slots is None or self.slots.numel() * 8 < need:
-            self.slots = torch.zeros(math.ceil(need / 8), dtype=torch.int64, device=self.device)
-
     def new_z(self):
         return torch.empty((self.n, self.k), dtype=torch.float32, device=self.device)
+
+    def reducer_for(self, g, z=None):
+        """Which pull kernels run: "blocks" (class stream + 32-row block
+        reducer + heavy items, k <= 255) or "wide" (label gather fused with a
+        per-row window, any k).  Both are exact and give the same bits."""
+        if self.k > 255 or not g.padded or g.max_block_arcs >= 2**31:
+            return "wide"
+        if z is not None and z.data_ptr() % 16:
+            return "wide"
+        return "blocks"
 
     def pull(self, g: DeviceGraph, z=None):
         if not g.has_pull:
@@ -493,75 +456,31 @@ class Embedder:
             raise ValidationError("label table does not match the graph's hot tier: call project(labels, g=graph)")
         if z is None:
             z = torch.empty((g.n, self.k), dtype=torch.float32, device=self.device)
-        if self.k > 255 and os.environ.get("GEE_WIDE", "1") != "0" or self.reducer == "wide":
-            # wide K: label gather fused with a per-row class window
+        if self.reducer_for(g, z) == "wide":
             check(lib.gee_reduce_wide(ptr(g.offsets), g.n, ptr(g.targets), ptr(g.weights), ptr(self.table), self.k,
                                       g.scale_exp, ptr(self.inv64), ptr(g.heavy_rows), g.n_heavy, ptr(z), _stream()),
                   "gee_reduce_wide")
             self._mark("wide", 1 + (1 if g.n_heavy else 0))
             return z
-        if self.split and self.k <= 255:
-            # split pass: class stream (random gathers, full occupancy), then
-            # the gather-free segmented reduction
-            if self.cls is None or self.cls.numel() < g.arcs + 64:
-                self.cls = torch.empty(g.arcs + 64, dtype=torch.uint8, device=self.device)
-            check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
-                                        _stream()), "gee_gather_labels")
-            self._mark("gather", 1)
-            reducer = self.reducer
-            if reducer == "blocks" and (g.max_block_arcs >= 2**31 or z.data_ptr() % 16):
-                reducer = "lists"
-            if reducer in ("blocks", "lists", "rows"):
-                if g.n_heavy and (self.heavy_acc is None or self.heavy_acc.numel() < g.n_heavy * self.k):
-                    self.heavy_acc = torch.zeros(g.n_heavy * self.k, dtype=torch.int64, device=self.device)
-                heavy = (g.HEAVY_ARCS, ptr(g.heavy_rows), g.n_heavy, ptr(g.chunk_first), ptr(g.chunk_heavy),
-                         g.n_chunks, ptr(self.heavy_acc) if g.n_heavy else None, ptr(z), _stream())
-                if reducer == "blocks":
-                    if g.padded == 8:
-                        check(lib.gee_reduce_blocks_pad8(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights),
-                                                         g.scale_exp, ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(z),
-                                                         _stream()), "gee_reduce_blocks_pad8")
-                    else:
-                        check(lib.gee_reduce_blocks(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                                    ptr(self.inv64), self.k, g.HEAVY_ARCS, None, 0, None, None, 0,
-                                                    None, ptr(z), _stream()), "gee_reduce_blocks")
-                    self._mark("blocks", 1)
-                    if g.n_mega and (self.mega_acc is None or self.mega_acc.numel() < g.n_mega * self.k):
-                        self.mega_acc = torch.zeros(g.n_mega * self.k, dtype=torch.int64, device=self.device)
-                    check(lib.gee_reduce_heavy(ptr(self.cls), ptr(g.weights), g.arcs, g.scale_exp, ptr(self.inv64),
-                                               self.k,
-                                               ptr(g.item_first), ptr(g.item_end), ptr(g.item_row), ptr(g.item_slot),
-                                               g.n_items, ptr(g.mega_rows), g.n_mega,
-                                               ptr(self.mega_acc) if g.n_mega else None, ptr(self.counter), ptr(z),
-                                               _stream()),
-                          "gee_reduce_heavy")
-                    self._mark("heavy", (1 if g.n_items else 0) + (1 if g.n_mega else 0))
-                elif reducer == "lists":
-                    g.ensure_bins()
-                    check(lib.gee_reduce_lists(ptr(g.offsets), ptr(g.small_rows), g.n_small, ptr(g.medium_rows),
-                                               g.n_medium, ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                               ptr(self.inv64), self.k, *heavy), "gee_reduce_lists")
-                    self._mark("lists", 2 + (2 if g.n_heavy else 0))
-                else:
-                    check(lib.gee_reduce_rows(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                              ptr(self.inv64), self.k, *heavy), "gee_reduce_rows")
-                    self._mark("rows", 1 + (2 if g.n_heavy else 0))
-                return z
-            g.ensure_tile_plan()
-            self._ensure_slots(g.arcs)
-            check(lib.gee_embed_csr_pull_cls(ptr(g.offsets), ptr(self.cls), ptr(g.weights), g.n, g.arcs,
-                                             ptr(g.tile_row), ptr(g.chunk_row), ptr(g.cut_tiles), g.n_cut,
-                                             g.scale_exp, ptr(self.inv64), self.k, ptr(z), ptr(self.slots),
-                                             _stream()), "gee_embed_csr_pull_cls")
-            self._mark("tiles", 3)
-            return z
-        g.ensure_tile_plan()
-        self._ensure_slots(g.arcs)
-        check(lib.gee_embed_csr_pull(ptr(g.offsets), ptr(g.targets), ptr(g.weights), g.n, g.arcs,
-                                     ptr(g.tile_row), ptr(g.chunk_row), ptr(g.cut_tiles), g.n_cut, g.scale_exp,
-                                     ptr(self.table), g.n_hot, ptr(self.inv64), self.k, ptr(z), ptr(self.slots),
-                                     _stream()), "gee_embed_csr_pull")
-        self._mark("fused", 3)
+        # split pass: class stream (random gathers, full occupancy), then the
+        # gather-free segmented reduction (light rows by 32-row blocks, heavy
+        # rows as work items)
+        if self.cls is None or self.cls.numel() < g.arcs + 64:
+            self.cls = torch.empty(g.arcs + 64, dtype=torch.uint8, device=self.device)
+        check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
+                                    _stream()), "gee_gather_labels")
+        self._mark("gather", 1)
+        check(lib.gee_reduce_blocks_pad8(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                         ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(z), _stream()),
+              "gee_reduce_blocks_pad8")
+        self._mark("blocks", 1)
+        if g.n_mega and (self.mega_acc is None or self.mega_acc.numel() < g.n_mega * self.k):
+            self.mega_acc = torch.zeros(g.n_mega * self.k, dtype=torch.int64, device=self.device)
+        check(lib.gee_reduce_heavy(ptr(self.cls), ptr(g.weights), g.arcs, g.scale_exp, ptr(self.inv64), self.k,
+                                   ptr(g.item_first), ptr(g.item_end), ptr(g.item_row), ptr(g.item_slot), g.n_items,
+                                   ptr(g.mega_rows), g.n_mega, ptr(self.mega_acc) if g.n_mega else None,
+                                   ptr(self.counter), ptr(z), _stream()), "gee_reduce_heavy")
+        self._mark("heavy", (1 if g.n_items else 0) + (1 if g.n_mega else 0))
         return z
 
     def _mark(self, phase, launches):
@@ -590,12 +509,12 @@ class Embedder:
               "gee_embed_coo")
         return z
 
-    def embed(self, g: DeviceGraph, labels_d, variant="auto", z=None, validate=True):
+    def embed(self, g: DeviceGraph, labels_d, variant="auto", z=None, validate=True, inv=None):
         """One edge pass: projection then the chosen edge map."""
         v = choose_variant(g, variant)
         if v == "pull":
             g.prepare_hot(self.k)
-        self.project(labels_d, validate=validate, g=g if v == "pull" else None)
+        self.project(labels_d, validate=validate, g=g if v == "pull" else None, inv=inv)
         return self.pull(g, z) if v == "pull" else self.push(g, z)
 
 

@@ -144,6 +144,72 @@ def _validate_projection(projection, n, k):
         raise ValidationError(f"projection is ({projection.n}, {projection.k}) but the pass is ({n}, {k})")
 
 
+def _projection_inv(projection, labels, k):
+    """Per-class values of a caller-supplied ProjectionMatrix.
+
+    The reference reads W as (labels, row_value) per node: embed_serial pairs
+    y.labels with projection.row_value (encoder.py:116-119), embed_parallel
+    reads projection.label and projection.row_value (encoder.py:155,
+    :180-181).  The edge pass here sums weights per (row, class) and scales
+    each class once, so row_value must be one value per class among the
+    labeled nodes (true of every build_projection output, whatever the
+    counts); that value replaces 1/count.  Per-node values that differ
+    within a class raise ValidationError instead of being ignored."""
+    import torch
+
+    lab = torch.as_tensor(labels).to(torch.int64).reshape(-1)
+    rv = torch.as_tensor(projection.row_value, dtype=torch.float64, device=lab.device).reshape(-1)
+    if rv.numel() != lab.numel():
+        raise ValidationError(f"projection.row_value has {rv.numel()} entries for {lab.numel()} nodes")
+    keep = (lab > 0) & (lab <= k)
+    lab, rv = lab[keep], rv[keep]
+    if not bool(torch.isfinite(rv).all()):
+        raise ValidationError("projection.row_value must be finite")
+    hi = torch.zeros(k + 1, dtype=torch.float64, device=lab.device).scatter_reduce_(0, lab, rv, "amax",
+                                                                                     include_self=False)
+    lo = torch.zeros(k + 1, dtype=torch.float64, device=lab.device).scatter_reduce_(0, lab, rv, "amin",
+                                                                                     include_self=False)
+    if not bool(torch.equal(hi, lo)):
+        raise ValidationError("projection.row_value must be constant within each class: the GPU edge pass "
+                              "scales per (row, class) sum, not per node")
+    hi[0] = 0.0
+    return hi
+
+
+# ---------------------------------------------------------------- variants
+# Which edge map a call runs ("auto").  embed_serial is the reference's
+# bit-reproducible oracle (encoder.py:106-113), so it always takes the exact
+# integer pull.  embed_parallel's reference pass is itself order-dependent
+# (CAS f64 atomics, encoder.py:139-142), so it takes whichever variant the
+# measured table says is faster for a whole call of that size: the push
+# needs no graph preparation (CSR mirror, hot tier, row sort, padding) and
+# wins on small graphs (profiles/r02_variant_table.json, one B200, host
+# arrays in and out: push 2.9 vs pull 5.0 ms at 2M arcs, 23.6 vs 26.4 ms at
+# 6M, even at 20M-60M arcs, where the resident pass then favours the pull).
+PUSH_MAX_ARCS = 1 << 23
+
+_last = {}
+
+
+def last_pass():
+    """Variant and kernels of the most recent embed_* call on this thread:
+    {"variant": "pull"|"push", "reducer": "blocks"|"wide"|None,
+    "reason": why}."""
+    return dict(_last)
+
+
+def _record(variant, reducer, reason):
+    _last.clear()
+    _last.update(variant=variant, reducer=reducer, reason=reason)
+    logger.debug("edge pass: variant=%s reducer=%s (%s)", variant, reducer, reason)
+
+
+def _gate_push_warning(rel_err):
+    logger.warning(
+        "weights span too wide a range for the exact fixed-point pull (worst per-term rounding %.2e > %.0e): "
+        "running the push variant (fp32 atomics; Z is not bit-stable run to run)", rel_err, 1e-5)
+
+
 def embed_serial(el: EdgeList, y: LabelVector, projection=None, *, variant="auto", out=None):
     """One pass over the listed edges (embed_serial, encoder.py:106-120).
 
@@ -152,7 +218,7 @@ def embed_serial(el: EdgeList, y: LabelVector, projection=None, *, variant="auto
     """
     import torch
 
-    from .device import DeviceGraph, Embedder, choose_variant, require_cuda, to_device
+    from .device import PULL_REL_ERR_MAX, DeviceGraph, Embedder, require_cuda, to_device
 
     if el.n != y.n:
         raise ValidationError(f"graph has {el.n} nodes but labels have {y.n}")
@@ -162,14 +228,21 @@ def embed_serial(el: EdgeList, y: LabelVector, projection=None, *, variant="auto
     host = not (_is_torch(el.src) and el.src.is_cuda)
     if el.n == 0:
         return _finish(torch.zeros((0, y.k), dtype=torch.float32, device=dev), out, host)
+    lab_d = to_device(y.labels, torch.int32, dev)
+    inv = None if projection is None else _projection_inv(projection, lab_d, y.k)
     want = variant if variant != "auto" else "pull"
+    reason = "requested" if variant != "auto" else "embed_serial is bit-reproducible: exact pull"
     g = DeviceGraph.from_edges(el.src, el.dst, el.w, el.n, device=dev, pull=(want == "pull"),
                                keep_coo=(want == "push"))
-    if variant == "auto" and choose_variant(g) != "pull":
+    if variant == "auto" and g.weighted and g.rel_err > PULL_REL_ERR_MAX:
+        _gate_push_warning(g.rel_err)
+        reason = f"fixed-point gate (rounding {g.rel_err:.2e})"
         g = DeviceGraph.from_edges(el.src, el.dst, el.w, el.n, device=dev, pull=False, keep_coo=True)
+        want = "push"
     emb = Embedder(el.n, y.k, dev)
     z_d = out if (_is_torch(out)) else None
-    z_d = emb.embed(g, to_device(y.labels, torch.int32, dev), variant=variant, z=z_d)
+    z_d = emb.embed(g, lab_d, variant=want, z=z_d, inv=inv)
+    _record(want, emb.reducer_for(g, z_d) if want == "pull" else None, reason)
     torch.cuda.current_stream().synchronize()
     return _finish(z_d, out, host)
 
@@ -213,16 +286,30 @@ def embed_parallel(
     if g.n == 0 or y.k == 0:
         return _finish(torch.zeros((g.n, y.k), dtype=torch.float32, device=dev), out, host)
     symmetric = accounting is EdgeAccounting.SOURCE_ONLY
-    want_push = variant == "push"
+    labels = projection.label if projection is not None else y.labels
+    lab_d = to_device(labels, torch.int32, dev)
+    inv = None if projection is None else _projection_inv(projection, lab_d, y.k)
+    arcs = int(g.targets.shape[0])
+    if variant != "auto":
+        want, reason = variant, "requested"
+    elif not atomics:
+        want, reason = "pull", "atomics=False: the atomic-free pull"
+    elif arcs <= PUSH_MAX_ARCS:
+        want, reason = "push", f"measured table: push for <= {PUSH_MAX_ARCS} arcs"
+    else:
+        want, reason = "pull", f"measured table: pull for > {PUSH_MAX_ARCS} arcs"
     dg = DeviceGraph.from_csr(g.offsets, g.targets, g.weights, g.n, symmetric, device=dev,
-                              pull=not want_push, keep_coo=want_push)
-    if variant == "auto" and dg.weighted and dg.rel_err > PULL_REL_ERR_MAX:
+                              pull=want == "pull", keep_coo=want == "push")
+    if variant == "auto" and want == "pull" and dg.weighted and dg.rel_err > PULL_REL_ERR_MAX:
+        _gate_push_warning(dg.rel_err)
+        reason = f"fixed-point gate (rounding {dg.rel_err:.2e})"
         dg = DeviceGraph.from_csr(g.offsets, g.targets, g.weights, g.n, symmetric, device=dev,
                                   pull=False, keep_coo=True)
-        variant = "push"
+        want = "push"
     emb = Embedder(g.n, y.k, dev)
     z_d = out if _is_torch(out) else None
-    z_d = emb.embed(dg, to_device(y.labels, torch.int32, dev), variant=variant, z=z_d)
+    z_d = emb.embed(dg, lab_d, variant=want, z=z_d, inv=inv)
+    _record(want, emb.reducer_for(dg, z_d) if want == "pull" else None, reason)
     torch.cuda.current_stream().synchronize()
     return _finish(z_d, out, host)
 

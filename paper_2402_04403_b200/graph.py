@@ -43,14 +43,43 @@ def _as_index(a, name):
     return np.ascontiguousarray(a, dtype=np.int32).reshape(-1)
 
 
-def _as_weights(w, name):
+_F32_MAX = float(np.finfo(np.float32).max)
+_F32_TINY = float(np.finfo(np.float32).tiny)  # smallest normal float32
+
+
+def _check_f32_range(finite, absmax, absmin_nz, name, what):
+    """Checks on the caller's dtype BEFORE narrowing to float32: a finite
+    f64 weight above FLT_MAX would become inf, and one below the normal
+    range would lose its precision (or vanish) -- both would break parity
+    with the reference's f64 pass without a diagnostic."""
+    if not finite:
+        raise ValidationError(f"{what} weights must be finite")
+    if absmax > _F32_MAX:
+        raise ValidationError(f"{name}: |weight| {absmax:.6g} exceeds the float32 range of the edge pass")
+    if 0.0 < absmin_nz < _F32_TINY:
+        raise ValidationError(f"{name}: nonzero |weight| {absmin_nz:.6g} is below the normal float32 range "
+                              f"({_F32_TINY:.6g}) of the edge pass")
+
+
+def _as_weights(w, name, what="edge"):
     if w is None:
         return None
     if _is_torch(w):
         import torch
 
-        return w.to(torch.float32).contiguous().reshape(-1)
-    return np.ascontiguousarray(w, dtype=np.float32).reshape(-1)
+        w = w.contiguous().reshape(-1)
+        if w.dtype != torch.float32 and w.numel():
+            a = w.to(torch.float64).abs()
+            nz = a[a > 0]
+            _check_f32_range(bool(torch.isfinite(a).all()), float(a.max()),
+                             float(nz.min()) if nz.numel() else 0.0, name, what)
+        return w.to(torch.float32)
+    w = np.asarray(w).reshape(-1)
+    if w.dtype != np.float32 and w.size:
+        a = np.abs(w.astype(np.float64))
+        nz = a[a > 0]
+        _check_f32_range(bool(np.isfinite(a).all()), float(a.max()), float(nz.min()) if nz.size else 0.0, name, what)
+    return np.ascontiguousarray(w, dtype=np.float32)
 
 
 def _minmax(a):
@@ -158,7 +187,7 @@ class CsrGraph:
         else:
             self.offsets = np.ascontiguousarray(self.offsets, dtype=np.int64).reshape(-1)
         self.targets = _as_index(self.targets, "targets")
-        self.weights = _as_weights(self.weights, "weights")
+        self.weights = _as_weights(self.weights, "weights", "arc")
         if self.n > MAX_NODES:
             raise ValidationError(f"node count {self.n} exceeds CSR limit {MAX_NODES}")
         if _length(self.offsets) != self.n + 1:

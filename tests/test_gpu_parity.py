@@ -296,11 +296,15 @@ def test_hot_plan_ranks_by_degree():
     assert all(rank[v] == -1 for v in range(6) if deg[v] < 2)
 
 
+def _force_wide(monkeypatch):
+    monkeypatch.setattr(Embedder, "reducer_for", lambda self, g, z=None: "wide")
+
+
 @pytest.mark.parametrize("k,weighted", [(50, True), (7, False), (2, True), (255, False)])
-def test_pull_reducers_agree_bitwise(k, weighted):
-    # every exact pull reducer (32-row blocks, degree lists, row-per-warp,
-    # tiles) sums the same integers: their Z must match bit for bit.  The
-    # graph mixes empty rows, dense blocks (> 16 nonempty rows: several
+def test_pull_reducers_agree_bitwise(k, weighted, monkeypatch):
+    # both exact pull paths (class stream + 32-row block reducer + heavy
+    # items; the fused wide kernel) sum the same integers: their Z must match
+    # bit for bit.  The graph mixes empty rows, dense blocks (several window
     # passes), a heavy row inside a block and ragged tails.
     rng = np.random.default_rng(k)
     n = 40_003
@@ -314,22 +318,21 @@ def test_pull_reducers_agree_bitwise(k, weighted):
                                None if w is None else torch.from_numpy(w), n, device=dev, pull=True)
     assert g.n_heavy >= 1
     exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
-    out = {}
-    for red in ("blocks", "lists", "rows", "tiles", "wide"):
-        emb = Embedder(n, k, dev)
-        emb.reducer = red
-        out[red] = emb.embed(g, torch.from_numpy(y.labels).to(dev), variant="pull").cpu().numpy()
-        assert rel_err(out[red], exp) <= TOL, red
-    for red in ("lists", "rows", "wide"):
-        assert np.array_equal(out["blocks"].view(np.uint32), out[red].view(np.uint32)), red
+    lab = torch.from_numpy(y.labels).to(dev)
+    emb = Embedder(n, k, dev)
+    z = emb.embed(g, lab, variant="pull").cpu().numpy()
+    assert emb.reducer_for(g) == "blocks"
+    assert rel_err(z, exp) <= TOL
+    _force_wide(monkeypatch)
+    zw = Embedder(n, k, dev).embed(g, lab, variant="pull").cpu().numpy()
+    assert np.array_equal(z.view(np.uint32), zw.view(np.uint32))
 
 
 @pytest.mark.parametrize("k,weighted", [(1000, False), (1000, True), (301, False), (1001, True), (4096, False)])
-def test_wide_k_pull(k, weighted, monkeypatch):
+def test_wide_k_pull(k, weighted):
     # K > 255 (BASELINE C5 is K = 1000): the fused wide reducer (warp per
     # light row, CTA per heavy row; vector and scalar write-outs for
-    # k % 4 == 0 / != 0) against the oracle, bit-stable, and bit-identical to
-    # the tiled pull it replaced
+    # k % 4 == 0 / != 0) against the oracle, and bit-stable
     rng = np.random.default_rng(k + weighted)
     n = 30_011
     hub = np.full(9_000, 11, np.int64)
@@ -344,12 +347,119 @@ def test_wide_k_pull(k, weighted, monkeypatch):
     exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
     lab = torch.from_numpy(y.labels).to(dev)
     emb = Embedder(n, k, dev)
+    assert emb.reducer_for(g) == "wide"
     z = emb.embed(g, lab, variant="pull").cpu().numpy()
     assert rel_err(z, exp) <= TOL
-    assert np.array_equal(z, emb.embed(g, lab, variant="pull").cpu().numpy())
-    monkeypatch.setenv("GEE_WIDE", "0")
-    old = Embedder(n, k, dev).embed(g, lab, variant="pull").cpu().numpy()
-    assert np.array_equal(z.view(np.uint32), old.view(np.uint32))
+    assert np.array_equal(z.view(np.uint32), emb.embed(g, lab, variant="pull").cpu().numpy().view(np.uint32))
+
+
+# ---------------------------------------------------------------- signed weights
+# The reference accepts any finite weight (graph.py:46-47) and
+# states scale equivariance for any constant (SPEC.md:270,
+# tests/test_encoder.py:112-119).  With mixed signs a class sum can cancel, so
+# the relative bar is taken against the entry's absolute mass
+# sum |w| * inv (the oracle run on |w|): |z - ref| <= 1e-4 * mass, and entries
+# whose mass is zero are exactly zero.
+
+def signed_err(z, ref, mass):
+    z = np.asarray(z, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    mass = np.asarray(mass, dtype=np.float64)
+    empty = mass == 0
+    assert np.all(z[empty] == 0)
+    nz = ~empty
+    if not nz.any():
+        return 0.0
+    return float(np.max(np.abs(z[nz] - ref[nz]) / mass[nz]))
+
+
+def _signed_case(seed, n, s, k, kind, hub=0):
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, s)
+    dst = rng.integers(0, n, s)
+    if hub:  # rows > 2048 arcs: heavy items (k <= 255) / CTA rows (wide)
+        src[:hub] = 3
+    if kind == "normal":  # |w| >= 1e-3 keeps the fixed-point gate open (rounding <= 1e-5 of min |w|)
+        w = rng.standard_normal(s)
+        w = np.where(np.abs(w) < 1e-3, np.copysign(1e-3, w), w).astype(np.float32)
+    elif kind == "negative":
+        w = -(1.0 - rng.random(s)).astype(np.float32)
+    else:  # "cancel": +-1 pairs and small residues, many class sums exactly 0
+        w = rng.choice(np.array([1.0, -1.0, 0.5, -0.5], np.float32), s)
+    y = gb.random_labels(n, k, 0.9, seed=seed + 1)
+    return src, dst, w, y
+
+
+@pytest.mark.parametrize("variant", ["pull", "push"])
+@pytest.mark.parametrize("kind", ["normal", "negative", "cancel"])
+@pytest.mark.parametrize("k", [7, 50, 255, 300])
+def test_signed_weights(kind, k, variant):
+    n, s = 20_011, 250_000
+    src, dst, w, y = _signed_case(k * 7 + len(kind), n, s, k, kind, hub=12_000)
+    el = gb.EdgeList(n=n, src=src, dst=dst, w=w, directed=True)
+    exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
+    mass = oracle.serial_embed(src, dst, np.abs(w), y.labels, n, k)
+    z = gb.embed_serial(el, y, variant=variant)
+    assert signed_err(z, exp, mass) <= TOL, (kind, k, variant)
+    if kind == "negative":  # no cancellation: the plain relative bar, and every nonzero entry < 0
+        assert rel_err(z, exp) <= TOL
+        assert np.all(z[exp != 0] < 0)
+    if variant == "pull":
+        assert np.array_equal(z.view(np.uint32), gb.embed_serial(el, y, variant="pull").view(np.uint32))
+
+
+def test_single_negative_arc_exact():
+    # the round-1 defect: a class sum of -1 decoded as +4095 * inv
+    el = gb.EdgeList(n=3, src=[0, 1], dst=[1, 2], w=[-1.0, 0.5], directed=True)
+    y = gb.LabelVector(labels=[1, 1, 2], k=2)
+    exp = oracle.serial_embed(el.src, el.dst, el.w, y.labels, 3, 2)
+    for variant in ("pull", "push"):
+        z = gb.embed_serial(el, y, variant=variant)
+        assert np.array_equal(z.astype(np.float64), exp), variant
+    assert exp[0, 0] < 0
+
+
+@pytest.mark.parametrize("c", [-3.5, 3.5, -1.0])
+def test_scale_equivariance_signed(c):
+    # SPEC.md:270 / test_encoder.py:112-119 (c = 3.5 there), here also for
+    # negative c: embed(c * w) == c * embed(w) against the oracle
+    n, s, k = 5_003, 80_000, 10
+    src, dst, w, y = _signed_case(11, n, s, k, "normal", hub=3_000)
+    el = gb.EdgeList(n=n, src=src, dst=dst, w=w, directed=False)
+    elc = gb.EdgeList(n=n, src=src, dst=dst, w=(np.float32(c) * w).astype(np.float32), directed=False)
+    mass = oracle.serial_embed(src, dst, np.abs(w), y.labels, n, k) * abs(c)
+    exp_c = oracle.serial_embed(src, dst, elc.w, y.labels, n, k)
+    for variant in ("pull", "push"):
+        z = gb.embed_serial(el, y, variant=variant)
+        zc = gb.embed_serial(elc, y, variant=variant)
+        assert signed_err(zc, exp_c, mass) <= TOL, variant
+        assert signed_err(zc, c * z.astype(np.float64), mass) <= 2 * TOL, variant
+    if c in (-1.0,):  # negation is exact in the fixed point: bitwise -z
+        z = gb.embed_serial(el, y, variant="pull")
+        zc = gb.embed_serial(elc, y, variant="pull")
+        assert np.array_equal(zc, -z)
+
+
+@pytest.mark.parametrize("k", [50, 300])
+def test_signed_reducers_agree_bitwise(k, monkeypatch):
+    # mixed-sign weights through the block reducer, the heavy items (one
+    # item and mega rows of several items) and the wide kernel: same bits
+    n, s = 70_001, 400_000
+    src, dst, w, y = _signed_case(k, n, s, k, "normal", hub=150_000)
+    dev = torch.device("cuda")
+    g = DeviceGraph.from_edges(torch.from_numpy(src).int(), torch.from_numpy(dst).int(), torch.from_numpy(w), n,
+                               device=dev, pull=True)
+    g.prepare_hot(k, enable=True)
+    assert g.n_heavy >= 1 and g.n_mega >= 1
+    lab = torch.from_numpy(y.labels).to(dev)
+    emb = Embedder(n, k, dev)
+    z = emb.embed(g, lab, variant="pull").cpu().numpy()
+    exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
+    mass = oracle.serial_embed(src, dst, np.abs(w), y.labels, n, k)
+    assert signed_err(z, exp, mass) <= TOL
+    _force_wide(monkeypatch)
+    zw = Embedder(n, k, dev).embed(g, lab, variant="pull").cpu().numpy()
+    assert np.array_equal(z.view(np.uint32), zw.view(np.uint32))
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -674,17 +784,15 @@ def test_pack_targets_rejects_unpadded():
     assert rc != 0 and b"padded layout" in _lib.lib.gee_last_error()
 
 
-@pytest.mark.parametrize("head", [None, "40000", "0"])
+@pytest.mark.parametrize("head", [-1, 40000, 0])
 @pytest.mark.parametrize("k", [5, 20, 50, 63, 64, 200])
-def test_gather_labels_heads(k, head, monkeypatch):
+def test_gather_labels_heads(k, head):
     # gee_gather_labels equals a plain gather for every kernel variant: the
     # shared-memory head packed 8 / 6 / 5 / 4 labels per word by k (full and
     # partial heads) and plain contiguous lookups; skewed slots hit the head,
     # the hot tier and the cold tier; ragged lengths exercise the tails
     from paper_2402_04403_b200 import _lib
 
-    if head:
-        monkeypatch.setenv("GEE_GATHER_SMEM_HOT", head)
     gen = torch.Generator(device="cuda").manual_seed(k)
     n_hot, n = 300_000, 2_000_000
     table = torch.randint(0, k + 1, (n_hot + n + 1,), dtype=torch.uint8, device="cuda", generator=gen)
@@ -694,8 +802,8 @@ def test_gather_labels_heads(k, head, monkeypatch):
             u < 0.75, (u * n_hot).long() % n_hot, torch.randint(0, n_hot + n + 1, (arcs,), device="cuda",
                                                                  generator=gen))).int()
         cls = torch.full((arcs + 16,), 255, dtype=torch.uint8, device="cuda")
-        _lib.check(_lib.lib.gee_gather_labels(_lib.ptr(t), arcs, _lib.ptr(table), n_hot, k, _lib.ptr(cls),
-                                              _lib.stream_handle()), "gee_gather_labels")
+        _lib.check(_lib.lib.gee_gather_labels_head(_lib.ptr(t), arcs, _lib.ptr(table), n_hot, k, head,
+                                                   _lib.ptr(cls), _lib.stream_handle()), "gee_gather_labels_head")
         torch.cuda.synchronize()
         assert torch.equal(cls[:arcs], table[t.long()]), arcs
         assert bool((cls[arcs:] == 255).all()), arcs
@@ -797,3 +905,74 @@ def test_host_pipeline_unit_weights(k, labeled):
     assert torch.equal(h_z, z_ref)
     exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), None, y.cpu().numpy(), n, k)
     assert rel_err(h_z.numpy(), exp) <= TOL
+
+
+# ---------------------------------------------------------------- projection= / variant policy
+def test_projection_is_honoured(golden):
+    # a caller-supplied ProjectionMatrix is used, not recomputed
+    # (encoder.py:116 embed_serial: y.labels with projection.row_value;
+    # encoder.py:155,180-181 embed_parallel: projection.label / row_value)
+    c = case(golden, "rand4")
+    el, y = _el(c), _y(c)
+    k = y.k
+    proj = gb.build_projection(y)
+    scale = np.arange(1, k + 2, dtype=np.float64)  # class c scaled by c + 1
+    custom = gb.ProjectionMatrix(n=proj.n, k=k, row_value=proj.row_value * scale[proj.label], label=proj.label)
+    exp = c["z_serial"] * scale[1:]
+    for variant in ("pull", "push"):
+        assert rel_err(gb.embed_serial(el, y, projection=custom, variant=variant), exp) <= TOL, variant
+        g = gb.build_csr(el)
+        assert rel_err(gb.embed_parallel(g, y, projection=custom, variant=variant), exp) <= TOL, variant
+    # embed_parallel reads the projection's labels, not y's
+    shifted = np.where(proj.label > 0, proj.label % k + 1, 0).astype(np.int32)
+    alt = gb.ProjectionMatrix(n=proj.n, k=k, row_value=proj.row_value, label=shifted)
+    z_alt = gb.embed_parallel(gb.build_csr(el), y, projection=alt, variant="pull")
+    exp_alt = oracle.serial_embed(el.src, el.dst, el.w, shifted, el.n, k)
+    # same labels as `shifted`, but each class keeps the value of the class it came from
+    _, inv_old, _ = oracle.projection(y.labels, k)
+    _, inv_new, _ = oracle.projection(shifted, k)
+    old_of_new = np.zeros(k + 1)
+    old_of_new[shifted[y.labels > 0]] = inv_old[y.labels[y.labels > 0]]
+    ratio = np.divide(old_of_new, inv_new, out=np.zeros(k + 1), where=inv_new > 0)
+    assert rel_err(z_alt, exp_alt * ratio[1:]) <= TOL
+
+
+def test_projection_per_node_values_rejected(golden):
+    c = case(golden, "rand4")
+    y = _y(c)
+    proj = gb.build_projection(y)
+    rv = proj.row_value.copy()
+    i = int(np.nonzero(proj.label)[0][0])
+    rv[i] *= 1.5
+    bad = gb.ProjectionMatrix(n=proj.n, k=proj.k, row_value=rv, label=proj.label)
+    with pytest.raises(gb.ValidationError, match="constant within each class"):
+        gb.embed_serial(_el(c), y, projection=bad)
+    with pytest.raises(gb.ValidationError):
+        gb.embed_serial(_el(c), y, projection=gb.ProjectionMatrix(n=proj.n + 1, k=proj.k, row_value=rv,
+                                                                    label=proj.label))
+
+
+def test_variant_policy_and_gate_warning(golden, caplog):
+    from paper_2402_04403_b200 import encoder
+
+    c = case(golden, "rand4")
+    el, y = _el(c), _y(c)
+    gb.embed_serial(el, y)
+    assert encoder.last_pass()["variant"] == "pull"
+    g = gb.build_csr(el)
+    gb.embed_parallel(g, y)
+    assert encoder.last_pass()["variant"] == "push"  # small graph: measured table
+    gb.embed_parallel(g, y, atomics=False)
+    assert encoder.last_pass()["variant"] == "pull"
+    # weights spanning 1e-9 .. 1: the fixed point refuses, auto falls back loudly
+    w = np.ones(el.s, np.float32)
+    w[0] = 1e-9
+    wide = gb.EdgeList(n=el.n, src=el.src, dst=el.dst, w=w, directed=el.directed)
+    with caplog.at_level("WARNING"):
+        z = gb.embed_serial(wide, y)
+    assert encoder.last_pass()["variant"] == "push" and "gate" in encoder.last_pass()["reason"]
+    assert any("push variant" in r.getMessage() for r in caplog.records)
+    exp = oracle.serial_embed(el.src, el.dst, w, y.labels, el.n, y.k)
+    assert rel_err(z, exp) <= TOL
+    with pytest.raises(gb.ValidationError, match="push"):
+        gb.embed_serial(wide, y, variant="pull")

@@ -38,14 +38,15 @@ def test_pure_functions_without_gpu():
     assert L.gee_version() >= 100
     assert [L.gee_label_bytes(k) for k in (1, 255, 256, 65535, 65536)] == [1, 1, 2, 2, 4]
     assert L.gee_label_table_bytes(100, 0, 50) == 112 and L.gee_label_table_bytes(100, 20, 300) == 256
-    T = _lib.TILE_ARCS
-    assert L.gee_pull_tiles(0) == 0 and L.gee_pull_tiles(1) == 1 and L.gee_pull_tiles(T + 1) == 2
-    assert L.gee_pull_slots_bytes(2 * T, 10) == 2 * 10 * 8
+    # fixed-point exponent: |q| = max|w| 2^e < 2^41 (signed split planes) and
+    # max row sum 2^e < 2^62
     e, rel = ctypes.c_int32(), ctypes.c_double()
-    assert L.gee_pull_scale_exp(1.0, 2.0 ** -24, ctypes.byref(e), ctypes.byref(rel)) == 0
-    assert e.value == 61 and rel.value == pytest.approx(2.0 ** -62 / 2.0 ** -24)
-    assert L.gee_pull_scale_exp(2.0 ** 20, 0.5, ctypes.byref(e), ctypes.byref(rel)) == 0
-    assert 2.0 ** 20 * 2.0 ** e.value < 2.0 ** 62
+    assert L.gee_block_scale_exp(1.0, 1.0, 2.0 ** -24, ctypes.byref(e), ctypes.byref(rel)) == 0
+    assert e.value == 40 and rel.value == pytest.approx(2.0 ** -41 / 2.0 ** -24)
+    assert L.gee_block_scale_exp(3.0, 0.999, 0.5, ctypes.byref(e), ctypes.byref(rel)) == 0
+    assert 0.999 * 2.0 ** e.value < 2.0 ** 41 and 0.999 * 2.0 ** (e.value + 1) >= 2.0 ** 41
+    assert L.gee_block_scale_exp(2.0 ** 30, 1.0, 0.5, ctypes.byref(e), ctypes.byref(rel)) == 0
+    assert 2.0 ** 30 * 2.0 ** e.value < 2.0 ** 62 and e.value == 31
     # argument validation happens before any CUDA call
     assert L.gee_build_projection(None, 10, 0, None, None, None, None, None, 0, None, None) == _lib.GEE_ERR_INVALID
     assert b"positive" in L.gee_last_error()
@@ -147,3 +148,21 @@ def test_product_package_never_imports_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "liboracle" not in text, f
+
+
+def test_weights_checked_before_float32_narrowing():
+    # finite f64 weights float32 cannot carry are rejected with a specific
+    # error instead of turning into inf / 0 (graph.py:46-47 checks finiteness
+    # on the caller's f64 array)
+    import paper_2402_04403_b200 as gb
+
+    with pytest.raises(ValidationError, match="float32 range"):
+        gb.EdgeList(n=2, src=[0], dst=[1], w=np.array([1e300]))
+    with pytest.raises(ValidationError, match="normal float32 range"):
+        gb.EdgeList(n=2, src=[0, 1], dst=[1, 0], w=np.array([1.0, 1e-300]))
+    with pytest.raises(ValidationError, match="edge weights must be finite"):
+        gb.EdgeList(n=2, src=[0], dst=[1], w=np.array([np.nan]))
+    with pytest.raises(ValidationError, match="arc weights must be finite"):
+        gb.CsrGraph(n=2, offsets=[0, 1, 1], targets=[1], weights=np.array([np.inf]))
+    el = gb.EdgeList(n=2, src=[0, 1], dst=[1, 0], w=np.array([0.0, -2.5]))
+    assert el.w.dtype == np.float32 and el.w.tolist() == [0.0, -2.5]

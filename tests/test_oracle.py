@@ -125,3 +125,38 @@ def test_random_labels_mirror_reproduces_reference_stream(golden):
         c = case(golden, f"rl{i}")
         n, k, seed = (int(x) for x in c["args"])
         assert np.array_equal(random_labels(n, k, float(c["fraction"]), seed).labels, c["labels"])
+
+
+@pytest.mark.parametrize("scale,s,seed,first,weighted", [(10, 5000, 3, 0, True), (16, 20000, 77, 12345, False),
+                                                         (27, 3000, 4, 10**9, True), (24, 4000, 3, 7, False)])
+def test_c_rmat_generator_matches_numpy_restatement(scale, s, seed, first, weighted):
+    # the reference arm builds C4 on the host with oracle.rmat_edges; it must
+    # be the workload's own stream (synth.rmat_edges_numpy, itself pinned to
+    # the GPU generator in tests/test_gpu_parity.py)
+    from paper_2402_04403_b200 import synth
+
+    got = oracle.rmat_edges(scale, s, seed, weighted=weighted, first=first, threads=3)
+    exp = synth.rmat_edges_numpy(scale, s, seed, weighted=weighted, first=first)
+    assert np.array_equal(got[0], exp[0]) and np.array_equal(got[1], exp[1])
+    assert (got[2] is None) == (exp[2] is None)
+    if weighted:
+        assert np.array_equal(got[2], exp[2])
+    assert np.array_equal(oracle.uniform_labels(7001, 50, seed), synth.uniform_labels_numpy(7001, 50, seed))
+
+
+def test_parallel_directed_csr_is_the_reference_csr_up_to_row_order():
+    rng = np.random.default_rng(9)
+    n, s = 500, 20_000
+    src, dst = rng.integers(0, n, s).astype(np.int32), rng.integers(0, n, s).astype(np.int32)
+    w = rng.random(s).astype(np.float32)
+    off, tgt, wt = oracle.build_csr_directed_par(src, dst, w, n, threads=4)
+    ro, rt, rw = oracle.build_csr(src, dst, w, n, True)
+    assert np.array_equal(off, ro)
+    for r in range(n):
+        a = sorted(zip(tgt[off[r]:off[r + 1]].tolist(), wt[off[r]:off[r + 1]].tolist()))
+        b = sorted(zip(rt[ro[r]:ro[r + 1]].tolist(), rw[ro[r]:ro[r + 1]].tolist()))
+        assert a == b
+    y = rng.integers(0, 6, n)
+    z1 = oracle.parallel_embed(off, tgt, wt, y, 5, True, 4)
+    z2 = oracle.serial_embed(src, dst, w, y, n, 5)
+    assert np.allclose(z1, z2, rtol=1e-12, atol=0)
