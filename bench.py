@@ -65,7 +65,6 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-push", action="store_true")
-    ap.add_argument("--cpu-sample-div", type=int, default=16)
     return ap.parse_args()
 
 
@@ -208,59 +207,135 @@ def sum_over_ranks(x, world):
 
 
 # ---------------------------------------------------------- CPU baseline
-def cpu_sample_graph(cfg_idx, div, scale_override):
-    """A self-similar 1/div sample of the workload in the reference's dtypes:
-    directed CSR (one arc per listed edge, BOTH_ENDPOINTS), int64 offsets,
-    int32 targets, f64 weights; int32 labels + f64 row_value."""
-    import torch
-
+def cpu_workload(cfg_idx, scale_override=None, edges_override=None):
+    """The bench workload built on the HOST in the reference's dtypes, with
+    the oracle's C generators and CSR build only (the product library is
+    never loaded on this path): int64 offsets, int32 targets, f64 weights;
+    directed lists keep one arc per listed edge with BOTH_ENDPOINTS
+    accounting, undirected ones the mirrored CSR with SOURCE_ONLY
+    (reference encoder.py:37-55, graph.py:159-184).  Same seeds and
+    generators as the GPU arm (oracle.rmat_edges is pinned bit for bit to
+    synth.rmat_edges_numpy, tests/test_oracle.py)."""
     import oracle
     from paper_2402_04403_b200 import synth
 
     cfg = synth.CONFIGS[cfg_idx]
-    base_scale = scale_override or {3: 24, 4: 27}.get(cfg_idx, None)
-    if base_scale is None:
-        raise SystemExit("CPU sample defined for R-MAT configs")
-    shift = int(round(np.log2(div)))
-    scale = base_scale - shift
-    n = 1 << scale
-    s = int(round(cfg.s / cfg.n * n)) if not scale_override else int(round(cfg.s / cfg.n * n))
-    src, dst, w = synth.rmat_edges(scale, s, seed=cfg_idx, weighted=cfg.weighted, device="cuda")
-    y = synth.uniform_labels(n, cfg.k, seed=cfg_idx, device="cuda") if cfg_idx == 4 else None
-    if y is None:
-        from paper_2402_04403_b200.labeling import random_labels
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    n, k = cfg.n, cfg.k
+    if cfg_idx in (3, 4):
+        scale = scale_override or (24 if cfg_idx == 3 else 27)
+        n = 1 << scale
+        s = edges_override or int(round(cfg.s / cfg.n * n))
+        src, dst, w = oracle.rmat_edges(scale, s, seed=cfg_idx, weighted=cfg.weighted, threads=threads)
+        if cfg_idx == 4:
+            y = oracle.uniform_labels(n, k, seed=4)
+        else:
+            from paper_2402_04403_b200.labeling import random_labels
 
-        y_h = random_labels(n, cfg.k, 0.1, seed=cfg_idx).labels
+            y = np.ascontiguousarray(random_labels(n, k, 0.1, seed=3).labels, dtype=np.int32)
+    elif cfg_idx == 2:
+        s = edges_override or cfg.s
+        src, dst, w, y = synth.sbm_directed(n, k, s, 0.5, seed=2)
+    elif cfg_idx == 1:
+        src, dst, y = synth.sbm_undirected(n, k, 0.01, 0.001, seed=0)
+        w = None
+    elif cfg_idx == 5:
+        s = edges_override or cfg.s
+        if edges_override:
+            n = max(1, int(round(cfg.n * s / cfg.s)))
+        src, dst, w = synth.er_edges_numpy(n, s, seed=5)
+        w = None
+        y = synth.zipf_labels(n, k, 1.1, seed=5)
     else:
-        y_h = y.cpu().numpy()
-    src_h, dst_h = src.cpu().numpy(), dst.cpu().numpy()
-    w_h = w.cpu().numpy().astype(np.float64) if w is not None else None
-    del src, dst, w
-    torch.cuda.empty_cache()
-    directed = True  # one arc per listed edge + BOTH accounting == the listed-edge pass
-    off, tgt, wts = oracle.build_csr(src_h, dst_h, w_h, n, directed)
-    del src_h, dst_h
-    _, _, row = oracle.projection(y_h, cfg.k)
-    return {"n": n, "s": s, "k": cfg.k, "scale": scale, "offsets": off, "targets": tgt,
-            "weights": None if w_h is None else wts, "labels": y_h.astype(np.int32), "row": row,
-            "sample": f"R-MAT scale {scale} (1/{div} of the workload's nodes and edges), {s} listed edges, "
-                      f"K={cfg.k}, same generator/weights/labels; reference dtypes (f64 Z)"}
+        raise SystemExit(f"unknown config {cfg_idx}")
+    src = np.ascontiguousarray(src, dtype=np.int32)
+    dst = np.ascontiguousarray(dst, dtype=np.int32)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    s = int(src.size)
+    t_gen = time.perf_counter() - t0
+    # the single-core serial pass (embed_serial) runs on a prefix of the
+    # listed edges: the generators are iid per edge, so a prefix is a
+    # uniform sample of the workload's edges over the full node set and Z
+    s_serial = min(s, max(1, s // 32))
+    serial = (src[:s_serial].astype(np.int64), dst[:s_serial].astype(np.int64),
+              None if w is None else w[:s_serial].astype(np.float64))
+    t0 = time.perf_counter()
+    if cfg.directed:
+        off, tgt, wts = oracle.build_csr_directed_par(src, dst, w, n, threads=threads)
+    else:
+        both_s, both_d = np.concatenate([src, dst]), np.concatenate([dst, src])
+        both_w = None if w is None else np.concatenate([w, w])
+        del src, dst
+        off, tgt, wts = oracle.build_csr_directed_par(both_s, both_d, both_w, n, threads=threads)
+        del both_s, both_d, both_w
+    src = dst = w = None
+    t_csr = time.perf_counter() - t0
+    _, _, row = oracle.projection(y, k)
+    return {"n": n, "s": s, "k": k, "directed": cfg.directed, "offsets": off, "targets": tgt, "weights": wts,
+            "labels": y, "row": row, "serial": serial, "s_serial": s_serial, "gen_s": t_gen, "csr_s": t_csr,
+            "sample": f"{'reduced ' if (scale_override or edges_override) else 'full '}{cfg.name} workload on the host "
+                      f"({n} nodes, {s} listed edges, K={k}), built by "
+                      f"oracle/ (C R-MAT + threaded build_csr), reference dtypes: int64 offsets, int32 targets, "
+                      f"f64 weights, f64 Z"}
 
 
-def time_cpu_reference(sample, steps, warmup, workers):
+def time_cpu_reference(work, steps, warmup, workers, budget_s=None):
+    """The reference's timed region (bench.py:54-95 there): embed_parallel
+    with a caller-owned out= (zero wave + arc wave), projection prebuilt."""
     import oracle
 
-    z = np.empty((sample["n"], sample["k"]), dtype=np.float64)
-    args = (sample["offsets"], sample["targets"], sample["weights"], sample["labels"], sample["k"], True, workers)
-    kw = dict(out=z, row_value=sample["row"], label32=sample["labels"])
+    z = np.empty((work["n"], work["k"]), dtype=np.float64)
+    args = (work["offsets"], work["targets"], work["weights"], work["labels"], work["k"], work["directed"], workers)
+    kw = dict(out=z, row_value=work["row"], label32=work["labels"])
     for _ in range(max(1, warmup)):
         oracle.parallel_embed(*args, **kw)
     times = []
+    t_all = time.perf_counter()
     for _ in range(max(1, steps)):
         t0 = time.perf_counter()
         oracle.parallel_embed(*args, **kw)
         times.append(time.perf_counter() - t0)
-    return float(np.median(times)), times
+        if budget_s is not None and time.perf_counter() - t_all > budget_s:
+            break
+    return float(np.median(times)), times, z
+
+
+def time_cpu_serial(work, z):
+    """embed_serial on one core (serial_pass, encoder.py:106-120) over the
+    serial sample; z (n, k) f64 is zeroed first, as embed_serial allocates
+    a zeroed Z (the zeroing is outside the timed pass)."""
+    import ctypes
+
+    import oracle
+
+    src, dst, w = work["serial"]
+    if w is None:
+        w = np.ones(src.size)
+    z.fill(0.0)
+    lab = work["labels"].astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.lib().oracle_serial_pass(*(x.ctypes.data_as(ctypes.c_void_p) for x in (src, dst, w)), src.size,
+                                    lab.ctypes.data_as(ctypes.c_void_p), work["row"].ctypes.data_as(ctypes.c_void_p),
+                                    z.ctypes.data_as(ctypes.c_void_p), work["k"])
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_line(args, steps, warmup, budget_s=None):
+    work = cpu_workload(args.config, args.scale, args.edges)
+    workers = os.cpu_count() or 1
+    med, times, z = time_cpu_reference(work, steps, warmup, workers, budget_s)
+    t_serial = time_cpu_serial(work, z)
+    del z
+    geps = work["s"] / med / 1e9
+    return geps, med, times, {
+        "value": geps, "unit": UNIT, "cores": workers, "kind": "port", "sample": work["sample"],
+        "same_config": not (args.scale or args.edges), "ms_per_step": med * 1e3, "steps": len(times),
+        "gen_s": round(work["gen_s"], 2), "csr_s": round(work["csr_s"], 2),
+        "serial_1core": {"value": work["s_serial"] / t_serial / 1e9, "unit": UNIT, "cores": 1,
+                         "sample": f"embed_serial (serial_pass) over the first {work['s_serial']} listed edges "
+                                   f"(1/32 prefix of the iid edge stream), full node set and Z",
+                         "s": t_serial}}
 
 
 def run_reference(args):
@@ -271,19 +346,20 @@ def run_reference(args):
     from paper_2402_04403_b200 import synth
 
     cfg = synth.CONFIGS[args.config]
-    workers = os.cpu_count() or 1
-    sample = cpu_sample_graph(args.config, args.cpu_sample_div, args.scale)
-    steps = max(1, min(args.steps, 5))
-    med, times = time_cpu_reference(sample, steps, min(args.warmup, 1), workers)
-    geps = sample["s"] / med / 1e9
+    warmup = min(args.warmup, 1)  # a CPU warm-up only faults pages and heats caches
+    geps, med, times, base = cpu_baseline_line(args, args.steps, warmup, budget_s=240.0)
     line = {
         "impl": "reference", "metric": METRIC, "value": geps, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": med * 1e3, "higher_is_better": True,
+        "steps": len(times), "warmup": warmup, "ms_per_step": med * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "sample": sample["sample"], "world_size": world},
-        "cpu_baseline": {"value": geps, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": sample["sample"]},
+        "config": {"workload": cfg.name if not (args.scale or args.edges) else
+                   f"{cfg.name}-reduced(scale={args.scale},s={args.edges})", "world_size": world,
+                   "same_config": base["same_config"], "sample": base["sample"]},
+        "cpu_baseline": base,
         "e2e": {"value": geps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host_peak_rss_gb": round(__import__("resource").getrusage(__import__("resource").RUSAGE_SELF).ru_maxrss / 2**20, 1),
+        "native_so_loaded": sorted({ln.split()[-1] for ln in open("/proc/self/maps") if ln.rstrip().endswith(".so")
+                                    and ROOT in ln}),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -474,17 +550,15 @@ def main():
     if not args.no_e2e:
         result["e2e"] = run_e2e(g, y, emb, z, s, args, world)
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline (rank 0, N=1 only): the oracle port on the same
+    # workload, built on the host (the GPU arm's buffers are released first)
     if not args.no_cpu and world == 1 and rank == 0:
-        try:
-            sample = cpu_sample_graph(args.config, args.cpu_sample_div, args.scale)
-            workers = os.cpu_count() or 1
-            med, _ = time_cpu_reference(sample, 3, 1, workers)
-            result["cpu_baseline"] = {"value": sample["s"] / med / 1e9, "unit": UNIT, "cores": workers,
-                                      "kind": "port", "sample": sample["sample"], "ms_per_step": med * 1e3}
-        except SystemExit as e:
-            result["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                                      "sample": str(e)}
+        del g, emb, z
+        torch.cuda.empty_cache()
+        if hasattr(torch._C, "_host_emptyCache"):
+            torch._C._host_emptyCache()
+        _, _, _, base = cpu_baseline_line(args, 3, 1)
+        result["cpu_baseline"] = base
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

@@ -55,6 +55,8 @@ def lib():
         L.oracle_sampled_rows.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, i64]
         L.oracle_sampled_rows.restype = None
         u64 = ctypes.c_uint64
+        L.oracle_sampled_rows_par.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, i64, vp, vp, i64, i32]
+        L.oracle_sampled_rows_par.restype = None
         L.oracle_rmat.argtypes = [vp, vp, vp, i64, i64, i32, dbl, dbl, dbl, u64, i32, i32]
         L.oracle_rmat.restype = None
         L.oracle_uniform_labels.argtypes = [vp, i64, i64, u64]
@@ -158,6 +160,30 @@ def sampled_rows(src, dst, w, labels, k, rows):
     lib().oracle_sampled_rows(_p(src), _p(dst), None if w is None else _p(w), src.size, _p(lab), _p(inv), _p(slot),
                               _p(zs), k)
     return zs
+
+
+def sampled_rows_par(src, dst, w, labels, k, rows, threads=None):
+    """sampled_rows over all host threads, plus the column mass: returns
+    (zs f64[len(rows), k], mass f64[k]) with mass[c-1] = sum_x Z[x, c].
+    For the full-size configurations (up to 1.8e9 listed edges)."""
+    src = np.ascontiguousarray(src, dtype=np.int32)
+    dst = np.ascontiguousarray(dst, dtype=np.int32)
+    w = None if w is None else np.ascontiguousarray(w, dtype=np.float32)
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    n = lab.size
+    _, inv, _ = projection(lab, k)
+    rows = np.asarray(rows, dtype=np.int64)
+    assert np.unique(rows).size == rows.size, "rows must be distinct"
+    keep = np.zeros((n + 63) // 64, dtype=np.uint64)
+    np.bitwise_or.at(keep, rows >> 6, np.left_shift(np.uint64(1), (rows & 63).astype(np.uint64)))
+    slot = np.zeros(n, dtype=np.int32)
+    slot[rows] = np.arange(rows.size, dtype=np.int32)
+    zs = np.empty((rows.size, k), dtype=np.float64)
+    mass = np.empty(k + 1, dtype=np.float64)
+    lib().oracle_sampled_rows_par(_p(src), _p(dst), None if w is None else _p(w), src.size, _p(lab), _p(inv),
+                                  _p(keep), _p(slot), rows.size, _p(zs), _p(mass), k,
+                                  threads or os.cpu_count() or 1)
+    return zs, mass[1:]
 
 
 def numpy_reference(src, dst, w, labels, n, k):

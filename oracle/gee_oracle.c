@@ -280,6 +280,76 @@ void oracle_sampled_rows(const int32_t *src, const int32_t *dst, const float *w,
     }
 }
 
+/* The same sampled-row rule, threaded, plus the column mass, for the
+ * full-size configurations (C3/C4/C5 at BASELINE sizes: up to 1.8e9 listed
+ * edges, whose f64 Z does not fit the sampled-row budget of a serial scan).
+ * Each thread takes a contiguous slice of the listed edges and accumulates
+ * into its own zs / mass copies, which are then summed in thread order:
+ * the f64 summation order differs from list order (as the reference's own
+ * embed_parallel's does), nothing else.  `keep` is a bitmap of the sampled
+ * rows (n bits) so that most edges are rejected from a 16 MB table;
+ * slot[r] is the row's index in zs.  mass[c] = sum over listed edges of
+ * w * inv[c] * ([Y[v]=c] + [Y[u]=c]) = sum_x Z[x, c] (the mass accounting
+ * of the reference's test_parallel.py:54-64), c = 1..k, mass[0] unused. */
+static inline double inv_mul(double inv, double w) { return inv * w; }
+
+typedef struct {
+    const int32_t *src, *dst;
+    const float *w;
+    int64_t lo, hi;
+    const int32_t *labels;
+    const double *inv;
+    const uint64_t *keep;
+    const int32_t *slot;
+    double *zs, *mass;
+    int64_t k;
+} sampled_job;
+
+static void *sampled_worker(void *arg)
+{
+    sampled_job *j = (sampled_job *)arg;
+    const int64_t k = j->k;
+    for (int64_t i = j->lo; i < j->hi; i++) {
+        const int64_t u = j->src[i], v = j->dst[i];
+        const double wi = j->w ? (double)j->w[i] : 1.0;
+        const int64_t yu = j->labels[u], yv = j->labels[v];
+        if (yv) j->mass[yv] += inv_mul(j->inv[yv], wi);
+        if (yu) j->mass[yu] += inv_mul(j->inv[yu], wi);
+        if (yv && ((j->keep[u >> 6] >> (u & 63)) & 1))
+            j->zs[(int64_t)j->slot[u] * k + (yv - 1)] += j->inv[yv] * wi;
+        if (yu && ((j->keep[v >> 6] >> (v & 63)) & 1))
+            j->zs[(int64_t)j->slot[v] * k + (yu - 1)] += j->inv[yu] * wi;
+    }
+    return NULL;
+}
+
+void oracle_sampled_rows_par(const int32_t *src, const int32_t *dst, const float *w, int64_t s,
+                             const int32_t *labels, const double *inv, const uint64_t *keep, const int32_t *slot,
+                             int64_t n_rows, double *zs, double *mass, int64_t k, int threads)
+{
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t t[256];
+    sampled_job jobs[256];
+    const size_t zlen = (size_t)(n_rows * k);
+    for (int i = 0; i < threads; i++) {
+        sampled_job jb = {src, dst, w, s * i / threads, s * (i + 1) / threads, labels, inv, keep, slot,
+                          (double *)calloc(zlen ? zlen : 1, sizeof(double)),
+                          (double *)calloc((size_t)(k + 1), sizeof(double)), k};
+        jobs[i] = jb;
+        pthread_create(&t[i], NULL, sampled_worker, &jobs[i]);
+    }
+    for (int i = 0; i < threads; i++) pthread_join(t[i], NULL);
+    memset(zs, 0, zlen * sizeof(double));
+    memset(mass, 0, (size_t)(k + 1) * sizeof(double));
+    for (int i = 0; i < threads; i++) {
+        for (size_t q = 0; q < zlen; q++) zs[q] += jobs[i].zs[q];
+        for (int64_t c = 0; c <= k; c++) mass[c] += jobs[i].mass[c];
+        free(jobs[i].zs);
+        free(jobs[i].mass);
+    }
+}
+
 /* ---- seeded synthetic inputs for the CPU arm (bench.py --impl reference) ----
  *
  * A C restatement of the counter-based generator the workload uses

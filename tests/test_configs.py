@@ -3,12 +3,12 @@
 * C1 and C2 at full size, C3 / C4 / C5 at reduced size: the full f64 oracle
   (oracle.serial_embed, the reference's serial_pass rule) against the pull
   and the push; the pull is bit-stable; class counts are exact.
-* C3 and C4 at FULL size: a row sample (uniform rows plus the highest-degree
-  hubs) against an f64 restatement of the same rule computed
-  with torch on the GPU in edge chunks, plus per-column mass accounting
-  (sum_x Z[x,c] = inv[c] * sum over edges of w * ([Y[v]=c] + [Y[u]=c])).
-  The f64 restatement is test infrastructure, like the oracle: the C oracle
-  would need minutes of random host-memory access for 1.8e9 edges.
+* C3, C4 and C5 at FULL size: a row sample (uniform rows plus the
+  highest-degree hubs) against the C oracle's threaded
+  sampled-row restatement of serial_pass (oracle.sampled_rows_par, pinned to
+  oracle.serial_embed in tests/test_oracle.py), plus per-column mass
+  accounting (sum_x Z[x,c] = inv[c] * sum over edges of w * ([Y[v]=c] +
+  [Y[u]=c])).
 """
 
 import numpy as np
@@ -58,31 +58,23 @@ def test_config_full_oracle(idx, override):
     assert rel_err(zq.cpu().numpy(), exp) <= TOL
 
 
-def _f64_rows_and_mass(src, dst, w, y, n, k, rows, chunk=1 << 27):
-    """f64 restatement of serial_pass (reference _kernels.py:210-226) on the
-    GPU: Z rows for `rows` and the per-column sums of the whole Z."""
-    counts = torch.bincount(y.long(), minlength=k + 1).double()
-    inv = torch.where(counts > 0, 1.0 / counts, torch.zeros_like(counts))
-    inv[0] = 0.0
-    slot = torch.full((n,), -1, dtype=torch.int64, device=DEV)
-    slot[rows] = torch.arange(rows.numel(), device=DEV)
-    zs = torch.zeros(rows.numel() * k, dtype=torch.float64, device=DEV)
-    mass = torch.zeros(k + 1, dtype=torch.float64, device=DEV)
-    for a in range(0, src.numel(), chunk):
-        u, v = src[a:a + chunk].long(), dst[a:a + chunk].long()
-        ww = w[a:a + chunk].double() if w is not None else torch.ones(u.numel(), dtype=torch.float64, device=DEV)
-        yu, yv = y[u].long(), y[v].long()
-        mass.index_add_(0, yv, ww * inv[yv])
-        mass.index_add_(0, yu, ww * inv[yu])
-        for row, cls, ws in ((u, yv, ww * inv[yv]), (v, yu, ww * inv[yu])):
-            sr = slot[row]
-            m = (sr >= 0) & (cls > 0)
-            zs.index_add_(0, sr[m] * k + cls[m] - 1, ws[m])
-    return zs.view(rows.numel(), k), mass[1:]
+def _sample_rows(src, dst, n, seed, uniform=65536, hubs=1024):
+    gen = torch.Generator(device=DEV).manual_seed(seed)
+    deg = torch.bincount(src.long(), minlength=n) + torch.bincount(dst.long(), minlength=n)
+    top = torch.topk(deg, min(hubs, n)).indices
+    rows = torch.unique(torch.cat([torch.randint(0, n, (uniform,), device=DEV, generator=gen), top]))
+    return rows
 
 
-@pytest.mark.parametrize("idx", [3, 4], ids=["C3-full", "C4-full"])
+@pytest.mark.parametrize("idx", [3, 4, 5], ids=["C3-full", "C4-full", "C5-full"])
 def test_config_full_size_sampled(idx):
+    """BASELINE sizes (C3: 268M undirected edges, K=100, 10% labeled; C4:
+    1.8e9 directed weighted edges, K=50; C5: n=4e6, 256M edges, K=1000):
+    the pull's Z on >= 65K uniform rows plus the 1024 highest-degree rows
+    against the pinned C oracle's sampled-row restatement of serial_pass
+    (oracle.sampled_rows_par, f64), and every column's mass sum_x Z[x, c]
+    against the oracle's mass accounting (reference test_parallel.py:54-64).
+    Counts exact; pull run-to-run bit-stable."""
     src, dst, w, y, n, k, directed = synth.make_config(idx)
     g = DeviceGraph.from_edges(src, dst, w, n, device=DEV, pull=True)
     emb = Embedder(n, k, DEV)
@@ -90,12 +82,18 @@ def test_config_full_size_sampled(idx):
     z2 = emb.pull(g)
     assert torch.equal(z, z2), "pull is not run-to-run bit-stable"
     del z2
-    gen = torch.Generator(device=DEV).manual_seed(idx)
-    deg = torch.bincount(src.long(), minlength=n) + torch.bincount(dst.long(), minlength=n)
-    hubs = torch.topk(deg, 1024).indices
-    rows = torch.unique(torch.cat([torch.randint(0, n, (65536,), device=DEV, generator=gen), hubs]))
-    del deg
-    zs, mass = _f64_rows_and_mass(src, dst, w, y, n, k, rows)
-    assert rel_err(z[rows].cpu().numpy(), zs.cpu().numpy()) <= TOL
-    col = sum(z[a:a + (1 << 24)].double().sum(0) for a in range(0, n, 1 << 24))
-    assert torch.allclose(col, mass, rtol=1e-5, atol=0)
+    yh = y.cpu().numpy()
+    assert np.array_equal(emb.counts.cpu().numpy(), np.bincount(yh, minlength=k + 1))
+    del g
+    torch.cuda.empty_cache()
+    rows = _sample_rows(src, dst, n, idx, uniform=65536 if idx != 5 else 131072)
+    zr = z[rows].cpu().numpy()
+    col = sum(z[a:a + (1 << 22)].double().sum(0) for a in range(0, n, 1 << 22)).cpu().numpy()
+    del z
+    torch.cuda.empty_cache()
+    src_h, dst_h = src.cpu().numpy(), dst.cpu().numpy()
+    w_h = None if w is None else w.cpu().numpy()
+    del src, dst, w
+    zs, mass = oracle.sampled_rows_par(src_h, dst_h, w_h, yh, k, rows.cpu().numpy())
+    assert rel_err(zr, zs) <= TOL
+    assert np.allclose(col, mass, rtol=1e-5, atol=1e-9)

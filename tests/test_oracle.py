@@ -160,3 +160,25 @@ def test_parallel_directed_csr_is_the_reference_csr_up_to_row_order():
     z1 = oracle.parallel_embed(off, tgt, wt, y, 5, True, 4)
     z2 = oracle.serial_embed(src, dst, w, y, n, 5)
     assert np.allclose(z1, z2, rtol=1e-12, atol=0)
+
+
+def test_threaded_sampled_rows_and_mass_match_serial_oracle(rng):
+    # the full-size config tests check sampled rows + column mass with this
+    # threaded restatement; pin it to the serial oracle (signed weights,
+    # unlabeled nodes, self loops, repeated edges)
+    n, s, k = 4000, 50_000, 9
+    src = rng.integers(0, n, s).astype(np.int32)
+    dst = rng.integers(0, n, s).astype(np.int32)
+    dst[:500] = src[:500]
+    src[500:900] = 7
+    w = rng.standard_normal(s).astype(np.float32)
+    y = rng.integers(0, k + 1, n).astype(np.int32)
+    z = oracle.serial_embed(src, dst, w, y, n, k)
+    rows = np.unique(np.concatenate([rng.integers(0, n, 400), [7, 0, n - 1]]))
+    for threads in (1, 6):
+        zs, mass = oracle.sampled_rows_par(src, dst, w, y, k, rows, threads=threads)
+        assert np.allclose(zs, z[rows], rtol=1e-12, atol=1e-12)
+        assert np.allclose(mass, z.sum(0), rtol=1e-12, atol=1e-12)
+    zs, mass = oracle.sampled_rows_par(src, dst, None, y, k, rows, threads=3)
+    zu = oracle.serial_embed(src, dst, None, y, n, k)
+    assert np.allclose(zs, zu[rows], rtol=1e-12, atol=0)
