@@ -382,7 +382,7 @@ def build_shard(args, world, rank):
     s = int(src.numel())
     t0 = time.perf_counter()
     if world == 1:
-        g = DeviceGraph.from_edges(src, dst, w, n, pull=True, keep_coo=not args.no_push)
+        g = DeviceGraph.from_edges(src, dst, w, n, pull=True, keep_coo=True)
         row_lo, row_hi = 0, n
     else:
         g, row_lo, row_hi = shard_mod.build_row_shard(src, dst, w, n, world, rank, k=k)
@@ -529,7 +529,7 @@ def main():
     }
 
     # ---- variant measurement: push on the same graph (chosen by measurement)
-    if world == 1 and g.has_push:
+    if world == 1 and g.has_push and not args.no_push:
         zp = torch.empty((n, k), dtype=torch.float32, device=dev)
         emb.push(g, zp)
         torch.cuda.synchronize()
@@ -543,17 +543,29 @@ def main():
         torch.cuda.synchronize()
         result["variants_ms_per_step"] = {"pull": ms_step, "push": a.elapsed_time(b) / reps}
         del zp
-        g.src = g.dst = g.w = None
         torch.cuda.empty_cache()
 
-    # ---- e2e through host buffers (every rank streams its own rows)
+    # ---- e2e through host buffers
     if not args.no_e2e:
-        result["e2e"] = run_e2e(g, y, emb, z, s, args, world)
+        if world == 1:
+            # the public call on reference-shaped host arrays: a stored
+            # CsrGraph (int64 offsets, int32 targets, f32 weights; one arc
+            # per listed edge) and host labels; graph preparation once
+            # (prepare), then embed_parallel(prepared, y, out=host Z)
+            csr_h = host_csr_from_coo(g, n, directed)
+            z_ref = z
+            del g, emb
+            torch.cuda.empty_cache()
+            result["e2e"] = run_e2e_prepared(csr_h, y, k, s, args, z_ref)
+            del csr_h, z_ref
+            g = emb = z = None
+        else:
+            result["e2e"] = run_e2e(g, y, emb, z, s, args, world)
 
     # ---- CPU baseline (rank 0, N=1 only): the oracle port on the same
     # workload, built on the host (the GPU arm's buffers are released first)
     if not args.no_cpu and world == 1 and rank == 0:
-        del g, emb, z
+        g = emb = z = None
         torch.cuda.empty_cache()
         if hasattr(torch._C, "_host_emptyCache"):
             torch._C._host_emptyCache()
@@ -566,6 +578,71 @@ def main():
 
         dist.destroy_process_group()
     return 0
+
+
+def host_csr_from_coo(g, n, directed):
+    """The stored graph a reference user holds: CsrGraph in host memory,
+    built from the listed edges with the GPU counting sort (graph prep)."""
+    import torch
+
+    from paper_2402_04403_b200 import CsrGraph, EdgeList, build_csr
+
+    el = EdgeList(n=n, src=g.src, dst=g.dst, w=g.w, directed=directed)
+    c = build_csr(el, stable=False)
+    h = CsrGraph(n=n, offsets=c.offsets.cpu().numpy(), targets=c.targets.cpu().numpy(),
+                 weights=None if c.weights is None else c.weights.cpu().numpy(), directed=directed)
+    del c, el
+    g.src = g.dst = g.w = None
+    torch.cuda.empty_cache()
+    return h
+
+
+def run_e2e_prepared(csr_h, y, k, s, args, z_ref):
+    """e2e through the public API: prepared = prepare(csr, k) once (graph
+    preparation, timed and reported apart), then every timed step is
+    embed_parallel(prepared, y, out=h_z): host labels in, the prepared graph
+    streamed from pinned host memory in row chunks, host Z out -- H2D,
+    kernels, D2H and the host-side expansion overlapping.  Wall clock
+    around the call."""
+    import torch
+
+    from paper_2402_04403_b200 import LabelVector, embed_parallel, prepare
+
+    y_h = LabelVector(labels=y.cpu().numpy(), k=k)
+    t0 = time.perf_counter()
+    prepared = prepare(csr_h, k, chunks=args.e2e_chunks)
+    prep_total = time.perf_counter() - t0
+    h_z = np.empty((csr_h.n, k), dtype=np.float32)
+    t0 = time.perf_counter()
+    embed_parallel(prepared, y_h, out=h_z)  # warm-up: registers h_z / labels, sizes the scratch
+    t_first = time.perf_counter() - t0
+    times = []
+    for _ in range(args.e2e_steps):
+        h_z.fill(np.nan)  # untimed: every entry must be rewritten by the call
+        t0 = time.perf_counter()
+        embed_parallel(prepared, y_h, out=h_z)
+        times.append(time.perf_counter() - t0)
+    ms = float(np.median(times)) * 1e3
+    # the streamed Z equals the resident pull's Z (exact integer sums; untimed)
+    same = True
+    step = max(1, (1 << 28) // k)
+    for r0 in range(0, csr_h.n, step):
+        same = same and bool(torch.equal(torch.from_numpy(h_z[r0:r0 + step]).to(z_ref.device), z_ref[r0:r0 + step]))
+    h2d = prepared.h2d_bytes_per_call
+    d2h = prepared.d2h_bytes_last_call
+    prepared.close()
+    return {"value": s / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": args.e2e_steps,
+            "chunks": args.e2e_chunks, "matches_resident_pull": same, "timing": "wall clock, median",
+            "path": "paper_2402_04403_b200.embed_parallel(prepare(CsrGraph host arrays, k), "
+                    "LabelVector(host int32), out=host float32 (n, k))",
+            "inside": "labels H2D | packed row chunks H2D | gee_unpack_targets, gee_build_projection, "
+                      "gee_gather_labels, gee_reduce_blocks, gee_reduce_heavy, gee_z_compact | D2H row-sparse Z | "
+                      "gee_io_expand_rows on the host threads into out",
+            "first_call_ms": t_first * 1e3,
+            "prep_s": {**{kx: round(v, 3) for kx, v in prepared.prep_s.items()}, "total": round(prep_total, 3)},
+            "stored_graph": f"CsrGraph(n={csr_h.n}, arcs={csr_h.s}, directed={csr_h.directed}, "
+                            f"weights={'f32' if csr_h.weights is not None else 'unit'}) in host memory"}
 
 
 def run_e2e(g, y, emb, z, s, args, world=1):

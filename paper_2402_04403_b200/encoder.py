@@ -260,6 +260,11 @@ def embed_parallel(
 ):
     """Edge map over all arcs of a stored CsrGraph (encoder.py:123-194).
 
+    ``g`` may also be a ``PreparedGraph`` (``prepare(g, k)``): graph
+    preparation then happened once, outside the call, and the call streams
+    the prepared layout from pinned host memory (or runs it from HBM) --
+    the path for repeated passes over a large graph.
+
     ``workers`` is validated like the reference (>= 1) and otherwise
     ignored: the GPU kernels size their own grids.  ``atomics=False`` (the
     reference's unsafe mode for measuring atomic cost) selects the pull
@@ -270,11 +275,26 @@ def embed_parallel(
     import torch
 
     from .device import PULL_REL_ERR_MAX, DeviceGraph, Embedder, require_cuda, to_device
+    from .prepared import PreparedGraph
 
     if g.n != y.n:
         raise ValidationError(f"graph has {g.n} nodes but labels have {y.n}")
     if workers is not None and workers < 1:
         raise ValidationError("workers must be at least 1")
+    if isinstance(g, PreparedGraph):
+        # graph preparation already done (prepare()): only the per-call pass
+        if variant not in ("auto", "pull"):
+            raise ValidationError("a prepared graph runs the pull variant")
+        _validate_projection(projection, g.n, y.k)
+        if projection is not None:
+            y = LabelVector(labels=projection.label, k=y.k)
+        out = _check_out(out, g.n, y.k)
+        inv = None
+        if projection is not None:
+            inv = _projection_inv(projection, to_device(y.labels, torch.int32, g.device), y.k)
+        res = g.run(y, out=out, inv=inv)
+        _record("pull", "prepared", f"prepared graph ({g.residency} residency)")
+        return res
     if accounting is None:
         accounting = edge_accounting(g)
     _validate_projection(projection, g.n, y.k)

@@ -198,8 +198,9 @@ class HostPipeline:
         self.h_tot = torch.zeros(max(1, len(self.views)), dtype=torch.int64).pin_memory()
         self.mw = mw
 
-    def run(self, h_labels, h_z, emb: Embedder, sparse=True):
-        """labels (pinned host int32[n]) -> h_z (pinned host float32[n, k])."""
+    def run(self, h_labels, h_z, emb: Embedder, sparse=True, inv=None):
+        """labels (pinned host int32[n]) -> h_z (pinned host float32[n, k]).
+        ``inv`` (float64[k+1]) replaces 1/count (a caller's projection)."""
         if h_z.shape != (self.n, self.k) or h_z.dtype != torch.float32 or not h_z.is_contiguous():
             raise ValidationError("h_z must be a contiguous float32 (n, k) host tensor")
         if sparse:
@@ -214,7 +215,7 @@ class HostPipeline:
             e_lab.record(self.s_in)
         self.s_cmp.wait_event(e_lab)
         with torch.cuda.stream(self.s_cmp):
-            emb.project(self.d_y, validate=False, g=self.proj)
+            emb.project(self.d_y, validate=False, g=self.proj, inv=inv)
         nv = len(self.views)
         e_in = [ev() for _ in self.views]
         e_cmp = [ev() for _ in self.views]

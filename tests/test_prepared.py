@@ -1,0 +1,110 @@
+"""prepare() + embed_parallel(prepared, y, out=...): the public host-buffer
+path (graph preparation once, the edge pass per call), against the stored
+graph's own embed_parallel and the CPU oracle (reference encoder.py:123-194:
+host CSR + labels in, host Z out, ``out=`` reused across calls)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import rel_err
+
+from paper_2402_04403_b200 import (CsrGraph, EdgeList, LabelVector, ProjectionMatrix, ValidationError,
+                                   build_projection, embed_parallel, prepare)
+from paper_2402_04403_b200.encoder import last_pass
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def _graph(seed, n=3000, s=40_000, weighted=True, directed=True, signed=False):
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, s).astype(np.int32)
+    dst = (src + rng.zipf(1.6, s) % n).astype(np.int32) % n  # some hubs and locality
+    src[: s // 50] = 3  # one heavy row
+    w = None
+    if weighted:
+        w = rng.random(s) + 0.01
+        if signed:
+            w *= np.where(rng.random(s) < 0.5, -1.0, 1.0)
+        w = w.astype(np.float32)
+    return src, dst, w
+
+
+def _csr(src, dst, w, n, directed):
+    off, tgt, wts = oracle.build_csr(src, dst, w, n, directed)
+    return CsrGraph(n=n, offsets=off, targets=tgt, weights=None if w is None else wts, directed=directed)
+
+
+@pytest.mark.parametrize("directed", [True, False])
+@pytest.mark.parametrize("weighted,signed", [(True, False), (True, True), (False, False)])
+@pytest.mark.parametrize("residency", ["host", "device"])
+def test_prepared_matches_stored_graph_and_oracle(directed, weighted, signed, residency):
+    n, k = 3000, 13
+    src, dst, w = _graph(7, n=n, weighted=weighted, signed=signed)
+    y = LabelVector(labels=np.random.default_rng(8).integers(0, k + 1, n), k=k)
+    g = _csr(src, dst, w, n, directed)
+    p = prepare(g, k, residency=residency, chunks=3)
+    assert p.n == n and p.k == k and p.s == src.size and p.directed == directed
+    exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
+    ref = embed_parallel(g, y, variant="pull")
+    out = np.full((n, k), np.nan, dtype=np.float32)
+    for _ in range(2):  # out= reused (registered once), every entry rewritten
+        got = embed_parallel(p, y, out=out)
+        assert got is out
+        assert last_pass()["reducer"] == "prepared"
+        assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+        out.fill(np.nan)
+    fresh = embed_parallel(p, y)
+    assert fresh.dtype == np.float32 and np.array_equal(fresh, ref)
+    assert rel_err(fresh, exp) <= 1e-4
+    z64 = np.empty((n, k))
+    embed_parallel(p, y, out=z64)
+    assert np.array_equal(z64, ref.astype(np.float64))
+    p.close()
+    with pytest.raises(ValidationError):
+        embed_parallel(p, y)
+
+
+def test_prepared_from_edge_list_and_device_labels():
+    n, k = 2500, 9
+    src, dst, w = _graph(11, n=n, s=30_000)
+    el = EdgeList(n=n, src=src, dst=dst, w=w, directed=True)
+    lab = np.random.default_rng(12).integers(0, k + 1, n)
+    p = prepare(el, k, chunks=2)
+    z_host = embed_parallel(p, LabelVector(labels=lab, k=k))
+    z_dev = embed_parallel(p, LabelVector(labels=torch.as_tensor(lab, device="cuda"), k=k))
+    assert np.array_equal(z_host, z_dev)
+    out_d = torch.empty((n, k), dtype=torch.float32, device="cuda")
+    embed_parallel(p, LabelVector(labels=lab, k=k), out=out_d)
+    assert np.array_equal(out_d.cpu().numpy(), z_host)
+    assert rel_err(z_host, oracle.serial_embed(src, dst, w, lab, n, k)) <= 1e-4
+
+
+def test_prepared_projection_and_errors():
+    n, k = 2000, 6
+    src, dst, w = _graph(21, n=n, s=20_000)
+    g = _csr(src, dst, w, n, True)
+    lab = np.random.default_rng(22).integers(0, k + 1, n)
+    y = LabelVector(labels=lab, k=k)
+    p = prepare(g, k, chunks=2)
+    proj = build_projection(y)
+    scaled = ProjectionMatrix(n=n, k=k, row_value=proj.row_value * 2.0, label=proj.label)
+    z = embed_parallel(p, y, projection=scaled)
+    assert np.array_equal(z, embed_parallel(g, y, projection=scaled, variant="pull"))
+    with pytest.raises(ValidationError, match="prepared for k=6"):
+        embed_parallel(p, LabelVector(labels=lab, k=k + 1))
+    with pytest.raises(ValidationError, match="nodes"):
+        embed_parallel(p, LabelVector(labels=lab[:-1], k=k))
+    with pytest.raises(ValidationError):
+        embed_parallel(p, y, out=np.empty((n, k + 1), dtype=np.float32))
+    with pytest.raises(ValidationError):
+        embed_parallel(p, y, variant="push")
+    with pytest.raises(ValidationError):
+        embed_parallel(p, y, workers=0)
+    wide = w.copy()
+    wide[0] = 1e-30
+    with pytest.raises(ValidationError, match="push"):
+        prepare(_csr(src, dst, wide, n, True), k)
