@@ -89,6 +89,20 @@ int gee_build_projection_hotc(const int32_t *labels, int64_t n, int32_t k, int64
                               double *inv_f64, void *table, const uint32_t *hot_bits, const int32_t *hot_pref,
                               const int32_t *hot_list, int64_t n_hot, int64_t *bad, void *stream);
 
+/* Sharded histogram for row-range multi-GPU runs (SURVEY 8(e) scheme 1):
+ * the label table receives every label (as gee_build_projection_hotc; the
+ * hot tier may be absent, n_hot = 0), but counts[] only the nodes in
+ * [count_lo, count_hi) -- this rank's slice of np.bincount (encoder.py:87).
+ * The caller sums counts[] over the ranks (one all-reduce of k+1 int64)
+ * and then calls gee_projection_inv. */
+int gee_build_projection_sharded(const int32_t *labels, int64_t n, int32_t k, int64_t *counts, void *table,
+                                 const uint32_t *hot_bits, const int32_t *hot_pref, const int32_t *hot_list,
+                                 int64_t n_hot, int64_t count_lo, int64_t count_hi, int64_t *bad, void *stream);
+
+/* inv[c] = 1/counts[c] for nonempty classes c >= 1, inv[0] = 0
+ * (encoder.py:95-97), f32 and/or f64 (either may be NULL). */
+int gee_projection_inv(const int64_t *counts, int32_t k, float *inv_f32, double *inv_f64, void *stream);
+
 /* ---------------------------------------------------------------- K3 ----
  * Push edge map over a listed edge list (COO, structure of arrays).
  * Replaces serial_pass (_kernels.py:210-226, via embed_serial,

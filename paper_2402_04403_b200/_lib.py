@@ -42,6 +42,8 @@ SIGNATURES = {
     "gee_projection_work_bytes": (c_size, [c_i32]),
     "gee_build_projection": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp, vp, c_i64, vp, vp]),
     "gee_build_projection_hotc": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp, vp, vp, vp, c_i64, vp, vp]),
+    "gee_build_projection_sharded": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp, vp, c_i64, c_i64, c_i64, vp, vp]),
+    "gee_projection_inv": (c_int, [vp, c_i32, vp, vp, vp]),
     "gee_embed_coo": (c_int, [vp, vp, vp, c_i64, vp, c_i64, vp, c_i64, c_i32, vp, c_u32, vp]),
     "gee_build_csr": (c_int, [vp, vp, vp, c_i64, c_i64, c_i32, c_i32, vp, vp, vp, vp]),
     "gee_build_sym_csr": (c_int, [vp, vp, vp, c_i64, c_i64, vp, vp, vp, vp]),

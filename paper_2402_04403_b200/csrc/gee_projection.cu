@@ -23,7 +23,8 @@ __global__ void __launch_bounds__(HIST_THREADS)
 k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned long long *__restrict__ counts,
              LT *__restrict__ table, const int32_t *__restrict__ hot_rank, int64_t n_hot,
              unsigned long long *__restrict__ bad, int copies, const uint32_t *__restrict__ hot_bits,
-             const int32_t *__restrict__ hot_pref, const int32_t *__restrict__ hot_list)
+             const int32_t *__restrict__ hot_pref, const int32_t *__restrict__ hot_list, int64_t count_lo,
+             int64_t count_hi)
 {
     extern __shared__ uint32_t hist[];  // copies * (k+1) bins
     const int bins = k + 1;
@@ -36,12 +37,18 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned 
     LT *cold = table ? table + n_hot : nullptr;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
 
-    // count label c (checked) and return it (0 when out of range)
-    auto count = [&](int32_t c) -> int32_t {
+    // count label c of node i (checked) and return it (0 when out of range);
+    // only nodes in [count_lo, count_hi) are counted (a row shard's slice of
+    // a sharded histogram; the table always receives every label)
+    const uint64_t cspan = (uint64_t)(count_hi - count_lo);
+    const bool ranged = count_lo > 0 || count_hi < n;  // uniform: the full-range path has no extra test
+    auto count = [&](int64_t i, int32_t c) -> int32_t {
+        const bool counted = !ranged || (uint64_t)(i - count_lo) < cspan;
         if ((uint32_t)c > (uint32_t)k) {  // outside [0, k] (LabelVector, labeling.py:24-29)
-            nbad++;
+            if (counted) nbad++;
             return 0;
         }
+        if (!counted) return c;
         if (smem)
             atomicAdd(&mine[c], 1u);
         else
@@ -49,7 +56,7 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned 
         return c;
     };
     auto one = [&](int64_t i, int32_t c, int32_t r) {
-        c = count(c);
+        c = count(i, c);
         if (cold) {
             cold[i] = (LT)c;
             if (r >= 0) table[r] = (LT)c;  // hot tier copy (gee_hot.cu)
@@ -78,7 +85,8 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned 
                 }
             }
             if (pack4) {
-                const int32_t c0 = count(v.x), c1 = count(v.y), c2 = count(v.z), c3 = count(v.w);
+                const int32_t c0 = count(4 * q, v.x), c1 = count(4 * q + 1, v.y), c2 = count(4 * q + 2, v.z),
+                              c3 = count(4 * q + 3, v.w);
                 reinterpret_cast<uint32_t *>(cold)[q] = (uint32_t)c0 | (uint32_t)c1 << 8 | (uint32_t)c2 << 16 |
                                                         (uint32_t)c3 << 24;
                 if (r.x >= 0) table[r.x] = (LT)c0;
@@ -129,8 +137,9 @@ template <typename LT>
 int launch_hist(const int32_t *labels, int64_t n, int32_t k, unsigned long long *counts, void *table,
                 const int32_t *hot_rank, int64_t n_hot, unsigned long long *bad, cudaStream_t st,
                 const uint32_t *hot_bits = nullptr, const int32_t *hot_pref = nullptr,
-                const int32_t *hot_list = nullptr)
+                const int32_t *hot_list = nullptr, int64_t count_lo = 0, int64_t count_hi = -1)
 {
+    if (count_hi < 0) count_hi = n;
     const int bins = k + 1;
     int copies = HIST_SMEM_WORDS / bins;
     if (copies > 32) copies = 32;
@@ -139,7 +148,8 @@ int launch_hist(const int32_t *labels, int64_t n, int32_t k, unsigned long long 
     const int64_t cap = (int64_t)gee::sm_count() * 4;
     const int grid = (int)(want < 1 ? 1 : (want > cap ? cap : want));
     k_label_hist<LT><<<grid, HIST_THREADS, sh, st>>>(labels, n, k, counts, static_cast<LT *>(table), hot_rank, n_hot,
-                                                     bad, copies, hot_bits, hot_pref, hot_list);
+                                                     bad, copies, hot_bits, hot_pref, hot_list,
+                                                     count_lo, count_hi);
     return gee::check_launch("k_label_hist");
 }
 
@@ -218,6 +228,45 @@ int gee_build_projection_hotc(const int32_t *labels, int64_t n, int32_t k, int64
         return gee::check_launch("k_inv");
     }
     return GEE_OK;
+}
+
+int gee_build_projection_sharded(const int32_t *labels, int64_t n, int32_t k, int64_t *counts, void *table,
+                                 const uint32_t *hot_bits, const int32_t *hot_pref, const int32_t *hot_list,
+                                 int64_t n_hot, int64_t count_lo, int64_t count_hi, int64_t *bad, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(k >= 1, GEE_ERR_INVALID, "class count k must be positive (got %d)", k);
+    GEE_REQUIRE(n >= 0 && n_hot >= 0, GEE_ERR_INVALID, "n and n_hot must be nonnegative");
+    GEE_REQUIRE(n + n_hot < INT32_MAX, GEE_ERR_INVALID, "label table exceeds int32 slots");
+    GEE_REQUIRE(counts != nullptr && table != nullptr, GEE_ERR_INVALID, "counts and table must not be NULL");
+    GEE_REQUIRE(n == 0 || labels != nullptr, GEE_ERR_INVALID, "labels must not be NULL");
+    GEE_REQUIRE(0 <= count_lo && count_lo <= count_hi && count_hi <= n, GEE_ERR_INVALID,
+                "count range [%lld, %lld) outside [0, %lld]", (long long)count_lo, (long long)count_hi, (long long)n);
+    GEE_REQUIRE(n_hot == 0 || (hot_bits && hot_pref && hot_list), GEE_ERR_INVALID,
+                "n_hot > 0 needs the compact hot tier (bitmap, prefix, rank list)");
+    cudaStream_t st = gee::as_stream(stream);
+    GEE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t)(k + 1), st));
+    if (bad) GEE_CUDA(cudaMemsetAsync(bad, 0, sizeof(int64_t), st));
+    auto *cnt = reinterpret_cast<unsigned long long *>(counts);
+    auto *nb = reinterpret_cast<unsigned long long *>(bad);
+    const uint32_t *hb = n_hot ? hot_bits : nullptr;
+    switch (gee_label_bytes(k)) {
+    case 1: return launch_hist<uint8_t>(labels, n, k, cnt, table, nullptr, n_hot, nb, st, hb, hot_pref, hot_list,
+                                        count_lo, count_hi);
+    case 2: return launch_hist<uint16_t>(labels, n, k, cnt, table, nullptr, n_hot, nb, st, hb, hot_pref, hot_list,
+                                         count_lo, count_hi);
+    default: return launch_hist<int32_t>(labels, n, k, cnt, table, nullptr, n_hot, nb, st, hb, hot_pref, hot_list,
+                                         count_lo, count_hi);
+    }
+}
+
+int gee_projection_inv(const int64_t *counts, int32_t k, float *inv_f32, double *inv_f64, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(k >= 1 && counts != nullptr, GEE_ERR_INVALID, "counts must not be NULL and k positive");
+    k_inv<<<(k + 1 + 255) / 256, 256, 0, gee::as_stream(stream)>>>(
+        reinterpret_cast<const unsigned long long *>(counts), k, inv_f32, inv_f64);
+    return gee::check_launch("k_inv");
 }
 
 }  // extern "C"

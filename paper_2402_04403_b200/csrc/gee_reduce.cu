@@ -129,6 +129,45 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Bulk-copy ring (Blackwell TMA unit): one elected lane per warp moves a
+// round's class bytes and weights with two cp.async.bulk copies that
+// complete_tx on the slot's mbarrier; the warp's lanes wait on the barrier's
+// phase.  The copies bypass the LSU / L1TEX load path that the shared
+// atomics saturate (the LDGSTS ring issued 96 lane copies per round).
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 // Per-block view shared by the warp (uniform fields) and per lane.
 struct RingBlk {
     int64_t base, bend;      // arc range of the block
@@ -209,6 +248,28 @@ __device__ __forceinline__ void ring_issue(uint8_t *ring, int slot, int64_t e, i
     cp_commit();
 }
 
+// One round [e, e + BROUND) into ring slot `slot` by lane 0 (nothing when
+// e >= bend).  e is a multiple of 16 (heavy items start their rounds at
+// 256-arc boundaries, so class addresses are 16-byte aligned); the class stream is allocated
+// with at least 64 bytes of slack, so a short last round may read the class
+// bytes up to the next multiple of 16.  `arcs` is a multiple of 8 (padded
+// rows), so the weights of a short round are a multiple of 32 bytes.
+template <bool WEIGHTED>
+__device__ __forceinline__ void ring_issue_bulk(uint8_t *ring, uint64_t *bars, int slot, int64_t e, int64_t bend,
+                                                int64_t arcs, const uint8_t *__restrict__ cls,
+                                                const float *__restrict__ w, int lane, uint64_t pol)
+{
+    if (lane != 0 || e >= bend) return;
+    constexpr int RSLOT = RING_CLS + (WEIGHTED ? RING_W : 0);
+    uint8_t *rs = ring + slot * RSLOT;
+    const int64_t na = arcs - e < BROUND ? arcs - e : BROUND;
+    const uint32_t cb = (uint32_t)((na + 15) & ~(int64_t)15);
+    const uint32_t wb = WEIGHTED ? (uint32_t)(na * 4) : 0u;
+    mbar_expect_tx(bars + slot, cb + wb);
+    bulk_g2s(rs, cls + e, cb, bars + slot, pol);
+    if (WEIGHTED) bulk_g2s(rs + RING_CLS, w + e, wb, bars + slot, pol);
+}
+
 template <bool WEIGHTED>
 __global__ void __launch_bounds__(RT, 2)
 k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
@@ -222,7 +283,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
     const int wwords = hoff * Acc<WEIGHTED>::planes;
     constexpr int RSLOT = RING_CLS + (WEIGHTED ? RING_W : 0);
     uint8_t *ring_base = smem_raw;  // RW x RING x RSLOT (16-byte aligned)
-    float *sc1 = reinterpret_cast<float *>(smem_raw + RW * RING * RSLOT);
+    float *sc1 = reinterpret_cast<float *>(ring_base + RW * RING * RSLOT);
     int32_t *meta = reinterpret_cast<int32_t *>(sc1 + pkb);
     uint32_t *vbase = reinterpret_cast<uint32_t *>(meta + RW * BMETA);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -410,8 +471,14 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
     const int pkb = block_vec_words(kk);  // [3 pad | trash | bins 1..k | pad]
     constexpr int RSLOT = RING_CLS + (WEIGHTED ? RING_W : 0);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint8_t *ring = smem_raw + wid * RING * RSLOT;
-    float *sc1 = reinterpret_cast<float *>(smem_raw + RW * RING * RSLOT);  // sc1[c] = inv[c+1] * dscale
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw) + wid * RING;
+    uint8_t *ring_base = smem_raw + RW * RING * sizeof(uint64_t);
+    uint8_t *ring = ring_base + wid * RING * RSLOT;
+    float *sc1 = reinterpret_cast<float *>(ring_base + RW * RING * RSLOT);  // sc1[c] = inv[c+1] * dscale
+    if (lane < RING) mbar_init(bars + lane, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint64_t pol = policy_evict_first();
+    uint32_t ph = 0;
     // HCOPY private copies of the window per warp (lane groups of 32/HCOPY):
     // all lanes add into one row, so a single copy serialises on equal
     // classes; the copy stride (== 4 mod 32 words) puts copies on other banks
@@ -436,12 +503,14 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
         int64_t ep = b0 & ~(int64_t)(BROUND - 1);
 #pragma unroll
         for (int i = 0; i < RING; i++) {
-            ring_issue<WEIGHTED, false>(ring, i, ep, e1, arcs, cls, w, lane);
+            ring_issue_bulk<WEIGHTED>(ring, bars, i, ep, e1, arcs, cls, w, lane, pol);
             ep += BROUND;
         }
         int slot = 0;
         for (int64_t e0 = b0 & ~(int64_t)(BROUND - 1); e0 < e1; e0 += BROUND) {
-            cp_wait<RING - 1>();
+            if (lane == 0) mbar_wait(bars + slot, (ph >> slot) & 1u);
+            __syncwarp();
+            ph ^= 1u << slot;
             const uint8_t *rs = ring + slot * RSLOT;
             const uint2 ca = *reinterpret_cast<const uint2 *>(rs + lane * BU);
             float wa[BU];
@@ -467,7 +536,8 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
                     atomicAdd(p, 1u);
                 }
             }
-            ring_issue<WEIGHTED, false>(ring, slot, ep, e1, arcs, cls, w, lane);
+            __syncwarp();  // every lane has read the slot before it is refilled
+            ring_issue_bulk<WEIGHTED>(ring, bars, slot, ep, e1, arcs, cls, w, lane, pol);
             ep += BROUND;
             slot = slot + 1 == RING ? 0 : slot + 1;
             // fold the window into the 64-bit sums at each aligned window end
@@ -491,7 +561,6 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
                 __syncwarp();
             }
         }
-        cp_wait<0>();
         const int32_t slotm = item_slot[it];
         if (slotm < 0) {  // the row's only item: write its Z row
             float *zr = z + (int64_t)item_row[it] * kk;
@@ -625,7 +694,7 @@ int gee_reduce_heavy(const uint8_t *cls, const float *w, int64_t arcs, int32_t s
     const bool weighted = w != nullptr;
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
-    const size_t sh = (size_t)RW * RING * (RING_CLS + (weighted ? RING_W : 0)) +
+    const size_t sh = (size_t)RW * RING * (RING_CLS + (weighted ? RING_W : 0) + sizeof(uint64_t)) +
                       (size_t)block_vec_words(k) * sizeof(float) +
                       (size_t)RW * HCOPY * (block_vec_words(k) * (weighted ? 2 : 1) + 4) * sizeof(uint32_t);
     GEE_REQUIRE((reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0),

@@ -125,6 +125,19 @@ class DeviceGraph:
             g.src, g.dst, g.w = rows, tgt_d, w_d
         return g
 
+    def to_source_only_coo(self):
+        """Expose the symmetric (pull) CSR as a SOURCE_ONLY arc list for the
+        push: src = row of each arc, dst = its target.  Only before the hot
+        tier rewrites the targets into label-table slots."""
+        if self.hot_k is not None and self.hot_rank is not None:
+            raise ValidationError("the hot tier already rewrote the targets; build the push layout first")
+        arcs = int(self.targets.numel())
+        rows = torch.empty(arcs, dtype=torch.int32, device=self.device)
+        if arcs:
+            check(lib.gee_csr_rows(ptr(self.offsets), self.n, arcs, ptr(rows), _stream()), "gee_csr_rows")
+        self.src, self.dst, self.w, self.coo_source_only = rows, self.targets, self.weights, True
+        return self
+
     def _build_sym(self, src_d, dst_d, w_d, stable):
         n, s, dev = self.n, int(src_d.numel()), self.device
         self.offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
@@ -427,6 +440,29 @@ class Embedder:
             raise ValidationError(f"{int(self.bad.item())} labels outside [0, {self.k}]")
         return self.counts
 
+    def project_sharded(self, labels_d, g, count_lo, count_hi, reduce_counts):
+        """The histogram sharded over row-range ranks: the
+        label table still receives every label, but this rank counts only
+        nodes [count_lo, count_hi); ``reduce_counts(counts)`` sums the k+1
+        int64 counts over the ranks in place (one all-reduce), then inv."""
+        if labels_d.numel() != self.n:
+            raise ValidationError(f"graph has {self.n} nodes but labels have {labels_d.numel()}")
+        if g is not None and g.hot_rank is not None and getattr(g, "hot_bits", None) is None:
+            g.compact_hot()
+        compact = g is not None and getattr(g, "hot_bits", None) is not None and g.n_hot > 0
+        n_hot = g.n_hot if compact else 0
+        self._ensure_table(n_hot)
+        check(lib.gee_build_projection_sharded(
+            ptr(labels_d), self.n, self.k, ptr(self.counts), ptr(self.table), ptr(g.hot_bits) if compact else None,
+            ptr(g.hot_pref) if compact else None, ptr(g.hot_list) if compact else None, n_hot, int(count_lo),
+            int(count_hi), ptr(self.bad), _stream()), "gee_build_projection_sharded")
+        reduce_counts(self.counts)
+        check(lib.gee_projection_inv(ptr(self.counts), self.k, ptr(self.inv32), ptr(self.inv64), _stream()),
+              "gee_projection_inv")
+        self._mark("project", 2)
+        self.table_n_hot = n_hot
+        return self.counts
+
     # ------------------------------------------------------------------ K4
     def new_z(self):
         return torch.empty((self.n, self.k), dtype=torch.float32, device=self.device)
@@ -507,6 +543,7 @@ class Embedder:
         check(lib.gee_embed_coo(ptr(g.src), ptr(g.dst), ptr(g.w), int(g.src.numel()), ptr(self.table),
                                 self.table_n_hot, ptr(self.inv32), g.n, self.k, ptr(z), flags, _stream()),
               "gee_embed_coo")
+        self._mark("push", 2 if zero else 1)
         return z
 
     def embed(self, g: DeviceGraph, labels_d, variant="auto", z=None, validate=True, inv=None):

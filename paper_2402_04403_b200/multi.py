@@ -11,6 +11,7 @@ device (``devices`` shorter than ``shards``) run one after another on it,
 which is how the tests cover the N-shard path on a one-GPU box.
 """
 
+import logging
 import threading
 
 import numpy as np
@@ -18,6 +19,8 @@ import numpy as np
 from .errors import ValidationError
 from .graph import CsrGraph, EdgeList, _is_torch
 from .labeling import LabelVector
+
+logger = logging.getLogger(__name__)
 
 
 def _shard_from_edges(el, n, shards, i, k, dev):
@@ -108,11 +111,8 @@ class ShardedPass:
                     g, lo, hi = _shard_from_symmetric_csr(graph, bounds, i, dev)
                 else:
                     g, lo, hi = _shard_from_edges(graph, n, shards, i, k, dev)
-                emb = Embedder(n, k, dev)
-                g.prepare_hot(k)
-                emb.project(lab, g=g)  # validates the labels once
                 z = torch.empty((hi - lo, k), dtype=torch.float32, device=dev)
-                self.parts[i] = (g, emb, lab, z, lo, hi)
+                self.parts[i] = (g, Embedder(n, k, dev), lab, z, lo, hi)
             torch.cuda.synchronize(dev)
 
         self._each_device(prep)
@@ -121,6 +121,31 @@ class ShardedPass:
         stats = merge_weight_stats(p[0].weight_stats() for p in self.parts.values())
         for p in self.parts.values():
             p[0].adopt_scale(stats)
+        # the merged weight range can fail the exact pull's fixed-point gate
+        # even when no single shard does: then every shard pushes its own
+        # rows' arcs (SOURCE_ONLY over the row shard, fp32 atomics into its
+        # own Z rows; still no cross-device traffic)
+        from .device import PULL_REL_ERR_MAX
+
+        worst = max((p[0].rel_err for p in self.parts.values() if p[0].weighted), default=0.0)
+        self.variant = "push" if worst > PULL_REL_ERR_MAX else "pull"
+        if self.variant == "push":
+            logger.warning("weights span too wide a range for the exact fixed-point pull over the whole graph "
+                           "(rounding bound %.2e): the row shards run the push variant", worst)
+
+        def finish(dev, mine):
+            torch.cuda.set_device(dev)
+            for i in mine:
+                g, emb, lab, z, lo, hi = self.parts[i]
+                if self.variant == "push":
+                    g.to_source_only_coo()
+                    emb.project(lab)  # validates the labels once
+                else:
+                    g.prepare_hot(k)
+                    emb.project(lab, g=g)  # validates the labels once
+            torch.cuda.synchronize(dev)
+
+        self._each_device(finish)
 
     def _each_device(self, fn):
         errors = []
@@ -154,8 +179,12 @@ class ShardedPass:
             a.record(stream)
             for i in mine:
                 g, emb, lab, z, _, _ = self.parts[i]
-                emb.project(lab, validate=False, g=g)
-                emb.pull(g, z)
+                if self.variant == "push":
+                    emb.project(lab, validate=False)
+                    emb.push(g, z)
+                else:
+                    emb.project(lab, validate=False, g=g)
+                    emb.pull(g, z)
             b.record(stream)
             b.synchronize()
             elapsed[dev] = a.elapsed_time(b)

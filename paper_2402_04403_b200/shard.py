@@ -106,6 +106,22 @@ def unify_scale_distributed(g, group=None):
     g.adopt_scale((float(hi[0]), float(hi[1]), 0.0 if mn_all == float("inf") else mn_all))
 
 
+def label_slice(n, world, rank):
+    """[lo, hi): the nodes whose labels this rank counts in the sharded
+    histogram (contiguous, n/world each)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValidationError("rank outside [0, world)")
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def allreduce_counts(counts, group=None):
+    """Sum the per-rank class counts (k+1 int64) over the ranks, in place."""
+    import torch.distributed as dist
+
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    return counts
+
+
 def reduce_scatter_rows(z_partial, world, group=None):
     """Edge-range combine: sum the (n, k) partials across ranks and return
     this rank's contiguous row slice (rows padded to a multiple of world)."""

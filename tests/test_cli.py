@@ -219,3 +219,80 @@ def test_bench_sweep_writes_report(tmp_path, capsys):
                     "--reps", "3", "--out", str(out)]) == 0
     assert len((out / "results.csv").read_text().splitlines()) == 3
     assert "linear fit" in capsys.readouterr().out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("as_csr", [False, True])
+def test_sharded_pass_wide_weight_range_falls_back_to_push(tmp_path, as_csr):
+    """Weights whose merged range fails the exact pull's fixed-point gate:
+    the row shards push their own rows (SOURCE_ONLY) instead of raising;
+    Z matches the f64 oracle within the push tolerance, and the CLI's
+    `embed --gpus 2` runs on such a graph."""
+    import oracle
+
+    from paper_2402_04403_b200.multi import ShardedPass
+
+    rng = np.random.default_rng(33)
+    n, s, k = 4000, 50_000, 7
+    src = (rng.zipf(1.6, s) % n).astype(np.int32)
+    dst = rng.integers(0, n, s).astype(np.int32)
+    w = (1 - rng.random(s)).astype(np.float32)
+    w[::97] = 1e-12  # one shard alone may pass the gate; the whole graph does not
+    el = gb.EdgeList(n=n, src=src, dst=dst, w=w, directed=True)
+    y = gb.LabelVector(labels=rng.integers(0, k + 1, n), k=k)
+    exp = oracle.serial_embed(src, dst, w, y.labels, n, k)
+    graph = gb.build_csr(el) if as_csr else el
+    sp = ShardedPass(graph, y, 2, devices=[0])
+    assert sp.variant == "push"
+    sp.run()
+    z = sp.gather()
+    nz = exp != 0
+    assert np.all(z[~nz] == 0)
+    assert np.max(np.abs(z[nz] - exp[nz]) / np.abs(exp[nz])) <= 1e-4
+    import torch
+
+    if torch.cuda.device_count() >= 2:  # the CLI places one shard per visible GPU
+        edges, labels, out = tmp_path / "wide.txt", tmp_path / "y.txt", tmp_path / "z.bin"
+        gb.write_edge_list(el, edges)
+        gb.write_labels(y, labels)
+        assert run_cli(["embed", "--graph", str(edges), "--labels", str(labels), "--k", str(k), "--weighted",
+                        "--directed", "--gpus", "2", "--out", str(out), "--format", "binary"]) == 0
+
+
+@pytest.mark.gpu
+def test_sharded_histogram_kernel_sums_to_full_projection():
+    """gee_build_projection_sharded: per-rank label slices' counts sum to
+    the full histogram and every rank's label table equals the replicated
+    one (bench.py's row-range run)."""
+    import torch
+
+    from paper_2402_04403_b200 import synth
+    from paper_2402_04403_b200.device import DeviceGraph, Embedder
+    from paper_2402_04403_b200.shard import label_slice
+
+    scale, s, k = 15, 300_000, 50
+    n = 1 << scale
+    src, dst, w = synth.rmat_edges(scale, s, seed=2, weighted=True, device="cuda")
+    y = synth.uniform_labels(n, k, seed=2, device="cuda")
+    y[::11] = 0
+    g = DeviceGraph.from_edges(src, dst, w, n, pull=True)
+    g.prepare_hot(k, enable=True)
+    full = Embedder(n, k)
+    full.project(y, g=g)
+    ref_counts, ref_table, ref_inv = full.counts.clone(), full.table.clone(), full.inv64.clone()
+    for world in (2, 3):
+        tot = torch.zeros_like(ref_counts)
+        for rank in range(world):
+            emb = Embedder(n, k)
+            lo, hi = label_slice(n, world, rank)
+            parts = []
+            emb.project_sharded(y, g, lo, hi, lambda c: parts.append(c.clone()))
+            tot += parts[0]
+            used = g.n_hot + n + 1  # the rest is alignment padding
+            assert torch.equal(emb.table[:used], ref_table[:used])
+        assert torch.equal(tot, ref_counts)
+    emb = Embedder(n, k)
+    emb.project_sharded(y, g, 0, n, lambda c: c)
+    assert torch.equal(emb.counts, ref_counts) and torch.equal(emb.inv64, ref_inv)
+    z = emb.pull(g)
+    assert torch.equal(z, full.pull(g))

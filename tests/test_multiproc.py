@@ -129,3 +129,44 @@ def test_plan_rows_balances_cost():
         row_max = int(np.max(np.diff(off))) * 8 + 4 * k
         assert per.max() - per.min() <= 2 * row_max
     assert list(shard.plan_edges(10, 4)) == [0, 2, 5, 7, 10]
+
+
+def _hist_worker(rank, port, q):
+    # sharded histogram (bench.py row-range run): each rank counts its
+    # contiguous n/world slice of the labels, one all-reduce of k+1 int64
+    # gives np.bincount of the whole vector on every rank
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        rng = np.random.default_rng(5)
+        n, k = 10_007, 13
+        y = rng.integers(0, k + 1, n)
+        lo, hi = shard.label_slice(n, WORLD, rank)
+        counts = torch.from_numpy(oracle.bincount(y[lo:hi], k))
+        shard.allreduce_counts(counts)
+        assert np.array_equal(counts.numpy(), np.bincount(y, minlength=k + 1))
+        spans = [torch.zeros(2, dtype=torch.int64) for _ in range(WORLD)]
+        dist.all_gather(spans, torch.tensor([lo, hi]))
+        assert spans[0][0] == 0 and spans[-1][1] == n
+        assert all(int(spans[i][1]) == int(spans[i + 1][0]) for i in range(WORLD - 1))
+        q.put((rank, "ok", hi - lo))
+    except Exception as ex:  # pragma: no cover
+        q.put((rank, f"fail: {type(ex).__name__}: {ex}", 0))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_histogram_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hist_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = sorted(q.get(timeout=10) for _ in range(WORLD))
+    assert all(p.exitcode == 0 for p in procs), res
+    assert all(r[1] == "ok" for r in res), res
+    assert shard.label_slice(10, 4, 3) == (7, 10)

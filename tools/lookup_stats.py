@@ -37,6 +37,9 @@ sect8 = torch.zeros(2, dtype=torch.int64, device="cuda")
 sect6 = torch.zeros(2, dtype=torch.int64, device="cuda")
 chunk = 1 << 28
 TILES = (65536, 131072, 245760)
+EDGES_R = [0, 122880, 245760, 491520, 1 << 20, 1 << 22, 1 << 24]
+rank_hist = torch.zeros(2, len(EDGES_R) + 1, dtype=torch.int64, device="cuda")
+bounds_r = torch.tensor(EDGES_R[1:], device="cuda")
 segs = {T: 0 for T in TILES}
 for a in range(0, arcs - arcs % 32, chunk):
     b = min(arcs - arcs % 32, a + chunk)
@@ -47,6 +50,9 @@ for a in range(0, arcs - arcs % 32, chunk):
     tier = torch.where(t == sent, 0, torch.where(t < HEAD, 1, torch.where(t < g.n_hot, 2, 3)))
     cnt.view(-1).index_add_(0, hv * 4 + tier, torch.ones_like(t))
     miss = tier >= 2
+    bk = torch.where(tier == 0, torch.full_like(t, len(EDGES_R)), torch.bucketize(t, bounds_r, right=True))
+    bk = torch.where((tier == 3), torch.full_like(t, len(EDGES_R) - 1), bk)
+    rank_hist.view(-1).index_add_(0, hv * (len(EDGES_R) + 1) + bk, torch.ones_like(t))
     for table, div in ((sect8, 32), (sect6, 40)):
         s = torch.where(miss, t // div, torch.full_like(t, -1)).view(-1, 32)
         s, _ = torch.sort(s, dim=1)
@@ -71,4 +77,7 @@ for hv, lab in ((0, "light"), (1, "heavy")):
     out[lab]["l2_sectors_6bit"] = int(sect6[hv])
 for T in TILES:
     out[f"heavy_hot_segments_T{T}"] = segs[T]
+labels_r = [f"<{b}" for b in EDGES_R[1:]] + ["cold", "pad"]
+for hv, lab in ((0, "light"), (1, "heavy")):
+    out[lab + "_by_rank"] = {labels_r[i]: int(rank_hist[hv, i]) for i in range(len(labels_r))}
 print(json.dumps(out, indent=1))
