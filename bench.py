@@ -530,7 +530,7 @@ def main():
 
     # warm-up (also validates labels once); the hot-label tier is graph prep
     t0 = time.perf_counter()
-    g.prepare_hot(k, keep_unsplit=world > 1 and not args.no_e2e)
+    g.prepare_hot(k)
     if world > 1:  # every rank rounds weights with the whole graph's exponent
         from paper_2402_04403_b200.shard import unify_scale_distributed
 
@@ -590,10 +590,7 @@ def main():
         # labels in, label table out; the compact hot tier (bitmap + prefix
         # per 32 vertices, ranks of the hot ones) in, their labels out again
         "project": 4 * rows + lb * rows + (rows // 4 + 4 * g.n_hot + lb * g.n_hot if g.n_hot else 0),
-        "gather": (g.light_arcs_real if g.split else arcs) * (4 + 1),
-        # two-region layout: the heavy rows' targets in, their classes out
-        # (lookups in shared-memory tiles; per-run descriptors 12 B)
-        "gather_heavy": ((arcs - g.light_arcs_real) * (4 + 1) + 12 * (g.tail_first + g.n_tails)) if g.split else 0,
+        "gather": arcs * (4 + 1),
         "blocks": 8 * (rows + 1) + light_arcs * (1 + 4 * weighted) + 4 * k * (rows - heavy_rows),
         "heavy": heavy_arcs * (1 + 4 * weighted) + 4 * k * heavy_rows,
         # wide K: label gather fused with the row windows (targets + weights
@@ -605,8 +602,7 @@ def main():
     # gee_gather_labels: packed shared-memory head of the hot tier, or
     # plain contiguous lookups without one
     gather_kernel = "k_gather_contig" if g.n_hot < 16384 else "k_gather_packed"
-    kernel_of = {"project": "k_label_hist", "gather": gather_kernel, "gather_heavy": "k_gather_tiles",
-                 "blocks": "k_reduce_blocks_ring",
+    kernel_of = {"project": "k_label_hist", "gather": gather_kernel, "blocks": "k_reduce_blocks_ring",
                  "heavy": "k_reduce_heavy_items", "wide": "k_wide_rows"}
     achieved = phase_bytes[dominant] / (phase_ms[dominant] * 1e-3) / 1e9
     step_bmin = s * (8 + 4 * weighted) + 4 * n + 4 * n * k  # SURVEY 8(d) B_min, whole graph
@@ -626,10 +622,7 @@ def main():
         "dtype": "f32 (exact integer fixed-point accumulation)" if weighted else "f32 (exact u32 counts)",
         "data": "synthetic (seeded R-MAT; Friendster unavailable)",
         "config": {"workload": workload, "n": n, "s_listed_edges": s, "k": k, "weighted": bool(weighted),
-                   "directed": bool(directed), "variant": "pull", "reducer": emb.reducer_for(g),
-                   "layout": (f"two-region (light {g.light_arcs} arcs | heavy {g.arcs - g.light_arcs} arcs; "
-                              f"{g.n_tiles} hot tiles of {g.tile} slots, {g.tail_first} runs, {g.n_tails} tails)")
-                   if g.split else "one-region", "sym_arcs": arcs,
+                   "directed": bool(directed), "variant": "pull", "reducer": emb.reducer_for(g), "sym_arcs": arcs,
                    "padded_arcs": g.arcs, "row_pad": g.padded,
                    "parallelism": f"row-range x{world}" if world > 1 else "single GPU",
                    "l2": "inputs (CSR %.1f GB) >> 126 MB L2; no flush needed" % (g.csr_bytes() / 1e9),

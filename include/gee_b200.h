@@ -282,46 +282,6 @@ int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls
                            int32_t scale_exp, const double *inv, int32_t k, int64_t heavy_arcs, float *z,
                            void *stream);
 
-/* Two-region layout (gee_split.cu, graph preparation DeviceGraph.split_heavy):
- * the heavy rows' arcs are relocated behind the light rows, so the block
- * reducer reads light-only offsets (heavy rows of length 0) and learns the
- * heavy rows from heavy_bits (u32 per 32 rows, bit r%32 of word r/32); it
- * does not write them (gee_reduce_heavy does). */
-int gee_reduce_blocks_split(const int64_t *light_offsets, int64_t n, const uint8_t *cls, const float *w,
-                            int32_t scale_exp, const double *inv, int32_t k, const uint32_t *heavy_bits, float *z,
-                            void *stream);
-
-/* Graph preparation of the two-region layout: copy row r's arcs
- * [offsets[r], offsets[r+1]) (targets, and weights unless NULL) to newpos[r]
- * of the output arrays. */
-int gee_split_relocate(const int64_t *offsets, const int64_t *newpos, int64_t n, const int32_t *targets,
-                       const float *weights, int32_t *out_targets, float *out_weights, void *stream);
-
-/* Graph preparation: the runs of heavy row h (arcs [hoff[h], hoff[h+1]) of a
- * slot-sorted layout) that fall into hot tile t = slots [t*tile, (t+1)*tile)
- * clipped to n_hot, split into pieces of at most 2048 arcs, and (t = n_tiles)
- * the row's cold tail (slots >= n_hot, row padding).  Pass 1 (out_start NULL)
- * writes the piece counts cnt[t * n_heavy + h]; pass 2 writes the pieces
- * (start arc, length) from base[t * n_heavy + h] (the exclusive scan of cnt). */
-int gee_split_runs(const int64_t *hoff, int64_t n_heavy, const int32_t *targets, int64_t n_hot, int64_t tile,
-                   int32_t n_tiles, int32_t *cnt, const int64_t *base, int64_t *out_start, int32_t *out_len,
-                   void *stream);
-
-/* Hot-tier slots per tile for `smem_bytes` of shared memory (6-bit labels 5
- * per word for k <= 63, bytes above). */
-int64_t gee_tile_slots(int32_t k, int64_t smem_bytes);
-
-/* Class stream of the heavy rows in the two-region layout (replaces
- * gee_gather_labels on them; same bytes, cls[e] = table[targets[e]]):
- * runs seg_off[t] .. seg_off[t+1] of tile t are looked up in shared memory
- * (one CTA per piece [piece[c], piece[c+1]) of the tile-major run list,
- * n_pieces CTAs, pieces balanced by arcs), then the n_tails cold-tail runs
- * from tail_first through L2.  k <= 255. */
-int gee_gather_heavy_tiled(const int32_t *targets, const void *table, int64_t n_hot, int32_t k, int64_t tile,
-                           int32_t n_tiles, const int64_t *seg_off, const int64_t *seg_start, const int32_t *seg_len,
-                           const int64_t *piece, int32_t n_pieces, int64_t tail_first, int64_t n_tails, uint8_t *cls,
-                           void *stream);
-
 /* Heavy rows (longer than the block reducer's heavy_arcs) as work items:
  * item i covers arcs [item_first[i], item_end[i]) of row item_row[i]
  * (cls / w hold `arcs` entries)

@@ -67,12 +67,6 @@ SIGNATURES = {
     "gee_pad_rows": (c_int, [vp, vp, c_i64, vp, vp, c_i32, vp, vp, vp]),
     "gee_sort_rows": (c_int, [vp, c_i64, vp, vp, vp]),
     "gee_reduce_blocks_pad8": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, vp]),
-    "gee_reduce_blocks_split": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, vp, vp, vp]),
-    "gee_split_relocate": (c_int, [vp, vp, c_i64, vp, vp, vp, vp, vp]),
-    "gee_split_runs": (c_int, [vp, c_i64, vp, c_i64, c_i64, c_i32, vp, vp, vp, vp, vp]),
-    "gee_tile_slots": (c_i64, [c_i32, c_i64]),
-    "gee_gather_heavy_tiled": (c_int, [vp, vp, c_i64, c_i32, c_i64, c_i32, vp, vp, vp, vp, c_i32, c_i64, c_i64, vp,
-                                       vp]),
     "gee_reduce_heavy": (c_int, [vp, vp, c_i64, c_i32, vp, c_i32, vp, vp, vp, vp, c_i64, vp, c_i64, vp, vp, vp, vp]),
     "gee_block_scale_exp": (c_int, [c_dbl, c_dbl, c_dbl, P_i32, P_dbl]),
     "gee_synth_word": (c_u64, [c_u64, c_u64, c_u64]),

@@ -176,16 +176,14 @@ struct RingBlk {
 };
 
 __device__ __forceinline__ RingBlk ring_open(int64_t r0, int64_t n, int64_t o_lo, int64_t o_hi31, int64_t heavy_arcs,
-                                             int lane, const uint32_t *__restrict__ heavy_bits)
+                                             int lane)
 {
     RingBlk B;
     int64_t o_hi = __shfl_down_sync(0xffffffffu, o_lo, 1);
     if (lane == 31) o_hi = o_hi31;
     const bool valid = r0 + lane < n;
     const int64_t d = valid ? o_hi - o_lo : 0;
-    // two-region layout (gee_split.cu): heavy rows have no arcs here and are
-    // marked in a bitmap word per 32-row block instead
-    const bool heavy = heavy_bits ? ((__ldg(heavy_bits + (r0 >> 5)) >> lane) & 1u) != 0u : d > heavy_arcs;
+    const bool heavy = d > heavy_arcs;
     B.nzm = __ballot_sync(0xffffffffu, d > 0 && !heavy);
     B.hvm = __ballot_sync(0xffffffffu, heavy);
     B.vm = __ballot_sync(0xffffffffu, valid);
@@ -276,8 +274,7 @@ template <bool WEIGHTED>
 __global__ void __launch_bounds__(RT, 2)
 k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
                      const float *__restrict__ w, float qscale, double dscale, const double *__restrict__ inv,
-                     int32_t k, int64_t heavy_arcs, int nslots, float *__restrict__ z,
-                     const uint32_t *__restrict__ heavy_bits)
+                     int32_t k, int64_t heavy_arcs, int nslots, float *__restrict__ z)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int kk = k;
@@ -313,7 +310,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         const int64_t r0 = 32 * b;
         const int64_t o_lo = __ldcs(offsets + min(r0 + lane, n));
         const int64_t o_31 = lane == 31 ? __ldcs(offsets + min(r0 + 32, n)) : 0;
-        B = ring_open(r0, n, o_lo, o_31, heavy_arcs, lane, heavy_bits);
+        B = ring_open(r0, n, o_lo, o_31, heavy_arcs, lane);
     }
     int64_t ep = ring_skip(B, B.base & ~(int64_t)(BU - 1), lane);  // next round to issue
 #pragma unroll
@@ -385,7 +382,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
             if (!last) {
                 ep = ring_skip(B, B.base & ~(int64_t)(BU - 1), lane);
             } else if (more) {
-                NB = ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane, heavy_bits);
+                NB = ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
                 opened = true;
                 ep = ring_skip(NB, NB.base & ~(int64_t)(BU - 1), lane);
             }
@@ -444,7 +441,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
             __syncwarp();
         }
         if (!more) break;
-        B = opened ? NB : ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane, heavy_bits);
+        B = opened ? NB : ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
     }
     cp_wait<0>();
 }
@@ -644,28 +641,8 @@ int gee_reduce_heavy_plan(const int64_t *offsets, int64_t n, int64_t heavy_arcs,
     return rc;
 }
 
-static int reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
-                         const double *inv, int32_t k, int64_t heavy_arcs, const uint32_t *heavy_bits, float *z,
-                         void *stream);
-
 int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
                            const double *inv, int32_t k, int64_t heavy_arcs, float *z, void *stream)
-{
-    return reduce_blocks(offsets, n, cls, w, scale_exp, inv, k, heavy_arcs, nullptr, z, stream);
-}
-
-int gee_reduce_blocks_split(const int64_t *light_offsets, int64_t n, const uint8_t *cls, const float *w,
-                            int32_t scale_exp, const double *inv, int32_t k, const uint32_t *heavy_bits, float *z,
-                            void *stream)
-{
-    gee::clear_error();
-    GEE_REQUIRE(heavy_bits != nullptr, GEE_ERR_INVALID, "heavy_bits must not be NULL");
-    return reduce_blocks(light_offsets, n, cls, w, scale_exp, inv, k, BLOCK_ROW_MAX, heavy_bits, z, stream);
-}
-
-static int reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
-                         const double *inv, int32_t k, int64_t heavy_arcs, const uint32_t *heavy_bits, float *z,
-                         void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs 1 <= k <= 255 (got %d)", k);
@@ -696,7 +673,7 @@ static int reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, 
     const int rgrid = (int)std::min<int64_t>((nblocks + RW - 1) / RW, (int64_t)gee::sm_count() * 2);
     auto kern = weighted ? k_reduce_blocks_ring<true> : k_reduce_blocks_ring<false>;
     GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shr));
-    kern<<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, ns, z, heavy_bits);
+    kern<<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, ns, z);
     return gee::check_launch("k_reduce_blocks_ring");
 }
 

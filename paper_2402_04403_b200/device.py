@@ -35,12 +35,6 @@ def _stream():
     return _lib.stream_handle()
 
 
-def gee_sm_count(device=None):
-    """SMs of the current (or given) device: one persistent CTA each."""
-    return torch.cuda.get_device_properties(device if device is not None else torch.cuda.current_device()
-                                            ).multi_processor_count
-
-
 class DeviceGraph:
     """A listed edge multiset resident in HBM, laid out for the edge pass.
 
@@ -77,8 +71,6 @@ class DeviceGraph:
         self._owns_targets = False
         self._owns_weights = False
         self.padded = 0  # rows padded to a multiple of this many arcs (0: not padded)
-        self.split = False  # two-region layout (split_heavy)
-        self.unsplit = None
         self.arcs_unpadded = None
 
     # ---------------------------------------------------------------- build
@@ -218,15 +210,11 @@ class DeviceGraph:
         # atomic order, which scatters both over 30 GB)
         rows = torch.sort(rows[:self.n_heavy])[0].contiguous()
         r64 = rows.to(torch.int64)
-        self._build_items(rows, self.offsets[r64], self.offsets[r64 + 1] - self.offsets[r64])
-
-    def _build_items(self, rows, first, deg):
-        """Work items of gee_reduce_heavy for heavy rows `rows` (int32,
-        ascending) whose arcs are [first, first + deg): runs of <=
-        HEAVY_ITEM_ARCS arcs; rows with several items ("mega" rows) combine
-        through acc + finalize."""
-        first, deg = first.cpu(), deg.cpu()
+        first = self.offsets[r64].cpu()
+        deg = (self.offsets[r64 + 1] - self.offsets[r64]).cpu()
         self.heavy_arc_total = int(deg.sum())
+        # work items of gee_reduce_heavy: runs of <= HEAVY_ITEM_ARCS arcs;
+        # rows with several items ("mega" rows) combine through acc + finalize
         nit = (deg + self.HEAVY_ITEM_ARCS - 1) // self.HEAVY_ITEM_ARCS
         it_row = torch.repeat_interleave(torch.arange(self.n_heavy), nit)
         it_j = torch.arange(int(nit.sum())) - torch.repeat_interleave(torch.cumsum(nit, 0) - nit, nit)
@@ -248,100 +236,6 @@ class DeviceGraph:
         self.n_mega = int(mega.sum())
         self.heavy_rows = rows
 
-    # Two-region layout (csrc/gee_split.cu): shared memory of one tiled-gather
-    # CTA (one per SM) holds a tile of the hot tier
-    SPLIT_SMEM = 192 * 1024
-
-    def split_heavy(self, k, tile=None, keep_unsplit=False):
-        """Relocate the heavy rows' arcs behind the light rows and list, per
-        hot tile, the heavy rows' runs in it (graph preparation for the
-        tiled gather, gee_split.cu).  Needs the padded, slot-sorted layout
-        with a hot tier and k <= 255; returns False (no change) otherwise.
-        keep_unsplit: keep the unsplit layout as ``self.unsplit`` (a view
-        graph for HostPipeline)."""
-        if self.split or not self.padded or self.n_hot == 0 or self.n_heavy == 0 or k > 255:
-            return False
-        import copy
-
-        if keep_unsplit:
-            self.unsplit = copy.copy(self)
-        dev, n = self.device, self.n
-        off = self.offsets
-        hrows = self.heavy_rows.to(torch.int64)
-        deg = off[1:] - off[:-1]
-        hdeg = deg[hrows]
-        ldeg = deg.clone()
-        ldeg[hrows] = 0
-        loff = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-        torch.cumsum(ldeg, 0, out=loff[1:])
-        light_arcs = int(loff[-1])
-        hoff = torch.empty(self.n_heavy + 1, dtype=torch.int64, device=dev)
-        hoff[0] = light_arcs
-        torch.cumsum(hdeg, 0, out=hoff[1:])
-        hoff[1:] += light_arcs
-        newpos = loff[:-1].clone()
-        newpos[hrows] = hoff[:-1]
-        del ldeg, deg
-        tgt = torch.empty_like(self.targets)
-        wts = torch.empty_like(self.weights) if self.weights is not None else None
-        check(lib.gee_split_relocate(ptr(off), ptr(newpos), n, ptr(self.targets), ptr(self.weights), ptr(tgt),
-                                     ptr(wts), _stream()), "gee_split_relocate")
-        del newpos
-        nw = (n + 31) // 32
-        hb = torch.zeros(nw * 32, dtype=torch.bool, device=dev)
-        hb[hrows] = True
-        hv = hb.view(nw, 32).to(torch.int64)
-        bits = (hv << torch.arange(32, device=dev, dtype=torch.int64)).sum(1)
-        self.heavy_bits = torch.where(bits >= 2**31, bits - 2**32, bits).to(torch.int32)
-        del hb, hv, bits
-        # runs of the heavy rows per hot tile, then the cold tails
-        tile = int(tile or lib.gee_tile_slots(k, self.SPLIT_SMEM))
-        per = 5 if k <= 63 else 4
-        tile -= tile % per
-        n_tiles = (self.n_hot + tile - 1) // tile
-        nh = self.n_heavy
-        cnt = torch.empty((n_tiles + 1) * nh, dtype=torch.int32, device=dev)
-        check(lib.gee_split_runs(ptr(hoff), nh, ptr(tgt), self.n_hot, tile, n_tiles, ptr(cnt), None, None, None,
-                                 _stream()), "gee_split_runs")
-        base = torch.zeros(cnt.numel() + 1, dtype=torch.int64, device=dev)
-        base[1:] = torch.cumsum(cnt.to(torch.int64), 0)
-        nseg = int(base[-1])
-        seg_start = torch.empty(max(nseg, 1), dtype=torch.int64, device=dev)
-        seg_len = torch.empty(max(nseg, 1), dtype=torch.int32, device=dev)
-        check(lib.gee_split_runs(ptr(hoff), nh, ptr(tgt), self.n_hot, tile, n_tiles, None, ptr(base), ptr(seg_start),
-                                 ptr(seg_len), _stream()), "gee_split_runs")
-        seg_off = base[torch.arange(0, n_tiles + 2, device=dev).clamp_(max=n_tiles + 1) * nh].contiguous()
-        seg_off[-1] = nseg
-        del cnt, base
-        tail_first = int(seg_off[n_tiles])
-        # pieces: the hot runs split into equal arc counts, one per SM
-        pieces = gee_sm_count()
-        cum = torch.cumsum(seg_len[:tail_first].to(torch.int64), 0)
-        total = int(cum[-1]) if tail_first else 0
-        want = torch.arange(1, pieces, device=dev, dtype=torch.int64) * total // pieces
-        piece = torch.zeros(pieces + 1, dtype=torch.int64, device=dev)
-        if tail_first:
-            piece[1:pieces] = torch.searchsorted(cum, want, right=True)
-        piece[pieces] = tail_first
-        del cum, want
-        sentinel = self.n_hot + self.n_nodes
-        real_light = 0
-        for a in range(0, light_arcs, 1 << 28):
-            real_light += int((tgt[a:min(light_arcs, a + (1 << 28))] != sentinel).sum())
-        self.offsets, self.targets, self.weights = loff, tgt, wts
-        self._owns_targets = self._owns_weights = True
-        self._build_items(self.heavy_rows, hoff[:-1], hdeg)
-        self.split = True
-        self.light_arcs, self.light_arcs_real = light_arcs, real_light
-        self.hoff = hoff
-        self.tile, self.n_tiles = tile, n_tiles
-        self.seg_off, self.seg_start, self.seg_len = seg_off, seg_start, seg_len
-        self.piece, self.n_pieces = piece, pieces
-        self.tail_first, self.n_tails = tail_first, nseg - tail_first
-        self.n_runs_hot = tail_first
-        torch.cuda.synchronize(dev)
-        return True
-
     # Hot-label tier (csrc/gee_hot.cu): worth it when the packed label array
     # outgrows what L2 keeps resident under random access and degrees are
     # skewed (R-MAT); ER graphs end up with few or no hot vertices.
@@ -353,10 +247,8 @@ class DeviceGraph:
     HOT_MAX = 16 << 20
     HOT_MIN_DEGREE = 1
 
-    def prepare_hot(self, k, enable=None, split=None, keep_unsplit=False):
-        """Plan the hot tier for k classes (once; rewrites the pull targets).
-        split: then move to the two-region layout (split_heavy; default: when
-        the hot tier exists, k <= 255 and there are heavy rows)."""
+    def prepare_hot(self, k, enable=None):
+        """Plan the hot tier for k classes (once; rewrites the pull targets)."""
         if self.hot_k == k or not self.has_pull:
             return
         if self.hot_k is not None:
@@ -396,8 +288,6 @@ class DeviceGraph:
         self.compact_hot()
         self._sort_rows()
         self._pad_rows()
-        if split is None or split:
-            self.split_heavy(k, keep_unsplit=keep_unsplit)
 
     def compact_hot(self):
         """hot_rank (int32 per vertex) -> hot_bits (u32 bitmap of the hot
@@ -602,10 +492,6 @@ class Embedder:
             raise ValidationError("label table does not match the graph's hot tier: call project(labels, g=graph)")
         if z is None:
             z = torch.empty((g.n, self.k), dtype=torch.float32, device=self.device)
-        if self.reducer_for(g, z) == "wide" and g.split:
-            if g.unsplit is None:
-                raise ValidationError("the two-region layout runs the block reducer: z must be 16-byte aligned")
-            g = g.unsplit
         if self.reducer_for(g, z) == "wide":
             check(lib.gee_reduce_wide(ptr(g.offsets), g.n, ptr(g.targets), ptr(g.weights), ptr(self.table), self.k,
                                       g.scale_exp, ptr(self.inv64), ptr(g.heavy_rows), g.n_heavy, ptr(z), _stream()),
@@ -617,27 +503,12 @@ class Embedder:
         # rows as work items)
         if self.cls is None or self.cls.numel() < g.arcs + 64:
             self.cls = torch.empty(g.arcs + 64, dtype=torch.uint8, device=self.device)
-        if g.split:
-            # two-region layout: the light region through the plain gather,
-            # the heavy rows through hot tiles staged in shared memory
-            check(lib.gee_gather_labels(ptr(g.targets), g.light_arcs, ptr(self.table), g.n_hot, self.k,
-                                        ptr(self.cls), _stream()), "gee_gather_labels")
-            self._mark("gather", 1)
-            check(lib.gee_gather_heavy_tiled(ptr(g.targets), ptr(self.table), g.n_hot, self.k, g.tile, g.n_tiles,
-                                             ptr(g.seg_off), ptr(g.seg_start), ptr(g.seg_len), ptr(g.piece),
-                                             g.n_pieces, g.tail_first, g.n_tails, ptr(self.cls), _stream()),
-                  "gee_gather_heavy_tiled")
-            self._mark("gather_heavy", (1 if g.n_pieces else 0) + (1 if g.n_tails else 0))
-            check(lib.gee_reduce_blocks_split(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                              ptr(self.inv64), self.k, ptr(g.heavy_bits), ptr(z), _stream()),
-                  "gee_reduce_blocks_split")
-        else:
-            check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
-                                        _stream()), "gee_gather_labels")
-            self._mark("gather", 1)
-            check(lib.gee_reduce_blocks_pad8(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                             ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(z), _stream()),
-                  "gee_reduce_blocks_pad8")
+        check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
+                                    _stream()), "gee_gather_labels")
+        self._mark("gather", 1)
+        check(lib.gee_reduce_blocks_pad8(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                         ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(z), _stream()),
+              "gee_reduce_blocks_pad8")
         self._mark("blocks", 1)
         if g.n_mega and (self.mega_acc is None or self.mega_acc.numel() < g.n_mega * self.k):
             self.mega_acc = torch.zeros(g.n_mega * self.k, dtype=torch.int64, device=self.device)

@@ -216,7 +216,7 @@ def prepare(g, k, *, device=None, residency="host", chunks=32, accounting=None):
             f"weights span too wide a range for the exact fixed-point pull (rounding bound {dg.rel_err:.2e}); "
             f"call embed_parallel(g, y) on the stored graph (push variant)")
     t0 = time.perf_counter()
-    dg.prepare_hot(k, split=residency == "device")
+    dg.prepare_hot(k)
     torch.cuda.synchronize(dev)
     p.prep_s["hot_sort_pad"] = time.perf_counter() - t0
     p._emb = Embedder(p.n, k, dev)

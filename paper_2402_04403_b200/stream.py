@@ -55,11 +55,6 @@ class HostPipeline:
     """Streams a prepared graph held in pinned host memory through one GPU."""
 
     def __init__(self, g: DeviceGraph, k, chunks=16, device=None, packed=None):
-        if getattr(g, "split", False):
-            if g.unsplit is None:
-                raise ValidationError("HostPipeline streams the one-region layout: prepare_hot(k, split=False) "
-                                      "or keep_unsplit=True")
-            g = g.unsplit
         if not g.has_pull or g.hot_k != k:
             raise ValidationError("HostPipeline needs a pull graph prepared for k (prepare_hot)")
         self.device = device or g.device

@@ -449,7 +449,7 @@ def test_signed_reducers_agree_bitwise(k, monkeypatch):
     dev = torch.device("cuda")
     g = DeviceGraph.from_edges(torch.from_numpy(src).int(), torch.from_numpy(dst).int(), torch.from_numpy(w), n,
                                device=dev, pull=True)
-    g.prepare_hot(k, enable=True, keep_unsplit=True)
+    g.prepare_hot(k, enable=True)
     assert g.n_heavy >= 1 and g.n_mega >= 1
     lab = torch.from_numpy(y.labels).to(dev)
     emb = Embedder(n, k, dev)
@@ -563,7 +563,7 @@ def test_host_pipeline_matches_resident_pull(chunks, packed):
     y = synth.uniform_labels(n, k, seed=42)
     dev = torch.device("cuda")
     g = DeviceGraph.from_edges(src, dst, w, n, device=dev, pull=True)
-    g.prepare_hot(k, enable=True, keep_unsplit=True)
+    g.prepare_hot(k, enable=True)
     emb = Embedder(n, k, dev)
     emb.project(y, g=g)
     z_ref = emb.pull(g).cpu()
@@ -893,7 +893,7 @@ def test_host_pipeline_unit_weights(k, labeled):
     y = torch.from_numpy(gb.random_labels(n, k, labeled, seed=k).labels).cuda()
     dev = torch.device("cuda")
     g = DeviceGraph.from_edges(src, dst, None, n, device=dev, pull=True)
-    g.prepare_hot(k, enable=True, keep_unsplit=True)
+    g.prepare_hot(k, enable=True)
     emb = Embedder(n, k, dev)
     emb.project(y, g=g)
     z_ref = emb.pull(g).cpu()
