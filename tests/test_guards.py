@@ -1,0 +1,123 @@
+"""Out-of-bounds writes and input corruption, checked without a sanitizer.
+
+compute-sanitizer is closed on the GPU pool (profiles/r02_sanitizer.txt), so
+every kernel family writes into outputs surrounded by poisoned guard rows
+(a NaN bit pattern the kernels never produce), and every read-only input is
+checksummed before and after: a stray store past an output or into an
+input fails here.  Each kernel's own result is checked against the oracle
+elsewhere; here it is also checked for run-to-run bit stability (pull)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2402_04403_b200 import synth  # noqa: E402
+from paper_2402_04403_b200.device import DeviceGraph, Embedder  # noqa: E402
+
+DEV = torch.device("cuda")
+POISON = 0x7FC0DEAD  # a quiet-NaN pattern no edge pass writes
+G = 64  # guard rows on each side
+
+
+def _guarded_z(n, k, device=DEV, pinned=False):
+    full = torch.full(((n + 2 * G) * k,), POISON, dtype=torch.int32, device=device)
+    if pinned:
+        full = full.pin_memory()
+    z = full[G * k:(G + n) * k].view(torch.float32).view(n, k)
+    assert z.data_ptr() % 16 == 0
+    return full, z
+
+
+def _guards_intact(full, n, k):
+    head, tail = full[:G * k], full[(G + n) * k:]
+    return bool((head == POISON).all()) and bool((tail == POISON).all())
+
+
+def _digest(*ts):
+    out = []
+    for t in ts:
+        if t is None:
+            out.append(None)
+        else:
+            v = t.reshape(-1).view(torch.uint8).to(torch.int64)
+            out.append((int(v.sum()), int((v * torch.arange(1, v.numel() + 1, device=v.device) % 1000003).sum())))
+    return out
+
+
+def _case(k, weighted, hub=6000, scale=15, s=250_000, seed=5):
+    src, dst, w = synth.rmat_edges(scale, s, seed=seed, weighted=weighted)
+    src[:hub] = 3  # a heavy row
+    n = 1 << scale
+    y = synth.uniform_labels(n, k, seed=seed)
+    return src, dst, w, y, n
+
+
+@pytest.mark.parametrize("k,weighted", [(50, True), (7, False), (300, True)])
+def test_pull_and_push_write_only_their_output(k, weighted):
+    src, dst, w, y, n = _case(k, weighted)
+    exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), None if w is None else w.cpu().numpy(),
+                              y.cpu().numpy(), n, k)
+    g = DeviceGraph.from_edges(src, dst, w, n, pull=True, keep_coo=True)
+    g.prepare_hot(k, enable=k <= 255)
+    assert g.n_heavy > 0
+    inputs = (g.offsets, g.targets, g.weights, y, src, dst, w)
+    before = _digest(*inputs)
+    emb = Embedder(n, k)
+    emb.project(y, g=g)
+    full, z = _guarded_z(n, k)
+    emb.pull(g, z)
+    assert _guards_intact(full, n, k), "pull wrote outside Z"
+    z1 = z.clone()
+    emb.pull(g, z)
+    assert torch.equal(z1, z), "pull is not bit-stable"
+    assert rel_err(z.cpu().numpy(), exp) <= 1e-4
+    full2, zp = _guarded_z(n, k)
+    emb.push(g, zp)
+    assert _guards_intact(full2, n, k), "push wrote outside Z"
+    assert rel_err(zp.cpu().numpy(), exp) <= 1e-4
+    assert _digest(*inputs) == before, "an edge pass modified its inputs"
+
+
+def test_streamed_pass_writes_only_the_callers_rows():
+    from paper_2402_04403_b200.stream import HostPipeline
+
+    k = 50
+    src, dst, w, y, n = _case(k, True, scale=16, s=600_000)
+    g = DeviceGraph.from_edges(src, dst, w, n, pull=True)
+    g.prepare_hot(k, enable=True)
+    emb = Embedder(n, k)
+    emb.project(y, g=g)
+    ref = emb.pull(g).cpu()
+    pipe = HostPipeline(g, k, chunks=5)
+    full, h_z = _guarded_z(n, k, device="cpu", pinned=True)
+    h_y = y.cpu().pin_memory()
+    y_before = h_y.clone()
+    for sparse in (True, False):
+        pipe.run(h_y, h_z, emb, sparse=sparse)
+        assert _guards_intact(full, n, k), f"streamed pass wrote outside Z (sparse={sparse})"
+        assert torch.equal(h_z, ref)
+    assert torch.equal(h_y, y_before)
+
+
+def test_projection_table_and_counts_stay_in_bounds():
+    # the label table is written for exactly n_hot + n + 1 slots; poison the
+    # allocation's slack and check it survives
+    k = 50
+    src, dst, w, y, n = _case(k, True)
+    g = DeviceGraph.from_edges(src, dst, w, n, pull=True)
+    g.prepare_hot(k, enable=True)
+    emb = Embedder(n, k)
+    emb._ensure_table(g.n_hot)
+    used = g.n_hot + n + 1
+    emb.table[used:] = 0xA5
+    slack = emb.table[used:].clone()
+    emb.project(y, g=g)
+    assert torch.equal(emb.table[used:], slack)
+    assert np.array_equal(emb.counts.cpu().numpy(), np.bincount(y.cpu().numpy(), minlength=k + 1))
