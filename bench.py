@@ -631,6 +631,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                      "frac": achieved / peak_gbs, "traffic": load_traffic(workload, kernel_of[dominant]) if world == 1 else None,
                      "kernel": kernel_of[dominant], "peak_kind": peak_kind,
+                     "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the committed "
+                                       "ncu --set full capture of the same command (profiles/ncu_traffic.json)",
                      "algorithmic_bytes_per_launch": phase_bytes[dominant],
                      "kernel_ms": phase_ms[dominant], "step_bmin_bytes": step_bmin,
                      "step_frac": step_bmin / (ms_step * 1e-3) / 1e9 / (peak_gbs * world),
