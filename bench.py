@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-push", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="also time the step replayed as one CUDA graph (Embedder.capture; launch-bound configs)")
     return ap.parse_args()
 
 
@@ -642,6 +644,24 @@ def main():
         "clocks": clk,
         "gpu_launches": launches,
     }
+
+    # ---- the same step recorded as a CUDA graph (one host launch per step)
+    if args.graph and world == 1:
+        zg = torch.empty_like(z)
+        graph = emb.capture(g, y, zg)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        gms = a.elapsed_time(b) / args.steps
+        result["cuda_graph"] = {"ms_per_step": gms, "value": s / (gms * 1e-3) / 1e9,
+                                "matches_eager": bool(torch.equal(zg, z))}
+        del graph, zg
 
     # ---- variant measurement: push on the same graph (chosen by measurement)
     if world == 1 and g.has_push and not args.no_push:

@@ -247,6 +247,10 @@ int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t group
                        const uint8_t *wpayload, int32_t sentinel, int32_t *targets, float *w_padded, void *scratch,
                        size_t scratch_bytes, void *stream);
 
+/* Chunk-relative CSR offsets travel host -> device as int32 (half the
+ * bytes); widen them to the int64 the pull reads (stream-ordered). */
+int gee_widen_offsets(const int32_t *in, int64_t count, int64_t *out, void *stream);
+
 /* Class stream: cls[e] = table[targets[e]] (u8, k <= 255) for every arc of
  * a pull layout -- the random half of the pull pass (the hottest label-table
  * slots staged in a packed shared-memory head of head_bytes, -1 = the tuned

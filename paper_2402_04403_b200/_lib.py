@@ -55,6 +55,7 @@ SIGNATURES = {
     "gee_hot_encode": (c_int, [vp, c_i64, vp, c_i64, vp]),
     "gee_gather_labels": (c_int, [vp, c_i64, vp, c_i64, c_i32, vp, vp]),
     "gee_gather_labels_head": (c_int, [vp, c_i64, vp, c_i64, c_i32, c_i64, vp, vp]),
+    "gee_widen_offsets": (c_int, [vp, c_i64, vp, vp]),
     "gee_zc_blocks": (c_i64, [c_i64]),
     "gee_z_compact": (c_int, [vp, c_i64, c_i32, vp, vp, vp, vp]),
     "gee_unpack_scratch_bytes": (c_size, [c_i64]),

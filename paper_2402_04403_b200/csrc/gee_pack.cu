@@ -268,6 +268,12 @@ size_t cub_scan_bytes(int64_t groups)
 
 inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+__global__ void k_widen_offsets(const int32_t *__restrict__ in, int64_t count, int64_t *__restrict__ out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)__ldcs(in + i);
+}
+
 }  // namespace
 
 extern "C" {
@@ -381,6 +387,18 @@ int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t group
     k_unpack_rows<<<grid_of(groups), PT, 0, st>>>(ctl, payload, groups, pos, seg, wctl, wpayload, (uint32_t)sentinel,
                                                   targets, wctl ? w_padded : nullptr);
     return gee::check_launch("k_unpack_rows");
+}
+
+int gee_widen_offsets(const int32_t *in, int64_t count, int64_t *out, void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(count >= 0, GEE_ERR_INVALID, "count must be nonnegative");
+    if (count == 0) return GEE_OK;
+    GEE_REQUIRE(in && out, GEE_ERR_INVALID, "NULL array argument");
+    int64_t grid = (count + 255) / 256;
+    if (grid > (int64_t)gee::sm_count() * 8) grid = (int64_t)gee::sm_count() * 8;
+    k_widen_offsets<<<(int)grid, 256, 0, gee::as_stream(stream)>>>(in, count, out);
+    return gee::check_launch("k_widen_offsets");
 }
 
 }  // extern "C"

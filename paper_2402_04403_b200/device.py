@@ -555,6 +555,28 @@ class Embedder:
         return self.pull(g, z) if v == "pull" else self.push(g, z)
 
 
+    def capture(self, g: DeviceGraph, labels_d, z, variant="pull"):
+        """Record one edge pass (histogram + the edge map into z) as a CUDA
+        graph; ``graph.replay()`` then re-runs it on the current contents of
+        ``labels_d`` with one launch from the host.  Worth it where launches
+        dominate (C1: 140K edges, six kernels); the buffers stay bound to the
+        graph.  The pass runs once eagerly first (kernel attributes, scratch
+        sizing, label validation)."""
+        v = choose_variant(g, variant)
+        if v == "pull":
+            g.prepare_hot(self.k)
+        self.project(labels_d, validate=True, g=g if v == "pull" else None)
+        (self.pull if v == "pull" else self.push)(g, z)
+        if g.n_mega and self.mega_acc is None:
+            self.mega_acc = torch.zeros(g.n_mega * self.k, dtype=torch.int64, device=self.device)
+        torch.cuda.synchronize(self.device)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.project(labels_d, validate=False, g=g if v == "pull" else None)
+            (self.pull if v == "pull" else self.push)(g, z)
+        return graph
+
+
 def choose_variant(g: DeviceGraph, variant="auto"):
     """Pull wherever its layout exists and its fixed point is exact enough.
 

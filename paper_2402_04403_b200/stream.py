@@ -282,8 +282,9 @@ class HostPipeline:
                     _lib.ptr(self.d_wpay[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
                     _lib.ptr(self.d_w[b]) if self.weighted else None, _lib.ptr(self.d_scratch),
                     self.scratch_bytes, _lib.stream_handle(self.s_cmp)), "gee_unpack_targets")
-            if self.h_off[i].dtype == torch.int32:
-                self.d_off[b][:hi - lo + 1].copy_(self.d_off32[b][:hi - lo + 1])  # widen on the device
+            if self.h_off[i].dtype == torch.int32:  # widen on the device
+                _lib.check(_lib.lib.gee_widen_offsets(_lib.ptr(self.d_off32[b]), hi - lo + 1, _lib.ptr(self.d_off[b]),
+                                                      _lib.stream_handle(self.s_cmp)), "gee_widen_offsets")
             v.offsets = self.d_off[b][:hi - lo + 1]
             v.targets = self.d_tgt[b][:a1 - a0]
             v.weights = self.d_w[b][:a1 - a0] if self.weighted else None

@@ -976,3 +976,27 @@ def test_variant_policy_and_gate_warning(golden, caplog):
     assert rel_err(z, exp) <= TOL
     with pytest.raises(gb.ValidationError, match="push"):
         gb.embed_serial(wide, y, variant="pull")
+
+
+@pytest.mark.parametrize("variant", ["pull", "push"])
+def test_captured_pass_replays_on_new_labels(variant):
+    # one edge pass recorded as a CUDA graph (Embedder.capture): replaying
+    # it after the labels change gives the eager result for the new labels
+    scale, s, k = 14, 200_000, 5
+    n = 1 << scale
+    src, dst, w = synth.rmat_edges(scale, s, seed=61, weighted=True)
+    g = DeviceGraph.from_edges(src, dst, w, n, pull=True, keep_coo=True)
+    emb = Embedder(n, k)
+    y = synth.uniform_labels(n, k, seed=61)
+    z = torch.empty((n, k), dtype=torch.float32, device="cuda")
+    graph = emb.capture(g, y, z, variant=variant)
+    for seed in (62, 63):
+        y.copy_(synth.uniform_labels(n, k, seed=seed))
+        z.fill_(float("nan"))
+        graph.replay()
+        torch.cuda.synchronize()
+        ref = Embedder(n, k).embed(g, y, variant=variant)
+        if variant == "pull":
+            assert torch.equal(z, ref)
+        else:
+            assert rel_err(z.cpu().numpy(), ref.cpu().numpy().astype(np.float64)) <= TOL

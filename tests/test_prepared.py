@@ -108,3 +108,21 @@ def test_prepared_projection_and_errors():
     wide[0] = 1e-30
     with pytest.raises(ValidationError, match="push"):
         prepare(_csr(src, dst, wide, n, True), k)
+
+
+def test_device_residency_replays_one_graph_over_label_sets():
+    # residency="device" records the pass as a CUDA graph on the first call
+    # and replays it: every later call equals the stored graph's own pass
+    n, k = 3000, 11
+    src, dst, w = _graph(31, n=n)
+    g = _csr(src, dst, w, n, True)
+    p = prepare(g, k, residency="device")
+    rng = np.random.default_rng(32)
+    for i in range(3):
+        y = LabelVector(labels=rng.integers(0, k + 1, n), k=k)
+        z = embed_parallel(p, y)
+        assert np.array_equal(z, embed_parallel(g, y, variant="pull")), i
+    assert p._graph is not None
+    yd = LabelVector(labels=torch.as_tensor(rng.integers(0, k + 1, n), device="cuda"), k=k)
+    zd = embed_parallel(p, yd)
+    assert zd.is_cuda and torch.equal(zd, embed_parallel(p, yd))
