@@ -209,6 +209,20 @@ __device__ __forceinline__ int64_t ring_skip(const RingBlk &B, int64_t e, int la
     return e;
 }
 
+// Arc span [lo, hi) of pass p0 (the nonempty light rows of ranks p0 ..
+// p0 + nslots - 1): a block whose rows need several passes streams each
+// pass's own arcs instead of the whole block again (C2: every block has 32
+// nonempty rows for ~19 slots).  Rows are padded, so the bounds stay
+// multiples of 8 arcs.  Warp-uniform.
+__device__ __forceinline__ void pass_span(const RingBlk &B, int p0, int nslots, int64_t &lo, int64_t &hi)
+{
+    const int nnz = __popc(B.nzm);
+    lo = B.base & ~(int64_t)(BU - 1);
+    hi = B.bend;
+    if (p0 > 0) lo = B.base + __shfl_sync(0xffffffffu, B.ol, (int)__fns(B.nzm, 0, p0 + 1));
+    if (p0 + nslots < nnz) hi = B.base + __shfl_sync(0xffffffffu, B.oh, (int)__fns(B.nzm, 0, p0 + nslots));
+}
+
 // SPANS: the two weight copies of a round each move 512 contiguous bytes
 // (lane l: arcs [4l, 4l + 4), then [128 + 4l, 128 + 4l + 4)), so every
 // 32-byte sector is read once; otherwise lane l copies its own 8 arcs' 32
@@ -312,11 +326,13 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         const int64_t o_31 = lane == 31 ? __ldcs(offsets + min(r0 + 32, n)) : 0;
         B = ring_open(r0, n, o_lo, o_31, heavy_arcs, lane);
     }
-    int64_t ep = ring_skip(B, B.base & ~(int64_t)(BU - 1), lane);  // next round to issue
+    int64_t plo, phi;
+    pass_span(B, 0, nslots, plo, phi);
+    int64_t ep = ring_skip(B, plo, lane);  // next round to issue
 #pragma unroll
     for (int i = 0; i < RING; i++) {
-        ring_issue<WEIGHTED>(ring, i, ep, B.bend, arcs, cls, w, lane);
-        if (ep < B.bend) ep = ring_skip(B, ep + BROUND, lane);
+        ring_issue<WEIGHTED>(ring, i, ep, phi, arcs, cls, w, lane);
+        if (ep < phi) ep = ring_skip(B, ep + BROUND, lane);
     }
     int slot0 = 0;  // ring slot of the pass's first round
     for (; b < nblocks; b += GW) {
@@ -350,9 +366,10 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
             if (mine) s_row[rank - p0] = lane;
             const int npass = min(nslots, nnz - p0);
             __syncwarp();
-            int64_t ec = ring_skip(B, B.base & ~(int64_t)(BU - 1), lane);  // next round to consume
+            pass_span(B, p0, nslots, plo, phi);
+            int64_t ec = ring_skip(B, plo, lane);  // next round to consume
             int slot = slot0;
-            while (ec < B.bend) {
+            while (ec < phi) {
                 cp_wait<RING - 1>();
                 const uint8_t *rs = ring + slot * RSLOT;
                 const uint2 ca = *reinterpret_cast<const uint2 *>(rs + lane * BU);
@@ -371,27 +388,30 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
                                               trash, qscale, ca, wa);
                 __syncwarp();
                 // refill the slot just consumed with the round RING ahead
-                ring_issue<WEIGHTED>(ring, slot, ep, B.bend, arcs, cls, w, lane);
-                if (ep < B.bend) ep = ring_skip(B, ep + BROUND, lane);
+                ring_issue<WEIGHTED>(ring, slot, ep, phi, arcs, cls, w, lane);
+                if (ep < phi) ep = ring_skip(B, ep + BROUND, lane);
                 slot = slot + 1 == RING ? 0 : slot + 1;
                 ec = ring_skip(B, ec + BROUND, lane);
             }
             // prime the ring for what comes next: this block's next pass, or
             // the next block's first rounds (in flight during the write-out)
             const bool last = p0 + nslots >= nnz;
+            int64_t nlo = 0, nhi = 0;
             if (!last) {
-                ep = ring_skip(B, B.base & ~(int64_t)(BU - 1), lane);
+                pass_span(B, p0 + nslots, nslots, nlo, nhi);
+                ep = ring_skip(B, nlo, lane);
             } else if (more) {
                 NB = ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
                 opened = true;
-                ep = ring_skip(NB, NB.base & ~(int64_t)(BU - 1), lane);
+                pass_span(NB, 0, nslots, nlo, nhi);
+                ep = ring_skip(NB, nlo, lane);
             }
             if (!last || more) {
                 const RingBlk &P = last ? NB : B;
 #pragma unroll
                 for (int i = 0; i < RING; i++) {
-                    ring_issue<WEIGHTED>(ring, (slot + i) % RING, ep, P.bend, arcs, cls, w, lane);
-                    if (ep < P.bend) ep = ring_skip(P, ep + BROUND, lane);
+                    ring_issue<WEIGHTED>(ring, (slot + i) % RING, ep, nhi, arcs, cls, w, lane);
+                    if (ep < nhi) ep = ring_skip(P, ep + BROUND, lane);
                 }
                 slot0 = slot;
             }
