@@ -316,8 +316,12 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
     const int64_t arcs = offsets[n];
     const int half = kk >> 1;
 
-    int64_t b = gw;
-    if (b >= nblocks) return;
+    // each warp takes a contiguous run of blocks: the last round of a block
+    // overshoots into the next block's arcs, which this warp then reads again
+    // at once (an L2 hit) instead of another warp much later (from DRAM)
+    const int64_t b_end = ((gw + 1) * nblocks) / GW;
+    int64_t b = (gw * nblocks) / GW;
+    if (b >= b_end) return;
     // open the first block and prime its first rounds
     RingBlk B;
     {
@@ -335,11 +339,11 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         if (ep < phi) ep = ring_skip(B, ep + BROUND, lane);
     }
     int slot0 = 0;  // ring slot of the pass's first round
-    for (; b < nblocks; b += GW) {
+    for (; b < b_end; b++) {
         const int64_t r0 = 32 * b;
-        const bool more = b + GW < nblocks;
+        const bool more = b + 1 < b_end;
         // next block's offsets, in flight during this block
-        const int64_t nr0 = 32 * (b + GW);
+        const int64_t nr0 = 32 * (b + 1);
         const int64_t o_lo_n = more ? __ldcs(offsets + min(nr0 + lane, n)) : 0;
         const int64_t o_31_n = (more && lane == 31) ? __ldcs(offsets + min(nr0 + 32, n)) : 0;
         const unsigned winm = B.nzm;
