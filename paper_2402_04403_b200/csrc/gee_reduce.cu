@@ -74,7 +74,8 @@ __device__ __forceinline__ long long plane_sum(uint32_t lo, uint32_t hi)
 template <bool WEIGHTED>
 __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const int32_t *__restrict__ s_soff, int lane,
                                                 bool owner, int32_t ol, int32_t lr, int32_t lend, int hoff, int trash,
-                                                float qscale, const uint2 &ca, const float (&wa)[BU])
+                                                float qscale, const uint2 &ca, const float (&wa)[BU],
+                                                float *__restrict__ zb, int kk, const float *__restrict__ sc1)
 {
     const unsigned startm = __ballot_sync(0xffffffffu, owner && ol <= lr);
     const int32_t pos = ol - lr;
@@ -82,7 +83,37 @@ __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const
     const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
     const int r = __popc(startm) + __popc(m & upto);  // owner rank + 1 (0: before the block)
     const int so = s_soff[r];
-    const bool ok = so >= 0 && lr + lane * BU < lend;
+    const bool inb = lr + lane * BU < lend;
+    const bool ok = so >= 0 && inb;
+    if (!WEIGHTED && so <= -2 && inb) {
+        // a single-chunk row (padded length 8: <= 8 real arcs, all in this
+        // lane's chunk; unit weights): equal classes combine in registers,
+        // exactly as the window would, and the lane stores the row's nonzero
+        // entries into the zero-filled Z row -- no atomics, no window slot,
+        // no read-out.  C3 1.58 -> 1.48 ms.  Weighted rows keep the window:
+        // the 64-bit combine, run in a divergent branch every round, cost
+        // C4 7.8 -> 9.1 ms.
+        float *zr = zb + (int64_t)(-so - 2) * kk;
+        uint32_t cc[BU];
+        unsigned long long qq[BU];
+#pragma unroll
+        for (int u = 0; u < BU; u++) {
+            cc[u] = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
+            qq[u] = WEIGHTED ? (unsigned long long)__float2ll_rn(wa[u] * qscale) : 1ull;
+        }
+#pragma unroll
+        for (int u = 0; u < BU; u++) {
+            bool first = cc[u] != 0u;
+#pragma unroll
+            for (int v = 0; v < u; v++) first = first && cc[v] != cc[u];
+            if (first) {
+                unsigned long long sum = qq[u];
+#pragma unroll
+                for (int v = u + 1; v < BU; v++) sum += cc[v] == cc[u] ? qq[v] : 0ull;
+                zr[cc[u] - 1] = (WEIGHTED ? (float)(long long)sum : (float)sum) * sc1[cc[u] - 1];
+            }
+        }
+    }
 #pragma unroll
     for (int u = 0; u < BU; u++) {
         const uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
@@ -214,13 +245,25 @@ __device__ __forceinline__ int64_t ring_skip(const RingBlk &B, int64_t e, int la
 // pass's own arcs instead of the whole block again (C2: every block has 32
 // nonempty rows for ~19 slots).  Rows are padded, so the bounds stay
 // multiples of 8 arcs.  Warp-uniform.
-__device__ __forceinline__ void pass_span(const RingBlk &B, int p0, int nslots, int64_t &lo, int64_t &hi)
+__device__ __forceinline__ void pass_span(const RingBlk &B, unsigned winm, int p0, int nslots, int64_t &lo,
+                                          int64_t &hi)
 {
-    const int nnz = __popc(B.nzm);
+    const int nnz = __popc(winm);
     lo = B.base & ~(int64_t)(BU - 1);
     hi = B.bend;
-    if (p0 > 0) lo = B.base + __shfl_sync(0xffffffffu, B.ol, (int)__fns(B.nzm, 0, p0 + 1));
-    if (p0 + nslots < nnz) hi = B.base + __shfl_sync(0xffffffffu, B.oh, (int)__fns(B.nzm, 0, p0 + nslots));
+    // the spans tile the block: a pass starts where the previous one ended,
+    // so the single-chunk rows between two passes' rows are met exactly once
+    if (p0 > 0) lo = B.base + __shfl_sync(0xffffffffu, B.oh, (int)__fns(winm, 0, p0));
+    if (p0 + nslots < nnz) hi = B.base + __shfl_sync(0xffffffffu, B.oh, (int)__fns(winm, 0, p0 + nslots));
+}
+
+// Single-chunk rows (padded length BU) of a block: reduced in registers by
+// the lane that holds their chunk (block_round_pad), not in the window
+// (unit weights only).
+template <bool WEIGHTED>
+__device__ __forceinline__ unsigned single_rows(const RingBlk &B, int lane)
+{
+    return WEIGHTED ? 0u : __ballot_sync(0xffffffffu, ((B.nzm >> lane) & 1u) && B.oh - B.ol == BU);
 }
 
 // SPANS: the two weight copies of a round each move 512 contiguous bytes
@@ -331,7 +374,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         B = ring_open(r0, n, o_lo, o_31, heavy_arcs, lane);
     }
     int64_t plo, phi;
-    pass_span(B, 0, nslots, plo, phi);
+    pass_span(B, B.nzm & ~single_rows<WEIGHTED>(B, lane), 0, nslots, plo, phi);
     int64_t ep = ring_skip(B, plo, lane);  // next round to issue
 #pragma unroll
     for (int i = 0; i < RING; i++) {
@@ -346,7 +389,8 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         const int64_t nr0 = 32 * (b + 1);
         const int64_t o_lo_n = more ? __ldcs(offsets + min(nr0 + lane, n)) : 0;
         const int64_t o_31_n = (more && lane == 31) ? __ldcs(offsets + min(nr0 + 32, n)) : 0;
-        const unsigned winm = B.nzm;
+        const unsigned singlem = single_rows<WEIGHTED>(B, lane);
+        const unsigned winm = B.nzm & ~singlem;
         const int rank = __popc(winm & below);
         const int orank = __popc(B.anym & below);
         const int nnz = __popc(winm);
@@ -366,11 +410,11 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         bool opened = false;
         for (int p0 = 0; p0 < max(nnz, 1); p0 += nslots) {
             const bool mine = nz && rank >= p0 && rank < p0 + nslots;
-            if (owner) s_soff[orank + 1] = mine ? (rank - p0) * pkb + 3 : -1;
+            if (owner) s_soff[orank + 1] = mine ? (rank - p0) * pkb + 3 : (((singlem >> lane) & 1u) ? -2 - lane : -1);
             if (mine) s_row[rank - p0] = lane;
             const int npass = min(nslots, nnz - p0);
             __syncwarp();
-            pass_span(B, p0, nslots, plo, phi);
+            pass_span(B, winm, p0, nslots, plo, phi);
             int64_t ec = ring_skip(B, plo, lane);  // next round to consume
             int slot = slot0;
             while (ec < phi) {
@@ -387,9 +431,9 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
 #pragma unroll
                     for (int u = 0; u < BU; u++) wa[u] = 1.f;
                 }
-                if (nnz > 0)
+                if (nnz > 0 || singlem)
                     block_round_pad<WEIGHTED>(vw, s_soff, lane, owner, B.ol, (int32_t)(ec - B.base), lend, hoff,
-                                              trash, qscale, ca, wa);
+                                              trash, qscale, ca, wa, zb, kk, sc1);
                 __syncwarp();
                 // refill the slot just consumed with the round RING ahead
                 ring_issue<WEIGHTED>(ring, slot, ep, phi, arcs, cls, w, lane);
@@ -402,12 +446,12 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
             const bool last = p0 + nslots >= nnz;
             int64_t nlo = 0, nhi = 0;
             if (!last) {
-                pass_span(B, p0 + nslots, nslots, nlo, nhi);
+                pass_span(B, winm, p0 + nslots, nslots, nlo, nhi);
                 ep = ring_skip(B, nlo, lane);
             } else if (more) {
                 NB = ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
                 opened = true;
-                pass_span(NB, 0, nslots, nlo, nhi);
+                pass_span(NB, NB.nzm & ~single_rows<WEIGHTED>(NB, lane), 0, nslots, nlo, nhi);
                 ep = ring_skip(NB, nlo, lane);
             }
             if (!last || more) {
