@@ -92,6 +92,8 @@ class PreparedGraph:
         for key in list(self._registered):
             torch.cuda.cudart().cudaHostUnregister(key[0])
         self._registered.clear()
+        if self._pipe is not None:
+            self._pipe.arena.close()
         self._dg = self._pipe = self._emb = None
         self._graph = self._lab_buf = self._z_buf = None
         self._closed = True

@@ -51,6 +51,44 @@ from .errors import ValidationError
 from .shard import plan_rows
 
 
+class PinnedArena:
+    """Page-locked host buffers of exact size: numpy memory registered with
+    cudaHostRegister and released by close().  torch's pinned allocator
+    rounds every block up to a power of two (a 9.3 GB payload would lock
+    16 GB of host RAM) and .cpu().pin_memory() copies twice; the arena's
+    buffers receive their device-to-host copy directly."""
+
+    def __init__(self):
+        self._held = []
+
+    def empty(self, n, dtype=torch.uint8):
+        itemsize = torch.empty(0, dtype=dtype).element_size()
+        a = np.empty(max(1, n * itemsize), dtype=np.uint8)
+        rc = int(torch.cuda.cudart().cudaHostRegister(a.ctypes.data, a.nbytes, 0))
+        if rc != 0:
+            raise ValidationError(f"cudaHostRegister of {a.nbytes} bytes failed ({rc})")
+        self._held.append(a)
+        return torch.from_numpy(a).view(dtype)[:n]
+
+    def copy_of(self, t):
+        """A pinned host copy of tensor t (device or host)."""
+        h = self.empty(t.numel(), t.dtype).view(t.shape) if t.numel() else torch.empty(0, dtype=t.dtype)
+        if t.numel():
+            h.copy_(t)
+        return h
+
+    def close(self):
+        for a in self._held:
+            torch.cuda.cudart().cudaHostUnregister(a.ctypes.data)
+        self._held.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class HostPipeline:
     """Streams a prepared graph held in pinned host memory through one GPU."""
 
@@ -65,7 +103,8 @@ class HostPipeline:
         dev = self.device
         off = g.offsets.cpu().numpy()
         self.bounds = plan_rows(off, max(1, chunks), k, self.weighted)
-        pin = lambda t: None if t is None else t.cpu().pin_memory()  # noqa: E731
+        self.arena = PinnedArena()
+        pin = lambda t: None if t is None else self.arena.copy_of(t)  # noqa: E731
         # host copies of the prepared layout (the "stored graph")
         # the hot tier travels in compact form (bitmap, prefix, ranks)
         self.h_hot = None
@@ -94,7 +133,7 @@ class HostPipeline:
             rel = off[lo:hi + 1] - off[lo]
             if rel[-1] < 2**31:
                 rel = rel.astype(np.int32)
-            self.h_off.append(torch.from_numpy(rel).pin_memory())
+            self.h_off.append(self.arena.copy_of(torch.from_numpy(rel)))
             v = DeviceGraph(hi - lo, 0, dev)
             v.n_nodes = g.n_nodes
             # plan the chunk's heavy rows / block spans on a temporary device
@@ -157,11 +196,12 @@ class HostPipeline:
                                              self.sentinel, _lib.ptr(ctl), _lib.ptr(pay), ctypes.byref(nb),
                                              _lib.ptr(wctl), _lib.ptr(wpay), ctypes.byref(nwb),
                                              _lib.stream_handle()), "gee_pack_targets")
-        self.h_ctl.append(ctl[:groups].cpu().pin_memory())
-        self.h_pay.append(pay[:int(nb.value)].cpu().pin_memory())
+        pin = self.arena.copy_of
+        self.h_ctl.append(pin(ctl[:groups]))
+        self.h_pay.append(pin(pay[:int(nb.value)]))
         empty = torch.empty(0, dtype=torch.uint8)
-        self.h_wctl.append(wctl[:groups].cpu().pin_memory() if self.weighted else empty)
-        self.h_wpay.append(wpay[:int(nwb.value)].cpu().pin_memory() if self.weighted else empty)
+        self.h_wctl.append(pin(wctl[:groups]) if self.weighted else empty)
+        self.h_wpay.append(pin(wpay[:int(nwb.value)]) if self.weighted else empty)
         del pay, wpay
 
     @property
@@ -192,10 +232,10 @@ class HostPipeline:
         self.cm = [torch.empty(rows * mw, dtype=torch.int64, device=dev) for _ in range(2)]
         self.cb = [torch.empty(nb + 1, dtype=torch.int64, device=dev) for _ in range(2)]
         self.cv = [torch.empty(rows * k, dtype=torch.float32, device=dev) for _ in range(2)]
-        self.hm = [torch.empty(rows * mw, dtype=torch.int64).pin_memory() for _ in range(2)]
-        self.hb = [torch.empty(nb + 1, dtype=torch.int64).pin_memory() for _ in range(2)]
-        self.hv = [torch.empty(rows * k, dtype=torch.float32).pin_memory() for _ in range(2)]
-        self.h_tot = torch.zeros(max(1, len(self.views)), dtype=torch.int64).pin_memory()
+        self.hm = [self.arena.empty(rows * mw, torch.int64) for _ in range(2)]
+        self.hb = [self.arena.empty(nb + 1, torch.int64) for _ in range(2)]
+        self.hv = [self.arena.empty(rows * k, torch.float32) for _ in range(2)]
+        self.h_tot = self.arena.empty(max(1, len(self.views)), torch.int64).zero_()
         self.mw = mw
 
     def run(self, h_labels, h_z, emb: Embedder, sparse=True, inv=None):
@@ -363,4 +403,4 @@ def pinned_like(shape, dtype=torch.float32):
     return torch.empty(shape, dtype=dtype).pin_memory()
 
 
-__all__ = ["HostPipeline", "pinned_like", "np"]
+__all__ = ["HostPipeline", "PinnedArena", "pinned_like", "np"]
