@@ -52,6 +52,7 @@ def main():
     out = {"workload": cfg.name, "scheme": args.scheme, "s_listed_edges": s, "steps": args.steps,
            "warmup": args.warmup, "per_n": {}}
     BUS_GBS = 725.0
+    ALLREDUCE_MS = 0.025  # NCCL all-reduce of k+1 int64 over NVLink: latency-bound, ~25 us
     for nshards in (int(x) for x in args.shards.split(",")):
         ranks = []
         for rank in range(nshards):
@@ -88,22 +89,34 @@ def main():
             emb = Embedder(n, k)
             z = torch.empty((hi - lo, k), dtype=torch.float32, device="cuda")
             emb.project(y, validate=True, g=g)
+            # as bench.py: with several ranks the histogram is sharded (each
+            # rank counts n/N labels; the all-reduce of k+1 counts is modelled)
+            c_lo, c_hi = shard_mod.label_slice(n, nshards, rank)
+
+            def proj():
+                if nshards > 1:
+                    emb.project_sharded(y, g, c_lo, c_hi, lambda c: c)
+                else:
+                    emb.project(y, validate=False, g=g)
+
             for _ in range(args.warmup):
-                emb.project(y, validate=False, g=g)
+                proj()
                 emb.pull(g, z)
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             for _ in range(args.steps):
-                emb.project(y, validate=False, g=g)
+                proj()
                 emb.pull(g, z)
             b.record()
             torch.cuda.synchronize()
             ms = a.elapsed_time(b) / args.steps
-            ranks.append({"rank": rank, "rows": hi - lo, "arcs": int(g.arcs), "ms_per_step": ms})
+            ranks.append({"rank": rank, "rows": hi - lo, "arcs": int(g.arcs), "ms_per_step": ms,
+                          "allreduce_ms_model": ALLREDUCE_MS if nshards > 1 else 0.0})
             del g, emb, z
             torch.cuda.empty_cache()
-        worst = max(r["ms_per_step"] + r.get("reduce_scatter_ms_model", 0.0) for r in ranks)
+        worst = max(r["ms_per_step"] + r.get("reduce_scatter_ms_model", 0.0) + r.get("allreduce_ms_model", 0.0)
+                    for r in ranks)
         mean = sum(r["ms_per_step"] for r in ranks) / len(ranks)
         out["per_n"][nshards] = {"max_ms": worst, "mean_ms": mean, "balance": mean / worst,
                                  "projected_geps": s / (worst * 1e-3) / 1e9, "ranks": ranks}
