@@ -524,7 +524,10 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
 // writes the Z row itself; the items of longer (mega) rows meet in acc[m]
 // through 64-bit atomics and a small finalize.
 constexpr int HCOL = 8;   // columns per lane: k <= 256
-constexpr int HCOPY = 4;  // private window copies per warp (heavy items)
+#ifndef GEE_HCOPY
+#define GEE_HCOPY 2
+#endif
+constexpr int HCOPY = GEE_HCOPY;  // private window copies per warp (heavy items)
 
 template <bool WEIGHTED>
 __global__ void __launch_bounds__(RT)
