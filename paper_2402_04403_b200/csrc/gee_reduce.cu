@@ -140,7 +140,14 @@ __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const
 // across passes and blocks so a block's first rounds arrive while the
 // previous block is written out.  Each lane copies and consumes the same 8
 // arcs of a round, so cp.async.wait_group alone orders them.
-constexpr int RING = 4;
+#ifndef GEE_RING
+#define GEE_RING 3
+#endif
+#ifndef GEE_RING_H
+#define GEE_RING_H 4
+#endif
+constexpr int RING = GEE_RING;      // block reducer
+constexpr int RING_H = GEE_RING_H;  // heavy items
 constexpr int RING_CLS = BROUND;                        // bytes per round
 constexpr int RING_W = BROUND * (int)sizeof(float);     // bytes per round (weighted)
 
@@ -542,11 +549,11 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
     const int pkb = block_vec_words(kk);  // [3 pad | trash | bins 1..k | pad]
     constexpr int RSLOT = RING_CLS + (WEIGHTED ? RING_W : 0);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw) + wid * RING;
-    uint8_t *ring_base = smem_raw + RW * RING * sizeof(uint64_t);
-    uint8_t *ring = ring_base + wid * RING * RSLOT;
-    float *sc1 = reinterpret_cast<float *>(ring_base + RW * RING * RSLOT);  // sc1[c] = inv[c+1] * dscale
-    if (lane < RING) mbar_init(bars + lane, 1);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw) + wid * RING_H;
+    uint8_t *ring_base = smem_raw + RW * RING_H * sizeof(uint64_t);
+    uint8_t *ring = ring_base + wid * RING_H * RSLOT;
+    float *sc1 = reinterpret_cast<float *>(ring_base + RW * RING_H * RSLOT);  // sc1[c] = inv[c+1] * dscale
+    if (lane < RING_H) mbar_init(bars + lane, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint64_t pol = policy_evict_first();
     uint32_t ph = 0;
@@ -561,7 +568,7 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
     __syncthreads();
     // items come largest first; warps fetch them dynamically.  Rounds are
     // 256-arc aligned, so each aligned BLOCK_ROW_MAX window holds whole
-    // rounds; RING rounds stay in flight (cp.async ring) within an item.
+    // rounds; RING_H rounds stay in flight (cp.async ring) within an item.
     for (;;) {
         int64_t it = 0;
         if (lane == 0) it = (int64_t)atomicAdd(counter, 1ull);
@@ -573,7 +580,7 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
         for (int j = 0; j < HCOL; j++) sum[j] = 0ull;
         int64_t ep = b0 & ~(int64_t)(BROUND - 1);
 #pragma unroll
-        for (int i = 0; i < RING; i++) {
+        for (int i = 0; i < RING_H; i++) {
             ring_issue_bulk<WEIGHTED>(ring, bars, i, ep, e1, arcs, cls, w, lane, pol);
             ep += BROUND;
         }
@@ -610,7 +617,7 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
             __syncwarp();  // every lane has read the slot before it is refilled
             ring_issue_bulk<WEIGHTED>(ring, bars, slot, ep, e1, arcs, cls, w, lane, pol);
             ep += BROUND;
-            slot = slot + 1 == RING ? 0 : slot + 1;
+            slot = slot + 1 == RING_H ? 0 : slot + 1;
             // fold the window into the 64-bit sums at each aligned window end
             const int64_t en = e0 + BROUND;
             if ((en & (BLOCK_ROW_MAX - 1)) == 0 || en >= e1) {
@@ -765,7 +772,7 @@ int gee_reduce_heavy(const uint8_t *cls, const float *w, int64_t arcs, int32_t s
     const bool weighted = w != nullptr;
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
-    const size_t sh = (size_t)RW * RING * (RING_CLS + (weighted ? RING_W : 0) + sizeof(uint64_t)) +
+    const size_t sh = (size_t)RW * RING_H * (RING_CLS + (weighted ? RING_W : 0) + sizeof(uint64_t)) +
                       (size_t)block_vec_words(k) * sizeof(float) +
                       (size_t)RW * HCOPY * (block_vec_words(k) * (weighted ? 2 : 1) + 4) * sizeof(uint32_t);
     GEE_REQUIRE((reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0),
