@@ -14,7 +14,15 @@
 
 namespace {
 
-constexpr int GTHREADS = 1024;
+#ifndef GEE_GTHREADS
+#define GEE_GTHREADS 1024
+#endif
+#ifndef GEE_GU
+#define GEE_GU 16
+#endif
+constexpr int GTHREADS = GEE_GTHREADS;  // threads of the one persistent CTA per SM
+constexpr int GU = GEE_GU;              // lookups per lane per step (a warp takes 32 GU arcs)
+constexpr int GSTEP = 32 * GU;
 
 // Label load of a cold-or-L2 slot, issued only when `on` (predicated, so
 // the 16 lookups of a thread stay independent and in flight together).
@@ -46,21 +54,21 @@ k_gather_contig(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    const int64_t steps = arcs / 512;
+    const int64_t steps = arcs / GSTEP;
     for (int64_t st = gw; st < steps; st += warps) {
-        const int32_t *tp = targets + st * 512 + lane;
-        uint32_t t[16];
+        const int32_t *tp = targets + st * GSTEP + lane;
+        uint32_t t[GU];
 #pragma unroll
-        for (int i = 0; i < 16; i++)
+        for (int i = 0; i < GU; i++)
             asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(t[i]) : "l"(tp + 32 * i));
-        uint32_t l[16];
+        uint32_t l[GU];
 #pragma unroll
-        for (int i = 0; i < 16; i++) l[i] = ld_label_pred<L1MODE>(table + t[i], true, pol);
-        uint8_t *cp = cls + st * 512 + lane;
+        for (int i = 0; i < GU; i++) l[i] = ld_label_pred<L1MODE>(table + t[i], true, pol);
+        uint8_t *cp = cls + st * GSTEP + lane;
 #pragma unroll
-        for (int i = 0; i < 16; i++) cp[32 * i] = (uint8_t)l[i];
+        for (int i = 0; i < GU; i++) cp[32 * i] = (uint8_t)l[i];
     }
-    for (int64_t e = steps * 512 + gw * 32 + lane; e < arcs; e += warps * 32) cls[e] = table[targets[e]];
+    for (int64_t e = steps * GSTEP + gw * 32 + lane; e < arcs; e += warps * 32) cls[e] = table[targets[e]];
 }
 
 // Packed shared-memory head: the first `hl` slots of the table as PER labels
@@ -89,16 +97,16 @@ k_gather_packed(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    const int64_t steps = arcs / 512;
+    const int64_t steps = arcs / GSTEP;
     for (int64_t st = gw; st < steps; st += warps) {
-        const int32_t *tp = targets + st * 512 + lane;
-        uint32_t t[16];
+        const int32_t *tp = targets + st * GSTEP + lane;
+        uint32_t t[GU];
 #pragma unroll
-        for (int i = 0; i < 16; i++)
+        for (int i = 0; i < GU; i++)
             asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(t[i]) : "l"(tp + 32 * i));
-        uint32_t l[16];
+        uint32_t l[GU];
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
+        for (int i = 0; i < GU; i++) {
             const uint32_t ti = t[i];
             const bool in_s = ti < hl;
             const uint32_t g = ld_label_pred<1>(table + ti, !in_s, pol);
@@ -106,11 +114,11 @@ k_gather_packed(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
             const uint32_t sv = (head_w[wi] >> (BITS * (ti - wi * PER))) & MASK;
             l[i] = in_s ? sv : g;
         }
-        uint8_t *cp = cls + st * 512 + lane;
+        uint8_t *cp = cls + st * GSTEP + lane;
 #pragma unroll
-        for (int i = 0; i < 16; i++) cp[32 * i] = (uint8_t)l[i];
+        for (int i = 0; i < GU; i++) cp[32 * i] = (uint8_t)l[i];
     }
-    for (int64_t e = steps * 512 + gw * 32 + lane; e < arcs; e += warps * 32) cls[e] = table[targets[e]];
+    for (int64_t e = steps * GSTEP + gw * 32 + lane; e < arcs; e += warps * 32) cls[e] = table[targets[e]];
 }
 
 }  // namespace
