@@ -63,7 +63,7 @@ class PinnedArena:
 
     def empty(self, n, dtype=torch.uint8):
         itemsize = torch.empty(0, dtype=dtype).element_size()
-        a = np.empty(max(1, n * itemsize), dtype=np.uint8)
+        a = np.empty(max(1, n) * itemsize, dtype=np.uint8)
         rc = int(torch.cuda.cudart().cudaHostRegister(a.ctypes.data, a.nbytes, 0))
         if rc != 0:
             raise ValidationError(f"cudaHostRegister of {a.nbytes} bytes failed ({rc})")
