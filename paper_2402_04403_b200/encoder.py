@@ -18,6 +18,7 @@ red.global atomics (order-dependent rounding).
 
 import enum
 import logging
+import threading
 
 import numpy as np
 
@@ -188,19 +189,18 @@ def _projection_inv(projection, labels, k):
 # 6M, even at 20M-60M arcs, where the resident pass then favours the pull).
 PUSH_MAX_ARCS = 1 << 23
 
-_last = {}
+_last = threading.local()
 
 
 def last_pass():
     """Variant and kernels of the most recent embed_* call on this thread:
-    {"variant": "pull"|"push", "reducer": "blocks"|"wide"|None,
+    {"variant": "pull"|"push", "reducer": "blocks"|"wide"|"prepared"|None,
     "reason": why}."""
-    return dict(_last)
+    return dict(getattr(_last, "info", {}))
 
 
 def _record(variant, reducer, reason):
-    _last.clear()
-    _last.update(variant=variant, reducer=reducer, reason=reason)
+    _last.info = dict(variant=variant, reducer=reducer, reason=reason)
     logger.debug("edge pass: variant=%s reducer=%s (%s)", variant, reducer, reason)
 
 
