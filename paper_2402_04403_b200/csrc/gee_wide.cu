@@ -29,6 +29,21 @@ constexpr int WW = WT / 32;
 constexpr int SPLIT = 21;      // == BLOCK_SPLIT of gee_reduce.cu (gee_block_scale_exp bounds |q| < 2^41)
 constexpr int LIGHT_MAX = 2048;
 constexpr int UNR = 8;         // 32-arc rounds in flight per warp (256 arcs)
+#ifndef GEE_WIDE_MINB
+#define GEE_WIDE_MINB 5
+#endif
+#ifndef GEE_WIDE_ST
+#define GEE_WIDE_ST 0  // Z row stores: 0 streaming (.cs), 1 default write-back
+#endif
+#ifndef GEE_WIDE_CONTIG
+#define GEE_WIDE_CONTIG 0
+#endif
+
+__device__ __forceinline__ void st_z4(float4 *p, float4 v)
+{
+    if (GEE_WIDE_ST == 0) __stcs(p, v);
+    else *p = v;
+}
 
 // Signed split decode (see gee_reduce.cu): the high plane holds the two's
 // complement of a sum in [-2^31, 2^31).
@@ -89,7 +104,7 @@ __device__ __forceinline__ void wide_load(const int32_t *__restrict__ targets, c
 // Only a row's first 32 * UNR arcs are pipelined; longer rows finish their
 // remaining segments in place.
 template <typename LT, bool WEIGHTED, bool VEC>
-__global__ void __launch_bounds__(WT, WEIGHTED ? 3 : 5)
+__global__ void __launch_bounds__(WT, WEIGHTED ? 3 : GEE_WIDE_MINB)
 k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__restrict__ targets,
             const float *__restrict__ w, const LT *__restrict__ table, float qscale, double dscale,
             const double *__restrict__ inv, int32_t k, int32_t kp, float *__restrict__ z)
@@ -102,8 +117,19 @@ k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__res
     for (int c = threadIdx.x; c < kp; c += WT) sc[c] = c < k ? (float)(inv[c + 1] * dscale) : 0.f;
     for (int i = lane; i < planes * kp; i += 32) win[i] = 0u;
     __syncthreads();
+#if GEE_WIDE_CONTIG
+    // each CTA owns a contiguous run of rows (its warps interleave in it), so
+    // the SM's Z rows go out as one sequential stream
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t r_beg = (int64_t)blockIdx.x * per;
+    const int64_t r_end = min(n, r_beg + per);
+    const int64_t GW = WW;
+    int64_t r = r_beg + wid;
+    n = r_end;  // the pipeline below stops at the end of the CTA's run
+#else
     const int64_t GW = (int64_t)gridDim.x * WW;
     int64_t r = (int64_t)blockIdx.x * WW + wid;
+#endif
     if (r >= n) return;
     auto seg_end = [](int64_t b0, int64_t b1) { return b1 - b0 <= LIGHT_MAX ? (b1 < b0 + 32 * UNR ? b1 : b0 + 32 * UNR) : b0; };
     // stage 0 (row r): labels in flight; stage 1 (row r+GW): targets in flight
@@ -171,7 +197,7 @@ k_wide_rows(const int64_t *__restrict__ offsets, int64_t n, const int32_t *__res
                         }
                         w4[g] = make_uint4(0u, 0u, 0u, 0u);
                     }
-                    __stcs(z4 + g, o);
+                    st_z4(z4 + g, o);
                 }
             } else {
                 for (int c = lane; c < k; c += 32) {
