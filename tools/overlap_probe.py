@@ -47,4 +47,4 @@ for _ in range(2):
     bl = timed(lambda: blocks(z2, s2))
     both = timed(lambda: (gather(cls2, s1), blocks(z2, s2)))
 print(f"gather {ga:.2f} ms  blocks {bl:.2f} ms  sum {ga + bl:.2f}  concurrent {both:.2f} ms "
-      f"(block={os.environ.get('GEE_GATHER_BLOCK', 1024)} ctas/SM={os.environ.get('GEE_GATHER_CTAS', 1)})")
+      "")
