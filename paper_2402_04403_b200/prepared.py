@@ -15,7 +15,10 @@ then runs only the per-call work:
   the kernels and the host-side expansion overlapping.  HBM only holds two
   chunks, so graphs larger than device memory work the same way.
 * ``residency="device"``: the layout stays in HBM; each call runs the
-  histogram and the pull and delivers Z where ``out`` lives.
+  histogram and the pull and delivers Z where ``out`` lives: into a CUDA
+  tensor through one replay of the pass recorded as a CUDA graph, into host
+  memory row-sparse per chunk (labels in, compacted Z out, host-side
+  expansion overlapping), as the streamed path does minus the graph copy.
 
 Host buffers passed as ``out`` (or as the labels) are page-locked with
 ``cudaHostRegister`` on first use and kept registered while the prepared
@@ -54,6 +57,8 @@ class PreparedGraph:
         self.device = None
         self._dg = None  # residency="device": the DeviceGraph
         self._pipe = None  # residency="host": the HostPipeline
+        self._pipe_res = None  # residency="device", host results: HostPipeline over the resident graph
+        self._chunks = 32
         self._emb = None
         self._graph = None  # residency="device": the pass recorded as a CUDA graph
         self._lab_buf = self._z_buf = None
@@ -92,9 +97,10 @@ class PreparedGraph:
         for key in list(self._registered):
             torch.cuda.cudart().cudaHostUnregister(key[0])
         self._registered.clear()
-        if self._pipe is not None:
-            self._pipe.arena.close()
-        self._dg = self._pipe = self._emb = None
+        for pipe in (self._pipe, self._pipe_res):
+            if pipe is not None:
+                pipe.arena.close()
+        self._dg = self._pipe = self._pipe_res = self._emb = None
         self._graph = self._lab_buf = self._z_buf = None
         self._closed = True
 
@@ -117,7 +123,9 @@ class PreparedGraph:
             raise ValidationError(f"graph has {self.n} nodes but labels have {y.n}")
         if y.k != self.k:
             raise ValidationError(f"graph was prepared for k={self.k} but labels have k={y.k}")
-        if self.residency == "device":
+        host_result = (out is not None and not (_is_torch(out) and out.is_cuda)) or \
+            (out is None and not (_is_torch(y.labels) and y.labels.is_cuda))
+        if self.residency == "device" and not host_result:
             if inv is None:
                 # the pass is recorded once as a CUDA graph and replayed on
                 # the new labels: one host launch per call (small graphs are
@@ -144,7 +152,17 @@ class PreparedGraph:
                 return out
             out[...] = z_d.cpu().numpy()
             return out
-        # host residency: labels and Z through pinned host memory
+        # host result: labels and Z through pinned host memory -- the graph
+        # streamed from pinned host memory (host residency) or read where it
+        # lies in HBM (device residency), Z copied out row-sparse per chunk
+        pipe = self._pipe
+        if self.residency == "device":
+            if self._pipe_res is None:
+                from .stream import HostPipeline
+
+                self._pipe_res = HostPipeline(self._dg, self.k, chunks=self._chunks, device=self.device,
+                                              resident=True)
+            pipe = self._pipe_res
         lab = y.labels
         if _is_torch(lab):
             lab = lab.cpu() if lab.is_cuda else lab
@@ -165,7 +183,7 @@ class PreparedGraph:
         else:  # float64 host array or a CUDA tensor: through a pinned f32 Z
             h_z = torch.empty((self.n, self.k), dtype=torch.float32).pin_memory()
             result = None
-        self._pipe.run(h_y, h_z, self._emb, inv=inv)
+        pipe.run(h_y, h_z, self._emb, inv=inv)
         if result is not None:
             return result
         if _is_torch(target):
@@ -176,17 +194,19 @@ class PreparedGraph:
 
     @property
     def h2d_bytes_per_call(self):
-        """Bytes one host-resident call copies in (graph chunks, hot tier,
-        labels)."""
-        if self._pipe is None:
+        """Bytes one host-result call copies in (labels, and for host
+        residency the graph chunks and the hot tier)."""
+        pipe = self._pipe if self._pipe is not None else self._pipe_res
+        if pipe is None:
             return 0
         import torch
 
-        return self._pipe.h2d_bytes(torch.empty(self.n, dtype=torch.int32))
+        return pipe.h2d_bytes(torch.empty(self.n, dtype=torch.int32))
 
     @property
     def d2h_bytes_last_call(self):
-        return 0 if self._pipe is None else int(self._pipe.d2h_bytes)
+        pipe = self._pipe if self._pipe is not None else self._pipe_res
+        return 0 if pipe is None else int(pipe.d2h_bytes)
 
 
 def prepare(g, k, *, device=None, residency="host", chunks=32, accounting=None):
@@ -214,7 +234,7 @@ def prepare(g, k, *, device=None, residency="host", chunks=32, accounting=None):
         raise ValidationError("chunks must be at least 1")
     dev = require_cuda(device)
     p = PreparedGraph()
-    p.k, p.device, p.residency = k, dev, residency
+    p.k, p.device, p.residency, p._chunks = k, dev, residency, chunks
     t0 = time.perf_counter()
     if isinstance(g, EdgeList):
         p.n, p.s, p.directed = g.n, g.s, g.directed

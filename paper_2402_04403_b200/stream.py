@@ -90,11 +90,19 @@ class PinnedArena:
 
 
 class HostPipeline:
-    """Streams a prepared graph held in pinned host memory through one GPU."""
+    """Streams a prepared graph held in pinned host memory through one GPU.
 
-    def __init__(self, g: DeviceGraph, k, chunks=16, device=None, packed=None):
+    ``resident=True``: the prepared graph stays in HBM (the caller keeps
+    ``g`` alive); a call then only copies the labels in and the row-sparse Z
+    out, chunk by chunk, with the same compaction and host-side expansion.
+    """
+
+    HOST_SLOTS = 3  # row-sparse Z chunks in host memory: one copying out while two expand
+
+    def __init__(self, g: DeviceGraph, k, chunks=16, device=None, packed=None, resident=False):
         if not g.has_pull or g.hot_k != k:
             raise ValidationError("HostPipeline needs a pull graph prepared for k (prepare_hot)")
+        self.resident = bool(resident)
         self.device = device or g.device
         self.dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         # a row shard streams its own rows; labels and hot ranks cover all nodes
@@ -108,19 +116,20 @@ class HostPipeline:
         # host copies of the prepared layout (the "stored graph")
         # the hot tier travels in compact form (bitmap, prefix, ranks)
         self.h_hot = None
-        if g.hot_rank is not None:
-            if g.hot_bits is None:
-                g.compact_hot()
+        if g.hot_rank is not None and g.hot_bits is None:
+            g.compact_hot()
+        if g.hot_rank is not None and not self.resident:
             self.h_hot = [pin(g.hot_bits), pin(g.hot_pref), pin(g.hot_list)]
         self.n_hot = g.n_hot
         # packed targets (gee_pack_targets): per-8-arc-group byte-width deltas
         # and the real arcs' weights (pads rebuilt on the device)
-        self.packed = (g.padded == 8) if packed is None else bool(packed)
-        if self.packed and g.padded != 8:
+        self.packed = (g.padded == 8 and not self.resident) if packed is None else bool(packed)
+        if self.packed and (g.padded != 8 or self.resident):
             raise ValidationError("packed targets need rows padded to 8 arcs")
         self.sentinel = g.n_hot + g.n_nodes
-        self.h_tgt = None if self.packed else pin(g.targets)
-        self.h_w = None if self.packed else pin(g.weights)
+        self.h_tgt = None if (self.packed or self.resident) else pin(g.targets)
+        self.h_w = None if (self.packed or self.resident) else pin(g.weights)
+        self.g = g if self.resident else None
         self.h_ctl, self.h_pay, self.h_wctl, self.h_wpay = [], [], [], []
         self.h_off = []
         self.views = []
@@ -131,14 +140,18 @@ class HostPipeline:
             # chunk-relative offsets travel as int32 when the chunk allows it
             # (widened on the device): C4 saves 0.54 GB of H2D per call
             rel = off[lo:hi + 1] - off[lo]
-            if rel[-1] < 2**31:
+            if rel[-1] < 2**31 and not self.resident:
                 rel = rel.astype(np.int32)
-            self.h_off.append(self.arena.copy_of(torch.from_numpy(rel)))
             v = DeviceGraph(hi - lo, 0, dev)
             v.n_nodes = g.n_nodes
+            if self.resident:  # the chunk's rebased offsets stay on the device
+                v.res_off = torch.from_numpy(rel).to(dev)
+                self.h_off.append(None)
+            else:
+                self.h_off.append(self.arena.copy_of(torch.from_numpy(rel)))
             # plan the chunk's heavy rows / block spans on a temporary device
             # copy of its rebased offsets (graph preparation)
-            v.offsets = self.h_off[c].to(dev).long()
+            v.offsets = v.res_off if self.resident else self.h_off[c].to(dev).long()
             v.targets = torch.empty(a1 - a0, dtype=torch.int32, device=dev)  # shape only
             v.weights = None
             v._plan_heavy()
@@ -164,17 +177,21 @@ class HostPipeline:
                            if self.weighted else None for _ in range(2)]
             self.scratch_bytes = int(_lib.lib.gee_unpack_scratch_bytes(max_arcs // 8))
             self.d_scratch = torch.empty(max(1, self.scratch_bytes), dtype=torch.uint8, device=dev)
-        self.d_off = [torch.empty(max_rows + 1, dtype=torch.int64, device=dev) for _ in range(2)]
-        self.d_off32 = [torch.empty(max_rows + 1, dtype=torch.int32, device=dev) for _ in range(2)]
-        self.d_tgt = [torch.empty(max_arcs, dtype=torch.int32, device=dev) for _ in range(2)]
+        slots = 0 if self.resident else 2
+        self.d_off = [torch.empty(max_rows + 1, dtype=torch.int64, device=dev) for _ in range(slots)]
+        self.d_off32 = [torch.empty(max_rows + 1, dtype=torch.int32, device=dev) for _ in range(slots)]
+        self.d_tgt = [torch.empty(max_arcs, dtype=torch.int32, device=dev) for _ in range(slots)]
         self.d_w = [torch.empty(max_arcs, dtype=torch.float32, device=dev) if self.weighted else None
-                    for _ in range(2)]
+                    for _ in range(slots)]
         self.d_z = [torch.empty(max_rows * k, dtype=torch.float32, device=dev) for _ in range(2)]
         self.d_y = torch.empty(self.n_nodes, dtype=torch.int32, device=dev)
         self.d_hot = [torch.empty_like(t, device=dev) for t in self.h_hot] if self.h_hot is not None else None
         self.proj = DeviceGraph(self.n_nodes, 0, dev)  # what project() needs: the hot tier of all nodes
         if self.d_hot is not None:
             self.proj.hot_bits, self.proj.hot_pref, self.proj.hot_list = self.d_hot
+            self.proj.n_hot = self.n_hot
+        elif self.resident and g.hot_rank is not None:
+            self.proj.hot_bits, self.proj.hot_pref, self.proj.hot_list = g.hot_bits, g.hot_pref, g.hot_list
             self.proj.n_hot = self.n_hot
         self.s_in = torch.cuda.Stream(dev)
         self.s_cmp = torch.cuda.Stream(dev)
@@ -210,6 +227,8 @@ class HostPipeline:
 
     def h2d_bytes(self, h_labels):
         b = h_labels.numel() * h_labels.element_size()
+        if self.resident:
+            return int(b)
         b += sum(t.numel() * t.element_size() for t in self.h_off)
         if self.packed:
             b += sum(t.numel() for t in self.h_ctl) + sum(t.numel() for t in self.h_pay)
@@ -232,9 +251,10 @@ class HostPipeline:
         self.cm = [torch.empty(rows * mw, dtype=torch.int64, device=dev) for _ in range(2)]
         self.cb = [torch.empty(nb + 1, dtype=torch.int64, device=dev) for _ in range(2)]
         self.cv = [torch.empty(rows * k, dtype=torch.float32, device=dev) for _ in range(2)]
-        self.hm = [self.arena.empty(rows * mw, torch.int64) for _ in range(2)]
-        self.hb = [self.arena.empty(nb + 1, torch.int64) for _ in range(2)]
-        self.hv = [self.arena.empty(rows * k, torch.float32) for _ in range(2)]
+        hs = self.HOST_SLOTS
+        self.hm = [self.arena.empty(rows * mw, torch.int64) for _ in range(hs)]
+        self.hb = [self.arena.empty(nb + 1, torch.int64) for _ in range(hs)]
+        self.hv = [self.arena.empty(rows * k, torch.float32) for _ in range(hs)]
         self.h_tot = self.arena.empty(max(1, len(self.views)), torch.int64).zero_()
         self.mw = mw
 
@@ -292,42 +312,50 @@ class HostPipeline:
         return h_z
 
     def _issue_chunk(self, i, v, emb, h_z, sparse, e_in, e_cmp, e_out, drained, errors):
-        """Main thread: queue chunk i's copy-in, decode, pull and compaction."""
+        """Main thread: queue chunk i's copy-in, decode, pull and compaction
+        (resident: the pull on the HBM-resident rows and the compaction)."""
         b = i & 1
         lo, hi, a0, a1 = v.span
         with torch.cuda.stream(self.s_in):
-            if i >= 2:
-                self.s_in.wait_event(e_cmp[i - 2])  # slot b's CSR is free
-            ho = self.h_off[i]
-            (self.d_off32 if ho.dtype == torch.int32 else self.d_off)[b][:hi - lo + 1].copy_(ho, non_blocking=True)
-            if self.packed:
-                self.d_ctl[b][:self.h_ctl[i].numel()].copy_(self.h_ctl[i], non_blocking=True)
-                self.d_pay[b][:self.h_pay[i].numel()].copy_(self.h_pay[i], non_blocking=True)
-                if self.weighted:
-                    self.d_wctl[b][:self.h_wctl[i].numel()].copy_(self.h_wctl[i], non_blocking=True)
-                    self.d_wpay[b][:self.h_wpay[i].numel()].copy_(self.h_wpay[i], non_blocking=True)
-            else:
-                self.d_tgt[b][:a1 - a0].copy_(self.h_tgt[a0:a1], non_blocking=True)
-                if self.weighted:
-                    self.d_w[b][:a1 - a0].copy_(self.h_w[a0:a1], non_blocking=True)
+            if not self.resident:
+                if i >= 2:
+                    self.s_in.wait_event(e_cmp[i - 2])  # slot b's CSR is free
+                ho = self.h_off[i]
+                (self.d_off32 if ho.dtype == torch.int32 else self.d_off)[b][:hi - lo + 1].copy_(ho, non_blocking=True)
+                if self.packed:
+                    self.d_ctl[b][:self.h_ctl[i].numel()].copy_(self.h_ctl[i], non_blocking=True)
+                    self.d_pay[b][:self.h_pay[i].numel()].copy_(self.h_pay[i], non_blocking=True)
+                    if self.weighted:
+                        self.d_wctl[b][:self.h_wctl[i].numel()].copy_(self.h_wctl[i], non_blocking=True)
+                        self.d_wpay[b][:self.h_wpay[i].numel()].copy_(self.h_wpay[i], non_blocking=True)
+                else:
+                    self.d_tgt[b][:a1 - a0].copy_(self.h_tgt[a0:a1], non_blocking=True)
+                    if self.weighted:
+                        self.d_w[b][:a1 - a0].copy_(self.h_w[a0:a1], non_blocking=True)
             e_in[i].record(self.s_in)
         self.s_cmp.wait_event(e_in[i])
         if i >= 2 and not sparse:
             self.s_cmp.wait_event(e_out[i - 2])  # Z slot b has been copied out
         with torch.cuda.stream(self.s_cmp):
-            if self.packed:
-                _lib.check(_lib.lib.gee_unpack_targets(
-                    _lib.ptr(self.d_ctl[b]), _lib.ptr(self.d_pay[b]), (a1 - a0) // 8,
-                    _lib.ptr(self.d_wctl[b]) if self.weighted else None,
-                    _lib.ptr(self.d_wpay[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
-                    _lib.ptr(self.d_w[b]) if self.weighted else None, _lib.ptr(self.d_scratch),
-                    self.scratch_bytes, _lib.stream_handle(self.s_cmp)), "gee_unpack_targets")
-            if self.h_off[i].dtype == torch.int32:  # widen on the device
-                _lib.check(_lib.lib.gee_widen_offsets(_lib.ptr(self.d_off32[b]), hi - lo + 1, _lib.ptr(self.d_off[b]),
-                                                      _lib.stream_handle(self.s_cmp)), "gee_widen_offsets")
-            v.offsets = self.d_off[b][:hi - lo + 1]
-            v.targets = self.d_tgt[b][:a1 - a0]
-            v.weights = self.d_w[b][:a1 - a0] if self.weighted else None
+            if self.resident:
+                v.offsets = v.res_off
+                v.targets = self.g.targets[a0:a1]
+                v.weights = self.g.weights[a0:a1] if self.weighted else None
+            else:
+                if self.packed:
+                    _lib.check(_lib.lib.gee_unpack_targets(
+                        _lib.ptr(self.d_ctl[b]), _lib.ptr(self.d_pay[b]), (a1 - a0) // 8,
+                        _lib.ptr(self.d_wctl[b]) if self.weighted else None,
+                        _lib.ptr(self.d_wpay[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
+                        _lib.ptr(self.d_w[b]) if self.weighted else None, _lib.ptr(self.d_scratch),
+                        self.scratch_bytes, _lib.stream_handle(self.s_cmp)), "gee_unpack_targets")
+                if self.h_off[i].dtype == torch.int32:  # widen on the device
+                    _lib.check(_lib.lib.gee_widen_offsets(_lib.ptr(self.d_off32[b]), hi - lo + 1,
+                                                          _lib.ptr(self.d_off[b]), _lib.stream_handle(self.s_cmp)),
+                               "gee_widen_offsets")
+                v.offsets = self.d_off[b][:hi - lo + 1]
+                v.targets = self.d_tgt[b][:a1 - a0]
+                v.weights = self.d_w[b][:a1 - a0] if self.weighted else None
             z = self.d_z[b][:(hi - lo) * self.k].view(hi - lo, self.k)
             emb.pull(v, z)
             if sparse:
@@ -350,39 +378,64 @@ class HostPipeline:
             self.d2h_bytes += z.numel() * 4
 
     def _sparse_worker(self, e_cmp, e_out, h_z, recorded, drained, errors):
-        """Host worker: drain chunk i, then expand chunk i-1 (slot reuse:
-        drain(i) overwrites the host slot that expand(i-2) has finished with)."""
+        """Host workers: a drainer queues chunk i's row-sparse copy-out as
+        soon as the chunk is compacted, and an expander rebuilds each copied
+        chunk's dense rows in h_z; HOST_SLOTS host slots let the next copies
+        proceed while a chunk expands (drain(i) reuses the slot of chunk
+        i - HOST_SLOTS once that one is expanded)."""
+        nv = len(self.views)
+        expanded = [threading.Event() for _ in range(nv)]
+
+        def expander():
+            try:
+                torch.cuda.set_device(self.dev_index)
+                for i in range(nv):
+                    drained[i].wait()
+                    if errors:
+                        return
+                    self._expand(i, e_out, h_z)
+                    expanded[i].set()
+            except BaseException as e:  # surfaced by run()
+                errors.append(e)
+            finally:
+                for x in expanded:
+                    x.set()
+
+        ex = threading.Thread(target=expander, daemon=True)
+        ex.start()
         try:
             torch.cuda.set_device(self.dev_index)
-            nv = len(self.views)
             for i in range(nv):
                 recorded[i].wait()
                 if errors:
                     return
+                if i >= self.HOST_SLOTS:
+                    expanded[i - self.HOST_SLOTS].wait()
+                    if errors:
+                        return
                 self._drain(i, e_cmp, e_out)
                 drained[i].set()
-                if i >= 1:
-                    self._expand(i - 1, e_out, h_z)
-            self._expand(nv - 1, e_out, h_z)
         except BaseException as e:  # surfaced by run()
             errors.append(e)
         finally:
             for d in drained:
                 d.set()
+            ex.join()
 
     def _drain(self, i, e_cmp, e_out):
         """Host: once chunk i is compacted, copy its sparse Z out (size now known)."""
         lo, hi, _, _ = self.views[i].span
-        b = i & 1
+        b = i & 1  # device compaction slot
+        h = i % self.HOST_SLOTS  # host slot
         e_cmp[i].synchronize()
         tot = int(self.h_tot[i])
         rows = hi - lo
         nb = int(_lib.lib.gee_zc_blocks(rows))
         with torch.cuda.stream(self.s_out):
-            self.hm[b][:rows * self.mw].copy_(self.cm[b][:rows * self.mw], non_blocking=True)
-            self.hb[b][:nb + 1].copy_(self.cb[b][:nb + 1], non_blocking=True)
+            self.hm[h][:rows * self.mw].copy_(self.cm[b][:rows * self.mw], non_blocking=True)
+            self.hb[h][:nb + 1].copy_(self.cb[b][:nb + 1], non_blocking=True)
             if tot:
-                self.hv[b][:tot].copy_(self.cv[b][:tot], non_blocking=True)
+                self.hv[h][:tot].copy_(self.cv[b][:tot], non_blocking=True)
             e_out[i].record(self.s_out)
         self.d2h_bytes += 8 * (rows * self.mw + nb + 1) + 4 * tot
 
@@ -391,9 +444,9 @@ class HostPipeline:
         from .formats import io_lib
 
         lo, hi, _, _ = self.views[i].span
-        b = i & 1
+        h = i % self.HOST_SLOTS
         e_out[i].synchronize()
-        rc = io_lib().gee_io_expand_rows(_lib.ptr(self.hm[b]), _lib.ptr(self.hv[b]), _lib.ptr(self.hb[b]), hi - lo,
+        rc = io_lib().gee_io_expand_rows(_lib.ptr(self.hm[h]), _lib.ptr(self.hv[h]), _lib.ptr(self.hb[h]), hi - lo,
                                          self.k, ctypes.c_void_p(h_z.data_ptr() + lo * self.k * 4), 0)
         if rc:
             raise ValidationError(io_lib().gee_io_last_error().decode())

@@ -111,21 +111,24 @@ def test_prepared_projection_and_errors():
 
 
 def test_device_residency_replays_one_graph_over_label_sets():
-    # residency="device" records the pass as a CUDA graph on the first call
-    # and replays it: every later call equals the stored graph's own pass
+    # residency="device": CUDA labels -> the pass recorded as a CUDA graph on
+    # the first call and replayed after; host labels / host out -> the
+    # resident chunked pipeline (labels in, row-sparse Z out).  Every call
+    # equals the stored graph's own pass.
     n, k = 3000, 11
     src, dst, w = _graph(31, n=n)
     g = _csr(src, dst, w, n, True)
-    p = prepare(g, k, residency="device")
+    p = prepare(g, k, residency="device", chunks=3)
     rng = np.random.default_rng(32)
     for i in range(3):
-        y = LabelVector(labels=rng.integers(0, k + 1, n), k=k)
-        z = embed_parallel(p, y)
-        assert np.array_equal(z, embed_parallel(g, y, variant="pull")), i
-    assert p._graph is not None
-    yd = LabelVector(labels=torch.as_tensor(rng.integers(0, k + 1, n), device="cuda"), k=k)
-    zd = embed_parallel(p, yd)
-    assert zd.is_cuda and torch.equal(zd, embed_parallel(p, yd))
+        lab = rng.integers(0, k + 1, n)
+        ref = embed_parallel(g, LabelVector(labels=lab, k=k), variant="pull")
+        zd = embed_parallel(p, LabelVector(labels=torch.as_tensor(lab, device="cuda"), k=k))
+        assert zd.is_cuda and np.array_equal(zd.cpu().numpy(), ref), i
+        zh = embed_parallel(p, LabelVector(labels=lab, k=k))
+        assert isinstance(zh, np.ndarray) and np.array_equal(zh, ref), i
+    assert p._graph is not None and p._pipe_res is not None and p._pipe_res.resident
+    assert p.h2d_bytes_per_call == n * 4  # only the labels cross PCIe
 
 
 @pytest.mark.parametrize("k", [1, 300])
