@@ -51,20 +51,26 @@ def build_io_library(force=False, verbose=False):
     return IO_LIB
 
 
-def build_library(force=False, verbose=False):
+CHECKED_LIB = os.path.join(PKG, "libgee_b200_checked.so")
+
+
+def build_library(force=False, verbose=False, checked=False):
     """Compile every CUDA source into paper_2402_04403_b200/libgee_b200.so
-    (one nvcc process per source, in parallel, then one link)."""
+    (one nvcc process per source, in parallel, then one link).  checked=True
+    builds libgee_b200_checked.so instead, with -DGEE_CHECKED: device-side
+    bounds checks (GEE_DCHECK) in the hot kernels; the GPU test suite runs
+    against it by putting it in place of libgee_b200.so."""
     from concurrent.futures import ThreadPoolExecutor
 
-    lib = LIB
+    lib = CHECKED_LIB if checked else LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(ROOT, "include", "gee_b200.h"), os.path.join(ROOT, "include", "gee_synth.h")]
     if not force and not _stale(lib, srcs + hdrs):
         return lib
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build_checked" if checked else "build")
     os.makedirs(objdir, exist_ok=True)
-    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + (["-DGEE_CHECKED"] if checked else [])
 
     def obj(src):
         o = os.path.join(objdir, os.path.basename(src) + ".o")

@@ -91,6 +91,26 @@ __device__ __forceinline__ uint64_t policy_evict_last()
 
 }  // namespace gee
 
+// Checked builds (_build.build_library(checked=True) -> libgee_b200_checked.so,
+// compiled with -DGEE_CHECKED): device-side bounds and invariant checks on
+// the hot kernels' memory accesses; a violation prints the condition and
+// traps the kernel.  compute-sanitizer is not available on the GPU pool, so
+// the GPU test suite is also run against this build (profiles/).
+#ifdef GEE_CHECKED
+#define GEE_DCHECK(cond)                                                                              \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("GEE_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,    \
+                   (int)blockIdx.x, (int)threadIdx.x);                                               \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define GEE_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 #define GEE_REQUIRE(cond, code, ...)      \
     do {                                  \
         if (!(cond)) {                    \

@@ -80,7 +80,7 @@ k_gather_contig(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
 template <int PER>
 __global__ void __launch_bounds__(GTHREADS, 1)
 k_gather_packed(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t *__restrict__ table, uint32_t hl,
-                uint8_t *__restrict__ cls)
+                uint8_t *__restrict__ cls, int32_t k)
 {
     constexpr uint32_t BITS = 32 / PER;
     constexpr uint32_t MASK = (1u << BITS) - 1u;
@@ -113,6 +113,7 @@ k_gather_packed(const int32_t *__restrict__ targets, int64_t arcs, const uint8_t
             const uint32_t wi = in_s ? ti / PER : 0u;
             const uint32_t sv = (head_w[wi] >> (BITS * (ti - wi * PER))) & MASK;
             l[i] = in_s ? sv : g;
+            GEE_DCHECK(wi < words && l[i] <= (uint32_t)k);
         }
         uint8_t *cp = cls + st * GSTEP + lane;
 #pragma unroll
@@ -162,7 +163,7 @@ extern "C" int gee_gather_labels_head(const int32_t *targets, int64_t arcs, cons
     auto kern = per == 8 ? k_gather_packed<8> : per == 6 ? k_gather_packed<6> : per == 5 ? k_gather_packed<5>
                                                                                        : k_gather_packed<4>;
     GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    kern<<<gee::sm_count(), GTHREADS, sh, gee::as_stream(stream)>>>(targets, arcs, tab, (uint32_t)hl, cls);
+    kern<<<gee::sm_count(), GTHREADS, sh, gee::as_stream(stream)>>>(targets, arcs, tab, (uint32_t)hl, cls, k);
     return gee::check_launch("k_gather_packed");
 }
 

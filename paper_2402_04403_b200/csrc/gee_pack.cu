@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(PT) k_unpack_rows(const uint8_t *__restrict__ 
             if (i < real) {
                 v += ld_delta(p + i * w, w);
                 o[i] = v;
+                GEE_DCHECK(v < sentinel);
             } else {
                 o[i] = sentinel;
             }

@@ -59,6 +59,7 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned 
         c = count(i, c);
         if (cold) {
             cold[i] = (LT)c;
+            GEE_DCHECK(r < n_hot);
             if (r >= 0) table[r] = (LT)c;  // hot tier copy (gee_hot.cu)
         }
     };
@@ -89,6 +90,7 @@ k_label_hist(const int32_t *__restrict__ labels, int64_t n, int32_t k, unsigned 
                               c3 = count(4 * q + 3, v.w);
                 reinterpret_cast<uint32_t *>(cold)[q] = (uint32_t)c0 | (uint32_t)c1 << 8 | (uint32_t)c2 << 16 |
                                                         (uint32_t)c3 << 24;
+                GEE_DCHECK(r.x < n_hot && r.y < n_hot && r.z < n_hot && r.w < n_hot);
                 if (r.x >= 0) table[r.x] = (LT)c0;
                 if (r.y >= 0) table[r.y] = (LT)c1;
                 if (r.z >= 0) table[r.z] = (LT)c2;

@@ -93,6 +93,7 @@ __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const
         // no read-out.  C3 1.58 -> 1.48 ms.  Weighted rows keep the window:
         // the 64-bit combine, run in a divergent branch every round, cost
         // C4 7.8 -> 9.1 ms.
+        GEE_DCHECK(-so - 2 < 32);
         float *zr = zb + (int64_t)(-so - 2) * kk;
         uint32_t cc[BU];
         unsigned long long qq[BU];
@@ -120,7 +121,9 @@ __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const
         // masked arcs (pads, unlabeled, other passes, past the block) add into
         // the lane's trash word: branch-free (predicating the atomics off
         // measured slower: 8.20 vs 8.01 ms on C4)
+        GEE_DCHECK(c <= (uint32_t)kk);
         const int idx = (ok && c != 0u) ? so + (int)c : trash;
+        GEE_DCHECK(idx >= 0 && idx < hoff);
         if (WEIGHTED) {
             const unsigned long long q = (unsigned long long)__float2ll_rn(wa[u] * qscale);
             atomicAdd(vw + idx, (uint32_t)q & ((1u << BLOCK_SPLIT) - 1u));
@@ -491,6 +494,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
                             s0 = (float)lo.x;
                             s1 = (float)lo.y;
                         }
+                        GEE_DCHECK(s_row[sl] >= 0 && s_row[sl] < 32 && r0 + s_row[sl] < n);
                         __stcs(reinterpret_cast<float2 *>(zc + s_row[sl] * kk), make_float2(s0 * f.x, s1 * f.y));
                     }
                 }
@@ -575,6 +579,7 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
         it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= n_items) break;
         const int64_t b0 = item_first[it], e1 = item_end[it];
+        GEE_DCHECK(b0 >= 0 && b0 < e1 && e1 <= arcs);
         unsigned long long sum[HCOL];
 #pragma unroll
         for (int j = 0; j < HCOL; j++) sum[j] = 0ull;
@@ -604,6 +609,7 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
             for (int u = 0; u < BU; u++) {
                 uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
                 if (!full && (a0 + u < b0 || a0 + u >= e1)) c = 0u;
+                GEE_DCHECK(c <= (uint32_t)kk);
                 if (c == 0u) continue;
                 uint32_t *p = v + 3 + c;
                 if (WEIGHTED) {

@@ -74,6 +74,7 @@ __device__ __forceinline__ void wide_add(const uint32_t (&lab)[UNR], const float
 #pragma unroll
     for (int u = 0; u < UNR; u++) {
         if (lab[u] == 0u) continue;
+        GEE_DCHECK(lab[u] - 1u < (uint32_t)kp);
         uint32_t *p = win + (lab[u] - 1);
         if (WEIGHTED) {
             const unsigned long long q = (unsigned long long)__float2ll_rn(wt[u] * qscale);
