@@ -98,6 +98,7 @@ class HostPipeline:
     """
 
     HOST_SLOTS = 3  # row-sparse Z chunks in host memory: one copying out while two expand
+    DENSE_EVERY_RESIDENT = 6  # resident: 1 chunk in 6 copied out dense (C4: none 298, 6 267, 4 273, 3 286, 2 338 ms)
 
     def __init__(self, g: DeviceGraph, k, chunks=16, device=None, packed=None, resident=False):
         if not g.has_pull or g.hot_k != k:
@@ -258,13 +259,24 @@ class HostPipeline:
         self.h_tot = self.arena.empty(max(1, len(self.views)), torch.int64).zero_()
         self.mw = mw
 
-    def run(self, h_labels, h_z, emb: Embedder, sparse=True, inv=None):
+    def run(self, h_labels, h_z, emb: Embedder, sparse=True, inv=None, dense_every=None):
         """labels (pinned host int32[n]) -> h_z (pinned host float32[n, k]).
-        ``inv`` (float64[k+1]) replaces 1/count (a caller's projection)."""
+        ``inv`` (float64[k+1]) replaces 1/count (a caller's projection).
+        With ``sparse``, every ``dense_every``-th chunk still leaves dense,
+        copied by the DMA engine straight into h_z: the host threads that
+        rebuild the row-sparse chunks are the bound once the graph does not
+        cross PCIe (resident), and the device-to-host direction is otherwise
+        idle (default: every 6th chunk when resident, none when streaming,
+        where the copy-in is the bound)."""
         if h_z.shape != (self.n, self.k) or h_z.dtype != torch.float32 or not h_z.is_contiguous():
             raise ValidationError("h_z must be a contiguous float32 (n, k) host tensor")
         if sparse:
             self._sparse_slots()
+        if dense_every is None:
+            dense_every = self.DENSE_EVERY_RESIDENT if self.resident else 0
+        nv = len(self.views)
+        self._dense = [(not sparse) or (dense_every > 0 and i % dense_every == dense_every - 1) for i in range(nv)]
+        self._last_compact = [-1, -1]  # last sparse chunk that used each device compaction slot
         ev = lambda: torch.cuda.Event()  # noqa: E731
         e_lab = ev()
         with torch.cuda.stream(self.s_in):
@@ -334,7 +346,8 @@ class HostPipeline:
                         self.d_w[b][:a1 - a0].copy_(self.h_w[a0:a1], non_blocking=True)
             e_in[i].record(self.s_in)
         self.s_cmp.wait_event(e_in[i])
-        if i >= 2 and not sparse:
+        dense = self._dense[i]
+        if i >= 2 and self._dense[i - 2]:
             self.s_cmp.wait_event(e_out[i - 2])  # Z slot b has been copied out
         with torch.cuda.stream(self.s_cmp):
             if self.resident:
@@ -358,19 +371,21 @@ class HostPipeline:
                 v.weights = self.d_w[b][:a1 - a0] if self.weighted else None
             z = self.d_z[b][:(hi - lo) * self.k].view(hi - lo, self.k)
             emb.pull(v, z)
-            if sparse:
-                if i >= 2:
-                    drained[i - 2].wait()  # the worker has queued chunk i-2's copy-out
+            if not dense:
+                j = self._last_compact[b]  # the previous sparse chunk on compaction slot b
+                if j >= 0:
+                    drained[j].wait()  # the worker has queued chunk j's copy-out
                     if errors:
                         raise errors[0]
-                    self.s_cmp.wait_event(e_out[i - 2])  # compact slot b has been copied out
+                    self.s_cmp.wait_event(e_out[j])  # compact slot b has been copied out
+                self._last_compact[b] = i
                 _lib.check(_lib.lib.gee_z_compact(_lib.ptr(z), hi - lo, self.k, _lib.ptr(self.cm[b]),
                                                   _lib.ptr(self.cb[b]), _lib.ptr(self.cv[b]),
                                                   _lib.stream_handle(self.s_cmp)), "gee_z_compact")
                 nb = int(_lib.lib.gee_zc_blocks(hi - lo))
                 self.h_tot[i:i + 1].copy_(self.cb[b][nb:nb + 1], non_blocking=True)
             e_cmp[i].record(self.s_cmp)
-        if not sparse:
+        if dense:
             self.s_out.wait_event(e_cmp[i])
             with torch.cuda.stream(self.s_out):
                 h_z[lo:hi].copy_(z, non_blocking=True)
@@ -393,7 +408,8 @@ class HostPipeline:
                     drained[i].wait()
                     if errors:
                         return
-                    self._expand(i, e_out, h_z)
+                    if not self._dense[i]:  # a dense chunk went straight into h_z
+                        self._expand(i, e_out, h_z)
                     expanded[i].set()
             except BaseException as e:  # surfaced by run()
                 errors.append(e)
@@ -409,11 +425,12 @@ class HostPipeline:
                 recorded[i].wait()
                 if errors:
                     return
-                if i >= self.HOST_SLOTS:
-                    expanded[i - self.HOST_SLOTS].wait()
-                    if errors:
-                        return
-                self._drain(i, e_cmp, e_out)
+                if not self._dense[i]:
+                    if i >= self.HOST_SLOTS:
+                        expanded[i - self.HOST_SLOTS].wait()
+                        if errors:
+                            return
+                    self._drain(i, e_cmp, e_out)
                 drained[i].set()
         except BaseException as e:  # surfaced by run()
             errors.append(e)

@@ -578,6 +578,10 @@ def test_host_pipeline_matches_resident_pull(chunks, packed):
             assert 0 < pipe.d2h_bytes < n * k * 4
         else:
             assert pipe.d2h_bytes == n * k * 4
+    for dense_every in (1, 2, 3):  # row-sparse chunks mixed with dense ones
+        h_z.fill_(float("nan"))
+        pipe.run(y.cpu().pin_memory(), h_z, emb, dense_every=dense_every)
+        assert torch.equal(h_z, z_ref), dense_every
     exp = oracle.serial_embed(src.cpu().numpy(), dst.cpu().numpy(), w.cpu().numpy(), y.cpu().numpy(), n, k)
     assert rel_err(h_z.numpy(), exp) <= TOL
 

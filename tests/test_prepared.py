@@ -118,7 +118,7 @@ def test_device_residency_replays_one_graph_over_label_sets():
     n, k = 3000, 11
     src, dst, w = _graph(31, n=n)
     g = _csr(src, dst, w, n, True)
-    p = prepare(g, k, residency="device", chunks=3)
+    p = prepare(g, k, residency="device", chunks=8)  # chunk 5 leaves dense, the rest row-sparse
     rng = np.random.default_rng(32)
     for i in range(3):
         lab = rng.integers(0, k + 1, n)
