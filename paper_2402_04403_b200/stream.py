@@ -98,6 +98,7 @@ class HostPipeline:
     """
 
     HOST_SLOTS = 3  # row-sparse Z chunks in host memory: one copying out while two expand
+    DENSE_EVERY_STREAMED = 0  # streaming: the copy-in is the bound, no dense chunks
     DENSE_EVERY_RESIDENT = 6  # resident: 1 chunk in 6 copied out dense (C4: none 298, 6 267, 4 273, 3 286, 2 338 ms)
 
     def __init__(self, g: DeviceGraph, k, chunks=16, device=None, packed=None, resident=False):
@@ -273,7 +274,7 @@ class HostPipeline:
         if sparse:
             self._sparse_slots()
         if dense_every is None:
-            dense_every = self.DENSE_EVERY_RESIDENT if self.resident else 0
+            dense_every = self.DENSE_EVERY_RESIDENT if self.resident else self.DENSE_EVERY_STREAMED
         nv = len(self.views)
         self._dense = [(not sparse) or (dense_every > 0 and i % dense_every == dense_every - 1) for i in range(nv)]
         self._last_compact = [-1, -1]  # last sparse chunk that used each device compaction slot

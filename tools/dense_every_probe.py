@@ -18,11 +18,12 @@ csr = CsrGraph(n=n, offsets=c.offsets.cpu().numpy(), targets=c.targets.cpu().num
 del c, src, dst, w
 torch.cuda.empty_cache()
 yl = LabelVector(labels=y.cpu().numpy(), k=k)
-p = prepare(csr, k, residency="device")
+mode = sys.argv[1] if len(sys.argv) > 1 else "device"
+p = prepare(csr, k, residency=mode)
 h_z = np.empty((n, k), dtype=np.float32)
 out = {}
 for de in (0, 6, 4, 3, 2, 0, 4):
-    HostPipeline.DENSE_EVERY_RESIDENT = de
+    HostPipeline.DENSE_EVERY_RESIDENT = HostPipeline.DENSE_EVERY_STREAMED = de
     embed_parallel(p, yl, out=h_z)
     ts = []
     for _ in range(3):
