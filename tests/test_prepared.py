@@ -131,14 +131,16 @@ def test_device_residency_replays_one_graph_over_label_sets():
     assert p.h2d_bytes_per_call == n * 4  # only the labels cross PCIe
 
 
+@pytest.mark.parametrize("residency", ["host", "device"])
 @pytest.mark.parametrize("k", [1, 300])
-def test_prepared_host_residency_small_and_wide_k(k):
-    # k = 1 and the wide-K reducer (k > 255) through the streamed path
+def test_prepared_host_results_small_and_wide_k(k, residency):
+    # k = 1 and the wide-K reducer (k > 255) through the streamed path and the
+    # resident chunked path (7 chunks: chunk 5 leaves dense)
     n = 2500
     src, dst, w = _graph(41, n=n, s=25_000)
     g = _csr(src, dst, w, n, True)
     y = LabelVector(labels=np.random.default_rng(42).integers(0, k + 1, n), k=k)
-    p = prepare(g, k, chunks=3)
+    p = prepare(g, k, chunks=7, residency=residency)
     z = embed_parallel(p, y)
     assert np.array_equal(z, embed_parallel(g, y, variant="pull"))
     assert rel_err(z, oracle.serial_embed(src, dst, w, y.labels, n, k)) <= 1e-4
