@@ -225,27 +225,33 @@ int gee_z_compact(const float *z, int64_t rows, int32_t k, unsigned long long *m
  * reference passes its CsrGraph to embed_parallel in host memory
  * (encoder.py:123-194, graph.py:54-91); these code the prepared, padded,
  * slot-sorted CSR in groups of 8 arcs so fewer bytes cross PCIe:
- *   ctl:  one byte per group ((W-1) | pads << 2 | row_start << 6);
- *   payload: the real arcs' targets as W-byte little-endian deltas (a row's
- *         first arc absolute);
+ *   ctl:  one byte per group ((b-1) | pads << 5), b = 1..32 bits per value;
+ *   payload: the real arcs' targets as b-bit deltas in one little-endian
+ *         stream of u32 words (a row's first arc absolute); row starts are
+ *         recovered from the padded offsets;
  *   wctl: one byte per group (B | e << 2): B = 1..3 bytes per weight of an
  *         integer k with w = k * 2^-e exactly (lossless group fixed point),
  *         B = 0 raw f32 bits;
  *   wpayload: the real arcs' weights (no pads).
  * gee_pack_targets (graph preparation; allocates, synchronises) writes
- * ctl[padded_arcs/8], up to 4*padded_arcs payload bytes and, given the
- * padded weights, wctl[padded_arcs/8] and up to 4*padded_arcs wpayload bytes,
- * returning both sizes.  gee_unpack_targets (stream-ordered, no allocation;
- * scratch >= gee_unpack_scratch_bytes(groups)) rebuilds the padded targets
- * (pads = sentinel) and, given wctl/wpayload, the padded weights (pads 0),
- * bit for bit. */
+ * ctl[padded_arcs/8], up to 4*padded_arcs payload bytes (4-byte aligned)
+ * and, given the padded weights, wctl[padded_arcs/8] and up to
+ * 4*padded_arcs wpayload bytes, returning both sizes (the payload size is a
+ * whole number of u32 words).  gee_unpack_targets (stream-ordered, no
+ * allocation; scratch >= gee_unpack_scratch_bytes(groups)) takes the chunk's
+ * padded offsets (int64[rows+1], chunk-relative) and rebuilds the padded
+ * targets (pads = sentinel) and, given wpayload and either wctl or
+ * wctl_uniform >= 0 (the wctl byte of every group), the padded weights
+ * (pads 0), bit for bit.  The payload buffer must extend 4 bytes past the
+ * packed size (the bit reader loads the word after a value's last word). */
 size_t gee_unpack_scratch_bytes(int64_t groups);
 int gee_pack_targets(const int64_t *padded_offsets, int64_t rows, const int32_t *targets, const float *w_padded,
                      int64_t padded_arcs, int32_t sentinel, uint8_t *ctl, uint8_t *payload, int64_t *payload_bytes,
                      uint8_t *wctl, uint8_t *wpayload, int64_t *wpayload_bytes, void *stream);
-int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t groups, const uint8_t *wctl,
-                       const uint8_t *wpayload, int32_t sentinel, int32_t *targets, float *w_padded, void *scratch,
-                       size_t scratch_bytes, void *stream);
+int gee_unpack_targets(const uint8_t *ctl, const uint8_t *payload, int64_t groups, const int64_t *padded_offsets,
+                       int64_t rows, const uint8_t *wctl, int32_t wctl_uniform, const uint8_t *wpayload,
+                       int32_t sentinel, int32_t *targets, float *w_padded, void *scratch, size_t scratch_bytes,
+                       void *stream);
 
 /* Chunk-relative CSR offsets travel host -> device as int32 (half the
  * bytes); widen them to the int64 the pull reads (stream-ordered). */

@@ -61,7 +61,7 @@ SIGNATURES = {
     "gee_unpack_scratch_bytes": (c_size, [c_i64]),
     "gee_pack_targets": (c_int, [vp, c_i64, vp, vp, c_i64, c_i32, vp, vp, ctypes.POINTER(c_i64), vp, vp,
                                  ctypes.POINTER(c_i64), vp]),
-    "gee_unpack_targets": (c_int, [vp, vp, c_i64, vp, vp, c_i32, vp, vp, vp, c_size, vp]),
+    "gee_unpack_targets": (c_int, [vp, vp, c_i64, vp, c_i64, vp, c_i32, vp, c_i32, vp, vp, vp, c_size, vp]),
     "gee_reduce_wide": (c_int, [vp, c_i64, vp, vp, vp, c_i32, c_i32, vp, vp, c_i64, vp, vp]),
     "gee_reduce_heavy_plan": (c_int, [vp, c_i64, c_i64, vp, ctypes.POINTER(c_i64), vp]),
     "gee_pad_offsets": (c_int, [vp, c_i64, c_i64, vp, vp, vp]),

@@ -27,12 +27,14 @@ queue stays ahead of both.
 
 The targets cross PCIe packed (``packed=True``, the default for the padded
 layout): gee_pack_targets codes each chunk's slot-sorted targets as groups of
-8 byte-width deltas at preparation time and its weights, without the row
+8 bit-width deltas at preparation time and its weights, without the row
 padding, as lossless group fixed point (1-3 bytes per weight when the group's
-weights are exact multiples of a common power of two, else raw f32);
-gee_unpack_targets rebuilds the padded targets and weights on the compute
-stream before the chunk's pull (C4: 31 GB of targets and weights become
-about 20 GB; the rebuilt arrays are bit-identical, so Z is too).
+weights are exact multiples of a common power of two, else raw f32; a chunk
+whose groups all share one weight code sends that code instead of the
+per-group bytes); gee_unpack_targets rebuilds the padded targets and weights
+on the compute stream before the chunk's pull (C4: 31 GB of targets and
+weights become about 18 GB; the rebuilt arrays are bit-identical, so Z is
+too).
 
 Graph preparation (CSR build, hot-label plan, per-chunk heavy-row items,
 pinned host copies) happens once in ``HostPipeline(...)``. It is outside
@@ -123,7 +125,7 @@ class HostPipeline:
         if g.hot_rank is not None and not self.resident:
             self.h_hot = [pin(g.hot_bits), pin(g.hot_pref), pin(g.hot_list)]
         self.n_hot = g.n_hot
-        # packed targets (gee_pack_targets): per-8-arc-group byte-width deltas
+        # packed targets (gee_pack_targets): per-8-arc-group bit-width deltas
         # and the real arcs' weights (pads rebuilt on the device)
         self.packed = (g.padded == 8 and not self.resident) if packed is None else bool(packed)
         if self.packed and (g.padded != 8 or self.resident):
@@ -132,7 +134,7 @@ class HostPipeline:
         self.h_tgt = None if (self.packed or self.resident) else pin(g.targets)
         self.h_w = None if (self.packed or self.resident) else pin(g.weights)
         self.g = g if self.resident else None
-        self.h_ctl, self.h_pay, self.h_wctl, self.h_wpay = [], [], [], []
+        self.h_ctl, self.h_pay, self.h_wctl, self.h_wpay, self.wuni = [], [], [], [], []
         self.h_off = []
         self.views = []
         max_rows = max_arcs = 0
@@ -171,7 +173,8 @@ class HostPipeline:
         # device slots (double-buffered) and the labels / hot ranks
         if self.packed:
             self.d_ctl = [torch.empty(max(1, max_arcs // 8), dtype=torch.uint8, device=dev) for _ in range(2)]
-            self.d_pay = [torch.empty(max(1, max(t.numel() for t in self.h_pay)), dtype=torch.uint8, device=dev)
+            # + 8 bytes: the bit reader loads the word after a value's last word
+            self.d_pay = [torch.empty(max(t.numel() for t in self.h_pay) + 8, dtype=torch.uint8, device=dev)
                           for _ in range(2)]
             self.d_wctl = [torch.empty(max(1, max_arcs // 8), dtype=torch.uint8, device=dev)
                            if self.weighted else None for _ in range(2)]
@@ -219,7 +222,15 @@ class HostPipeline:
         self.h_ctl.append(pin(ctl[:groups]))
         self.h_pay.append(pin(pay[:int(nb.value)]))
         empty = torch.empty(0, dtype=torch.uint8)
-        self.h_wctl.append(pin(wctl[:groups]) if self.weighted else empty)
+        # one weight code for the whole chunk (C4: every group is 3-byte fixed
+        # point with e = 24): send it instead of the per-group bytes
+        wu = -1
+        if self.weighted and groups:
+            w0 = int(wctl[0])
+            if bool((wctl[:groups] == w0).all()):
+                wu = w0
+        self.wuni.append(wu)
+        self.h_wctl.append(pin(wctl[:groups]) if self.weighted and wu < 0 else empty)
         self.h_wpay.append(pin(wpay[:int(nwb.value)]) if self.weighted else empty)
         del pay, wpay
 
@@ -339,7 +350,8 @@ class HostPipeline:
                     self.d_ctl[b][:self.h_ctl[i].numel()].copy_(self.h_ctl[i], non_blocking=True)
                     self.d_pay[b][:self.h_pay[i].numel()].copy_(self.h_pay[i], non_blocking=True)
                     if self.weighted:
-                        self.d_wctl[b][:self.h_wctl[i].numel()].copy_(self.h_wctl[i], non_blocking=True)
+                        if self.h_wctl[i].numel():
+                            self.d_wctl[b][:self.h_wctl[i].numel()].copy_(self.h_wctl[i], non_blocking=True)
                         self.d_wpay[b][:self.h_wpay[i].numel()].copy_(self.h_wpay[i], non_blocking=True)
                 else:
                     self.d_tgt[b][:a1 - a0].copy_(self.h_tgt[a0:a1], non_blocking=True)
@@ -356,17 +368,18 @@ class HostPipeline:
                 v.targets = self.g.targets[a0:a1]
                 v.weights = self.g.weights[a0:a1] if self.weighted else None
             else:
-                if self.packed:
-                    _lib.check(_lib.lib.gee_unpack_targets(
-                        _lib.ptr(self.d_ctl[b]), _lib.ptr(self.d_pay[b]), (a1 - a0) // 8,
-                        _lib.ptr(self.d_wctl[b]) if self.weighted else None,
-                        _lib.ptr(self.d_wpay[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
-                        _lib.ptr(self.d_w[b]) if self.weighted else None, _lib.ptr(self.d_scratch),
-                        self.scratch_bytes, _lib.stream_handle(self.s_cmp)), "gee_unpack_targets")
                 if self.h_off[i].dtype == torch.int32:  # widen on the device
                     _lib.check(_lib.lib.gee_widen_offsets(_lib.ptr(self.d_off32[b]), hi - lo + 1,
                                                           _lib.ptr(self.d_off[b]), _lib.stream_handle(self.s_cmp)),
                                "gee_widen_offsets")
+                if self.packed:  # (the decoder marks row starts from the offsets)
+                    wu = self.wuni[i]
+                    _lib.check(_lib.lib.gee_unpack_targets(
+                        _lib.ptr(self.d_ctl[b]), _lib.ptr(self.d_pay[b]), (a1 - a0) // 8, _lib.ptr(self.d_off[b]),
+                        hi - lo, _lib.ptr(self.d_wctl[b]) if self.weighted and wu < 0 else None, wu,
+                        _lib.ptr(self.d_wpay[b]) if self.weighted else None, self.sentinel, _lib.ptr(self.d_tgt[b]),
+                        _lib.ptr(self.d_w[b]) if self.weighted else None, _lib.ptr(self.d_scratch),
+                        self.scratch_bytes, _lib.stream_handle(self.s_cmp)), "gee_unpack_targets")
                 v.offsets = self.d_off[b][:hi - lo + 1]
                 v.targets = self.d_tgt[b][:a1 - a0]
                 v.weights = self.d_w[b][:a1 - a0] if self.weighted else None
