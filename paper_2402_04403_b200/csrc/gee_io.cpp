@@ -1104,6 +1104,57 @@ inline void stream_copy(char *dst, const char *src, size_t bytes)
     memcpy(dst + body, src + body, bytes - body);
 }
 
+// AVX-512 rebuild of rows [s0, s1) into stage (row-major, k floats per row):
+// each 16-class piece of a row is one masked expand-load of the row's next
+// packed values (zeros where the mask is clear) and one masked store, so no
+// zero fill and no per-value scatter; returns the advanced value position.
+// The masked stores never write past a row's k floats.
+__attribute__((target("avx512f,avx512vl,popcnt"))) int64_t expand_rows_avx512(const uint64_t *mask, const float *vals,
+                                                                               int64_t pos, int64_t s0, int64_t s1,
+                                                                               int k, int mw, float *stage)
+{
+    for (int64_t r = s0; r < s1; r++) {
+        float *row = stage + (r - s0) * k;
+        for (int j = 0; j < mw; j++) {
+            const uint64_t m = mask[r * mw + j];
+            for (int q = 0; q < 4; q++) {
+                const int c0 = 64 * j + 16 * q;
+                if (c0 >= k) break;
+                const __mmask16 mm = (__mmask16)(m >> (16 * q));
+                const __m512 v = _mm512_maskz_expandloadu_ps(mm, vals + pos);
+                pos += _mm_popcnt_u32((unsigned)mm);
+                const int valid = k - c0 < 16 ? k - c0 : 16;
+                _mm512_mask_storeu_ps(row + c0, (__mmask16)(valid == 16 ? 0xffffu : (1u << valid) - 1u), v);
+            }
+        }
+    }
+    return pos;
+}
+
+// dst <- src (bytes), 64-byte non-temporal stores where dst is aligned
+__attribute__((target("avx512f"))) void stream_copy64(char *dst, const char *src, size_t bytes)
+{
+    size_t head = (64 - ((uintptr_t)dst & 63)) & 63;
+    if (head > bytes) head = bytes;
+    memcpy(dst, src, head);
+    dst += head, src += head, bytes -= head;
+    const size_t body = bytes & ~(size_t)63;
+    for (size_t i = 0; i < body; i += 64)
+        _mm512_stream_si512(reinterpret_cast<__m512i *>(dst + i),
+                            _mm512_loadu_si512(reinterpret_cast<const void *>(src + i)));
+    memcpy(dst + body, src + body, bytes - body);
+}
+
+// AVX-512 path unless the CPU lacks it or GEE_IO_SCALAR is set (tests
+// compare both paths)
+bool use_avx512()
+{
+    static const bool cpu = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512vl");
+    if (!cpu) return false;
+    const char *e = getenv("GEE_IO_SCALAR");
+    return !(e && *e && *e != '0');
+}
+
 }  // namespace
 
 extern "C" int gee_io_expand_rows(const uint64_t *mask, const float *vals, const int64_t *block_off, int64_t rows,
@@ -1116,12 +1167,22 @@ extern "C" int gee_io_expand_rows(const uint64_t *mask, const float *vals, const
     const int64_t nb = (rows + GEE_ZC_BLOCK_ROWS - 1) / GEE_ZC_BLOCK_ROWS;
     if (block_off[nb] > 0 && !vals) return fail(GEE_IO_ERR_INVALID, "NULL vals");
     constexpr int SUB = 32;  // rows staged per streaming copy
+    const bool simd = use_avx512();
     parallel_for(nb, threads, [&](int64_t b) {
         thread_local std::vector<float> stage;
         if (stage.size() < (size_t)SUB * k) stage.resize((size_t)SUB * k);
         int64_t pos = block_off[b];
         const int64_t r0 = b * GEE_ZC_BLOCK_ROWS;
         const int64_t r1 = std::min(rows, r0 + GEE_ZC_BLOCK_ROWS);
+        if (simd) {
+            for (int64_t s0 = r0; s0 < r1; s0 += SUB) {
+                const int64_t s1 = std::min(r1, s0 + SUB);
+                pos = expand_rows_avx512(mask, vals, pos, s0, s1, k, mw, stage.data());
+                stream_copy64(reinterpret_cast<char *>(z + s0 * k), reinterpret_cast<const char *>(stage.data()),
+                              (size_t)(s1 - s0) * k * sizeof(float));
+            }
+            return;
+        }
         for (int64_t s0 = r0; s0 < r1; s0 += SUB) {
             const int64_t s1 = std::min(r1, s0 + SUB);
             std::fill(stage.begin(), stage.begin() + (s1 - s0) * k, 0.0f);

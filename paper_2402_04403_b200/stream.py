@@ -101,7 +101,17 @@ class HostPipeline:
 
     HOST_SLOTS = 3  # row-sparse Z chunks in host memory: one copying out while two expand
     DENSE_EVERY_STREAMED = 0  # streaming: the copy-in is the bound, no dense chunks
-    DENSE_EVERY_RESIDENT = 6  # resident: 1 chunk in 6 copied out dense (C4: none 298, 6 267, 4 273, 3 286, 2 338 ms)
+    # resident: 1 chunk in 8 copied out dense (C4 with the AVX-512 expansion: none 239-241, 12 251, 8 232-235,
+    # 6 247-252, 4 266 ms; with the scalar expansion: none 298, 6 267, 4 273, 3 286, 2 338 ms)
+    DENSE_EVERY_RESIDENT = 8
+    # host threads rebuilding a chunk's dense rows (0: all).  Streaming, the
+    # expansion's stores share host memory with the copy-in's DMA reads, so
+    # fewer threads finish sooner (C4, AVX-512 expansion: 4 / 8 / 12 / 16
+    # threads 571 / 387 / 419 / 434 ms); resident, the expansion is the bound
+    # (4 / 8 / 12 / 16: 474 / 282 / 249 / 244 ms)
+    EXPAND_THREADS_STREAMED = 8
+    EXPAND_THREADS_RESIDENT = 0
+    EXPAND_THREADS = None  # overrides both when set
 
     def __init__(self, g: DeviceGraph, k, chunks=16, device=None, packed=None, resident=False):
         if not g.has_pull or g.hot_k != k:
@@ -278,7 +288,7 @@ class HostPipeline:
         copied by the DMA engine straight into h_z: the host threads that
         rebuild the row-sparse chunks are the bound once the graph does not
         cross PCIe (resident), and the device-to-host direction is otherwise
-        idle (default: every 6th chunk when resident, none when streaming,
+        idle (default: every 8th chunk when resident, none when streaming,
         where the copy-in is the bound)."""
         if h_z.shape != (self.n, self.k) or h_z.dtype != torch.float32 or not h_z.is_contiguous():
             raise ValidationError("h_z must be a contiguous float32 (n, k) host tensor")
@@ -302,6 +312,8 @@ class HostPipeline:
             emb.project(self.d_y, validate=False, g=self.proj, inv=inv)
         nv = len(self.views)
         e_in = [ev() for _ in self.views]
+        self._copyin_done = e_in[-1] if e_in else None
+        self._last_issued = False  # (an event not yet recorded queries as complete)
         e_cmp = [ev() for _ in self.views]
         e_out = [ev() for _ in self.views]
         self.d2h_bytes = 0
@@ -319,6 +331,7 @@ class HostPipeline:
         try:
             for i, v in enumerate(self.views):
                 self._issue_chunk(i, v, emb, h_z, sparse, e_in, e_cmp, e_out, drained, errors)
+                self._last_issued = i == nv - 1
                 recorded[i].set()
         except BaseException as e:
             errors.append(e)  # stops the worker before it drains an unissued chunk
@@ -470,6 +483,18 @@ class HostPipeline:
             e_out[i].record(self.s_out)
         self.d2h_bytes += 8 * (rows * self.mw + nb + 1) + 4 * tot
 
+    def _expand_threads(self):
+        if self.EXPAND_THREADS is not None:
+            return int(self.EXPAND_THREADS)
+        if self.resident:
+            return self.EXPAND_THREADS_RESIDENT
+        # once the last chunk's copy-in has landed, the DMA reads are done:
+        # the tail chunks expand on every host thread
+        done = self._copyin_done
+        if self._last_issued and done is not None and done.query():
+            return 0
+        return self.EXPAND_THREADS_STREAMED
+
     def _expand(self, i, e_out, h_z):
         """Host: rebuild chunk i's dense Z rows in the caller's buffer."""
         from .formats import io_lib
@@ -478,7 +503,8 @@ class HostPipeline:
         h = i % self.HOST_SLOTS
         e_out[i].synchronize()
         rc = io_lib().gee_io_expand_rows(_lib.ptr(self.hm[h]), _lib.ptr(self.hv[h]), _lib.ptr(self.hb[h]), hi - lo,
-                                         self.k, ctypes.c_void_p(h_z.data_ptr() + lo * self.k * 4), 0)
+                                         self.k, ctypes.c_void_p(h_z.data_ptr() + lo * self.k * 4),
+                                         self._expand_threads())
         if rc:
             raise ValidationError(io_lib().gee_io_last_error().decode())
 

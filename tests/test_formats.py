@@ -237,11 +237,15 @@ def test_weight_repr_matches_python(tmp_path):
     assert got == [repr(float(x)) for x in w]
 
 
-@pytest.mark.parametrize("rows,k", [(1, 1), (3000, 50), (2048, 64), (1500, 130), (0, 5)])
-def test_expand_rows_rebuilds_dense_z(rows, k):
+@pytest.mark.parametrize("scalar", [False, True])
+@pytest.mark.parametrize("rows,k", [(1, 1), (3000, 50), (2048, 64), (1500, 130), (700, 17), (1100, 200), (0, 5)])
+def test_expand_rows_rebuilds_dense_z(rows, k, scalar, monkeypatch):
     """gee_io_expand_rows (the host half of the streamed pass's row-sparse
     Z copy) from the format built in numpy: u64 row masks, packed nonzeros,
-    per-1024-row value offsets; every bit pattern survives, -0.0 included."""
+    per-1024-row value offsets; every bit pattern survives, -0.0 included.
+    Both the AVX-512 expand-load path (where the CPU has it) and the scalar
+    path (GEE_IO_SCALAR=1)."""
+    monkeypatch.setenv("GEE_IO_SCALAR", "1" if scalar else "0")
     rng = np.random.default_rng(rows * 7 + k)
     z = np.where(rng.random((rows, k)) < 0.2, rng.standard_normal((rows, k)), 0.0).astype(np.float32)
     if rows:

@@ -22,7 +22,7 @@ mode = sys.argv[1] if len(sys.argv) > 1 else "device"
 p = prepare(csr, k, residency=mode)
 h_z = np.empty((n, k), dtype=np.float32)
 out = {}
-for de in (0, 6, 4, 3, 2, 0, 4):
+for de in (0, 12, 8, 6, 4, 0, 8, 6):
     HostPipeline.DENSE_EVERY_RESIDENT = HostPipeline.DENSE_EVERY_STREAMED = de
     embed_parallel(p, yl, out=h_z)
     ts = []
