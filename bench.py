@@ -70,6 +70,11 @@ def parse():
                     help="skip the secondary e2e line with the prepared graph resident in HBM")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-push", action="store_true")
+    ap.add_argument("--heavy-layout", default="tiles", choices=["rows", "tiles"],
+                    help="heavy rows inside the row-major CSR, or relocated into the tile-major region "
+                         "(DeviceGraph.tile_heavy; graph preparation)")
+    ap.add_argument("--tile-slots", type=int, default=None, help="label-table slots per shared-memory tile")
+    ap.add_argument("--tile-max", type=int, default=None, help="tiles (slots past them stay on the L2 path)")
     ap.add_argument("--graph", action="store_true",
                     help="also time the step replayed as one CUDA graph (Embedder.capture; launch-bound configs)")
     return ap.parse_args()
@@ -535,6 +540,8 @@ def main():
     # warm-up (also validates labels once); the hot-label tier is graph prep
     t0 = time.perf_counter()
     g.prepare_hot(k)
+    if args.heavy_layout == "tiles":
+        g.tile_heavy(tile_slots=args.tile_slots, max_tiles=args.tile_max)
     if world > 1:  # every rank rounds weights with the whole graph's exponent
         from paper_2402_04403_b200.shard import unify_scale_distributed
 
@@ -586,15 +593,19 @@ def main():
     # per-unit figures x the units one launch processes)
     weighted = g.weighted
     arcs = g.arcs_unpadded or g.arcs  # algorithmic: the real arcs (row padding is our overhead)
-    heavy_arcs = g.heavy_arc_total
-    light_arcs = g.arcs - heavy_arcs - (g.arcs - arcs)
+    heavy_arcs = g.heavy_arc_total  # heavy rows' arcs before the tile layout (<= 7 pads per row)
+    light_arcs = arcs - heavy_arcs
+    tiled = g.heavy_layout == "tiles"
     heavy_rows = g.n_heavy
     lb = 1 if k <= 255 else (2 if k <= 65535 else 4)
     phase_bytes = {
         # labels in, label table out; the compact hot tier (bitmap + prefix
         # per 32 vertices, ranks of the hot ones) in, their labels out again
         "project": 4 * rows + lb * rows + (rows // 4 + 4 * g.n_hot + lb * g.n_hot if g.n_hot else 0),
-        "gather": arcs * (4 + 1),
+        # tile layout: "gather" is the light rows' L2-path gather, "tiles" the
+        # heavy rows' (tail through L2, then the shared-memory tiles)
+        "gather": (light_arcs if tiled else arcs) * (4 + 1),
+        "tiles": heavy_arcs * (4 + 1),
         "blocks": 8 * (rows + 1) + light_arcs * (1 + 4 * weighted) + 4 * k * (rows - heavy_rows),
         "heavy": heavy_arcs * (1 + 4 * weighted) + 4 * k * heavy_rows,
         # wide K: label gather fused with the row windows (targets + weights
@@ -606,7 +617,8 @@ def main():
     # gee_gather_labels: packed shared-memory head of the hot tier, or
     # plain contiguous lookups without one
     gather_kernel = "k_gather_contig" if g.n_hot < 16384 else "k_gather_packed"
-    kernel_of = {"project": "k_label_hist", "gather": gather_kernel, "blocks": "k_reduce_blocks_ring",
+    kernel_of = {"project": "k_label_hist", "gather": gather_kernel, "tiles": "k_gather_tiles",
+                 "blocks": "k_reduce_blocks_ring",
                  "heavy": "k_reduce_heavy_items", "wide": "k_wide_rows"}
     achieved = phase_bytes[dominant] / (phase_ms[dominant] * 1e-3) / 1e9
     step_bmin = s * (8 + 4 * weighted) + 4 * n + 4 * n * k  # SURVEY 8(d) B_min, whole graph
@@ -631,7 +643,8 @@ def main():
                    "parallelism": f"row-range x{world}" if world > 1 else "single GPU",
                    "l2": "inputs (CSR %.1f GB) >> 126 MB L2; no flush needed" % (g.csr_bytes() / 1e9),
                    "gen_s": round(t_gen, 3), "prep_s": round(t_prep, 3), "hot_prep_s": round(t_hot, 3),
-                   "hot_vertices": g.n_hot, "heavy_rows": heavy_rows},
+                   "hot_vertices": g.n_hot, "heavy_rows": heavy_rows, "heavy_layout": g.heavy_layout,
+                   "tiles": g.n_tiles, "tile_slots": getattr(g, "tile_slots", 0), "l2_path_arcs": g.l2_arcs or g.arcs},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                      "frac": achieved / peak_gbs, "traffic": load_traffic(workload, kernel_of[dominant]) if world == 1 else None,
                      "kernel": kernel_of[dominant], "peak_kind": peak_kind,

@@ -307,6 +307,36 @@ int gee_reduce_heavy(const uint8_t *cls, const float *w, int64_t arcs, int32_t s
                      const int32_t *item_slot, int64_t n_items, const int32_t *mega_rows, int64_t n_mega,
                      void *mega_acc, int64_t *counter, float *z, void *stream);
 
+/* Tile-major heavy region (graph preparation + its gather; round 2).  The
+ * reference's arc wave looks a label up per arc (arc_pass_worker,
+ * _kernels.py:183-207); here the heavy rows' TARGETS are regrouped by slot
+ * tile so those lookups hit shared memory, while their class bytes and
+ * weights stay row-major for gee_reduce_heavy.
+ *   gee_tile_bounds  bounds[b * n_heavy + j] = first arc of heavy row
+ *       heavy_rows[j] (rows sorted by slot) whose slot is >= thresholds[b].
+ *   gee_span_copy    span s: out[dst_first[s] .. + src_len[s]) = in[src_first[s]
+ *       ..), padded with (sentinel, 0) up to dst_len[s] (int64 arrays);
+ *       targets / out_targets or w / out_w may be NULL (that array is skipped).
+ *   gee_gather_tiles for the arcs [tile_start[0], tile_start[n_tiles]) of
+ *       `targets`, where [tile_start[t], tile_start[t+1]) (multiples of 16)
+ *       holds slots of tile t = [t * tile_slots, (t + 1) * tile_slots) or
+ *       padding (any other slot: class 0): the class of arc e goes to
+ *       cls[16 * group_dst[(e - region_start) / 16] + e % 16] -- the 16-arc
+ *       group's place in the row-major class stream.  Tile labels are staged
+ *       in shared memory (tile_slots bytes, a multiple of 16).
+ *   gee_gather_scatter the same scatter for arcs [first, end) whose slots
+ *       are looked up in the table itself (the tail past the last tile). */
+int gee_tile_bounds(const int64_t *offsets, const int32_t *heavy_rows, int64_t n_heavy, const int32_t *targets,
+                    const int64_t *thresholds, int32_t n_thresholds, int64_t *bounds, void *stream);
+int gee_span_copy(int64_t n_spans, const int64_t *src_first, const int64_t *src_len, const int64_t *dst_first,
+                  const int64_t *dst_len, const int32_t *targets, const float *w, int32_t sentinel,
+                  int32_t *out_targets, float *out_w, void *stream);
+int gee_gather_tiles(const int32_t *targets, const int64_t *tile_start, int32_t n_tiles, int64_t region_start,
+                     const int32_t *group_dst, const void *table, int64_t table_bytes, int64_t tile_slots, int32_t k,
+                     uint8_t *cls, void *stream);
+int gee_gather_scatter(const int32_t *targets, int64_t first, int64_t end, int64_t region_start,
+                       const int32_t *group_dst, const void *table, int32_t k, uint8_t *cls, void *stream);
+
 /* Fixed-point exponent valid for every pull reducer: the largest e with
  * max_row_abs * 2^e < 2^62 (64-bit row sums) and max_abs * 2^e < 2^41 (the
  * signed split planes of a 2048-arc row cannot overflow).

@@ -7,7 +7,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libgee_b200.so")
-SOURCES = ["gee_capi.cu", "gee_projection.cu", "gee_push.cu", "gee_prep.cu", "gee_hot.cu", "gee_gather.cu", "gee_reduce.cu", "gee_wide.cu", "gee_compact.cu", "gee_pack.cu", "gee_synth.cu"]
+SOURCES = ["gee_capi.cu", "gee_projection.cu", "gee_push.cu", "gee_prep.cu", "gee_hot.cu", "gee_gather.cu", "gee_tiles.cu", "gee_reduce.cu", "gee_wide.cu", "gee_compact.cu", "gee_pack.cu", "gee_synth.cu"]
 HEADERS = ["gee_common.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

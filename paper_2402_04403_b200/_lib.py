@@ -70,6 +70,10 @@ SIGNATURES = {
     "gee_reduce_blocks_pad8": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, vp]),
     "gee_reduce_heavy": (c_int, [vp, vp, c_i64, c_i32, vp, c_i32, vp, vp, vp, vp, c_i64, vp, c_i64, vp, vp, vp, vp]),
     "gee_block_scale_exp": (c_int, [c_dbl, c_dbl, c_dbl, P_i32, P_dbl]),
+    "gee_tile_bounds": (c_int, [vp, vp, c_i64, vp, vp, c_i32, vp, vp]),
+    "gee_span_copy": (c_int, [c_i64, vp, vp, vp, vp, vp, vp, c_i32, vp, vp, vp]),
+    "gee_gather_tiles": (c_int, [vp, vp, c_i32, c_i64, vp, vp, c_i64, c_i64, c_i32, vp, vp]),
+    "gee_gather_scatter": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, c_i32, vp, vp]),
     "gee_synth_word": (c_u64, [c_u64, c_u64, c_u64]),
     "gee_synth_rmat": (c_int, [vp, vp, vp, c_i64, c_i64, c_i32, c_dbl, c_dbl, c_dbl, c_u64, c_i32, vp]),
     "gee_synth_er": (c_int, [vp, vp, vp, c_i64, c_i64, c_i64, c_u64, vp]),

@@ -71,6 +71,12 @@ class DeviceGraph:
         self._owns_targets = False
         self._owns_weights = False
         self.padded = 0  # rows padded to a multiple of this many arcs (0: not padded)
+        # "rows": heavy rows inside the row-major CSR; "tiles": relocated into
+        # the tile-major region behind the light rows (tile_heavy)
+        self.heavy_layout = "rows"
+        self.n_tiles = 0
+        self.l2_arcs = self.light_arcs = 0
+        self.group_dst = None
         self.arcs_unpadded = None
 
     # ---------------------------------------------------------------- build
@@ -213,6 +219,12 @@ class DeviceGraph:
         first = self.offsets[r64].cpu()
         deg = (self.offsets[r64 + 1] - self.offsets[r64]).cpu()
         self.heavy_arc_total = int(deg.sum())
+        self._make_items(rows, first, deg)
+
+    def _make_items(self, rows, first, deg):
+        """Work items of gee_reduce_heavy for the heavy `rows` (device int32,
+        ascending) whose arcs are cls / weights [first, first + deg) (host
+        int64)."""
         # work items of gee_reduce_heavy: runs of <= HEAVY_ITEM_ARCS arcs;
         # rows with several items ("mega" rows) combine through acc + finalize
         nit = (deg + self.HEAVY_ITEM_ARCS - 1) // self.HEAVY_ITEM_ARCS
@@ -331,6 +343,108 @@ class DeviceGraph:
         self._owns_targets = self._owns_weights = True
         self.padded = align
         self._plan()
+
+    # Tile-major heavy region (csrc/gee_tiles.cu).  A tile is a run of
+    # label-table slots that fits one CTA's shared memory as bytes; slots past
+    # TILE_MAX tiles stay on the L2 lookup path (the region's tail segment).
+    # C4 step by tile count (192 KB tiles): 8: 18.5 ms, 21: 18.3, 42: 18.5,
+    # 86 (the whole hot tier): 19.5 -- the sparse upper tiles hold spans of a
+    # few arcs, whose scattered class writes cost more than their L2 lookups
+    # (224 KB tiles: slower, the streams need some L1).
+    TILE_SLOTS = 196608
+    TILE_MAX = 21
+    SPAN_ALIGN = 16  # arcs per span unit; 32 (whole sectors): tiles -0.15 ms, heavy +0.07 ms
+
+    def tile_heavy(self, tile_slots=None, max_tiles=None):
+        """Regroup the heavy rows' targets by slot tile (graph preparation;
+        after prepare_hot).  The arrays become
+            targets  [ light rows, row-major | heavy tail | tile 0 | tile 1 | ... ]
+            weights  [ light rows, row-major | heavy rows, row-major (row, tile, slot) ]
+        (the class stream is indexed like the weights), every (tile, row)
+        span padded to 16 arcs in both orders, and group_dst maps the 16-arc
+        groups of the heavy targets to their place in the row-major order.
+        Heavy rows keep an empty run in `offsets` (the block reducer
+        zero-fills them, gee_reduce_heavy then writes them).  Returns True
+        when the layout changed."""
+        if self.heavy_layout == "tiles" or not self.padded or self.n_heavy == 0 or self.hot_k is None:
+            return False
+        if self.hot_k > 255:
+            return False
+        ts = int(tile_slots or self.TILE_SLOTS)
+        mt = int(max_tiles or self.TILE_MAX)
+        if ts % 16 or ts < 16:
+            raise ValidationError("tile_slots must be a multiple of 16")
+        dev, n, H = self.device, self.n, self.n_heavy
+        sentinel = self.n_hot + self.n_nodes
+        T = min(mt, (sentinel + ts - 1) // ts)
+        if T <= 0:
+            return False
+        st = _stream()
+        thr = torch.tensor([s * ts for s in range(T)] + [min(T * ts, sentinel), sentinel], dtype=torch.int64,
+                           device=dev)
+        bounds = torch.empty((T + 2) * H, dtype=torch.int64, device=dev)
+        check(lib.gee_tile_bounds(ptr(self.offsets), ptr(self.heavy_rows), H, ptr(self.targets), ptr(thr), T + 2,
+                                  ptr(bounds), st), "gee_tile_bounds")
+        bounds = bounds.view(T + 2, H)
+        seg_len = bounds[1:] - bounds[:-1]  # (T + 1, H): tiles 0..T-1, then the tail; row padding dropped
+        al = self.SPAN_ALIGN
+        seg_pad = (seg_len + al - 1) // al * al
+        # light rows, compacted
+        lens = self.offsets[1:] - self.offsets[:-1]
+        lens[self.heavy_rows.to(torch.int64)] = 0
+        poff = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(lens, 0, out=poff[1:])
+        light = int(poff[-1].item())
+        light16 = (light + 31) // 32 * 32
+        total = int(light16 + seg_pad.sum().item())
+        # tile-major order of the targets: tail first, then the tiles
+        order = [T] + list(range(T))
+        src_first = bounds[:-1][order].reshape(-1).contiguous()
+        src_len = seg_len[order].reshape(-1).contiguous()
+        dst_len = seg_pad[order].reshape(-1).contiguous()
+        t_first = torch.cumsum(dst_len, 0) - dst_len + light16  # (T + 1, H) flattened, region order
+        # row-major order of the weights / class stream: (row, tile 0..T-1, tail)
+        rp = seg_pad.t().contiguous()  # (H, T + 1)
+        r_first = (torch.cumsum(rp.reshape(-1), 0) - rp.reshape(-1) + light16).view(H, T + 1)
+        r_first_o = r_first.t()[order].reshape(-1).contiguous()  # same span order as t_first
+        tgt = torch.empty(total, dtype=torch.int32, device=dev)
+        wts = torch.empty(total, dtype=torch.float32, device=dev) if self.weights is not None else None
+        if light16 > light:
+            tgt[light:light16] = sentinel
+            if wts is not None:
+                wts[light:light16] = 0
+        check(lib.gee_span_copy(n, ptr(self.offsets), ptr(lens), ptr(poff), ptr(lens), ptr(self.targets),
+                                ptr(self.weights), sentinel, ptr(tgt), ptr(wts), st), "gee_span_copy")
+        ns = (T + 1) * H
+        check(lib.gee_span_copy(ns, ptr(src_first), ptr(src_len), ptr(t_first), ptr(dst_len), ptr(self.targets), None,
+                                sentinel, ptr(tgt), None, st), "gee_span_copy")
+        if wts is not None:
+            check(lib.gee_span_copy(ns, ptr(src_first), ptr(src_len), ptr(r_first_o), ptr(dst_len), None,
+                                    ptr(self.weights), sentinel, None, ptr(wts), st), "gee_span_copy")
+        # 16-arc groups: tile-major position -> row-major position
+        ng = dst_len // 16
+        gstart = torch.cumsum(ng, 0) - ng
+        gdst = torch.arange(int(ng.sum().item()), dtype=torch.int64, device=dev)
+        gdst -= torch.repeat_interleave(gstart, ng)
+        gdst += torch.repeat_interleave(r_first_o // 16, ng)
+        self.group_dst = gdst.to(torch.int32)
+        del gdst, ng, gstart
+        seg_tot = dst_len.view(T + 1, H).sum(1)
+        starts = torch.cumsum(seg_tot, 0) - seg_tot + light16  # tail, tile 0, ..., tile T-1
+        self.tile_start = torch.cat([starts[1:], torch.tensor([total], dtype=torch.int64, device=dev)]).contiguous()
+        self.light_arcs = light16
+        self.l2_arcs = int(starts[1].item())  # light rows + the heavy tail
+        self.n_tiles, self.tile_slots = T, ts
+        row_len = rp.sum(1).cpu()
+        row_first = r_first[:, 0].cpu()
+        torch.cuda.current_stream(dev).synchronize()
+        self.offsets, self.targets, self.weights = poff, tgt, wts
+        self._owns_targets = self._owns_weights = True
+        self._make_items(self.heavy_rows, row_first, row_len)
+        ends = self.offsets[torch.arange(0, n + 32, 32, device=dev).clamp_(max=n)]
+        self.max_block_arcs = int((ends[1:] - ends[:-1]).max().item()) if n else 0
+        self.heavy_layout = "tiles"
+        return True
 
     def _own_pull_arrays(self):
         """Private copies of the pull targets / weights before they are
@@ -503,9 +617,20 @@ class Embedder:
         # rows as work items)
         if self.cls is None or self.cls.numel() < g.arcs + 64:
             self.cls = torch.empty(g.arcs + 64, dtype=torch.uint8, device=self.device)
-        check(lib.gee_gather_labels(ptr(g.targets), g.arcs, ptr(self.table), g.n_hot, self.k, ptr(self.cls),
-                                    _stream()), "gee_gather_labels")
+        tiles = g.heavy_layout == "tiles"
+        # light rows alone take a 128 KB head (no hub rows' lines to merge in L1):
+        # C4 0 / 64 / 96 / 112 / 128 / 144 / 160 KB: 5.10 / 4.89 / 4.89 / 4.77 / 4.73 / 5.14 / 5.04 ms
+        check(lib.gee_gather_labels_head(ptr(g.targets), g.light_arcs if tiles else g.arcs, ptr(self.table), g.n_hot,
+                                         self.k, 131072 if tiles else -1, ptr(self.cls), _stream()),
+              "gee_gather_labels")
         self._mark("gather", 1)
+        if tiles:
+            check(lib.gee_gather_scatter(ptr(g.targets), g.light_arcs, g.l2_arcs, g.light_arcs, ptr(g.group_dst),
+                                         ptr(self.table), self.k, ptr(self.cls), _stream()), "gee_gather_scatter")
+            check(lib.gee_gather_tiles(ptr(g.targets), ptr(g.tile_start), g.n_tiles, g.light_arcs, ptr(g.group_dst),
+                                       ptr(self.table), g.n_hot + self.n + 1, g.tile_slots, self.k, ptr(self.cls),
+                                       _stream()), "gee_gather_tiles")
+            self._mark("tiles", 2 if g.l2_arcs > g.light_arcs else 1)
         check(lib.gee_reduce_blocks_pad8(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
                                          ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(z), _stream()),
               "gee_reduce_blocks_pad8")

@@ -142,6 +142,7 @@ class ShardedPass:
                     emb.project(lab)  # validates the labels once
                 else:
                     g.prepare_hot(k)
+                    g.tile_heavy()  # repeated passes: heavy rows' targets regrouped by slot tile
                     emb.project(lab, g=g)  # validates the labels once
             torch.cuda.synchronize(dev)
 

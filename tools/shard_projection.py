@@ -86,6 +86,7 @@ def main():
             else:
                 g, lo, hi = shard_mod.build_row_shard(src, dst, w, n, nshards, rank, k=k)
             g.prepare_hot(k)
+            g.tile_heavy()
             emb = Embedder(n, k)
             z = torch.empty((hi - lo, k), dtype=torch.float32, device="cuda")
             emb.project(y, validate=True, g=g)
