@@ -147,10 +147,15 @@ __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const
 #define GEE_RING 3
 #endif
 #ifndef GEE_RING_H
-#define GEE_RING_H 4
+#define GEE_RING_H 2
 #endif
 constexpr int RING = GEE_RING;      // block reducer
 constexpr int RING_H = GEE_RING_H;  // heavy items
+#ifndef GEE_HSUB
+#define GEE_HSUB 2
+#endif
+constexpr int HSUB = GEE_HSUB;            // 256-arc rounds per heavy ring slot (one pair of bulk copies each)
+constexpr int HROUND = HSUB * BROUND;     // arcs per heavy ring slot
 constexpr int RING_CLS = BROUND;                        // bytes per round
 constexpr int RING_W = BROUND * (int)sizeof(float);     // bytes per round (weighted)
 
@@ -327,14 +332,17 @@ __device__ __forceinline__ void ring_issue_bulk(uint8_t *ring, uint64_t *bars, i
                                                 const float *__restrict__ w, int lane, uint64_t pol)
 {
     if (lane != 0 || e >= bend) return;
-    constexpr int RSLOT = RING_CLS + (WEIGHTED ? RING_W : 0);
+    constexpr int RSLOT = HSUB * (RING_CLS + (WEIGHTED ? RING_W : 0));
     uint8_t *rs = ring + slot * RSLOT;
-    const int64_t na = arcs - e < BROUND ? arcs - e : BROUND;
+    int64_t na = arcs - e < HROUND ? arcs - e : HROUND;
+    // no further than the 256-arc round that holds the item's last arc
+    const int64_t need = ((bend - e + BROUND - 1) / BROUND) * BROUND;
+    if (need < na) na = need;
     const uint32_t cb = (uint32_t)((na + 15) & ~(int64_t)15);
     const uint32_t wb = WEIGHTED ? (uint32_t)(na * 4) : 0u;
     mbar_expect_tx(bars + slot, cb + wb);
     bulk_g2s(rs, cls + e, cb, bars + slot, pol);
-    if (WEIGHTED) bulk_g2s(rs + RING_CLS, w + e, wb, bars + slot, pol);
+    if (WEIGHTED) bulk_g2s(rs + HSUB * RING_CLS, w + e, wb, bars + slot, pol);
 }
 
 template <bool WEIGHTED>
@@ -551,7 +559,7 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int kk = k;
     const int pkb = block_vec_words(kk);  // [3 pad | trash | bins 1..k | pad]
-    constexpr int RSLOT = RING_CLS + (WEIGHTED ? RING_W : 0);
+    constexpr int RSLOT = HSUB * (RING_CLS + (WEIGHTED ? RING_W : 0));
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw) + wid * RING_H;
     uint8_t *ring_base = smem_raw + RW * RING_H * sizeof(uint64_t);
@@ -583,23 +591,27 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
         unsigned long long sum[HCOL];
 #pragma unroll
         for (int j = 0; j < HCOL; j++) sum[j] = 0ull;
-        int64_t ep = b0 & ~(int64_t)(BROUND - 1);
+        int64_t ep = b0 & ~(int64_t)(HROUND - 1);
 #pragma unroll
         for (int i = 0; i < RING_H; i++) {
             ring_issue_bulk<WEIGHTED>(ring, bars, i, ep, e1, arcs, cls, w, lane, pol);
-            ep += BROUND;
+            ep += HROUND;
         }
         int slot = 0;
-        for (int64_t e0 = b0 & ~(int64_t)(BROUND - 1); e0 < e1; e0 += BROUND) {
-            if (lane == 0) mbar_wait(bars + slot, (ph >> slot) & 1u);
-            __syncwarp();
-            ph ^= 1u << slot;
-            const uint8_t *rs = ring + slot * RSLOT;
+        for (int64_t e0 = b0 & ~(int64_t)(HROUND - 1); e0 < e1; e0 += BROUND) {
+            const int sub = (int)((e0 & (HROUND - 1)) / BROUND);  // 256-arc round inside the slot
+            if (sub == 0) {
+                if (lane == 0) mbar_wait(bars + slot, (ph >> slot) & 1u);
+                __syncwarp();
+                ph ^= 1u << slot;
+            }
+            const uint8_t *rs = ring + slot * RSLOT + sub * RING_CLS;
+            const uint8_t *rw = ring + slot * RSLOT + HSUB * RING_CLS + sub * RING_W;
             const uint2 ca = *reinterpret_cast<const uint2 *>(rs + lane * BU);
             float wa[BU];
             if (WEIGHTED) {
-                const float4 x0 = *reinterpret_cast<const float4 *>(rs + RING_CLS + lane * BU * 4);
-                const float4 x1 = *reinterpret_cast<const float4 *>(rs + RING_CLS + lane * BU * 4 + 16);
+                const float4 x0 = *reinterpret_cast<const float4 *>(rw + lane * BU * 4);
+                const float4 x1 = *reinterpret_cast<const float4 *>(rw + lane * BU * 4 + 16);
                 wa[0] = x0.x, wa[1] = x0.y, wa[2] = x0.z, wa[3] = x0.w;
                 wa[4] = x1.x, wa[5] = x1.y, wa[6] = x1.z, wa[7] = x1.w;
             }
@@ -620,10 +632,12 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
                     atomicAdd(p, 1u);
                 }
             }
-            __syncwarp();  // every lane has read the slot before it is refilled
-            ring_issue_bulk<WEIGHTED>(ring, bars, slot, ep, e1, arcs, cls, w, lane, pol);
-            ep += BROUND;
-            slot = slot + 1 == RING_H ? 0 : slot + 1;
+            if (sub == HSUB - 1 || e0 + BROUND >= e1) {
+                __syncwarp();  // every lane has read the slot before it is refilled
+                ring_issue_bulk<WEIGHTED>(ring, bars, slot, ep, e1, arcs, cls, w, lane, pol);
+                ep += HROUND;
+                slot = slot + 1 == RING_H ? 0 : slot + 1;
+            }
             // fold the window into the 64-bit sums at each aligned window end
             const int64_t en = e0 + BROUND;
             if ((en & (BLOCK_ROW_MAX - 1)) == 0 || en >= e1) {
@@ -778,7 +792,7 @@ int gee_reduce_heavy(const uint8_t *cls, const float *w, int64_t arcs, int32_t s
     const bool weighted = w != nullptr;
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
-    const size_t sh = (size_t)RW * RING_H * (RING_CLS + (weighted ? RING_W : 0) + sizeof(uint64_t)) +
+    const size_t sh = (size_t)RW * RING_H * (HSUB * (RING_CLS + (weighted ? RING_W : 0)) + sizeof(uint64_t)) +
                       (size_t)block_vec_words(k) * sizeof(float) +
                       (size_t)RW * HCOPY * (block_vec_words(k) * (weighted ? 2 : 1) + 4) * sizeof(uint32_t);
     GEE_REQUIRE((reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0),

@@ -12,7 +12,7 @@ per = collections.OrderedDict()
 for r in rows[1:]:
     name = r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
     per.setdefault(name, []).append(float(r[vi].replace(",", "")) * scale[r[ui]])
-ours = ("k_label_hist", "k_inv", "k_gather", "k_reduce_blocks", "k_reduce_heavy", "k_heavy_finalize")
+ours = ("k_label_hist", "k_inv", "k_gather", "k_reduce_blocks", "k_reduce_heavy", "k_heavy_finalize")  # k_gather: packed, scatter, tiles
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else None
 print(f"{'kernel':48s} {'launches':>8s} {'mean ms':>10s} {'total ms':>10s}")
 step_total = 0.0
