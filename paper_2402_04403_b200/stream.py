@@ -116,6 +116,9 @@ class HostPipeline:
     def __init__(self, g: DeviceGraph, k, chunks=16, device=None, packed=None, resident=False):
         if not g.has_pull or g.hot_k != k:
             raise ValidationError("HostPipeline needs a pull graph prepared for k (prepare_hot)")
+        if g.heavy_layout != "rows":
+            raise ValidationError("HostPipeline streams row chunks: it needs the row-major layout "
+                                  "(a graph regrouped by tile_heavy serves device-resident passes only)")
         self.resident = bool(resident)
         self.device = device or g.device
         self.dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()

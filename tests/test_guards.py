@@ -85,6 +85,34 @@ def test_pull_and_push_write_only_their_output(k, weighted):
     assert _digest(*inputs) == before, "an edge pass modified its inputs"
 
 
+@pytest.mark.parametrize("k,weighted", [(50, True), (7, False)])
+def test_tile_layout_writes_only_its_outputs(k, weighted):
+    # the tile-major heavy region: Z between guard rows, the class stream
+    # between guard bytes (the tile gather scatters class bytes through
+    # group_dst), and every graph array unchanged by the pass
+    src, dst, w, y, n = _case(k, weighted)
+    g = DeviceGraph.from_edges(src, dst, w, n, pull=True)
+    g.prepare_hot(k, enable=True)
+    emb = Embedder(n, k)
+    emb.project(y, g=g)
+    ref = emb.pull(g).clone()
+    assert g.tile_heavy(tile_slots=4096, max_tiles=3) and g.l2_arcs > g.light_arcs
+    inputs = (g.offsets, g.targets, g.weights, g.group_dst, g.tile_start, g.item_first, g.item_end, y)
+    before = _digest(*inputs)
+    guard = 4096
+    cls_full = torch.full((g.arcs + 64 + 2 * guard,), 0xA5, dtype=torch.uint8, device=DEV)
+    emb.cls = cls_full[guard:guard + g.arcs + 64]
+    assert emb.cls.data_ptr() % 16 == 0
+    full, z = _guarded_z(n, k)
+    emb.pull(g, z)
+    assert _guards_intact(full, n, k), "tile-layout pull wrote outside Z"
+    assert bool((cls_full[:guard] == 0xA5).all()) and bool((cls_full[guard + g.arcs + 64:] == 0xA5).all()), \
+        "the gather wrote outside the class stream"
+    assert int(emb.cls[:g.arcs].max()) <= k
+    assert torch.equal(z, ref), "tile layout changed Z"
+    assert _digest(*inputs) == before, "the pass modified its inputs"
+
+
 def test_streamed_pass_writes_only_the_callers_rows():
     from paper_2402_04403_b200.stream import HostPipeline
 

@@ -144,3 +144,28 @@ def test_prepared_host_results_small_and_wide_k(k, residency):
     z = embed_parallel(p, y)
     assert np.array_equal(z, embed_parallel(g, y, variant="pull"))
     assert rel_err(z, oracle.serial_embed(src, dst, w, y.labels, n, k)) <= 1e-4
+
+
+def test_device_residency_tile_layout_device_results_only():
+    # layout="tiles": heavy rows' targets regrouped by slot tile; CUDA labels
+    # in, CUDA Z out through the recorded pass; same bits as the stored
+    # graph's pass.  Host results are refused (that path reads row chunks).
+    n, k = 3000, 11
+    src, dst, w = _graph(41, n=n, s=150_000)  # row 3 has 3000 arcs: one heavy row
+    g = _csr(src, dst, w, n, True)
+    p = prepare(g, k, residency="device", layout="tiles")
+    assert p.layout == "tiles" and p._dg.heavy_layout == "tiles"
+    rng = np.random.default_rng(42)
+    out = torch.empty((n, k), dtype=torch.float32, device="cuda")
+    for i in range(3):
+        lab = rng.integers(0, k + 1, n)
+        ref = embed_parallel(g, LabelVector(labels=lab, k=k), variant="pull")
+        zd = embed_parallel(p, LabelVector(labels=torch.as_tensor(lab, device="cuda"), k=k), out=out)
+        assert zd is out and np.array_equal(zd.cpu().numpy(), ref), i
+    with pytest.raises(ValidationError, match="tiles"):
+        embed_parallel(p, LabelVector(labels=lab, k=k))
+    with pytest.raises(ValidationError, match="residency"):
+        prepare(g, k, layout="tiles")
+    with pytest.raises(ValidationError, match="layout"):
+        prepare(g, k, residency="device", layout="columns")
+    p.close()
