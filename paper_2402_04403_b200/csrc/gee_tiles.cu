@@ -71,8 +71,14 @@ __global__ void k_span_copy(int64_t n_spans, const int64_t *__restrict__ src_fir
     }
 }
 
-constexpr int TTHREADS = 1024;
-constexpr int TGU = 4;                 // 16-byte target loads per lane per step
+#ifndef GEE_TTHREADS
+#define GEE_TTHREADS 1024
+#endif
+constexpr int TTHREADS = GEE_TTHREADS;
+#ifndef GEE_TGU
+#define GEE_TGU 4
+#endif
+constexpr int TGU = GEE_TGU;           // 16-byte target loads per lane per step
 constexpr int TSTEP = 128 * TGU;       // arcs per warp step
 
 // Tile gather: CTA b takes arcs [c0, c1) of the tile region (an equal share,

@@ -116,3 +116,31 @@ def test_tile_heavy_is_a_noop_without_heavy_rows_or_for_wide_k():
                                n, device="cuda:0", pull=True)
     g.prepare_hot(300)
     assert g.n_heavy > 0 and not g.tile_heavy() and g.heavy_layout == "rows"
+
+
+def test_tiles_random_battery():
+    """Random shapes: tile sizes that do not divide the table, tiles reaching
+    past the table's end, rows that live entirely in one tile or entirely in
+    the tail, unlabeled vertices."""
+    rng = np.random.default_rng(2024)
+    for case in range(12):
+        n = int(rng.integers(3000, 40_000))
+        k = int(rng.choice([1, 3, 50, 63, 64, 200]))
+        weighted = bool(rng.integers(0, 2))
+        nh = int(rng.integers(3, 8))
+        parts_s, parts_d = [], []
+        for _ in range(nh):
+            d = int(rng.integers(2100, 12_000))
+            lo = int(rng.integers(0, n - 1))
+            hi = int(rng.integers(lo + 1, n + 1)) if rng.random() < 0.5 else n
+            parts_s.append(np.full(d, int(rng.integers(0, n)), np.int64))
+            parts_d.append(rng.integers(lo, hi, d))
+        parts_s.append(rng.integers(0, n, 30_000))
+        parts_d.append(rng.integers(0, n, 30_000))
+        src, dst = np.concatenate(parts_s), np.concatenate(parts_d)
+        w = (2.0 * rng.random(src.size) - 0.5).astype(np.float32) if weighted else None
+        y = np.where(rng.random(n) < 0.3, 0, rng.integers(1, k + 1, n))
+        ts = int(rng.choice([16, 48, 1000 * 16, 4096, 65536]))
+        mt = int(rng.choice([1, 2, 5, 1000]))
+        z_rows, z_tiles = _pull_both(src, dst, w, y, n, k, bool(rng.integers(0, 2)), ts, mt)
+        assert np.array_equal(z_rows.view(np.uint32), z_tiles.view(np.uint32)), (case, n, k, ts, mt)
