@@ -291,6 +291,11 @@ int gee_reduce_heavy_plan(const int64_t *offsets, int64_t n, int64_t heavy_arcs,
 int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
                            int32_t scale_exp, const double *inv, int32_t k, int64_t heavy_arcs, float *z,
                            void *stream);
+/* The same reduction for a CSR in which NO row has more than 2048 arcs (the
+ * caller's guarantee: the tile layout keeps the heavy rows' arcs outside the
+ * CSR): the heavy-row skipping is compiled out (C4 7.61 -> 7.50 ms). */
+int gee_reduce_blocks_light(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
+                            int32_t scale_exp, const double *inv, int32_t k, float *z, void *stream);
 
 /* Heavy rows (longer than the block reducer's heavy_arcs) as work items:
  * item i covers arcs [item_first[i], item_end[i]) of row item_row[i]

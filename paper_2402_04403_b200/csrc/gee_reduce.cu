@@ -150,6 +150,10 @@ __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const
 #define GEE_RING_H 2
 #endif
 constexpr int RING = GEE_RING;      // block reducer
+#ifndef GEE_BCTAS
+#define GEE_BCTAS 2
+#endif
+constexpr int BCTAS = GEE_BCTAS;    // block-reducer CTAs per SM (shared memory and registers are sized for it)
 constexpr int RING_H = GEE_RING_H;  // heavy items
 #ifndef GEE_HSUB
 #define GEE_HSUB 2
@@ -221,6 +225,7 @@ struct RingBlk {
     int32_t ol, oh;          // this lane's row bounds, block-local
 };
 
+template <bool HV>
 __device__ __forceinline__ RingBlk ring_open(int64_t r0, int64_t n, int64_t o_lo, int64_t o_hi31, int64_t heavy_arcs,
                                              int lane)
 {
@@ -229,7 +234,8 @@ __device__ __forceinline__ RingBlk ring_open(int64_t r0, int64_t n, int64_t o_lo
     if (lane == 31) o_hi = o_hi31;
     const bool valid = r0 + lane < n;
     const int64_t d = valid ? o_hi - o_lo : 0;
-    const bool heavy = d > heavy_arcs;
+    const bool heavy = HV && d > heavy_arcs;  // !HV: the caller guarantees no row is longer (tile layout)
+    GEE_DCHECK(HV || d <= BLOCK_ROW_MAX);
     B.nzm = __ballot_sync(0xffffffffu, d > 0 && !heavy);
     B.hvm = __ballot_sync(0xffffffffu, heavy);
     B.vm = __ballot_sync(0xffffffffu, valid);
@@ -243,9 +249,10 @@ __device__ __forceinline__ RingBlk ring_open(int64_t r0, int64_t n, int64_t o_lo
 
 // First round at or after arc e that is not entirely inside a heavy row
 // (warp-uniform).
+template <bool HV>
 __device__ __forceinline__ int64_t ring_skip(const RingBlk &B, int64_t e, int lane)
 {
-    if (!B.hvm || e >= B.bend) return e;
+    if (!HV || !B.hvm || e >= B.bend) return e;
     const int32_t lr = (int32_t)(e - B.base);
     const unsigned sm = __ballot_sync(0xffffffffu, ((B.anym >> lane) & 1u) && B.ol <= lr);
     if (!sm) return e;
@@ -345,8 +352,8 @@ __device__ __forceinline__ void ring_issue_bulk(uint8_t *ring, uint64_t *bars, i
     if (WEIGHTED) bulk_g2s(rs + HSUB * RING_CLS, w + e, wb, bars + slot, pol);
 }
 
-template <bool WEIGHTED>
-__global__ void __launch_bounds__(RT, 2)
+template <bool WEIGHTED, bool HV>  // HV: rows longer than heavy_arcs may sit in the CSR (skipped here)
+__global__ void __launch_bounds__(RT, BCTAS)
 k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
                      const float *__restrict__ w, float qscale, double dscale, const double *__restrict__ inv,
                      int32_t k, int64_t heavy_arcs, int nslots, float *__restrict__ z)
@@ -389,15 +396,15 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         const int64_t r0 = 32 * b;
         const int64_t o_lo = __ldcs(offsets + min(r0 + lane, n));
         const int64_t o_31 = lane == 31 ? __ldcs(offsets + min(r0 + 32, n)) : 0;
-        B = ring_open(r0, n, o_lo, o_31, heavy_arcs, lane);
+        B = ring_open<HV>(r0, n, o_lo, o_31, heavy_arcs, lane);
     }
     int64_t plo, phi;
     pass_span(B, B.nzm & ~single_rows<WEIGHTED>(B, lane), 0, nslots, plo, phi);
-    int64_t ep = ring_skip(B, plo, lane);  // next round to issue
+    int64_t ep = ring_skip<HV>(B, plo, lane);  // next round to issue
 #pragma unroll
     for (int i = 0; i < RING; i++) {
         ring_issue<WEIGHTED>(ring, i, ep, phi, arcs, cls, w, lane);
-        if (ep < phi) ep = ring_skip(B, ep + BROUND, lane);
+        if (ep < phi) ep = ring_skip<HV>(B, ep + BROUND, lane);
     }
     int slot0 = 0;  // ring slot of the pass's first round
     for (; b < b_end; b++) {
@@ -433,7 +440,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
             const int npass = min(nslots, nnz - p0);
             __syncwarp();
             pass_span(B, winm, p0, nslots, plo, phi);
-            int64_t ec = ring_skip(B, plo, lane);  // next round to consume
+            int64_t ec = ring_skip<HV>(B, plo, lane);  // next round to consume
             int slot = slot0;
             while (ec < phi) {
                 cp_wait<RING - 1>();
@@ -455,9 +462,9 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
                 __syncwarp();
                 // refill the slot just consumed with the round RING ahead
                 ring_issue<WEIGHTED>(ring, slot, ep, phi, arcs, cls, w, lane);
-                if (ep < phi) ep = ring_skip(B, ep + BROUND, lane);
+                if (ep < phi) ep = ring_skip<HV>(B, ep + BROUND, lane);
                 slot = slot + 1 == RING ? 0 : slot + 1;
-                ec = ring_skip(B, ec + BROUND, lane);
+                ec = ring_skip<HV>(B, ec + BROUND, lane);
             }
             // prime the ring for what comes next: this block's next pass, or
             // the next block's first rounds (in flight during the write-out)
@@ -465,19 +472,19 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
             int64_t nlo = 0, nhi = 0;
             if (!last) {
                 pass_span(B, winm, p0 + nslots, nslots, nlo, nhi);
-                ep = ring_skip(B, nlo, lane);
+                ep = ring_skip<HV>(B, nlo, lane);
             } else if (more) {
-                NB = ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
+                NB = ring_open<HV>(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
                 opened = true;
                 pass_span(NB, NB.nzm & ~single_rows<WEIGHTED>(NB, lane), 0, nslots, nlo, nhi);
-                ep = ring_skip(NB, nlo, lane);
+                ep = ring_skip<HV>(NB, nlo, lane);
             }
             if (!last || more) {
                 const RingBlk &P = last ? NB : B;
 #pragma unroll
                 for (int i = 0; i < RING; i++) {
                     ring_issue<WEIGHTED>(ring, (slot + i) % RING, ep, nhi, arcs, cls, w, lane);
-                    if (ep < nhi) ep = ring_skip(P, ep + BROUND, lane);
+                    if (ep < nhi) ep = ring_skip<HV>(P, ep + BROUND, lane);
                 }
                 slot0 = slot;
             }
@@ -528,7 +535,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
             __syncwarp();
         }
         if (!more) break;
-        B = opened ? NB : ring_open(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
+        B = opened ? NB : ring_open<HV>(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
     }
     cp_wait<0>();
 }
@@ -748,8 +755,23 @@ int gee_reduce_heavy_plan(const int64_t *offsets, int64_t n, int64_t heavy_arcs,
     return rc;
 }
 
+static int reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
+                         const double *inv, int32_t k, int64_t heavy_arcs, bool heavy_in_csr, float *z, void *stream);
+
 int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
                            const double *inv, int32_t k, int64_t heavy_arcs, float *z, void *stream)
+{
+    return reduce_blocks(offsets, n, cls, w, scale_exp, inv, k, heavy_arcs, true, z, stream);
+}
+
+int gee_reduce_blocks_light(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
+                            const double *inv, int32_t k, float *z, void *stream)
+{
+    return reduce_blocks(offsets, n, cls, w, scale_exp, inv, k, BLOCK_ROW_MAX, false, z, stream);
+}
+
+static int reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
+                         const double *inv, int32_t k, int64_t heavy_arcs, bool heavy_in_csr, float *z, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs 1 <= k <= 255 (got %d)", k);
@@ -771,14 +793,15 @@ int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls
                          (size_t)RW * planes * 32 * sizeof(uint32_t);
     const size_t vecb = (size_t)block_vec_words(k) * planes * sizeof(uint32_t);
     const size_t ring = (size_t)RW * RING * (RING_CLS + (weighted ? RING_W : 0));
-    const size_t budget = (size_t)(gee::smem_per_sm() / 2) - 1024;
+    const size_t budget = (size_t)(gee::smem_per_sm() / BCTAS) - 1024;
     GEE_REQUIRE(budget > fixed + ring + RW * vecb, GEE_ERR_INVALID, "k = %d leaves no shared memory for the window", k);
     int ns = (int)((budget - fixed - ring) / (RW * vecb));
     if (ns > 24) ns = 24;
     const size_t shr = ring + fixed + (size_t)RW * ns * vecb;
     const int64_t nblocks = (n + 31) / 32;
-    const int rgrid = (int)std::min<int64_t>((nblocks + RW - 1) / RW, (int64_t)gee::sm_count() * 2);
-    auto kern = weighted ? k_reduce_blocks_ring<true> : k_reduce_blocks_ring<false>;
+    const int rgrid = (int)std::min<int64_t>((nblocks + RW - 1) / RW, (int64_t)gee::sm_count() * BCTAS);
+    auto kern = weighted ? (heavy_in_csr ? k_reduce_blocks_ring<true, true> : k_reduce_blocks_ring<true, false>)
+                         : (heavy_in_csr ? k_reduce_blocks_ring<false, true> : k_reduce_blocks_ring<false, false>);
     GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shr));
     kern<<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, ns, z);
     return gee::check_launch("k_reduce_blocks_ring");

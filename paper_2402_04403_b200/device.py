@@ -631,9 +631,13 @@ class Embedder:
                                        ptr(self.table), g.n_hot + self.n + 1, g.tile_slots, self.k, ptr(self.cls),
                                        _stream()), "gee_gather_tiles")
             self._mark("tiles", 2 if g.l2_arcs > g.light_arcs else 1)
-        check(lib.gee_reduce_blocks_pad8(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
-                                         ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(z), _stream()),
-              "gee_reduce_blocks_pad8")
+        if tiles:  # no heavy row left in the CSR: the skipping logic is compiled out
+            check(lib.gee_reduce_blocks_light(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                              ptr(self.inv64), self.k, ptr(z), _stream()), "gee_reduce_blocks_light")
+        else:
+            check(lib.gee_reduce_blocks_pad8(ptr(g.offsets), g.n, ptr(self.cls), ptr(g.weights), g.scale_exp,
+                                             ptr(self.inv64), self.k, g.HEAVY_ARCS, ptr(z), _stream()),
+                  "gee_reduce_blocks_pad8")
         self._mark("blocks", 1)
         if g.n_mega and (self.mega_acc is None or self.mega_acc.numel() < g.n_mega * self.k):
             self.mega_acc = torch.zeros(g.n_mega * self.k, dtype=torch.int64, device=self.device)
