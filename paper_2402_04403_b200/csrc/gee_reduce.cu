@@ -544,18 +544,70 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
 // Heavy rows for gee_reduce_heavy, one warp per work item: an item is a
 // run of up to HEAVY_ITEM_ARCS arcs of one heavy row.  Lanes take 8
 // contiguous arcs per round (one 8-byte class load, two 16-byte weight
-// loads; the next round in flight) into the carry-free split window of the
-// block kernel; every BLOCK_ROW_MAX arcs the window is folded into per-lane
-// 64-bit column sums in registers.  An item that is its row's only item
-// writes the Z row itself; the items of longer (mega) rows meet in acc[m]
-// through 64-bit atomics and a small finalize.
-constexpr int HCOL = 8;   // columns per lane: k <= 256
-#ifndef GEE_HCOPY
-#define GEE_HCOPY 2
+// loads from the bulk-copy ring) into the carry-free split planes of the
+// block kernel; before a plane can wrap, the window is folded into per-lane
+// 64-bit sums in registers.  An item that is its row's only item writes the
+// Z row itself; the items of longer (mega) rows meet in acc[m] through
+// 64-bit atomics and a small finalize.
+//
+// Window copies per warp (heavy items).  All 32 lanes add into one row, and
+// the kernel is bound by its shared atomics: on C4 (k = 50) it streams in
+// 1.78 ms with no atomics, 1.86 ms with one per arc, 1.89 ms with two
+// conflict-free ones and 2.50 ms with two into a copy-major window of 2
+// copies (1 / 4 copies: 2.63 / 2.55 ms), whose banks are random.  A shared
+// atomic serialises on lanes that meet in one bank -- on one word most of
+// all.  The window is therefore kept in NC copies, INTERLEAVED: bin c of
+// copy q is word c * NC + q of its plane, and lane l adds into copy l % NC.
+// Lanes of different copies never share a bank; the 32 / NC lanes of one
+// copy do when their classes agree mod 32 / NC.  A copy takes 1 / NC of the
+// arcs, so the planes are folded every NC * 2048 arcs, by contiguous 16-byte
+// loads; the copies of a bin meet by shuffles once per item.  C4: NC = 4 /
+// 8 / 16 / 32 -> 2.31 / 2.25 / 2.37 / 4.30 ms (the window grows with NC:
+// fewer warps per SM); C3 0.28 -> 0.18 ms.
+#ifndef GEE_HNC
+#define GEE_HNC 8
 #endif
-constexpr int HCOPY = GEE_HCOPY;  // private window copies per warp (heavy items)
+constexpr int HNC_SMALL = GEE_HNC;  // k <= 64
+constexpr int HNC_LARGE = 4;        // k <= 255 (the window grows with k * NC)
+__host__ __device__ constexpr int heavy_plane_words(int k, int nc) { return (((k + 1) * nc + 3) & ~3) + 32; }
 
-template <bool WEIGHTED>
+__device__ __forceinline__ void red_shared_u32(uint32_t addr, uint32_t v)
+{
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// One 256-arc round of a heavy item: the lane's 8 arcs add into its window
+// copy (vb: shared byte address of bin 0 of the low plane; the high plane's
+// bin lies pb bytes further).  Branch-free: class 0 (pads, unlabeled
+// targets) and, in an item's first and last round (FULL = false), arcs
+// outside the item add into the lane's own trash word tb, whose twin at
+// tb + pb takes the high-plane add, so one select serves both planes.  A
+// divergent skip per arc spent 30% of the kernel's instructions on branch
+// bookkeeping (C4 2.58 -> 2.48 ms); dropping the per-arc mask test and the
+// second select from the inner rounds halved the instructions again (22 ->
+// 11 per arc) without changing the time: the shared atomics bind.
+template <bool WEIGHTED, bool FULL, int NC>
+__device__ __forceinline__ void heavy_round(uint32_t vb, uint32_t tb, uint32_t pb, const uint2 &ca,
+                                            const float (&wa)[BU], float qscale, unsigned vm, int kk)
+{
+#pragma unroll
+    for (int u = 0; u < BU; u++) {
+        const uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
+        GEE_DCHECK(c <= (uint32_t)kk);
+        const bool on = FULL ? c != 0u : (c != 0u && ((vm >> u) & 1u));
+        const uint32_t a = on ? vb + (4u * NC) * c : tb;
+        if (WEIGHTED) {
+            const unsigned long long qv = (unsigned long long)__float2ll_rn(wa[u] * qscale);
+            red_shared_u32(a, (uint32_t)qv & ((1u << BLOCK_SPLIT) - 1u));
+            red_shared_u32(a + pb, (uint32_t)(qv >> BLOCK_SPLIT));
+        } else {
+            red_shared_u32(a, 1u);
+        }
+    }
+}
+
+
+template <bool WEIGHTED, int NC, int KMAX>  // NC copies (a multiple of 4), k <= KMAX
 __global__ void __launch_bounds__(RT)
 k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__restrict__ item_end,
                      const int32_t *__restrict__ item_row, const int32_t *__restrict__ item_slot, int64_t n_items,
@@ -576,15 +628,14 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint64_t pol = policy_evict_first();
     uint32_t ph = 0;
-    // HCOPY private copies of the window per warp (lane groups of 32/HCOPY):
-    // all lanes add into one row, so a single copy serialises on equal
-    // classes; the copy stride (== 4 mod 32 words) puts copies on other banks
-    const int cs = pkb * Acc<WEIGHTED>::planes + 4;
-    uint32_t *vw = reinterpret_cast<uint32_t *>(sc1 + pkb) + wid * (HCOPY * cs + 32);
-    uint32_t *v = vw + (lane / (32 / HCOPY)) * cs;
-    uint32_t *trash = vw + HCOPY * cs + lane;  // one word per lane, never read
+    // the warp's window: per plane [bins (class, copy) | one trash word per
+    // lane]; the high plane follows the low one, so a lane's trash word has
+    // its twin pb bytes further, like every bin (never read)
+    const int pw = heavy_plane_words(kk, NC), nbw = (kk + 1) * NC;  // plane words; bin words
+    uint32_t *vw = reinterpret_cast<uint32_t *>(sc1 + pkb) + wid * (pw * Acc<WEIGHTED>::planes);
+    const uint32_t vb = smem_u32(vw + (lane & (NC - 1))), tb = smem_u32(vw + pw - 32 + lane), pb = (uint32_t)pw * 4u;
     for (int c = threadIdx.x; c < pkb; c += RT) sc1[c] = c < kk ? (float)(inv[c + 1] * dscale) : 0.f;
-    for (int i = lane; i < HCOPY * cs + 32; i += 32) vw[i] = 0u;
+    for (int i = lane; i < pw * Acc<WEIGHTED>::planes; i += 32) vw[i] = 0u;
     __syncthreads();
     // items come largest first; warps fetch them dynamically.  Rounds are
     // 256-arc aligned, so each aligned BLOCK_ROW_MAX window holds whole
@@ -596,9 +647,14 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
         if (it >= n_items) break;
         const int64_t b0 = item_first[it], e1 = item_end[it];
         GEE_DCHECK(b0 >= 0 && b0 < e1 && e1 <= arcs);
-        unsigned long long sum[HCOL];
+        // fold mapping: lane l reads the 4 plane words [4l + 128m, +4) -- copies
+        // 4(l % LPC) .. +3 of bin l / LPC + CPI m -- so a fold's loads are
+        // contiguous across the warp; the LPC lanes of a bin meet at the item's end
+        constexpr int LPC = NC / 4, CPI = 32 / LPC, NIT = (KMAX + CPI) / CPI;
+        static_assert(NC % 4 == 0 && NC <= 32, "copies: a multiple of 4");
+        unsigned long long sum[NIT];
 #pragma unroll
-        for (int j = 0; j < HCOL; j++) sum[j] = 0ull;
+        for (int j = 0; j < NIT; j++) sum[j] = 0ull;
         int64_t ep = b0 & ~(int64_t)(HROUND - 1);
 #pragma unroll
         for (int i = 0; i < RING_H; i++) {
@@ -623,30 +679,16 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
                 wa[0] = x0.x, wa[1] = x0.y, wa[2] = x0.z, wa[3] = x0.w;
                 wa[4] = x1.x, wa[5] = x1.y, wa[6] = x1.z, wa[7] = x1.w;
             }
-            // arcs of this lane's chunk inside the item: bits [vlo, vhi) (all 8 except
-            // in an item's first and last round)
-            const int64_t a0 = e0 + lane * BU;
-            const int vlo = (int)min((int64_t)BU, max((int64_t)0, b0 - a0));
-            const int vhi = (int)min((int64_t)BU, max((int64_t)0, e1 - a0));
-            const unsigned vm = ((1u << vhi) - 1u) & ~((1u << vlo) - 1u);
-            // branch-free: class 0 (pads, unlabeled targets) and arcs outside the
-            // item add into the lane's own trash word.  The kernel is bound by
-            // instruction issue (81% of the slots, ncu), and a divergent skip per
-            // arc spent 30% of its instructions on branch bookkeeping (BSSY /
-            // BSYNC / BRA): C4 2.58 -> 2.48 ms.
-#pragma unroll
-            for (int u = 0; u < BU; u++) {
-                const uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
-                GEE_DCHECK(c <= (uint32_t)kk);
-                const bool on = c != 0u && ((vm >> u) & 1u);
-                uint32_t *p = on ? v + 3 + c : trash;
-                if (WEIGHTED) {
-                    const unsigned long long qv = (unsigned long long)__float2ll_rn(wa[u] * qscale);
-                    atomicAdd(p, (uint32_t)qv & ((1u << BLOCK_SPLIT) - 1u));
-                    atomicAdd(on ? p + pkb : trash, (uint32_t)(qv >> BLOCK_SPLIT));
-                } else {
-                    atomicAdd(p, 1u);
-                }
+            // rounds that lie inside the item (all but its first and last) take
+            // the mask-free body (warp-uniform choice)
+            if (e0 >= b0 && e0 + BROUND <= e1) {
+                heavy_round<WEIGHTED, true, NC>(vb, tb, pb, ca, wa, qscale, 0xffu, kk);
+            } else {
+                // arcs of this lane's chunk inside the item: bits [vlo, vhi)
+                const int64_t a0 = e0 + lane * BU;
+                const int vlo = (int)min((int64_t)BU, max((int64_t)0, b0 - a0));
+                const int vhi = (int)min((int64_t)BU, max((int64_t)0, e1 - a0));
+                heavy_round<WEIGHTED, false, NC>(vb, tb, pb, ca, wa, qscale, ((1u << vhi) - 1u) & ~((1u << vlo) - 1u), kk);
             }
             if (sub == HSUB - 1 || e0 + BROUND >= e1) {
                 __syncwarp();  // every lane has read the slot before it is refilled
@@ -654,21 +696,27 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
                 ep += HROUND;
                 slot = slot + 1 == RING_H ? 0 : slot + 1;
             }
-            // fold the window into the 64-bit sums at each aligned window end
+            // fold the window into the 64-bit sums at each aligned window end: a
+            // copy takes 1 / NC of every round's arcs, so its u32 planes hold
+            // NC * BLOCK_ROW_MAX arcs of the item without wrapping
             const int64_t en = e0 + BROUND;
-            if ((en & (BLOCK_ROW_MAX - 1)) == 0 || en >= e1) {
+            if ((en & (NC * BLOCK_ROW_MAX - 1)) == 0 || en >= e1) {
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < HCOL; j++) {
-                    const int c = lane + 32 * j;
-                    if (c < kk) {
-#pragma unroll
-                        for (int q = 0; q < HCOPY; q++) {
-                            uint32_t *p = vw + q * cs + 4 + c;
+                for (int m = 0; m < NIT; m++) {
+                    const int word = 4 * lane + 128 * m;
+                    if (word < nbw) {
+                        uint32_t *p = vw + word;
+                        const uint4 lo = *reinterpret_cast<uint4 *>(p);
+                        *reinterpret_cast<uint4 *>(p) = make_uint4(0u, 0u, 0u, 0u);
+                        if (WEIGHTED) {
+                            const uint4 hi = *reinterpret_cast<uint4 *>(p + pw);
+                            *reinterpret_cast<uint4 *>(p + pw) = make_uint4(0u, 0u, 0u, 0u);
                             // wrapping u64 adds of the signed plane sums
-                            sum[j] += WEIGHTED ? (unsigned long long)plane_sum(p[0], p[pkb]) : (unsigned long long)p[0];
-                            p[0] = 0u;
-                            if (WEIGHTED) p[pkb] = 0u;
+                            sum[m] += (unsigned long long)plane_sum(lo.x, hi.x) + (unsigned long long)plane_sum(lo.y, hi.y) +
+                                      (unsigned long long)plane_sum(lo.z, hi.z) + (unsigned long long)plane_sum(lo.w, hi.w);
+                        } else {
+                            sum[m] += (unsigned long long)lo.x + lo.y + lo.z + lo.w;
                         }
                     }
                 }
@@ -676,18 +724,18 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
             }
         }
         const int32_t slotm = item_slot[it];
-        if (slotm < 0) {  // the row's only item: write its Z row
-            float *zr = z + (int64_t)item_row[it] * kk;
+        float *zr = z + (int64_t)item_row[it] * kk;
 #pragma unroll
-            for (int j = 0; j < HCOL; j++) {
-                const int c = lane + 32 * j;
-                if (c < kk) zr[c] = (WEIGHTED ? (float)(long long)sum[j] : (float)sum[j]) * sc1[c];
-            }
-        } else {
+        for (int m = 0; m < NIT; m++) {
+            unsigned long long t = sum[m];
 #pragma unroll
-            for (int j = 0; j < HCOL; j++) {
-                const int c = lane + 32 * j;
-                if (c < kk && sum[j]) atomicAdd(&acc[(int64_t)slotm * kk + c], sum[j]);
+            for (int d = 1; d < LPC; d <<= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+            const int c = lane / LPC + CPI * m - 1;  // bin 0 is no class
+            if (lane % LPC == 0 && c >= 0 && c < kk) {
+                if (slotm < 0)  // the row's only item: write its Z row
+                    zr[c] = (WEIGHTED ? (float)(long long)t : (float)t) * sc1[c];
+                else if (t)
+                    atomicAdd(&acc[(int64_t)slotm * kk + c], t);
             }
         }
     }
@@ -824,25 +872,22 @@ int gee_reduce_heavy(const uint8_t *cls, const float *w, int64_t arcs, int32_t s
     const bool weighted = w != nullptr;
     const float qscale = ldexpf(1.0f, scale_exp);
     const double dscale = weighted ? ldexp(1.0, -scale_exp) : 1.0;
+    const int nc = k <= 64 ? HNC_SMALL : HNC_LARGE;
     const size_t sh = (size_t)RW * RING_H * (HSUB * (RING_CLS + (weighted ? RING_W : 0)) + sizeof(uint64_t)) +
                       (size_t)block_vec_words(k) * sizeof(float) +
-                      (size_t)RW * (HCOPY * (block_vec_words(k) * (weighted ? 2 : 1) + 4) + 32) * sizeof(uint32_t);
+                      (size_t)RW * heavy_plane_words(k, nc) * (weighted ? 2 : 1) * sizeof(uint32_t);
     GEE_REQUIRE((reinterpret_cast<uintptr_t>(cls) & 7) == 0 && (!weighted || (reinterpret_cast<uintptr_t>(w) & 15) == 0),
                 GEE_ERR_INVALID, "cls must be 8-byte and w 16-byte aligned");
     auto *acc = static_cast<unsigned long long *>(mega_acc);
     auto *ctr = reinterpret_cast<unsigned long long *>(counter);
     GEE_CUDA(cudaMemsetAsync(ctr, 0, sizeof(*ctr), st));
     const int hgrid = grid_for(n_items * 32, RT, 8);
-    if (weighted)
-        GEE_CUDA(cudaFuncSetAttribute(k_reduce_heavy_items<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    else
-        GEE_CUDA(cudaFuncSetAttribute(k_reduce_heavy_items<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-    if (weighted)
-        k_reduce_heavy_items<true><<<hgrid, RT, sh, st>>>(item_first, item_end, item_row, item_slot, n_items, cls, w,
-                                                          qscale, dscale, inv, k, arcs, acc, ctr, z);
-    else
-        k_reduce_heavy_items<false><<<hgrid, RT, sh, st>>>(item_first, item_end, item_row, item_slot, n_items, cls, w,
-                                                           qscale, dscale, inv, k, arcs, acc, ctr, z);
+    auto kern = weighted ? (k <= 64 ? k_reduce_heavy_items<true, HNC_SMALL, 64> : k_reduce_heavy_items<true, HNC_LARGE, 255>)
+                         : (k <= 64 ? k_reduce_heavy_items<false, HNC_SMALL, 64>
+                                    : k_reduce_heavy_items<false, HNC_LARGE, 255>);
+    GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+    kern<<<hgrid, RT, sh, st>>>(item_first, item_end, item_row, item_slot, n_items, cls, w, qscale, dscale, inv, k, arcs,
+                                acc, ctr, z);
     int rc;
     if ((rc = gee::check_launch("k_reduce_heavy_items"))) return rc;
     if (n_mega == 0) return GEE_OK;
