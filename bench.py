@@ -75,6 +75,9 @@ def parse():
                          "(DeviceGraph.tile_heavy; graph preparation)")
     ap.add_argument("--tile-slots", type=int, default=None, help="label-table slots per shared-memory tile")
     ap.add_argument("--tile-max", type=int, default=None, help="tiles (slots past them stay on the L2 path)")
+    ap.add_argument("--short-row-arcs", type=int, default=None,
+                    help="rows of at most this many arcs skip the weighted block reducer's windows (0..4; default "
+                         "DeviceGraph.SHORT_ROW_ARCS)")
     ap.add_argument("--graph", action="store_true",
                     help="also time the step replayed as one CUDA graph (Embedder.capture; launch-bound configs)")
     return ap.parse_args()
@@ -539,6 +542,8 @@ def main():
 
     # warm-up (also validates labels once); the hot-label tier is graph prep
     t0 = time.perf_counter()
+    if args.short_row_arcs is not None:
+        g.SHORT_ROW_ARCS = args.short_row_arcs
     g.prepare_hot(k)
     if args.heavy_layout == "tiles":
         g.tile_heavy(tile_slots=args.tile_slots, max_tiles=args.tile_max)

@@ -296,6 +296,16 @@ int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls
  * CSR): the heavy-row skipping is compiled out (C4 7.61 -> 7.50 ms). */
 int gee_reduce_blocks_light(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
                             int32_t scale_exp, const double *inv, int32_t k, float *z, void *stream);
+/* gee_reduce_blocks_light with the shortest rows flagged: bit i of
+ * short_rows[b] (uint32 per 32-row block, device) is set when row 32 b + i
+ * holds 1 .. short_arcs arcs before padding (short_arcs in 1..4; its padded
+ * run is [the arcs | pads]).  Weighted graphs: the lane that holds such a
+ * row's chunk combines its arcs in registers and stores the row's nonzero
+ * Z entries itself, without a window slot.  Same bits.  short_rows NULL or
+ * unit weights: exactly gee_reduce_blocks_light. */
+int gee_reduce_blocks_short(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w,
+                            int32_t scale_exp, const double *inv, int32_t k, const uint32_t *short_rows,
+                            int32_t short_arcs, float *z, void *stream);
 
 /* Heavy rows (longer than the block reducer's heavy_arcs) as work items:
  * item i covers arcs [item_first[i], item_end[i]) of row item_row[i]

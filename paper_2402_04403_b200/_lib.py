@@ -69,6 +69,7 @@ SIGNATURES = {
     "gee_sort_rows": (c_int, [vp, c_i64, vp, vp, vp]),
     "gee_reduce_blocks_pad8": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, c_i64, vp, vp]),
     "gee_reduce_blocks_light": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, vp, vp]),
+    "gee_reduce_blocks_short": (c_int, [vp, c_i64, vp, vp, c_i32, vp, c_i32, vp, c_i32, vp, vp]),
     "gee_reduce_heavy": (c_int, [vp, vp, c_i64, c_i32, vp, c_i32, vp, vp, vp, vp, c_i64, vp, c_i64, vp, vp, vp, vp]),
     "gee_block_scale_exp": (c_int, [c_dbl, c_dbl, c_dbl, P_i32, P_dbl]),
     "gee_tile_bounds": (c_int, [vp, vp, c_i64, vp, vp, c_i32, vp, vp]),

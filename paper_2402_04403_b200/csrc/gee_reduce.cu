@@ -71,7 +71,7 @@ __device__ __forceinline__ long long plane_sum(uint32_t lo, uint32_t hi)
 // each lane's 8 arcs belong to one row): the lane's owner rank is the count
 // of rows started before the round plus the row starts at lane chunks <= its
 // own -- one ballot, one OR-reduction, two popcounts, no shared masks.
-template <bool WEIGHTED>
+template <bool WEIGHTED, int SHORT = 0>  // SHORT: <= 4 (the arcs' classes lie in the chunk's first word)
 __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const int32_t *__restrict__ s_soff, int lane,
                                                 bool owner, int32_t ol, int32_t lr, int32_t lend, int hoff, int trash,
                                                 float qscale, const uint2 &ca, const float (&wa)[BU],
@@ -85,6 +85,38 @@ __device__ __forceinline__ void block_round_pad(uint32_t *__restrict__ vw, const
     const int so = s_soff[r];
     const bool inb = lr + lane * BU < lend;
     const bool ok = so >= 0 && inb;
+    if (WEIGHTED && SHORT > 0 && so <= -2 && inb) {
+        // a row of at most SHORT arcs (flagged at graph preparation; its
+        // chunk is [the arcs | pads, class 0]): equal classes combine in
+        // registers, exactly as the window would (plane_sum of the q's is
+        // their sum), and the lane stores the row's nonzero entries into the
+        // zero-filled Z row -- no window slot, no read-out.  Doing this for
+        // every single-chunk row (8 arcs, 28 compares, 64-bit selects) cost
+        // more than the window (C4 7.8 -> 9.1 ms); for the shortest rows it pays.
+        GEE_DCHECK(-so - 2 < 32);
+        float *zr = zb + (int64_t)(-so - 2) * kk;
+        constexpr int NS = SHORT > 0 ? SHORT : 1;
+        uint32_t cc[NS];
+        long long qq[NS];
+#pragma unroll
+        for (int u = 0; u < SHORT; u++) {
+            cc[u] = __byte_perm(ca.x, 0u, 0x4440 + u);
+            GEE_DCHECK(cc[u] <= (uint32_t)kk);
+            qq[u] = __float2ll_rn(wa[u] * qscale);
+        }
+#pragma unroll
+        for (int u = 0; u < SHORT; u++) {
+            bool first = cc[u] != 0u;
+#pragma unroll
+            for (int v = 0; v < u; v++) first = first && cc[v] != cc[u];
+            if (first) {
+                long long sum = qq[u];
+#pragma unroll
+                for (int v = u + 1; v < SHORT; v++) sum += cc[v] == cc[u] ? qq[v] : 0ll;
+                zr[cc[u] - 1] = (float)sum * sc1[cc[u] - 1];
+            }
+        }
+    }
     if (!WEIGHTED && so <= -2 && inb) {
         // a single-chunk row (padded length 8: <= 8 real arcs, all in this
         // lane's chunk; unit weights): equal classes combine in registers,
@@ -283,9 +315,10 @@ __device__ __forceinline__ void pass_span(const RingBlk &B, unsigned winm, int p
 // the lane that holds their chunk (block_round_pad), not in the window
 // (unit weights only).
 template <bool WEIGHTED>
-__device__ __forceinline__ unsigned single_rows(const RingBlk &B, int lane)
+__device__ __forceinline__ unsigned single_rows(const RingBlk &B, int lane, unsigned one = 0u)
 {
-    return WEIGHTED ? 0u : __ballot_sync(0xffffffffu, ((B.nzm >> lane) & 1u) && B.oh - B.ol == BU);
+    // weighted: the short rows flagged at graph preparation (block_round_pad)
+    return WEIGHTED ? (one & B.nzm) : __ballot_sync(0xffffffffu, ((B.nzm >> lane) & 1u) && B.oh - B.ol == BU);
 }
 
 // SPANS: the two weight copies of a round each move 512 contiguous bytes
@@ -352,11 +385,14 @@ __device__ __forceinline__ void ring_issue_bulk(uint8_t *ring, uint64_t *bars, i
     if (WEIGHTED) bulk_g2s(rs + HSUB * RING_CLS, w + e, wb, bars + slot, pol);
 }
 
-template <bool WEIGHTED, bool HV>  // HV: rows longer than heavy_arcs may sit in the CSR (skipped here)
+// HV: rows longer than heavy_arcs may sit in the CSR (skipped here).  SHORT > 0 (weighted): one_arc[b]
+// flags the rows of block b that hold at most SHORT arcs.
+template <bool WEIGHTED, bool HV, int SHORT = 0>
 __global__ void __launch_bounds__(RT, BCTAS)
 k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8_t *__restrict__ cls,
                      const float *__restrict__ w, float qscale, double dscale, const double *__restrict__ inv,
-                     int32_t k, int64_t heavy_arcs, int nslots, float *__restrict__ z)
+                     int32_t k, int64_t heavy_arcs, int nslots, const uint32_t *__restrict__ one_arc,
+                     float *__restrict__ z)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int kk = k;
@@ -398,8 +434,9 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         const int64_t o_31 = lane == 31 ? __ldcs(offsets + min(r0 + 32, n)) : 0;
         B = ring_open<HV>(r0, n, o_lo, o_31, heavy_arcs, lane);
     }
+    unsigned one_b = SHORT ? __ldg(one_arc + b) : 0u;  // this block's short rows
     int64_t plo, phi;
-    pass_span(B, B.nzm & ~single_rows<WEIGHTED>(B, lane), 0, nslots, plo, phi);
+    pass_span(B, B.nzm & ~single_rows<WEIGHTED>(B, lane, one_b), 0, nslots, plo, phi);
     int64_t ep = ring_skip<HV>(B, plo, lane);  // next round to issue
 #pragma unroll
     for (int i = 0; i < RING; i++) {
@@ -414,7 +451,8 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         const int64_t nr0 = 32 * (b + 1);
         const int64_t o_lo_n = more ? __ldcs(offsets + min(nr0 + lane, n)) : 0;
         const int64_t o_31_n = (more && lane == 31) ? __ldcs(offsets + min(nr0 + 32, n)) : 0;
-        const unsigned singlem = single_rows<WEIGHTED>(B, lane);
+        const unsigned one_n = (SHORT && more) ? __ldg(one_arc + b + 1) : 0u;
+        const unsigned singlem = single_rows<WEIGHTED>(B, lane, one_b);
         const unsigned winm = B.nzm & ~singlem;
         const int rank = __popc(winm & below);
         const int orank = __popc(B.anym & below);
@@ -457,7 +495,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
                     for (int u = 0; u < BU; u++) wa[u] = 1.f;
                 }
                 if (nnz > 0 || singlem)
-                    block_round_pad<WEIGHTED>(vw, s_soff, lane, owner, B.ol, (int32_t)(ec - B.base), lend, hoff,
+                    block_round_pad<WEIGHTED, SHORT>(vw, s_soff, lane, owner, B.ol, (int32_t)(ec - B.base), lend, hoff,
                                               trash, qscale, ca, wa, zb, kk, sc1);
                 __syncwarp();
                 // refill the slot just consumed with the round RING ahead
@@ -476,7 +514,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
             } else if (more) {
                 NB = ring_open<HV>(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
                 opened = true;
-                pass_span(NB, NB.nzm & ~single_rows<WEIGHTED>(NB, lane), 0, nslots, nlo, nhi);
+                pass_span(NB, NB.nzm & ~single_rows<WEIGHTED>(NB, lane, one_n), 0, nslots, nlo, nhi);
                 ep = ring_skip<HV>(NB, nlo, lane);
             }
             if (!last || more) {
@@ -536,6 +574,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
         }
         if (!more) break;
         B = opened ? NB : ring_open<HV>(nr0, n, o_lo_n, o_31_n, heavy_arcs, lane);
+        one_b = one_n;
     }
     cp_wait<0>();
 }
@@ -669,26 +708,28 @@ k_reduce_heavy_items(const int64_t *__restrict__ item_first, const int64_t *__re
                 __syncwarp();
                 ph ^= 1u << slot;
             }
-            const uint8_t *rs = ring + slot * RSLOT + sub * RING_CLS;
-            const uint8_t *rw = ring + slot * RSLOT + HSUB * RING_CLS + sub * RING_W;
-            const uint2 ca = *reinterpret_cast<const uint2 *>(rs + lane * BU);
-            float wa[BU];
-            if (WEIGHTED) {
-                const float4 x0 = *reinterpret_cast<const float4 *>(rw + lane * BU * 4);
-                const float4 x1 = *reinterpret_cast<const float4 *>(rw + lane * BU * 4 + 16);
-                wa[0] = x0.x, wa[1] = x0.y, wa[2] = x0.z, wa[3] = x0.w;
-                wa[4] = x1.x, wa[5] = x1.y, wa[6] = x1.z, wa[7] = x1.w;
-            }
-            // rounds that lie inside the item (all but its first and last) take
-            // the mask-free body (warp-uniform choice)
-            if (e0 >= b0 && e0 + BROUND <= e1) {
-                heavy_round<WEIGHTED, true, NC>(vb, tb, pb, ca, wa, qscale, 0xffu, kk);
-            } else {
-                // arcs of this lane's chunk inside the item: bits [vlo, vhi)
-                const int64_t a0 = e0 + lane * BU;
-                const int vlo = (int)min((int64_t)BU, max((int64_t)0, b0 - a0));
-                const int vhi = (int)min((int64_t)BU, max((int64_t)0, e1 - a0));
-                heavy_round<WEIGHTED, false, NC>(vb, tb, pb, ca, wa, qscale, ((1u << vhi) - 1u) & ~((1u << vlo) - 1u), kk);
+            if (e0 + BROUND > b0) {  // (a slot's first round may lie wholly before the item: rounds are slot-aligned)
+                const uint8_t *rs = ring + slot * RSLOT + sub * RING_CLS;
+                const uint8_t *rw = ring + slot * RSLOT + HSUB * RING_CLS + sub * RING_W;
+                const uint2 ca = *reinterpret_cast<const uint2 *>(rs + lane * BU);
+                float wa[BU];
+                if (WEIGHTED) {
+                    const float4 x0 = *reinterpret_cast<const float4 *>(rw + lane * BU * 4);
+                    const float4 x1 = *reinterpret_cast<const float4 *>(rw + lane * BU * 4 + 16);
+                    wa[0] = x0.x, wa[1] = x0.y, wa[2] = x0.z, wa[3] = x0.w;
+                    wa[4] = x1.x, wa[5] = x1.y, wa[6] = x1.z, wa[7] = x1.w;
+                }
+                // rounds that lie inside the item (all but its first and last) take
+                // the mask-free body (warp-uniform choice)
+                if (e0 >= b0 && e0 + BROUND <= e1) {
+                    heavy_round<WEIGHTED, true, NC>(vb, tb, pb, ca, wa, qscale, 0xffu, kk);
+                } else {
+                    // arcs of this lane's chunk inside the item: bits [vlo, vhi)
+                    const int64_t a0 = e0 + lane * BU;
+                    const int vlo = (int)min((int64_t)BU, max((int64_t)0, b0 - a0));
+                    const int vhi = (int)min((int64_t)BU, max((int64_t)0, e1 - a0));
+                    heavy_round<WEIGHTED, false, NC>(vb, tb, pb, ca, wa, qscale, ((1u << vhi) - 1u) & ~((1u << vlo) - 1u), kk);
+                }
             }
             if (sub == HSUB - 1 || e0 + BROUND >= e1) {
                 __syncwarp();  // every lane has read the slot before it is refilled
@@ -804,22 +845,34 @@ int gee_reduce_heavy_plan(const int64_t *offsets, int64_t n, int64_t heavy_arcs,
 }
 
 static int reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
-                         const double *inv, int32_t k, int64_t heavy_arcs, bool heavy_in_csr, float *z, void *stream);
+                         const double *inv, int32_t k, int64_t heavy_arcs, bool heavy_in_csr, const uint32_t *one_arc,
+                         int32_t short_arcs, float *z, void *stream);
 
 int gee_reduce_blocks_pad8(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
                            const double *inv, int32_t k, int64_t heavy_arcs, float *z, void *stream)
 {
-    return reduce_blocks(offsets, n, cls, w, scale_exp, inv, k, heavy_arcs, true, z, stream);
+    return reduce_blocks(offsets, n, cls, w, scale_exp, inv, k, heavy_arcs, true, nullptr, 0, z, stream);
 }
 
 int gee_reduce_blocks_light(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
                             const double *inv, int32_t k, float *z, void *stream)
 {
-    return reduce_blocks(offsets, n, cls, w, scale_exp, inv, k, BLOCK_ROW_MAX, false, z, stream);
+    return reduce_blocks(offsets, n, cls, w, scale_exp, inv, k, BLOCK_ROW_MAX, false, nullptr, 0, z, stream);
+}
+
+int gee_reduce_blocks_short(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
+                            const double *inv, int32_t k, const uint32_t *short_rows, int32_t short_arcs, float *z,
+                            void *stream)
+{
+    gee::clear_error();
+    GEE_REQUIRE(short_rows == nullptr || (short_arcs >= 1 && short_arcs <= 4), GEE_ERR_INVALID,
+                "short_arcs must be 1..4 (got %d)", short_arcs);
+    return reduce_blocks(offsets, n, cls, w, scale_exp, inv, k, BLOCK_ROW_MAX, false, short_rows, short_arcs, z, stream);
 }
 
 static int reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, const float *w, int32_t scale_exp,
-                         const double *inv, int32_t k, int64_t heavy_arcs, bool heavy_in_csr, float *z, void *stream)
+                         const double *inv, int32_t k, int64_t heavy_arcs, bool heavy_in_csr, const uint32_t *one_arc,
+                         int32_t short_arcs, float *z, void *stream)
 {
     gee::clear_error();
     GEE_REQUIRE(k >= 1 && k <= 255, GEE_ERR_INVALID, "class stream needs 1 <= k <= 255 (got %d)", k);
@@ -848,10 +901,16 @@ static int reduce_blocks(const int64_t *offsets, int64_t n, const uint8_t *cls, 
     const size_t shr = ring + fixed + (size_t)RW * ns * vecb;
     const int64_t nblocks = (n + 31) / 32;
     const int rgrid = (int)std::min<int64_t>((nblocks + RW - 1) / RW, (int64_t)gee::sm_count() * BCTAS);
+    const int sh_arcs = (weighted && !heavy_in_csr && one_arc != nullptr) ? short_arcs : 0;
     auto kern = weighted ? (heavy_in_csr ? k_reduce_blocks_ring<true, true> : k_reduce_blocks_ring<true, false>)
                          : (heavy_in_csr ? k_reduce_blocks_ring<false, true> : k_reduce_blocks_ring<false, false>);
+    if (sh_arcs == 1) kern = k_reduce_blocks_ring<true, false, 1>;
+    if (sh_arcs == 2) kern = k_reduce_blocks_ring<true, false, 2>;
+    if (sh_arcs == 3) kern = k_reduce_blocks_ring<true, false, 3>;
+    if (sh_arcs == 4) kern = k_reduce_blocks_ring<true, false, 4>;
+    const bool one = sh_arcs > 0;
     GEE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shr));
-    kern<<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, ns, z);
+    kern<<<rgrid, RT, shr, st>>>(offsets, n, cls, w, qscale, dscale, inv, k, heavy_arcs, ns, one ? one_arc : nullptr, z);
     return gee::check_launch("k_reduce_blocks_ring");
 }
 

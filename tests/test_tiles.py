@@ -82,6 +82,32 @@ def test_tiles_match_row_layout_bitwise(hot, weighted, signed, tile_slots, max_t
         assert rel_err(z_tiles, exp) <= TOL
 
 
+@pytest.mark.parametrize("short", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("k", [1, 3, 50])
+def test_short_rows_skip_the_windows_bitwise(monkeypatch, short, k):
+    """Weighted rows of at most SHORT_ROW_ARCS arcs are reduced in registers
+    by the lane that holds them (gee_reduce_blocks_short): same bits as the
+    windows for every threshold, with repeated classes (k = 1, 3), signed
+    weights that cancel, unlabeled targets and self-loops."""
+    monkeypatch.setattr(DeviceGraph, "SHORT_ROW_ARCS", short)
+    n = 40_000
+    rng = np.random.default_rng(100 + short)
+    src0, dst0, w0 = _hub_graph(23, n, True, signed=True)
+    # a sparse background: most rows end up with 1-4 arcs
+    s1, d1 = rng.integers(0, n, 30_000), rng.integers(0, n, 30_000)
+    loops = rng.integers(0, n, 500)
+    src = np.concatenate([src0, s1, loops, s1[:2000]])
+    dst = np.concatenate([dst0, d1, loops, d1[:2000]])
+    w1 = (1.0 - rng.random(s1.size)).astype(np.float32) * rng.choice([-1.0, 1.0], s1.size).astype(np.float32)
+    w = np.concatenate([w0, w1, np.ones(500, np.float32), -w1[:2000]])  # the last 2000 cancel their twins
+    y = rng.integers(0, k + 1, n)
+    z_rows, z_tiles = _pull_both(src, dst, w, y, n, k, True, 1024, 8)
+    assert np.array_equal(z_rows.view(np.uint32), z_tiles.view(np.uint32))
+    exp = oracle.serial_embed(src, dst, w, y.astype(np.int64), n, k)
+    big = np.abs(exp) > 1e-3 * np.abs(exp).max()
+    assert np.max(np.abs(z_tiles[big] - exp[big]) / np.abs(exp[big])) <= TOL
+
+
 @pytest.mark.parametrize("k", [1, 7, 255])
 def test_tiles_mega_rows_and_k(k):
     n = 30_000
