@@ -632,8 +632,8 @@ __device__ __forceinline__ void heavy_round(uint32_t vb, uint32_t tb, uint32_t p
 #pragma unroll
     for (int u = 0; u < BU; u++) {
         const uint32_t c = __byte_perm(u < 4 ? ca.x : ca.y, 0u, 0x4440 + (u & 3));
-        GEE_DCHECK(c <= (uint32_t)kk);
         const bool on = FULL ? c != 0u : (c != 0u && ((vm >> u) & 1u));
+        GEE_DCHECK(!on || c <= (uint32_t)kk);  // (bytes past the item's last arc are whatever the ring slot held)
         const uint32_t a = on ? vb + (4u * NC) * c : tb;
         if (WEIGHTED) {
             const unsigned long long qv = (unsigned long long)__float2ll_rn(wa[u] * qscale);
