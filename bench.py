@@ -75,6 +75,9 @@ def parse():
                          "(DeviceGraph.tile_heavy; graph preparation)")
     ap.add_argument("--tile-slots", type=int, default=None, help="label-table slots per shared-memory tile")
     ap.add_argument("--tile-max", type=int, default=None, help="tiles (slots past them stay on the L2 path)")
+    ap.add_argument("--span-align", type=int, default=None,
+                    help="tile layout: arcs each (tile, row) span is padded to (a multiple of 16; default "
+                         "DeviceGraph.SPAN_ALIGN)")
     ap.add_argument("--short-row-arcs", type=int, default=None,
                     help="rows of at most this many arcs skip the weighted block reducer's windows (0..4; default "
                          "DeviceGraph.SHORT_ROW_ARCS)")
@@ -545,6 +548,8 @@ def main():
     if args.short_row_arcs is not None:
         g.SHORT_ROW_ARCS = args.short_row_arcs
     g.prepare_hot(k)
+    if args.span_align is not None:
+        g.SPAN_ALIGN = args.span_align
     if args.heavy_layout == "tiles":
         g.tile_heavy(tile_slots=args.tile_slots, max_tiles=args.tile_max)
     if world > 1:  # every rank rounds weights with the whole graph's exponent

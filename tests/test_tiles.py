@@ -108,6 +108,18 @@ def test_short_rows_skip_the_windows_bitwise(monkeypatch, short, k):
     assert np.max(np.abs(z_tiles[big] - exp[big]) / np.abs(exp[big])) <= TOL
 
 
+@pytest.mark.parametrize("align", [16, 32, 48])
+def test_span_alignment_changes_no_bits(monkeypatch, align):
+    """(tile, row) spans padded to 16, 32 (the default: whole sectors of
+    class bytes) or 48 arcs: same Z bits as the row-major layout."""
+    monkeypatch.setattr(DeviceGraph, "SPAN_ALIGN", align)
+    n, k = 20_000, 50
+    src, dst, w = _hub_graph(41, n, True, signed=True)
+    y = synth.uniform_labels_numpy(n, k, seed=13)
+    z_rows, z_tiles = _pull_both(src, dst, w, y, n, k, True, 512, 6)
+    assert np.array_equal(z_rows.view(np.uint32), z_tiles.view(np.uint32))
+
+
 @pytest.mark.parametrize("k", [1, 7, 255])
 def test_tiles_mega_rows_and_k(k):
     n = 30_000
