@@ -10,7 +10,8 @@
 // CSR into a region ordered by (slot tile, row, slot), where a tile is a run
 // of `tile_slots` label-table slots that fits shared memory; their class
 // bytes and weights stay row-major (row, tile, slot), which is what the
-// heavy reducer streams.  Every (tile, row) span is padded to 16 arcs in
+// heavy reducer streams.  Every (tile, row) span is padded to a multiple of
+// 16 arcs (DeviceGraph.SPAN_ALIGN: 32, whole sectors of class bytes) in
 // both orders, and group_dst maps each 16-arc group of the tile-major order
 // to its group in the row-major order.  The gather of the region is then a
 // pure stream: every CTA takes an equal arc range, stages the range's

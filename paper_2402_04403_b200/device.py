@@ -380,7 +380,7 @@ class DeviceGraph:
             targets  [ light rows, row-major | heavy tail | tile 0 | tile 1 | ... ]
             weights  [ light rows, row-major | heavy rows, row-major (row, tile, slot) ]
         (the class stream is indexed like the weights), every (tile, row)
-        span padded to 16 arcs in both orders, and group_dst maps the 16-arc
+        span padded to SPAN_ALIGN arcs in both orders, and group_dst maps the 16-arc
         groups of the heavy targets to their place in the row-major order.
         Heavy rows keep an empty run in `offsets` (the block reducer
         zero-fills them, gee_reduce_heavy then writes them).  Returns True
