@@ -191,6 +191,17 @@ def dist_setup(n_gpus):
     return world, rank, local
 
 
+def extra_steps(ms_timed, steps, world):
+    """How many untimed steps keep the same load running for about another
+    second, so that the nvidia-smi clock record covers a short timed region.
+    A count every rank agrees on (the slowest rank's step time): a step holds
+    collectives (the sharded histogram's all-reduce, the edge scheme's
+    reduce-scatter), so ranks looping on their own wall clocks would issue
+    different numbers of them and hang."""
+    ms = max_over_ranks(float(ms_timed), world) / max(int(steps), 1)
+    return int(min(2000, max(1, -(-1000.0 // max(ms, 1e-3)))))
+
+
 def barrier(world):
     if world > 1:
         import torch
@@ -479,8 +490,7 @@ def run_edges(args):
         end.record(stream)
         launches = emb.launches
         torch.cuda.synchronize()
-        t_extra = time.perf_counter()
-        while time.perf_counter() - t_extra < 1.0:
+        for _ in range(extra_steps(start.elapsed_time(end), args.steps, world)):
             step()
         torch.cuda.synchronize()
     barrier(world)
@@ -579,8 +589,7 @@ def main():
         torch.cuda.synchronize()
         # short timed regions get few nvidia-smi samples: keep the same load
         # running (untimed) for another second so the clock record covers it
-        t_extra = time.perf_counter()
-        while time.perf_counter() - t_extra < 1.0:
+        for _ in range(extra_steps(start.elapsed_time(end), args.steps, world)):
             step(z)
         torch.cuda.synchronize()
     barrier(world)

@@ -166,3 +166,19 @@ def test_weights_checked_before_float32_narrowing():
         gb.CsrGraph(n=2, offsets=[0, 1, 1], targets=[1], weights=np.array([np.inf]))
     el = gb.EdgeList(n=2, src=[0, 1], dst=[1, 0], w=np.array([0.0, -2.5]))
     assert el.w.dtype == np.float32 and el.w.tolist() == [0.0, -2.5]
+
+
+def test_bench_extra_steps_is_a_count_not_a_clock():
+    """bench.py keeps the load up after the timed region for a number of
+    steps derived from the (max-over-ranks) step time, never from a rank's
+    own wall clock: the step holds collectives."""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert bench.extra_steps(180.0, 10, 1) == 56  # 18 ms steps: about a second
+    assert bench.extra_steps(1.0, 10, 1) == 2000  # capped
+    assert bench.extra_steps(50000.0, 10, 1) == 1
+    assert bench.extra_steps(0.0, 0, 1) == 2000
