@@ -729,6 +729,17 @@ def main():
             del csr_h, z_ref
             g = emb = z = None
         else:
+            if g.heavy_layout == "tiles":
+                # the streamed pipeline reads the graph in row chunks: this rank's
+                # shard again, in the row-major layout (graph preparation, untimed)
+                from paper_2402_04403_b200.shard import unify_scale_distributed
+
+                del g
+                torch.cuda.empty_cache()
+                g = build_shard(args, world, rank)[0]
+                g.prepare_hot(k)
+                unify_scale_distributed(g)
+                torch.cuda.synchronize()
             result["e2e"] = run_e2e(g, y, emb, z, s, args, world)
 
     # ---- CPU baseline (rank 0, N=1 only): the oracle port on the same
