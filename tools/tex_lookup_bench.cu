@@ -121,6 +121,14 @@ int main()
         if (tex1) cudaDestroyTextureObject(tex1);
         if (tex4) cudaDestroyTextureObject(tex4);
     }
+    // per-SM or chip-wide limit?  The same ld.global lookups (16 MB table) from fewer CTAs.
+    fill_targets<<<2048, 256>>>(targets, arcs, 16u << 20);
+    CK(cudaDeviceSynchronize());
+    for (int g : {37, 74, 111, 148}) {
+        char name[128];
+        snprintf(name, sizeof name, "ld.global.nc.u8 over 16 MB, %d CTAs", g);
+        run<0>(name, targets, arcs, table, 0, cls, g);
+    }
     printf("done\n");
     return 0;
 }
