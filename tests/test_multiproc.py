@@ -170,3 +170,47 @@ def test_sharded_histogram_world2_gloo():
     assert all(p.exitcode == 0 for p in procs), res
     assert all(r[1] == "ok" for r in res), res
     assert shard.label_slice(10, 4, 3) == (7, 10)
+
+
+def _extra_steps_worker(rank, port, q):
+    # bench.py after the timed region: every rank runs the SAME number of
+    # untimed steps (a step holds collectives), derived from the slowest
+    # rank's step time, whatever its own clock says
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        import importlib.util
+
+        spec = importlib.util.spec_from_file_location(
+            "bench_mod", os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "bench.py"))
+        bench = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(bench)
+        mine = [90.0, 250.0][rank]  # ms over 10 timed steps: 9 and 25 ms per step
+        count = bench.extra_steps(mine, 10, WORLD)
+        counts = [torch.zeros(1, dtype=torch.int64) for _ in range(WORLD)]
+        dist.all_gather(counts, torch.tensor([count]))
+        assert int(counts[0]) == int(counts[1]) == 40, counts
+        # the steps' collectives then match: WORLD ranks, `count` all-reduces each
+        t = torch.ones(1)
+        for _ in range(count):
+            dist.all_reduce(t)
+        q.put((rank, "ok", count))
+    except Exception as ex:  # pragma: no cover
+        q.put((rank, f"fail: {type(ex).__name__}: {ex}", 0))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_extra_steps_agree_across_ranks_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_extra_steps_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = sorted(q.get(timeout=10) for _ in range(WORLD))
+    assert all(p.exitcode == 0 for p in procs), res
+    assert all(r[1] == "ok" for r in res), res
