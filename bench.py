@@ -64,7 +64,8 @@ def parse():
     ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (smaller runs)")
     ap.add_argument("--edges", type=int, default=None, help="edge-count override")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-chunks", type=int, default=32)
+    ap.add_argument("--e2e-chunks", type=int, default=None,
+                    help="row chunks of the e2e calls (default: prepare()'s own, 96 streamed / 32 resident)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-e2e-resident", action="store_true",
                     help="skip the secondary e2e line with the prepared graph resident in HBM")
@@ -792,6 +793,7 @@ def run_e2e_prepared(csr_h, y, k, s, args, z_ref):
     t0 = time.perf_counter()
     prepared = prepare(csr_h, k, chunks=args.e2e_chunks)
     prep_total = time.perf_counter() - t0
+    n_chunks = prepared._chunks
     h_z = np.empty((csr_h.n, k), dtype=np.float32)
     t0 = time.perf_counter()
     embed_parallel(prepared, y_h, out=h_z)  # warm-up: registers h_z / labels, sizes the scratch
@@ -845,7 +847,7 @@ def run_e2e_prepared(csr_h, y, k, s, args, z_ref):
         torch.cuda.empty_cache()
     return {"value": s / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": args.e2e_steps,
-            "chunks": args.e2e_chunks, "matches_resident_pull": same, "timing": "wall clock, median",
+            "chunks": n_chunks, "matches_resident_pull": same, "timing": "wall clock, median",
             "path": "paper_2402_04403_b200.embed_parallel(prepare(CsrGraph host arrays, k), "
                     "LabelVector(host int32), out=host float32 (n, k))",
             "inside": "labels H2D | packed row chunks H2D | gee_unpack_targets, gee_build_projection, "
@@ -873,7 +875,7 @@ def run_e2e(g, y, emb, z, s, args, world=1):
 
     sparse = os.environ.get("GEE_E2E_DENSE") is None
     packed = None if os.environ.get("GEE_E2E_UNPACKED") is None else False
-    pipe = HostPipeline(g, emb.k, chunks=max(1, args.e2e_chunks // world), packed=packed)
+    pipe = HostPipeline(g, emb.k, chunks=max(1, (args.e2e_chunks or 96) // world), packed=packed)
     h_y = y.cpu().pin_memory()
     h_z = pinned_like((g.n, emb.k))
     pipe.run(h_y, h_z, emb, sparse=sparse)  # warm-up (sizes the scratch buffers)
