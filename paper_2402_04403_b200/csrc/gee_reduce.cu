@@ -548,7 +548,9 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
                             s1 = (float)lo.y;
                         }
                         GEE_DCHECK(s_row[sl] >= 0 && s_row[sl] < 32 && r0 + s_row[sl] < n);
-                        __stcs(reinterpret_cast<float2 *>(zc + s_row[sl] * kk), make_float2(s0 * f.x, s1 * f.y));
+                        // (write-back, like the zero fill whose lines these rows overwrite in L2:
+                        // 7.08 ms against 7.16 ms with streaming stores on C4)
+                        *reinterpret_cast<float2 *>(zc + s_row[sl] * kk) = make_float2(s0 * f.x, s1 * f.y);
                     }
                 }
             } else {
@@ -566,7 +568,7 @@ k_reduce_blocks_ring(const int64_t *__restrict__ offsets, int64_t n, const uint8
                         } else {
                             s0 = (float)lo;
                         }
-                        __stcs(zb + s_row[sl] * kk + c, s0 * f);
+                        zb[s_row[sl] * kk + c] = s0 * f;
                     }
                 }
             }
